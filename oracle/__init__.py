@@ -1,0 +1,217 @@
+"""CPU oracle of the Hi^2-GSLoc 3DGS forward rasterizer -- TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2507_15683_b200``) never imports it, and the two share no code: this
+wrapper only marshals numpy arrays into ``liboracle.so`` (built from
+``gs_oracle.cpp`` with ``g++ -O2 -ffp-contract=off -fno-fast-math``).
+
+See ``gs_oracle.cpp`` for what each function computes and which PAPER.md /
+SPEC.md passage it follows; DESIGN.md §5 lists the pin of every function.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+import subprocess
+from typing import Dict, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "gs_oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CXXFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (single-threaded, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["g++", *CXXFLAGS, "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _View(ctypes.Structure):
+    _fields_ = [("R", ctypes.c_float * 9), ("t", ctypes.c_float * 3), ("fx", ctypes.c_float),
+                ("fy", ctypes.c_float), ("cx", ctypes.c_float), ("cy", ctypes.c_float),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [("z_near", ctypes.c_float), ("dilation", ctypes.c_float), ("clamp_margin", ctypes.c_float),
+                ("alpha_min", ctypes.c_float), ("alpha_max", ctypes.c_float), ("t_min", ctypes.c_float)]
+
+
+@dataclasses.dataclass
+class Params:
+    """Readings Q5, Q7, Q6, Q14, Q15."""
+    z_near: float = 0.2
+    dilation: float = 0.3
+    clamp_margin: float = 0.15
+    alpha_min: float = 1.0 / 255.0
+    alpha_max: float = 0.99
+    t_min: float = 1e-4
+
+    def c(self) -> _Params:
+        return _Params(self.z_near, self.dilation, self.clamp_margin, self.alpha_min, self.alpha_max, self.t_min)
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        _lib.oracle_project.restype = ctypes.c_int64
+        _lib.oracle_count_pairs.restype = ctypes.c_int64
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _view_c(view) -> _View:
+    v = _View()
+    R = np.asarray(view.R, np.float32).reshape(9)
+    t = np.asarray(view.t, np.float32).reshape(3)
+    for k in range(9):
+        v.R[k] = float(R[k])
+    for k in range(3):
+        v.t[k] = float(t[k])
+    v.fx, v.fy, v.cx, v.cy = view.fx, view.fy, view.cx, view.cy
+    v.width, v.height = view.width, view.height
+    return v
+
+
+def _c32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def project(scene, view, params: Optional[Params] = None) -> Dict[str, np.ndarray]:
+    """O1-O10 for one view: records of visible Gaussians in gid order."""
+    params = params or Params()
+    n = scene.n
+    pos, quat, scale, op, sh = _c32(scene.pos), _c32(scene.quat), _c32(scene.scale), _c32(scene.opacity), _c32(scene.sh)
+    gid = np.empty(n, np.int32)
+    u = np.empty(n, np.float32)
+    v = np.empty(n, np.float32)
+    z = np.empty(n, np.float32)
+    conic = np.empty((n, 3), np.float32)
+    radius = np.empty(n, np.float32)
+    rect = np.empty((n, 4), np.int32)
+    rgb = np.empty((n, 3), np.float32)
+    opac = np.empty(n, np.float32)
+    cov = np.empty((n, 3), np.float32)
+    diag = np.zeros(4, np.int64)
+    vc, pc = _view_c(view), params.c()
+    cnt = lib().oracle_project(ctypes.c_int64(n), _p(pos), _p(quat), _p(scale), _p(op), _p(sh),
+                               ctypes.c_int32(scene.sh_degree), ctypes.byref(vc), ctypes.byref(pc),
+                               _p(gid), _p(u), _p(v), _p(z), _p(conic), _p(radius), _p(rect), _p(rgb),
+                               _p(opac), _p(cov), _p(diag))
+    return dict(gid=gid[:cnt].copy(), u=u[:cnt].copy(), v=v[:cnt].copy(), z=z[:cnt].copy(),
+                conic=conic[:cnt].copy(), radius=radius[:cnt].copy(), rect=rect[:cnt].copy(),
+                rgb=rgb[:cnt].copy(), opacity=opac[:cnt].copy(), cov=cov[:cnt].copy(),
+                diag=dict(near=int(diag[0]), transparent=int(diag[1]), degenerate=int(diag[2]),
+                          offscreen=int(diag[3])))
+
+
+def tiles(view):
+    return (view.width + 15) // 16, (view.height + 15) // 16
+
+
+def bin_keys(rec, view) -> Dict[str, np.ndarray]:
+    """O11: sorted (tile, depth_bits, gid) keys, their record index, ranges [T][2]."""
+    tx, ty = tiles(view)
+    cnt = len(rec["gid"])
+    rect = np.ascontiguousarray(rec["rect"], np.int32)
+    P = int(lib().oracle_count_pairs(ctypes.c_int64(cnt), _p(rect)))
+    kt = np.empty(P, np.uint32)
+    kd = np.empty(P, np.uint32)
+    kg = np.empty(P, np.uint32)
+    kr = np.empty(P, np.uint32)
+    ranges = np.empty((tx * ty, 2), np.uint32)
+    lib().oracle_bin(ctypes.c_int64(cnt), _p(np.ascontiguousarray(rec["gid"])), _p(_c32(rec["z"])), _p(rect),
+                     ctypes.c_int32(tx), ctypes.c_int32(ty), _p(kt), _p(kd), _p(kg), _p(kr), _p(ranges))
+    return dict(tile=kt, depth=kd, gid=kg, rec=kr, ranges=ranges)
+
+
+def _alloc_images(view, D):
+    H, W = view.height, view.width
+    return (np.zeros((3, H, W), np.float32), np.zeros((H, W), np.float32), np.zeros((H, W), np.float32),
+            np.zeros((max(D, 0), H, W), np.float32), np.zeros((H, W), np.uint8))
+
+
+def _feat(scene_or_feat, D):
+    if D == 0:
+        return np.zeros(1, np.float32)
+    return _c32(scene_or_feat)
+
+
+def composite(view, rec, keys, feat=None, params: Optional[Params] = None) -> Dict[str, np.ndarray]:
+    """O12 + O14 over the binned lists."""
+    params = params or Params()
+    D = 0 if feat is None else int(feat.shape[1])
+    rgb, depth, alpha, F, flags = _alloc_images(view, D)
+    counters = np.zeros(2, np.int64)
+    vc, pc = _view_c(view), params.c()
+    lib().oracle_composite(ctypes.byref(vc), ctypes.byref(pc), _p(_c32(rec["u"])), _p(_c32(rec["v"])),
+                           _p(_c32(rec["conic"])), _p(_c32(rec["opacity"])), _p(_c32(rec["rgb"])),
+                           _p(_c32(rec["z"])), _p(np.ascontiguousarray(rec["gid"], np.int32)), _p(_feat(feat, D)),
+                           ctypes.c_int32(D), _p(keys["rec"]), _p(keys["ranges"]), _p(rgb), _p(depth), _p(alpha),
+                           _p(F), _p(flags), _p(counters))
+    return dict(rgb=rgb, depth=depth, alpha=alpha, feat=F, flags=flags, evals=int(counters[0]),
+                blends=int(counters[1]))
+
+
+def brute_force(view, rec, feat=None, params: Optional[Params] = None) -> Dict[str, np.ndarray]:
+    """Per-pixel brute force over all records (plain definition)."""
+    params = params or Params()
+    D = 0 if feat is None else int(feat.shape[1])
+    rgb, depth, alpha, F, flags = _alloc_images(view, D)
+    vc, pc = _view_c(view), params.c()
+    cnt = len(rec["gid"])
+    lib().oracle_brute_force(ctypes.byref(vc), ctypes.byref(pc), ctypes.c_int64(cnt), _p(_c32(rec["u"])),
+                             _p(_c32(rec["v"])), _p(_c32(rec["conic"])), _p(_c32(rec["opacity"])),
+                             _p(_c32(rec["rgb"])), _p(_c32(rec["z"])),
+                             _p(np.ascontiguousarray(rec["gid"], np.int32)),
+                             _p(np.ascontiguousarray(rec["rect"], np.int32)), _p(_feat(feat, D)), ctypes.c_int32(D),
+                             _p(rgb), _p(depth), _p(alpha), _p(F), _p(flags))
+    return dict(rgb=rgb, depth=depth, alpha=alpha, feat=F, flags=flags)
+
+
+def backproject(view, depth, alpha, a_min: float = 0.5, flags=None):
+    """O13: rendered depth -> world points; returns xyz [3][H][W], valid [H][W], flags."""
+    H, W = view.height, view.width
+    xyz = np.zeros((3, H, W), np.float32)
+    valid = np.zeros((H, W), np.uint8)
+    fl = np.zeros((H, W), np.uint8) if flags is None else np.ascontiguousarray(flags, np.uint8).copy()
+    vc = _view_c(view)
+    lib().oracle_backproject(ctypes.byref(vc), _p(_c32(depth)), _p(_c32(alpha)), ctypes.c_float(a_min),
+                             _p(xyz), _p(valid), _p(fl))
+    return xyz, valid, fl
+
+
+def render(scene, view, params: Optional[Params] = None, a_min: Optional[float] = None):
+    """Full oracle pipeline for one view: project -> bin -> composite (-> backproject)."""
+    rec = project(scene, view, params)
+    keys = bin_keys(rec, view)
+    img = composite(view, rec, keys, scene.feat, params)
+    out = dict(rec=rec, keys=keys, **img)
+    if a_min is not None:
+        xyz, valid, fl = backproject(view, img["depth"], img["alpha"], a_min, img["flags"])
+        out.update(xyz=xyz, valid=valid, flags=fl)
+    return out
+
+
+def sh_color(deg: int, coeff, direction) -> np.ndarray:
+    """O10 for one direction (fp64): coeff [(deg+1)^2][3]."""
+    c = np.ascontiguousarray(coeff, np.float64).reshape(-1)
+    d = np.ascontiguousarray(direction, np.float64).reshape(3)
+    out = np.zeros(3, np.float64)
+    lib().oracle_sh_color(ctypes.c_int32(deg), _p(c), _p(d), _p(out))
+    return out
