@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 3DGS forward-rasterizer hot path (Hi^2-GSLoc).
+
+One step = the whole hot path (gs_project -> gs_bin_sort -> gs_rasterize ->
+gs_backproject) over one batch of views.  Default workload:
+BASELINE.json configs[3] "C4" -- 5M-Gaussian aerial scene (SH 3, D = 32
+features), 256 sampled 1024x768 poses, on one GPU.  Synthetic seeded data
+(synth/), no trained weights.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config C4] [--scale 1.0]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+  python bench.py --impl reference      # the CPU oracle (the reference arm)
+
+Rank 0 prints ONE JSON line.  See DESIGN.md §6 for the metric definitions.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "Mpixels/s and ms/view (RGB+depth)"
+UNIT = "Mpixels/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--scale", type=float, default=1.0, help="Gaussian-count scale (1.0 = BASELINE size)")
+    ap.add_argument("--views", type=int, default=0, help="limit views per rank (0 = config's batch)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--gather", action="store_true", help="NCCL all_gather of RGB+depth+opacity (N>1)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-views", type=int, default=2)
+    ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run only this many untimed steps")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- helpers
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(config_key: str):
+    """DRAM bytes per gs_rasterize launch from a committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(config_key)
+    return None if e is None else e.get("rasterize_dram_bytes_per_launch")
+
+
+def workload(cfg: str, scale: float, rank: int, world: int, scaling: str, views_limit: int):
+    import synth
+    scene, views = synth.make_config(cfg, scale=scale)
+    if cfg == "C4" and scaling == "weak" and world > 1 and rank > 0:
+        # weak scaling: every rank renders its own full 256-pose batch (rank-seeded poses)
+        ext = 1000.0 * math.sqrt(scale)
+        views = synth.c4_views(extent=ext, seed=4 + 1000 * rank)
+    return scene, views
+
+
+def algorithmic_raster_bytes(n_pairs: int, n_visible: int, total_pixels: int, D: int) -> int:
+    """P*4 (sorted list) + V*(48 + 4D) (records + features,
+    read once) + H*W*(5 + D)*4 (planar outputs)."""
+    return 4 * n_pairs + n_visible * (48 + 4 * D) + total_pixels * (5 + D) * 4
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return 0
+    import oracle
+    import synth
+    scene, views = synth.make_config(args.config, scale=args.scale)
+    oracle.build()
+    n = len(views)
+    times = []
+    pix = 0
+    for s in range(args.warmup + args.steps):
+        v = views[(s * 37) % n]
+        t0 = time.perf_counter()
+        oracle.render(scene, v, a_min=0.5)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            pix += v.width * v.height
+    total = sum(times)
+    value = pix / total / 1e6
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": 0, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "ms_per_view": 1e3 * total / args.steps,
+           "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic", "config": {"workload": args.config, "scale": args.scale},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": f"1 view of the {n}-view {args.config} batch per step (single-threaded C++ oracle)"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def cpu_baseline(scene, views, n_sample: int):
+    import oracle
+    oracle.build()
+    n = len(views)
+    pick = [(k * 97) % n for k in range(n_sample)]
+    t0 = time.perf_counter()
+    pix = 0
+    for i in pick:
+        oracle.render(scene, views[i], a_min=0.5)
+        pix += views[i].width * views[i].height
+    dt = time.perf_counter() - t0
+    return {"value": pix / dt / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n_sample} of {n} views (project+bin+composite+backproject, single-threaded), {dt:.1f} s"}
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2507_15683_b200 as G
+    from paper_2507_15683_b200 import dist as GD
+
+    rank, world, local = GD.env_rank_world()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    scene, views_all = workload(args.config, args.scale, rank, world, args.scaling, args.views)
+    if args.scaling == "strong" and world > 1:
+        my = GD.shard_views(len(views_all), world, rank)
+        views = [views_all[i] for i in my]
+    else:
+        views = views_all
+    if args.views:
+        views = views[:args.views]
+    ds = G.DeviceScene(scene, device=dev)
+    r = G.Renderer(ds, views, device=dev, backproject=True)
+    r.render()
+    r.fit_capacities()
+    r.render()
+    torch.cuda.synchronize()
+    n_pairs = r.n_pairs()
+    n_visible = int(r.proj.n_rec.sum().item())
+    total_px = r.vb.total_pixels
+    n_views = r.vb.n
+    stream = torch.cuda.current_stream()
+
+    if args.profile_steps:
+        for _ in range(args.profile_steps):
+            r.run()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    gather_payload = None
+    if args.gather and world > 1:
+        hw = views[0].width * views[0].height
+        pad = max(GD.shard_sizes(len(views_all), world)) if args.scaling == "strong" else n_views
+
+    def step():
+        r.run(stream)
+        if args.gather and world > 1:
+            p = GD.pack_planes(r.images.rgb, r.images.depth, r.images.alpha, n_views, hw, pad)
+            GD.gather_planes(p, world)
+
+    # warm-up
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # timed region: CUDA events on the launching stream, per-stage events for the roofline
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device() if world == 1 else local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        start.record(stream)
+        for k in range(K):
+            e = ev[k]
+            r.proj.status.zero_()
+            e[0].record(stream)
+            G.gs_project(r.scene, r.vb, r.params, r.proj, r.ws_proj, stream, scene_struct=r.scene_struct)
+            e[1].record(stream)
+            G.gs_bin_sort(r.proj, r.vb, r.bins, r.ws_bin, stream)
+            e[2].record(stream)
+            G.gs_rasterize(r.scene, r.proj, r.bins, r.vb, r.params, r.images, stream)
+            e[3].record(stream)
+            G.gs_backproject(r.images, r.vb, r.a_min, r.xyz, r.valid, stream)
+            e[4].record(stream)
+            if args.gather and world > 1:
+                GD.gather_planes(GD.pack_planes(r.images.rgb, r.images.depth, r.images.alpha, n_views, hw, pad),
+                                 world)
+        end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    assert r.status() == 0, "capacity overflow inside the timed region"
+    ms_total = start.elapsed_time(end)
+    stage = np.array([[ev[k][j].elapsed_time(ev[k][j + 1]) for j in range(4)] for k in range(K)])
+    stage_ms = stage.mean(axis=0)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        tot_px = torch.tensor([float(total_px)], device=dev)
+        dist.all_reduce(tot_px, op=dist.ReduceOp.SUM)
+        all_px = float(tot_px.item())
+        tv = torch.tensor([float(n_views)], device=dev)
+        dist.all_reduce(tv, op=dist.ReduceOp.SUM)
+        all_views = float(tv.item())
+    else:
+        all_px, all_views = float(total_px), float(n_views)
+    ms_step = ms_total / K
+    value = all_px * K / (ms_total / 1e3) / 1e6
+
+    # e2e through the public API with host buffers: H2D of the pose batch from pinned
+    # memory + the hot path + D2H of RGB + depth + opacity into pinned memory.
+    e2e = None
+    if not args.no_e2e:
+        host_out = torch.empty(5 * total_px, dtype=torch.float32, pin_memory=True)
+        Ke = max(2, min(K, 5))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(Ke):
+            r.vb.upload()
+            r.run(stream)
+            host_out[:3 * total_px].copy_(r.images.rgb, non_blocking=True)
+            host_out[3 * total_px:4 * total_px].copy_(r.images.depth, non_blocking=True)
+            host_out[4 * total_px:].copy_(r.images.alpha, non_blocking=True)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        ms_e = s0.elapsed_time(s1)
+        if world > 1:
+            t = torch.tensor([ms_e], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e = float(t.item())
+        e2e = {"value": all_px * Ke / (ms_e / 1e3) / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": int(r.vb.pinned.numel()), "d2h_bytes_per_step": int(5 * total_px * 4)}
+        del host_out
+
+    # roofline of the dominant kernel
+    peak, peak_src = measured_peaks()
+    dom = int(np.argmax(stage_ms))
+    names = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_backproject"]
+    D = scene.feat_dim
+    raster_bytes = algorithmic_raster_bytes(n_pairs, n_visible, total_px, D)
+    achieved = raster_bytes / (stage_ms[2] / 1e3) / 1e9
+    traffic = ncu_traffic(f"{args.config}@{args.scale}")
+    roof = {"bound": "hbm", "kernel": "gs_rasterize", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": raster_bytes, "dominant_stage": names[dom]}
+    launches_per_step = (3 if ds.n_blocks else 2) + 7 + 1 + 1
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+           "ms_per_step": ms_step, "ms_per_view": ms_step * world / all_views if args.scaling == "strong" else
+           ms_step / n_views, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+           "dtype": "f32", "data": "synthetic",
+           "config": {"workload": args.config, "scale": args.scale, "gaussians": scene.n, "views_per_rank": n_views,
+                      "resolution": f"{views[0].width}x{views[0].height}", "sh_degree": scene.sh_degree,
+                      "feat_dim": D, "l2": "inputs larger than L2 (scene %.2f GB, %.1f GB written per step)" % (
+                          ds.nbytes() / 1e9, (total_px * (5 + D) * 4 + total_px * 13) / 1e9),
+                      "gather": bool(args.gather and world > 1)},
+           "stages_ms": {n: float(m) for n, m in zip(names, stage_ms)},
+           "counts": {"visible_records": n_visible, "pairs": n_pairs, "pixels": total_px},
+           "roofline": roof, "gpu_launches": launches_per_step * K, "e2e": e2e, "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(scene, views, args.cpu_sample_views)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,259 @@
+/*
+ * gs.h -- C ABI of the B200 (sm_100a) 3D Gaussian Splatting forward rasterizer,
+ * the data-parallel hot path of Hi^2-GSLoc (arXiv 2507.15683).
+ *
+ * Citations: P:<n> = PAPER.md line n (section / equation / algorithm named),
+ * S:<n> = SPEC.md line n, Q<n> = reading n in DESIGN.md §2.
+ *
+ * The hot path is four calls, each batched over poses and pyramid levels
+ * ("views"):
+ *
+ *   gs_project     -> per (view, Gaussian): camera transform, cull, EWA 2D
+ *                     covariance + conic + radius, tile rectangle, SH colour
+ *                     (Alg. 1 l.9-12; "tile-based rasterization";
+ *                     P:134 Theta_i).
+ *   gs_bin_sort    -> duplicate records into (16x16 tile, depth) pairs, order
+ *                     each tile's list by (depth_bits, gid), tile ranges
+ *                     ("Tile size 16x16; front-to-back sort by
+ *                     primitive depth per tile with stable index tiebreak").
+ *   gs_rasterize   -> per pixel front-to-back alpha compositing of colour,
+ *                     depth (sum w z), accumulated opacity A = 1 - T and an
+ *                     optional D-channel feature ("alpha blending",
+ *                     "identical rasterization"; "render dense feature and
+ *                     depth maps").
+ *   gs_backproject -> rendered depth -> world points for 2D-3D constraints
+ *                     ("fully leverage the depth information from
+ *                     Gaussian rendering for 3D constraints"; S:519 drop
+ *                     accum_alpha < 0.5).
+ *
+ * Conventions common to every call
+ * --------------------------------
+ * - All data pointers are DEVICE pointers unless the name ends in _host.
+ * - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   All work is enqueued asynchronously on it; no call synchronises the host.
+ * - The caller allocates and frees every buffer (outputs and workspaces).
+ *   The library never allocates device memory, never frees, and keeps no
+ *   pointer after a call returns.  Calls are stateless and re-entrant:
+ *   concurrent calls on different streams with distinct outputs/workspaces
+ *   are safe.  Inputs and outputs must not alias.
+ * - Return value: host-side validation result.  GS_OK means the work was
+ *   enqueued.  Validation never reads device memory.  On error nothing is
+ *   enqueued and gs_last_error() (thread-local) names the bad argument.
+ * - Data-dependent conditions are NOT errors: degenerate / near / transparent /
+ *   off-screen Gaussians are skipped and counted; capacity overflow
+ *   sets bits in the device status word and the required sizes, and every
+ *   later call of the batch that sees the bit writes nothing.  The caller
+ *   reads the status once per batch and re-runs with larger buffers.
+ * - Views of one batch own disjoint, contiguous slices of a flat pixel space
+ *   (pix_offset) and a flat tile space (tile_offset); gs_views_layout() fills
+ *   both.  Per view, images are planar: rgb [3][H][W] at 3*pix_offset,
+ *   depth/alpha [H][W] at pix_offset, feat [D][H][W] at D*pix_offset.
+ */
+#ifndef GS_H_
+#define GS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_ABI_VERSION 1
+#define GS_TILE 16           /* tile edge in pixels */
+#define GS_MAX_FEAT_DIM 64   /* D in [0, 64], D % 4 == 0 */
+#define GS_MAX_VIEWS 65535   /* view index is stored in 16 bits of a record */
+
+typedef enum gs_status {
+    GS_OK = 0,
+    GS_INVALID_ARG = 1,          /* NULL pointer, bad size, inconsistent layout */
+    GS_UNSUPPORTED = 2,          /* sh_degree > 3, D % 4 != 0, D > 64, too many views */
+    GS_WORKSPACE_TOO_SMALL = 3,  /* ws_bytes < the matching *_workspace_bytes() */
+    GS_CUDA_ERROR = 4            /* a launch failed; gs_last_error() has cudaGetErrorString */
+} gs_status;
+
+/* Device status word bits (gs_projected.status). */
+#define GS_STATUS_RECORD_OVERFLOW 0x1u  /* some view had > rec_capacity visible Gaussians */
+#define GS_STATUS_PAIR_OVERFLOW 0x2u    /* the batch had > pair_capacity tile pairs */
+
+/*
+ * Pinhole camera + pose.  R, t map WORLD points to CAMERA points:
+ * p = R x + t (Alg. 1 l.10 applies T_wc to world points; reading Q1).
+ * Camera axes: x right, y down, z forward.  Pixel (px, py) is centred at the
+ * integer coordinates (px, py) (Q4; S:44 maps (0,0,5) to pixel (50,50)).
+ */
+typedef struct gs_view {
+    float R[9];            /* row-major world->camera rotation */
+    float t[3];
+    float fx, fy, cx, cy;  /* K (pixels) */
+    int32_t width, height; /* image size (pixels), each in [1, 65535*16] */
+    int64_t pix_offset;    /* first pixel of this view in the batch pixel space */
+    uint32_t tile_offset;  /* first tile of this view in the batch tile space */
+    uint32_t reserved;     /* must be 0 */
+} gs_view;                 /* 88 bytes */
+
+/*
+ * Scene G: SoA planes of N Gaussians Theta_i = {mu, q, s, alpha, c, f}
+ * (P:134).  q is (w,x,y,z), normalised inside (Q2).  scale and
+ * opacity are linear, already-activated values (Q3).  Colour is real
+ * SH of degree 0..3 ([3DGS] basis; flat RGB c is degree 0 with
+ * k0 = (c - 0.5)/0.28209479177387814, Q23).  Features f are view-independent
+ * and blended unnormalised (Q18).
+ * Optional block partition (the cells of P:134, "divided into multiple
+ * cells"): Gaussians stored block-major; block b owns [block_offsets[b],
+ * block_offsets[b+1]); block_bounds[b] = {min x,y,z of centres, max x,y,z of
+ * centres, max scale component, 0}.  gs_project uses them only for a
+ * conservative per-(view, block) cull; results are identical with
+ * n_blocks = 0.  gs_scene_block_bounds() computes block_bounds.
+ */
+typedef struct gs_scene {
+    int64_t n;
+    int32_t sh_degree;             /* 0..3 */
+    int32_t feat_dim;              /* D: 0..64, multiple of 4 */
+    const float* pos;              /* [3][n] */
+    const float* quat;             /* [4][n] */
+    const float* scale;            /* [3][n] */
+    const float* opacity;          /* [n] */
+    const float* sh;               /* [(deg+1)^2 * 3][n]; row k*3+c = coefficient k of channel c */
+    const float* feat;             /* [n][D] row-major (NULL iff D == 0) */
+    int32_t n_blocks;              /* 0 = no partition */
+    int32_t reserved;
+    const int64_t* block_offsets;  /* [n_blocks + 1] */
+    const float* block_bounds;     /* [n_blocks][8] */
+} gs_scene;
+
+/* Readings Q5, Q7, Q6, Q14, Q15; gs_default_params() returns these. */
+typedef struct gs_params {
+    float z_near;        /* 0.2   near cull, scene units (Q5) */
+    float dilation;      /* 0.3   px^2 added to the 2D covariance diagonal (Q7) */
+    float clamp_margin;  /* 0.15  off-screen Jacobian guard, fraction of W/H (Q6) */
+    float alpha_min;     /* 1/255 skip threshold (Q14) */
+    float alpha_max;     /* 0.99  opacity clamp (Q14) */
+    float t_min;         /* 1e-4  stop before blending when T(1-alpha) < t_min (Q15) */
+} gs_params;
+
+/*
+ * One projected (view, Gaussian) record, 64 bytes.  u, v, z, conic, rect,
+ * radius are computed in IEEE fp32 in the operation order of DESIGN.md §4.1
+ * (bit-identical to the oracle); rgb is SH colour (tolerance only); ext_x/y
+ * are the half-extents of the bounding box of the alpha >= alpha_min ellipse,
+ * inflated by a safety margin (used only to skip provably-zero work).
+ */
+typedef struct gs_record {
+    float u, v;                       /* pixel-space mean */
+    float conic_a, conic_b, conic_c;  /* inverse 2D covariance (a, b; b, c) */
+    float opacity;
+    float ext_x, ext_y;
+    float rgb[3];
+    float z;                          /* camera-space depth (depth key = its bits, O9) */
+    uint32_t gid;                     /* Gaussian index in the scene */
+    uint32_t view_radius;             /* view (low 16 bits) | min(radius, 65535) << 16 */
+    uint16_t x0, x1, y0, y1;          /* inclusive tile rectangle in the view's tile grid */
+} gs_record;
+
+typedef struct gs_projected {
+    gs_record* rec;          /* [n_views * rec_capacity]; view v owns slots [v*cap, v*cap + n_rec[v]) */
+    int64_t rec_capacity;    /* records per view */
+    uint32_t* n_rec;         /* [n_views] visible count (may exceed cap: = required capacity) */
+    uint64_t* diag;          /* [4] += near, transparent, degenerate, off-screen (Gaussians
+                                skipped by the block cull are not visited and not counted) */
+    uint32_t* status;        /* [1] GS_STATUS_* bits; caller zeroes before the batch */
+} gs_projected;
+
+typedef struct gs_bins {
+    uint32_t* ranges;        /* [total_tiles][2]: [start, end) into sorted_rec (lower bound, Q13) */
+    uint32_t* sorted_rec;    /* [pair_capacity] record slot of each pair, ordered by
+                                (tile in batch, depth_bits, gid) (Q12, Q22) */
+    int64_t pair_capacity;
+    uint64_t* n_pairs;       /* [1] pairs in the batch (= required capacity on overflow) */
+    uint64_t* sorted_key;    /* optional [pair_capacity]: (tile in batch << 32) | depth_bits */
+} gs_bins;
+
+typedef struct gs_images {
+    float* rgb;     /* [3 * total_pixels] */
+    float* depth;   /* [total_pixels]  sum of w z (un-normalised, Q16) */
+    float* alpha;   /* [total_pixels]  A = 1 - T_final */
+    float* feat;    /* [D * total_pixels] or NULL when D == 0 */
+} gs_images;
+
+/* ---------------------------------------------------------------------- */
+
+/* Library ABI version (GS_ABI_VERSION). */
+int32_t gs_abi_version(void);
+
+/* Thread-local description of the last non-OK status (never NULL). */
+const char* gs_last_error(void);
+
+/* Defaults of the readings Q5-Q7, Q14, Q15. */
+gs_params gs_default_params(void);
+
+/*
+ * Fill pix_offset / tile_offset of views_host[0..n_views) contiguously in view
+ * order and return the batch totals.  Host only; no device access.
+ * Errors: GS_INVALID_ARG for NULL pointers, n_views < 1 or bad image sizes;
+ * GS_UNSUPPORTED if n_views > GS_MAX_VIEWS or total tiles >= 2^31.
+ */
+gs_status gs_views_layout(gs_view* views_host, int32_t n_views, int64_t* total_pixels,
+                          int64_t* total_tiles);
+
+/*
+ * block_bounds_out[b] = {min centre xyz, max centre xyz, max scale, 0} for
+ * every block of `scene` (its block_bounds field is ignored).  Not on the
+ * hot path: call once after loading a partitioned scene.
+ */
+gs_status gs_scene_block_bounds(const gs_scene* scene, float* block_bounds_out, void* stream);
+
+/* Workspace of gs_project: a (view x block) visibility bitmask. */
+size_t gs_project_workspace_bytes(int32_t n_blocks, int32_t n_views);
+
+/*
+ * gs_project -- O1-O10 for every (view, Gaussian) of the batch.
+ * views_host and views_dev hold identical contents (host copy for
+ * validation/launch sizing, device copy for the kernels).  Writes the
+ * visible records of view v to out->rec[v*cap ...] in an unspecified order
+ * (the sort makes the result canonical), n_rec[v], diag; sets
+ * GS_STATUS_RECORD_OVERFLOW if a view has more than rec_capacity.
+ * out->n_rec and out->diag are overwritten (zeroed by this call).
+ */
+gs_status gs_project(const gs_scene* scene, const gs_view* views_host, const gs_view* views_dev,
+                     int32_t n_views, const gs_params* params, gs_projected* out, void* ws,
+                     size_t ws_bytes, void* stream);
+
+/* Workspace of gs_bin_sort for a batch of total_tiles tiles and pair_capacity pairs. */
+size_t gs_bin_sort_workspace_bytes(int64_t pair_capacity, int64_t total_tiles);
+
+/*
+ * gs_bin_sort -- O11: one pair per tile of each record's rectangle, each
+ * tile's pairs ordered by (depth_bits, gid) ascending (Q12), lower-bound
+ * ranges (Q13).  The pair list and ranges are bit-identical to the oracle's
+ * and run-to-run deterministic.  Sets GS_STATUS_PAIR_OVERFLOW (and n_pairs)
+ * if the batch needs more than pair_capacity pairs.
+ */
+gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const gs_view* views_dev,
+                      int32_t n_views, gs_bins* out, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * gs_rasterize -- O12: for every pixel of every view, front to back over its
+ * tile's list: power = -0.5(ca dx^2 + cc dy^2) - cb dx dy, skip if > 0;
+ * alpha = min(alpha_max, o exp(power)), skip if < alpha_min;
+ * Tn = T(1 - alpha), stop before blending if Tn < t_min;
+ * C += w rgb, Dz += w z, F += w f with w = alpha T; T = Tn.  A = 1 - T.
+ * Every output pixel is written (background 0).  `scene` supplies feat / D.
+ */
+gs_status gs_rasterize(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins,
+                       const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
+                       const gs_params* params, gs_images* out, void* stream);
+
+/*
+ * gs_backproject -- O13: valid iff A >= a_min and Dz/A > 0;
+ * X = R^T(((px - cx)/fx zbar, (py - cy)/fy zbar, zbar) - t), zbar = Dz/A.
+ * xyz is planar [3][H][W] per view at 3*pix_offset; invalid pixels get
+ * X = 0 and valid = 0.
+ */
+gs_status gs_backproject(const gs_images* in, const gs_view* views_host, const gs_view* views_dev,
+                         int32_t n_views, float a_min, float* xyz, uint8_t* valid, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GS_H_ */

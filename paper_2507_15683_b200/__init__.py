@@ -1,0 +1,14 @@
+"""B200-native (sm_100a) 3DGS forward rasterizer -- the data-parallel hot path
+of Hi^2-GSLoc (arXiv 2507.15683).  See include/gs.h and DESIGN.md.
+
+The compute path is ``libgs.so`` (hand-written CUDA for sm_100a); this package
+is the thin binding (``gs``), a buffer-managing batch harness (``pipeline``)
+and the multi-GPU pose-sharding host logic (``dist``).  There is no CPU
+fallback.
+"""
+from .gs import (GSError, DeviceScene, ViewBatch, Projected, Bins, Images, default_params,  # noqa: F401
+                 gs_project, gs_bin_sort, gs_rasterize, gs_backproject, lib, LIB_PATH, EXPORTS)
+from .pipeline import Renderer  # noqa: F401
+
+__all__ = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_backproject", "DeviceScene", "ViewBatch",
+           "Projected", "Bins", "Images", "Renderer", "default_params", "GSError"]

@@ -1,0 +1,115 @@
+// gs_api.cu -- host-side helpers of the C ABI (include/gs.h): version, error
+// string, default parameters, batch layout, argument validation.
+#include <cmath>
+#include <cstring>
+
+#include "gs_common.cuh"
+
+namespace gs {
+
+static thread_local char g_err[512] = "no error";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+gs_status validate_views(const gs_view* vh, const gs_view* vd, int32_t n_views, int64_t* total_pixels,
+                         int64_t* total_tiles) {
+    GS_REQUIRE(vh != nullptr, GS_INVALID_ARG, "views_host is NULL");
+    GS_REQUIRE(vd != nullptr, GS_INVALID_ARG, "views_dev is NULL");
+    GS_REQUIRE(n_views >= 1, GS_INVALID_ARG, "n_views = %d < 1", n_views);
+    GS_REQUIRE(n_views <= GS_MAX_VIEWS, GS_UNSUPPORTED, "n_views = %d > %d", n_views, GS_MAX_VIEWS);
+    int64_t pix = 0, tiles = 0;
+    for (int32_t i = 0; i < n_views; ++i) {
+        const gs_view& v = vh[i];
+        GS_REQUIRE(v.width >= 1 && v.height >= 1 && v.width <= 65535 * 16 && v.height <= 65535 * 16,
+                   GS_INVALID_ARG, "views[%d]: bad image size %dx%d", i, v.width, v.height);
+        GS_REQUIRE(std::isfinite(v.fx) && std::isfinite(v.fy) && v.fx > 0.f && v.fy > 0.f &&
+                       std::isfinite(v.cx) && std::isfinite(v.cy),
+                   GS_INVALID_ARG, "views[%d]: bad intrinsics", i);
+        for (int k = 0; k < 9; ++k)
+            GS_REQUIRE(std::isfinite(v.R[k]), GS_INVALID_ARG, "views[%d].R[%d] not finite", i, k);
+        for (int k = 0; k < 3; ++k)
+            GS_REQUIRE(std::isfinite(v.t[k]), GS_INVALID_ARG, "views[%d].t[%d] not finite", i, k);
+        GS_REQUIRE(v.pix_offset == pix, GS_INVALID_ARG,
+                   "views[%d].pix_offset = %lld, expected %lld (use gs_views_layout)", i,
+                   (long long)v.pix_offset, (long long)pix);
+        GS_REQUIRE((int64_t)v.tile_offset == tiles, GS_INVALID_ARG,
+                   "views[%d].tile_offset = %u, expected %lld (use gs_views_layout)", i, v.tile_offset,
+                   (long long)tiles);
+        pix += (int64_t)v.width * v.height;
+        tiles += (int64_t)tiles_x(v) * tiles_y(v);
+    }
+    GS_REQUIRE(tiles < (int64_t(1) << 31), GS_UNSUPPORTED, "total tiles %lld >= 2^31", (long long)tiles);
+    if (total_pixels) *total_pixels = pix;
+    if (total_tiles) *total_tiles = tiles;
+    return GS_OK;
+}
+
+gs_status validate_scene(const gs_scene* s, bool need_geometry) {
+    GS_REQUIRE(s != nullptr, GS_INVALID_ARG, "scene is NULL");
+    GS_REQUIRE(s->n >= 0 && s->n < (int64_t(1) << 32), GS_INVALID_ARG, "scene->n = %lld out of range",
+               (long long)s->n);
+    GS_REQUIRE(s->sh_degree >= 0 && s->sh_degree <= 3, GS_UNSUPPORTED, "sh_degree = %d not in 0..3",
+               s->sh_degree);
+    GS_REQUIRE(s->feat_dim >= 0 && s->feat_dim <= GS_MAX_FEAT_DIM && s->feat_dim % 4 == 0, GS_UNSUPPORTED,
+               "feat_dim = %d (need 0..64, multiple of 4)", s->feat_dim);
+    GS_REQUIRE(s->feat_dim == 0 || s->feat != nullptr || s->n == 0, GS_INVALID_ARG,
+               "feat_dim = %d but feat is NULL", s->feat_dim);
+    if (need_geometry && s->n > 0) {
+        GS_REQUIRE(s->pos && s->quat && s->scale && s->opacity && s->sh, GS_INVALID_ARG,
+                   "scene geometry pointer is NULL");
+    }
+    GS_REQUIRE(s->n_blocks >= 0, GS_INVALID_ARG, "n_blocks = %d < 0", s->n_blocks);
+    if (s->n_blocks > 0 && need_geometry) {
+        GS_REQUIRE(s->block_offsets && s->block_bounds, GS_INVALID_ARG,
+                   "n_blocks = %d but block_offsets/block_bounds is NULL", s->n_blocks);
+    }
+    return GS_OK;
+}
+
+}  // namespace gs
+
+extern "C" {
+
+int32_t gs_abi_version(void) { return GS_ABI_VERSION; }
+
+const char* gs_last_error(void) { return gs::g_err; }
+
+gs_params gs_default_params(void) {
+    gs_params p;
+    p.z_near = 0.2f;
+    p.dilation = 0.3f;
+    p.clamp_margin = 0.15f;
+    p.alpha_min = 1.0f / 255.0f;
+    p.alpha_max = 0.99f;
+    p.t_min = 1e-4f;
+    return p;
+}
+
+gs_status gs_views_layout(gs_view* views_host, int32_t n_views, int64_t* total_pixels, int64_t* total_tiles) {
+    GS_REQUIRE(views_host != nullptr, GS_INVALID_ARG, "views_host is NULL");
+    GS_REQUIRE(n_views >= 1, GS_INVALID_ARG, "n_views = %d < 1", n_views);
+    GS_REQUIRE(n_views <= GS_MAX_VIEWS, GS_UNSUPPORTED, "n_views = %d > %d", n_views, GS_MAX_VIEWS);
+    int64_t pix = 0, tiles = 0;
+    for (int32_t i = 0; i < n_views; ++i) {
+        gs_view& v = views_host[i];
+        GS_REQUIRE(v.width >= 1 && v.height >= 1 && v.width <= 65535 * 16 && v.height <= 65535 * 16,
+                   GS_INVALID_ARG, "views[%d]: bad image size %dx%d", i, v.width, v.height);
+        GS_REQUIRE(tiles < (int64_t(1) << 31), GS_UNSUPPORTED, "total tiles >= 2^31");
+        v.pix_offset = pix;
+        v.tile_offset = (uint32_t)tiles;
+        v.reserved = 0;
+        pix += (int64_t)v.width * v.height;
+        tiles += (int64_t)gs::tiles_x(v) * gs::tiles_y(v);
+    }
+    GS_REQUIRE(tiles < (int64_t(1) << 31), GS_UNSUPPORTED, "total tiles %lld >= 2^31", (long long)tiles);
+    if (total_pixels) *total_pixels = pix;
+    if (total_tiles) *total_tiles = tiles;
+    return GS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// gs_backproject.cu -- O13: rendered depth -> world points.
+// P:278 "we fully leverage the depth information from Gaussian rendering for
+// 3D constraints ... 2D-3D PnP algorithm with RANSAC"; S:492 back-project each
+// matched rendered pixel via rendered depth; "matches with accum_alpha
+// < 0.5 at that pixel are discarded"; readings Q16, Q24.
+//
+// A streaming HBM-bound pass: per pixel read depth + alpha (8 B), write xyz
+// (12 B) + valid (1 B).  One thread per 4 consecutive pixels of a row-major
+// view (float4 loads / stores when aligned), views on grid.y.
+#include "gs_common.cuh"
+
+namespace gs {
+namespace {
+
+__device__ __forceinline__ void bp_pixel(const gs_view& V, float Dz, float A, float a_min, int px, int py, float& X,
+                                         float& Y, float& Z, uint8_t& ok) {
+    // validity decided in fp32 on the fp32 A (same precision as the oracle)
+    const bool valid = A >= a_min && (Dz / A) > 0.0f;
+    if (!valid) { X = Y = Z = 0.f; ok = 0; return; }
+    const float zb = Dz / A;
+    const float c0 = ((float)px - V.cx) / V.fx * zb - V.t[0];
+    const float c1 = ((float)py - V.cy) / V.fy * zb - V.t[1];
+    const float c2 = zb - V.t[2];
+    X = V.R[0] * c0 + V.R[3] * c1 + V.R[6] * c2;
+    Y = V.R[1] * c0 + V.R[4] * c1 + V.R[7] * c2;
+    Z = V.R[2] * c0 + V.R[5] * c1 + V.R[8] * c2;
+    ok = 1;
+}
+
+__global__ void __launch_bounds__(256)
+backproject_kernel(const gs_view* __restrict__ views, const float* __restrict__ depth,
+                   const float* __restrict__ alpha, float a_min, float* __restrict__ xyz,
+                   uint8_t* __restrict__ valid) {
+    const gs_view V = views[blockIdx.y];
+    const int64_t HW = (int64_t)V.width * V.height;
+    const int64_t base = V.pix_offset;
+    const float* dz = depth + base;
+    const float* al = alpha + base;
+    float* ox = xyz + 3 * base;
+    uint8_t* ov = valid + base;
+    const bool vec = ((base & 3) == 0) && ((HW & 3) == 0);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q * 4 < HW; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p0 = q * 4;
+        if (vec) {
+            const float4 d4 = __ldcs(reinterpret_cast<const float4*>(dz + p0));
+            const float4 a4 = __ldcs(reinterpret_cast<const float4*>(al + p0));
+            float X[4], Y[4], Z[4];
+            uint8_t ok[4];
+            const float dd[4] = {d4.x, d4.y, d4.z, d4.w}, aa[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t p = p0 + k;
+                bp_pixel(V, dd[k], aa[k], a_min, (int)(p % V.width), (int)(p / V.width), X[k], Y[k], Z[k], ok[k]);
+            }
+            __stcs(reinterpret_cast<float4*>(ox + p0), make_float4(X[0], X[1], X[2], X[3]));
+            __stcs(reinterpret_cast<float4*>(ox + HW + p0), make_float4(Y[0], Y[1], Y[2], Y[3]));
+            __stcs(reinterpret_cast<float4*>(ox + 2 * HW + p0), make_float4(Z[0], Z[1], Z[2], Z[3]));
+            const uint32_t packed = (uint32_t)ok[0] | ((uint32_t)ok[1] << 8) | ((uint32_t)ok[2] << 16) |
+                                    ((uint32_t)ok[3] << 24);
+            *reinterpret_cast<uint32_t*>(ov + p0) = packed;
+        } else {
+            for (int k = 0; k < 4 && p0 + k < HW; ++k) {
+                const int64_t p = p0 + k;
+                float X, Y, Z;
+                uint8_t ok;
+                bp_pixel(V, dz[p], al[p], a_min, (int)(p % V.width), (int)(p / V.width), X, Y, Z, ok);
+                ox[p] = X; ox[HW + p] = Y; ox[2 * HW + p] = Z;
+                ov[p] = ok;
+            }
+        }
+    }
+}
+
+}  // namespace
+}  // namespace gs
+
+using namespace gs;
+
+extern "C" gs_status gs_backproject(const gs_images* in, const gs_view* views_host, const gs_view* views_dev,
+                                    int32_t n_views, float a_min, float* xyz, uint8_t* valid, void* stream) {
+    int64_t total_pixels = 0, T = 0;
+    gs_status st = validate_views(views_host, views_dev, n_views, &total_pixels, &T);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(in && in->depth && in->alpha, GS_INVALID_ARG, "images depth/alpha is NULL");
+    GS_REQUIRE(xyz && valid, GS_INVALID_ARG, "xyz/valid is NULL");
+    GS_REQUIRE(a_min == a_min, GS_INVALID_ARG, "a_min is NaN");
+    GS_REQUIRE(((uintptr_t)xyz & 15) == 0 && ((uintptr_t)in->depth & 15) == 0 && ((uintptr_t)in->alpha & 15) == 0 &&
+                   ((uintptr_t)valid & 3) == 0,
+               GS_INVALID_ARG, "xyz/depth/alpha must be 16-byte and valid 4-byte aligned");
+    int64_t maxhw = 0;
+    for (int i = 0; i < n_views; ++i) maxhw = std::max<int64_t>(maxhw, (int64_t)views_host[i].width * views_host[i].height);
+    const int64_t quads = (maxhw + 3) / 4;
+    int64_t gx = (quads + 255) / 256;
+    const int64_t target = std::max<int64_t>(1, (int64_t)num_sms() * 8 / n_views);
+    gx = std::min(gx, std::max<int64_t>(target, 1));
+    dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)n_views);
+    backproject_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(views_dev, in->depth, in->alpha, a_min, xyz, valid);
+    return check_launch("backproject_kernel");
+}

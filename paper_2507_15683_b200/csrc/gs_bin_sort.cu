@@ -1,0 +1,439 @@
+// gs_bin_sort.cu -- O11: duplicate each projected record
+// into one pair per 16x16 tile of its rectangle, order every tile's pairs by
+// (depth_bits, gid) and emit lower-bound tile ranges.  P:132 "tile-based
+// rasterization"; "Tile size 16x16; front-to-back sort by primitive
+// depth per tile with stable index tiebreak"; readings Q10, Q12, Q13, Q22.
+//
+// Design (B200, no global radix sort): the range table IS the exclusive scan
+// of a per-tile histogram, so the sort is only needed inside each tile:
+//   1. count    : per record, atomic histogram over the tiles of its rectangle
+//   2. scan     : exclusive scan -> ranges [start, end) and scatter cursors
+//   3. scatter  : per record, (depth_bits << 32 | gid, record slot) into its
+//                 tiles' buckets (order inside a bucket is arbitrary)
+//   4. tile sort: one WARP per tile sorts up to 512 pairs in registers
+//                 (bitonic network over shuffles); longer tiles go to a
+//                 persistent CTA pass: shared-memory bitonic up to 8192, then
+//                 merge-path merges in global memory for the rare longer lists
+//                 (coarse pyramid levels).
+// (depth_bits, gid) keys are unique inside a tile, so the result is canonical
+// and bit-identical run to run whatever order the atomics produced.
+#include <algorithm>
+
+#include "gs_common.cuh"
+
+namespace gs {
+namespace {
+
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_PER_THREAD = 4;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_PER_THREAD;
+constexpr int WARP_SORT_MAX = 512;      // 16 keys per lane
+constexpr int SMEM_SORT_MAX = 8192;     // 96 KB of shared memory
+constexpr int BIG_THREADS = 512;
+constexpr uint64_t PAD_KEY = ~0ull;
+
+struct BinWs {
+    uint32_t* counts;
+    uint32_t* cursor;
+    unsigned long long* block_sums;
+    uint32_t* big_count;
+    uint32_t* big_list;
+    uint64_t* keys;
+    uint32_t* vals;
+    uint64_t* keys2;
+    uint32_t* vals2;
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+BinWs carve(void* ws, int64_t cap, int64_t T) {
+    char* p = static_cast<char*>(ws);
+    BinWs w;
+    const int64_t nb = (T + SCAN_TILE - 1) / SCAN_TILE + 1;
+    w.counts = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * T);
+    w.cursor = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * T);
+    w.block_sums = reinterpret_cast<unsigned long long*>(p); p += align256(sizeof(unsigned long long) * nb);
+    w.big_count = reinterpret_cast<uint32_t*>(p); p += 256;
+    w.big_list = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * T);
+    w.keys = reinterpret_cast<uint64_t*>(p); p += align256(sizeof(uint64_t) * cap);
+    w.vals = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * cap);
+    w.keys2 = reinterpret_cast<uint64_t*>(p); p += align256(sizeof(uint64_t) * cap);
+    w.vals2 = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * cap);
+    return w;
+}
+
+size_t ws_bytes(int64_t cap, int64_t T) {
+    const int64_t nb = (T + SCAN_TILE - 1) / SCAN_TILE + 1;
+    return align256(sizeof(uint32_t) * T) * 2 + align256(sizeof(unsigned long long) * nb) + 256 +
+           align256(sizeof(uint32_t) * T) + (align256(sizeof(uint64_t) * cap) + align256(sizeof(uint32_t) * cap)) * 2;
+}
+
+// ---------------------------------------------------------------- 1. count
+__global__ void count_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
+                             const gs_view* __restrict__ views, uint32_t* __restrict__ counts,
+                             const uint32_t* __restrict__ status) {
+    if (*status & GS_STATUS_RECORD_OVERFLOW) return;
+    const int v = blockIdx.y;
+    const uint32_t nv = min((uint64_t)n_rec[v], (uint64_t)cap);
+    const uint32_t toff = views[v].tile_offset;
+    const int TX = view_tiles_x(views[v]);
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nv; k += gridDim.x * blockDim.x) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(rec + (int64_t)v * cap + k) + 3);
+        const uint32_t x0 = q.z & 0xffffu, x1 = q.z >> 16, y0 = q.w & 0xffffu, y1 = q.w >> 16;
+        for (uint32_t ty = y0; ty <= y1; ++ty)
+            for (uint32_t tx = x0; tx <= x1; ++tx) atomicAdd(&counts[toff + ty * TX + tx], 1u);
+    }
+}
+
+// ---------------------------------------------------------------- 2. scan
+__device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long long x,
+                                                                   unsigned long long* total) {
+    __shared__ unsigned long long wsum[SCAN_THREADS / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long s = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0ull;
+        unsigned long long si = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long y = __shfl_up_sync(0xffffffffu, si, o);
+            if (lane >= o) si += y;
+        }
+        if (lane < (int)(blockDim.x >> 5)) wsum[lane] = si - s;
+        if (lane == 31) *total = si;
+    }
+    __syncthreads();
+    const unsigned long long r = wsum[warp] + inc - x;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS)
+scan_reduce_kernel(const uint32_t* __restrict__ counts, int64_t T, unsigned long long* __restrict__ block_sums) {
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_PER_THREAD;
+    unsigned long long s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_PER_THREAD; ++k)
+        if (base + k < T) s += counts[base + k];
+    __shared__ unsigned long long tot;
+    unsigned long long dummy = block_exclusive_scan(s, &tot);
+    (void)dummy;
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
+}
+
+// single CTA: exclusive scan of block sums; writes n_pairs and the overflow bit
+__global__ void __launch_bounds__(SCAN_THREADS)
+scan_blocks_kernel(unsigned long long* __restrict__ block_sums, int64_t nb, uint64_t* __restrict__ n_pairs,
+                   int64_t pair_cap, uint32_t* __restrict__ status) {
+    __shared__ unsigned long long tot;
+    unsigned long long carry = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += SCAN_THREADS) {
+        const int64_t b = b0 + threadIdx.x;
+        const unsigned long long x = b < nb ? block_sums[b] : 0ull;
+        const unsigned long long ex = block_exclusive_scan(x, &tot);
+        if (b < nb) block_sums[b] = carry + ex;
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *n_pairs = carry;
+        if ((int64_t)carry > pair_cap) atomicOr(status, GS_STATUS_PAIR_OVERFLOW);
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS)
+scan_down_kernel(const uint32_t* __restrict__ counts, int64_t T, const unsigned long long* __restrict__ block_sums,
+                 uint32_t* __restrict__ ranges, uint32_t* __restrict__ cursor) {
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_PER_THREAD;
+    uint32_t c[SCAN_PER_THREAD];
+    unsigned long long s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_PER_THREAD; ++k) {
+        c[k] = base + k < T ? counts[base + k] : 0u;
+        s += c[k];
+    }
+    __shared__ unsigned long long tot;
+    unsigned long long run = block_sums[blockIdx.x] + block_exclusive_scan(s, &tot);
+#pragma unroll
+    for (int k = 0; k < SCAN_PER_THREAD; ++k) {
+        if (base + k < T) {
+            const uint32_t st = (uint32_t)run;
+            ranges[2 * (base + k)] = st;
+            ranges[2 * (base + k) + 1] = st + c[k];
+            cursor[base + k] = st;
+        }
+        run += c[k];
+    }
+}
+
+// ---------------------------------------------------------------- 3. scatter
+__global__ void scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
+                               const gs_view* __restrict__ views, uint32_t* __restrict__ cursor,
+                               uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                               const uint32_t* __restrict__ status) {
+    if (*status) return;
+    const int v = blockIdx.y;
+    const uint32_t nv = min((uint64_t)n_rec[v], (uint64_t)cap);
+    const uint32_t toff = views[v].tile_offset;
+    const int TX = view_tiles_x(views[v]);
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nv; k += gridDim.x * blockDim.x) {
+        const uint32_t slot = (uint32_t)((int64_t)v * cap + k);
+        const uint4* q4 = reinterpret_cast<const uint4*>(rec + slot);
+        const uint4 q2 = __ldg(q4 + 2), q3 = __ldg(q4 + 3);
+        const uint64_t key = ((uint64_t)q2.w << 32) | q3.x;   // (bits(z), gid)
+        const uint32_t x0 = q3.z & 0xffffu, x1 = q3.z >> 16, y0 = q3.w & 0xffffu, y1 = q3.w >> 16;
+        for (uint32_t ty = y0; ty <= y1; ++ty)
+            for (uint32_t tx = x0; tx <= x1; ++tx) {
+                const uint32_t pos = atomicAdd(&cursor[toff + ty * TX + tx], 1u);
+                keys[pos] = key;
+                vals[pos] = slot;
+            }
+    }
+}
+
+// ---------------------------------------------------------------- 4. tile sort
+__device__ __forceinline__ void cmp_swap(uint64_t& ka, uint32_t& va, uint64_t& kb, uint32_t& vb, bool up) {
+    if ((ka > kb) == up) {
+        uint64_t tk = ka; ka = kb; kb = tk;
+        uint32_t tv = va; va = vb; vb = tv;
+    }
+}
+
+// Bitonic sort of N = 32*PER keys held as element e = j*32 + lane.
+template <int PER>
+__device__ __forceinline__ void warp_bitonic(uint64_t (&k)[PER], uint32_t (&v)[PER], uint32_t lane) {
+    constexpr int LOGN = 5 + (PER == 1 ? 0 : PER == 2 ? 1 : PER == 4 ? 2 : PER == 8 ? 3 : 4);
+#pragma unroll
+    for (int s = 1; s <= LOGN; ++s) {           // merge blocks of size 2^s
+#pragma unroll
+        for (int d = s - 1; d >= 0; --d) {      // partner distance 2^d
+            if (d >= 5) {
+                const int jd = 1 << (d - 5);
+#pragma unroll
+                for (int j = 0; j < PER; ++j) {
+                    if ((j & jd) == 0) {
+                        const uint32_t e = (uint32_t)j * 32u + lane;
+                        const bool up = ((e >> s) & 1u) == 0u;
+                        cmp_swap(k[j], v[j], k[j + jd], v[j + jd], up);
+                    }
+                }
+            } else {
+                const uint32_t ld = 1u << d;
+#pragma unroll
+                for (int j = 0; j < PER; ++j) {
+                    const uint32_t e = (uint32_t)j * 32u + lane;
+                    const bool up = ((e >> s) & 1u) == 0u;
+                    const bool lower = (lane & ld) == 0u;
+                    const uint64_t ok = __shfl_xor_sync(0xffffffffu, k[j], ld);
+                    const uint32_t ov = __shfl_xor_sync(0xffffffffu, v[j], ld);
+                    // lower element keeps min when ascending, max when descending
+                    const bool take_other = lower ? ((ok < k[j]) == up) : ((ok > k[j]) == up);
+                    if (take_other) { k[j] = ok; v[j] = ov; }
+                }
+            }
+        }
+    }
+}
+
+template <int PER>
+__device__ __forceinline__ void warp_sort_tile(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                               uint32_t s, uint32_t len, uint32_t tile, uint32_t lane,
+                                               uint32_t* __restrict__ out, uint64_t* __restrict__ dbg) {
+    uint64_t k[PER];
+    uint32_t v[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const uint32_t e = (uint32_t)j * 32u + lane;
+        k[j] = e < len ? keys[s + e] : PAD_KEY;
+        v[j] = e < len ? vals[s + e] : 0u;
+    }
+    warp_bitonic<PER>(k, v, lane);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const uint32_t e = (uint32_t)j * 32u + lane;
+        if (e < len) {
+            out[s + e] = v[j];
+            if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | (k[j] >> 32);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256)
+warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint64_t* __restrict__ keys,
+                 const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, uint64_t* __restrict__ dbg,
+                 uint32_t* __restrict__ big_count, uint32_t* __restrict__ big_list,
+                 const uint32_t* __restrict__ status) {
+    if (*status) return;
+    const uint32_t lane = threadIdx.x & 31u;
+    const int64_t tile = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (tile >= T) return;
+    const uint32_t s = ranges[2 * tile], e = ranges[2 * tile + 1], len = e - s;
+    if (len == 0) return;
+    if (len <= 32) warp_sort_tile<1>(keys, vals, s, len, (uint32_t)tile, lane, out, dbg);
+    else if (len <= 64) warp_sort_tile<2>(keys, vals, s, len, (uint32_t)tile, lane, out, dbg);
+    else if (len <= 128) warp_sort_tile<4>(keys, vals, s, len, (uint32_t)tile, lane, out, dbg);
+    else if (len <= 256) warp_sort_tile<8>(keys, vals, s, len, (uint32_t)tile, lane, out, dbg);
+    else if (len <= WARP_SORT_MAX) warp_sort_tile<16>(keys, vals, s, len, (uint32_t)tile, lane, out, dbg);
+    else if (lane == 0) big_list[atomicAdd(big_count, 1u)] = (uint32_t)tile;
+}
+
+// CTA-wide bitonic sort of n (power of two) keys in shared memory
+__device__ void smem_bitonic(uint64_t* sk, uint32_t* sv, uint32_t n) {
+    for (uint32_t size = 2; size <= n; size <<= 1) {
+        for (uint32_t d = size >> 1; d > 0; d >>= 1) {
+            for (uint32_t t = threadIdx.x; t < n / 2; t += blockDim.x) {
+                const uint32_t i = 2 * t - (t & (d - 1));   // lower index of the pair
+                const uint32_t j = i + d;
+                const bool up = (i & size) == 0;
+                uint64_t a = sk[i], b = sk[j];
+                if ((a > b) == up) {
+                    sk[i] = b; sk[j] = a;
+                    uint32_t tv = sv[i]; sv[i] = sv[j]; sv[j] = tv;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// merge sorted runs A = src[a0, a0+na), B = src[a0+na, a0+na+nb) into dst[a0 ...] (keys unique)
+__device__ void cta_merge(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, uint64_t* __restrict__ dk,
+                          uint32_t* __restrict__ dv, uint32_t a0, uint32_t na, uint32_t nb) {
+    const uint32_t total = na + nb;
+    const uint32_t per = (total + blockDim.x - 1) / blockDim.x;
+    const uint32_t lo = min(total, threadIdx.x * per), hi = min(total, lo + per);
+    if (lo >= hi) return;
+    const uint64_t* A = sk + a0;
+    const uint64_t* B = sk + a0 + na;
+    // merge path: find i (from A) with i + j = lo
+    uint32_t ilo = lo > nb ? lo - nb : 0u, ihi = min(lo, na);
+    while (ilo < ihi) {
+        const uint32_t i = (ilo + ihi) >> 1;
+        const uint32_t j = lo - i;
+        if (A[i] < B[j - 1]) ilo = i + 1; else ihi = i;
+    }
+    uint32_t i = ilo, j = lo - ilo;
+    for (uint32_t o = lo; o < hi; ++o) {
+        const bool takeA = j >= nb || (i < na && A[i] < B[j]);
+        if (takeA) { dk[a0 + o] = A[i]; dv[a0 + o] = sv[a0 + i]; ++i; }
+        else { dk[a0 + o] = B[j]; dv[a0 + o] = sv[a0 + na + j]; ++j; }
+    }
+}
+
+__global__ void __launch_bounds__(BIG_THREADS)
+big_sort_kernel(const uint32_t* __restrict__ ranges, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                uint64_t* __restrict__ keys2, uint32_t* __restrict__ vals2, uint32_t* __restrict__ out,
+                uint64_t* __restrict__ dbg, const uint32_t* __restrict__ big_count,
+                const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ status) {
+    if (*status) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
+    uint32_t* sv = reinterpret_cast<uint32_t*>(smem_raw + SMEM_SORT_MAX * sizeof(uint64_t));
+    const uint32_t nbig = *big_count;
+    for (uint32_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+        const uint32_t tile = big_list[bi];
+        const uint32_t s = ranges[2 * tile], len = ranges[2 * tile + 1] - s;
+        // phase 1: sort runs of up to SMEM_SORT_MAX in shared memory
+        for (uint32_t r0 = 0; r0 < len; r0 += SMEM_SORT_MAX) {
+            const uint32_t rl = min((uint32_t)SMEM_SORT_MAX, len - r0);
+            uint32_t n2 = 1;
+            while (n2 < rl) n2 <<= 1;
+            for (uint32_t e = threadIdx.x; e < n2; e += blockDim.x) {
+                sk[e] = e < rl ? keys[s + r0 + e] : PAD_KEY;
+                sv[e] = e < rl ? vals[s + r0 + e] : 0u;
+            }
+            __syncthreads();
+            smem_bitonic(sk, sv, n2);
+            for (uint32_t e = threadIdx.x; e < rl; e += blockDim.x) {
+                keys[s + r0 + e] = sk[e];
+                vals[s + r0 + e] = sv[e];
+            }
+            __syncthreads();
+        }
+        // phase 2: merge passes (ping-pong keys <-> keys2)
+        uint64_t* ck = keys + s; uint32_t* cv = vals + s;
+        uint64_t* nk = keys2 + s; uint32_t* nv = vals2 + s;
+        for (uint32_t width = SMEM_SORT_MAX; width < len; width <<= 1) {
+            for (uint32_t a0 = 0; a0 < len; a0 += 2 * width) {
+                const uint32_t na = min(width, len - a0);
+                const uint32_t nb = a0 + na < len ? min(width, len - a0 - na) : 0u;
+                cta_merge(ck, cv, nk, nv, a0, na, nb);
+            }
+            __syncthreads();
+            uint64_t* tk = ck; ck = nk; nk = tk;
+            uint32_t* tv = cv; cv = nv; nv = tv;
+        }
+        for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) {
+            out[s + e] = cv[e];
+            if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | (ck[e] >> 32);
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+}  // namespace gs
+
+using namespace gs;
+
+extern "C" {
+
+size_t gs_bin_sort_workspace_bytes(int64_t pair_capacity, int64_t total_tiles) {
+    if (pair_capacity < 1) pair_capacity = 1;
+    if (total_tiles < 1) total_tiles = 1;
+    return ws_bytes(pair_capacity, total_tiles);
+}
+
+gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const gs_view* views_dev,
+                      int32_t n_views, gs_bins* out, void* ws, size_t ws_size, void* stream) {
+    int64_t total_pixels = 0, T = 0;
+    gs_status st = validate_views(views_host, views_dev, n_views, &total_pixels, &T);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(proj && proj->rec && proj->n_rec && proj->status, GS_INVALID_ARG, "proj has a NULL pointer");
+    GS_REQUIRE(out && out->ranges && out->sorted_rec && out->n_pairs, GS_INVALID_ARG, "bins has a NULL pointer");
+    GS_REQUIRE(out->pair_capacity >= 1 && out->pair_capacity < (int64_t(1) << 32), GS_INVALID_ARG,
+               "pair_capacity = %lld not in [1, 2^32)", (long long)out->pair_capacity);
+    const size_t need = ws_bytes(out->pair_capacity, T);
+    GS_REQUIRE(ws != nullptr && ws_size >= need, GS_WORKSPACE_TOO_SMALL, "gs_bin_sort workspace %zu < %zu", ws_size,
+               need);
+    cudaStream_t s = (cudaStream_t)stream;
+    BinWs w = carve(ws, out->pair_capacity, T);
+    const int64_t cap = proj->rec_capacity;
+    cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * T, s);
+    cudaMemsetAsync(w.big_count, 0, sizeof(uint32_t), s);
+
+    const int64_t blocks_per_view = std::min<int64_t>((cap + 255) / 256, std::max(1, 4 * num_sms() / n_views + 1));
+    dim3 rgrid((unsigned)std::max<int64_t>(1, blocks_per_view), (unsigned)n_views);
+    count_kernel<<<rgrid, 256, 0, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.counts, proj->status);
+    if ((st = check_launch("count_kernel")) != GS_OK) return st;
+    const int64_t nb = (T + SCAN_TILE - 1) / SCAN_TILE;
+    scan_reduce_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(w.counts, T, w.block_sums);
+    scan_blocks_kernel<<<1, SCAN_THREADS, 0, s>>>(w.block_sums, nb, out->n_pairs, out->pair_capacity, proj->status);
+    scan_down_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(w.counts, T, w.block_sums, out->ranges, w.cursor);
+    if ((st = check_launch("scan kernels")) != GS_OK) return st;
+    scatter_kernel<<<rgrid, 256, 0, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.cursor, w.keys, w.vals,
+                                         proj->status);
+    if ((st = check_launch("scatter_kernel")) != GS_OK) return st;
+    warp_sort_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(out->ranges, T, w.keys, w.vals, out->sorted_rec,
+                                                             out->sorted_key, w.big_count, w.big_list, proj->status);
+    if ((st = check_launch("warp_sort_kernel")) != GS_OK) return st;
+    static bool attr_set = false;
+    const int smem = SMEM_SORT_MAX * (sizeof(uint64_t) + sizeof(uint32_t));
+    if (!attr_set) {
+        cudaFuncSetAttribute(big_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr_set = true;
+    }
+    big_sort_kernel<<<num_sms(), BIG_THREADS, smem, s>>>(out->ranges, w.keys, w.vals, w.keys2, w.vals2,
+                                                         out->sorted_rec, out->sorted_key, w.big_count, w.big_list,
+                                                         proj->status);
+    return check_launch("big_sort_kernel");
+}
+
+}  // extern "C"

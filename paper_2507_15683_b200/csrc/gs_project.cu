@@ -1,0 +1,451 @@
+// gs_project.cu -- O1-O10: per (view, Gaussian) camera
+// transform, cull, EWA 2D covariance, conic, radius, tile rectangle, depth
+// key and SH colour.  PAPER.md Alg. 1 l.9-12.
+//
+// THIS TRANSLATION UNIT IS COMPILED WITH -fmad=false (no FMA contraction),
+// IEEE division and square root, no flush-to-zero: every fp32 expression in
+// the "pinned" sections below is evaluated exactly in the written order, so
+// u, v, z, conic, radius and the tile rectangle are bit-identical to the
+// oracle's (and hence so are the duplicated keys).
+//
+// Design (B200): one thread per Gaussian reads its 44 B of geometry ONCE per
+// batch (coalesced SoA loads), builds the view-independent 3D covariance once,
+// then loops over the views of the batch that can see its block (a
+// conservative per-(view, block) frustum test fills a bitmask first).  The
+// view loop is warp-uniform, so record slots are reserved with one atomic per
+// warp per view.  SH coefficients are read only for visible records.
+#include "gs_common.cuh"
+
+namespace gs {
+namespace {
+
+struct ViewConst {        // per-view constants (pinned fp32, computed once per batch)
+    float lox, hix, loy, hiy;   // Jacobian clamp bounds on x/z, y/z (Q6)
+    float ccx, ccy, ccz;        // camera centre in world, -R^T t (SH direction)
+    float kbound;               // fx^2 (1 + tx^2) + fy^2 (1 + ty^2): ||J||_F^2 z^2 bound
+    float wpix, hpix;           // 16*TX, 16*TY (grid extent in pixels)
+    float txf, tyf;             // TX, TY as float
+    int32_t tx, ty;
+    int32_t pad0, pad1;
+};
+
+__global__ void view_const_kernel(const gs_view* __restrict__ views, int n_views, gs_params P,
+                                  ViewConst* __restrict__ vc) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_views) return;
+    const gs_view V = views[i];
+    ViewConst c;
+    const float W = (float)V.width, H = (float)V.height;
+    const float m = P.clamp_margin;
+    // pinned (same expressions as the oracle)
+    c.lox = (-(m * W) - V.cx) / V.fx;
+    c.hix = ((1.0f + m) * W - V.cx) / V.fx;
+    c.loy = (-(m * H) - V.cy) / V.fy;
+    c.hiy = ((1.0f + m) * H - V.cy) / V.fy;
+    // not pinned (tolerance / conservative bound only)
+    c.ccx = -(V.R[0] * V.t[0] + V.R[3] * V.t[1] + V.R[6] * V.t[2]);
+    c.ccy = -(V.R[1] * V.t[0] + V.R[4] * V.t[1] + V.R[7] * V.t[2]);
+    c.ccz = -(V.R[2] * V.t[0] + V.R[5] * V.t[1] + V.R[8] * V.t[2]);
+    const float txm = fmaxf(fabsf(c.lox), fabsf(c.hix)), tym = fmaxf(fabsf(c.loy), fabsf(c.hiy));
+    c.kbound = V.fx * V.fx * (1.0f + txm * txm) + V.fy * V.fy * (1.0f + tym * tym);
+    c.tx = (V.width + GS_TILE - 1) / GS_TILE;
+    c.ty = (V.height + GS_TILE - 1) / GS_TILE;
+    c.txf = (float)c.tx;
+    c.tyf = (float)c.ty;
+    c.wpix = 16.0f * c.txf;
+    c.hpix = 16.0f * c.tyf;
+    c.pad0 = c.pad1 = 0;
+    vc[i] = c;
+}
+
+// Conservative radius bound (px) for a Gaussian with max scale smax at depth z:
+// lambda_max(Sigma') <= smax^2 ||J||_F^2 + dilation, ||J||_F^2 <= kbound / z^2
+// (DESIGN.md §4.1).  Inflated to absorb fp32 rounding.
+__device__ __forceinline__ float radius_bound(float smax, float kbound, float z, float dil) {
+    const float lam = smax * smax * kbound / (z * z) + dil;
+    return 3.0f * sqrtf(lam) * 1.01f + 2.0f;
+}
+
+// One thread per (block, 32-view word): bit set unless the whole block is
+// provably culled (all centres behind z_near, or every Gaussian's rectangle
+// provably off the tile grid).  Conservative: never clears a needed bit.
+__global__ void block_cull_kernel(const gs_view* __restrict__ views, const ViewConst* __restrict__ vcs,
+                                  int n_views, int n_blocks, const float* __restrict__ bounds, gs_params P,
+                                  uint32_t* __restrict__ mask) {
+    const int nw = (n_views + 31) >> 5;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)n_blocks * nw) return;
+    const int b = (int)(idx / nw), w = (int)(idx % nw);
+    const float* bb = bounds + (int64_t)b * 8;
+    const float lo[3] = {bb[0], bb[1], bb[2]}, hi[3] = {bb[3], bb[4], bb[5]};
+    const float smax = bb[6];
+    uint32_t word = 0;
+    const bool empty = !(lo[0] <= hi[0]);   // empty block: bounds are +inf/-inf
+    for (int j = 0; j < 32; ++j) {
+        const int v = w * 32 + j;
+        if (v >= n_views || empty) break;
+        const gs_view& V = views[v];
+        const ViewConst& c = vcs[v];
+        float zmin = 3.4e38f, zmax = -3.4e38f, umin = 3.4e38f, umax = -3.4e38f, vmin = 3.4e38f, vmax = -3.4e38f;
+        float slack = 0.f;
+        bool all_front = true;
+        for (int k = 0; k < 8; ++k) {
+            const float x = (k & 1) ? hi[0] : lo[0], y = (k & 2) ? hi[1] : lo[1], z = (k & 4) ? hi[2] : lo[2];
+            const float pz = V.R[6] * x + V.R[7] * y + V.R[8] * z + V.t[2];
+            const float mag = fabsf(V.R[6] * x) + fabsf(V.R[7] * y) + fabsf(V.R[8] * z) + fabsf(V.t[2]);
+            slack = fmaxf(slack, 1e-5f * mag + 1e-6f);
+            zmin = fminf(zmin, pz);
+            zmax = fmaxf(zmax, pz);
+            if (!(pz > P.z_near + 2.0f * slack)) { all_front = false; continue; }
+            const float px = V.R[0] * x + V.R[1] * y + V.R[2] * z + V.t[0];
+            const float py = V.R[3] * x + V.R[4] * y + V.R[5] * z + V.t[1];
+            const float u = V.fx * (px / pz) + V.cx, vv = V.fy * (py / pz) + V.cy;
+            umin = fminf(umin, u); umax = fmaxf(umax, u);
+            vmin = fminf(vmin, vv); vmax = fmaxf(vmax, vv);
+        }
+        bool visible = true;
+        if (zmax < P.z_near - 2.0f * slack) {
+            visible = false;                                   // every centre is near-culled
+        } else if (all_front) {
+            // projection of the box = hull of corner projections (z > 0 everywhere)
+            const float rb = radius_bound(smax, c.kbound, zmin, P.dilation);
+            const float mu = 1e-4f * (fabsf(umin) + fabsf(umax) + fabsf(vmin) + fabsf(vmax)) + 1.0f;
+            if (umax + rb < -mu || umin - rb >= c.wpix + mu || vmax + rb < -mu || vmin - rb >= c.hpix + mu)
+                visible = false;
+        }
+        if (visible) word |= 1u << j;
+    }
+    mask[idx] = word;
+}
+
+__global__ void block_bounds_kernel(const float* __restrict__ pos, const float* __restrict__ scale, int64_t n,
+                                    const int64_t* __restrict__ offs, int n_blocks, float* __restrict__ out) {
+    const int b = blockIdx.x;
+    if (b >= n_blocks) return;
+    const int64_t s = offs[b], e = offs[b + 1];
+    float lo[3] = {3.4e38f, 3.4e38f, 3.4e38f}, hi[3] = {-3.4e38f, -3.4e38f, -3.4e38f}, sm = 0.f;
+    for (int64_t i = s + threadIdx.x; i < e; i += blockDim.x) {
+        for (int k = 0; k < 3; ++k) {
+            const float p = pos[k * n + i];
+            lo[k] = fminf(lo[k], p);
+            hi[k] = fmaxf(hi[k], p);
+            sm = fmaxf(sm, scale[k * n + i]);
+        }
+    }
+    __shared__ float red[7][32];
+    float vals[7] = {lo[0], lo[1], lo[2], -hi[0], -hi[1], -hi[2], -sm};
+    for (int k = 0; k < 7; ++k) {
+        float x = vals[k];
+        for (int o = 16; o; o >>= 1) x = fminf(x, __shfl_xor_sync(0xffffffffu, x, o));
+        if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < 7) {
+        float x = 3.4e38f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) x = fminf(x, red[threadIdx.x][w]);
+        out[(int64_t)b * 8 + threadIdx.x] = threadIdx.x < 3 ? x : -x;
+    }
+    if (threadIdx.x == 7) out[(int64_t)b * 8 + 7] = 0.f;
+}
+
+__device__ __forceinline__ bool finite3(float a, float b, float c) {
+    return isfinite(a) && isfinite(b) && isfinite(c);
+}
+
+// SH colour (O10, fp32, tolerance-checked): [3DGS] real SH basis up to degree 3
+__device__ __forceinline__ void sh_color(int deg, const float* __restrict__ sh, int64_t n, int64_t i, float dx,
+                                         float dy, float dz, float* rgb) {
+    const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+    float b[16];
+    b[0] = C0;
+    int nk = 1;
+    if (deg >= 1) {
+        b[1] = -C1 * dy; b[2] = C1 * dz; b[3] = -C1 * dx;
+        nk = 4;
+    }
+    if (deg >= 2) {
+        const float xx = dx * dx, yy = dy * dy, zz = dz * dz, xy = dx * dy, yz = dy * dz, xz = dx * dz;
+        b[4] = 1.0925484305920792f * xy;
+        b[5] = -1.0925484305920792f * yz;
+        b[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+        b[7] = -1.0925484305920792f * xz;
+        b[8] = 0.5462742152960396f * (xx - yy);
+        nk = 9;
+        if (deg >= 3) {
+            b[9] = -0.5900435899266435f * dy * (3.0f * xx - yy);
+            b[10] = 2.890611442640554f * xy * dz;
+            b[11] = -0.4570457994644658f * dy * (4.0f * zz - xx - yy);
+            b[12] = 0.3731763325901154f * dz * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+            b[13] = -0.4570457994644658f * dx * (4.0f * zz - xx - yy);
+            b[14] = 1.445305721320277f * dz * (xx - yy);
+            b[15] = -0.5900435899266435f * dx * (xx - 3.0f * yy);
+            nk = 16;
+        }
+    }
+    float r = 0.5f, g = 0.5f, bl = 0.5f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        if (k < nk) {
+            r += b[k] * __ldg(&sh[(int64_t)(k * 3 + 0) * n + i]);
+            g += b[k] * __ldg(&sh[(int64_t)(k * 3 + 1) * n + i]);
+            bl += b[k] * __ldg(&sh[(int64_t)(k * 3 + 2) * n + i]);
+        }
+    }
+    rgb[0] = fmaxf(r, 0.f);
+    rgb[1] = fmaxf(g, 0.f);
+    rgb[2] = fmaxf(bl, 0.f);
+}
+
+constexpr int PROJ_THREADS = 256;
+
+__global__ void __launch_bounds__(PROJ_THREADS)
+project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* __restrict__ vcs, int n_views,
+               gs_params P, const uint32_t* __restrict__ mask, gs_record* __restrict__ rec, int64_t cap,
+               uint32_t* __restrict__ n_rec, uint64_t* __restrict__ diag, uint32_t* __restrict__ status) {
+    const int64_t n = S.n;
+    const int64_t i = (int64_t)blockIdx.x * PROJ_THREADS + threadIdx.x;
+    const bool in = i < n;
+    const uint32_t lane = threadIdx.x & 31u;
+    const int nw = (n_views + 31) >> 5;
+
+    // ---- view-independent part (once per Gaussian per batch) ----
+    float mx = 0.f, my = 0.f, mz = 0.f, op = 0.f, s0 = 1.f, s1 = 1.f, s2 = 1.f;
+    float qw = 1.f, qx = 0.f, qy = 0.f, qz = 0.f;
+    if (in) {
+        mx = __ldg(&S.pos[i]); my = __ldg(&S.pos[n + i]); mz = __ldg(&S.pos[2 * n + i]);
+        op = __ldg(&S.opacity[i]);
+        s0 = __ldg(&S.scale[i]); s1 = __ldg(&S.scale[n + i]); s2 = __ldg(&S.scale[2 * n + i]);
+        qw = __ldg(&S.quat[i]); qx = __ldg(&S.quat[n + i]); qy = __ldg(&S.quat[2 * n + i]);
+        qz = __ldg(&S.quat[3 * n + i]);
+    }
+    const bool transparent = !(op >= P.alpha_min);
+    bool degenerate = !(s0 > 0.0f) || !(s1 > 0.0f) || !(s2 > 0.0f) || !finite3(s0, s1, s2) ||
+                      !finite3(qw, qx, qy) || !isfinite(qz);
+    // O4 (pinned): Sigma = M M^T, M = R(q) diag(s), q normalised
+    float Sg[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // S00 S01 S02 S11 S12 S22
+    {
+        const float qn2 = ((qw * qw + qx * qx) + qy * qy) + qz * qz;
+        bool qbad = !(qn2 > 0.0f);
+        if (!degenerate && !qbad) {
+            const float qn = sqrtf(qn2);
+            const float w = qw / qn, x = qx / qn, y = qy / qn, z = qz / qn;
+            const float xx = x * x, yy = y * y, zz = z * z;
+            const float xy = x * y, xz = x * z, yz = y * z;
+            const float wx = w * x, wy = w * y, wz = w * z;
+            const float M0 = (1.0f - 2.0f * (yy + zz)) * s0, M1 = (2.0f * (xy - wz)) * s1, M2 = (2.0f * (xz + wy)) * s2;
+            const float M3 = (2.0f * (xy + wz)) * s0, M4 = (1.0f - 2.0f * (xx + zz)) * s1, M5 = (2.0f * (yz - wx)) * s2;
+            const float M6 = (2.0f * (xz - wy)) * s0, M7 = (2.0f * (yz + wx)) * s1, M8 = (1.0f - 2.0f * (xx + yy)) * s2;
+            Sg[0] = (M0 * M0 + M1 * M1) + M2 * M2;
+            Sg[1] = (M0 * M3 + M1 * M4) + M2 * M5;
+            Sg[2] = (M0 * M6 + M1 * M7) + M2 * M8;
+            Sg[3] = (M3 * M3 + M4 * M4) + M5 * M5;
+            Sg[4] = (M3 * M6 + M4 * M7) + M5 * M8;
+            Sg[5] = (M6 * M6 + M7 * M7) + M8 * M8;
+        }
+        // a zero/non-finite quaternion is degenerate, but only after the near /
+        // transparent tests (oracle order)
+        if (qbad) degenerate = true;
+    }
+    const float smax = fmaxf(fmaxf(s0, s1), s2);
+    // block of this Gaussian
+    int blk = -1;
+    if (S.n_blocks > 0 && in) {
+        int lo = 0, hi = S.n_blocks - 1;
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (__ldg(&S.block_offsets[mid]) <= i) lo = mid; else hi = mid - 1;
+        }
+        blk = lo;
+    }
+    uint32_t c_near = 0, c_transp = 0, c_degen = 0, c_off = 0;
+    const float thr = in && !transparent ? 2.0f * logf(op / P.alpha_min) : 0.f;
+
+    for (int w = 0; w < nw; ++w) {
+        uint32_t my_mask = 0;
+        if (in) {
+            if (S.n_blocks > 0) my_mask = __ldg(&mask[(int64_t)blk * nw + w]);
+            else my_mask = (w == nw - 1 && (n_views & 31)) ? ((1u << (n_views & 31)) - 1u) : 0xffffffffu;
+        }
+        uint32_t any = __reduce_or_sync(0xffffffffu, my_mask);
+        while (any) {
+            const int j = __ffs(any) - 1;
+            any &= any - 1u;
+            const int vi = w * 32 + j;
+            bool visible = false;
+            gs_record r;
+            if ((my_mask >> j) & 1u) {
+                const gs_view& V = views[vi];
+                const ViewConst& c = vcs[vi];
+                // O1 (pinned)
+                const float px = ((V.R[0] * mx + V.R[1] * my) + V.R[2] * mz) + V.t[0];
+                const float py = ((V.R[3] * mx + V.R[4] * my) + V.R[5] * mz) + V.t[1];
+                const float pz = ((V.R[6] * mx + V.R[7] * my) + V.R[8] * mz) + V.t[2];
+                if (!(pz > P.z_near)) { ++c_near; goto done; }
+                if (transparent) { ++c_transp; goto done; }
+                if (degenerate || !finite3(px, py, pz)) { ++c_degen; goto done; }
+                {
+                    // O3 (pinned): divide by depth first, then apply K (Alg. 1 l.12-14)
+                    const float xn = px / pz, yn = py / pz;
+                    const float u = V.fx * xn + V.cx;
+                    const float v = V.fy * yn + V.cy;
+                    // conservative early off-screen test (never culls a Gaussian the exact test keeps)
+                    if (isfinite(u) && isfinite(v) && P.dilation > 0.f) {
+                        const float rb = radius_bound(smax, c.kbound, pz, P.dilation);
+                        const float mu = 1e-5f * (fabsf(u) + fabsf(v)) + 1.0f;
+                        if (u + rb < -mu || u - rb >= c.wpix + mu || v + rb < -mu || v - rb >= c.hpix + mu) {
+                            ++c_off;
+                            goto done;
+                        }
+                    }
+                    // O5 (pinned): EWA with the clamped Jacobian
+                    const float xc = fminf(fmaxf(xn, c.lox), c.hix) * pz;
+                    const float yc = fminf(fmaxf(yn, c.loy), c.hiy) * pz;
+                    const float z2 = pz * pz;
+                    const float j00 = V.fx / pz, j02 = -((V.fx * xc) / z2);
+                    const float j11 = V.fy / pz, j12 = -((V.fy * yc) / z2);
+                    float T0[3], T1[3];
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        T0[k] = j00 * V.R[0 * 3 + k] + j02 * V.R[2 * 3 + k];
+                        T1[k] = j11 * V.R[1 * 3 + k] + j12 * V.R[2 * 3 + k];
+                    }
+                    // Vt = T Sigma (Sigma symmetric: S(r,c) with S01=S10 ...)
+                    const float S00 = Sg[0], S01 = Sg[1], S02 = Sg[2], S11 = Sg[3], S12 = Sg[4], S22 = Sg[5];
+                    const float V00 = (T0[0] * S00 + T0[1] * S01) + T0[2] * S02;
+                    const float V01 = (T0[0] * S01 + T0[1] * S11) + T0[2] * S12;
+                    const float V02 = (T0[0] * S02 + T0[1] * S12) + T0[2] * S22;
+                    const float V10 = (T1[0] * S00 + T1[1] * S01) + T1[2] * S02;
+                    const float V11 = (T1[0] * S01 + T1[1] * S11) + T1[2] * S12;
+                    const float V12 = (T1[0] * S02 + T1[1] * S12) + T1[2] * S22;
+                    const float s00 = (V00 * T0[0] + V01 * T0[1]) + V02 * T0[2];
+                    const float s01 = (V00 * T1[0] + V01 * T1[1]) + V02 * T1[2];
+                    const float s11 = (V10 * T1[0] + V11 * T1[1]) + V12 * T1[2];
+                    const float a = s00 + P.dilation, b = s01, cc = s11 + P.dilation;
+                    // O6 (pinned)
+                    const float det = a * cc - b * b;
+                    if (!(det > 0.0f)) { ++c_degen; goto done; }
+                    const float ca = cc / det, cb = -(b / det), ccn = a / det;
+                    // O7 (pinned)
+                    const float mid = 0.5f * (a + cc);
+                    const float lam = mid + sqrtf(fmaxf(mid * mid - det, 0.0f));
+                    const float rad = ceilf(3.0f * sqrtf(lam));
+                    // O8 (pinned)
+                    if (!isfinite(u) || !isfinite(v) || !isfinite(rad)) { ++c_degen; goto done; }
+                    const float fx0 = floorf((u - rad) * 0.0625f), fx1 = floorf((u + rad) * 0.0625f);
+                    const float fy0 = floorf((v - rad) * 0.0625f), fy1 = floorf((v + rad) * 0.0625f);
+                    if (fx1 < 0.0f || fx0 >= c.txf || fy1 < 0.0f || fy0 >= c.tyf) { ++c_off; goto done; }
+                    r.x0 = (uint16_t)fmaxf(fx0, 0.0f);
+                    r.x1 = (uint16_t)fminf(fx1, c.txf - 1.0f);
+                    r.y0 = (uint16_t)fmaxf(fy0, 0.0f);
+                    r.y1 = (uint16_t)fminf(fy1, c.tyf - 1.0f);
+                    r.u = u; r.v = v; r.z = pz;
+                    r.conic_a = ca; r.conic_b = cb; r.conic_c = ccn;
+                    r.opacity = op;
+                    // alpha >= alpha_min ellipse q <= thr: bbox half extents sqrt(thr a), sqrt(thr c),
+                    // inflated 2% (+0.05 px) so fp32 evaluation noise can never reach outside
+                    r.ext_x = sqrtf(thr * a) * 1.02f + 0.05f;
+                    r.ext_y = sqrtf(thr * cc) * 1.02f + 0.05f;
+                    r.gid = (uint32_t)i;
+                    r.view_radius = (uint32_t)vi | ((uint32_t)fminf(rad, 65535.0f) << 16);
+                    // O10: SH colour at d = (mu - c_cam)/|mu - c_cam|
+                    const float dx = mx - c.ccx, dy = my - c.ccy, dz = mz - c.ccz;
+                    const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
+                    sh_color(S.sh_degree, S.sh, n, i, dx * inv, dy * inv, dz * inv, r.rgb);
+                    visible = true;
+                }
+            done:;
+            }
+            // warp-aggregated slot reservation for view vi
+            const uint32_t vm = __ballot_sync(0xffffffffu, visible);
+            if (vm) {
+                uint32_t base = 0;
+                const uint32_t leader = __ffs(vm) - 1;
+                if (lane == leader) base = atomicAdd(&n_rec[vi], (uint32_t)__popc(vm));
+                base = __shfl_sync(0xffffffffu, base, leader);
+                if (visible) {
+                    const uint32_t slot = base + __popc(vm & ((1u << lane) - 1u));
+                    if ((int64_t)slot < cap) {
+                        float4* dst = reinterpret_cast<float4*>(rec + (int64_t)vi * cap + slot);
+                        const float4* src = reinterpret_cast<const float4*>(&r);
+                        dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2]; dst[3] = src[3];
+                    } else {
+                        atomicOr(status, GS_STATUS_RECORD_OVERFLOW);
+                    }
+                }
+            }
+        }
+    }
+    // diagnostics: warp-reduce then one atomic per counter per warp
+    uint32_t cnt[4] = {c_near, c_transp, c_degen, c_off};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t s = __reduce_add_sync(0xffffffffu, cnt[k]);
+        if (lane == 0 && s) atomicAdd((unsigned long long*)&diag[k], (unsigned long long)s);
+    }
+}
+
+}  // namespace
+}  // namespace gs
+
+using namespace gs;
+
+extern "C" {
+
+size_t gs_project_workspace_bytes(int32_t n_blocks, int32_t n_views) {
+    if (n_views < 1) n_views = 1;
+    const size_t nw = ((size_t)n_views + 31) / 32;
+    size_t bytes = (size_t)n_views * sizeof(ViewConst);
+    bytes = (bytes + 255) & ~size_t(255);
+    bytes += (size_t)(n_blocks > 0 ? n_blocks : 0) * nw * sizeof(uint32_t);
+    return (bytes + 255) & ~size_t(255);
+}
+
+gs_status gs_scene_block_bounds(const gs_scene* scene, float* block_bounds_out, void* stream) {
+    gs_status st = validate_scene(scene, false);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(scene->n_blocks > 0, GS_INVALID_ARG, "scene has no blocks");
+    GS_REQUIRE(scene->block_offsets && scene->pos && scene->scale && block_bounds_out, GS_INVALID_ARG,
+               "NULL pointer");
+    block_bounds_kernel<<<scene->n_blocks, 256, 0, (cudaStream_t)stream>>>(
+        scene->pos, scene->scale, scene->n, scene->block_offsets, scene->n_blocks, block_bounds_out);
+    return check_launch("block_bounds_kernel");
+}
+
+gs_status gs_project(const gs_scene* scene, const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
+                     const gs_params* params, gs_projected* out, void* ws, size_t ws_bytes, void* stream) {
+    gs_status st = validate_scene(scene, true);
+    if (st != GS_OK) return st;
+    st = validate_views(views_host, views_dev, n_views, nullptr, nullptr);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(params != nullptr, GS_INVALID_ARG, "params is NULL");
+    GS_REQUIRE(out && out->rec && out->n_rec && out->diag && out->status, GS_INVALID_ARG,
+               "out (gs_projected) has a NULL pointer");
+    GS_REQUIRE(out->rec_capacity >= 1 && out->rec_capacity * (int64_t)n_views < (int64_t(1) << 32),
+               GS_INVALID_ARG, "rec_capacity = %lld invalid (n_views * cap must be < 2^32)",
+               (long long)out->rec_capacity);
+    const size_t need = gs_project_workspace_bytes(scene->n_blocks, n_views);
+    GS_REQUIRE(ws != nullptr && ws_bytes >= need, GS_WORKSPACE_TOO_SMALL, "gs_project workspace %zu < %zu",
+               ws_bytes, need);
+    cudaStream_t s = (cudaStream_t)stream;
+    ViewConst* vc = reinterpret_cast<ViewConst*>(ws);
+    size_t off = ((size_t)n_views * sizeof(ViewConst) + 255) & ~size_t(255);
+    uint32_t* mask = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + off);
+
+    cudaMemsetAsync(out->n_rec, 0, sizeof(uint32_t) * n_views, s);
+    cudaMemsetAsync(out->diag, 0, sizeof(uint64_t) * 4, s);
+    view_const_kernel<<<(n_views + 127) / 128, 128, 0, s>>>(views_dev, n_views, *params, vc);
+    if ((st = check_launch("view_const_kernel")) != GS_OK) return st;
+    if (scene->n == 0) return GS_OK;
+    if (scene->n_blocks > 0) {
+        const int64_t work = (int64_t)scene->n_blocks * ((n_views + 31) / 32);
+        block_cull_kernel<<<(unsigned)((work + 127) / 128), 128, 0, s>>>(views_dev, vc, n_views, scene->n_blocks,
+                                                                        scene->block_bounds, *params, mask);
+        if ((st = check_launch("block_cull_kernel")) != GS_OK) return st;
+    }
+    const unsigned grid = (unsigned)((scene->n + PROJ_THREADS - 1) / PROJ_THREADS);
+    project_kernel<<<grid, PROJ_THREADS, 0, s>>>(*scene, views_dev, vc, n_views, *params, mask, out->rec,
+                                                 out->rec_capacity, out->n_rec, out->diag, out->status);
+    return check_launch("project_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,293 @@
+"""Thin Python binding of libgs.so (include/gs.h) -- argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of ``csrc/``; this module
+only turns torch tensors (device memory owned by PyTorch) into the plain
+pointers and structs of the C ABI and raises on a non-OK status.  There is no
+CPU fallback: importing it without the built library raises.
+
+The four calls keep the C names: ``gs_project``, ``gs_bin_sort``,
+``gs_rasterize``, ``gs_backproject``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libgs.so")
+
+GS_OK, GS_INVALID_ARG, GS_UNSUPPORTED, GS_WORKSPACE_TOO_SMALL, GS_CUDA_ERROR = range(5)
+GS_STATUS_RECORD_OVERFLOW = 0x1
+GS_STATUS_PAIR_OVERFLOW = 0x2
+RECORD_BYTES = 64
+
+
+class GSError(RuntimeError):
+    pass
+
+
+# ------------------------------------------------------------------ structs
+class gs_view(ctypes.Structure):
+    _fields_ = [("R", ctypes.c_float * 9), ("t", ctypes.c_float * 3), ("fx", ctypes.c_float),
+                ("fy", ctypes.c_float), ("cx", ctypes.c_float), ("cy", ctypes.c_float),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32), ("pix_offset", ctypes.c_int64),
+                ("tile_offset", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+class gs_scene(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("sh_degree", ctypes.c_int32), ("feat_dim", ctypes.c_int32),
+                ("pos", ctypes.c_void_p), ("quat", ctypes.c_void_p), ("scale", ctypes.c_void_p),
+                ("opacity", ctypes.c_void_p), ("sh", ctypes.c_void_p), ("feat", ctypes.c_void_p),
+                ("n_blocks", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("block_offsets", ctypes.c_void_p), ("block_bounds", ctypes.c_void_p)]
+
+
+class gs_params(ctypes.Structure):
+    _fields_ = [("z_near", ctypes.c_float), ("dilation", ctypes.c_float), ("clamp_margin", ctypes.c_float),
+                ("alpha_min", ctypes.c_float), ("alpha_max", ctypes.c_float), ("t_min", ctypes.c_float)]
+
+
+class gs_projected(ctypes.Structure):
+    _fields_ = [("rec", ctypes.c_void_p), ("rec_capacity", ctypes.c_int64), ("n_rec", ctypes.c_void_p),
+                ("diag", ctypes.c_void_p), ("status", ctypes.c_void_p)]
+
+
+class gs_bins(ctypes.Structure):
+    _fields_ = [("ranges", ctypes.c_void_p), ("sorted_rec", ctypes.c_void_p), ("pair_capacity", ctypes.c_int64),
+                ("n_pairs", ctypes.c_void_p), ("sorted_key", ctypes.c_void_p)]
+
+
+class gs_images(ctypes.Structure):
+    _fields_ = [("rgb", ctypes.c_void_p), ("depth", ctypes.c_void_p), ("alpha", ctypes.c_void_p),
+                ("feat", ctypes.c_void_p)]
+
+
+EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_layout", "gs_scene_block_bounds",
+           "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
+           "gs_rasterize", "gs_backproject"]
+
+_lib = None
+
+
+def lib():
+    """Load libgs.so (fails loudly when missing -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise GSError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        L.gs_abi_version.restype = ctypes.c_int32
+        L.gs_last_error.restype = ctypes.c_char_p
+        L.gs_default_params.restype = gs_params
+        L.gs_project_workspace_bytes.restype = ctypes.c_size_t
+        L.gs_project_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32]
+        L.gs_bin_sort_workspace_bytes.restype = ctypes.c_size_t
+        L.gs_bin_sort_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]
+        for f in ("gs_views_layout", "gs_scene_block_bounds", "gs_project", "gs_bin_sort", "gs_rasterize",
+                  "gs_backproject"):
+            getattr(L, f).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st: int, what: str):
+    if st != GS_OK:
+        raise GSError(f"{what} failed with status {st}: {lib().gs_last_error().decode()}")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    assert t.is_cuda and t.is_contiguous(), "expected a contiguous CUDA tensor"
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def default_params() -> gs_params:
+    return lib().gs_default_params()
+
+
+# ------------------------------------------------------------------ device containers
+class DeviceScene:
+    """Scene planes resident in HBM (SoA float32, block-major when partitioned)."""
+
+    def __init__(self, scene, device="cuda", compute_block_bounds: bool = True):
+        dev = torch.device(device)
+        t = lambda a, dt=torch.float32: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)
+        self.n = scene.n
+        self.sh_degree = scene.sh_degree
+        self.feat_dim = scene.feat_dim
+        self.pos, self.quat, self.scale = t(scene.pos), t(scene.quat), t(scene.scale)
+        self.opacity, self.sh = t(scene.opacity), t(scene.sh)
+        self.feat = t(scene.feat) if scene.feat is not None else None
+        self.block_offsets = None
+        self.block_bounds = None
+        if scene.block_offsets is not None and len(scene.block_offsets) > 1:
+            self.block_offsets = t(scene.block_offsets, torch.int64)
+            self.block_bounds = torch.zeros((len(scene.block_offsets) - 1, 8), device=dev)
+        self.struct = self._make_struct()
+        if self.block_bounds is not None and compute_block_bounds:
+            _check(lib().gs_scene_block_bounds(ctypes.byref(self.struct), _ptr(self.block_bounds), _stream(None)),
+                   "gs_scene_block_bounds")
+
+    @property
+    def n_blocks(self):
+        return 0 if self.block_offsets is None else self.block_offsets.numel() - 1
+
+    def _make_struct(self, use_blocks: bool = True) -> gs_scene:
+        s = gs_scene()
+        s.n, s.sh_degree, s.feat_dim = self.n, self.sh_degree, self.feat_dim
+        s.pos, s.quat, s.scale = _ptr(self.pos), _ptr(self.quat), _ptr(self.scale)
+        s.opacity, s.sh, s.feat = _ptr(self.opacity), _ptr(self.sh), _ptr(self.feat)
+        if use_blocks and self.block_offsets is not None:
+            s.n_blocks = self.n_blocks
+            s.block_offsets, s.block_bounds = _ptr(self.block_offsets), _ptr(self.block_bounds)
+        return s
+
+    def without_blocks(self) -> gs_scene:
+        return self._make_struct(use_blocks=False)
+
+    def nbytes(self) -> int:
+        ts = [self.pos, self.quat, self.scale, self.opacity, self.sh, self.feat]
+        return sum(x.numel() * x.element_size() for x in ts if x is not None)
+
+
+class ViewBatch:
+    """Host + device copies of a batch of gs_view descriptors (contiguous layout)."""
+
+    def __init__(self, views: Sequence, device="cuda"):
+        n = len(views)
+        arr = (gs_view * n)()
+        for i, v in enumerate(views):
+            R = np.asarray(v.R, np.float32).reshape(9)
+            t = np.asarray(v.t, np.float32).reshape(3)
+            for k in range(9):
+                arr[i].R[k] = float(R[k])
+            for k in range(3):
+                arr[i].t[k] = float(t[k])
+            arr[i].fx, arr[i].fy, arr[i].cx, arr[i].cy = v.fx, v.fy, v.cx, v.cy
+            arr[i].width, arr[i].height = v.width, v.height
+        tp, tt = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().gs_views_layout(arr, ctypes.c_int32(n), ctypes.byref(tp), ctypes.byref(tt)), "gs_views_layout")
+        self.host = arr
+        self.n = n
+        self.total_pixels = tp.value
+        self.total_tiles = tt.value
+        self.views = list(views)
+        raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
+        self.pinned = torch.from_numpy(raw).pin_memory() if torch.cuda.is_available() else torch.from_numpy(raw)
+        self.dev = torch.empty(raw.size, dtype=torch.uint8, device=device)
+        self.dev.copy_(self.pinned, non_blocking=True)
+
+    def upload(self, stream=None):
+        """Re-copy the descriptors (H2D, pinned) -- e2e path."""
+        self.dev.copy_(self.pinned, non_blocking=True)
+
+    @property
+    def dev_ptr(self):
+        return ctypes.c_void_p(self.dev.data_ptr())
+
+    def pix_offset(self, i):
+        return self.host[i].pix_offset
+
+    def tile_offset(self, i):
+        return self.host[i].tile_offset
+
+
+class Projected:
+    def __init__(self, n_views: int, rec_capacity: int, device="cuda"):
+        self.rec_capacity = int(rec_capacity)
+        self.rec = torch.empty(n_views * self.rec_capacity * (RECORD_BYTES // 4), dtype=torch.int32, device=device)
+        self.n_rec = torch.zeros(n_views, dtype=torch.int32, device=device)
+        self.diag = torch.zeros(4, dtype=torch.int64, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        s = gs_projected()
+        s.rec, s.rec_capacity = _ptr(self.rec), self.rec_capacity
+        s.n_rec, s.diag, s.status = _ptr(self.n_rec), _ptr(self.diag), _ptr(self.status)
+        self.struct = s
+
+    def records(self):
+        """Record view as a [n_views*cap, 16] int32 tensor (test inspection)."""
+        return self.rec.view(-1, RECORD_BYTES // 4)
+
+
+class Bins:
+    def __init__(self, total_tiles: int, pair_capacity: int, device="cuda", debug_keys: bool = False):
+        self.pair_capacity = int(pair_capacity)
+        self.ranges = torch.empty(total_tiles * 2, dtype=torch.int32, device=device)
+        self.sorted_rec = torch.empty(self.pair_capacity, dtype=torch.int32, device=device)
+        self.n_pairs = torch.zeros(1, dtype=torch.int64, device=device)
+        self.sorted_key = torch.empty(self.pair_capacity, dtype=torch.int64, device=device) if debug_keys else None
+        s = gs_bins()
+        s.ranges, s.sorted_rec, s.pair_capacity = _ptr(self.ranges), _ptr(self.sorted_rec), self.pair_capacity
+        s.n_pairs, s.sorted_key = _ptr(self.n_pairs), _ptr(self.sorted_key)
+        self.struct = s
+
+
+class Images:
+    def __init__(self, total_pixels: int, feat_dim: int, device="cuda"):
+        self.rgb = torch.empty(3 * total_pixels, dtype=torch.float32, device=device)
+        self.depth = torch.empty(total_pixels, dtype=torch.float32, device=device)
+        self.alpha = torch.empty(total_pixels, dtype=torch.float32, device=device)
+        self.feat = torch.empty(feat_dim * total_pixels, dtype=torch.float32, device=device) if feat_dim else None
+        s = gs_images()
+        s.rgb, s.depth, s.alpha, s.feat = _ptr(self.rgb), _ptr(self.depth), _ptr(self.alpha), _ptr(self.feat)
+        self.struct = s
+        self.feat_dim = feat_dim
+
+    def view_planes(self, vb: ViewBatch, i: int):
+        v = vb.views[i]
+        H, W = v.height, v.width
+        o = vb.pix_offset(i)
+        hw = H * W
+        out = dict(rgb=self.rgb[3 * o:3 * o + 3 * hw].view(3, H, W), depth=self.depth[o:o + hw].view(H, W),
+                   alpha=self.alpha[o:o + hw].view(H, W))
+        if self.feat is not None:
+            D = self.feat_dim
+            out["feat"] = self.feat[D * o:D * o + D * hw].view(D, H, W)
+        return out
+
+
+# ------------------------------------------------------------------ the four calls
+def project_workspace_bytes(n_blocks: int, n_views: int) -> int:
+    return int(lib().gs_project_workspace_bytes(n_blocks, n_views))
+
+
+def bin_sort_workspace_bytes(pair_capacity: int, total_tiles: int) -> int:
+    return int(lib().gs_bin_sort_workspace_bytes(pair_capacity, total_tiles))
+
+
+def gs_project(scene: DeviceScene, views: ViewBatch, params: gs_params, proj: Projected, ws: torch.Tensor,
+               stream=None, scene_struct: Optional[gs_scene] = None):
+    s = scene.struct if scene_struct is None else scene_struct
+    _check(lib().gs_project(ctypes.byref(s), views.host, views.dev_ptr, ctypes.c_int32(views.n), ctypes.byref(params),
+                            ctypes.byref(proj.struct), _ptr(ws), ctypes.c_size_t(ws.numel() * ws.element_size()),
+                            _stream(stream)), "gs_project")
+
+
+def gs_bin_sort(proj: Projected, views: ViewBatch, bins: Bins, ws: torch.Tensor, stream=None):
+    _check(lib().gs_bin_sort(ctypes.byref(proj.struct), views.host, views.dev_ptr, ctypes.c_int32(views.n),
+                             ctypes.byref(bins.struct), _ptr(ws), ctypes.c_size_t(ws.numel() * ws.element_size()),
+                             _stream(stream)), "gs_bin_sort")
+
+
+def gs_rasterize(scene: DeviceScene, proj: Projected, bins: Bins, views: ViewBatch, params: gs_params,
+                 images: Images, stream=None):
+    _check(lib().gs_rasterize(ctypes.byref(scene.struct), ctypes.byref(proj.struct), ctypes.byref(bins.struct),
+                              views.host, views.dev_ptr, ctypes.c_int32(views.n), ctypes.byref(params),
+                              ctypes.byref(images.struct), _stream(stream)), "gs_rasterize")
+
+
+def gs_backproject(images: Images, views: ViewBatch, a_min: float, xyz: torch.Tensor, valid: torch.Tensor,
+                   stream=None):
+    _check(lib().gs_backproject(ctypes.byref(images.struct), views.host, views.dev_ptr, ctypes.c_int32(views.n),
+                                ctypes.c_float(a_min), _ptr(xyz), _ptr(valid), _stream(stream)), "gs_backproject")

@@ -1,0 +1,124 @@
+"""Batch harness around the four C-ABI calls (buffer management only).
+
+``Renderer`` owns the caller-side buffers the C ABI asks for (records, pairs,
+images, workspaces), sizes them once from the device counters (the only
+host<->device sync), and then enqueues
+gs_project -> gs_bin_sort -> gs_rasterize -> gs_backproject on a stream with
+no host synchronisation.  No arithmetic of the method happens here.
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import torch
+
+from . import gs as G
+
+
+class Renderer:
+    def __init__(self, scene: G.DeviceScene, views: Sequence, params: Optional[G.gs_params] = None,
+                 a_min: float = 0.5, backproject: bool = True, rec_capacity: Optional[int] = None,
+                 pair_capacity: Optional[int] = None, debug_keys: bool = False, use_blocks: bool = True,
+                 device="cuda"):
+        self.device = torch.device(device)
+        self.scene = scene
+        self.scene_struct = scene.struct if use_blocks else scene.without_blocks()
+        self.vb = views if isinstance(views, G.ViewBatch) else G.ViewBatch(views, device=device)
+        self.params = params if params is not None else G.default_params()
+        self.a_min = a_min
+        self.do_backproject = backproject
+        self.debug_keys = debug_keys
+        n_views = self.vb.n
+        self.ws_proj = torch.empty(max(1, G.project_workspace_bytes(scene.n_blocks if use_blocks else 0, n_views)),
+                                   dtype=torch.uint8, device=self.device)
+        self.images = G.Images(self.vb.total_pixels, scene.feat_dim, device=self.device)
+        self.xyz = torch.empty(3 * self.vb.total_pixels, dtype=torch.float32, device=self.device) if backproject else None
+        self.valid = torch.empty(self.vb.total_pixels + 4, dtype=torch.uint8, device=self.device) if backproject else None
+        self.proj = None
+        self.bins = None
+        self.ws_bin = None
+        self._alloc(rec_capacity, pair_capacity)
+
+    # ------------------------------------------------------------- buffers
+    def _alloc(self, rec_capacity, pair_capacity):
+        n_views = self.vb.n
+        if rec_capacity is None:
+            # first guess: visible Gaussians ~ pixels, bounded to ~4 GB of records;
+            # render() grows it to the device-reported count on overflow
+            max_px = max(v.width * v.height for v in self.vb.views)
+            rec_capacity = min(max(self.scene.n, 1), max(4096, max_px // 2),
+                               max(4096, (4 << 30) // (G.RECORD_BYTES * n_views)))
+        if pair_capacity is None:
+            # ~4 pairs per record, bounded to ~8 GB of pair buffers (28 B / pair)
+            pair_capacity = min(max(1 << 16, 4 * rec_capacity * n_views), (8 << 30) // 28)
+        pair_capacity = min(pair_capacity, (1 << 32) - 1)
+        rec_capacity = min(rec_capacity, ((1 << 32) - 1) // n_views)
+        if self.proj is None or self.proj.rec_capacity != rec_capacity:
+            self.proj = None
+            self.proj = G.Projected(n_views, rec_capacity, device=self.device)
+        if self.bins is None or self.bins.pair_capacity != pair_capacity:
+            self.bins = None
+            self.ws_bin = None
+            self.bins = G.Bins(self.vb.total_tiles, pair_capacity, device=self.device, debug_keys=self.debug_keys)
+            self.ws_bin = torch.empty(G.bin_sort_workspace_bytes(pair_capacity, self.vb.total_tiles),
+                                      dtype=torch.uint8, device=self.device)
+
+    # ------------------------------------------------------------- hot path
+    def run(self, stream=None):
+        """Enqueue the whole hot path for the batch (asynchronous)."""
+        self.proj.status.zero_()
+        G.gs_project(self.scene, self.vb, self.params, self.proj, self.ws_proj, stream, scene_struct=self.scene_struct)
+        G.gs_bin_sort(self.proj, self.vb, self.bins, self.ws_bin, stream)
+        G.gs_rasterize(self.scene, self.proj, self.bins, self.vb, self.params, self.images, stream)
+        if self.do_backproject:
+            G.gs_backproject(self.images, self.vb, self.a_min, self.xyz, self.valid, stream)
+
+    def status(self) -> int:
+        return int(self.proj.status.item())
+
+    def render(self, max_retries: int = 4):
+        """Run, and on capacity overflow grow the buffers to the reported sizes and re-run."""
+        for _ in range(max_retries):
+            self.run()
+            st = self.status()
+            if st == 0:
+                return self
+            rec_cap = self.proj.rec_capacity
+            pair_cap = self.bins.pair_capacity
+            if st & G.GS_STATUS_RECORD_OVERFLOW:
+                rec_cap = int(self.proj.n_rec.max().item() * 1.1) + 64
+            else:
+                pair_cap = int(self.bins.n_pairs.item() * 1.1) + 1024
+            self._alloc(rec_cap, pair_cap)
+        raise G.GSError(f"capacity overflow persisted after {max_retries} retries")
+
+    def fit_capacities(self, slack: float = 1.05):
+        """Shrink/grow the buffers to the counts of the last successful run."""
+        rec = int(self.proj.n_rec.max().item() * slack) + 64
+        pairs = int(self.bins.n_pairs.item() * slack) + 1024
+        self._alloc(rec, pairs)
+        return self
+
+    # ------------------------------------------------------------- outputs
+    def view_images(self, i: int):
+        out = self.images.view_planes(self.vb, i)
+        if self.do_backproject:
+            v = self.vb.views[i]
+            o = self.vb.pix_offset(i)
+            hw = v.width * v.height
+            out["xyz"] = self.xyz[3 * o:3 * o + 3 * hw].view(3, v.height, v.width)
+            out["valid"] = self.valid[o:o + hw].view(v.height, v.width)
+        return out
+
+    def view_records(self, i: int) -> torch.Tensor:
+        n = min(int(self.proj.n_rec[i].item()), self.proj.rec_capacity)
+        base = i * self.proj.rec_capacity
+        return self.proj.records()[base:base + n]
+
+    def n_pairs(self) -> int:
+        return int(self.bins.n_pairs.item())
+
+    def bytes_allocated(self) -> int:
+        ts = [self.proj.rec, self.bins.sorted_rec, self.ws_bin, self.images.rgb, self.images.depth,
+              self.images.alpha, self.images.feat, self.xyz, self.valid]
+        return sum(t.numel() * t.element_size() for t in ts if t is not None)

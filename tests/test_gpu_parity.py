@@ -1,0 +1,255 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bit-exact records / keys / ranges; images within the
+north_star tolerances (tests/parity.py).  All tests need a B200."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from helpers import random_tiny_scene, scene_of
+import parity as PT
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def G():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2507_15683_b200 as G
+    G.lib()
+    return G
+
+
+def _gpu_render(G, scene, views, use_blocks=True, debug_keys=True, feat=True, **kw):
+    ds = G.DeviceScene(scene)
+    r = G.Renderer(ds, views, debug_keys=debug_keys, use_blocks=use_blocks, **kw)
+    r.render()
+    torch.cuda.synchronize()
+    return r
+
+
+def compare_view(G, r, i, scene, view, orc, check_bp=True, report=None):
+    cap = r.proj.rec_capacity
+    n = min(int(r.proj.n_rec[i].item()), cap)
+    recs = PT.decode_records(r.proj.records()[i * cap:i * cap + n].cpu().numpy())
+    PT.check_records(recs, orc["rec"], i)
+    TX, TY = (view.width + 15) // 16, (view.height + 15) // 16
+    t0 = r.vb.tile_offset(i)
+    rg = r.bins.ranges.view(-1, 2)[t0:t0 + TX * TY].cpu().numpy().view(np.uint32)
+    s0, s1 = int(rg[0, 0]), int(rg[-1, 1])
+    sorted_rec = r.bins.sorted_rec[s0:s1].cpu().numpy().view(np.uint32).astype(np.int64)
+    idx = sorted_rec - i * cap
+    assert ((idx >= 0) & (idx < n)).all(), "pair points outside its view's records"
+    tiles = np.repeat(np.arange(TX * TY, dtype=np.uint32), (rg[:, 1] - rg[:, 0]).astype(np.int64))
+    gk = (tiles, recs["z"][idx].view(np.uint32), recs["gid"][idx], (rg.astype(np.int64) - s0).astype(np.uint32))
+    PT.check_keys(gk, orc["keys"])
+    if r.bins.sorted_key is not None:
+        sk = r.bins.sorted_key[s0:s1].cpu().numpy().view(np.uint64)
+        np.testing.assert_array_equal((sk >> np.uint64(32)).astype(np.uint32) - np.uint32(t0), orc["keys"]["tile"])
+        np.testing.assert_array_equal((sk & np.uint64(0xFFFFFFFF)).astype(np.uint32), orc["keys"]["depth"])
+    img = {k: v.cpu().numpy() for k, v in r.view_images(i).items()}
+    stats = PT.check_images(img, orc, report=report)
+    if check_bp and "xyz" in img and "xyz" in orc:
+        PT.check_backproject(img["xyz"], img["valid"], orc["xyz"], orc["valid"], orc["flags"], orc["depth"],
+                             orc["alpha"])
+    return stats
+
+
+# ------------------------------------------------------------------ C1 + tiny
+def test_c1_full_parity(G, orc):
+    sc, vs = synth.make_config("C1")
+    r = _gpu_render(G, sc, vs)
+    o = orc.render(sc, vs[0], a_min=0.5)
+    compare_view(G, r, 0, sc, vs[0], o)
+
+
+def test_c1_features_D8(G, orc):
+    sc = synth.box_v1(1000, seed=11, feat_dim=8)
+    v = synth.box_view()
+    r = _gpu_render(G, sc, [v])
+    o = orc.render(sc, v, a_min=0.5)
+    compare_view(G, r, 0, sc, v, o)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_tiny_ragged(G, orc, seed):
+    """Ragged image sizes (partial edge tiles), behind-camera / off-screen /
+    transparent Gaussians, depth ties, un-normalised q, SH 0-3, D in {0, 4, 12}."""
+    rng = np.random.default_rng(500 + seed)
+    D = [0, 4, 12][seed % 3]
+    sc = random_tiny_scene(rng, int(rng.integers(20, 400)), feat_dim=D, sh_degree=seed % 4)
+    W, H = int(rng.integers(1, 90)), int(rng.integers(1, 70))
+    v = synth.make_view(np.eye(3), np.zeros(3), 40.0, 40.0, W / 2 - 0.5, H / 2 - 0.5, W, H)
+    r = _gpu_render(G, sc, [v])
+    o = orc.render(sc, v, a_min=0.5)
+    compare_view(G, r, 0, sc, v, o)
+
+
+def test_empty_scene(G, orc):
+    sc = scene_of([])
+    v = synth.box_view()
+    r = _gpu_render(G, sc, [v])
+    img = r.view_images(0)
+    assert not img["rgb"].any() and not img["alpha"].any() and not img["depth"].any()
+    assert not img["valid"].any()
+
+
+def test_all_culled(G, orc):
+    sc = scene_of([{"mu": [0, 0, -5]}, {"mu": [100, 0, 5]}, {"mu": [0, 0, 5], "opacity": 0.001}])
+    v = synth.box_view()
+    r = _gpu_render(G, sc, [v])
+    assert int(r.proj.n_rec[0]) == 0 and r.n_pairs() == 0
+    d = r.proj.diag.cpu().numpy()
+    assert list(d) == [1, 1, 0, 1]
+    assert not r.view_images(0)["alpha"].any()
+
+
+def test_diag_counters_match_oracle(G, orc):
+    sc = scene_of([{"mu": [0, 0, 5], "scale": [0.1, 0.0, 0.1]}, {"mu": [0, 0, 5], "opacity": 0.001},
+                   {"mu": [-10.0, 0, 5], "scale": 0.01}, {"mu": [0, 0, 0.1]}, {"mu": [0, 0, 5], "quat": [0, 0, 0, 0]},
+                   {"mu": [0, 0, 5]}])
+    v = synth.make_view(np.eye(3), np.zeros(3), 100, 100, 50, 50, 100, 100)
+    r = _gpu_render(G, sc, [v])
+    o = orc.project(sc, v)
+    d = r.proj.diag.cpu().numpy()
+    assert list(d) == [o["diag"]["near"], o["diag"]["transparent"], o["diag"]["degenerate"], o["diag"]["offscreen"]]
+
+
+def test_overflow_then_recovery(G, orc):
+    """Tiny capacities set the status bits; Renderer.render re-runs with the
+    sizes the device reported and then matches the oracle."""
+    sc, vs = synth.make_config("C1")
+    ds = G.DeviceScene(sc)
+    r = G.Renderer(ds, vs, rec_capacity=16, pair_capacity=64, debug_keys=True)
+    r.run()
+    assert r.status() & 1
+    r.render()
+    assert r.status() == 0
+    o = orc.render(sc, vs[0], a_min=0.5)
+    compare_view(G, r, 0, sc, vs[0], o)
+    r2 = G.Renderer(ds, vs, pair_capacity=64)
+    r2.run()
+    assert r2.status() == 2 and r2.n_pairs() == len(o["keys"]["tile"])
+
+
+# ------------------------------------------------------------------ aerial configs
+def test_c2_full_size_parity(G, orc):
+    """C2 at its BASELINE size (200k Gaussians, SH 3, 1024x768): whole image."""
+    sc, vs = synth.make_config("C2")
+    r = _gpu_render(G, sc, vs)
+    o = orc.render(sc, vs[0], a_min=0.5)
+    st = compare_view(G, r, 0, sc, vs[0], o)
+    print("C2 stats", st)
+
+
+def test_c2_blocks_do_not_change_result(G, orc):
+    sc, vs = synth.make_config("C2", scale=0.25)
+    a = _gpu_render(G, sc, vs, use_blocks=True)
+    b = _gpu_render(G, sc, vs, use_blocks=False)
+    for k in ("rgb", "depth", "alpha"):
+        assert torch.equal(a.view_images(0)[k], b.view_images(0)[k])
+
+
+def test_c3_pyramid_parity(G, orc):
+    """C3 shape (5-level pyramid 64x48 -> 1024x768, D = 32, SH 3) at reduced N;
+    each level against the oracle; level 4 == the same camera rendered alone
+    (batching invariance, Q21)."""
+    sc, vs = synth.make_config("C3", scale=0.02)
+    r = _gpu_render(G, sc, vs)
+    for i, v in enumerate(vs):
+        o = orc.render(sc, v, a_min=0.5)
+        compare_view(G, r, i, sc, v, o)
+    alone = _gpu_render(G, sc, [vs[-1]])
+    for k in ("rgb", "depth", "alpha", "feat"):
+        assert torch.equal(alone.view_images(0)[k], r.view_images(len(vs) - 1)[k])
+
+
+def test_c3_coarse_level_long_lists(G, orc):
+    """Coarse pyramid level with very long tile lists (> 8192 entries per tile):
+    exercises the shared-memory bitonic + merge-path path of gs_bin_sort."""
+    sc, vs = synth.make_config("C3", scale=0.1)
+    v = vs[0]
+    r = _gpu_render(G, sc, [v])
+    o = orc.render(sc, v, a_min=0.5)
+    rg = o["keys"]["ranges"]
+    assert (rg[:, 1] - rg[:, 0]).max() > 8192
+    compare_view(G, r, 0, sc, v, o)
+
+
+def test_c4_batch_parity_and_invariance(G, orc):
+    """C4 shape (256-pose grid, D = 32) at reduced N: 6 views of the batch vs
+    the oracle; a view rendered inside the batch equals the view alone."""
+    sc, vs = synth.make_config("C4", scale=0.02)
+    vs = vs[:24]
+    r = _gpu_render(G, sc, vs)
+    for i in (0, 5, 11, 17, 23):
+        o = orc.render(sc, vs[i], a_min=0.5)
+        compare_view(G, r, i, sc, vs[i], o)
+    alone = _gpu_render(G, sc, [vs[11]])
+    for k in ("rgb", "depth", "alpha", "feat", "xyz", "valid"):
+        assert torch.equal(alone.view_images(0)[k], r.view_images(11)[k])
+
+
+def test_c5_oblique_parity(G, orc):
+    """C5 shape (oblique 1920x1080, 8 blocks, backprojection) at reduced N."""
+    sc, vs = synth.make_config("C5", scale=0.005)
+    vs = vs[:4]
+    r = _gpu_render(G, sc, vs)
+    for i in (0, 3):
+        o = orc.render(sc, vs[i], a_min=0.5)
+        compare_view(G, r, i, sc, vs[i], o)
+
+
+def test_determinism_run_to_run(G, orc):
+    sc, vs = synth.make_config("C4", scale=0.01)
+    vs = vs[:8]
+    ds = G.DeviceScene(sc)
+    r = G.Renderer(ds, vs)
+    r.render()
+    first = {k: v.clone() for k, v in r.view_images(3).items()}
+    keys = r.bins.sorted_rec.clone()
+    for _ in range(3):
+        r.run()
+        torch.cuda.synchronize()
+        for k, v in r.view_images(3).items():
+            assert torch.equal(v, first[k]), k
+        assert torch.equal(keys, r.bins.sorted_rec)
+
+
+def test_backproject_kernel_on_oracle_images(G, orc):
+    """gs_backproject in isolation: fed the oracle's own depth/alpha planes,
+    it must match the oracle's back-projection (|dX| <= 1e-3 scene scale,
+    identical valid masks except flagged pixels)."""
+    sc, vs = synth.make_config("C2", scale=0.25)
+    v = vs[0]
+    o = orc.render(sc, v, a_min=0.5)
+    vb = G.ViewBatch([v])
+    img = G.Images(vb.total_pixels, 0)
+    img.depth.copy_(torch.from_numpy(o["depth"].reshape(-1)))
+    img.alpha.copy_(torch.from_numpy(o["alpha"].reshape(-1)))
+    xyz = torch.empty(3 * vb.total_pixels, device="cuda")
+    valid = torch.empty(vb.total_pixels, dtype=torch.uint8, device="cuda")
+    G.gs_backproject(img, vb, 0.5, xyz, valid)
+    torch.cuda.synchronize()
+    H, W = v.height, v.width
+    PT.check_backproject(xyz.view(3, H, W).cpu().numpy(), valid.view(H, W).cpu().numpy(), o["xyz"], o["valid"],
+                         o["flags"], o["depth"], o["alpha"])
+
+
+# ------------------------------------------------------------------ full-size sampled parity
+@pytest.mark.parametrize("cfg,views", [("C4", (0, 137)), ("C5", (9,))])
+def test_full_size_sampled_views(G, orc, cfg, views):
+    """BASELINE sizes in the bench's launch configuration (whole batch in one
+    launch of each kernel): sampled views compared whole against the oracle."""
+    sc, vs = synth.make_config(cfg)
+    ds = G.DeviceScene(sc)
+    r = G.Renderer(ds, vs, debug_keys=False)
+    r.render()
+    torch.cuda.synchronize()
+    for i in views:
+        o = orc.render(sc, vs[i], a_min=0.5)
+        compare_view(G, r, i, sc, vs[i], o)
