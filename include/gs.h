@@ -135,15 +135,17 @@ typedef struct gs_params {
 /*
  * One projected (view, Gaussian) record, 64 bytes.  u, v, z, conic, rect,
  * radius are computed in IEEE fp32 in the operation order of DESIGN.md §4.1
- * (bit-identical to the oracle); rgb is SH colour (tolerance only); ext_x/y
- * are the half-extents of the bounding box of the alpha >= alpha_min ellipse,
- * inflated by a safety margin (used only to skip provably-zero work).
+ * (bit-identical to the oracle); rgb is SH colour (tolerance only); q_cut is
+ * the alpha >= alpha_min ellipse threshold on q(d) = d^T conic d,
+ * 2 ln(opacity / alpha_min), inflated by 5% + 0.01 (used only by the
+ * rasterizer to skip provably-zero work).
  */
 typedef struct gs_record {
     float u, v;                       /* pixel-space mean */
     float conic_a, conic_b, conic_c;  /* inverse 2D covariance (a, b; b, c) */
     float opacity;
-    float ext_x, ext_y;
+    float q_cut;
+    float reserved;
     float rgb[3];
     float z;                          /* camera-space depth (depth key = its bits, O9) */
     uint32_t gid;                     /* Gaussian index in the scene */

@@ -341,10 +341,11 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
                     r.u = u; r.v = v; r.z = pz;
                     r.conic_a = ca; r.conic_b = cb; r.conic_c = ccn;
                     r.opacity = op;
-                    // alpha >= alpha_min ellipse q <= thr: bbox half extents sqrt(thr a), sqrt(thr c),
-                    // inflated 2% (+0.05 px) so fp32 evaluation noise can never reach outside
-                    r.ext_x = sqrtf(thr * a) * 1.02f + 0.05f;
-                    r.ext_y = sqrtf(thr * cc) * 1.02f + 0.05f;
+                    // alpha >= alpha_min  <=>  q(d) = d^T conic d <= thr = 2 ln(o / alpha_min).
+                    // q_cut inflates thr (5% + 0.01) so the rasterizer's per-warp ellipse cull stays
+                    // conservative against fp32 evaluation noise of power and exp.
+                    r.q_cut = thr * 1.05f + 0.01f;
+                    r.reserved = 0.0f;
                     r.gid = (uint32_t)i;
                     r.view_radius = (uint32_t)vi | ((uint32_t)fminf(rad, 65535.0f) << 16);
                     // O10: SH colour at d = (mu - c_cam)/|mu - c_cam|

@@ -5,52 +5,163 @@
 // rasterization"; "render dense feature and depth maps"; S:157;
 // readings Q4, Q11, Q14-Q18.
 //
-// Design (B200, SIMT -- not a dense contraction, no tensor cores):
-//   * one 256-thread CTA per 16x16 tile; each warp owns an 8x4 sub-tile;
-//   * the tile's sorted list is staged through shared memory in chunks of 64
-//     records (+ their feature rows) with cp.async (LDGSTS) bulk copies;
-//   * warp-level culling: the 32 lanes test 32 list entries at once against
-//     the warp's 8x4 sub-tile using the bounding box of each Gaussian's
-//     alpha >= 1/255 ellipse (conservative, so it never drops a Gaussian the
-//     oracle would blend -- Q11); a ballot gives the entries the warp walks;
-//   * warp-ballot early termination: a warp stops when all 32 pixels have
-//     hit T < t_min; the CTA stops when all warps have.
-// The per-pixel arithmetic that decides a skip / stop (power, alpha, Tn) is
-// written with explicit _rn intrinsics in the oracle's operation order.
+// Design (B200):
+//   * one CTA per 16x16 tile = 8 consumer warps (one 8x4 sub-tile each) + 1
+//     producer warp;
+//   * the producer streams the tile's sorted list through a 4-stage
+//     shared-memory ring with TMA bulk copies (cp.async.bulk, one 64-B record
+//     and one D*4-B feature row per entry) completing on mbarriers; consumers
+//     release stages through "empty" mbarriers -- no CTA-wide barrier in the
+//     loop;
+//   * exact warp-level culling: each lane tests one staged entry: does the
+//     entry's alpha >= alpha_min ellipse (q <= q_cut, inflated) touch the warp's
+//     8x4 pixel rectangle?  A ballot gives the entries the warp walks
+//     (conservative, so it never drops a Gaussian the oracle blends -- Q11);
+//   * per pixel the skip / stop decisions (power, alpha, Tn) are evaluated with
+//     explicit _rn intrinsics in the oracle's operation order;
+//   * the feature blend F[px][:] += w[px][k] f[k][:] -- the one dense
+//     contraction of the path -- runs on the tensor cores: each warp compacts
+//     the weights of its walked entries into an 8-entry shared buffer and
+//     issues m16n8k8 TF32 MMAs (weights split hi+lo, features rounded once:
+//     error <= 2^-11 sum w|f|, inside the 1e-3 max(1,|f|) tolerance);
+//   * warp-ballot early termination once all 32 pixels have T < t_min.
 #include "gs_common.cuh"
 
 namespace gs {
 namespace {
 
-constexpr int RT_THREADS = 256;
-constexpr int CH = 64;  // list entries staged per chunk
+constexpr int NCW = 8;                 // consumer warps
+constexpr int RT_THREADS = (NCW + 1) * 32;
+constexpr int SE = 64;                 // entries per stage
+constexpr int NST = 4;                 // ring stages
+constexpr int WB_STRIDE = 40;          // weight-buffer row stride (conflict-free A fragments)
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// TMA 1-D bulk copy global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
 
 template <int D>
-struct SmemT {
-    float4 rec[CH][4];               // full 64-byte records
-    float feat[D > 0 ? CH : 1][D > 0 ? D : 1];
+struct RasterSmem {
+    static constexpr int FS = D > 0 ? D + 8 : 1;   // feature row stride (floats)
+    float4 rec[NST][SE][4];                        // 64-byte records
+    float feat[D > 0 ? NST : 1][D > 0 ? SE : 1][FS];
+    float wbuf[D > 0 ? NCW : 1][8][WB_STRIDE];     // per-warp compacted weights [k][pixel]
+    int ent[NCW][8];                               // per-warp compacted entry index
+    uint64_t full[NST];
+    uint64_t empty[NST];
     int view;
 };
 
+// min over the 8x4 pixel-centre rectangle [x0,x1]x[y0,y1] of
+// q(d) = ca dx^2 + 2 cb dx dy + cc dy^2 (d = p - mean), compared with q_cut.
+__device__ __forceinline__ bool ellipse_hits_rect(float u, float v, float ca, float cb, float cc, float qcut,
+                                                  float x0, float x1, float y0, float y1) {
+    const bool inx = u >= x0 && u <= x1, iny = v >= y0 && v <= y1;
+    if (inx && iny) return true;
+    float qmin = 3.4e38f;
+    if (!inx) {               // facing vertical edge
+        const float dx = (u < x0 ? x0 : x1) - u;
+        const float dy = fminf(fmaxf(-cb * dx * __frcp_rn(cc), y0 - v), y1 - v);
+        qmin = fminf(qmin, ca * dx * dx + 2.f * cb * dx * dy + cc * dy * dy);
+    }
+    if (!iny) {               // facing horizontal edge
+        const float dy = (v < y0 ? y0 : y1) - v;
+        const float dx = fminf(fmaxf(-cb * dy * __frcp_rn(ca), x0 - u), x1 - u);
+        qmin = fminf(qmin, ca * dx * dx + 2.f * cb * dx * dy + cc * dy * dy);
+    }
+    return qmin <= qcut;
+}
+
 template <int D>
-__global__ void __launch_bounds__(RT_THREADS)
+__global__ void __launch_bounds__(RT_THREADS, (D > 32 ? 1 : 2))
 rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record* __restrict__ rec,
                  const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ ranges,
                  const float* __restrict__ feat, gs_params P, float* __restrict__ out_rgb,
                  float* __restrict__ out_depth, float* __restrict__ out_alpha, float* __restrict__ out_feat,
                  const uint32_t* __restrict__ status) {
     if (*status) return;
-    __shared__ __align__(16) SmemT<D> sm;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    RasterSmem<D>& sm = *reinterpret_cast<RasterSmem<D>*>(smem_raw);
     const uint32_t tile = blockIdx.x;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) sm.view = find_view_by_tile(views, n_views, tile);
+    if (threadIdx.x == 0) {
+        sm.view = find_view_by_tile(views, n_views, tile);
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     __syncthreads();
+    const uint32_t rs = __ldg(&ranges[2 * tile]), re = __ldg(&ranges[2 * tile + 1]);
+    const uint32_t L = re - rs;
+    const int nstage = (int)((L + SE - 1) / SE);
+
+    if (warp == NCW) {
+        // ------------------------------------------------------------ producer
+        for (int s = 0; s < nstage; ++s) {
+            const int buf = s % NST;
+            if (s >= NST) mbar_wait(&sm.empty[buf], ((s / NST) & 1) ^ 1);
+            const uint32_t c0 = rs + (uint32_t)s * SE;
+            const int cnt = (int)min((uint32_t)SE, re - c0);
+            if (lane == 0) mbar_arrive_expect_tx(&sm.full[buf], (uint32_t)cnt * (64u + 4u * D));
+            __syncwarp();
+            for (int j = (int)lane; j < cnt; j += 32) {
+                const uint32_t slot = __ldg(&sorted_rec[c0 + j]);
+                bulk_g2s(&sm.rec[buf][j][0], rec + slot, 64u, &sm.full[buf]);
+                if (D > 0) {
+                    const uint32_t gid = __ldg(&rec[slot].gid);
+                    bulk_g2s(&sm.feat[buf][j][0], feat + (int64_t)gid * D, 4u * D, &sm.full[buf]);
+                }
+            }
+        }
+        // drain: the CTA must not retire while bulk copies into its smem are in flight
+        for (int s = (nstage > NST ? nstage - NST : 0); s < nstage; ++s)
+            mbar_wait(&sm.full[s % NST], (s / NST) & 1);
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
     const gs_view& V = views[sm.view];
     const int W = V.width, H = V.height;
     const int TX = (W + GS_TILE - 1) / GS_TILE;
@@ -60,98 +171,170 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     const int px = sx + (int)(lane & 7u), py = sy + (int)(lane >> 3);
     const bool inside = px < W && py < H;
     const float pxf = (float)px, pyf = (float)py;
-    const float sx0 = (float)sx, sx1 = (float)(sx + 7), sy0 = (float)sy, sy1 = (float)(sy + 3);
+    const float rx0 = (float)sx, rx1 = (float)(sx + 7), ry0 = (float)sy, ry1 = (float)(sy + 3);
 
-    const uint32_t rs = ranges[2 * tile], re = ranges[2 * tile + 1];
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Dz = 0.f;
-    float F[D > 0 ? D : 1];
-#pragma unroll
-    for (int c = 0; c < (D > 0 ? D : 1); ++c) F[c] = 0.f;
     bool done = !inside;
+    bool warp_done = __all_sync(0xffffffffu, done);
+    constexpr int NT = D > 0 ? D / 8 : 1;   // n-tiles of 8 features (D % 8 == 4 handled by a padded tile)
+    constexpr int NTP = D > 0 ? (D + 7) / 8 : 1;
+    float acc[2][NTP][4];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int n = 0; n < NTP; ++n) acc[m][n][0] = acc[m][n][1] = acc[m][n][2] = acc[m][n][3] = 0.f;
+    (void)NT;
+    int nc = 0;   // compacted weights pending in this warp's buffer
+    const int g = (int)(lane >> 2), t4 = (int)(lane & 3u);
 
-    for (uint32_t c0 = rs; c0 < re; c0 += CH) {
-        const int cnt = (int)min((uint32_t)CH, re - c0);
-        // ---- stage records (and feature rows) of this chunk ----
-        {
-            const int j = threadIdx.x >> 2, piece = threadIdx.x & 3;
-            if (j < cnt) {
-                const uint32_t slot = __ldg(&sorted_rec[c0 + j]);
-                cp_async16(&sm.rec[j][piece], reinterpret_cast<const float4*>(rec + slot) + piece);
-                if (D > 0) {
-                    const uint32_t gid = __ldg(&rec[slot].gid);
-                    const float4* src = reinterpret_cast<const float4*>(feat + (int64_t)gid * D);
-                    for (int q = piece; q < D / 4; q += 4) cp_async16(&sm.feat[j][q * 4], src + q);
+    auto mma_flush = [&](int buf) {
+        if constexpr (D > 0) {
+            // pad rows nc..7 with zero weights, point them at a valid entry
+            for (int k = nc; k < 8; ++k) {
+                sm.wbuf[warp][k][lane] = 0.f;
+                if (lane == 0) sm.ent[warp][k] = sm.ent[warp][0];
+            }
+            __syncwarp();
+            uint32_t ahi[2][4], alo[2][4];
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+                const float a0 = sm.wbuf[warp][t4][m * 16 + g], a1 = sm.wbuf[warp][t4][m * 16 + g + 8];
+                const float a2 = sm.wbuf[warp][t4 + 4][m * 16 + g], a3 = sm.wbuf[warp][t4 + 4][m * 16 + g + 8];
+                const float av[4] = {a0, a1, a2, a3};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    ahi[m][i] = to_tf32(av[i]);
+                    alo[m][i] = to_tf32(av[i] - __uint_as_float(ahi[m][i]));
                 }
             }
-            cp_async_wait_all();
-            __syncthreads();
+            const int e0 = sm.ent[warp][t4], e1 = sm.ent[warp][t4 + 4];
+            const float* f0 = &sm.feat[buf][e0][0];
+            const float* f1 = &sm.feat[buf][e1][0];
+#pragma unroll
+            for (int n = 0; n < NTP; ++n) {
+                const int ch = n * 8 + g;
+                const uint32_t b0 = to_tf32(ch < D ? f0[ch] : 0.f), b1 = to_tf32(ch < D ? f1[ch] : 0.f);
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    mma_tf32(acc[m][n], ahi[m], b0, b1);
+                    mma_tf32(acc[m][n], alo[m], b0, b1);
+                }
+            }
+            __syncwarp();
+            nc = 0;
         }
-        // ---- walk the chunk (warp-uniform) ----
-        if (!__all_sync(0xffffffffu, done)) {
-            for (int base = 0; base < cnt; base += 32) {
-                const int j = base + (int)lane;
+    };
+
+    for (int s = 0; s < nstage; ++s) {
+        const int buf = s % NST;
+        mbar_wait(&sm.full[buf], (s / NST) & 1);
+        if (!warp_done) {
+            const int cnt = (int)min((uint32_t)SE, re - (rs + (uint32_t)s * SE));
+#pragma unroll 1
+            for (int half = 0; half < SE / 32; ++half) {
+                const int j = half * 32 + (int)lane;
                 bool hit = false;
                 if (j < cnt) {
-                    const float4 a = sm.rec[j][0], b = sm.rec[j][1];
-                    hit = a.x + b.z >= sx0 && a.x - b.z <= sx1 && a.y + b.w >= sy0 && a.y - b.w <= sy1;
+                    const float4 a = sm.rec[buf][j][0];   // u, v, ca, cb
+                    const float4 b = sm.rec[buf][j][1];   // cc, o, q_cut, -
+                    hit = ellipse_hits_rect(a.x, a.y, a.z, a.w, b.x, b.z, rx0, rx1, ry0, ry1);
                 }
-                uint32_t m = __ballot_sync(0xffffffffu, hit);
-                while (m) {
-                    const int k = base + __ffs(m) - 1;
-                    m &= m - 1u;
-                    if (done) continue;
-                    const float4 a = sm.rec[k][0];   // u, v, ca, cb
-                    const float4 b = sm.rec[k][1];   // cc, o, ex, ey
-                    const float dx = __fsub_rn(a.x, pxf), dy = __fsub_rn(a.y, pyf);
-                    const float t1 = __fmul_rn(__fmul_rn(a.z, dx), dx);
-                    const float t2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
-                    const float t3 = __fmul_rn(__fmul_rn(a.w, dx), dy);
-                    const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), t3);
-                    if (power > 0.0f) continue;
-                    const float alpha = fminf(P.alpha_max, __fmul_rn(b.y, __expf(power)));
-                    if (alpha < P.alpha_min) continue;
-                    const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-                    if (Tn < P.t_min) { done = true; continue; }
-                    const float w = __fmul_rn(alpha, T);
-                    const float4 c = sm.rec[k][2];   // r, g, b, z
-                    C0 += w * c.x; C1 += w * c.y; C2 += w * c.z; Dz += w * c.w;
-                    if (D > 0) {
-#pragma unroll
-                        for (int q = 0; q < D; q += 4) {
-                            const float4 f = *reinterpret_cast<const float4*>(&sm.feat[k][q]);
-                            F[q] += w * f.x; F[q + 1] += w * f.y; F[q + 2] += w * f.z; F[q + 3] += w * f.w;
+                uint32_t msk = __ballot_sync(0xffffffffu, hit);
+                while (msk) {
+                    const int k = half * 32 + __ffs(msk) - 1;
+                    msk &= msk - 1u;
+                    float wgt = 0.f;
+                    if (!done) {
+                        const float4 a = sm.rec[buf][k][0];
+                        const float4 b = sm.rec[buf][k][1];
+                        const float dx = __fsub_rn(a.x, pxf), dy = __fsub_rn(a.y, pyf);
+                        const float t1 = __fmul_rn(__fmul_rn(a.z, dx), dx);
+                        const float t2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
+                        const float t3 = __fmul_rn(__fmul_rn(a.w, dx), dy);
+                        const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), t3);
+                        if (!(power > 0.0f)) {          // oracle: skip iff power > 0
+                            const float alpha = fminf(P.alpha_max, __fmul_rn(b.y, __expf(power)));
+                            if (!(alpha < P.alpha_min)) {   // oracle: skip iff alpha < alpha_min
+                                const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+                                if (Tn < P.t_min) {
+                                    done = true;
+                                } else {
+                                    wgt = __fmul_rn(alpha, T);
+                                    const float4 c = sm.rec[buf][k][2];   // r, g, b, z
+                                    C0 = fmaf(wgt, c.x, C0);
+                                    C1 = fmaf(wgt, c.y, C1);
+                                    C2 = fmaf(wgt, c.z, C2);
+                                    Dz = fmaf(wgt, c.w, Dz);
+                                    T = Tn;
+                                }
+                            }
                         }
                     }
-                    T = Tn;
+                    if constexpr (D > 0) {
+                        sm.wbuf[warp][nc][lane] = wgt;
+                        if (lane == 0) sm.ent[warp][nc] = k;
+                        if (++nc == 8) {
+                            __syncwarp();
+                            mma_flush(buf);
+                        }
+                    }
                 }
-                if (__all_sync(0xffffffffu, done)) break;
+                warp_done = __all_sync(0xffffffffu, done);
+                if (warp_done) break;
+            }
+            if (D > 0 && nc > 0) {
+                __syncwarp();
+                mma_flush(buf);
             }
         }
-        const int active = __syncthreads_count(!done);
-        if (active == 0) break;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[buf]);
     }
+
+    // ---------------------------------------------------------------- outputs
+    const int64_t HW = (int64_t)W * H;
     if (inside) {
-        const int64_t HW = (int64_t)W * H;
-        const int64_t pix = V.pix_offset + (int64_t)py * W + px;
         const int64_t loc = (int64_t)py * W + px;
         out_rgb[3 * V.pix_offset + loc] = C0;
         out_rgb[3 * V.pix_offset + HW + loc] = C1;
         out_rgb[3 * V.pix_offset + 2 * HW + loc] = C2;
-        out_depth[pix] = Dz;
-        out_alpha[pix] = 1.0f - T;
-        if (D > 0) {
+        out_depth[V.pix_offset + loc] = Dz;
+        out_alpha[V.pix_offset + loc] = 1.0f - T;
+    }
+    if (D > 0) {
+        // accumulator (m, n, i): pixel p = 16 m + g + 8 (i >> 1) -> (sx + g, sy + 2 m + (i >> 1)),
+        // channel n*8 + 2 t4 + (i & 1)
+        float* fo = out_feat + (int64_t)D * V.pix_offset;
+        const int fx = sx + g;
 #pragma unroll
-            for (int c = 0; c < D; ++c) out_feat[(int64_t)D * V.pix_offset + (int64_t)c * HW + loc] = F[c];
-        }
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int fy = sy + 2 * m + (i >> 1);
+                if (fx < W && fy < H) {
+                    const int64_t loc = (int64_t)fy * W + fx;
+#pragma unroll
+                    for (int n = 0; n < NTP; ++n) {
+                        const int ch = n * 8 + 2 * t4 + (i & 1);
+                        if (ch < D) fo[(int64_t)ch * HW + loc] = acc[m][n][i];
+                    }
+                }
+            }
     }
 }
 
 template <int D>
 gs_status launch(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins, const gs_view* views_dev,
                  int n_views, int64_t T, const gs_params* P, gs_images* out, cudaStream_t s) {
-    rasterize_kernel<D><<<(unsigned)T, RT_THREADS, 0, s>>>(views_dev, n_views, proj->rec, bins->sorted_rec,
-                                                           bins->ranges, scene->feat, *P, out->rgb, out->depth,
-                                                           out->alpha, out->feat, proj->status);
+    const int smem = (int)sizeof(RasterSmem<D>);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(rasterize_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    rasterize_kernel<D><<<(unsigned)T, RT_THREADS, smem, s>>>(views_dev, n_views, proj->rec, bins->sorted_rec,
+                                                              bins->ranges, scene->feat, *P, out->rgb, out->depth,
+                                                              out->alpha, out->feat, proj->status);
     return check_launch("rasterize_kernel");
 }
 
@@ -175,6 +358,8 @@ extern "C" gs_status gs_rasterize(const gs_scene* scene, const gs_projected* pro
     GS_REQUIRE(scene->feat_dim == 0 || out->feat != nullptr, GS_INVALID_ARG, "feat_dim = %d but images.feat is NULL",
                scene->feat_dim);
     GS_REQUIRE(scene->feat_dim == 0 || scene->feat != nullptr, GS_INVALID_ARG, "scene feat is NULL");
+    GS_REQUIRE(((uintptr_t)proj->rec & 15) == 0 && (scene->feat_dim == 0 || ((uintptr_t)scene->feat & 15) == 0),
+               GS_INVALID_ARG, "records and features must be 16-byte aligned");
     cudaStream_t s = (cudaStream_t)stream;
     switch (scene->feat_dim) {
 #define GS_CASE(d) \

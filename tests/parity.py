@@ -27,7 +27,7 @@ def decode_records(rec_i32: np.ndarray):
     r = np.ascontiguousarray(rec_i32)
     f = r.view(np.float32)
     u32 = r.view(np.uint32)
-    return dict(u=f[:, 0], v=f[:, 1], conic=f[:, 2:5], opacity=f[:, 5], ext=f[:, 6:8], rgb=f[:, 8:11],
+    return dict(u=f[:, 0], v=f[:, 1], conic=f[:, 2:5], opacity=f[:, 5], q_cut=f[:, 6], rgb=f[:, 8:11],
                 z=f[:, 11], gid=u32[:, 12], view=u32[:, 13] & 0xFFFF, radius=(u32[:, 13] >> 16).astype(np.float32),
                 rect=np.stack([u32[:, 14] & 0xFFFF, u32[:, 14] >> 16, u32[:, 15] & 0xFFFF, u32[:, 15] >> 16], 1))
 
