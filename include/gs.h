@@ -169,6 +169,8 @@ typedef struct gs_bins {
     int64_t pair_capacity;
     uint64_t* n_pairs;       /* [1] pairs in the batch (= required capacity on overflow) */
     uint64_t* sorted_key;    /* optional [pair_capacity]: (tile in batch << 32) | depth_bits */
+    uint32_t* sorted_gid;    /* optional [pair_capacity]: gid of each pair (lets gs_rasterize fetch
+                                feature rows without a dependent record load) */
 } gs_bins;
 
 typedef struct gs_images {

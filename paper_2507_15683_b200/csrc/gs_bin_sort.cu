@@ -245,7 +245,8 @@ __device__ __forceinline__ void warp_bitonic(uint64_t (&k)[PER], uint32_t (&v)[P
 template <int PER>
 __device__ __forceinline__ void warp_sort_tile(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                                                uint32_t s, uint32_t len, uint32_t tile, uint32_t lane,
-                                               uint32_t* __restrict__ out, uint64_t* __restrict__ dbg) {
+                                               uint32_t* __restrict__ out, uint32_t* __restrict__ ogid,
+                                               uint64_t* __restrict__ dbg) {
     uint64_t k[PER];
     uint32_t v[PER];
 #pragma unroll
@@ -260,6 +261,7 @@ __device__ __forceinline__ void warp_sort_tile(const uint64_t* __restrict__ keys
         const uint32_t e = (uint32_t)j * 32u + lane;
         if (e < len) {
             out[s + e] = v[j];
+            if (ogid) ogid[s + e] = (uint32_t)k[j];
             if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | (k[j] >> 32);
         }
     }
@@ -267,8 +269,8 @@ __device__ __forceinline__ void warp_sort_tile(const uint64_t* __restrict__ keys
 
 __global__ void __launch_bounds__(256)
 warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint64_t* __restrict__ keys,
-                 const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, uint64_t* __restrict__ dbg,
-                 uint32_t* __restrict__ big_count, uint32_t* __restrict__ big_list,
+                 const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, uint32_t* __restrict__ ogid,
+                 uint64_t* __restrict__ dbg, uint32_t* __restrict__ big_count, uint32_t* __restrict__ big_list,
                  const uint32_t* __restrict__ status) {
     if (*status) return;
     const uint32_t lane = threadIdx.x & 31u;
@@ -276,11 +278,11 @@ warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint64_t*
     if (tile >= T) return;
     const uint32_t s = ranges[2 * tile], e = ranges[2 * tile + 1], len = e - s;
     if (len == 0) return;
-    if (len <= 32) warp_sort_tile<1>(keys, vals, s, len, (uint32_t)tile, lane, out, dbg);
-    else if (len <= 64) warp_sort_tile<2>(keys, vals, s, len, (uint32_t)tile, lane, out, dbg);
-    else if (len <= 128) warp_sort_tile<4>(keys, vals, s, len, (uint32_t)tile, lane, out, dbg);
-    else if (len <= 256) warp_sort_tile<8>(keys, vals, s, len, (uint32_t)tile, lane, out, dbg);
-    else if (len <= WARP_SORT_MAX) warp_sort_tile<16>(keys, vals, s, len, (uint32_t)tile, lane, out, dbg);
+    if (len <= 32) warp_sort_tile<1>(keys, vals, s, len, (uint32_t)tile, lane, out, ogid, dbg);
+    else if (len <= 64) warp_sort_tile<2>(keys, vals, s, len, (uint32_t)tile, lane, out, ogid, dbg);
+    else if (len <= 128) warp_sort_tile<4>(keys, vals, s, len, (uint32_t)tile, lane, out, ogid, dbg);
+    else if (len <= 256) warp_sort_tile<8>(keys, vals, s, len, (uint32_t)tile, lane, out, ogid, dbg);
+    else if (len <= WARP_SORT_MAX) warp_sort_tile<16>(keys, vals, s, len, (uint32_t)tile, lane, out, ogid, dbg);
     else if (lane == 0) big_list[atomicAdd(big_count, 1u)] = (uint32_t)tile;
 }
 
@@ -330,7 +332,7 @@ __device__ void cta_merge(const uint64_t* __restrict__ sk, const uint32_t* __res
 __global__ void __launch_bounds__(BIG_THREADS)
 big_sort_kernel(const uint32_t* __restrict__ ranges, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
                 uint64_t* __restrict__ keys2, uint32_t* __restrict__ vals2, uint32_t* __restrict__ out,
-                uint64_t* __restrict__ dbg, const uint32_t* __restrict__ big_count,
+                uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg, const uint32_t* __restrict__ big_count,
                 const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ status) {
     if (*status) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -372,6 +374,7 @@ big_sort_kernel(const uint32_t* __restrict__ ranges, uint64_t* __restrict__ keys
         }
         for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) {
             out[s + e] = cv[e];
+            if (ogid) ogid[s + e] = (uint32_t)ck[e];
             if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | (ck[e] >> 32);
         }
         __syncthreads();
@@ -422,7 +425,7 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
                                          proj->status);
     if ((st = check_launch("scatter_kernel")) != GS_OK) return st;
     warp_sort_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(out->ranges, T, w.keys, w.vals, out->sorted_rec,
-                                                             out->sorted_key, w.big_count, w.big_list, proj->status);
+                                                             out->sorted_gid, out->sorted_key, w.big_count, w.big_list, proj->status);
     if ((st = check_launch("warp_sort_kernel")) != GS_OK) return st;
     static bool attr_set = false;
     const int smem = SMEM_SORT_MAX * (sizeof(uint64_t) + sizeof(uint32_t));
@@ -431,7 +434,7 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
         attr_set = true;
     }
     big_sort_kernel<<<num_sms(), BIG_THREADS, smem, s>>>(out->ranges, w.keys, w.vals, w.keys2, w.vals2,
-                                                         out->sorted_rec, out->sorted_key, w.big_count, w.big_list,
+                                                         out->sorted_rec, out->sorted_gid, out->sorted_key, w.big_count, w.big_list,
                                                          proj->status);
     return check_launch("big_sort_kernel");
 }

@@ -6,13 +6,14 @@
 // readings Q4, Q11, Q14-Q18.
 //
 // Design (B200):
-//   * one CTA per 16x16 tile = 8 consumer warps (one 8x4 sub-tile each) + 1
-//     producer warp;
-//   * the producer streams the tile's sorted list through a 4-stage
-//     shared-memory ring with TMA bulk copies (cp.async.bulk, one 64-B record
-//     and one D*4-B feature row per entry) completing on mbarriers; consumers
-//     release stages through "empty" mbarriers -- no CTA-wide barrier in the
-//     loop;
+//   * a 16x16 tile is rendered by 8 consumer warps (one 8x4 sub-tile each)
+//     fed by 1 producer warp;
+//   * persistent CTAs (grid = SMs x resident CTAs); the producer streams
+//     the sorted lists of the CTA's tiles through a 6-stage shared-memory ring
+//     (cp.async 16-B gathers of the 64-B records and D*4-B feature rows,
+//     completion signalled on "full" mbarriers via cp.async.mbarrier.arrive),
+//     running ahead across tile boundaries; consumers release stages through
+//     "empty" mbarriers -- no CTA-wide barrier anywhere in the loop;
 //   * exact warp-level culling: each lane tests one staged entry: does the
 //     entry's alpha >= alpha_min ellipse (q <= q_cut, inflated) touch the warp's
 //     8x4 pixel rectangle?  A ballot gives the entries the warp walks
@@ -33,8 +34,9 @@ namespace {
 constexpr int NCW = 8;                 // consumer warps
 constexpr int RT_THREADS = (NCW + 1) * 32;
 constexpr int SE = 64;                 // entries per stage
-constexpr int NST = 4;                 // ring stages
+constexpr int NST = 6;                 // ring stages
 constexpr int WB_STRIDE = 40;          // weight-buffer row stride (conflict-free A fragments)
+constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -42,34 +44,34 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
 }
-// TMA 1-D bulk copy global -> shared, completion counted on an mbarrier
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+// the mbarrier receives one arrival when all prior cp.async of this thread have landed
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ uint32_t to_tf32(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(r) : "f"(x));
     return r;
 }
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -80,6 +82,12 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+struct StageMeta {
+    uint32_t tile, c0;
+    int32_t cnt, view;
+    uint32_t flags, pad0, pad1, pad2;
+};
+
 template <int D>
 struct RasterSmem {
     static constexpr int FS = D > 0 ? D + 8 : 1;   // feature row stride (floats)
@@ -87,9 +95,9 @@ struct RasterSmem {
     float feat[D > 0 ? NST : 1][D > 0 ? SE : 1][FS];
     float wbuf[D > 0 ? NCW : 1][8][WB_STRIDE];     // per-warp compacted weights [k][pixel]
     int ent[NCW][8];                               // per-warp compacted entry index
+    StageMeta meta[NST];
     uint64_t full[NST];
     uint64_t empty[NST];
-    int view;
 };
 
 // min over the 8x4 pixel-centre rectangle [x0,x1]x[y0,y1] of
@@ -112,85 +120,104 @@ __device__ __forceinline__ bool ellipse_hits_rect(float u, float v, float ca, fl
     return qmin <= qcut;
 }
 
+// alpha of entry k at this lane's pixel, or -1 when the oracle skips it
+// (power > 0 or alpha < alpha_min).  power in the oracle's op order.
+__device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, float pxf, float pyf,
+                                             const gs_params& P) {
+    const float dx = __fsub_rn(a.x, pxf), dy = __fsub_rn(a.y, pyf);
+    const float t1 = __fmul_rn(__fmul_rn(a.z, dx), dx);
+    const float t2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
+    const float t3 = __fmul_rn(__fmul_rn(a.w, dx), dy);
+    const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), t3);
+    const float alpha = fminf(P.alpha_max, __fmul_rn(b.y, ex2_ftz(power * 1.4426950408889634f)));
+    return ((power > 0.0f) || (alpha < P.alpha_min)) ? -1.0f : alpha;
+}
+
+// Persistent kernel: CTA c renders tiles c, c + grid, c + 2 grid, ...  The
+// producer warp runs ahead across tile boundaries so the consumers never wait
+// for a tile's first records.
 template <int D>
 __global__ void __launch_bounds__(RT_THREADS, (D > 32 ? 1 : 2))
 rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record* __restrict__ rec,
-                 const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ ranges,
-                 const float* __restrict__ feat, gs_params P, float* __restrict__ out_rgb,
-                 float* __restrict__ out_depth, float* __restrict__ out_alpha, float* __restrict__ out_feat,
-                 const uint32_t* __restrict__ status) {
+                 const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ sorted_gid,
+                 const uint32_t* __restrict__ ranges, uint32_t n_tiles, const float* __restrict__ feat,
+                 gs_params P, float* __restrict__ out_rgb, float* __restrict__ out_depth,
+                 float* __restrict__ out_alpha, float* __restrict__ out_feat, const uint32_t* __restrict__ status) {
     if (*status) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     RasterSmem<D>& sm = *reinterpret_cast<RasterSmem<D>*>(smem_raw);
-    const uint32_t tile = blockIdx.x;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
-        sm.view = find_view_by_tile(views, n_views, tile);
         for (int s = 0; s < NST; ++s) {
-            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.full[s], 33);     // 32 cp.async arrivals + 1 metadata arrival
             mbar_init(&sm.empty[s], NCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    const uint32_t rs = __ldg(&ranges[2 * tile]), re = __ldg(&ranges[2 * tile + 1]);
-    const uint32_t L = re - rs;
-    const int nstage = (int)((L + SE - 1) / SE);
 
     if (warp == NCW) {
         // ------------------------------------------------------------ producer
-        for (int s = 0; s < nstage; ++s) {
-            const int buf = s % NST;
-            if (s >= NST) mbar_wait(&sm.empty[buf], ((s / NST) & 1) ^ 1);
-            const uint32_t c0 = rs + (uint32_t)s * SE;
-            const int cnt = (int)min((uint32_t)SE, re - c0);
-            if (lane == 0) mbar_arrive_expect_tx(&sm.full[buf], (uint32_t)cnt * (64u + 4u * D));
-            __syncwarp();
-            for (int j = (int)lane; j < cnt; j += 32) {
-                const uint32_t slot = __ldg(&sorted_rec[c0 + j]);
-                bulk_g2s(&sm.rec[buf][j][0], rec + slot, 64u, &sm.full[buf]);
-                if (D > 0) {
-                    const uint32_t gid = __ldg(&rec[slot].gid);
-                    bulk_g2s(&sm.feat[buf][j][0], feat + (int64_t)gid * D, 4u * D, &sm.full[buf]);
+        uint32_t s = 0;
+        for (uint32_t tile = blockIdx.x;; tile += gridDim.x) {
+            const bool end = tile >= n_tiles;
+            uint32_t rs = 0, re = 0;
+            int view = 0;
+            if (!end) {
+                rs = __ldg(&ranges[2 * tile]);
+                re = __ldg(&ranges[2 * tile + 1]);
+                view = find_view_by_tile(views, n_views, tile);
+            }
+            const uint32_t nst = end ? 1u : max(1u, (re - rs + SE - 1) / SE);
+            for (uint32_t k = 0; k < nst; ++k, ++s) {
+                const uint32_t buf = s % NST;
+                if (s >= NST) mbar_wait(&sm.empty[buf], ((s / NST) & 1u) ^ 1u);
+                const uint32_t c0 = rs + k * SE;
+                const int cnt = end ? 0 : (int)min((uint32_t)SE, re - c0);
+                for (int j = (int)lane; j < cnt; j += 32) {
+                    const uint32_t slot = __ldg(&sorted_rec[c0 + j]);
+                    const uint32_t gid = D > 0 ? (sorted_gid ? __ldg(&sorted_gid[c0 + j]) : __ldg(&rec[slot].gid)) : 0u;
+                    const float4* src = reinterpret_cast<const float4*>(rec + slot);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) cp_async16(&sm.rec[buf][j][q], src + q);
+                    if constexpr (D > 0) {
+                        const float4* fs = reinterpret_cast<const float4*>(feat + (int64_t)gid * D);
+#pragma unroll
+                        for (int q = 0; q < D / 4; ++q) cp_async16(&sm.feat[buf][j][q * 4], fs + q);
+                    }
+                }
+                cp_async_mbar_arrive(&sm.full[buf]);
+                if (lane == 0) {
+                    StageMeta m;
+                    m.tile = tile; m.c0 = c0; m.cnt = cnt; m.view = view;
+                    m.flags = (k == 0 ? ST_FIRST : 0u) | (k == nst - 1 ? ST_LAST : 0u) | (end ? ST_END : 0u);
+                    m.pad0 = m.pad1 = m.pad2 = 0;
+                    sm.meta[buf] = m;
+                    mbar_arrive(&sm.full[buf]);
                 }
             }
+            if (end) break;
         }
-        // drain: the CTA must not retire while bulk copies into its smem are in flight
-        for (int s = (nstage > NST ? nstage - NST : 0); s < nstage; ++s)
-            mbar_wait(&sm.full[s % NST], (s / NST) & 1);
+        // drain: the CTA must not retire while copies into its smem are in flight
+        for (uint32_t q = (s > NST ? s - NST : 0u); q < s; ++q) mbar_wait(&sm.full[q % NST], (q / NST) & 1u);
         return;
     }
 
     // ---------------------------------------------------------------- consumers
-    const gs_view& V = views[sm.view];
-    const int W = V.width, H = V.height;
-    const int TX = (W + GS_TILE - 1) / GS_TILE;
-    const uint32_t lt = tile - V.tile_offset;
-    const int tx = (int)(lt % (uint32_t)TX), ty = (int)(lt / (uint32_t)TX);
-    const int sx = tx * 16 + (int)(warp & 1u) * 8, sy = ty * 16 + (int)(warp >> 1) * 4;
-    const int px = sx + (int)(lane & 7u), py = sy + (int)(lane >> 3);
-    const bool inside = px < W && py < H;
-    const float pxf = (float)px, pyf = (float)py;
-    const float rx0 = (float)sx, rx1 = (float)(sx + 7), ry0 = (float)sy, ry1 = (float)(sy + 3);
-
-    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Dz = 0.f;
-    bool done = !inside;
-    bool warp_done = __all_sync(0xffffffffu, done);
-    constexpr int NT = D > 0 ? D / 8 : 1;   // n-tiles of 8 features (D % 8 == 4 handled by a padded tile)
+    const int g = (int)(lane >> 2), t4 = (int)(lane & 3u);
     constexpr int NTP = D > 0 ? (D + 7) / 8 : 1;
     float acc[2][NTP][4];
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-        for (int n = 0; n < NTP; ++n) acc[m][n][0] = acc[m][n][1] = acc[m][n][2] = acc[m][n][3] = 0.f;
-    (void)NT;
     int nc = 0;   // compacted weights pending in this warp's buffer
-    const int g = (int)(lane >> 2), t4 = (int)(lane & 3u);
+    // per-tile state
+    const gs_view* V = nullptr;
+    int W = 0, H = 0, sx = 0, sy = 0, px = 0, py = 0;
+    bool inside = false, done = true, warp_done = true;
+    float pxf = 0.f, pyf = 0.f, rx0 = 0.f, rx1 = 0.f, ry0 = 0.f, ry1 = 0.f;
+    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Dz = 0.f;
 
     auto mma_flush = [&](int buf) {
         if constexpr (D > 0) {
-            // pad rows nc..7 with zero weights, point them at a valid entry
-            for (int k = nc; k < 8; ++k) {
+            for (int k = nc; k < 8; ++k) {      // pad with zero weights on a valid entry
                 sm.wbuf[warp][k][lane] = 0.f;
                 if (lane == 0) sm.ent[warp][k] = sm.ent[warp][0];
             }
@@ -198,18 +225,16 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             uint32_t ahi[2][4], alo[2][4];
 #pragma unroll
             for (int m = 0; m < 2; ++m) {
-                const float a0 = sm.wbuf[warp][t4][m * 16 + g], a1 = sm.wbuf[warp][t4][m * 16 + g + 8];
-                const float a2 = sm.wbuf[warp][t4 + 4][m * 16 + g], a3 = sm.wbuf[warp][t4 + 4][m * 16 + g + 8];
-                const float av[4] = {a0, a1, a2, a3};
+                const float av[4] = {sm.wbuf[warp][t4][m * 16 + g], sm.wbuf[warp][t4][m * 16 + g + 8],
+                                     sm.wbuf[warp][t4 + 4][m * 16 + g], sm.wbuf[warp][t4 + 4][m * 16 + g + 8]};
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     ahi[m][i] = to_tf32(av[i]);
                     alo[m][i] = to_tf32(av[i] - __uint_as_float(ahi[m][i]));
                 }
             }
-            const int e0 = sm.ent[warp][t4], e1 = sm.ent[warp][t4 + 4];
-            const float* f0 = &sm.feat[buf][e0][0];
-            const float* f1 = &sm.feat[buf][e1][0];
+            const float* f0 = &sm.feat[buf][sm.ent[warp][t4]][0];
+            const float* f1 = &sm.feat[buf][sm.ent[warp][t4 + 4]][0];
 #pragma unroll
             for (int n = 0; n < NTP; ++n) {
                 const int ch = n * 8 + g;
@@ -224,60 +249,92 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             nc = 0;
         }
     };
+    auto push_weight = [&](int buf, float wgt, int k) {
+        if constexpr (D > 0) {
+            sm.wbuf[warp][nc][lane] = wgt;
+            if (lane == 0) sm.ent[warp][nc] = k;
+            if (++nc == 8) {
+                __syncwarp();
+                mma_flush(buf);
+            }
+        }
+    };
 
-    for (int s = 0; s < nstage; ++s) {
-        const int buf = s % NST;
-        mbar_wait(&sm.full[buf], (s / NST) & 1);
-        if (!warp_done) {
-            const int cnt = (int)min((uint32_t)SE, re - (rs + (uint32_t)s * SE));
+    for (uint32_t s = 0;; ++s) {
+        const int buf = (int)(s % NST);
+        mbar_wait(&sm.full[buf], (s / NST) & 1u);
+        const StageMeta m = sm.meta[buf];
+        if (m.flags & ST_END) break;
+        if (m.flags & ST_FIRST) {
+            V = &views[m.view];
+            W = V->width;
+            H = V->height;
+            const int TX = (W + GS_TILE - 1) / GS_TILE;
+            const uint32_t lt = m.tile - V->tile_offset;
+            const int tx = (int)(lt % (uint32_t)TX), ty = (int)(lt / (uint32_t)TX);
+            sx = tx * 16 + (int)(warp & 1u) * 8;
+            sy = ty * 16 + (int)(warp >> 1) * 4;
+            px = sx + (int)(lane & 7u);
+            py = sy + (int)(lane >> 3);
+            inside = px < W && py < H;
+            pxf = (float)px; pyf = (float)py;
+            rx0 = (float)sx; rx1 = (float)(sx + 7); ry0 = (float)sy; ry1 = (float)(sy + 3);
+            T = 1.0f; C0 = C1 = C2 = Dz = 0.f;
+            done = !inside;
+            warp_done = __all_sync(0xffffffffu, done);
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int n = 0; n < NTP; ++n) acc[a][n][0] = acc[a][n][1] = acc[a][n][2] = acc[a][n][3] = 0.f;
+        }
+        if (!warp_done && m.cnt > 0) {
 #pragma unroll 1
-            for (int half = 0; half < SE / 32; ++half) {
+            for (int half = 0; half * 32 < m.cnt; ++half) {
                 const int j = half * 32 + (int)lane;
                 bool hit = false;
-                if (j < cnt) {
+                if (j < m.cnt) {
                     const float4 a = sm.rec[buf][j][0];   // u, v, ca, cb
                     const float4 b = sm.rec[buf][j][1];   // cc, o, q_cut, -
                     hit = ellipse_hits_rect(a.x, a.y, a.z, a.w, b.x, b.z, rx0, rx1, ry0, ry1);
                 }
                 uint32_t msk = __ballot_sync(0xffffffffu, hit);
                 while (msk) {
-                    const int k = half * 32 + __ffs(msk) - 1;
+                    // two entries per iteration: their alphas are independent (ILP 2);
+                    // the transmittance updates are applied in list order
+                    const int k1 = half * 32 + __ffs(msk) - 1;
                     msk &= msk - 1u;
-                    float wgt = 0.f;
-                    if (!done) {
-                        const float4 a = sm.rec[buf][k][0];
-                        const float4 b = sm.rec[buf][k][1];
-                        const float dx = __fsub_rn(a.x, pxf), dy = __fsub_rn(a.y, pyf);
-                        const float t1 = __fmul_rn(__fmul_rn(a.z, dx), dx);
-                        const float t2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
-                        const float t3 = __fmul_rn(__fmul_rn(a.w, dx), dy);
-                        const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), t3);
-                        if (!(power > 0.0f)) {          // oracle: skip iff power > 0
-                            const float alpha = fminf(P.alpha_max, __fmul_rn(b.y, __expf(power)));
-                            if (!(alpha < P.alpha_min)) {   // oracle: skip iff alpha < alpha_min
-                                const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-                                if (Tn < P.t_min) {
-                                    done = true;
-                                } else {
-                                    wgt = __fmul_rn(alpha, T);
-                                    const float4 c = sm.rec[buf][k][2];   // r, g, b, z
-                                    C0 = fmaf(wgt, c.x, C0);
-                                    C1 = fmaf(wgt, c.y, C1);
-                                    C2 = fmaf(wgt, c.z, C2);
-                                    Dz = fmaf(wgt, c.w, Dz);
-                                    T = Tn;
-                                }
-                            }
+                    const bool two = msk != 0u;
+                    const int k2 = two ? half * 32 + __ffs(msk) - 1 : k1;
+                    if (two) msk &= msk - 1u;
+                    const float a1 = entry_alpha(sm.rec[buf][k1][0], sm.rec[buf][k1][1], pxf, pyf, P);
+                    const float a2 = entry_alpha(sm.rec[buf][k2][0], sm.rec[buf][k2][1], pxf, pyf, P);
+                    float w1 = 0.f, w2 = 0.f;
+                    if (!done && a1 >= 0.f) {
+                        const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a1));
+                        if (Tn < P.t_min) {
+                            done = true;
+                        } else {
+                            w1 = __fmul_rn(a1, T);
+                            const float4 c = sm.rec[buf][k1][2];   // r, g, b, z
+                            C0 = fmaf(w1, c.x, C0); C1 = fmaf(w1, c.y, C1); C2 = fmaf(w1, c.z, C2);
+                            Dz = fmaf(w1, c.w, Dz);
+                            T = Tn;
                         }
                     }
-                    if constexpr (D > 0) {
-                        sm.wbuf[warp][nc][lane] = wgt;
-                        if (lane == 0) sm.ent[warp][nc] = k;
-                        if (++nc == 8) {
-                            __syncwarp();
-                            mma_flush(buf);
+                    if (two && !done && a2 >= 0.f) {
+                        const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a2));
+                        if (Tn < P.t_min) {
+                            done = true;
+                        } else {
+                            w2 = __fmul_rn(a2, T);
+                            const float4 c = sm.rec[buf][k2][2];
+                            C0 = fmaf(w2, c.x, C0); C1 = fmaf(w2, c.y, C1); C2 = fmaf(w2, c.z, C2);
+                            Dz = fmaf(w2, c.w, Dz);
+                            T = Tn;
                         }
                     }
+                    push_weight(buf, w1, k1);
+                    if (two) push_weight(buf, w2, k2);
                 }
                 warp_done = __all_sync(0xffffffffu, done);
                 if (warp_done) break;
@@ -287,39 +344,40 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 mma_flush(buf);
             }
         }
+        if (m.flags & ST_LAST) {
+            // -------------------------------------------------------- outputs
+            const int64_t HW = (int64_t)W * H;
+            const int64_t po = V->pix_offset;
+            if (inside) {
+                const int64_t loc = (int64_t)py * W + px;
+                out_rgb[3 * po + loc] = C0;
+                out_rgb[3 * po + HW + loc] = C1;
+                out_rgb[3 * po + 2 * HW + loc] = C2;
+                out_depth[po + loc] = Dz;
+                out_alpha[po + loc] = 1.0f - T;
+            }
+            if constexpr (D > 0) {
+                // accumulator (a, n, i): pixel (sx + g, sy + 2a + (i >> 1)), channel 8n + 2 t4 + (i & 1)
+                float* fo = out_feat + (int64_t)D * po;
+                const int fx = sx + g;
+#pragma unroll
+                for (int a = 0; a < 2; ++a)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int fy = sy + 2 * a + (i >> 1);
+                        if (fx < W && fy < H) {
+                            const int64_t loc = (int64_t)fy * W + fx;
+#pragma unroll
+                            for (int n = 0; n < NTP; ++n) {
+                                const int ch = n * 8 + 2 * t4 + (i & 1);
+                                if (ch < D) fo[(int64_t)ch * HW + loc] = acc[a][n][i];
+                            }
+                        }
+                    }
+            }
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[buf]);
-    }
-
-    // ---------------------------------------------------------------- outputs
-    const int64_t HW = (int64_t)W * H;
-    if (inside) {
-        const int64_t loc = (int64_t)py * W + px;
-        out_rgb[3 * V.pix_offset + loc] = C0;
-        out_rgb[3 * V.pix_offset + HW + loc] = C1;
-        out_rgb[3 * V.pix_offset + 2 * HW + loc] = C2;
-        out_depth[V.pix_offset + loc] = Dz;
-        out_alpha[V.pix_offset + loc] = 1.0f - T;
-    }
-    if (D > 0) {
-        // accumulator (m, n, i): pixel p = 16 m + g + 8 (i >> 1) -> (sx + g, sy + 2 m + (i >> 1)),
-        // channel n*8 + 2 t4 + (i & 1)
-        float* fo = out_feat + (int64_t)D * V.pix_offset;
-        const int fx = sx + g;
-#pragma unroll
-        for (int m = 0; m < 2; ++m)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int fy = sy + 2 * m + (i >> 1);
-                if (fx < W && fy < H) {
-                    const int64_t loc = (int64_t)fy * W + fx;
-#pragma unroll
-                    for (int n = 0; n < NTP; ++n) {
-                        const int ch = n * 8 + 2 * t4 + (i & 1);
-                        if (ch < D) fo[(int64_t)ch * HW + loc] = acc[m][n][i];
-                    }
-                }
-            }
     }
 }
 
@@ -327,14 +385,18 @@ template <int D>
 gs_status launch(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins, const gs_view* views_dev,
                  int n_views, int64_t T, const gs_params* P, gs_images* out, cudaStream_t s) {
     const int smem = (int)sizeof(RasterSmem<D>);
-    static bool attr = false;
-    if (!attr) {
+    static int blocks_per_sm = 0;
+    if (blocks_per_sm == 0) {
         cudaFuncSetAttribute(rasterize_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
+        cudaFuncSetAttribute(rasterize_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rasterize_kernel<D>, RT_THREADS, smem);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
-    rasterize_kernel<D><<<(unsigned)T, RT_THREADS, smem, s>>>(views_dev, n_views, proj->rec, bins->sorted_rec,
-                                                              bins->ranges, scene->feat, *P, out->rgb, out->depth,
-                                                              out->alpha, out->feat, proj->status);
+    const int64_t grid = std::min<int64_t>(T, (int64_t)num_sms() * blocks_per_sm);
+    if (grid <= 0) return GS_OK;
+    rasterize_kernel<D><<<(unsigned)grid, RT_THREADS, smem, s>>>(
+        views_dev, n_views, proj->rec, bins->sorted_rec, bins->sorted_gid, bins->ranges, (uint32_t)T, scene->feat,
+        *P, out->rgb, out->depth, out->alpha, out->feat, proj->status);
     return check_launch("rasterize_kernel");
 }
 
