@@ -34,8 +34,9 @@ namespace {
 constexpr int NCW = 8;                 // consumer warps
 constexpr int RT_THREADS = (NCW + 1) * 32;
 constexpr int SE = 64;                 // entries per stage
-constexpr int NST = 6;                 // ring stages
+constexpr int NST = 4;                 // ring stages
 constexpr int WB_STRIDE = 40;          // weight-buffer row stride (conflict-free A fragments)
+constexpr int WB_ROWS = 32;            // one ballot's entries
 constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -93,8 +94,8 @@ struct RasterSmem {
     static constexpr int FS = D > 0 ? D + 8 : 1;   // feature row stride (floats)
     float4 rec[NST][SE][4];                        // 64-byte records
     float feat[D > 0 ? NST : 1][D > 0 ? SE : 1][FS];
-    float wbuf[D > 0 ? NCW : 1][8][WB_STRIDE];     // per-warp compacted weights [k][pixel]
-    int ent[NCW][8];                               // per-warp compacted entry index
+    float wbuf[D > 0 ? NCW : 1][WB_ROWS][WB_STRIDE]; // per-warp compacted weights [k][pixel]
+    int ent[NCW][WB_ROWS];                           // per-warp compacted entry indices
     StageMeta meta[NST];
     uint64_t full[NST];
     uint64_t empty[NST];
@@ -207,7 +208,6 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     const int g = (int)(lane >> 2), t4 = (int)(lane & 3u);
     constexpr int NTP = D > 0 ? (D + 7) / 8 : 1;
     float acc[2][NTP][4];
-    int nc = 0;   // compacted weights pending in this warp's buffer
     // per-tile state
     const gs_view* V = nullptr;
     int W = 0, H = 0, sx = 0, sy = 0, px = 0, py = 0;
@@ -215,49 +215,48 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     float pxf = 0.f, pyf = 0.f, rx0 = 0.f, rx1 = 0.f, ry0 = 0.f, ry1 = 0.f;
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Dz = 0.f;
 
-    auto mma_flush = [&](int buf) {
+    // F[px][:] += W[px][0..nk) F_entries[0..nk)[:] on the tensor cores (nk multiple of 8)
+    auto mma_block = [&](int buf, int nk) {
         if constexpr (D > 0) {
-            for (int k = nc; k < 8; ++k) {      // pad with zero weights on a valid entry
-                sm.wbuf[warp][k][lane] = 0.f;
-                if (lane == 0) sm.ent[warp][k] = sm.ent[warp][0];
-            }
-            __syncwarp();
-            uint32_t ahi[2][4], alo[2][4];
-#pragma unroll
-            for (int m = 0; m < 2; ++m) {
-                const float av[4] = {sm.wbuf[warp][t4][m * 16 + g], sm.wbuf[warp][t4][m * 16 + g + 8],
-                                     sm.wbuf[warp][t4 + 4][m * 16 + g], sm.wbuf[warp][t4 + 4][m * 16 + g + 8]};
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    ahi[m][i] = to_tf32(av[i]);
-                    alo[m][i] = to_tf32(av[i] - __uint_as_float(ahi[m][i]));
-                }
-            }
-            const float* f0 = &sm.feat[buf][sm.ent[warp][t4]][0];
-            const float* f1 = &sm.feat[buf][sm.ent[warp][t4 + 4]][0];
-#pragma unroll
-            for (int n = 0; n < NTP; ++n) {
-                const int ch = n * 8 + g;
-                const uint32_t b0 = to_tf32(ch < D ? f0[ch] : 0.f), b1 = to_tf32(ch < D ? f1[ch] : 0.f);
+            for (int k0 = 0; k0 < nk; k0 += 8) {
+                uint32_t ahi[2][4], alo[2][4];
 #pragma unroll
                 for (int m = 0; m < 2; ++m) {
-                    mma_tf32(acc[m][n], ahi[m], b0, b1);
-                    mma_tf32(acc[m][n], alo[m], b0, b1);
+                    const float av[4] = {sm.wbuf[warp][k0 + t4][m * 16 + g], sm.wbuf[warp][k0 + t4][m * 16 + g + 8],
+                                         sm.wbuf[warp][k0 + t4 + 4][m * 16 + g],
+                                         sm.wbuf[warp][k0 + t4 + 4][m * 16 + g + 8]};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        ahi[m][i] = to_tf32(av[i]);
+                        alo[m][i] = to_tf32(av[i] - __uint_as_float(ahi[m][i]));
+                    }
+                }
+                const float* f0 = &sm.feat[buf][sm.ent[warp][k0 + t4]][0];
+                const float* f1 = &sm.feat[buf][sm.ent[warp][k0 + t4 + 4]][0];
+#pragma unroll
+                for (int n = 0; n < NTP; ++n) {
+                    const int ch = n * 8 + g;
+                    const uint32_t b0 = to_tf32(ch < D ? f0[ch] : 0.f), b1 = to_tf32(ch < D ? f1[ch] : 0.f);
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) {
+                        mma_tf32(acc[m][n], ahi[m], b0, b1);
+                        mma_tf32(acc[m][n], alo[m], b0, b1);
+                    }
                 }
             }
-            __syncwarp();
-            nc = 0;
         }
     };
-    auto push_weight = [&](int buf, float wgt, int k) {
-        if constexpr (D > 0) {
-            sm.wbuf[warp][nc][lane] = wgt;
-            if (lane == 0) sm.ent[warp][nc] = k;
-            if (++nc == 8) {
-                __syncwarp();
-                mma_flush(buf);
-            }
-        }
+    // apply one evaluated entry to this lane's pixel (branch-free; oracle order)
+    auto blend = [&](float a, const float4& c) -> float {
+        const bool ok = (a >= 0.0f) && !done;
+        const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
+        const bool stop = ok && (Tn < P.t_min);
+        const bool bl = ok && !stop;
+        const float wgt = bl ? __fmul_rn(a, T) : 0.0f;
+        C0 = fmaf(wgt, c.x, C0); C1 = fmaf(wgt, c.y, C1); C2 = fmaf(wgt, c.z, C2); Dz = fmaf(wgt, c.w, Dz);
+        T = bl ? Tn : T;
+        done = done || stop;
+        return wgt;
     };
 
     for (uint32_t s = 0;; ++s) {
@@ -297,51 +296,37 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     const float4 b = sm.rec[buf][j][1];   // cc, o, q_cut, -
                     hit = ellipse_hits_rect(a.x, a.y, a.z, a.w, b.x, b.z, rx0, rx1, ry0, ry1);
                 }
-                uint32_t msk = __ballot_sync(0xffffffffu, hit);
-                while (msk) {
-                    // two entries per iteration: their alphas are independent (ILP 2);
-                    // the transmittance updates are applied in list order
-                    const int k1 = half * 32 + __ffs(msk) - 1;
-                    msk &= msk - 1u;
-                    const bool two = msk != 0u;
-                    const int k2 = two ? half * 32 + __ffs(msk) - 1 : k1;
-                    if (two) msk &= msk - 1u;
+                const uint32_t msk = __ballot_sync(0xffffffffu, hit);
+                const int n = __popc(msk);
+                if (n == 0) continue;
+                if (hit) sm.ent[warp][__popc(msk & ((1u << lane) - 1u))] = j;   // compacted list, in order
+                __syncwarp();
+#pragma unroll 1
+                for (int i = 0; i < n; i += 2) {
+                    // two entries per iteration: independent alphas (ILP 2), transmittance in list order
+                    const bool two = i + 1 < n;
+                    const int k1 = sm.ent[warp][i];
+                    const int k2 = two ? sm.ent[warp][i + 1] : k1;
                     const float a1 = entry_alpha(sm.rec[buf][k1][0], sm.rec[buf][k1][1], pxf, pyf, P);
-                    const float a2 = entry_alpha(sm.rec[buf][k2][0], sm.rec[buf][k2][1], pxf, pyf, P);
-                    float w1 = 0.f, w2 = 0.f;
-                    if (!done && a1 >= 0.f) {
-                        const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a1));
-                        if (Tn < P.t_min) {
-                            done = true;
-                        } else {
-                            w1 = __fmul_rn(a1, T);
-                            const float4 c = sm.rec[buf][k1][2];   // r, g, b, z
-                            C0 = fmaf(w1, c.x, C0); C1 = fmaf(w1, c.y, C1); C2 = fmaf(w1, c.z, C2);
-                            Dz = fmaf(w1, c.w, Dz);
-                            T = Tn;
-                        }
+                    float a2 = entry_alpha(sm.rec[buf][k2][0], sm.rec[buf][k2][1], pxf, pyf, P);
+                    if (!two) a2 = -1.0f;
+                    const float w1 = blend(a1, sm.rec[buf][k1][2]);
+                    const float w2 = blend(a2, sm.rec[buf][k2][2]);
+                    if constexpr (D > 0) {
+                        sm.wbuf[warp][i][lane] = w1;
+                        sm.wbuf[warp][i + 1][lane] = w2;
                     }
-                    if (two && !done && a2 >= 0.f) {
-                        const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a2));
-                        if (Tn < P.t_min) {
-                            done = true;
-                        } else {
-                            w2 = __fmul_rn(a2, T);
-                            const float4 c = sm.rec[buf][k2][2];
-                            C0 = fmaf(w2, c.x, C0); C1 = fmaf(w2, c.y, C1); C2 = fmaf(w2, c.z, C2);
-                            Dz = fmaf(w2, c.w, Dz);
-                            T = Tn;
-                        }
-                    }
-                    push_weight(buf, w1, k1);
-                    if (two) push_weight(buf, w2, k2);
                 }
+                if constexpr (D > 0) {
+                    const int nk = (n + 7) & ~7;
+                    for (int r = (n + 1) & ~1; r < nk; ++r) sm.wbuf[warp][r][lane] = 0.f;   // zero padding
+                    if (lane < (uint32_t)(nk - n)) sm.ent[warp][n + lane] = sm.ent[warp][0];
+                    __syncwarp();
+                    mma_block(buf, nk);
+                }
+                __syncwarp();
                 warp_done = __all_sync(0xffffffffu, done);
                 if (warp_done) break;
-            }
-            if (D > 0 && nc > 0) {
-                __syncwarp();
-                mma_flush(buf);
             }
         }
         if (m.flags & ST_LAST) {
