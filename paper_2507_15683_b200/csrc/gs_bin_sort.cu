@@ -8,10 +8,13 @@
 // of a per-tile histogram, so the sort is only needed inside each tile:
 //   1. count    : per record, atomic histogram over the tiles of its rectangle
 //   2. scan     : exclusive scan -> ranges [start, end) and scatter cursors
-//   3. scatter  : per record, (depth_bits << 32 | gid, record slot) into its
-//                 tiles' buckets (order inside a bucket is arbitrary)
-//   4. tile sort: one WARP per tile sorts up to 512 pairs in registers
-//                 (bitonic network over shuffles); longer tiles go to a
+//   3. scatter  : per record, {depth_bits, record slot, gid} into its tiles'
+//                 buckets (order inside a bucket is arbitrary)
+//   4. tile sort: one WARP per tile sorts up to 1024 pairs in registers
+//                 (bitonic network, keys held transposed so most steps are
+//                 in-register; key = depth_bits << 32 | bucket index, so the
+//                 payload rides in the key); a tile with a depth tie is
+//                 re-sorted on (depth_bits, gid).  Longer tiles go to a
 //                 persistent CTA pass: shared-memory bitonic up to 8192, then
 //                 merge-path merges in global memory for the rare longer lists
 //                 (coarse pyramid levels).
@@ -27,8 +30,8 @@ namespace {
 constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_PER_THREAD = 4;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_PER_THREAD;
-constexpr int WARP_SORT_MAX = 512;      // 16 keys per lane
-constexpr int SMEM_SORT_MAX = 8192;     // 96 KB of shared memory
+constexpr int WARP_SORT_MAX = 1024;     // 32 keys per lane
+constexpr int SMEM_SORT_MAX = 8192;     // 64 KB of shared memory
 constexpr int BIG_THREADS = 512;
 constexpr uint64_t PAD_KEY = ~0ull;
 
@@ -38,10 +41,9 @@ struct BinWs {
     unsigned long long* block_sums;
     uint32_t* big_count;
     uint32_t* big_list;
-    uint64_t* keys;
-    uint32_t* vals;
-    uint64_t* keys2;
-    uint32_t* vals2;
+    uint4* bucket;
+    uint64_t* ka;
+    uint64_t* kb;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -55,17 +57,16 @@ BinWs carve(void* ws, int64_t cap, int64_t T) {
     w.block_sums = reinterpret_cast<unsigned long long*>(p); p += align256(sizeof(unsigned long long) * nb);
     w.big_count = reinterpret_cast<uint32_t*>(p); p += 256;
     w.big_list = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * T);
-    w.keys = reinterpret_cast<uint64_t*>(p); p += align256(sizeof(uint64_t) * cap);
-    w.vals = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * cap);
-    w.keys2 = reinterpret_cast<uint64_t*>(p); p += align256(sizeof(uint64_t) * cap);
-    w.vals2 = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * cap);
+    w.bucket = reinterpret_cast<uint4*>(p); p += align256(sizeof(uint4) * cap);
+    w.ka = reinterpret_cast<uint64_t*>(p); p += align256(sizeof(uint64_t) * cap);
+    w.kb = reinterpret_cast<uint64_t*>(p); p += align256(sizeof(uint64_t) * cap);
     return w;
 }
 
 size_t ws_bytes(int64_t cap, int64_t T) {
     const int64_t nb = (T + SCAN_TILE - 1) / SCAN_TILE + 1;
     return align256(sizeof(uint32_t) * T) * 2 + align256(sizeof(unsigned long long) * nb) + 256 +
-           align256(sizeof(uint32_t) * T) + (align256(sizeof(uint64_t) * cap) + align256(sizeof(uint32_t) * cap)) * 2;
+           align256(sizeof(uint32_t) * T) + align256(sizeof(uint4) * cap) + 2 * align256(sizeof(uint64_t) * cap);
 }
 
 // ---------------------------------------------------------------- 1. count
@@ -174,10 +175,10 @@ scan_down_kernel(const uint32_t* __restrict__ counts, int64_t T, const unsigned 
 }
 
 // ---------------------------------------------------------------- 3. scatter
+// bucket entry: {depth_bits, record slot, gid, 0}; order inside a bucket is arbitrary
 __global__ void scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
                                const gs_view* __restrict__ views, uint32_t* __restrict__ cursor,
-                               uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                               const uint32_t* __restrict__ status) {
+                               uint4* __restrict__ bucket, const uint32_t* __restrict__ status) {
     if (*status) return;
     const int v = blockIdx.y;
     const uint32_t nv = min((uint64_t)n_rec[v], (uint64_t)cap);
@@ -187,90 +188,135 @@ __global__ void scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, c
         const uint32_t slot = (uint32_t)((int64_t)v * cap + k);
         const uint4* q4 = reinterpret_cast<const uint4*>(rec + slot);
         const uint4 q2 = __ldg(q4 + 2), q3 = __ldg(q4 + 3);
-        const uint64_t key = ((uint64_t)q2.w << 32) | q3.x;   // (bits(z), gid)
+        const uint4 ent = make_uint4(q2.w, slot, q3.x, 0u);   // bits(z), slot, gid
         const uint32_t x0 = q3.z & 0xffffu, x1 = q3.z >> 16, y0 = q3.w & 0xffffu, y1 = q3.w >> 16;
-        for (uint32_t ty = y0; ty <= y1; ++ty)
-            for (uint32_t tx = x0; tx <= x1; ++tx) {
-                const uint32_t pos = atomicAdd(&cursor[toff + ty * TX + tx], 1u);
-                keys[pos] = key;
-                vals[pos] = slot;
+        const uint32_t nx = x1 - x0 + 1, npair = nx * (y1 - y0 + 1);
+        // batches of 4 independent atomics so their latencies overlap
+        for (uint32_t p0 = 0; p0 < npair; p0 += 4) {
+            uint32_t pos[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t p = p0 + q;
+                if (p < npair) {
+                    const uint32_t ty = y0 + p / nx, tx = x0 + p % nx;
+                    pos[q] = atomicAdd(&cursor[toff + ty * TX + tx], 1u);
+                }
             }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (p0 + q < npair) bucket[pos[q]] = ent;
+        }
     }
 }
 
 // ---------------------------------------------------------------- 4. tile sort
-__device__ __forceinline__ void cmp_swap(uint64_t& ka, uint32_t& va, uint64_t& kb, uint32_t& vb, bool up) {
-    if ((ka > kb) == up) {
-        uint64_t tk = ka; ka = kb; kb = tk;
-        uint32_t tv = va; va = vb; vb = tv;
-    }
-}
+// Sort key (fast path): (depth_bits << 32) | index in the bucket -- unique, and
+// it carries its own payload.  Equal depth_bits are then in bucket order, so a
+// tile with a depth tie is re-sorted on (depth_bits << 32) | gid with the
+// bucket index as payload (Q12: stable index tie-break = ascending gid).
 
-// Bitonic sort of N = 32*PER keys held as element e = j*32 + lane.
-template <int PER>
-__device__ __forceinline__ void warp_bitonic(uint64_t (&k)[PER], uint32_t (&v)[PER], uint32_t lane) {
-    constexpr int LOGN = 5 + (PER == 1 ? 0 : PER == 2 ? 1 : PER == 4 ? 2 : PER == 8 ? 3 : 4);
+// warp bitonic of 32*PER keys held transposed: element e = lane*PER + j
+template <int PER, bool PAY>
+__device__ __forceinline__ void warp_bitonic_t(uint64_t (&k)[PER], uint32_t (&v)[PER], uint32_t lane) {
+    constexpr int LP = PER == 1 ? 0 : PER == 2 ? 1 : PER == 4 ? 2 : PER == 8 ? 3 : PER == 16 ? 4 : 5;
+    constexpr int LOGN = 5 + LP;
 #pragma unroll
-    for (int s = 1; s <= LOGN; ++s) {           // merge blocks of size 2^s
+    for (int s = 1; s <= LOGN; ++s) {
 #pragma unroll
-        for (int d = s - 1; d >= 0; --d) {      // partner distance 2^d
-            if (d >= 5) {
-                const int jd = 1 << (d - 5);
+        for (int d = s - 1; d >= 0; --d) {
+            if (d < LP) {                         // partner in the same lane
+                const int jd = 1 << d;
 #pragma unroll
                 for (int j = 0; j < PER; ++j) {
                     if ((j & jd) == 0) {
-                        const uint32_t e = (uint32_t)j * 32u + lane;
+                        const uint32_t e = lane * PER + (uint32_t)j;
                         const bool up = ((e >> s) & 1u) == 0u;
-                        cmp_swap(k[j], v[j], k[j + jd], v[j + jd], up);
+                        if ((k[j] > k[j + jd]) == up) {
+                            const uint64_t t = k[j]; k[j] = k[j + jd]; k[j + jd] = t;
+                            if (PAY) { const uint32_t tv = v[j]; v[j] = v[j + jd]; v[j + jd] = tv; }
+                        }
                     }
                 }
-            } else {
-                const uint32_t ld = 1u << d;
+            } else {                              // partner lane = lane ^ 2^(d - LP)
+                const uint32_t ld = 1u << (d - LP);
+                const bool lower = (lane & ld) == 0u;
 #pragma unroll
                 for (int j = 0; j < PER; ++j) {
-                    const uint32_t e = (uint32_t)j * 32u + lane;
+                    const uint32_t e = lane * PER + (uint32_t)j;
                     const bool up = ((e >> s) & 1u) == 0u;
-                    const bool lower = (lane & ld) == 0u;
                     const uint64_t ok = __shfl_xor_sync(0xffffffffu, k[j], ld);
-                    const uint32_t ov = __shfl_xor_sync(0xffffffffu, v[j], ld);
-                    // lower element keeps min when ascending, max when descending
-                    const bool take_other = lower ? ((ok < k[j]) == up) : ((ok > k[j]) == up);
-                    if (take_other) { k[j] = ok; v[j] = ov; }
+                    uint32_t ov = 0;
+                    if (PAY) ov = __shfl_xor_sync(0xffffffffu, v[j], ld);
+                    const bool take = lower ? ((ok < k[j]) == up) : ((ok > k[j]) == up);
+                    if (take) { k[j] = ok; if (PAY) v[j] = ov; }
                 }
             }
         }
     }
 }
 
+// returns false (nothing written) when a depth tie needs the big path (PER == 32 only)
 template <int PER>
-__device__ __forceinline__ void warp_sort_tile(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
-                                               uint32_t s, uint32_t len, uint32_t tile, uint32_t lane,
-                                               uint32_t* __restrict__ out, uint32_t* __restrict__ ogid,
-                                               uint64_t* __restrict__ dbg) {
+__device__ __forceinline__ bool warp_sort_tile(const uint4* __restrict__ bucket, uint32_t s, uint32_t len,
+                                               uint32_t tile, uint32_t lane, uint32_t* __restrict__ out,
+                                               uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg) {
     uint64_t k[PER];
     uint32_t v[PER];
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-        const uint32_t e = (uint32_t)j * 32u + lane;
-        k[j] = e < len ? keys[s + e] : PAD_KEY;
-        v[j] = e < len ? vals[s + e] : 0u;
+        const uint32_t e = lane * PER + (uint32_t)j;
+        k[j] = e < len ? (((uint64_t)__ldg(&bucket[s + e].x) << 32) | e) : PAD_KEY;
     }
-    warp_bitonic<PER>(k, v, lane);
+    warp_bitonic_t<PER, false>(k, v, lane);
+    // depth tie between neighbours?  (element e+1 is k[j+1] or k[0] of lane+1)
+    const uint64_t nxt0 = __shfl_down_sync(0xffffffffu, k[0], 1);
+    bool tie = false;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-        const uint32_t e = (uint32_t)j * 32u + lane;
+        const uint64_t nb = j + 1 < PER ? k[j + 1] : nxt0;
+        const uint32_t e = lane * PER + (uint32_t)j;
+        if (e + 1 < len && (k[j] >> 32) == (nb >> 32)) tie = true;
+    }
+    if (__any_sync(0xffffffffu, tie)) {
+        if constexpr (PER >= 32) {
+            return false;   // registers: let the CTA path order the ties
+        } else {
+        // rare: re-sort on (depth_bits, gid) carrying the bucket index
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const uint32_t e = lane * PER + (uint32_t)j;
+            if (e < len) {
+                const uint4 b = bucket[s + e];
+                k[j] = ((uint64_t)b.x << 32) | b.z;
+                v[j] = e;
+            } else {
+                k[j] = PAD_KEY;
+                v[j] = 0u;
+            }
+        }
+        warp_bitonic_t<PER, true>(k, v, lane);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) v[j] = (uint32_t)k[j];
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const uint32_t e = lane * PER + (uint32_t)j;
         if (e < len) {
-            out[s + e] = v[j];
-            if (ogid) ogid[s + e] = (uint32_t)k[j];
-            if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | (k[j] >> 32);
+            const uint4 b = bucket[s + v[j]];   // L1-resident: this warp just read the bucket
+            out[s + e] = b.y;
+            if (ogid) ogid[s + e] = b.z;
+            if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | b.x;
         }
     }
+    return true;
 }
 
-__global__ void __launch_bounds__(256)
-warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint64_t* __restrict__ keys,
-                 const uint32_t* __restrict__ vals, uint32_t* __restrict__ out, uint32_t* __restrict__ ogid,
-                 uint64_t* __restrict__ dbg, uint32_t* __restrict__ big_count, uint32_t* __restrict__ big_list,
+__global__ void __launch_bounds__(256, 1)
+warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint4* __restrict__ bucket,
+                 uint32_t* __restrict__ out, uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg,
+                 uint32_t* __restrict__ big_count, uint32_t* __restrict__ big_list,
                  const uint32_t* __restrict__ status) {
     if (*status) return;
     const uint32_t lane = threadIdx.x & 31u;
@@ -278,104 +324,123 @@ warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint64_t*
     if (tile >= T) return;
     const uint32_t s = ranges[2 * tile], e = ranges[2 * tile + 1], len = e - s;
     if (len == 0) return;
-    if (len <= 32) warp_sort_tile<1>(keys, vals, s, len, (uint32_t)tile, lane, out, ogid, dbg);
-    else if (len <= 64) warp_sort_tile<2>(keys, vals, s, len, (uint32_t)tile, lane, out, ogid, dbg);
-    else if (len <= 128) warp_sort_tile<4>(keys, vals, s, len, (uint32_t)tile, lane, out, ogid, dbg);
-    else if (len <= 256) warp_sort_tile<8>(keys, vals, s, len, (uint32_t)tile, lane, out, ogid, dbg);
-    else if (len <= WARP_SORT_MAX) warp_sort_tile<16>(keys, vals, s, len, (uint32_t)tile, lane, out, ogid, dbg);
-    else if (lane == 0) big_list[atomicAdd(big_count, 1u)] = (uint32_t)tile;
+    if (len == 1) {
+        if (lane == 0) {
+            const uint4 b = bucket[s];
+            out[s] = b.y;
+            if (ogid) ogid[s] = b.z;
+            if (dbg) dbg[s] = ((uint64_t)tile << 32) | b.x;
+        }
+    } else if (len <= 32) warp_sort_tile<1>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
+    else if (len <= 64) warp_sort_tile<2>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
+    else if (len <= 128) warp_sort_tile<4>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
+    else if (len <= 256) warp_sort_tile<8>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
+    else if (len <= 512) warp_sort_tile<16>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
+    else if (len > WARP_SORT_MAX || !warp_sort_tile<32>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg)) {
+        if (lane == 0) big_list[atomicAdd(big_count, 1u)] = (uint32_t)tile;
+    }
 }
 
-// CTA-wide bitonic sort of n (power of two) keys in shared memory
-__device__ void smem_bitonic(uint64_t* sk, uint32_t* sv, uint32_t n) {
+// CTA-wide bitonic sort of n (power of two) 64-bit keys in shared memory
+__device__ void smem_bitonic(uint64_t* sk, uint32_t n) {
     for (uint32_t size = 2; size <= n; size <<= 1) {
         for (uint32_t d = size >> 1; d > 0; d >>= 1) {
             for (uint32_t t = threadIdx.x; t < n / 2; t += blockDim.x) {
                 const uint32_t i = 2 * t - (t & (d - 1));   // lower index of the pair
                 const uint32_t j = i + d;
                 const bool up = (i & size) == 0;
-                uint64_t a = sk[i], b = sk[j];
-                if ((a > b) == up) {
-                    sk[i] = b; sk[j] = a;
-                    uint32_t tv = sv[i]; sv[i] = sv[j]; sv[j] = tv;
-                }
+                const uint64_t a = sk[i], b = sk[j];
+                if ((a > b) == up) { sk[i] = b; sk[j] = a; }
             }
             __syncthreads();
         }
     }
 }
 
-// merge sorted runs A = src[a0, a0+na), B = src[a0+na, a0+na+nb) into dst[a0 ...] (keys unique)
-__device__ void cta_merge(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, uint64_t* __restrict__ dk,
-                          uint32_t* __restrict__ dv, uint32_t a0, uint32_t na, uint32_t nb) {
+// merge sorted runs A = src[a0, a0+na), B = src[a0+na, a0+na+nb) into dst[a0 ...] (unique keys)
+__device__ void cta_merge(const uint64_t* __restrict__ sk, uint64_t* __restrict__ dk, uint32_t a0, uint32_t na,
+                          uint32_t nb) {
     const uint32_t total = na + nb;
     const uint32_t per = (total + blockDim.x - 1) / blockDim.x;
     const uint32_t lo = min(total, threadIdx.x * per), hi = min(total, lo + per);
     if (lo >= hi) return;
     const uint64_t* A = sk + a0;
     const uint64_t* B = sk + a0 + na;
-    // merge path: find i (from A) with i + j = lo
     uint32_t ilo = lo > nb ? lo - nb : 0u, ihi = min(lo, na);
-    while (ilo < ihi) {
+    while (ilo < ihi) {   // merge path: i elements of A among the first lo outputs
         const uint32_t i = (ilo + ihi) >> 1;
-        const uint32_t j = lo - i;
-        if (A[i] < B[j - 1]) ilo = i + 1; else ihi = i;
+        if (A[i] < B[lo - i - 1]) ilo = i + 1; else ihi = i;
     }
     uint32_t i = ilo, j = lo - ilo;
     for (uint32_t o = lo; o < hi; ++o) {
         const bool takeA = j >= nb || (i < na && A[i] < B[j]);
-        if (takeA) { dk[a0 + o] = A[i]; dv[a0 + o] = sv[a0 + i]; ++i; }
-        else { dk[a0 + o] = B[j]; dv[a0 + o] = sv[a0 + na + j]; ++j; }
+        dk[a0 + o] = takeA ? A[i++] : B[j++];
     }
 }
 
+// Long lists (> 1024 pairs; coarse pyramid levels): one CTA per tile, runs of
+// up to 8192 keys sorted in shared memory, then merge-path merges in global
+// memory.  Keys are (depth_bits << 32 | bucket index); depth ties are fixed by a
+// serial insertion pass on (depth_bits, gid) (ties are rare).
 __global__ void __launch_bounds__(BIG_THREADS)
-big_sort_kernel(const uint32_t* __restrict__ ranges, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                uint64_t* __restrict__ keys2, uint32_t* __restrict__ vals2, uint32_t* __restrict__ out,
-                uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg, const uint32_t* __restrict__ big_count,
+big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ bucket, uint64_t* __restrict__ ka,
+                uint64_t* __restrict__ kb, uint32_t* __restrict__ out, uint32_t* __restrict__ ogid,
+                uint64_t* __restrict__ dbg, const uint32_t* __restrict__ big_count,
                 const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ status) {
     if (*status) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
-    uint32_t* sv = reinterpret_cast<uint32_t*>(smem_raw + SMEM_SORT_MAX * sizeof(uint64_t));
+    __shared__ int tie;
     const uint32_t nbig = *big_count;
     for (uint32_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
         const uint32_t tile = big_list[bi];
         const uint32_t s = ranges[2 * tile], len = ranges[2 * tile + 1] - s;
-        // phase 1: sort runs of up to SMEM_SORT_MAX in shared memory
         for (uint32_t r0 = 0; r0 < len; r0 += SMEM_SORT_MAX) {
             const uint32_t rl = min((uint32_t)SMEM_SORT_MAX, len - r0);
             uint32_t n2 = 1;
             while (n2 < rl) n2 <<= 1;
-            for (uint32_t e = threadIdx.x; e < n2; e += blockDim.x) {
-                sk[e] = e < rl ? keys[s + r0 + e] : PAD_KEY;
-                sv[e] = e < rl ? vals[s + r0 + e] : 0u;
-            }
+            for (uint32_t e = threadIdx.x; e < n2; e += blockDim.x)
+                sk[e] = e < rl ? (((uint64_t)bucket[s + r0 + e].x << 32) | (r0 + e)) : PAD_KEY;
             __syncthreads();
-            smem_bitonic(sk, sv, n2);
-            for (uint32_t e = threadIdx.x; e < rl; e += blockDim.x) {
-                keys[s + r0 + e] = sk[e];
-                vals[s + r0 + e] = sv[e];
-            }
+            smem_bitonic(sk, n2);
+            for (uint32_t e = threadIdx.x; e < rl; e += blockDim.x) ka[s + r0 + e] = sk[e];
             __syncthreads();
         }
-        // phase 2: merge passes (ping-pong keys <-> keys2)
-        uint64_t* ck = keys + s; uint32_t* cv = vals + s;
-        uint64_t* nk = keys2 + s; uint32_t* nv = vals2 + s;
+        uint64_t* ck = ka + s;
+        uint64_t* nk = kb + s;
         for (uint32_t width = SMEM_SORT_MAX; width < len; width <<= 1) {
             for (uint32_t a0 = 0; a0 < len; a0 += 2 * width) {
                 const uint32_t na = min(width, len - a0);
                 const uint32_t nb = a0 + na < len ? min(width, len - a0 - na) : 0u;
-                cta_merge(ck, cv, nk, nv, a0, na, nb);
+                cta_merge(ck, nk, a0, na, nb);
             }
             __syncthreads();
-            uint64_t* tk = ck; ck = nk; nk = tk;
-            uint32_t* tv = cv; cv = nv; nv = tv;
+            uint64_t* t = ck; ck = nk; nk = t;
         }
+        if (threadIdx.x == 0) tie = 0;
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e + 1 < len; e += blockDim.x)
+            if ((ck[e] >> 32) == (ck[e + 1] >> 32)) tie = 1;
+        __syncthreads();
+        if (tie && threadIdx.x == 0) {
+            // insertion pass over equal-depth runs, ordering them by gid
+            for (uint32_t e = 1; e < len; ++e) {
+                const uint64_t key = ck[e];
+                const uint32_t gk = bucket[s + (uint32_t)key].z;
+                uint32_t f = e;
+                while (f > 0 && (ck[f - 1] >> 32) == (key >> 32) && bucket[s + (uint32_t)ck[f - 1]].z > gk) {
+                    ck[f] = ck[f - 1];
+                    --f;
+                }
+                ck[f] = key;
+            }
+        }
+        __syncthreads();
         for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) {
-            out[s + e] = cv[e];
-            if (ogid) ogid[s + e] = (uint32_t)ck[e];
-            if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | (ck[e] >> 32);
+            const uint4 b = bucket[s + (uint32_t)ck[e]];
+            out[s + e] = b.y;
+            if (ogid) ogid[s + e] = b.z;
+            if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | b.x;
         }
         __syncthreads();
     }
@@ -421,20 +486,20 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     scan_blocks_kernel<<<1, SCAN_THREADS, 0, s>>>(w.block_sums, nb, out->n_pairs, out->pair_capacity, proj->status);
     scan_down_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(w.counts, T, w.block_sums, out->ranges, w.cursor);
     if ((st = check_launch("scan kernels")) != GS_OK) return st;
-    scatter_kernel<<<rgrid, 256, 0, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.cursor, w.keys, w.vals,
-                                         proj->status);
+    scatter_kernel<<<rgrid, 256, 0, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.cursor, w.bucket, proj->status);
     if ((st = check_launch("scatter_kernel")) != GS_OK) return st;
-    warp_sort_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(out->ranges, T, w.keys, w.vals, out->sorted_rec,
-                                                             out->sorted_gid, out->sorted_key, w.big_count, w.big_list, proj->status);
+    warp_sort_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(out->ranges, T, w.bucket, out->sorted_rec,
+                                                             out->sorted_gid, out->sorted_key, w.big_count,
+                                                             w.big_list, proj->status);
     if ((st = check_launch("warp_sort_kernel")) != GS_OK) return st;
     static bool attr_set = false;
-    const int smem = SMEM_SORT_MAX * (sizeof(uint64_t) + sizeof(uint32_t));
+    const int smem = SMEM_SORT_MAX * (int)sizeof(uint64_t);
     if (!attr_set) {
         cudaFuncSetAttribute(big_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
-    big_sort_kernel<<<num_sms(), BIG_THREADS, smem, s>>>(out->ranges, w.keys, w.vals, w.keys2, w.vals2,
-                                                         out->sorted_rec, out->sorted_gid, out->sorted_key, w.big_count, w.big_list,
+    big_sort_kernel<<<num_sms(), BIG_THREADS, smem, s>>>(out->ranges, w.bucket, w.ka, w.kb, out->sorted_rec,
+                                                         out->sorted_gid, out->sorted_key, w.big_count, w.big_list,
                                                          proj->status);
     return check_launch("big_sort_kernel");
 }

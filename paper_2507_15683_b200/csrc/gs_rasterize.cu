@@ -65,11 +65,9 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
-    return r;
-}
+// round a finite fp32 to the nearest tf32 (ties away from zero) with integer ops; the
+// tensor core reads only the top 19 bits of a .tf32 operand
+__device__ __forceinline__ uint32_t to_tf32(float x) { return (__float_as_uint(x) + 0x1000u) & 0xffffe000u; }
 __device__ __forceinline__ float ex2_ftz(float x) {
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(r) : "f"(x));
@@ -175,16 +173,27 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 if (s >= NST) mbar_wait(&sm.empty[buf], ((s / NST) & 1u) ^ 1u);
                 const uint32_t c0 = rs + k * SE;
                 const int cnt = end ? 0 : (int)min((uint32_t)SE, re - c0);
-                for (int j = (int)lane; j < cnt; j += 32) {
-                    const uint32_t slot = __ldg(&sorted_rec[c0 + j]);
-                    const uint32_t gid = D > 0 ? (sorted_gid ? __ldg(&sorted_gid[c0 + j]) : __ldg(&rec[slot].gid)) : 0u;
-                    const float4* src = reinterpret_cast<const float4*>(rec + slot);
+                // issue the (independent) index loads of both entries first, then the gathers
+                uint32_t slot[SE / 32], gid[SE / 32];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) cp_async16(&sm.rec[buf][j][q], src + q);
-                    if constexpr (D > 0) {
-                        const float4* fs = reinterpret_cast<const float4*>(feat + (int64_t)gid * D);
+                for (int q = 0; q < SE / 32; ++q) {
+                    const int j = q * 32 + (int)lane;
+                    slot[q] = j < cnt ? __ldg(&sorted_rec[c0 + j]) : 0u;
+                    gid[q] = (D > 0 && j < cnt && sorted_gid) ? __ldg(&sorted_gid[c0 + j]) : 0u;
+                }
 #pragma unroll
-                        for (int q = 0; q < D / 4; ++q) cp_async16(&sm.feat[buf][j][q * 4], fs + q);
+                for (int q = 0; q < SE / 32; ++q) {
+                    const int j = q * 32 + (int)lane;
+                    if (j < cnt) {
+                        const float4* src = reinterpret_cast<const float4*>(rec + slot[q]);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) cp_async16(&sm.rec[buf][j][e], src + e);
+                        if constexpr (D > 0) {
+                            const uint32_t gg = sorted_gid ? gid[q] : __ldg(&rec[slot[q]].gid);
+                            const float4* fs = reinterpret_cast<const float4*>(feat + (int64_t)gg * D);
+#pragma unroll
+                            for (int e = 0; e < D / 4; ++e) cp_async16(&sm.feat[buf][j][e * 4], fs + e);
+                        }
                     }
                 }
                 cp_async_mbar_arrive(&sm.full[buf]);
@@ -228,7 +237,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         ahi[m][i] = to_tf32(av[i]);
-                        alo[m][i] = to_tf32(av[i] - __uint_as_float(ahi[m][i]));
+                        alo[m][i] = __float_as_uint(av[i] - __uint_as_float(ahi[m][i]));   // exact remainder
                     }
                 }
                 const float* f0 = &sm.feat[buf][sm.ent[warp][k0 + t4]][0];
@@ -305,8 +314,9 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 for (int i = 0; i < n; i += 2) {
                     // two entries per iteration: independent alphas (ILP 2), transmittance in list order
                     const bool two = i + 1 < n;
-                    const int k1 = sm.ent[warp][i];
-                    const int k2 = two ? sm.ent[warp][i + 1] : k1;
+                    const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i]);   // i is even
+                    const int k1 = kk.x;
+                    const int k2 = two ? kk.y : k1;
                     const float a1 = entry_alpha(sm.rec[buf][k1][0], sm.rec[buf][k1][1], pxf, pyf, P);
                     float a2 = entry_alpha(sm.rec[buf][k2][0], sm.rec[buf][k2][1], pxf, pyf, P);
                     if (!two) a2 = -1.0f;
