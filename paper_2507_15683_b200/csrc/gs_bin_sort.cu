@@ -10,7 +10,7 @@
 //   2. scan     : exclusive scan -> ranges [start, end) and scatter cursors
 //   3. scatter  : per record, {depth_bits, record slot, gid} into its tiles'
 //                 buckets (order inside a bucket is arbitrary)
-//   4. tile sort: one WARP per tile sorts up to 1024 pairs in registers
+//   4. tile sort: one WARP per tile sorts up to 512 pairs in registers
 //                 (bitonic network, keys held transposed so most steps are
 //                 in-register; key = depth_bits << 32 | bucket index, so the
 //                 payload rides in the key); a tile with a depth tie is
@@ -30,7 +30,7 @@ namespace {
 constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_PER_THREAD = 4;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_PER_THREAD;
-constexpr int WARP_SORT_MAX = 1024;     // 32 keys per lane
+constexpr int WARP_SORT_MAX = 512;      // 16 keys per lane
 constexpr int SMEM_SORT_MAX = 8192;     // 64 KB of shared memory
 constexpr int BIG_THREADS = 512;
 constexpr uint64_t PAD_KEY = ~0ull;
@@ -313,7 +313,7 @@ __device__ __forceinline__ bool warp_sort_tile(const uint4* __restrict__ bucket,
     return true;
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256)
 warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint4* __restrict__ bucket,
                  uint32_t* __restrict__ out, uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg,
                  uint32_t* __restrict__ big_count, uint32_t* __restrict__ big_list,
@@ -335,10 +335,8 @@ warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint4* __
     else if (len <= 64) warp_sort_tile<2>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
     else if (len <= 128) warp_sort_tile<4>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
     else if (len <= 256) warp_sort_tile<8>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
-    else if (len <= 512) warp_sort_tile<16>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
-    else if (len > WARP_SORT_MAX || !warp_sort_tile<32>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg)) {
-        if (lane == 0) big_list[atomicAdd(big_count, 1u)] = (uint32_t)tile;
-    }
+    else if (len <= WARP_SORT_MAX) warp_sort_tile<16>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
+    else if (lane == 0) big_list[atomicAdd(big_count, 1u)] = (uint32_t)tile;
 }
 
 // CTA-wide bitonic sort of n (power of two) 64-bit keys in shared memory
