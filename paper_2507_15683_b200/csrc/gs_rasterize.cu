@@ -92,8 +92,8 @@ struct RasterSmem {
     static constexpr int FS = D > 0 ? D + 8 : 1;   // feature row stride (floats)
     float4 rec[NST][SE][4];                        // 64-byte records
     float feat[D > 0 ? NST : 1][D > 0 ? SE : 1][FS];
-    float wbuf[D > 0 ? NCW : 1][WB_ROWS][WB_STRIDE]; // per-warp compacted weights [k][pixel]
-    int ent[NCW][WB_ROWS];                           // per-warp compacted entry indices
+    alignas(16) float wbuf[D > 0 ? NCW : 1][WB_ROWS][WB_STRIDE]; // per-warp compacted weights [k][pixel]
+    alignas(16) int ent[NCW][WB_ROWS];               // per-warp compacted entry indices
     StageMeta meta[NST];
     uint64_t full[NST];
     uint64_t empty[NST];
