@@ -12,9 +12,9 @@
 //                 buckets (order inside a bucket is arbitrary)
 //   4. tile sort: one WARP per tile sorts up to 512 pairs in registers
 //                 (bitonic network, keys held transposed so most steps are
-//                 in-register; key = depth_bits << 32 | bucket index, so the
-//                 payload rides in the key); a tile with a depth tie is
-//                 re-sorted on (depth_bits, gid).  Longer tiles go to a
+//                 in-register; (depth - min depth | gid | bucket index) packed
+//                 in one 64-bit key when it fits, so the payload rides in the
+//                 key; else a 64-bit key + 32-bit payload).  Longer tiles go to a
 //                 persistent CTA pass: shared-memory bitonic up to 8192, then
 //                 merge-path merges in global memory for the rare longer lists
 //                 (coarse pyramid levels).
@@ -31,7 +31,7 @@ constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_PER_THREAD = 4;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_PER_THREAD;
 constexpr int WARP_SORT_MAX = 512;      // 16 keys per lane
-constexpr int SMEM_SORT_MAX = 8192;     // 64 KB of shared memory
+constexpr int SMEM_SORT_MAX = 8192;     // 96 KB of shared memory
 constexpr int BIG_THREADS = 512;
 constexpr uint64_t PAD_KEY = ~0ull;
 
@@ -43,7 +43,9 @@ struct BinWs {
     uint32_t* big_list;
     uint4* bucket;
     uint64_t* ka;
+    uint32_t* va;
     uint64_t* kb;
+    uint32_t* vb;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -59,14 +61,17 @@ BinWs carve(void* ws, int64_t cap, int64_t T) {
     w.big_list = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * T);
     w.bucket = reinterpret_cast<uint4*>(p); p += align256(sizeof(uint4) * cap);
     w.ka = reinterpret_cast<uint64_t*>(p); p += align256(sizeof(uint64_t) * cap);
+    w.va = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * cap);
     w.kb = reinterpret_cast<uint64_t*>(p); p += align256(sizeof(uint64_t) * cap);
+    w.vb = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * cap);
     return w;
 }
 
 size_t ws_bytes(int64_t cap, int64_t T) {
     const int64_t nb = (T + SCAN_TILE - 1) / SCAN_TILE + 1;
     return align256(sizeof(uint32_t) * T) * 2 + align256(sizeof(unsigned long long) * nb) + 256 +
-           align256(sizeof(uint32_t) * T) + align256(sizeof(uint4) * cap) + 2 * align256(sizeof(uint64_t) * cap);
+           align256(sizeof(uint32_t) * T) + align256(sizeof(uint4) * cap) +
+           2 * (align256(sizeof(uint64_t) * cap) + align256(sizeof(uint32_t) * cap));
 }
 
 // ---------------------------------------------------------------- 1. count
@@ -210,10 +215,12 @@ __global__ void scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, c
 }
 
 // ---------------------------------------------------------------- 4. tile sort
-// Sort key (fast path): (depth_bits << 32) | index in the bucket -- unique, and
-// it carries its own payload.  Equal depth_bits are then in bucket order, so a
-// tile with a depth tie is re-sorted on (depth_bits << 32) | gid with the
-// bucket index as payload (Q12: stable index tie-break = ascending gid).
+// The order is (depth_bits, gid) ascending (Q12).  Depth ties are frequent (an
+// fp32 depth at 150 m has a 1.5e-5 m ulp), so gid is always part of the key.
+// Fast path (per warp): pack (depth_bits - min_depth) | gid | bucket index into
+// one 64-bit key when the tile's depth spread fits -- the payload rides in the
+// key and a compare-exchange moves 64 bits.  Otherwise sort the 64-bit key
+// (depth_bits << 32 | gid) with the bucket index as a 32-bit payload.
 
 // warp bitonic of 32*PER keys held transposed: element e = lane*PER + j
 template <int PER, bool PAY>
@@ -255,62 +262,66 @@ __device__ __forceinline__ void warp_bitonic_t(uint64_t (&k)[PER], uint32_t (&v)
     }
 }
 
-// returns false (nothing written) when a depth tie needs the big path (PER == 32 only)
+__device__ __forceinline__ uint32_t warp_min(uint32_t x) { return __reduce_min_sync(0xffffffffu, x); }
+__device__ __forceinline__ uint32_t warp_max(uint32_t x) { return __reduce_max_sync(0xffffffffu, x); }
+
 template <int PER>
-__device__ __forceinline__ bool warp_sort_tile(const uint4* __restrict__ bucket, uint32_t s, uint32_t len,
+__device__ __forceinline__ void warp_sort_tile(const uint4* __restrict__ bucket, uint32_t s, uint32_t len,
                                                uint32_t tile, uint32_t lane, uint32_t* __restrict__ out,
                                                uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg) {
+    constexpr int IB = 5 + (PER == 1 ? 0 : PER == 2 ? 1 : PER == 4 ? 2 : PER == 8 ? 3 : 4);   // index bits
+    uint32_t dep[PER], gid[PER];
+    uint32_t dmin = 0xffffffffu, dmax = 0u, gmax = 0u;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const uint32_t e = lane * PER + (uint32_t)j;
+        if (e < len) {
+            const uint4 b = __ldg(&bucket[s + e]);
+            dep[j] = b.x;
+            gid[j] = b.z;
+            dmin = min(dmin, b.x);
+            dmax = max(dmax, b.x);
+            gmax = max(gmax, b.z);
+        } else {
+            dep[j] = gid[j] = 0u;
+        }
+    }
+    dmin = warp_min(dmin);
+    dmax = warp_max(dmax);
+    gmax = warp_max(gmax);
+    const int GB = 32 - __clz(gmax | 1u);          // bits to hold every gid of the tile
+    const int DB = 64 - GB - IB;                   // bits left for the depth offset
     uint64_t k[PER];
     uint32_t v[PER];
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-        const uint32_t e = lane * PER + (uint32_t)j;
-        k[j] = e < len ? (((uint64_t)__ldg(&bucket[s + e].x) << 32) | e) : PAD_KEY;
-    }
-    warp_bitonic_t<PER, false>(k, v, lane);
-    // depth tie between neighbours?  (element e+1 is k[j+1] or k[0] of lane+1)
-    const uint64_t nxt0 = __shfl_down_sync(0xffffffffu, k[0], 1);
-    bool tie = false;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-        const uint64_t nb = j + 1 < PER ? k[j + 1] : nxt0;
-        const uint32_t e = lane * PER + (uint32_t)j;
-        if (e + 1 < len && (k[j] >> 32) == (nb >> 32)) tie = true;
-    }
-    if (__any_sync(0xffffffffu, tie)) {
-        if constexpr (PER >= 32) {
-            return false;   // registers: let the CTA path order the ties
-        } else {
-        // rare: re-sort on (depth_bits, gid) carrying the bucket index
+    if (DB >= 32 || (uint64_t)(dmax - dmin) < (1ull << DB)) {
+        const int sg = IB, sd = GB + IB;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
             const uint32_t e = lane * PER + (uint32_t)j;
-            if (e < len) {
-                const uint4 b = bucket[s + e];
-                k[j] = ((uint64_t)b.x << 32) | b.z;
-                v[j] = e;
-            } else {
-                k[j] = PAD_KEY;
-                v[j] = 0u;
-            }
+            k[j] = e < len ? (((uint64_t)(dep[j] - dmin) << sd) | ((uint64_t)gid[j] << sg) | e) : PAD_KEY;
         }
-        warp_bitonic_t<PER, true>(k, v, lane);
-        }
+        warp_bitonic_t<PER, false>(k, v, lane);
+#pragma unroll
+        for (int j = 0; j < PER; ++j) v[j] = (uint32_t)k[j] & ((1u << IB) - 1u);
     } else {
 #pragma unroll
-        for (int j = 0; j < PER; ++j) v[j] = (uint32_t)k[j];
+        for (int j = 0; j < PER; ++j) {
+            const uint32_t e = lane * PER + (uint32_t)j;
+            k[j] = e < len ? (((uint64_t)dep[j] << 32) | gid[j]) : PAD_KEY;
+            v[j] = e;
+        }
+        warp_bitonic_t<PER, true>(k, v, lane);
     }
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         const uint32_t e = lane * PER + (uint32_t)j;
         if (e < len) {
-            const uint4 b = bucket[s + v[j]];   // L1-resident: this warp just read the bucket
+            const uint4 b = __ldg(&bucket[s + v[j]]);   // L1-resident: this warp just read the bucket
             out[s + e] = b.y;
             if (ogid) ogid[s + e] = b.z;
             if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | b.x;
         }
     }
-    return true;
 }
 
 __global__ void __launch_bounds__(256)
@@ -339,8 +350,8 @@ warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint4* __
     else if (lane == 0) big_list[atomicAdd(big_count, 1u)] = (uint32_t)tile;
 }
 
-// CTA-wide bitonic sort of n (power of two) 64-bit keys in shared memory
-__device__ void smem_bitonic(uint64_t* sk, uint32_t n) {
+// CTA-wide bitonic sort of n (power of two) 64-bit keys + 32-bit payloads in shared memory
+__device__ void smem_bitonic(uint64_t* sk, uint32_t* sv, uint32_t n) {
     for (uint32_t size = 2; size <= n; size <<= 1) {
         for (uint32_t d = size >> 1; d > 0; d >>= 1) {
             for (uint32_t t = threadIdx.x; t < n / 2; t += blockDim.x) {
@@ -348,16 +359,19 @@ __device__ void smem_bitonic(uint64_t* sk, uint32_t n) {
                 const uint32_t j = i + d;
                 const bool up = (i & size) == 0;
                 const uint64_t a = sk[i], b = sk[j];
-                if ((a > b) == up) { sk[i] = b; sk[j] = a; }
+                if ((a > b) == up) {
+                    sk[i] = b; sk[j] = a;
+                    const uint32_t tv = sv[i]; sv[i] = sv[j]; sv[j] = tv;
+                }
             }
             __syncthreads();
         }
     }
 }
 
-// merge sorted runs A = src[a0, a0+na), B = src[a0+na, a0+na+nb) into dst[a0 ...] (unique keys)
-__device__ void cta_merge(const uint64_t* __restrict__ sk, uint64_t* __restrict__ dk, uint32_t a0, uint32_t na,
-                          uint32_t nb) {
+// merge sorted runs A = [a0, a0+na), B = [a0+na, a0+na+nb) of (key, val) into dst (unique keys)
+__device__ void cta_merge(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, uint64_t* __restrict__ dk,
+                          uint32_t* __restrict__ dv, uint32_t a0, uint32_t na, uint32_t nb) {
     const uint32_t total = na + nb;
     const uint32_t per = (total + blockDim.x - 1) / blockDim.x;
     const uint32_t lo = min(total, threadIdx.x * per), hi = min(total, lo + per);
@@ -372,70 +386,75 @@ __device__ void cta_merge(const uint64_t* __restrict__ sk, uint64_t* __restrict_
     uint32_t i = ilo, j = lo - ilo;
     for (uint32_t o = lo; o < hi; ++o) {
         const bool takeA = j >= nb || (i < na && A[i] < B[j]);
-        dk[a0 + o] = takeA ? A[i++] : B[j++];
+        if (takeA) { dk[a0 + o] = A[i]; dv[a0 + o] = sv[a0 + i]; ++i; }
+        else { dk[a0 + o] = B[j]; dv[a0 + o] = sv[a0 + na + j]; ++j; }
     }
 }
 
-// Long lists (> 1024 pairs; coarse pyramid levels): one CTA per tile, runs of
-// up to 8192 keys sorted in shared memory, then merge-path merges in global
-// memory.  Keys are (depth_bits << 32 | bucket index); depth ties are fixed by a
-// serial insertion pass on (depth_bits, gid) (ties are rare).
+// Long lists (> 512 pairs; dense areas and coarse pyramid levels): one CTA per
+// tile, runs of up to 8192 (depth_bits << 32 | gid, bucket index) pairs sorted
+// in shared memory, then merge-path merges in global memory.
 __global__ void __launch_bounds__(BIG_THREADS)
 big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ bucket, uint64_t* __restrict__ ka,
-                uint64_t* __restrict__ kb, uint32_t* __restrict__ out, uint32_t* __restrict__ ogid,
-                uint64_t* __restrict__ dbg, const uint32_t* __restrict__ big_count,
-                const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ status) {
+                uint32_t* __restrict__ va, uint64_t* __restrict__ kb, uint32_t* __restrict__ vb,
+                uint32_t* __restrict__ out, uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg,
+                const uint32_t* __restrict__ big_count, const uint32_t* __restrict__ big_list,
+                const uint32_t* __restrict__ status) {
     if (*status) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
-    __shared__ int tie;
+    uint32_t* sv = reinterpret_cast<uint32_t*>(smem_raw + SMEM_SORT_MAX * sizeof(uint64_t));
     const uint32_t nbig = *big_count;
     for (uint32_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
         const uint32_t tile = big_list[bi];
         const uint32_t s = ranges[2 * tile], len = ranges[2 * tile + 1] - s;
+        const bool one_run = len <= SMEM_SORT_MAX;
         for (uint32_t r0 = 0; r0 < len; r0 += SMEM_SORT_MAX) {
             const uint32_t rl = min((uint32_t)SMEM_SORT_MAX, len - r0);
             uint32_t n2 = 1;
             while (n2 < rl) n2 <<= 1;
-            for (uint32_t e = threadIdx.x; e < n2; e += blockDim.x)
-                sk[e] = e < rl ? (((uint64_t)bucket[s + r0 + e].x << 32) | (r0 + e)) : PAD_KEY;
+            for (uint32_t e = threadIdx.x; e < n2; e += blockDim.x) {
+                if (e < rl) {
+                    const uint4 b = bucket[s + r0 + e];
+                    sk[e] = ((uint64_t)b.x << 32) | b.z;
+                    sv[e] = r0 + e;
+                } else {
+                    sk[e] = PAD_KEY;
+                    sv[e] = 0u;
+                }
+            }
             __syncthreads();
-            smem_bitonic(sk, n2);
-            for (uint32_t e = threadIdx.x; e < rl; e += blockDim.x) ka[s + r0 + e] = sk[e];
+            smem_bitonic(sk, sv, n2);
+            if (one_run) {
+                for (uint32_t e = threadIdx.x; e < rl; e += blockDim.x) {
+                    const uint4 b = bucket[s + sv[e]];
+                    out[s + e] = b.y;
+                    if (ogid) ogid[s + e] = b.z;
+                    if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | b.x;
+                }
+            } else {
+                for (uint32_t e = threadIdx.x; e < rl; e += blockDim.x) {
+                    ka[s + r0 + e] = sk[e];
+                    va[s + r0 + e] = sv[e];
+                }
+            }
             __syncthreads();
         }
-        uint64_t* ck = ka + s;
-        uint64_t* nk = kb + s;
+        if (one_run) continue;
+        uint64_t* ck = ka + s; uint32_t* cv = va + s;
+        uint64_t* nk = kb + s; uint32_t* nv = vb + s;
         for (uint32_t width = SMEM_SORT_MAX; width < len; width <<= 1) {
             for (uint32_t a0 = 0; a0 < len; a0 += 2 * width) {
                 const uint32_t na = min(width, len - a0);
                 const uint32_t nb = a0 + na < len ? min(width, len - a0 - na) : 0u;
-                cta_merge(ck, nk, a0, na, nb);
+                cta_merge(ck, cv, nk, nv, a0, na, nb);
             }
             __syncthreads();
             uint64_t* t = ck; ck = nk; nk = t;
+            uint32_t* tv = cv; cv = nv; nv = tv;
         }
-        if (threadIdx.x == 0) tie = 0;
-        __syncthreads();
-        for (uint32_t e = threadIdx.x; e + 1 < len; e += blockDim.x)
-            if ((ck[e] >> 32) == (ck[e + 1] >> 32)) tie = 1;
-        __syncthreads();
-        if (tie && threadIdx.x == 0) {
-            // insertion pass over equal-depth runs, ordering them by gid
-            for (uint32_t e = 1; e < len; ++e) {
-                const uint64_t key = ck[e];
-                const uint32_t gk = bucket[s + (uint32_t)key].z;
-                uint32_t f = e;
-                while (f > 0 && (ck[f - 1] >> 32) == (key >> 32) && bucket[s + (uint32_t)ck[f - 1]].z > gk) {
-                    ck[f] = ck[f - 1];
-                    --f;
-                }
-                ck[f] = key;
-            }
-        }
-        __syncthreads();
         for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) {
-            const uint4 b = bucket[s + (uint32_t)ck[e]];
+            const uint4 b = bucket[s + cv[e]];
             out[s + e] = b.y;
             if (ogid) ogid[s + e] = b.z;
             if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | b.x;
@@ -491,12 +510,13 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
                                                              w.big_list, proj->status);
     if ((st = check_launch("warp_sort_kernel")) != GS_OK) return st;
     static bool attr_set = false;
-    const int smem = SMEM_SORT_MAX * (int)sizeof(uint64_t);
+    const int smem = SMEM_SORT_MAX * (int)(sizeof(uint64_t) + sizeof(uint32_t));
     if (!attr_set) {
         cudaFuncSetAttribute(big_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
-    big_sort_kernel<<<num_sms(), BIG_THREADS, smem, s>>>(out->ranges, w.bucket, w.ka, w.kb, out->sorted_rec,
+    big_sort_kernel<<<2 * num_sms(), BIG_THREADS, smem, s>>>(out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb,
+                                                             out->sorted_rec,
                                                          out->sorted_gid, out->sorted_key, w.big_count, w.big_list,
                                                          proj->status);
     return check_launch("big_sort_kernel");
