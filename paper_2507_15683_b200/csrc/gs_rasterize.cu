@@ -119,7 +119,7 @@ __device__ __forceinline__ bool ellipse_hits_rect(float u, float v, float ca, fl
     return qmin <= qcut;
 }
 
-// alpha of entry k at this lane's pixel, or -1 when the oracle skips it
+// alpha of entry k at this lane's pixel, or 0 when the oracle skips it
 // (power > 0 or alpha < alpha_min).  power in the oracle's op order.
 __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, float pxf, float pyf,
                                              const gs_params& P) {
@@ -129,7 +129,7 @@ __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, f
     const float t3 = __fmul_rn(__fmul_rn(a.w, dx), dy);
     const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), t3);
     const float alpha = fminf(P.alpha_max, __fmul_rn(b.y, ex2_ftz(power * 1.4426950408889634f)));
-    return ((power > 0.0f) || (alpha < P.alpha_min)) ? -1.0f : alpha;
+    return ((power > 0.0f) || (alpha < P.alpha_min)) ? 0.0f : alpha;
 }
 
 // Persistent kernel: CTA c renders tiles c, c + grid, c + 2 grid, ...  The
@@ -255,15 +255,15 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             }
         }
     };
-    // apply one evaluated entry to this lane's pixel (branch-free; oracle order)
+    // apply one evaluated entry to this lane's pixel, branch-free.  A skipped
+    // entry (power > 0, alpha < alpha_min, or pixel already stopped) arrives as
+    // alpha = 0, which is an exact no-op: Tn = T(1 - 0) = T >= t_min, w = 0.
     auto blend = [&](float a, const float4& c) -> float {
-        const bool ok = (a >= 0.0f) && !done;
         const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
-        const bool stop = ok && (Tn < P.t_min);
-        const bool bl = ok && !stop;
-        const float wgt = bl ? __fmul_rn(a, T) : 0.0f;
+        const bool stop = Tn < P.t_min;
+        const float wgt = stop ? 0.0f : __fmul_rn(a, T);
         C0 = fmaf(wgt, c.x, C0); C1 = fmaf(wgt, c.y, C1); C2 = fmaf(wgt, c.z, C2); Dz = fmaf(wgt, c.w, Dz);
-        T = bl ? Tn : T;
+        T = stop ? T : Tn;
         done = done || stop;
         return wgt;
     };
@@ -317,10 +317,11 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i]);   // i is even
                     const int k1 = kk.x;
                     const int k2 = two ? kk.y : k1;
-                    const float a1 = entry_alpha(sm.rec[buf][k1][0], sm.rec[buf][k1][1], pxf, pyf, P);
+                    float a1 = entry_alpha(sm.rec[buf][k1][0], sm.rec[buf][k1][1], pxf, pyf, P);
                     float a2 = entry_alpha(sm.rec[buf][k2][0], sm.rec[buf][k2][1], pxf, pyf, P);
-                    if (!two) a2 = -1.0f;
+                    a1 = done ? 0.0f : a1;
                     const float w1 = blend(a1, sm.rec[buf][k1][2]);
+                    a2 = (done || !two) ? 0.0f : a2;
                     const float w2 = blend(a2, sm.rec[buf][k2][2]);
                     if constexpr (D > 0) {
                         sm.wbuf[warp][i][lane] = w1;

@@ -1,0 +1,111 @@
+"""Multi-process host logic of the pose-sharded path on CPU (gloo, world size 2):
+view sharding, RGB+depth+opacity packing, the all_gather and the unshard back to
+global view order.  Each rank "renders" its shard with the CPU oracle (test
+infrastructure), so the gathered planes must equal a single-process render
+bit for bit."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2507_15683_b200 import dist as GD  # noqa: E402
+
+
+def test_shard_views_partition_properties():
+    for n in (1, 7, 256):
+        for world in (1, 2, 3, 8):
+            shards = [GD.shard_views(n, world, r) for r in range(world)]
+            flat = sorted(i for s in shards for i in s)
+            assert flat == list(range(n))
+            sizes = [len(s) for s in shards]
+            assert max(sizes) - min(sizes) <= 1
+            assert all(s == sorted(s) and (not s or s == list(range(s[0], s[-1] + 1))) for s in shards)
+
+
+def test_cost_balanced_sharding():
+    rng = np.random.default_rng(0)
+    costs = rng.lognormal(0, 1, 256)
+    for world in (2, 4, 8):
+        shards = [GD.shard_views(256, world, r, costs) for r in range(world)]
+        assert sorted(i for s in shards for i in s) == list(range(256))
+        loads = [costs[s].sum() for s in shards]
+        # LPT bound: max load <= mean + max single cost
+        assert max(loads) <= np.mean(loads) + costs.max() + 1e-9
+        assert shards == [GD.shard_views(256, world, r, costs) for r in range(world)]   # deterministic
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n_views, use_costs, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import synth
+    scene = synth.box_v1(300, seed=9)
+    views = [synth.make_view(np.eye(3), [0.05 * i, -0.03 * i, 0.0], 48, 48, 23.5, 15.5, 48, 32)
+             for i in range(n_views)]
+    costs = [float(i % 3 + 1) for i in range(n_views)] if use_costs else None
+    mine = GD.shard_views(n_views, world, rank, costs)
+    hw = 48 * 32
+    rgb = np.zeros((len(mine), 3, hw), np.float32)
+    dep = np.zeros((len(mine), hw), np.float32)
+    alp = np.zeros((len(mine), hw), np.float32)
+    for k, i in enumerate(mine):
+        r = oracle.render(scene, views[i])
+        rgb[k] = r["rgb"].reshape(3, hw)
+        dep[k] = r["depth"].reshape(hw)
+        alp[k] = r["alpha"].reshape(hw)
+    pad = max(GD.shard_sizes(n_views, world, costs))
+    payload = GD.pack_planes(torch.from_numpy(rgb.reshape(-1)), torch.from_numpy(dep.reshape(-1)),
+                             torch.from_numpy(alp.reshape(-1)), len(mine), hw, pad)
+    gathered = GD.gather_planes(payload, world)
+    full = GD.unshard(gathered, n_views, world, costs)
+    if rank == 0:
+        torch.save(full, out_path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("use_costs", [False, True])
+def test_gloo_gather_equals_single_process(tmp_path, use_costs):
+    import oracle
+    import synth
+    oracle.build()
+    n_views = 5
+    out = str(tmp_path / "gathered.pt")
+    mp.spawn(_worker, args=(2, _free_port(), n_views, use_costs, out), nprocs=2, join=True)
+    full = torch.load(out)
+    scene = synth.box_v1(300, seed=9)
+    for i in range(n_views):
+        v = synth.make_view(np.eye(3), [0.05 * i, -0.03 * i, 0.0], 48, 48, 23.5, 15.5, 48, 32)
+        r = oracle.render(scene, v)
+        assert np.array_equal(full[i, 0:3].numpy(), r["rgb"].reshape(3, -1))
+        assert np.array_equal(full[i, 3].numpy(), r["depth"].reshape(-1))
+        assert np.array_equal(full[i, 4].numpy(), r["alpha"].reshape(-1))
+
+
+def test_bench_reference_arm_json():
+    """bench.py --impl reference prints one JSON line with the contract keys."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "C1",
+                          "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "Mpixels/s" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["e2e"]["h2d_bytes_per_step"] == 0
