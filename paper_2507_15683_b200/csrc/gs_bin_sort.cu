@@ -39,7 +39,8 @@ struct BinWs {
     uint32_t* counts;
     uint32_t* cursor;
     unsigned long long* block_sums;
-    uint32_t* big_count;
+    uint32_t* big_count;   // [0] mid list size, [1] big list size
+    uint32_t* mid_list;
     uint32_t* big_list;
     uint4* bucket;
     uint64_t* ka;
@@ -58,6 +59,7 @@ BinWs carve(void* ws, int64_t cap, int64_t T) {
     w.cursor = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * T);
     w.block_sums = reinterpret_cast<unsigned long long*>(p); p += align256(sizeof(unsigned long long) * nb);
     w.big_count = reinterpret_cast<uint32_t*>(p); p += 256;
+    w.mid_list = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * T);
     w.big_list = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * T);
     w.bucket = reinterpret_cast<uint4*>(p); p += align256(sizeof(uint4) * cap);
     w.ka = reinterpret_cast<uint64_t*>(p); p += align256(sizeof(uint64_t) * cap);
@@ -70,7 +72,7 @@ BinWs carve(void* ws, int64_t cap, int64_t T) {
 size_t ws_bytes(int64_t cap, int64_t T) {
     const int64_t nb = (T + SCAN_TILE - 1) / SCAN_TILE + 1;
     return align256(sizeof(uint32_t) * T) * 2 + align256(sizeof(unsigned long long) * nb) + 256 +
-           align256(sizeof(uint32_t) * T) + align256(sizeof(uint4) * cap) +
+           2 * align256(sizeof(uint32_t) * T) + align256(sizeof(uint4) * cap) +
            2 * (align256(sizeof(uint64_t) * cap) + align256(sizeof(uint32_t) * cap));
 }
 
@@ -267,25 +269,37 @@ __device__ __forceinline__ uint32_t warp_max(uint32_t x) { return __reduce_max_s
 
 template <int PER>
 __device__ __forceinline__ void warp_sort_tile(const uint4* __restrict__ bucket, uint32_t s, uint32_t len,
-                                               uint32_t tile, uint32_t lane, uint32_t* __restrict__ out,
-                                               uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg) {
+                                               uint32_t tile, uint32_t lane, uint2* __restrict__ stage,
+                                               uint32_t* __restrict__ out, uint32_t* __restrict__ ogid,
+                                               uint64_t* __restrict__ dbg) {
     constexpr int IB = 5 + (PER == 1 ? 0 : PER == 2 ? 1 : PER == 4 ? 2 : PER == 8 ? 3 : 4);   // index bits
+    // coalesced load of (depth_bits, gid) through this warp's shared staging buffer, then read transposed
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const uint32_t e = (uint32_t)j * 32u + lane;
+        if (e < len) {
+            const uint4 b = __ldg(&bucket[s + e]);
+            stage[e] = make_uint2(b.x, b.z);
+        }
+    }
+    __syncwarp();
     uint32_t dep[PER], gid[PER];
     uint32_t dmin = 0xffffffffu, dmax = 0u, gmax = 0u;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         const uint32_t e = lane * PER + (uint32_t)j;
         if (e < len) {
-            const uint4 b = __ldg(&bucket[s + e]);
+            const uint2 b = stage[e];
             dep[j] = b.x;
-            gid[j] = b.z;
+            gid[j] = b.y;
             dmin = min(dmin, b.x);
             dmax = max(dmax, b.x);
-            gmax = max(gmax, b.z);
+            gmax = max(gmax, b.y);
         } else {
             dep[j] = gid[j] = 0u;
         }
     }
+    __syncwarp();
     dmin = warp_min(dmin);
     dmax = warp_max(dmax);
     gmax = warp_max(gmax);
@@ -312,29 +326,41 @@ __device__ __forceinline__ void warp_sort_tile(const uint4* __restrict__ bucket,
         }
         warp_bitonic_t<PER, true>(k, v, lane);
     }
+    // write out in the transposed order via the staging buffer so global stores coalesce
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         const uint32_t e = lane * PER + (uint32_t)j;
+        if (e < len) stage[e] = make_uint2(v[j], 0u);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const uint32_t e = (uint32_t)j * 32u + lane;
         if (e < len) {
-            const uint4 b = __ldg(&bucket[s + v[j]]);   // L1-resident: this warp just read the bucket
+            const uint4 b = __ldg(&bucket[s + stage[e].x]);   // L1-resident: this warp just read the bucket
             out[s + e] = b.y;
             if (ogid) ogid[s + e] = b.z;
             if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | b.x;
         }
     }
+    __syncwarp();
 }
+
+constexpr int SMALL_MAX = 256;   // warp_sort_kernel: PER <= 8
 
 __global__ void __launch_bounds__(256)
 warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint4* __restrict__ bucket,
                  uint32_t* __restrict__ out, uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg,
-                 uint32_t* __restrict__ big_count, uint32_t* __restrict__ big_list,
-                 const uint32_t* __restrict__ status) {
+                 uint32_t* __restrict__ lists_count, uint32_t* __restrict__ mid_list,
+                 uint32_t* __restrict__ big_list, const uint32_t* __restrict__ status) {
     if (*status) return;
-    const uint32_t lane = threadIdx.x & 31u;
-    const int64_t tile = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    __shared__ uint2 stage[8][SMALL_MAX];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const int64_t tile = (int64_t)blockIdx.x * 8 + warp;
     if (tile >= T) return;
     const uint32_t s = ranges[2 * tile], e = ranges[2 * tile + 1], len = e - s;
     if (len == 0) return;
+    uint2* st = stage[warp];
     if (len == 1) {
         if (lane == 0) {
             const uint4 b = bucket[s];
@@ -342,12 +368,30 @@ warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint4* __
             if (ogid) ogid[s] = b.z;
             if (dbg) dbg[s] = ((uint64_t)tile << 32) | b.x;
         }
-    } else if (len <= 32) warp_sort_tile<1>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
-    else if (len <= 64) warp_sort_tile<2>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
-    else if (len <= 128) warp_sort_tile<4>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
-    else if (len <= 256) warp_sort_tile<8>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
-    else if (len <= WARP_SORT_MAX) warp_sort_tile<16>(bucket, s, len, (uint32_t)tile, lane, out, ogid, dbg);
-    else if (lane == 0) big_list[atomicAdd(big_count, 1u)] = (uint32_t)tile;
+    } else if (len <= 32) warp_sort_tile<1>(bucket, s, len, (uint32_t)tile, lane, st, out, ogid, dbg);
+    else if (len <= 64) warp_sort_tile<2>(bucket, s, len, (uint32_t)tile, lane, st, out, ogid, dbg);
+    else if (len <= 128) warp_sort_tile<4>(bucket, s, len, (uint32_t)tile, lane, st, out, ogid, dbg);
+    else if (len <= SMALL_MAX) warp_sort_tile<8>(bucket, s, len, (uint32_t)tile, lane, st, out, ogid, dbg);
+    else if (lane == 0) {
+        if (len <= WARP_SORT_MAX) mid_list[atomicAdd(&lists_count[0], 1u)] = (uint32_t)tile;
+        else big_list[atomicAdd(&lists_count[1], 1u)] = (uint32_t)tile;
+    }
+}
+
+// 257..512 pairs: one warp per tile (PER = 16), persistent over the mid list
+__global__ void __launch_bounds__(256)
+mid_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ bucket, uint32_t* __restrict__ out,
+                uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg, const uint32_t* __restrict__ lists_count,
+                const uint32_t* __restrict__ mid_list, const uint32_t* __restrict__ status) {
+    if (*status) return;
+    __shared__ uint2 stage[8][WARP_SORT_MAX];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t n = lists_count[0];
+    for (uint32_t i = blockIdx.x * 8 + warp; i < n; i += gridDim.x * 8) {
+        const uint32_t tile = mid_list[i];
+        const uint32_t s = ranges[2 * tile], len = ranges[2 * tile + 1] - s;
+        warp_sort_tile<16>(bucket, s, len, tile, lane, stage[warp], out, ogid, dbg);
+    }
 }
 
 // CTA-wide bitonic sort of n (power of two) 64-bit keys + 32-bit payloads in shared memory
@@ -404,7 +448,7 @@ big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ b
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
     uint32_t* sv = reinterpret_cast<uint32_t*>(smem_raw + SMEM_SORT_MAX * sizeof(uint64_t));
-    const uint32_t nbig = *big_count;
+    const uint32_t nbig = big_count[1];
     for (uint32_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
         const uint32_t tile = big_list[bi];
         const uint32_t s = ranges[2 * tile], len = ranges[2 * tile + 1] - s;
@@ -492,7 +536,7 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     BinWs w = carve(ws, out->pair_capacity, T);
     const int64_t cap = proj->rec_capacity;
     cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * T, s);
-    cudaMemsetAsync(w.big_count, 0, sizeof(uint32_t), s);
+    cudaMemsetAsync(w.big_count, 0, 2 * sizeof(uint32_t), s);
 
     const int64_t blocks_per_view = std::min<int64_t>((cap + 255) / 256, std::max(1, 4 * num_sms() / n_views + 1));
     dim3 rgrid((unsigned)std::max<int64_t>(1, blocks_per_view), (unsigned)n_views);
@@ -507,7 +551,9 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     if ((st = check_launch("scatter_kernel")) != GS_OK) return st;
     warp_sort_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(out->ranges, T, w.bucket, out->sorted_rec,
                                                              out->sorted_gid, out->sorted_key, w.big_count,
-                                                             w.big_list, proj->status);
+                                                             w.mid_list, w.big_list, proj->status);
+    mid_sort_kernel<<<4 * num_sms(), 256, 0, s>>>(out->ranges, w.bucket, out->sorted_rec, out->sorted_gid,
+                                                  out->sorted_key, w.big_count, w.mid_list, proj->status);
     if ((st = check_launch("warp_sort_kernel")) != GS_OK) return st;
     static bool attr_set = false;
     const int smem = SMEM_SORT_MAX * (int)(sizeof(uint64_t) + sizeof(uint32_t));
