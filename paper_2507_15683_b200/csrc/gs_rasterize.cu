@@ -36,7 +36,7 @@ constexpr int RT_THREADS = (NCW + 1) * 32;
 constexpr int SE = 64;                 // entries per stage
 constexpr int NST = 4;                 // ring stages
 constexpr int WB_STRIDE = 40;          // weight-buffer row stride (conflict-free A fragments)
-constexpr int WB_ROWS = 32;            // one ballot's entries
+constexpr int WB_ROWS = 40;            // pending (< 8) + one ballot (<= 32) entries
 constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -90,8 +90,8 @@ struct StageMeta {
 template <int D>
 struct RasterSmem {
     static constexpr int FS = D > 0 ? D + 8 : 1;   // feature row stride (floats)
-    float4 rec[NST][SE][4];                        // 64-byte records
-    float feat[D > 0 ? NST : 1][D > 0 ? SE : 1][FS];
+    float4 rec[NST][SE + 1][4];                    // 64-byte records; row SE = null record (opacity 0)
+    float feat[D > 0 ? NST : 1][D > 0 ? SE + 1 : 1][FS];
     alignas(16) float wbuf[D > 0 ? NCW : 1][WB_ROWS][WB_STRIDE]; // per-warp compacted weights [k][pixel]
     alignas(16) int ent[NCW][WB_ROWS];               // per-warp compacted entry indices
     StageMeta meta[NST];
@@ -146,6 +146,10 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     extern __shared__ __align__(128) unsigned char smem_raw[];
     RasterSmem<D>& sm = *reinterpret_cast<RasterSmem<D>*>(smem_raw);
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < NST * 4; i += blockDim.x) sm.rec[i / 4][SE][i % 4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (D > 0)
+        for (int i = threadIdx.x; i < NST * RasterSmem<D>::FS; i += blockDim.x)
+            sm.feat[i / RasterSmem<D>::FS][SE][i % RasterSmem<D>::FS] = 0.f;
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(&sm.full[s], 33);     // 32 cp.async arrivals + 1 metadata arrival
@@ -157,57 +161,83 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
 
     if (warp == NCW) {
         // ------------------------------------------------------------ producer
-        uint32_t s = 0;
-        for (uint32_t tile = blockIdx.x;; tile += gridDim.x) {
-            const bool end = tile >= n_tiles;
-            uint32_t rs = 0, re = 0;
-            int view = 0;
+        // Stage iterator over this CTA's tiles; the index loads (sorted slot / gid) of
+        // stage s+1 are issued before waiting for stage s's ring slot, so their
+        // latency hides behind the wait and the gathers of stage s.
+        uint32_t tile = blockIdx.x, rs = 0, re = 0, k = 0, nst = 1;
+        int view = 0;
+        bool end = false;
+        auto tile_begin = [&](uint32_t t) {
+            tile = t;
+            end = t >= n_tiles;
+            k = 0;
             if (!end) {
-                rs = __ldg(&ranges[2 * tile]);
-                re = __ldg(&ranges[2 * tile + 1]);
-                view = find_view_by_tile(views, n_views, tile);
+                rs = __ldg(&ranges[2 * t]);
+                re = __ldg(&ranges[2 * t + 1]);
+                view = find_view_by_tile(views, n_views, t);
+                nst = max(1u, (re - rs + SE - 1) / SE);
+            } else {
+                rs = re = 0;
+                nst = 1;
             }
-            const uint32_t nst = end ? 1u : max(1u, (re - rs + SE - 1) / SE);
-            for (uint32_t k = 0; k < nst; ++k, ++s) {
-                const uint32_t buf = s % NST;
-                if (s >= NST) mbar_wait(&sm.empty[buf], ((s / NST) & 1u) ^ 1u);
-                const uint32_t c0 = rs + k * SE;
-                const int cnt = end ? 0 : (int)min((uint32_t)SE, re - c0);
-                // issue the (independent) index loads of both entries first, then the gathers
-                uint32_t slot[SE / 32], gid[SE / 32];
+        };
+        auto load_idx = [&](uint32_t c0, int cnt, uint32_t (&sl)[SE / 32], uint32_t (&gd)[SE / 32]) {
 #pragma unroll
-                for (int q = 0; q < SE / 32; ++q) {
-                    const int j = q * 32 + (int)lane;
-                    slot[q] = j < cnt ? __ldg(&sorted_rec[c0 + j]) : 0u;
-                    gid[q] = (D > 0 && j < cnt && sorted_gid) ? __ldg(&sorted_gid[c0 + j]) : 0u;
-                }
+            for (int q = 0; q < SE / 32; ++q) {
+                const int j = q * 32 + (int)lane;
+                sl[q] = j < cnt ? __ldg(&sorted_rec[c0 + j]) : 0u;
+                gd[q] = (D > 0 && j < cnt) ? (sorted_gid ? __ldg(&sorted_gid[c0 + j]) : __ldg(&rec[sl[q]].gid)) : 0u;
+            }
+        };
+        tile_begin(blockIdx.x);
+        uint32_t slot[SE / 32], gid[SE / 32];
+        uint32_t c0 = rs;
+        int cnt = end ? 0 : (int)min((uint32_t)SE, re - c0);
+        load_idx(c0, cnt, slot, gid);
+        uint32_t s = 0;
+        for (;; ++s) {
+            const uint32_t buf = s % NST;
+            // descriptor of this stage
+            const uint32_t ctile = tile, cc0 = c0;
+            const int ccnt = cnt, cview = view;
+            const uint32_t flags = (k == 0 ? ST_FIRST : 0u) | (k == nst - 1 ? ST_LAST : 0u) | (end ? ST_END : 0u);
+            const bool cend = end;
+            // advance the iterator and prefetch the next stage's indices
+            uint32_t nslot[SE / 32], ngid[SE / 32];
+            if (!cend) {
+                if (++k == nst) tile_begin(tile + gridDim.x);
+                c0 = rs + k * SE;
+                cnt = end ? 0 : (int)min((uint32_t)SE, re - c0);
+                load_idx(c0, cnt, nslot, ngid);
+            }
+            if (s >= NST) mbar_wait(&sm.empty[buf], ((s / NST) & 1u) ^ 1u);
 #pragma unroll
-                for (int q = 0; q < SE / 32; ++q) {
-                    const int j = q * 32 + (int)lane;
-                    if (j < cnt) {
-                        const float4* src = reinterpret_cast<const float4*>(rec + slot[q]);
+            for (int q = 0; q < SE / 32; ++q) {
+                const int j = q * 32 + (int)lane;
+                if (j < ccnt) {
+                    const float4* src = reinterpret_cast<const float4*>(rec + slot[q]);
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) cp_async16(&sm.rec[buf][j][e], src + e);
-                        if constexpr (D > 0) {
-                            const uint32_t gg = sorted_gid ? gid[q] : __ldg(&rec[slot[q]].gid);
-                            const float4* fs = reinterpret_cast<const float4*>(feat + (int64_t)gg * D);
+                    for (int e = 0; e < 4; ++e) cp_async16(&sm.rec[buf][j][e], src + e);
+                    if constexpr (D > 0) {
+                        const float4* fs = reinterpret_cast<const float4*>(feat + (int64_t)gid[q] * D);
 #pragma unroll
-                            for (int e = 0; e < D / 4; ++e) cp_async16(&sm.feat[buf][j][e * 4], fs + e);
-                        }
+                        for (int e = 0; e < D / 4; ++e) cp_async16(&sm.feat[buf][j][e * 4], fs + e);
                     }
                 }
-                cp_async_mbar_arrive(&sm.full[buf]);
-                if (lane == 0) {
-                    StageMeta m;
-                    m.tile = tile; m.c0 = c0; m.cnt = cnt; m.view = view;
-                    m.flags = (k == 0 ? ST_FIRST : 0u) | (k == nst - 1 ? ST_LAST : 0u) | (end ? ST_END : 0u);
-                    m.pad0 = m.pad1 = m.pad2 = 0;
-                    sm.meta[buf] = m;
-                    mbar_arrive(&sm.full[buf]);
-                }
             }
-            if (end) break;
+            cp_async_mbar_arrive(&sm.full[buf]);
+            if (lane == 0) {
+                StageMeta m;
+                m.tile = ctile; m.c0 = cc0; m.cnt = ccnt; m.view = cview; m.flags = flags;
+                m.pad0 = m.pad1 = m.pad2 = 0;
+                sm.meta[buf] = m;
+                mbar_arrive(&sm.full[buf]);
+            }
+            if (cend) break;
+#pragma unroll
+            for (int q = 0; q < SE / 32; ++q) { slot[q] = nslot[q]; gid[q] = ngid[q]; }
         }
+        ++s;
         // drain: the CTA must not retire while copies into its smem are in flight
         for (uint32_t q = (s > NST ? s - NST : 0u); q < s; ++q) mbar_wait(&sm.full[q % NST], (q / NST) & 1u);
         return;
@@ -225,9 +255,9 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Dz = 0.f;
 
     // F[px][:] += W[px][0..nk) F_entries[0..nk)[:] on the tensor cores (nk multiple of 8)
-    auto mma_block = [&](int buf, int nk) {
+    auto mma_block = [&](int buf, int kb, int ke) {
         if constexpr (D > 0) {
-            for (int k0 = 0; k0 < nk; k0 += 8) {
+            for (int k0 = kb; k0 < ke; k0 += 8) {
                 uint32_t ahi[2][4], alo[2][4];
 #pragma unroll
                 for (int m = 0; m < 2; ++m) {
@@ -296,6 +326,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 for (int n = 0; n < NTP; ++n) acc[a][n][0] = acc[a][n][1] = acc[a][n][2] = acc[a][n][3] = 0.f;
         }
         if (!warp_done && m.cnt > 0) {
+            int pend = 0;   // weights of walked entries not yet fed to the tensor cores
 #pragma unroll 1
             for (int half = 0; half * 32 < m.cnt; ++half) {
                 const int j = half * 32 + (int)lane;
@@ -308,36 +339,63 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 const uint32_t msk = __ballot_sync(0xffffffffu, hit);
                 const int n = __popc(msk);
                 if (n == 0) continue;
-                if (hit) sm.ent[warp][__popc(msk & ((1u << lane) - 1u))] = j;   // compacted list, in order
+                if constexpr (D > 0) {
+                    if (pend + n > WB_ROWS - 1) {          // no room: flush the pending rows first
+                        for (int r = pend; r < ((pend + 7) & ~7); ++r) sm.wbuf[warp][r][lane] = 0.f;
+                        if (lane < (uint32_t)(((pend + 7) & ~7) - pend)) sm.ent[warp][pend + lane] = SE;
+                        __syncwarp();
+                        mma_block(buf, 0, (pend + 7) & ~7);
+                        __syncwarp();
+                        pend = 0;
+                    }
+                }
+                const int base = D > 0 ? pend : 0;
+                // compacted in-order entry list; an odd tail is padded with the null record
+                if (hit) sm.ent[warp][base + __popc(msk & ((1u << lane) - 1u))] = j;
+                if (lane == 0 && (n & 1)) sm.ent[warp][base + n] = SE;
                 __syncwarp();
 #pragma unroll 1
-                for (int i = 0; i < n; i += 2) {
+                for (int i = base; i < base + n; i += 2) {
                     // two entries per iteration: independent alphas (ILP 2), transmittance in list order
-                    const bool two = i + 1 < n;
                     const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i]);   // i is even
-                    const int k1 = kk.x;
-                    const int k2 = two ? kk.y : k1;
-                    float a1 = entry_alpha(sm.rec[buf][k1][0], sm.rec[buf][k1][1], pxf, pyf, P);
-                    float a2 = entry_alpha(sm.rec[buf][k2][0], sm.rec[buf][k2][1], pxf, pyf, P);
+                    float a1 = entry_alpha(sm.rec[buf][kk.x][0], sm.rec[buf][kk.x][1], pxf, pyf, P);
+                    float a2 = entry_alpha(sm.rec[buf][kk.y][0], sm.rec[buf][kk.y][1], pxf, pyf, P);
                     a1 = done ? 0.0f : a1;
-                    const float w1 = blend(a1, sm.rec[buf][k1][2]);
-                    a2 = (done || !two) ? 0.0f : a2;
-                    const float w2 = blend(a2, sm.rec[buf][k2][2]);
+                    const float w1 = blend(a1, sm.rec[buf][kk.x][2]);
+                    a2 = done ? 0.0f : a2;
+                    const float w2 = blend(a2, sm.rec[buf][kk.y][2]);
                     if constexpr (D > 0) {
                         sm.wbuf[warp][i][lane] = w1;
                         sm.wbuf[warp][i + 1][lane] = w2;
                     }
                 }
                 if constexpr (D > 0) {
-                    const int nk = (n + 7) & ~7;
-                    for (int r = (n + 1) & ~1; r < nk; ++r) sm.wbuf[warp][r][lane] = 0.f;   // zero padding
-                    if (lane < (uint32_t)(nk - n)) sm.ent[warp][n + lane] = sm.ent[warp][0];
-                    __syncwarp();
-                    mma_block(buf, nk);
+                    pend = base + ((n + 1) & ~1);          // rows written (even)
+                    const int full = pend & ~7;
+                    if (full > 0) {
+                        __syncwarp();
+                        mma_block(buf, 0, full);
+                        __syncwarp();
+                        // move the < 8 leftover rows to the front
+                        const int left = pend - full;
+                        for (int r = 0; r < left; ++r) sm.wbuf[warp][r][lane] = sm.wbuf[warp][full + r][lane];
+                        if (lane < (uint32_t)left) sm.ent[warp][lane] = sm.ent[warp][full + lane];
+                        __syncwarp();
+                        pend = left;
+                    }
                 }
                 __syncwarp();
                 warp_done = __all_sync(0xffffffffu, done);
                 if (warp_done) break;
+            }
+            if constexpr (D > 0) {
+                if (pend > 0) {                            // stage end: pad to 8 and flush
+                    for (int r = pend; r < 8; ++r) sm.wbuf[warp][r][lane] = 0.f;
+                    if (lane < (uint32_t)(8 - pend)) sm.ent[warp][pend + lane] = SE;
+                    __syncwarp();
+                    mma_block(buf, 0, 8);
+                    __syncwarp();
+                }
             }
         }
         if (m.flags & ST_LAST) {
