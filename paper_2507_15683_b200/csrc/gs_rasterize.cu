@@ -33,8 +33,8 @@ namespace {
 
 constexpr int NCW = 8;                 // consumer warps
 constexpr int RT_THREADS = (NCW + 1) * 32;
-constexpr int SE = 64;                 // entries per stage
-constexpr int NST = 4;                 // ring stages
+constexpr int SE = 32;                 // entries per stage (one ballot)
+constexpr int NST = 8;                 // ring stages
 constexpr int WB_STRIDE = 40;          // weight-buffer row stride (conflict-free A fragments)
 constexpr int WB_ROWS = 40;            // pending (< 8) + one ballot (<= 32) entries
 constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
@@ -255,7 +255,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Dz = 0.f;
 
     // F[px][:] += W[px][0..nk) F_entries[0..nk)[:] on the tensor cores (nk multiple of 8)
-    auto mma_block = [&](int buf, int kb, int ke) {
+    auto mma_block = [&](int kb, int ke) {
         if constexpr (D > 0) {
             for (int k0 = kb; k0 < ke; k0 += 8) {
                 uint32_t ahi[2][4], alo[2][4];
@@ -270,8 +270,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                         alo[m][i] = __float_as_uint(av[i] - __uint_as_float(ahi[m][i]));   // exact remainder
                     }
                 }
-                const float* f0 = &sm.feat[buf][sm.ent[warp][k0 + t4]][0];
-                const float* f1 = &sm.feat[buf][sm.ent[warp][k0 + t4 + 4]][0];
+                const float* f0 = &sm.feat[0][0][0] + sm.ent[warp][k0 + t4] * RasterSmem<D>::FS;
+                const float* f1 = &sm.feat[0][0][0] + sm.ent[warp][k0 + t4 + 4] * RasterSmem<D>::FS;
 #pragma unroll
                 for (int n = 0; n < NTP; ++n) {
                     const int ch = n * 8 + g;
@@ -296,6 +296,27 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
         T = stop ? T : Tn;
         done = done || stop;
         return wgt;
+    };
+
+    // Weights of walked entries are fed to the tensor cores 8 at a time; fewer than
+    // 8 may stay pending across stages, so a stage's ring slot is released only when
+    // no pending row references it.  Ring rows are addressed flat: stage buffer b,
+    // entry j -> b * (SE + 1) + j (row SE of every buffer is the null record).
+    const float4* recf = &sm.rec[0][0][0];
+    int pend = 0;             // pending weight rows (< 8 between stages)
+    uint32_t hold = 0;        // oldest stage a pending row references
+    uint32_t rel = 0;         // next stage to release
+    auto flush_pending = [&]() {
+        if constexpr (D > 0) {
+            if (pend > 0) {
+                for (int r = pend; r < 8; ++r) sm.wbuf[warp][r][lane] = 0.f;
+                if (lane < (uint32_t)(8 - pend)) sm.ent[warp][pend + lane] = SE;   // null row
+                __syncwarp();
+                mma_block(0, 8);
+                __syncwarp();
+                pend = 0;
+            }
+        }
     };
 
     for (uint32_t s = 0;; ++s) {
@@ -326,79 +347,63 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 for (int n = 0; n < NTP; ++n) acc[a][n][0] = acc[a][n][1] = acc[a][n][2] = acc[a][n][3] = 0.f;
         }
         if (!warp_done && m.cnt > 0) {
-            int pend = 0;   // weights of walked entries not yet fed to the tensor cores
-#pragma unroll 1
-            for (int half = 0; half * 32 < m.cnt; ++half) {
-                const int j = half * 32 + (int)lane;
-                bool hit = false;
-                if (j < m.cnt) {
-                    const float4 a = sm.rec[buf][j][0];   // u, v, ca, cb
-                    const float4 b = sm.rec[buf][j][1];   // cc, o, q_cut, -
-                    hit = ellipse_hits_rect(a.x, a.y, a.z, a.w, b.x, b.z, rx0, rx1, ry0, ry1);
-                }
-                const uint32_t msk = __ballot_sync(0xffffffffu, hit);
-                const int n = __popc(msk);
-                if (n == 0) continue;
-                if constexpr (D > 0) {
-                    if (pend + n > WB_ROWS - 1) {          // no room: flush the pending rows first
-                        for (int r = pend; r < ((pend + 7) & ~7); ++r) sm.wbuf[warp][r][lane] = 0.f;
-                        if (lane < (uint32_t)(((pend + 7) & ~7) - pend)) sm.ent[warp][pend + lane] = SE;
-                        __syncwarp();
-                        mma_block(buf, 0, (pend + 7) & ~7);
-                        __syncwarp();
-                        pend = 0;
-                    }
-                }
+            const int flat0 = buf * (SE + 1);
+            const int j = (int)lane;
+            bool hit = false;
+            if (j < m.cnt) {
+                const float4 a = sm.rec[buf][j][0];   // u, v, ca, cb
+                const float4 b = sm.rec[buf][j][1];   // cc, o, q_cut, -
+                hit = ellipse_hits_rect(a.x, a.y, a.z, a.w, b.x, b.z, rx0, rx1, ry0, ry1);
+            }
+            const uint32_t msk = __ballot_sync(0xffffffffu, hit);
+            const int n = __popc(msk);
+            if (n > 0) {
                 const int base = D > 0 ? pend : 0;
                 // compacted in-order entry list; an odd tail is padded with the null record
-                if (hit) sm.ent[warp][base + __popc(msk & ((1u << lane) - 1u))] = j;
-                if (lane == 0 && (n & 1)) sm.ent[warp][base + n] = SE;
+                if (hit) sm.ent[warp][base + __popc(msk & ((1u << lane) - 1u))] = flat0 + j;
+                if (lane == 0 && (n & 1)) sm.ent[warp][base + n] = flat0 + SE;
                 __syncwarp();
 #pragma unroll 1
                 for (int i = base; i < base + n; i += 2) {
                     // two entries per iteration: independent alphas (ILP 2), transmittance in list order
                     const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i]);   // i is even
-                    float a1 = entry_alpha(sm.rec[buf][kk.x][0], sm.rec[buf][kk.x][1], pxf, pyf, P);
-                    float a2 = entry_alpha(sm.rec[buf][kk.y][0], sm.rec[buf][kk.y][1], pxf, pyf, P);
+                    const float4* r1 = recf + 4 * kk.x;
+                    const float4* r2 = recf + 4 * kk.y;
+                    float a1 = entry_alpha(r1[0], r1[1], pxf, pyf, P);
+                    float a2 = entry_alpha(r2[0], r2[1], pxf, pyf, P);
                     a1 = done ? 0.0f : a1;
-                    const float w1 = blend(a1, sm.rec[buf][kk.x][2]);
+                    const float w1 = blend(a1, r1[2]);
                     a2 = done ? 0.0f : a2;
-                    const float w2 = blend(a2, sm.rec[buf][kk.y][2]);
+                    const float w2 = blend(a2, r2[2]);
                     if constexpr (D > 0) {
                         sm.wbuf[warp][i][lane] = w1;
                         sm.wbuf[warp][i + 1][lane] = w2;
                     }
                 }
                 if constexpr (D > 0) {
+                    if (pend == 0) hold = s;
                     pend = base + ((n + 1) & ~1);          // rows written (even)
                     const int full = pend & ~7;
                     if (full > 0) {
                         __syncwarp();
-                        mma_block(buf, 0, full);
+                        mma_block(0, full);
                         __syncwarp();
-                        // move the < 8 leftover rows to the front
+                        // move the < 8 leftover rows (all from this stage) to the front
                         const int left = pend - full;
                         for (int r = 0; r < left; ++r) sm.wbuf[warp][r][lane] = sm.wbuf[warp][full + r][lane];
                         if (lane < (uint32_t)left) sm.ent[warp][lane] = sm.ent[warp][full + lane];
                         __syncwarp();
                         pend = left;
+                        hold = s;
                     }
                 }
-                __syncwarp();
                 warp_done = __all_sync(0xffffffffu, done);
-                if (warp_done) break;
-            }
-            if constexpr (D > 0) {
-                if (pend > 0) {                            // stage end: pad to 8 and flush
-                    for (int r = pend; r < 8; ++r) sm.wbuf[warp][r][lane] = 0.f;
-                    if (lane < (uint32_t)(8 - pend)) sm.ent[warp][pend + lane] = SE;
-                    __syncwarp();
-                    mma_block(buf, 0, 8);
-                    __syncwarp();
-                }
             }
         }
+        // never pin more than half the ring: the producer must be able to refill
+        if (D > 0 && pend > 0 && s - hold >= NST / 2) flush_pending();
         if (m.flags & ST_LAST) {
+            flush_pending();
             // -------------------------------------------------------- outputs
             const int64_t HW = (int64_t)W * H;
             const int64_t po = V->pix_offset;
@@ -411,27 +416,32 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 out_alpha[po + loc] = 1.0f - T;
             }
             if constexpr (D > 0) {
-                // accumulator (a, n, i): pixel (sx + g, sy + 2a + (i >> 1)), channel 8n + 2 t4 + (i & 1)
-                float* fo = out_feat + (int64_t)D * po;
+                // accumulator (a, n, i): pixel (sx + g, sy + 2a + (i >> 1)), channel 8n + 2 t4 + (i & 1);
+                // one 64-bit base pointer per (a, i) and a plain pointer walk over the channel planes
                 const int fx = sx + g;
+                float* fbase = out_feat + (int64_t)D * po + (int64_t)(2 * t4) * HW + fx;
+                const int64_t step8 = 8 * HW;
 #pragma unroll
                 for (int a = 0; a < 2; ++a)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const int fy = sy + 2 * a + (i >> 1);
                         if (fx < W && fy < H) {
-                            const int64_t loc = (int64_t)fy * W + fx;
+                            float* q = fbase + (int64_t)fy * W + ((i & 1) ? HW : 0);
 #pragma unroll
                             for (int n = 0; n < NTP; ++n) {
-                                const int ch = n * 8 + 2 * t4 + (i & 1);
-                                if (ch < D) fo[(int64_t)ch * HW + loc] = acc[a][n][i];
+                                if (n * 8 + 2 * t4 + (i & 1) < D) *q = acc[a][n][i];
+                                q += step8;
                             }
                         }
                     }
             }
         }
+        // release every stage no pending row references, in order
+        const uint32_t lim = (D > 0 && pend > 0) ? hold : s + 1;
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[buf]);
+        for (; rel < lim; ++rel)
+            if (lane == 0) mbar_arrive(&sm.empty[rel % NST]);
     }
 }
 
