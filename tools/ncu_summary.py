@@ -22,3 +22,18 @@ for r in rows[2:]:
     for w in want:
         if w in hdr:
             i = hdr.index(w); print(f'  {w}: {r[i]} {units[i]}')
+    tot = 0.0
+    st = {}
+    for i, h in enumerate(hdr):
+        if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued"):
+            try:
+                st[h.replace("smsp__pcsamp_warps_issue_stalled_", "")] = float(r[i])
+            except ValueError:
+                pass
+    tot = sum(st.values())
+    if tot:
+        print("  stall samples: " + ", ".join(f"{k} {v / tot * 100:.1f}%" for k, v in
+                                              sorted(st.items(), key=lambda x: -x[1])[:8]))
+    for w in ("smsp__inst_executed.sum", "sm__inst_executed.sum"):
+        if w in hdr:
+            print(f"  {w}: {r[hdr.index(w)]}")
