@@ -363,28 +363,18 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 if (hit) sm.ent[warp][base + __popc(msk & ((1u << lane) - 1u))] = flat0 + j;
                 if (lane == 0 && (n & 1)) sm.ent[warp][base + n] = flat0 + SE;
                 __syncwarp();
-                // software-pipelined: the next pair's entry indices and geometry are read
-                // from shared memory while the current pair is evaluated
-                int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][base]);
-                float4 ga1 = recf[4 * kk.x], gb1 = recf[4 * kk.x + 1];
-                float4 ga2 = recf[4 * kk.y], gb2 = recf[4 * kk.y + 1];
 #pragma unroll 1
                 for (int i = base; i < base + n; i += 2) {
                     // two entries per iteration: independent alphas (ILP 2), transmittance in list order
+                    const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i]);   // i is even
                     const float4* r1 = recf + 4 * kk.x;
                     const float4* r2 = recf + 4 * kk.y;
-                    float a1 = entry_alpha(ga1, gb1, pxf, pyf, P);
-                    float a2 = entry_alpha(ga2, gb2, pxf, pyf, P);
-                    const float4 c1 = r1[2], c2 = r2[2];
-                    if (i + 2 < base + n) {
-                        kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i + 2]);
-                        ga1 = recf[4 * kk.x]; gb1 = recf[4 * kk.x + 1];
-                        ga2 = recf[4 * kk.y]; gb2 = recf[4 * kk.y + 1];
-                    }
+                    float a1 = entry_alpha(r1[0], r1[1], pxf, pyf, P);
+                    float a2 = entry_alpha(r2[0], r2[1], pxf, pyf, P);
                     a1 = done ? 0.0f : a1;
-                    const float w1 = blend(a1, c1);
+                    const float w1 = blend(a1, r1[2]);
                     a2 = done ? 0.0f : a2;
-                    const float w2 = blend(a2, c2);
+                    const float w2 = blend(a2, r2[2]);
                     if constexpr (D > 0) {
                         sm.wbuf[warp][i][lane] = w1;
                         sm.wbuf[warp][i + 1][lane] = w2;
