@@ -6,7 +6,8 @@
 //
 // Design (B200, no global radix sort): the range table IS the exclusive scan
 // of a per-tile histogram, so the sort is only needed inside each tile:
-//   1. count    : per record, atomic histogram over the tiles of its rectangle
+//   1. count    : per record, histogram over the tiles of its rectangle (on-chip
+//                 per CTA chunk, merged with one global atomic per non-zero bin)
 //   2. scan     : exclusive scan -> ranges [start, end) and scatter cursors
 //   3. scatter  : per record, {depth_bits, record slot, gid} into its tiles'
 //                 buckets (order inside a bucket is arbitrary)
@@ -31,7 +32,7 @@ constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_PER_THREAD = 4;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_PER_THREAD;
 constexpr int WARP_SORT_MAX = 512;      // 16 keys per lane
-constexpr int SMEM_SORT_MAX = 8192;     // 96 KB of shared memory
+constexpr int SMEM_SORT_MAX = 8192;     // run length sorted on chip (2 padded buffers: 209 KB)
 constexpr int BIG_THREADS = 512;
 constexpr uint64_t PAD_KEY = ~0ull;
 
@@ -77,19 +78,59 @@ size_t ws_bytes(int64_t cap, int64_t T) {
 }
 
 // ---------------------------------------------------------------- 1. count
-__global__ void count_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
-                             const gs_view* __restrict__ views, uint32_t* __restrict__ counts,
-                             const uint32_t* __restrict__ status) {
+// One CTA per (view, contiguous chunk of its records).  When the view's tile
+// grid fits in shared memory the CTA histograms its chunk on chip and merges
+// the non-zero bins with one global atomic each (few global atomics even for a
+// single view where every counter is hot); otherwise it falls back to one
+// global reduction per pair.
+constexpr int BIN_THREADS = 512;
+constexpr int HIST_MAX = 16384;   // tiles per view handled on chip (64 KB)
+
+__device__ __forceinline__ void chunk_of(uint32_t nv, uint32_t& k0, uint32_t& k1) {
+    const uint32_t per = (nv + gridDim.x - 1) / gridDim.x;
+    k0 = min(nv, blockIdx.x * per);
+    k1 = min(nv, k0 + per);
+}
+
+__device__ __forceinline__ void rect_of(const uint4& q3, uint32_t& x0, uint32_t& y0, uint32_t& nx, uint32_t& npair) {
+    x0 = q3.z & 0xffffu;
+    y0 = q3.w & 0xffffu;
+    nx = (q3.z >> 16) - x0 + 1;
+    npair = nx * ((q3.w >> 16) - y0 + 1);
+}
+
+__global__ void __launch_bounds__(BIN_THREADS)
+count_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
+             const gs_view* __restrict__ views, uint32_t* __restrict__ counts, const uint32_t* __restrict__ status) {
     if (*status & GS_STATUS_RECORD_OVERFLOW) return;
+    extern __shared__ uint32_t hist[];
     const int v = blockIdx.y;
     const uint32_t nv = min((uint64_t)n_rec[v], (uint64_t)cap);
     const uint32_t toff = views[v].tile_offset;
     const int TX = view_tiles_x(views[v]);
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nv; k += gridDim.x * blockDim.x) {
-        const uint4 q = __ldg(reinterpret_cast<const uint4*>(rec + (int64_t)v * cap + k) + 3);
-        const uint32_t x0 = q.z & 0xffffu, x1 = q.z >> 16, y0 = q.w & 0xffffu, y1 = q.w >> 16;
-        for (uint32_t ty = y0; ty <= y1; ++ty)
-            for (uint32_t tx = x0; tx <= x1; ++tx) atomicAdd(&counts[toff + ty * TX + tx], 1u);
+    const int Tv = TX * ((views[v].height + GS_TILE - 1) / GS_TILE);
+    const bool onchip = Tv <= HIST_MAX;
+    uint32_t k0, k1;
+    chunk_of(nv, k0, k1);
+    if (k0 >= k1) return;
+    if (onchip) {
+        for (int t = threadIdx.x; t < Tv; t += blockDim.x) hist[t] = 0u;
+        __syncthreads();
+    }
+    for (uint32_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        const uint4 q3 = __ldg(reinterpret_cast<const uint4*>(rec + (int64_t)v * cap + k) + 3);
+        uint32_t x0, y0, nx, np;
+        rect_of(q3, x0, y0, nx, np);
+        for (uint32_t p = 0; p < np; ++p) {
+            const uint32_t t = (y0 + p / nx) * TX + x0 + p % nx;
+            if (onchip) atomicAdd(&hist[t], 1u);
+            else atomicAdd(&counts[toff + t], 1u);
+        }
+    }
+    if (onchip) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < Tv; t += blockDim.x)
+            if (hist[t]) atomicAdd(&counts[toff + t], hist[t]);
     }
 }
 
@@ -182,36 +223,60 @@ scan_down_kernel(const uint32_t* __restrict__ counts, int64_t T, const unsigned 
 }
 
 // ---------------------------------------------------------------- 3. scatter
-// bucket entry: {depth_bits, record slot, gid, 0}; order inside a bucket is arbitrary
-__global__ void scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
-                               const gs_view* __restrict__ views, uint32_t* __restrict__ cursor,
-                               uint4* __restrict__ bucket, const uint32_t* __restrict__ status) {
+// bucket entry: {depth_bits, record slot, gid, 0}; order inside a bucket is
+// arbitrary.  On-chip path: histogram the chunk, reserve each non-zero bin's
+// range with one global atomic, then place pairs with shared-memory atomics.
+__global__ void __launch_bounds__(BIN_THREADS)
+scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
+               const gs_view* __restrict__ views, uint32_t* __restrict__ cursor, uint4* __restrict__ bucket,
+               const uint32_t* __restrict__ status) {
     if (*status) return;
+    extern __shared__ uint32_t hist[];
     const int v = blockIdx.y;
     const uint32_t nv = min((uint64_t)n_rec[v], (uint64_t)cap);
     const uint32_t toff = views[v].tile_offset;
     const int TX = view_tiles_x(views[v]);
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nv; k += gridDim.x * blockDim.x) {
+    const int Tv = TX * ((views[v].height + GS_TILE - 1) / GS_TILE);
+    const bool onchip = Tv <= HIST_MAX;
+    uint32_t k0, k1;
+    chunk_of(nv, k0, k1);
+    if (k0 >= k1) return;
+    if (onchip) {
+        for (int t = threadIdx.x; t < Tv; t += blockDim.x) hist[t] = 0u;
+        __syncthreads();
+        for (uint32_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+            const uint4 q3 = __ldg(reinterpret_cast<const uint4*>(rec + (int64_t)v * cap + k) + 3);
+            uint32_t x0, y0, nx, np;
+            rect_of(q3, x0, y0, nx, np);
+            for (uint32_t p = 0; p < np; ++p) atomicAdd(&hist[(y0 + p / nx) * TX + x0 + p % nx], 1u);
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < Tv; t += blockDim.x) {
+            const uint32_t c = hist[t];
+            hist[t] = c ? atomicAdd(&cursor[toff + t], c) : 0u;   // this chunk's base in bucket t
+        }
+        __syncthreads();
+    }
+    for (uint32_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
         const uint32_t slot = (uint32_t)((int64_t)v * cap + k);
         const uint4* q4 = reinterpret_cast<const uint4*>(rec + slot);
         const uint4 q2 = __ldg(q4 + 2), q3 = __ldg(q4 + 3);
         const uint4 ent = make_uint4(q2.w, slot, q3.x, 0u);   // bits(z), slot, gid
-        const uint32_t x0 = q3.z & 0xffffu, x1 = q3.z >> 16, y0 = q3.w & 0xffffu, y1 = q3.w >> 16;
-        const uint32_t nx = x1 - x0 + 1, npair = nx * (y1 - y0 + 1);
-        // batches of 4 independent atomics so their latencies overlap
-        for (uint32_t p0 = 0; p0 < npair; p0 += 4) {
+        uint32_t x0, y0, nx, np;
+        rect_of(q3, x0, y0, nx, np);
+        for (uint32_t p0 = 0; p0 < np; p0 += 4) {
             uint32_t pos[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t p = p0 + q;
-                if (p < npair) {
-                    const uint32_t ty = y0 + p / nx, tx = x0 + p % nx;
-                    pos[q] = atomicAdd(&cursor[toff + ty * TX + tx], 1u);
+                if (p < np) {
+                    const uint32_t t = (y0 + p / nx) * TX + x0 + p % nx;
+                    pos[q] = onchip ? atomicAdd(&hist[t], 1u) : atomicAdd(&cursor[toff + t], 1u);
                 }
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (p0 + q < npair) bucket[pos[q]] = ent;
+                if (p0 + q < np) bucket[pos[q]] = ent;
         }
     }
 }
@@ -394,25 +459,6 @@ mid_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ b
     }
 }
 
-// CTA-wide bitonic sort of n (power of two) 64-bit keys + 32-bit payloads in shared memory
-__device__ void smem_bitonic(uint64_t* sk, uint32_t* sv, uint32_t n) {
-    for (uint32_t size = 2; size <= n; size <<= 1) {
-        for (uint32_t d = size >> 1; d > 0; d >>= 1) {
-            for (uint32_t t = threadIdx.x; t < n / 2; t += blockDim.x) {
-                const uint32_t i = 2 * t - (t & (d - 1));   // lower index of the pair
-                const uint32_t j = i + d;
-                const bool up = (i & size) == 0;
-                const uint64_t a = sk[i], b = sk[j];
-                if ((a > b) == up) {
-                    sk[i] = b; sk[j] = a;
-                    const uint32_t tv = sv[i]; sv[i] = sv[j]; sv[j] = tv;
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-
 // merge sorted runs A = [a0, a0+na), B = [a0+na, a0+na+nb) of (key, val) into dst (unique keys)
 __device__ void cta_merge(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, uint64_t* __restrict__ dk,
                           uint32_t* __restrict__ dv, uint32_t a0, uint32_t na, uint32_t nb) {
@@ -435,9 +481,78 @@ __device__ void cta_merge(const uint64_t* __restrict__ sk, const uint32_t* __res
     }
 }
 
-// Long lists (> 512 pairs; dense areas and coarse pyramid levels): one CTA per
-// tile, runs of up to 8192 (depth_bits << 32 | gid, bucket index) pairs sorted
-// in shared memory, then merge-path merges in global memory.
+// Long lists (> 512 pairs; dense areas and coarse pyramid levels): one CTA of
+// 16 warps per tile.  Runs of up to 8192 (depth_bits << 32 | gid, bucket index)
+// pairs are sorted in shared memory as 512-element warp register sorts
+// (transposed bitonic, as in the warp path) followed by merge-path merges in
+// shared memory; lists longer than 8192 merge those runs in global memory.
+// Shared arrays are padded one slot every 16 elements so the transposed
+// (lane*16 + j) register loads are (at most) 2-way bank conflicted.
+__device__ __forceinline__ uint32_t pidx(uint32_t e) { return e + (e >> 4); }
+constexpr int RUN_PAD = SMEM_SORT_MAX + SMEM_SORT_MAX / 16;
+
+// merge sorted runs [a0, a0+na) and [a0+na, a0+na+nb) of padded shared arrays
+__device__ void smem_merge(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, uint64_t* __restrict__ dk,
+                           uint32_t* __restrict__ dv, uint32_t a0, uint32_t na, uint32_t nb) {
+    const uint32_t total = na + nb;
+    const uint32_t per = (total + blockDim.x - 1) / blockDim.x;
+    const uint32_t lo = min(total, threadIdx.x * per), hi = min(total, lo + per);
+    if (lo >= hi) return;
+    const uint32_t A = a0, B = a0 + na;
+    uint32_t ilo = lo > nb ? lo - nb : 0u, ihi = min(lo, na);
+    while (ilo < ihi) {
+        const uint32_t i = (ilo + ihi) >> 1;
+        if (sk[pidx(A + i)] < sk[pidx(B + lo - i - 1)]) ilo = i + 1; else ihi = i;
+    }
+    uint32_t i = ilo, j = lo - ilo;
+    for (uint32_t o = lo; o < hi; ++o) {
+        const bool takeA = j >= nb || (i < na && sk[pidx(A + i)] < sk[pidx(B + j)]);
+        const uint32_t src = takeA ? A + i : B + j;
+        dk[pidx(a0 + o)] = sk[pidx(src)];
+        dv[pidx(a0 + o)] = sv[pidx(src)];
+        if (takeA) ++i; else ++j;
+    }
+}
+
+// sort rl <= SMEM_SORT_MAX pairs already placed in (ak, av); returns 0 if the
+// result is in (ak, av), 1 if in (bk, bv)
+__device__ int smem_sort_run(uint64_t* ak, uint32_t* av, uint64_t* bk, uint32_t* bv, uint32_t rl) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    const uint32_t nrun = (rl + 511) / 512;
+    for (uint32_t r = warp; r < nrun; r += nwarp) {
+        uint64_t k[16];
+        uint32_t v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t e = r * 512 + lane * 16 + (uint32_t)j;
+            k[j] = e < rl ? ak[pidx(e)] : PAD_KEY;
+            v[j] = e < rl ? av[pidx(e)] : 0u;
+        }
+        warp_bitonic_t<16, true>(k, v, lane);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t e = r * 512 + lane * 16 + (uint32_t)j;
+            if (e < rl) { ak[pidx(e)] = k[j]; av[pidx(e)] = v[j]; }
+        }
+    }
+    __syncthreads();
+    int in_b = 0;
+    for (uint32_t width = 512; width < rl; width <<= 1) {
+        const uint64_t* sk = in_b ? bk : ak;
+        const uint32_t* sv = in_b ? bv : av;
+        uint64_t* dk = in_b ? ak : bk;
+        uint32_t* dv = in_b ? av : bv;
+        for (uint32_t a0 = 0; a0 < rl; a0 += 2 * width) {
+            const uint32_t na = min(width, rl - a0);
+            const uint32_t nb = a0 + na < rl ? min(width, rl - a0 - na) : 0u;
+            smem_merge(sk, sv, dk, dv, a0, na, nb);
+        }
+        __syncthreads();
+        in_b ^= 1;
+    }
+    return in_b;
+}
+
 __global__ void __launch_bounds__(BIG_THREADS)
 big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ bucket, uint64_t* __restrict__ ka,
                 uint32_t* __restrict__ va, uint64_t* __restrict__ kb, uint32_t* __restrict__ vb,
@@ -446,8 +561,10 @@ big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ b
                 const uint32_t* __restrict__ status) {
     if (*status) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
-    uint32_t* sv = reinterpret_cast<uint32_t*>(smem_raw + SMEM_SORT_MAX * sizeof(uint64_t));
+    uint64_t* sk0 = reinterpret_cast<uint64_t*>(smem_raw);
+    uint64_t* sk1 = sk0 + RUN_PAD;
+    uint32_t* sv0 = reinterpret_cast<uint32_t*>(sk1 + RUN_PAD);
+    uint32_t* sv1 = sv0 + RUN_PAD;
     const uint32_t nbig = big_count[1];
     for (uint32_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
         const uint32_t tile = big_list[bi];
@@ -455,31 +572,26 @@ big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ b
         const bool one_run = len <= SMEM_SORT_MAX;
         for (uint32_t r0 = 0; r0 < len; r0 += SMEM_SORT_MAX) {
             const uint32_t rl = min((uint32_t)SMEM_SORT_MAX, len - r0);
-            uint32_t n2 = 1;
-            while (n2 < rl) n2 <<= 1;
-            for (uint32_t e = threadIdx.x; e < n2; e += blockDim.x) {
-                if (e < rl) {
-                    const uint4 b = bucket[s + r0 + e];
-                    sk[e] = ((uint64_t)b.x << 32) | b.z;
-                    sv[e] = r0 + e;
-                } else {
-                    sk[e] = PAD_KEY;
-                    sv[e] = 0u;
-                }
+            for (uint32_t e = threadIdx.x; e < rl; e += blockDim.x) {
+                const uint4 b = bucket[s + r0 + e];
+                sk0[pidx(e)] = ((uint64_t)b.x << 32) | b.z;
+                sv0[pidx(e)] = r0 + e;
             }
             __syncthreads();
-            smem_bitonic(sk, sv, n2);
+            const int in_b = smem_sort_run(sk0, sv0, sk1, sv1, rl);
+            const uint64_t* rk = in_b ? sk1 : sk0;
+            const uint32_t* rv = in_b ? sv1 : sv0;
             if (one_run) {
                 for (uint32_t e = threadIdx.x; e < rl; e += blockDim.x) {
-                    const uint4 b = bucket[s + sv[e]];
+                    const uint4 b = bucket[s + rv[pidx(e)]];
                     out[s + e] = b.y;
                     if (ogid) ogid[s + e] = b.z;
                     if (dbg) dbg[s + e] = ((uint64_t)tile << 32) | b.x;
                 }
             } else {
                 for (uint32_t e = threadIdx.x; e < rl; e += blockDim.x) {
-                    ka[s + r0 + e] = sk[e];
-                    va[s + r0 + e] = sv[e];
+                    ka[s + r0 + e] = rk[pidx(e)];
+                    va[s + r0 + e] = rv[pidx(e)];
                 }
             }
             __syncthreads();
@@ -538,16 +650,29 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * T, s);
     cudaMemsetAsync(w.big_count, 0, 2 * sizeof(uint32_t), s);
 
-    const int64_t blocks_per_view = std::min<int64_t>((cap + 255) / 256, std::max(1, 4 * num_sms() / n_views + 1));
-    dim3 rgrid((unsigned)std::max<int64_t>(1, blocks_per_view), (unsigned)n_views);
-    count_kernel<<<rgrid, 256, 0, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.counts, proj->status);
+    // chunks of >= 1024 records, ~2 CTAs per SM over the whole batch
+    const int64_t blocks_per_view =
+        std::max<int64_t>(1, std::min<int64_t>((cap + 1023) / 1024, (2 * num_sms() + n_views - 1) / n_views));
+    dim3 rgrid((unsigned)blocks_per_view, (unsigned)n_views);
+    int max_tiles = 0;
+    for (int i = 0; i < n_views; ++i)
+        max_tiles = std::max(max_tiles, tiles_x(views_host[i]) * tiles_y(views_host[i]));
+    const int hist_smem = (int)sizeof(uint32_t) * std::min(max_tiles, HIST_MAX);
+    static bool hist_attr = false;
+    if (!hist_attr) {
+        cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_MAX * 4);
+        cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_MAX * 4);
+        hist_attr = true;
+    }
+    count_kernel<<<rgrid, BIN_THREADS, hist_smem, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.counts, proj->status);
     if ((st = check_launch("count_kernel")) != GS_OK) return st;
     const int64_t nb = (T + SCAN_TILE - 1) / SCAN_TILE;
     scan_reduce_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(w.counts, T, w.block_sums);
     scan_blocks_kernel<<<1, SCAN_THREADS, 0, s>>>(w.block_sums, nb, out->n_pairs, out->pair_capacity, proj->status);
     scan_down_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(w.counts, T, w.block_sums, out->ranges, w.cursor);
     if ((st = check_launch("scan kernels")) != GS_OK) return st;
-    scatter_kernel<<<rgrid, 256, 0, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.cursor, w.bucket, proj->status);
+    scatter_kernel<<<rgrid, BIN_THREADS, hist_smem, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.cursor, w.bucket,
+                                                          proj->status);
     if ((st = check_launch("scatter_kernel")) != GS_OK) return st;
     warp_sort_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(out->ranges, T, w.bucket, out->sorted_rec,
                                                              out->sorted_gid, out->sorted_key, w.big_count,
@@ -556,12 +681,12 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
                                                   out->sorted_key, w.big_count, w.mid_list, proj->status);
     if ((st = check_launch("warp_sort_kernel")) != GS_OK) return st;
     static bool attr_set = false;
-    const int smem = SMEM_SORT_MAX * (int)(sizeof(uint64_t) + sizeof(uint32_t));
+    const int smem = 2 * RUN_PAD * (int)(sizeof(uint64_t) + sizeof(uint32_t));
     if (!attr_set) {
         cudaFuncSetAttribute(big_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
-    big_sort_kernel<<<2 * num_sms(), BIG_THREADS, smem, s>>>(out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb,
+    big_sort_kernel<<<num_sms(), BIG_THREADS, smem, s>>>(out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb,
                                                              out->sorted_rec,
                                                          out->sorted_gid, out->sorted_key, w.big_count, w.big_list,
                                                          proj->status);
