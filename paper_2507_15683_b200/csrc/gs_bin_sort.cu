@@ -32,8 +32,8 @@ constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_PER_THREAD = 4;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_PER_THREAD;
 constexpr int WARP_SORT_MAX = 512;      // 16 keys per lane
-constexpr int SMEM_SORT_MAX = 8192;     // run length sorted on chip (2 padded buffers: 209 KB)
-constexpr int BIG_THREADS = 512;
+constexpr int SMEM_SORT_MAX = 2048;     // run length sorted on chip (2 padded buffers: 52 KB)
+constexpr int BIG_THREADS = 128;        // 4 warps: one 512-element register run each
 constexpr uint64_t PAD_KEY = ~0ull;
 
 struct BinWs {
@@ -482,10 +482,10 @@ __device__ void cta_merge(const uint64_t* __restrict__ sk, const uint32_t* __res
 }
 
 // Long lists (> 512 pairs; dense areas and coarse pyramid levels): one CTA of
-// 16 warps per tile.  Runs of up to 8192 (depth_bits << 32 | gid, bucket index)
+// 4 warps per tile.  Runs of up to 2048 (depth_bits << 32 | gid, bucket index)
 // pairs are sorted in shared memory as 512-element warp register sorts
 // (transposed bitonic, as in the warp path) followed by merge-path merges in
-// shared memory; lists longer than 8192 merge those runs in global memory.
+// shared memory; lists longer than 2048 merge those runs in global memory.
 // Shared arrays are padded one slot every 16 elements so the transposed
 // (lane*16 + j) register loads are (at most) 2-way bank conflicted.
 __device__ __forceinline__ uint32_t pidx(uint32_t e) { return e + (e >> 4); }
@@ -686,7 +686,7 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
         cudaFuncSetAttribute(big_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
-    big_sort_kernel<<<num_sms(), BIG_THREADS, smem, s>>>(out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb,
+    big_sort_kernel<<<4 * num_sms(), BIG_THREADS, smem, s>>>(out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb,
                                                              out->sorted_rec,
                                                          out->sorted_gid, out->sorted_key, w.big_count, w.big_list,
                                                          proj->status);
