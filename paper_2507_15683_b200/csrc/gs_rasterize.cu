@@ -36,7 +36,7 @@ constexpr int RT_THREADS = (NCW + 1) * 32;
 constexpr int SE = 32;                 // entries per stage (one ballot)
 constexpr int NST = 8;                 // ring stages
 constexpr int WB_STRIDE = 40;          // weight-buffer row stride (conflict-free A fragments)
-constexpr int WB_ROWS = 40;            // pending (< 8) + one ballot (<= 32) entries
+constexpr int WB_ROWS = 8;             // one tensor-core k-step of weights
 constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -93,7 +93,8 @@ struct RasterSmem {
     float4 rec[NST][SE + 1][4];                    // 64-byte records; row SE = null record (opacity 0)
     float feat[D > 0 ? NST : 1][D > 0 ? SE + 1 : 1][FS];
     alignas(16) float wbuf[D > 0 ? NCW : 1][WB_ROWS][WB_STRIDE]; // per-warp compacted weights [k][pixel]
-    alignas(16) int ent[NCW][WB_ROWS];               // per-warp compacted entry indices
+    alignas(16) int ent[NCW][SE + 2];                // per-warp compacted ballot list (flat ring rows)
+    int kent[NCW][WB_ROWS];                          // ring row of each pending weight row
     StageMeta meta[NST];
     uint64_t full[NST];
     uint64_t empty[NST];
@@ -136,7 +137,7 @@ __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, f
 // producer warp runs ahead across tile boundaries so the consumers never wait
 // for a tile's first records.
 template <int D>
-__global__ void __launch_bounds__(RT_THREADS, (D > 32 ? 1 : 2))
+__global__ void __launch_bounds__(RT_THREADS, (D > 32 ? 1 : (D > 0 ? 3 : 4)))
 rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record* __restrict__ rec,
                  const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ sorted_gid,
                  const uint32_t* __restrict__ ranges, uint32_t n_tiles, const float* __restrict__ feat,
@@ -270,8 +271,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                         alo[m][i] = __float_as_uint(av[i] - __uint_as_float(ahi[m][i]));   // exact remainder
                     }
                 }
-                const float* f0 = &sm.feat[0][0][0] + sm.ent[warp][k0 + t4] * RasterSmem<D>::FS;
-                const float* f1 = &sm.feat[0][0][0] + sm.ent[warp][k0 + t4 + 4] * RasterSmem<D>::FS;
+                const float* f0 = &sm.feat[0][0][0] + sm.kent[warp][k0 + t4] * RasterSmem<D>::FS;
+                const float* f1 = &sm.feat[0][0][0] + sm.kent[warp][k0 + t4 + 4] * RasterSmem<D>::FS;
 #pragma unroll
                 for (int n = 0; n < NTP; ++n) {
                     const int ch = n * 8 + g;
@@ -310,7 +311,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
         if constexpr (D > 0) {
             if (pend > 0) {
                 for (int r = pend; r < 8; ++r) sm.wbuf[warp][r][lane] = 0.f;
-                if (lane < (uint32_t)(8 - pend)) sm.ent[warp][pend + lane] = SE;   // null row
+                if (lane < (uint32_t)(8 - pend)) sm.kent[warp][pend + lane] = SE;   // null row
                 __syncwarp();
                 mma_block(0, 8);
                 __syncwarp();
@@ -358,13 +359,12 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             const uint32_t msk = __ballot_sync(0xffffffffu, hit);
             const int n = __popc(msk);
             if (n > 0) {
-                const int base = D > 0 ? pend : 0;
                 // compacted in-order entry list; an odd tail is padded with the null record
-                if (hit) sm.ent[warp][base + __popc(msk & ((1u << lane) - 1u))] = flat0 + j;
-                if (lane == 0 && (n & 1)) sm.ent[warp][base + n] = flat0 + SE;
+                if (hit) sm.ent[warp][__popc(msk & ((1u << lane) - 1u))] = flat0 + j;
+                if (lane == 0 && (n & 1)) sm.ent[warp][n] = flat0 + SE;
                 __syncwarp();
 #pragma unroll 1
-                for (int i = base; i < base + n; i += 2) {
+                for (int i = 0; i < n; i += 2) {
                     // two entries per iteration: independent alphas (ILP 2), transmittance in list order
                     const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i]);   // i is even
                     const float4* r1 = recf + 4 * kk.x;
@@ -376,25 +376,17 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     a2 = done ? 0.0f : a2;
                     const float w2 = blend(a2, r2[2]);
                     if constexpr (D > 0) {
-                        sm.wbuf[warp][i][lane] = w1;
-                        sm.wbuf[warp][i + 1][lane] = w2;
-                    }
-                }
-                if constexpr (D > 0) {
-                    if (pend == 0) hold = s;
-                    pend = base + ((n + 1) & ~1);          // rows written (even)
-                    const int full = pend & ~7;
-                    if (full > 0) {
-                        __syncwarp();
-                        mma_block(0, full);
-                        __syncwarp();
-                        // move the < 8 leftover rows (all from this stage) to the front
-                        const int left = pend - full;
-                        for (int r = 0; r < left; ++r) sm.wbuf[warp][r][lane] = sm.wbuf[warp][full + r][lane];
-                        if (lane < (uint32_t)left) sm.ent[warp][lane] = sm.ent[warp][full + lane];
-                        __syncwarp();
-                        pend = left;
-                        hold = s;
+                        if (pend == 0) hold = s;
+                        sm.wbuf[warp][pend][lane] = w1;
+                        sm.wbuf[warp][pend + 1][lane] = w2;
+                        if (lane == 0) { sm.kent[warp][pend] = kk.x; sm.kent[warp][pend + 1] = kk.y; }
+                        pend += 2;
+                        if (pend == WB_ROWS) {             // a full k-step: feed the tensor cores
+                            __syncwarp();
+                            mma_block(0, WB_ROWS);
+                            __syncwarp();
+                            pend = 0;
+                        }
                     }
                 }
                 warp_done = __all_sync(0xffffffffu, done);
