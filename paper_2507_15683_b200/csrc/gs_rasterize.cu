@@ -137,7 +137,7 @@ __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, f
 // producer warp runs ahead across tile boundaries so the consumers never wait
 // for a tile's first records.
 template <int D>
-__global__ void __launch_bounds__(RT_THREADS, (D > 32 ? 1 : (D > 0 ? 3 : 4)))
+__global__ void __launch_bounds__(RT_THREADS, (D > 32 ? 1 : (D > 0 ? 2 : 4)))
 rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record* __restrict__ rec,
                  const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ sorted_gid,
                  const uint32_t* __restrict__ ranges, uint32_t n_tiles, const float* __restrict__ feat,
