@@ -58,8 +58,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+// 16-B global->shared copy that asks L2 to keep the line (records and feature rows
+// are re-read by the ~4 neighbouring tiles a Gaussian overlaps)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint64_t policy) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+                 "l"(policy)
+                 : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
 }
 // the mbarrier receives one arrival when all prior cp.async of this thread have landed
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
@@ -191,6 +200,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             }
         };
         tile_begin(blockIdx.x);
+        const uint64_t pol = l2_evict_last_policy();
         uint32_t slot[SE / 32], gid[SE / 32];
         uint32_t c0 = rs;
         int cnt = end ? 0 : (int)min((uint32_t)SE, re - c0);
@@ -218,11 +228,11 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 if (j < ccnt) {
                     const float4* src = reinterpret_cast<const float4*>(rec + slot[q]);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) cp_async16(&sm.rec[buf][j][e], src + e);
+                    for (int e = 0; e < 4; ++e) cp_async16(&sm.rec[buf][j][e], src + e, pol);
                     if constexpr (D > 0) {
                         const float4* fs = reinterpret_cast<const float4*>(feat + (int64_t)gid[q] * D);
 #pragma unroll
-                        for (int e = 0; e < D / 4; ++e) cp_async16(&sm.feat[buf][j][e * 4], fs + e);
+                        for (int e = 0; e < D / 4; ++e) cp_async16(&sm.feat[buf][j][e * 4], fs + e, pol);
                     }
                 }
             }
@@ -401,11 +411,13 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             const int64_t po = V->pix_offset;
             if (inside) {
                 const int64_t loc = (int64_t)py * W + px;
-                out_rgb[3 * po + loc] = C0;
-                out_rgb[3 * po + HW + loc] = C1;
-                out_rgb[3 * po + 2 * HW + loc] = C2;
-                out_depth[po + loc] = Dz;
-                out_alpha[po + loc] = 1.0f - T;
+                // streaming stores (evict-first in L2): the 37-plane output stream must not
+                // evict the records / feature rows that neighbouring tiles re-read
+                __stcs(&out_rgb[3 * po + loc], C0);
+                __stcs(&out_rgb[3 * po + HW + loc], C1);
+                __stcs(&out_rgb[3 * po + 2 * HW + loc], C2);
+                __stcs(&out_depth[po + loc], Dz);
+                __stcs(&out_alpha[po + loc], 1.0f - T);
             }
             if constexpr (D > 0) {
                 // accumulator (a, n, i): pixel (sx + g, sy + 2a + (i >> 1)), channel 8n + 2 t4 + (i & 1);
@@ -422,7 +434,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                             float* q = fbase + (int64_t)fy * W + ((i & 1) ? HW : 0);
 #pragma unroll
                             for (int n = 0; n < NTP; ++n) {
-                                if (n * 8 + 2 * t4 + (i & 1) < D) *q = acc[a][n][i];
+                                if (n * 8 + 2 * t4 + (i & 1) < D) __stcs(q, acc[a][n][i]);
                                 q += step8;
                             }
                         }
