@@ -171,6 +171,8 @@ typedef struct gs_bins {
     uint64_t* sorted_key;    /* optional [pair_capacity]: (tile in batch << 32) | depth_bits */
     uint32_t* sorted_gid;    /* optional [pair_capacity]: gid of each pair (lets gs_rasterize fetch
                                 feature rows without a dependent record load) */
+    uint32_t* tile_sched;    /* optional [1]: scratch counter of gs_rasterize's dynamic tile
+                                scheduler (zeroed by gs_rasterize on its stream); NULL = static */
 } gs_bins;
 
 typedef struct gs_images {

@@ -38,6 +38,7 @@ constexpr int NST = 8;                 // ring stages
 constexpr int WB_STRIDE = 40;          // weight-buffer row stride (conflict-free A fragments)
 constexpr int WB_ROWS = 8;             // one tensor-core k-step of weights
 constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
+constexpr uint32_t SCHED_CHUNK = 2;    // tiles per scheduler claim
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -142,14 +143,15 @@ __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, f
     return ((power > 0.0f) || (alpha < P.alpha_min)) ? 0.0f : alpha;
 }
 
-// Persistent kernel: CTA c renders tiles c, c + grid, c + 2 grid, ...  The
-// producer warp runs ahead across tile boundaries so the consumers never wait
-// for a tile's first records.
+// Persistent kernel: each CTA renders a sequence of tiles handed out in order by
+// a dynamic scheduler.  The producer warp runs ahead across tile boundaries so
+// the consumers never wait for a tile's first records.
 template <int D>
 __global__ void __launch_bounds__(RT_THREADS, (D > 32 ? 1 : (D > 0 ? 2 : 4)))
 rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record* __restrict__ rec,
                  const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ sorted_gid,
-                 const uint32_t* __restrict__ ranges, uint32_t n_tiles, const float* __restrict__ feat,
+                 const uint32_t* __restrict__ ranges, uint32_t n_tiles, uint32_t* __restrict__ tile_sched,
+                 const float* __restrict__ feat,
                  gs_params P, float* __restrict__ out_rgb, float* __restrict__ out_depth,
                  float* __restrict__ out_alpha, float* __restrict__ out_feat, const uint32_t* __restrict__ status) {
     if (*status) return;
@@ -177,6 +179,25 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
         uint32_t tile = blockIdx.x, rs = 0, re = 0, k = 0, nst = 1;
         int view = 0;
         bool end = false;
+        // Dynamic tile scheduler: chunks of SCHED_CHUNK consecutive tiles are handed
+        // out in order from a global counter, so all CTAs work on one compact window
+        // of tiles (records / feature rows stay L2-resident); the next chunk is
+        // claimed one chunk ahead to hide the atomic's latency.  CTA c's first chunk
+        // is static.  Without a counter: static round-robin chunks.
+        uint32_t ch_base = blockIdx.x * SCHED_CHUNK, ch_i = 0;
+        auto claim = [&]() -> uint32_t {
+            uint32_t b = 0;
+            if (lane == 0) b = atomicAdd(tile_sched, SCHED_CHUNK);
+            return gridDim.x * SCHED_CHUNK + __shfl_sync(0xffffffffu, b, 0);
+        };
+        uint32_t ch_next = tile_sched ? claim() : ch_base + gridDim.x * SCHED_CHUNK;
+        auto next_tile = [&]() -> uint32_t {
+            if (++ch_i < SCHED_CHUNK) return ch_base + ch_i;
+            ch_base = ch_next;
+            ch_i = 0;
+            ch_next = tile_sched ? (ch_base < n_tiles ? claim() : ch_base) : ch_base + gridDim.x * SCHED_CHUNK;
+            return ch_base;
+        };
         auto tile_begin = [&](uint32_t t) {
             tile = t;
             end = t >= n_tiles;
@@ -199,7 +220,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 gd[q] = (D > 0 && j < cnt) ? (sorted_gid ? __ldg(&sorted_gid[c0 + j]) : __ldg(&rec[sl[q]].gid)) : 0u;
             }
         };
-        tile_begin(blockIdx.x);
+        tile_begin(ch_base);
         const uint64_t pol = l2_evict_last_policy();
         uint32_t slot[SE / 32], gid[SE / 32];
         uint32_t c0 = rs;
@@ -216,7 +237,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             // advance the iterator and prefetch the next stage's indices
             uint32_t nslot[SE / 32], ngid[SE / 32];
             if (!cend) {
-                if (++k == nst) tile_begin(tile + gridDim.x);
+                if (++k == nst) tile_begin(next_tile());
                 c0 = rs + k * SE;
                 cnt = end ? 0 : (int)min((uint32_t)SE, re - c0);
                 load_idx(c0, cnt, nslot, ngid);
@@ -460,10 +481,13 @@ gs_status launch(const gs_scene* scene, const gs_projected* proj, const gs_bins*
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rasterize_kernel<D>, RT_THREADS, smem);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
-    const int64_t grid = std::min<int64_t>(T, (int64_t)num_sms() * blocks_per_sm);
+    const int64_t grid =
+        std::min<int64_t>((T + SCHED_CHUNK - 1) / SCHED_CHUNK, (int64_t)num_sms() * blocks_per_sm);
     if (grid <= 0) return GS_OK;
+    if (bins->tile_sched) cudaMemsetAsync(bins->tile_sched, 0, sizeof(uint32_t), s);
     rasterize_kernel<D><<<(unsigned)grid, RT_THREADS, smem, s>>>(
-        views_dev, n_views, proj->rec, bins->sorted_rec, bins->sorted_gid, bins->ranges, (uint32_t)T, scene->feat,
+        views_dev, n_views, proj->rec, bins->sorted_rec, bins->sorted_gid, bins->ranges, (uint32_t)T, bins->tile_sched,
+        scene->feat,
         *P, out->rgb, out->depth, out->alpha, out->feat, proj->status);
     return check_launch("rasterize_kernel");
 }

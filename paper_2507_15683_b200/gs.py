@@ -58,7 +58,8 @@ class gs_projected(ctypes.Structure):
 
 class gs_bins(ctypes.Structure):
     _fields_ = [("ranges", ctypes.c_void_p), ("sorted_rec", ctypes.c_void_p), ("pair_capacity", ctypes.c_int64),
-                ("n_pairs", ctypes.c_void_p), ("sorted_key", ctypes.c_void_p), ("sorted_gid", ctypes.c_void_p)]
+                ("n_pairs", ctypes.c_void_p), ("sorted_key", ctypes.c_void_p), ("sorted_gid", ctypes.c_void_p),
+                ("tile_sched", ctypes.c_void_p)]
 
 
 class gs_images(ctypes.Structure):
@@ -229,9 +230,11 @@ class Bins:
         self.n_pairs = torch.zeros(1, dtype=torch.int64, device=device)
         self.sorted_key = torch.empty(self.pair_capacity, dtype=torch.int64, device=device) if debug_keys else None
         self.sorted_gid = torch.empty(self.pair_capacity, dtype=torch.int32, device=device) if with_gid else None
+        self.tile_sched = torch.zeros(1, dtype=torch.int32, device=device)
         s = gs_bins()
         s.ranges, s.sorted_rec, s.pair_capacity = _ptr(self.ranges), _ptr(self.sorted_rec), self.pair_capacity
         s.n_pairs, s.sorted_key, s.sorted_gid = _ptr(self.n_pairs), _ptr(self.sorted_key), _ptr(self.sorted_gid)
+        s.tile_sched = _ptr(self.tile_sched)
         self.struct = s
 
 
