@@ -34,7 +34,7 @@ namespace {
 constexpr int NCW = 8;                 // consumer warps
 constexpr int RT_THREADS = (NCW + 1) * 32;
 constexpr int SE = 32;                 // entries per stage (one ballot)
-constexpr int NST = 4;                 // ring stages
+constexpr int NST = 8;                 // ring stages
 constexpr int WB_STRIDE = 40;          // weight-buffer row stride (conflict-free A fragments)
 constexpr int WB_ROWS = 8;             // one tensor-core k-step of weights
 constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
@@ -105,9 +105,6 @@ struct RasterSmem {
     alignas(16) float wbuf[D > 0 ? NCW : 1][WB_ROWS][WB_STRIDE]; // per-warp compacted weights [k][pixel]
     alignas(16) int ent[NCW][SE + 2];                // per-warp compacted ballot list (flat ring rows)
     int kent[NCW][WB_ROWS];                          // ring row of each pending weight row
-    // tensor-core feature accumulators (mma C fragments) parked in shared memory between
-    // k-steps, so the consumer loop runs in fewer registers (3 CTAs / SM)
-    float4 acc[D > 0 ? NCW : 1][2][D > 0 ? (D + 7) / 8 : 1][32];
     StageMeta meta[NST];
     uint64_t full[NST];
     uint64_t empty[NST];
@@ -150,7 +147,7 @@ __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, f
 // a dynamic scheduler.  The producer warp runs ahead across tile boundaries so
 // the consumers never wait for a tile's first records.
 template <int D>
-__global__ void __launch_bounds__(RT_THREADS, (D > 32 ? 2 : (D > 0 ? 3 : 4)))
+__global__ void __launch_bounds__(RT_THREADS, (D > 32 ? 1 : (D > 0 ? 2 : 4)))
 rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record* __restrict__ rec,
                  const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ sorted_gid,
                  const uint32_t* __restrict__ ranges, uint32_t n_tiles, uint32_t* __restrict__ tile_sched,
@@ -281,6 +278,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     // ---------------------------------------------------------------- consumers
     const int g = (int)(lane >> 2), t4 = (int)(lane & 3u);
     constexpr int NTP = D > 0 ? (D + 7) / 8 : 1;
+    float acc[2][NTP][4];
     // per-tile state
     const gs_view* V = nullptr;
     int W = 0, H = 0, sx = 0, sy = 0, px = 0, py = 0;
@@ -312,11 +310,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     const uint32_t b0 = to_tf32(ch < D ? f0[ch] : 0.f), b1 = to_tf32(ch < D ? f1[ch] : 0.f);
 #pragma unroll
                     for (int m = 0; m < 2; ++m) {
-                        const float4 c4 = sm.acc[warp][m][n][lane];
-                        float c[4] = {c4.x, c4.y, c4.z, c4.w};
-                        mma_tf32(c, ahi[m], b0, b1);
-                        mma_tf32(c, alo[m], b0, b1);
-                        sm.acc[warp][m][n][lane] = make_float4(c[0], c[1], c[2], c[3]);
+                        mma_tf32(acc[m][n], ahi[m], b0, b1);
+                        mma_tf32(acc[m][n], alo[m], b0, b1);
                     }
                 }
             }
@@ -378,12 +373,10 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             T = 1.0f; C0 = C1 = C2 = Dz = 0.f;
             done = !inside;
             warp_done = __all_sync(0xffffffffu, done);
-            if constexpr (D > 0) {
 #pragma unroll
-                for (int a = 0; a < 2; ++a)
+            for (int a = 0; a < 2; ++a)
 #pragma unroll
-                    for (int n = 0; n < NTP; ++n) sm.acc[warp][a][n][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
+                for (int n = 0; n < NTP; ++n) acc[a][n][0] = acc[a][n][1] = acc[a][n][2] = acc[a][n][3] = 0.f;
         }
         if (!warp_done && m.cnt > 0) {
             const int flat0 = buf * (SE + 1);
@@ -462,9 +455,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                             float* q = fbase + (int64_t)fy * W + ((i & 1) ? HW : 0);
 #pragma unroll
                             for (int n = 0; n < NTP; ++n) {
-                                const float4 c4 = sm.acc[warp][a][n][lane];
-                                const float cv = i == 0 ? c4.x : i == 1 ? c4.y : i == 2 ? c4.z : c4.w;
-                                if (n * 8 + 2 * t4 + (i & 1) < D) __stcs(q, cv);
+                                if (n * 8 + 2 * t4 + (i & 1) < D) __stcs(q, acc[a][n][i]);
                                 q += step8;
                             }
                         }
