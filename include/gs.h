@@ -160,6 +160,11 @@ typedef struct gs_projected {
     uint64_t* diag;          /* [4] += near, transparent, degenerate, off-screen (Gaussians
                                 skipped by the block cull are not visited and not counted) */
     uint32_t* status;        /* [1] GS_STATUS_* bits; caller zeroes before the batch */
+    unsigned long long* contrib; /* optional [n_views * rec_capacity]: per record, the sum over all
+                                    pixels of its blend weight w (N1, the forward visibility criterion
+                                    of SPEC S:180), in units of 2^-32; zeroed and written by
+                                    gs_rasterize when non-NULL (order-independent fixed point, so
+                                    run-to-run deterministic) */
 } gs_projected;
 
 typedef struct gs_bins {
@@ -258,6 +263,30 @@ gs_status gs_rasterize(const gs_scene* scene, const gs_projected* proj, const gs
  */
 gs_status gs_backproject(const gs_images* in, const gs_view* views_host, const gs_view* views_dev,
                          int32_t n_views, float a_min, float* xyz, uint8_t* valid, void* stream);
+
+/*
+ * gs_visibility_score -- N1: Alg. 1 render-visibility check with
+ * projection filtering and significance scoring (Eq. 4-6,
+ * P:174-185) for every record of the batch.  Needs out->contrib from
+ * gs_rasterize.
+ *   M^r = contrib > eps (the forward criterion; eps default 1e-6),
+ *   M^i = 0 <= u < W and 0 <= v < H (Alg. 1 l.17), visible = M^i and M^r;
+ *   visible[slot] = 1/0 for each record slot (the (U', V') of Alg. 1 are the
+ *   records' u, v where visible), n_visible[v] = count per view;
+ *   count[gid] += 1 per view in which gid is visible (Eq. 6's M);
+ *   if fmaps != NULL: score_sum[gid] += cos(f_gid, F^t_v(cell)) (Eq. 4-5) as
+ *   signed 2^-32 fixed point (two's complement in a u64), with F^t_v the view's
+ *   target feature map [D][ceil(H/stride)][ceil(W/stride)] (maps of all views
+ *   concatenated in view order) sampled at the nearest cell
+ *   (floor((u + 0.5)/stride), floor((v + 0.5)/stride)) (reading Q27); the
+ *   cosine of a zero vector is 0 (Q28).  S(g) = score_sum / count (Eq. 6) is
+ *   formed by the caller.  n_visible is overwritten; count and score_sum
+ *   accumulate (the caller zeroes them once for a multi-batch pass).
+ */
+gs_status gs_visibility_score(const gs_projected* proj, const gs_view* views_host, const gs_view* views_dev,
+                              int32_t n_views, float eps, const float* feat /* scene [N][D] */, int32_t feat_dim,
+                              const float* fmaps, int32_t stride, uint8_t* visible, uint32_t* n_visible,
+                              unsigned long long* score_sum, uint32_t* count, void* stream);
 
 #ifdef __cplusplus
 }

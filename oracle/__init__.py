@@ -153,19 +153,20 @@ def _feat(scene_or_feat, D):
 
 
 def composite(view, rec, keys, feat=None, params: Optional[Params] = None) -> Dict[str, np.ndarray]:
-    """O12 + O14 over the binned lists."""
+    """O12 + O14 over the binned lists (+ N1 per-record contribution sums, fp64)."""
     params = params or Params()
     D = 0 if feat is None else int(feat.shape[1])
     rgb, depth, alpha, F, flags = _alloc_images(view, D)
     counters = np.zeros(2, np.int64)
+    contrib = np.zeros(max(1, len(rec["gid"])), np.float64)
     vc, pc = _view_c(view), params.c()
     lib().oracle_composite(ctypes.byref(vc), ctypes.byref(pc), _p(_c32(rec["u"])), _p(_c32(rec["v"])),
                            _p(_c32(rec["conic"])), _p(_c32(rec["opacity"])), _p(_c32(rec["rgb"])),
                            _p(_c32(rec["z"])), _p(np.ascontiguousarray(rec["gid"], np.int32)), _p(_feat(feat, D)),
                            ctypes.c_int32(D), _p(keys["rec"]), _p(keys["ranges"]), _p(rgb), _p(depth), _p(alpha),
-                           _p(F), _p(flags), _p(counters))
+                           _p(F), _p(flags), _p(counters), _p(contrib))
     return dict(rgb=rgb, depth=depth, alpha=alpha, feat=F, flags=flags, evals=int(counters[0]),
-                blends=int(counters[1]))
+                blends=int(counters[1]), contrib=contrib[:len(rec["gid"])])
 
 
 def brute_force(view, rec, feat=None, params: Optional[Params] = None) -> Dict[str, np.ndarray]:
@@ -175,13 +176,14 @@ def brute_force(view, rec, feat=None, params: Optional[Params] = None) -> Dict[s
     rgb, depth, alpha, F, flags = _alloc_images(view, D)
     vc, pc = _view_c(view), params.c()
     cnt = len(rec["gid"])
+    contrib = np.zeros(max(1, cnt), np.float64)
     lib().oracle_brute_force(ctypes.byref(vc), ctypes.byref(pc), ctypes.c_int64(cnt), _p(_c32(rec["u"])),
                              _p(_c32(rec["v"])), _p(_c32(rec["conic"])), _p(_c32(rec["opacity"])),
                              _p(_c32(rec["rgb"])), _p(_c32(rec["z"])),
                              _p(np.ascontiguousarray(rec["gid"], np.int32)),
                              _p(np.ascontiguousarray(rec["rect"], np.int32)), _p(_feat(feat, D)), ctypes.c_int32(D),
-                             _p(rgb), _p(depth), _p(alpha), _p(F), _p(flags))
-    return dict(rgb=rgb, depth=depth, alpha=alpha, feat=F, flags=flags)
+                             _p(rgb), _p(depth), _p(alpha), _p(F), _p(flags), _p(contrib))
+    return dict(rgb=rgb, depth=depth, alpha=alpha, feat=F, flags=flags, contrib=contrib[:cnt])
 
 
 def backproject(view, depth, alpha, a_min: float = 0.5, flags=None):
@@ -205,6 +207,34 @@ def render(scene, view, params: Optional[Params] = None, a_min: Optional[float] 
     if a_min is not None:
         xyz, valid, fl = backproject(view, img["depth"], img["alpha"], a_min, img["flags"])
         out.update(xyz=xyz, valid=valid, flags=fl)
+    return out
+
+
+def visibility_score(view, rec, contrib, n_gauss: int, eps: float = 1e-6, feat=None, fmap=None, stride: int = 1,
+                     score_sum=None, count=None):
+    """N1 for one view: Alg. 1 visibility (M = M^i and M^r) of every record and
+    Eq. 4-5 accumulation into score_sum / count (arrays over all Gaussians,
+    updated in place and returned).  fmap: [D][ceil(H/s)][ceil(W/s)] or None."""
+    cnt = len(rec["gid"])
+    D = 0 if feat is None else int(feat.shape[1])
+    visible = np.zeros(max(1, cnt), np.uint8)
+    score_sum = np.zeros(n_gauss, np.float64) if score_sum is None else score_sum
+    count = np.zeros(n_gauss, np.int64) if count is None else count
+    vc = _view_c(view)
+    lib().oracle_visibility_score(ctypes.byref(vc), ctypes.c_int64(cnt), _p(_c32(rec["u"])), _p(_c32(rec["v"])),
+                                  _p(np.ascontiguousarray(rec["gid"], np.int32)),
+                                  _p(np.ascontiguousarray(contrib, np.float64)), ctypes.c_double(eps),
+                                  _p(_feat(feat, D)), ctypes.c_int32(D),
+                                  None if fmap is None else _p(_c32(fmap)), ctypes.c_int32(stride),
+                                  _p(visible), _p(score_sum), _p(count))
+    return visible[:cnt], score_sum, count
+
+
+def final_scores(score_sum, count):
+    """Eq. 6: S(g_j) = S(G_j) / M; -inf where M = 0."""
+    out = np.full(score_sum.shape, -np.inf)
+    m = count > 0
+    out[m] = score_sum[m] / count[m]
     return out
 
 

@@ -352,7 +352,7 @@ const double FLAG_ALPHA_REL = 1.0 / 262144.0;
 const double FLAG_T_REL = 1.0 / 4096.0;
 
 void composite_pixel(const Records& rc, const or_params* P, int32_t pxi, int32_t pyi,
-                     const uint32_t* list, int64_t len, PixelOut& o) {
+                     const uint32_t* list, int64_t len, PixelOut& o, double* contrib) {
     const float pxf = (float)pxi, pyf = (float)pyi;
     float T = 1.0f;
     o.C[0] = o.C[1] = o.C[2] = 0.0;
@@ -392,6 +392,7 @@ void composite_pixel(const Records& rc, const or_params* P, int32_t pxi, int32_t
             for (int c = 0; c < rc.D; ++c) o.F[c] += (double)w * f[c];
         }
         o.blends++;
+        if (contrib) contrib[i] += (double)w;   // N1: per-Gaussian accumulated blend weight
         // 8. T = Tn
         T = Tn;
     }
@@ -412,7 +413,8 @@ void oracle_composite(const or_view* V, const or_params* P, const float* u, cons
                       const float* conic, const float* opac, const float* rgb, const float* z,
                       const int32_t* gid, const float* feat, int32_t D, const uint32_t* key_rec,
                       const uint32_t* ranges, float* out_rgb, float* out_depth, float* out_alpha,
-                      float* out_feat, uint8_t* flags, int64_t* counters /*[2] E, B*/) {
+                      float* out_feat, uint8_t* flags, int64_t* counters /*[2] E, B*/,
+                      double* contrib /*[cnt] or NULL*/) {
     Records rc{u, v, conic, opac, rgb, z, gid, feat, D};
     const int32_t W = V->width, H = V->height, TX = (W + 15) / 16;
     const int64_t HW = (int64_t)W * H;
@@ -421,7 +423,7 @@ void oracle_composite(const or_view* V, const or_params* P, const float* u, cons
         for (int32_t px = 0; px < W; ++px) {
             const int64_t t = (int64_t)(py / 16) * TX + px / 16;
             const uint32_t s = ranges[t * 2], e = ranges[t * 2 + 1];
-            composite_pixel(rc, P, px, py, key_rec + s, (int64_t)e - s, o);
+            composite_pixel(rc, P, px, py, key_rec + s, (int64_t)e - s, o, contrib);
             const int64_t pix = (int64_t)py * W + px;
             store_pixel(o, HW, pix, out_rgb, out_depth, out_alpha, out_feat, flags, D);
             counters[0] += o.evals;
@@ -436,7 +438,7 @@ void oracle_brute_force(const or_view* V, const or_params* P, int64_t cnt, const
                         const float* v, const float* conic, const float* opac, const float* rgb,
                         const float* z, const int32_t* gid, const int32_t* rect, const float* feat,
                         int32_t D, float* out_rgb, float* out_depth, float* out_alpha,
-                        float* out_feat, uint8_t* flags) {
+                        float* out_feat, uint8_t* flags, double* contrib /*[cnt] or NULL*/) {
     Records rc{u, v, conic, opac, rgb, z, gid, feat, D};
     const int32_t W = V->width, H = V->height;
     const int64_t HW = (int64_t)W * H;
@@ -455,9 +457,52 @@ void oracle_brute_force(const or_view* V, const or_params* P, int64_t cnt, const
                 if (da != db) return da < db;
                 return gid[a] < gid[b];
             });
-            composite_pixel(rc, P, px, py, list.data(), (int64_t)list.size(), o);
+            composite_pixel(rc, P, px, py, list.data(), (int64_t)list.size(), o, contrib);
             store_pixel(o, HW, (int64_t)py * W + px, out_rgb, out_depth, out_alpha, out_feat, flags, D);
         }
+}
+
+// ---------------------------------------------------------------------------
+// N1: render-visibility check with projection filtering and
+// significance scoring, for one view.
+//   Alg. 1: M^r[j] = render-gradient visibility, read
+//     as the forward criterion contrib[j] > eps, contrib[j] = sum over pixels of
+//     the blend weight w of Gaussian j (O12); M^i = 0 <= U < W and 0 <= V < H
+//     (Alg. 1 l.17); M = M^i and M^r; (U', V') = (U, V)[:, M].
+//   Eq. 4: S(G_i) = cos(F_G, F^t(U', V')), the target map sampled at
+//     the nearest feature cell (reading Q27: cell = floor((U+0.5)/s)).
+//   Eq. 5: S(G) = sum over views; Eq. 6: S(g_j) = S(G_j)/M,
+//     M = number of views in which g_j is visible (formed by the caller).
+// cos of a zero vector is 0 (reading Q28).  fp64.
+// ---------------------------------------------------------------------------
+void oracle_visibility_score(const or_view* V, int64_t cnt, const float* u, const float* v,
+                             const int32_t* gid, const double* contrib, double eps, const float* feat,
+                             int32_t D, const float* fmap /*[D][H'][W'] or NULL*/, int32_t stride,
+                             uint8_t* visible /*[cnt]*/, double* score_sum /*[N]*/,
+                             int64_t* count /*[N]*/) {
+    const int32_t Wf = (V->width + stride - 1) / stride, Hf = (V->height + stride - 1) / stride;
+    for (int64_t i = 0; i < cnt; ++i) {
+        const bool mi = u[i] >= 0.0f && u[i] < (float)V->width && v[i] >= 0.0f && v[i] < (float)V->height;
+        const bool mr = contrib[i] > eps;
+        visible[i] = (uint8_t)(mi && mr);
+        if (!visible[i]) continue;
+        count[gid[i]] += 1;
+        if (fmap == nullptr || D == 0) continue;
+        int32_t cx = (int32_t)std::floor(((double)u[i] + 0.5) / stride);
+        int32_t cy = (int32_t)std::floor(((double)v[i] + 0.5) / stride);
+        cx = std::min(std::max(cx, 0), Wf - 1);
+        cy = std::min(std::max(cy, 0), Hf - 1);
+        const float* f = feat + (int64_t)gid[i] * D;
+        double dot = 0.0, nf = 0.0, nt = 0.0;
+        for (int32_t c = 0; c < D; ++c) {
+            const double t = fmap[((int64_t)c * Hf + cy) * Wf + cx];
+            dot += (double)f[c] * t;
+            nf += (double)f[c] * f[c];
+            nt += t * t;
+        }
+        const double cs = (nf > 0.0 && nt > 0.0) ? dot / (std::sqrt(nf) * std::sqrt(nt)) : 0.0;
+        score_sum[gid[i]] += cs;
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -29,6 +29,7 @@ SOURCES = {
     "gs_bin_sort.cu": [],
     "gs_rasterize.cu": [],
     "gs_backproject.cu": [],
+    "gs_visibility.cu": [],
 }
 HEADERS = [os.path.join(INCLUDE, "gs.h"), os.path.join(CSRC, "gs_common.cuh")]
 

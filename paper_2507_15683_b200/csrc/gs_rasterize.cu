@@ -97,12 +97,14 @@ struct StageMeta {
     uint32_t flags, pad0, pad1, pad2;
 };
 
-template <int D>
+template <int D, bool CONTRIB>
 struct RasterSmem {
     static constexpr int FS = D > 0 ? D + 8 : 1;   // feature row stride (floats)
+    static constexpr bool WB = D > 0 || CONTRIB;   // weight rows are staged (features and/or contributions)
     float4 rec[NST][SE + 1][4];                    // 64-byte records; row SE = null record (opacity 0)
     float feat[D > 0 ? NST : 1][D > 0 ? SE + 1 : 1][FS];
-    alignas(16) float wbuf[D > 0 ? NCW : 1][WB_ROWS][WB_STRIDE]; // per-warp compacted weights [k][pixel]
+    alignas(16) float wbuf[WB ? NCW : 1][WB_ROWS][WB_STRIDE]; // per-warp compacted weights [k][pixel]
+    uint32_t slots[CONTRIB ? NST * (SE + 1) : 1];  // record slot of each ring row (contributions)
     alignas(16) int ent[NCW][SE + 2];                // per-warp compacted ballot list (flat ring rows)
     int kent[NCW][WB_ROWS];                          // ring row of each pending weight row
     StageMeta meta[NST];
@@ -146,22 +148,24 @@ __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, f
 // Persistent kernel: each CTA renders a sequence of tiles handed out in order by
 // a dynamic scheduler.  The producer warp runs ahead across tile boundaries so
 // the consumers never wait for a tile's first records.
-template <int D>
+template <int D, bool CONTRIB>
 __global__ void __launch_bounds__(RT_THREADS, (D > 32 ? 1 : (D > 0 ? 2 : 4)))
 rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record* __restrict__ rec,
                  const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ sorted_gid,
                  const uint32_t* __restrict__ ranges, uint32_t n_tiles, uint32_t* __restrict__ tile_sched,
                  const float* __restrict__ feat,
                  gs_params P, float* __restrict__ out_rgb, float* __restrict__ out_depth,
-                 float* __restrict__ out_alpha, float* __restrict__ out_feat, const uint32_t* __restrict__ status) {
+                 float* __restrict__ out_alpha, float* __restrict__ out_feat,
+                 unsigned long long* __restrict__ contrib, const uint32_t* __restrict__ status) {
+    constexpr bool WB = RasterSmem<D, CONTRIB>::WB;
     if (*status) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    RasterSmem<D>& sm = *reinterpret_cast<RasterSmem<D>*>(smem_raw);
+    RasterSmem<D, CONTRIB>& sm = *reinterpret_cast<RasterSmem<D, CONTRIB>*>(smem_raw);
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < NST * 4; i += blockDim.x) sm.rec[i / 4][SE][i % 4] = make_float4(0.f, 0.f, 0.f, 0.f);
     if constexpr (D > 0)
-        for (int i = threadIdx.x; i < NST * RasterSmem<D>::FS; i += blockDim.x)
-            sm.feat[i / RasterSmem<D>::FS][SE][i % RasterSmem<D>::FS] = 0.f;
+        for (int i = threadIdx.x; i < NST * RasterSmem<D, CONTRIB>::FS; i += blockDim.x)
+            sm.feat[i / RasterSmem<D, CONTRIB>::FS][SE][i % RasterSmem<D, CONTRIB>::FS] = 0.f;
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(&sm.full[s], 33);     // 32 cp.async arrivals + 1 metadata arrival
@@ -248,6 +252,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 const int j = q * 32 + (int)lane;
                 if (j < ccnt) {
                     const float4* src = reinterpret_cast<const float4*>(rec + slot[q]);
+                    if constexpr (CONTRIB) sm.slots[buf * (SE + 1) + j] = slot[q];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) cp_async16(&sm.rec[buf][j][e], src + e, pol);
                     if constexpr (D > 0) {
@@ -258,6 +263,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 }
             }
             cp_async_mbar_arrive(&sm.full[buf]);
+            __syncwarp();   // order the lanes' slot writes before lane 0's release arrival
             if (lane == 0) {
                 StageMeta m;
                 m.tile = ctile; m.c0 = cc0; m.cnt = ccnt; m.view = cview; m.flags = flags;
@@ -288,6 +294,22 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
 
     // F[px][:] += W[px][0..nk) F_entries[0..nk)[:] on the tensor cores (nk multiple of 8)
     auto mma_block = [&](int kb, int ke) {
+        if constexpr (CONTRIB) {
+            // N1: per-entry sum of the warp's 32 pixel weights (lane l: row l/4, columns
+            // 8 (l%4) .. +7, then a 4-lane shuffle reduction), added to the record's
+            // contribution as 2^-32 fixed point: order-independent, hence deterministic
+            for (int k0 = kb; k0 < ke; k0 += 8) {
+                const int r = k0 + (int)(lane >> 2), c0 = (int)(lane & 3u) * 8;
+                float sum = 0.f;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) sum += sm.wbuf[warp][r][c0 + c];
+                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+                sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+                const int kr = sm.kent[warp][r];
+                if ((lane & 3u) == 0u && sum > 0.f && (kr % (SE + 1)) != SE)
+                    atomicAdd(&contrib[sm.slots[kr]], (unsigned long long)__float2ll_rn(sum * 4294967296.0f));
+            }
+        }
         if constexpr (D > 0) {
             for (int k0 = kb; k0 < ke; k0 += 8) {
                 uint32_t ahi[2][4], alo[2][4];
@@ -302,8 +324,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                         alo[m][i] = __float_as_uint(av[i] - __uint_as_float(ahi[m][i]));   // exact remainder
                     }
                 }
-                const float* f0 = &sm.feat[0][0][0] + sm.kent[warp][k0 + t4] * RasterSmem<D>::FS;
-                const float* f1 = &sm.feat[0][0][0] + sm.kent[warp][k0 + t4 + 4] * RasterSmem<D>::FS;
+                const float* f0 = &sm.feat[0][0][0] + sm.kent[warp][k0 + t4] * RasterSmem<D, CONTRIB>::FS;
+                const float* f1 = &sm.feat[0][0][0] + sm.kent[warp][k0 + t4 + 4] * RasterSmem<D, CONTRIB>::FS;
 #pragma unroll
                 for (int n = 0; n < NTP; ++n) {
                     const int ch = n * 8 + g;
@@ -339,7 +361,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     uint32_t hold = 0;        // oldest stage a pending row references
     uint32_t rel = 0;         // next stage to release
     auto flush_pending = [&]() {
-        if constexpr (D > 0) {
+        if constexpr (WB) {
             if (pend > 0) {
                 for (int r = pend; r < 8; ++r) sm.wbuf[warp][r][lane] = 0.f;
                 if (lane < (uint32_t)(8 - pend)) sm.kent[warp][pend + lane] = SE;   // null row
@@ -406,7 +428,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     const float w1 = blend(a1, r1[2]);
                     a2 = done ? 0.0f : a2;
                     const float w2 = blend(a2, r2[2]);
-                    if constexpr (D > 0) {
+                    if constexpr (WB) {
                         if (pend == 0) hold = s;
                         sm.wbuf[warp][pend][lane] = w1;
                         sm.wbuf[warp][pend + 1][lane] = w2;
@@ -424,7 +446,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             }
         }
         // never pin more than half the ring: the producer must be able to refill
-        if (D > 0 && pend > 0 && s - hold >= NST / 2) flush_pending();
+        if (WB && pend > 0 && s - hold >= NST / 2) flush_pending();
         if (m.flags & ST_LAST) {
             flush_pending();
             // -------------------------------------------------------- outputs
@@ -463,32 +485,33 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             }
         }
         // release every stage no pending row references, in order
-        const uint32_t lim = (D > 0 && pend > 0) ? hold : s + 1;
+        const uint32_t lim = (WB && pend > 0) ? hold : s + 1;
         __syncwarp();
         for (; rel < lim; ++rel)
             if (lane == 0) mbar_arrive(&sm.empty[rel % NST]);
     }
 }
 
-template <int D>
+template <int D, bool CONTRIB>
 gs_status launch(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins, const gs_view* views_dev,
                  int n_views, int64_t T, const gs_params* P, gs_images* out, cudaStream_t s) {
-    const int smem = (int)sizeof(RasterSmem<D>);
+    const int smem = (int)sizeof(RasterSmem<D, CONTRIB>);
     static int blocks_per_sm = 0;
     if (blocks_per_sm == 0) {
-        cudaFuncSetAttribute(rasterize_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(rasterize_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rasterize_kernel<D>, RT_THREADS, smem);
+        cudaFuncSetAttribute(rasterize_kernel<D, CONTRIB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(rasterize_kernel<D, CONTRIB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rasterize_kernel<D, CONTRIB>, RT_THREADS, smem);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     const int64_t grid =
         std::min<int64_t>((T + SCHED_CHUNK - 1) / SCHED_CHUNK, (int64_t)num_sms() * blocks_per_sm);
     if (grid <= 0) return GS_OK;
     if (bins->tile_sched) cudaMemsetAsync(bins->tile_sched, 0, sizeof(uint32_t), s);
-    rasterize_kernel<D><<<(unsigned)grid, RT_THREADS, smem, s>>>(
+    if (CONTRIB) cudaMemsetAsync(proj->contrib, 0, sizeof(unsigned long long) * (size_t)n_views * proj->rec_capacity, s);
+    rasterize_kernel<D, CONTRIB><<<(unsigned)grid, RT_THREADS, smem, s>>>(
         views_dev, n_views, proj->rec, bins->sorted_rec, bins->sorted_gid, bins->ranges, (uint32_t)T, bins->tile_sched,
         scene->feat,
-        *P, out->rgb, out->depth, out->alpha, out->feat, proj->status);
+        *P, out->rgb, out->depth, out->alpha, out->feat, proj->contrib, proj->status);
     return check_launch("rasterize_kernel");
 }
 
@@ -517,7 +540,9 @@ extern "C" gs_status gs_rasterize(const gs_scene* scene, const gs_projected* pro
     cudaStream_t s = (cudaStream_t)stream;
     switch (scene->feat_dim) {
 #define GS_CASE(d) \
-    case d: return launch<d>(scene, proj, bins, views_dev, n_views, T, params, out, s);
+    case d:                                                                                       \
+        return proj->contrib ? launch<d, true>(scene, proj, bins, views_dev, n_views, T, params, out, s) \
+                             : launch<d, false>(scene, proj, bins, views_dev, n_views, T, params, out, s);
         GS_CASE(0) GS_CASE(4) GS_CASE(8) GS_CASE(12) GS_CASE(16) GS_CASE(20) GS_CASE(24) GS_CASE(28) GS_CASE(32)
         GS_CASE(36) GS_CASE(40) GS_CASE(44) GS_CASE(48) GS_CASE(52) GS_CASE(56) GS_CASE(60) GS_CASE(64)
 #undef GS_CASE

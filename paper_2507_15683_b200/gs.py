@@ -53,7 +53,7 @@ class gs_params(ctypes.Structure):
 
 class gs_projected(ctypes.Structure):
     _fields_ = [("rec", ctypes.c_void_p), ("rec_capacity", ctypes.c_int64), ("n_rec", ctypes.c_void_p),
-                ("diag", ctypes.c_void_p), ("status", ctypes.c_void_p)]
+                ("diag", ctypes.c_void_p), ("status", ctypes.c_void_p), ("contrib", ctypes.c_void_p)]
 
 
 class gs_bins(ctypes.Structure):
@@ -69,7 +69,7 @@ class gs_images(ctypes.Structure):
 
 EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_layout", "gs_scene_block_bounds",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
-           "gs_rasterize", "gs_backproject"]
+           "gs_rasterize", "gs_backproject", "gs_visibility_score"]
 
 _lib = None
 
@@ -89,7 +89,7 @@ def lib():
         L.gs_bin_sort_workspace_bytes.restype = ctypes.c_size_t
         L.gs_bin_sort_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]
         for f in ("gs_views_layout", "gs_scene_block_bounds", "gs_project", "gs_bin_sort", "gs_rasterize",
-                  "gs_backproject"):
+                  "gs_backproject", "gs_visibility_score"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -205,15 +205,17 @@ class ViewBatch:
 
 
 class Projected:
-    def __init__(self, n_views: int, rec_capacity: int, device="cuda"):
+    def __init__(self, n_views: int, rec_capacity: int, device="cuda", contrib: bool = False):
         self.rec_capacity = int(rec_capacity)
         self.rec = torch.empty(n_views * self.rec_capacity * (RECORD_BYTES // 4), dtype=torch.int32, device=device)
         self.n_rec = torch.zeros(n_views, dtype=torch.int32, device=device)
         self.diag = torch.zeros(4, dtype=torch.int64, device=device)
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        self.contrib = torch.zeros(n_views * self.rec_capacity, dtype=torch.int64, device=device) if contrib else None
         s = gs_projected()
         s.rec, s.rec_capacity = _ptr(self.rec), self.rec_capacity
         s.n_rec, s.diag, s.status = _ptr(self.n_rec), _ptr(self.diag), _ptr(self.status)
+        s.contrib = _ptr(self.contrib)
         self.struct = s
 
     def records(self):
@@ -296,3 +298,15 @@ def gs_backproject(images: Images, views: ViewBatch, a_min: float, xyz: torch.Te
                    stream=None):
     _check(lib().gs_backproject(ctypes.byref(images.struct), views.host, views.dev_ptr, ctypes.c_int32(views.n),
                                 ctypes.c_float(a_min), _ptr(xyz), _ptr(valid), _stream(stream)), "gs_backproject")
+
+
+FIXED_ONE = float(1 << 32)   # 2^-32 fixed point of contributions and scores
+
+
+def gs_visibility_score(proj: Projected, views: ViewBatch, eps: float, scene: "DeviceScene", visible: torch.Tensor,
+                        n_visible: torch.Tensor, score_sum: torch.Tensor, count: torch.Tensor,
+                        fmaps: Optional[torch.Tensor] = None, stride: int = 1, stream=None):
+    _check(lib().gs_visibility_score(ctypes.byref(proj.struct), views.host, views.dev_ptr, ctypes.c_int32(views.n),
+                                     ctypes.c_float(eps), _ptr(scene.feat), ctypes.c_int32(scene.feat_dim),
+                                     _ptr(fmaps), ctypes.c_int32(stride), _ptr(visible), _ptr(n_visible),
+                                     _ptr(score_sum), _ptr(count), _stream(stream)), "gs_visibility_score")

@@ -19,7 +19,7 @@ class Renderer:
     def __init__(self, scene: G.DeviceScene, views: Sequence, params: Optional[G.gs_params] = None,
                  a_min: float = 0.5, backproject: bool = True, rec_capacity: Optional[int] = None,
                  pair_capacity: Optional[int] = None, debug_keys: bool = False, use_blocks: bool = True,
-                 device="cuda"):
+                 contrib: bool = False, device="cuda"):
         self.device = torch.device(device)
         self.scene = scene
         self.scene_struct = scene.struct if use_blocks else scene.without_blocks()
@@ -28,6 +28,7 @@ class Renderer:
         self.a_min = a_min
         self.do_backproject = backproject
         self.debug_keys = debug_keys
+        self.with_contrib = contrib
         n_views = self.vb.n
         self.ws_proj = torch.empty(max(1, G.project_workspace_bytes(scene.n_blocks if use_blocks else 0, n_views)),
                                    dtype=torch.uint8, device=self.device)
@@ -55,7 +56,7 @@ class Renderer:
         rec_capacity = min(rec_capacity, ((1 << 32) - 1) // n_views)
         if self.proj is None or self.proj.rec_capacity != rec_capacity:
             self.proj = None
-            self.proj = G.Projected(n_views, rec_capacity, device=self.device)
+            self.proj = G.Projected(n_views, rec_capacity, device=self.device, contrib=self.with_contrib)
         if self.bins is None or self.bins.pair_capacity != pair_capacity:
             self.bins = None
             self.ws_bin = None
@@ -122,3 +123,34 @@ class Renderer:
         ts = [self.proj.rec, self.bins.sorted_rec, self.ws_bin, self.images.rgb, self.images.depth,
               self.images.alpha, self.images.feat, self.xyz, self.valid]
         return sum(t.numel() * t.element_size() for t in ts if t is not None)
+
+
+class SignificanceScorer:
+    """N1: Alg. 1 visibility + Eq. 4-6 significance over batches of views.
+
+    ``add(renderer, fmaps)`` runs gs_visibility_score on a rendered batch (the
+    renderer must be built with ``contrib=True``); ``scores()`` returns
+    S(g) = S(G)/M (Eq. 6) with -inf where M = 0."""
+
+    def __init__(self, scene: G.DeviceScene, eps: float = 1e-6, stride: int = 1):
+        self.scene = scene
+        self.eps = eps
+        self.stride = stride
+        dev = scene.pos.device
+        self.score_sum = torch.zeros(scene.n, dtype=torch.int64, device=dev)
+        self.count = torch.zeros(scene.n, dtype=torch.int32, device=dev)
+
+    def add(self, r: "Renderer", fmaps: Optional[torch.Tensor] = None, stream=None):
+        n_views = r.vb.n
+        r.visible = torch.empty(n_views * r.proj.rec_capacity, dtype=torch.uint8, device=self.count.device)
+        r.n_visible = torch.zeros(n_views, dtype=torch.int32, device=self.count.device)
+        G.gs_visibility_score(r.proj, r.vb, self.eps, self.scene, r.visible, r.n_visible, self.score_sum, self.count,
+                              fmaps, self.stride, stream)
+        return r.visible, r.n_visible
+
+    def scores(self) -> torch.Tensor:
+        s = self.score_sum.double() / G.FIXED_ONE
+        m = self.count > 0
+        out = torch.full_like(s, float("-inf"))
+        out[m] = s[m] / self.count[m].double()
+        return out
