@@ -71,10 +71,11 @@ def test_contrib_c2_and_determinism(G, orc):
     o = orc.render(sc, vs[0])
     gid, contrib, _ = _gpu_view(r, 0)
     _check_view(o, gid, contrib)
-    first = r.proj.contrib.clone()
+    # record slots depend on atomic order; per-Gaussian sums must not (fixed point)
     r.run()
     torch.cuda.synchronize()
-    assert torch.equal(first, r.proj.contrib)          # fixed-point sums: order independent
+    gid2, contrib2, _ = _gpu_view(r, 0)
+    assert np.array_equal(gid, gid2) and np.array_equal(contrib, contrib2)
 
 
 @pytest.mark.parametrize("stride", [1, 8])
