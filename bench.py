@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-views", type=int, default=2)
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run only this many untimed steps")
+    ap.add_argument("--n1", action="store_true",
+                    help="also time N1 (per-Gaussian contributions + Alg. 1 visibility + Eq. 4-6 scoring "
+                         "against stride-8 synthetic target maps) inside the step")
     return ap.parse_args()
 
 
@@ -220,7 +223,15 @@ def main():
     if args.views:
         views = views[:args.views]
     ds = G.DeviceScene(scene, device=dev)
-    r = G.Renderer(ds, views, device=dev, backproject=True)
+    r = G.Renderer(ds, views, device=dev, backproject=True, contrib=args.n1)
+    scorer, fmaps = None, None
+    if args.n1:
+        if scene.feat_dim == 0:
+            raise SystemExit("--n1 needs a feature scene (C3 / C4)")
+        scorer = G.SignificanceScorer(ds, eps=1e-6, stride=8)
+        g = torch.Generator(device=dev).manual_seed(1234 + rank)
+        nmap = sum(scene.feat_dim * ((v.height + 7) // 8) * ((v.width + 7) // 8) for v in views)
+        fmaps = torch.randn(nmap, generator=g, device=dev)
     r.render()
     r.fit_capacities()
     r.render()
@@ -246,6 +257,8 @@ def main():
 
     def step():
         r.run(stream)
+        if scorer is not None:
+            scorer.add(r, fmaps, stream)
         if args.gather and world > 1:
             p = GD.pack_planes(r.images.rgb, r.images.depth, r.images.alpha, n_views, hw, pad)
             GD.gather_planes(p, world)
@@ -259,7 +272,7 @@ def main():
 
     # timed region: CUDA events on the launching stream, per-stage events for the roofline
     K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device() if world == 1 else local) as clk:
         if world > 1:
@@ -278,6 +291,9 @@ def main():
             e[3].record(stream)
             G.gs_backproject(r.images, r.vb, r.a_min, r.xyz, r.valid, stream)
             e[4].record(stream)
+            if scorer is not None:
+                scorer.add(r, fmaps, stream)
+            e[5].record(stream)
             if args.gather and world > 1:
                 GD.gather_planes(GD.pack_planes(r.images.rgb, r.images.depth, r.images.alpha, n_views, hw, pad),
                                  world)
@@ -287,7 +303,7 @@ def main():
             dist.barrier()
     assert r.status() == 0, "capacity overflow inside the timed region"
     ms_total = start.elapsed_time(end)
-    stage = np.array([[ev[k][j].elapsed_time(ev[k][j + 1]) for j in range(4)] for k in range(K)])
+    stage = np.array([[ev[k][j].elapsed_time(ev[k][j + 1]) for j in range(5)] for k in range(K)])
     stage_ms = stage.mean(axis=0)
     if world > 1:
         t = torch.tensor([ms_total], device=dev)
@@ -334,8 +350,8 @@ def main():
 
     # roofline of the dominant kernel
     peak, peak_src = measured_peaks()
-    dom = int(np.argmax(stage_ms))
-    names = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_backproject"]
+    dom = int(np.argmax(stage_ms[:4]))
+    names = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_backproject", "n1_visibility_score"]
     D = scene.feat_dim
     raster_bytes = algorithmic_raster_bytes(n_pairs, n_visible, total_px, D)
     achieved = raster_bytes / (stage_ms[2] / 1e3) / 1e9
@@ -343,7 +359,7 @@ def main():
     roof = {"bound": "hbm", "kernel": "gs_rasterize", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": raster_bytes, "dominant_stage": names[dom]}
-    launches_per_step = (3 if ds.n_blocks else 2) + 7 + 1 + 1
+    launches_per_step = (3 if ds.n_blocks else 2) + 8 + 1 + 1 + (1 if scorer is not None else 0)
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
            "ms_per_step": ms_step, "ms_per_view": ms_step * world / all_views if args.scaling == "strong" else
@@ -353,8 +369,8 @@ def main():
                       "resolution": f"{views[0].width}x{views[0].height}", "sh_degree": scene.sh_degree,
                       "feat_dim": D, "l2": "inputs larger than L2 (scene %.2f GB, %.1f GB written per step)" % (
                           ds.nbytes() / 1e9, (total_px * (5 + D) * 4 + total_px * 13) / 1e9),
-                      "gather": bool(args.gather and world > 1)},
-           "stages_ms": {n: float(m) for n, m in zip(names, stage_ms)},
+                      "gather": bool(args.gather and world > 1), "n1": bool(args.n1)},
+           "stages_ms": {n: float(m) for n, m in zip(names, stage_ms) if n != names[4] or scorer is not None},
            "counts": {"visible_records": n_visible, "pairs": n_pairs, "pixels": total_px},
            "roofline": roof, "gpu_launches": launches_per_step * K, "e2e": e2e, "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
