@@ -26,6 +26,8 @@
 //     issues m16n8k8 TF32 MMAs (weights split hi+lo, features rounded once:
 //     error <= 2^-11 sum w|f|, inside the 1e-3 max(1,|f|) tolerance);
 //   * warp-ballot early termination once all 32 pixels have T < t_min.
+#include <cuda_fp16.h>
+
 #include "gs_common.cuh"
 
 namespace gs {
@@ -35,8 +37,8 @@ constexpr int NCW = 8;                 // consumer warps
 constexpr int RT_THREADS = (NCW + 1) * 32;
 constexpr int SE = 32;                 // entries per stage (one ballot)
 constexpr int NST = 8;                 // ring stages
-constexpr int WB_STRIDE = 40;          // weight-buffer row stride (conflict-free A fragments)
-constexpr int WB_ROWS = 8;             // one tensor-core k-step of weights
+constexpr int WB_STRIDE = 36;          // weight-buffer row stride (conflict-free m16n8k16 A fragments)
+constexpr int WB_ROWS = 16;            // one tensor-core k-step of weights (m16n8k16)
 constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
 constexpr uint32_t SCHED_CHUNK = 2;    // tiles per scheduler claim
 
@@ -82,6 +84,13 @@ __device__ __forceinline__ float ex2_ftz(float x) {
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(r) : "f"(x));
     return r;
+}
+__device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile(
@@ -311,29 +320,42 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             }
         }
         if constexpr (D > 0) {
-            for (int k0 = kb; k0 < ke; k0 += 8) {
+            // m16n8k16 FP16 MMAs: weights split hi + lo (fp16 pairs, ~2^-22 exact), feature
+            // rows rounded once to fp16 (error <= 2^-11 sum w|f|, inside 1e-3 max(1,|f|))
+            for (int k0 = kb; k0 < ke; k0 += 16) {
                 uint32_t ahi[2][4], alo[2][4];
 #pragma unroll
                 for (int m = 0; m < 2; ++m) {
-                    const float av[4] = {sm.wbuf[warp][k0 + t4][m * 16 + g], sm.wbuf[warp][k0 + t4][m * 16 + g + 8],
-                                         sm.wbuf[warp][k0 + t4 + 4][m * 16 + g],
-                                         sm.wbuf[warp][k0 + t4 + 4][m * 16 + g + 8]};
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        ahi[m][i] = to_tf32(av[i]);
-                        alo[m][i] = __float_as_uint(av[i] - __uint_as_float(ahi[m][i]));   // exact remainder
+                        const int px = m * 16 + g + ((i & 1) ? 8 : 0);
+                        const int k = k0 + 2 * t4 + ((i & 2) ? 8 : 0);
+                        const float w0 = sm.wbuf[warp][k][px], w1 = sm.wbuf[warp][k + 1][px];
+                        const __half2 h = __floats2half2_rn(w0, w1);
+                        const float2 hf = __half22float2(h);
+                        const __half2 l = __floats2half2_rn(w0 - hf.x, w1 - hf.y);
+                        ahi[m][i] = *reinterpret_cast<const uint32_t*>(&h);
+                        alo[m][i] = *reinterpret_cast<const uint32_t*>(&l);
                     }
                 }
-                const float* f0 = &sm.feat[0][0][0] + sm.kent[warp][k0 + t4] * RasterSmem<D, CONTRIB>::FS;
-                const float* f1 = &sm.feat[0][0][0] + sm.kent[warp][k0 + t4 + 4] * RasterSmem<D, CONTRIB>::FS;
+                const float* fb = &sm.feat[0][0][0];
+                constexpr int FS = RasterSmem<D, CONTRIB>::FS;
+                const float* f0 = fb + sm.kent[warp][k0 + 2 * t4] * FS;
+                const float* f1 = fb + sm.kent[warp][k0 + 2 * t4 + 1] * FS;
+                const float* f2 = fb + sm.kent[warp][k0 + 2 * t4 + 8] * FS;
+                const float* f3 = fb + sm.kent[warp][k0 + 2 * t4 + 9] * FS;
 #pragma unroll
                 for (int n = 0; n < NTP; ++n) {
                     const int ch = n * 8 + g;
-                    const uint32_t b0 = to_tf32(ch < D ? f0[ch] : 0.f), b1 = to_tf32(ch < D ? f1[ch] : 0.f);
+                    const bool in = ch < D;
+                    const __half2 b0h = __floats2half2_rn(in ? f0[ch] : 0.f, in ? f1[ch] : 0.f);
+                    const __half2 b1h = __floats2half2_rn(in ? f2[ch] : 0.f, in ? f3[ch] : 0.f);
+                    const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&b0h);
+                    const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&b1h);
 #pragma unroll
                     for (int m = 0; m < 2; ++m) {
-                        mma_tf32(acc[m][n], ahi[m], b0, b1);
-                        mma_tf32(acc[m][n], alo[m], b0, b1);
+                        mma_f16(acc[m][n], ahi[m], b0, b1);
+                        mma_f16(acc[m][n], alo[m], b0, b1);
                     }
                 }
             }
@@ -357,16 +379,16 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     // no pending row references it.  Ring rows are addressed flat: stage buffer b,
     // entry j -> b * (SE + 1) + j (row SE of every buffer is the null record).
     const float4* recf = &sm.rec[0][0][0];
-    int pend = 0;             // pending weight rows (< 8 between stages)
+    int pend = 0;             // pending weight rows (< WB_ROWS between stages)
     uint32_t hold = 0;        // oldest stage a pending row references
     uint32_t rel = 0;         // next stage to release
     auto flush_pending = [&]() {
         if constexpr (WB) {
             if (pend > 0) {
-                for (int r = pend; r < 8; ++r) sm.wbuf[warp][r][lane] = 0.f;
-                if (lane < (uint32_t)(8 - pend)) sm.kent[warp][pend + lane] = SE;   // null row
+                for (int r = pend; r < WB_ROWS; ++r) sm.wbuf[warp][r][lane] = 0.f;
+                if (lane < (uint32_t)(WB_ROWS - pend)) sm.kent[warp][pend + lane] = SE;   // null row
                 __syncwarp();
-                mma_block(0, 8);
+                mma_block(0, WB_ROWS);
                 __syncwarp();
                 pend = 0;
             }
