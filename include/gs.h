@@ -282,11 +282,16 @@ gs_status gs_backproject(const gs_images* in, const gs_view* views_host, const g
  *   cosine of a zero vector is 0 (Q28).  S(g) = score_sum / count (Eq. 6) is
  *   formed by the caller.  n_visible is overwritten; count and score_sum
  *   accumulate (the caller zeroes them once for a multi-batch pass).
+ *   ws (optional, >= gs_visibility_workspace_bytes()) receives a channels-last
+ *   copy of the maps so each sample reads one contiguous feature row; with
+ *   ws == NULL the planar maps are sampled channel by channel (slower).
  */
+size_t gs_visibility_workspace_bytes(const gs_view* views_host, int32_t n_views, int32_t feat_dim, int32_t stride);
+
 gs_status gs_visibility_score(const gs_projected* proj, const gs_view* views_host, const gs_view* views_dev,
                               int32_t n_views, float eps, const float* feat /* scene [N][D] */, int32_t feat_dim,
-                              const float* fmaps, int32_t stride, uint8_t* visible, uint32_t* n_visible,
-                              unsigned long long* score_sum, uint32_t* count, void* stream);
+                              const float* fmaps, int32_t stride, void* ws, size_t ws_bytes, uint8_t* visible,
+                              uint32_t* n_visible, unsigned long long* score_sum, uint32_t* count, void* stream);
 
 #ifdef __cplusplus
 }

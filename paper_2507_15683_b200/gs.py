@@ -69,7 +69,7 @@ class gs_images(ctypes.Structure):
 
 EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_layout", "gs_scene_block_bounds",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
-           "gs_rasterize", "gs_backproject", "gs_visibility_score"]
+           "gs_rasterize", "gs_backproject", "gs_visibility_score", "gs_visibility_workspace_bytes"]
 
 _lib = None
 
@@ -88,6 +88,7 @@ def lib():
         L.gs_project_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32]
         L.gs_bin_sort_workspace_bytes.restype = ctypes.c_size_t
         L.gs_bin_sort_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]
+        L.gs_visibility_workspace_bytes.restype = ctypes.c_size_t
         for f in ("gs_views_layout", "gs_scene_block_bounds", "gs_project", "gs_bin_sort", "gs_rasterize",
                   "gs_backproject", "gs_visibility_score"):
             getattr(L, f).restype = ctypes.c_int
@@ -303,10 +304,18 @@ def gs_backproject(images: Images, views: ViewBatch, a_min: float, xyz: torch.Te
 FIXED_ONE = float(1 << 32)   # 2^-32 fixed point of contributions and scores
 
 
+def visibility_workspace_bytes(views: ViewBatch, feat_dim: int, stride: int) -> int:
+    return int(lib().gs_visibility_workspace_bytes(views.host, ctypes.c_int32(views.n), ctypes.c_int32(feat_dim),
+                                                   ctypes.c_int32(stride)))
+
+
 def gs_visibility_score(proj: Projected, views: ViewBatch, eps: float, scene: "DeviceScene", visible: torch.Tensor,
                         n_visible: torch.Tensor, score_sum: torch.Tensor, count: torch.Tensor,
-                        fmaps: Optional[torch.Tensor] = None, stride: int = 1, stream=None):
+                        fmaps: Optional[torch.Tensor] = None, stride: int = 1, ws: Optional[torch.Tensor] = None,
+                        stream=None):
+    nbytes = 0 if ws is None else ws.numel() * ws.element_size()
     _check(lib().gs_visibility_score(ctypes.byref(proj.struct), views.host, views.dev_ptr, ctypes.c_int32(views.n),
                                      ctypes.c_float(eps), _ptr(scene.feat), ctypes.c_int32(scene.feat_dim),
-                                     _ptr(fmaps), ctypes.c_int32(stride), _ptr(visible), _ptr(n_visible),
-                                     _ptr(score_sum), _ptr(count), _stream(stream)), "gs_visibility_score")
+                                     _ptr(fmaps), ctypes.c_int32(stride), _ptr(ws), ctypes.c_size_t(nbytes),
+                                     _ptr(visible), _ptr(n_visible), _ptr(score_sum), _ptr(count), _stream(stream)),
+           "gs_visibility_score")

@@ -142,10 +142,18 @@ class SignificanceScorer:
 
     def add(self, r: "Renderer", fmaps: Optional[torch.Tensor] = None, stream=None):
         n_views = r.vb.n
-        r.visible = torch.empty(n_views * r.proj.rec_capacity, dtype=torch.uint8, device=self.count.device)
-        r.n_visible = torch.zeros(n_views, dtype=torch.int32, device=self.count.device)
+        dev = self.count.device
+        if getattr(r, "visible", None) is None or r.visible.numel() != n_views * r.proj.rec_capacity:
+            r.visible = torch.empty(n_views * r.proj.rec_capacity, dtype=torch.uint8, device=dev)
+            r.n_visible = torch.zeros(n_views, dtype=torch.int32, device=dev)
+        ws = None
+        if fmaps is not None:
+            nb = G.visibility_workspace_bytes(r.vb, self.scene.feat_dim, self.stride)
+            if getattr(r, "vis_ws", None) is None or r.vis_ws.numel() < nb:
+                r.vis_ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=dev)
+            ws = r.vis_ws
         G.gs_visibility_score(r.proj, r.vb, self.eps, self.scene, r.visible, r.n_visible, self.score_sum, self.count,
-                              fmaps, self.stride, stream)
+                              fmaps, self.stride, ws, stream)
         return r.visible, r.n_visible
 
     def scores(self) -> torch.Tensor:

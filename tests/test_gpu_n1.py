@@ -111,3 +111,26 @@ def test_visibility_and_scores_c4_batch(G, orc, stride):
     s_orc = orc.final_scores(ssum, cnt)
     np.testing.assert_allclose(s_gpu[ok & (cnt > 0)], s_orc[ok & (cnt > 0)], atol=3e-5)
     assert np.all(np.isneginf(s_gpu[cnt == 0] if ok.all() else s_gpu[(cnt == 0) & ok]))
+
+
+def test_channels_last_and_planar_sampling_agree(G, orc):
+    """gs_visibility_score with a workspace (channels-last copy) and without
+    (planar sampling) give the same counts and score sums (up to fp32 order)."""
+    sc, vs = synth.make_config("C4", scale=0.01)
+    vs = vs[:3]
+    ds, r = _render(G, sc, vs)
+    rng = np.random.default_rng(5)
+    n = sum(32 * ((v.height + 3) // 4) * ((v.width + 3) // 4) for v in vs)
+    fmaps = torch.from_numpy(rng.standard_normal(n).astype(np.float32)).cuda()
+    outs = []
+    for use_ws in (True, False):
+        vis = torch.empty(len(vs) * r.proj.rec_capacity, dtype=torch.uint8, device="cuda")
+        nvis = torch.zeros(len(vs), dtype=torch.int32, device="cuda")
+        ssum = torch.zeros(sc.n, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(sc.n, dtype=torch.int32, device="cuda")
+        ws = torch.empty(G.gs.visibility_workspace_bytes(r.vb, 32, 4), dtype=torch.uint8, device="cuda") if use_ws else None
+        G.gs_visibility_score(r.proj, r.vb, 1e-6, ds, vis, nvis, ssum, cnt, fmaps, 4, ws)
+        torch.cuda.synchronize()
+        outs.append((cnt.cpu().numpy(), ssum.cpu().numpy().astype(np.float64) / FIXED, nvis.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][2], outs[1][2])
+    np.testing.assert_allclose(outs[0][1], outs[1][1], atol=1e-5)
