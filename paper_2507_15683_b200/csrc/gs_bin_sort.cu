@@ -33,7 +33,9 @@ constexpr int SCAN_PER_THREAD = 4;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_PER_THREAD;
 constexpr int WARP_SORT_MAX = 512;      // 16 keys per lane
 constexpr int SMEM_SORT_MAX = 2048;     // run length sorted on chip (2 padded buffers: 52 KB)
-constexpr int BIG_THREADS = 128;        // 4 warps: one 512-element register run each
+constexpr int BIG_THREADS = 128;        // 4 warps per long list (throughput mode)
+constexpr int LAT_THREADS = 512;        // 16 warps per list > 256 (latency mode, small batches)
+constexpr int64_t LAT_TILES = 16384;    // batches with at most this many tiles use latency mode
 constexpr uint64_t PAD_KEY = ~0ull;
 
 struct BinWs {
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(256)
 warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint4* __restrict__ bucket,
                  uint32_t* __restrict__ out, uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg,
                  uint32_t* __restrict__ lists_count, uint32_t* __restrict__ mid_list,
-                 uint32_t* __restrict__ big_list, const uint32_t* __restrict__ status) {
+                 uint32_t* __restrict__ big_list, uint32_t mid_max, const uint32_t* __restrict__ status) {
     if (*status) return;
     __shared__ uint2 stage[8][SMALL_MAX];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -438,7 +440,7 @@ warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint4* __
     else if (len <= 128) warp_sort_tile<4>(bucket, s, len, (uint32_t)tile, lane, st, out, ogid, dbg);
     else if (len <= SMALL_MAX) warp_sort_tile<8>(bucket, s, len, (uint32_t)tile, lane, st, out, ogid, dbg);
     else if (lane == 0) {
-        if (len <= WARP_SORT_MAX) mid_list[atomicAdd(&lists_count[0], 1u)] = (uint32_t)tile;
+        if (len <= mid_max) mid_list[atomicAdd(&lists_count[0], 1u)] = (uint32_t)tile;
         else big_list[atomicAdd(&lists_count[1], 1u)] = (uint32_t)tile;
     }
 }
@@ -491,69 +493,76 @@ __device__ void cta_merge(const uint64_t* __restrict__ sk, const uint32_t* __res
 __device__ __forceinline__ uint32_t pidx(uint32_t e) { return e + (e >> 4); }
 constexpr int RUN_PAD = SMEM_SORT_MAX + SMEM_SORT_MAX / 16;
 
-// merge sorted runs [a0, a0+na) and [a0+na, a0+na+nb) of padded shared arrays
-__device__ void smem_merge(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv, uint64_t* __restrict__ dk,
-                           uint32_t* __restrict__ dv, uint32_t a0, uint32_t na, uint32_t nb) {
-    const uint32_t total = na + nb;
-    const uint32_t per = (total + blockDim.x - 1) / blockDim.x;
-    const uint32_t lo = min(total, threadIdx.x * per), hi = min(total, lo + per);
-    if (lo >= hi) return;
-    const uint32_t A = a0, B = a0 + na;
-    uint32_t ilo = lo > nb ? lo - nb : 0u, ihi = min(lo, na);
-    while (ilo < ihi) {
-        const uint32_t i = (ilo + ihi) >> 1;
-        if (sk[pidx(A + i)] < sk[pidx(B + lo - i - 1)]) ilo = i + 1; else ihi = i;
-    }
-    uint32_t i = ilo, j = lo - ilo;
-    for (uint32_t o = lo; o < hi; ++o) {
-        const bool takeA = j >= nb || (i < na && sk[pidx(A + i)] < sk[pidx(B + j)]);
-        const uint32_t src = takeA ? A + i : B + j;
-        dk[pidx(a0 + o)] = sk[pidx(src)];
-        dv[pidx(a0 + o)] = sv[pidx(src)];
-        if (takeA) ++i; else ++j;
+// one merge round over all adjacent run pairs of width w (padded shared arrays):
+// every output element is placed independently (merge-path split of its pair +
+// one comparison), so all threads stay busy however many pairs there are
+__device__ void smem_merge_round(const uint64_t* __restrict__ sk, const uint32_t* __restrict__ sv,
+                                 uint64_t* __restrict__ dk, uint32_t* __restrict__ dv, uint32_t rl, uint32_t w) {
+    for (uint32_t o = threadIdx.x; o < rl; o += blockDim.x) {
+        const uint32_t a0 = o / (2 * w) * (2 * w);
+        const uint32_t na = min(w, rl - a0);
+        const uint32_t nb = a0 + na < rl ? min(w, rl - a0 - na) : 0u;
+        const uint32_t j = o - a0, A = a0, B = a0 + na;
+        // i = number of A elements among the first j outputs
+        uint32_t ilo = j > nb ? j - nb : 0u, ihi = min(j, na);
+        while (ilo < ihi) {
+            const uint32_t i = (ilo + ihi) >> 1;
+            if (sk[pidx(A + i)] < sk[pidx(B + j - i - 1)]) ilo = i + 1; else ihi = i;
+        }
+        const uint32_t i = ilo, jb = j - ilo;
+        const bool takeA = jb >= nb || (i < na && sk[pidx(A + i)] < sk[pidx(B + jb)]);
+        const uint32_t src = takeA ? A + i : B + jb;
+        dk[pidx(o)] = sk[pidx(src)];
+        dv[pidx(o)] = sv[pidx(src)];
     }
 }
 
-// sort rl <= SMEM_SORT_MAX pairs already placed in (ak, av); returns 0 if the
-// result is in (ak, av), 1 if in (bk, bv)
-__device__ int smem_sort_run(uint64_t* ak, uint32_t* av, uint64_t* bk, uint32_t* bv, uint32_t rl) {
+template <int PER>
+__device__ void warp_runs(uint64_t* ak, uint32_t* av, uint32_t rl) {
+    constexpr uint32_t RUN = 32u * PER;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    const uint32_t nrun = (rl + 511) / 512;
+    const uint32_t nrun = (rl + RUN - 1) / RUN;
     for (uint32_t r = warp; r < nrun; r += nwarp) {
-        uint64_t k[16];
-        uint32_t v[16];
+        uint64_t k[PER];
+        uint32_t v[PER];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint32_t e = r * 512 + lane * 16 + (uint32_t)j;
+        for (int j = 0; j < PER; ++j) {
+            const uint32_t e = r * RUN + lane * PER + (uint32_t)j;
             k[j] = e < rl ? ak[pidx(e)] : PAD_KEY;
             v[j] = e < rl ? av[pidx(e)] : 0u;
         }
-        warp_bitonic_t<16, true>(k, v, lane);
+        warp_bitonic_t<PER, true>(k, v, lane);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint32_t e = r * 512 + lane * 16 + (uint32_t)j;
+        for (int j = 0; j < PER; ++j) {
+            const uint32_t e = r * RUN + lane * PER + (uint32_t)j;
             if (e < rl) { ak[pidx(e)] = k[j]; av[pidx(e)] = v[j]; }
         }
     }
+}
+
+// sort rl <= SMEM_SORT_MAX pairs already placed in (ak, av): warp register sorts of
+// runs of `run` (32..512) elements, then merge rounds; returns 0 if the result is
+// in (ak, av), 1 if in (bk, bv).  Short runs + more merge rounds = lower latency
+// for a CTA working on one list; long runs = fewer instructions.
+__device__ int smem_sort_run(uint64_t* ak, uint32_t* av, uint64_t* bk, uint32_t* bv, uint32_t rl, uint32_t run) {
+    switch (run) {
+        case 32: warp_runs<1>(ak, av, rl); break;
+        case 64: warp_runs<2>(ak, av, rl); break;
+        case 128: warp_runs<4>(ak, av, rl); break;
+        case 256: warp_runs<8>(ak, av, rl); break;
+        default: warp_runs<16>(ak, av, rl); run = 512; break;
+    }
     __syncthreads();
     int in_b = 0;
-    for (uint32_t width = 512; width < rl; width <<= 1) {
-        const uint64_t* sk = in_b ? bk : ak;
-        const uint32_t* sv = in_b ? bv : av;
-        uint64_t* dk = in_b ? ak : bk;
-        uint32_t* dv = in_b ? av : bv;
-        for (uint32_t a0 = 0; a0 < rl; a0 += 2 * width) {
-            const uint32_t na = min(width, rl - a0);
-            const uint32_t nb = a0 + na < rl ? min(width, rl - a0 - na) : 0u;
-            smem_merge(sk, sv, dk, dv, a0, na, nb);
-        }
+    for (uint32_t width = run; width < rl; width <<= 1) {
+        smem_merge_round(in_b ? bk : ak, in_b ? bv : av, in_b ? ak : bk, in_b ? av : bv, rl, width);
         __syncthreads();
         in_b ^= 1;
     }
     return in_b;
 }
 
-__global__ void __launch_bounds__(BIG_THREADS)
+__global__ void __launch_bounds__(LAT_THREADS)
 big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ bucket, uint64_t* __restrict__ ka,
                 uint32_t* __restrict__ va, uint64_t* __restrict__ kb, uint32_t* __restrict__ vb,
                 uint32_t* __restrict__ out, uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg,
@@ -561,6 +570,7 @@ big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ b
                 const uint32_t* __restrict__ status) {
     if (*status) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t nwarp = blockDim.x >> 5;
     uint64_t* sk0 = reinterpret_cast<uint64_t*>(smem_raw);
     uint64_t* sk1 = sk0 + RUN_PAD;
     uint32_t* sv0 = reinterpret_cast<uint32_t*>(sk1 + RUN_PAD);
@@ -578,7 +588,10 @@ big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ b
                 sv0[pidx(e)] = r0 + e;
             }
             __syncthreads();
-            const int in_b = smem_sort_run(sk0, sv0, sk1, sv1, rl);
+            // runs sized so every warp of the CTA gets one (latency), at least 32
+            uint32_t run = 32;
+            while (run < 512 && run * nwarp < rl) run <<= 1;
+            const int in_b = smem_sort_run(sk0, sv0, sk1, sv1, rl, run);
             const uint64_t* rk = in_b ? sk1 : sk0;
             const uint32_t* rv = in_b ? sv1 : sv0;
             if (one_run) {
@@ -674,22 +687,30 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     scatter_kernel<<<rgrid, BIN_THREADS, hist_smem, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.cursor, w.bucket,
                                                           proj->status);
     if ((st = check_launch("scatter_kernel")) != GS_OK) return st;
+    // small batches (single views, pyramids): every list > 256 gets a 16-warp CTA
+    // (latency); large batches: one warp per list <= 512, 4-warp CTAs above (throughput)
+    const bool latency = T <= LAT_TILES;
     warp_sort_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(out->ranges, T, w.bucket, out->sorted_rec,
                                                              out->sorted_gid, out->sorted_key, w.big_count,
-                                                             w.mid_list, w.big_list, proj->status);
-    mid_sort_kernel<<<4 * num_sms(), 256, 0, s>>>(out->ranges, w.bucket, out->sorted_rec, out->sorted_gid,
-                                                  out->sorted_key, w.big_count, w.mid_list, proj->status);
+                                                             w.mid_list, w.big_list, latency ? 0u : WARP_SORT_MAX,
+                                                             proj->status);
     if ((st = check_launch("warp_sort_kernel")) != GS_OK) return st;
+    if (!latency) {
+        mid_sort_kernel<<<4 * num_sms(), 256, 0, s>>>(out->ranges, w.bucket, out->sorted_rec, out->sorted_gid,
+                                                      out->sorted_key, w.big_count, w.mid_list, proj->status);
+        if ((st = check_launch("mid_sort_kernel")) != GS_OK) return st;
+    }
     static bool attr_set = false;
     const int smem = 2 * RUN_PAD * (int)(sizeof(uint64_t) + sizeof(uint32_t));
     if (!attr_set) {
         cudaFuncSetAttribute(big_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
-    big_sort_kernel<<<4 * num_sms(), BIG_THREADS, smem, s>>>(out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb,
-                                                             out->sorted_rec,
-                                                         out->sorted_gid, out->sorted_key, w.big_count, w.big_list,
-                                                         proj->status);
+    const int big_threads = latency ? LAT_THREADS : BIG_THREADS;
+    const int big_grid = latency ? 2 * num_sms() : 4 * num_sms();
+    big_sort_kernel<<<big_grid, big_threads, smem, s>>>(out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb,
+                                                        out->sorted_rec, out->sorted_gid, out->sorted_key, w.big_count,
+                                                        w.big_list, proj->status);
     return check_launch("big_sort_kernel");
 }
 
