@@ -59,7 +59,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 1
+#define GS_ABI_VERSION 2
 #define GS_TILE 16           /* tile edge in pixels */
 #define GS_MAX_FEAT_DIM 64   /* D in [0, 64], D % 4 == 0 */
 #define GS_MAX_VIEWS 65535   /* view index is stored in 16 bits of a record */
@@ -120,7 +120,12 @@ typedef struct gs_scene {
     int32_t reserved;
     const int64_t* block_offsets;  /* [n_blocks + 1] */
     const float* block_bounds;     /* [n_blocks][8] */
-} gs_scene;
+    const void* feat_h;            /* [n][D] IEEE binary16 copy of feat (round to nearest even), or
+                                      NULL; filled by gs_scene_features_f16().  When present and
+                                      D is 16, 32, 48 or 64, gs_rasterize gathers these rows and
+                                      runs the feature contraction on tcgen05 (the features are
+                                      rounded to fp16 either way) */
+} gs_scene;                        /* 96 bytes */
 
 /* Readings Q5, Q7, Q6, Q14, Q15; gs_default_params() returns these. */
 typedef struct gs_params {
@@ -213,6 +218,16 @@ gs_status gs_views_layout(gs_view* views_host, int32_t n_views, int64_t* total_p
  * hot path: call once after loading a partitioned scene.
  */
 gs_status gs_scene_block_bounds(const gs_scene* scene, float* block_bounds_out, void* stream);
+
+/*
+ * feat_h_out[i][c] = (binary16, round to nearest even) scene->feat[i][c] for
+ * the n x D feature matrix of `scene` (its feat_h field is ignored); device
+ * buffer of n * D * 2 bytes, 16-byte aligned, owned by the caller.  Not on the
+ * hot path: call once after loading a scene with features, then set
+ * scene->feat_h.  Errors: GS_INVALID_ARG if D == 0 or a pointer is NULL or
+ * misaligned.
+ */
+gs_status gs_scene_features_f16(const gs_scene* scene, void* feat_h_out, void* stream);
 
 /* Workspace of gs_project: a (view x block) visibility bitmask. */
 size_t gs_project_workspace_bytes(int32_t n_blocks, int32_t n_views);

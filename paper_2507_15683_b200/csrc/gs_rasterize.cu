@@ -21,12 +21,27 @@
 //   * per pixel the skip / stop decisions (power, alpha, Tn) are evaluated with
 //     explicit _rn intrinsics in the oracle's operation order;
 //   * the feature blend F[px][:] += w[px][k] f[k][:] -- the one dense
-//     contraction of the path -- runs on the tensor cores: each warp compacts
-//     the weights of its walked entries into an 8-entry shared buffer and
-//     issues m16n8k8 TF32 MMAs (weights split hi+lo, features rounded once:
-//     error <= 2^-11 sum w|f|, inside the 1e-3 max(1,|f|) tolerance);
+//     contraction of the path -- runs on the tensor cores.  Each warp compacts
+//     the weights of its walked entries into a 16-row shared buffer; a full
+//     buffer is one K = 16 step.  tcgen05 path (D in {16,32,48,64}, fp16
+//     feature rows from gs_scene_features_f16): the warp writes its 32 pixel
+//     rows of A (weights as fp16 hi + lo) to TMEM with tcgen05.st, copies the
+//     16 feature rows into a canonical (no-swizzle, MN-major) smem B tile, and
+//     one lane issues two M=128 N=D K=16 kind::f16 MMAs whose
+//     disable-output-lane mask leaves only the warp's own 32 TMEM lanes
+//     writable -- the 8 warps share two D-column accumulators (one per lane
+//     group of 4 warps) without synchronising with each other; completion is
+//     tracked per warp and buffer by tcgen05.commit -> mbarrier, and the tile's
+//     epilogue reads the accumulator row with tcgen05.ld.  mma.sync path
+//     (other D, or no fp16 copy): m16n8k16 FP16 MMAs with register
+//     accumulators.  Both: weights split hi + lo (~2^-22 relative), features
+//     rounded once to fp16: error <= 2^-11 sum w|f|, inside the 1e-3
+//     max(1,|f|) tolerance;
 //   * warp-ballot early termination once all 32 pixels have T < t_min.
 #include <cuda_fp16.h>
+
+#include <cstdio>
+#include <cstdlib>
 
 #include "gs_common.cuh"
 
@@ -100,18 +115,69 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// ---- tcgen05 (5th-gen tensor cores, TMEM accumulators) -------------------------
+// Used for the feature contraction when D is a multiple of 16 (N = D of an M = 128
+// MMA).  Each consumer warp owns the 32 TMEM lanes of its lane quarter (warp % 4)
+// inside a D-column accumulator region shared with the three other warps of its
+// group (warp / 4); its MMAs disable every other lane (disable-output-lane mask),
+// so the 8 warps issue independently without racing on TMEM.
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* f) {
+    uint32_t d[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]),
+          "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(d[i]);
+}
+// D[tmem] (+)= A[tmem] B[smem]: M = 128, N = n, K = 16, fp16 inputs, fp32 accumulation;
+// only the 32 TMEM lanes of quarter q are written
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate, uint32_t q) {
+    const uint32_t m0 = q == 0 ? 0u : 0xffffffffu, m1 = q == 1 ? 0u : 0xffffffffu;
+    const uint32_t m2 = q == 2 ? 0u : 0xffffffffu, m3 = q == 3 ? 0u : 0xffffffffu;
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(m0), "r"(m1), "r"(m2), "r"(m3)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+// TMEM columns of a CTA: two group accumulators (D columns each) + per group two
+// A buffers of 16 columns (fp16 weight pairs: 8 hi + 8 lo)
+template <int D>
+struct TcCfg {
+    static constexpr bool eligible = D == 16 || D == 32 || D == 48 || D == 64;
+    static constexpr uint32_t need = 2 * D + 64;
+    static constexpr uint32_t cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
+};
+
 struct StageMeta {
     uint32_t tile, c0;
     int32_t cnt, view;
     uint32_t flags, pad0, pad1, pad2;
 };
 
-template <int D, bool CONTRIB>
+template <int D, bool CONTRIB, bool TC>
 struct RasterSmem {
-    static constexpr int FS = D > 0 ? D + 8 : 1;   // feature row stride (floats)
+    static constexpr int FS = D > 0 ? D + 8 : 1;   // fp32 feature row stride (floats)
+    static constexpr int FSH = D + 8;              // fp16 feature row stride (halves; 16-B aligned rows)
     static constexpr bool WB = D > 0 || CONTRIB;   // weight rows are staged (features and/or contributions)
     float4 rec[NST][SE + 1][4];                    // 64-byte records; row SE = null record (opacity 0)
-    float feat[D > 0 ? NST : 1][D > 0 ? SE + 1 : 1][FS];
+    float feat[(D > 0 && !TC) ? NST : 1][(D > 0 && !TC) ? SE + 1 : 1][FS];
+    alignas(16) __half feath[TC ? NST : 1][TC ? SE + 1 : 1][TC ? FSH : 8];   // tcgen05 path: fp16 rows
     alignas(16) float wbuf[WB ? NCW : 1][WB_ROWS][WB_STRIDE]; // per-warp compacted weights [k][pixel]
     uint32_t slots[CONTRIB ? NST * (SE + 1) : 1];  // record slot of each ring row (contributions)
     alignas(16) int ent[NCW][SE + 2];                // per-warp compacted ballot list (flat ring rows)
@@ -119,6 +185,11 @@ struct RasterSmem {
     StageMeta meta[NST];
     uint64_t full[NST];
     uint64_t empty[NST];
+    // tcgen05 path: per-warp double-buffered B tile (16 x D fp16, canonical MN-major,
+    // no swizzle) and the MMA-completion barriers of its two buffers
+    alignas(128) __half bbuf[TC ? NCW : 1][2][TC ? 16 * D : 8];
+    uint64_t mma_bar[TC ? NCW : 1][2];
+    uint32_t tmem_base;
 };
 
 // min over the 8x4 pixel-centre rectangle [x0,x1]x[y0,y1] of
@@ -157,32 +228,52 @@ __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, f
 // Persistent kernel: each CTA renders a sequence of tiles handed out in order by
 // a dynamic scheduler.  The producer warp runs ahead across tile boundaries so
 // the consumers never wait for a tile's first records.
-template <int D, bool CONTRIB>
-__global__ void __launch_bounds__(RT_THREADS, (D > 32 ? 1 : (D > 0 ? 2 : 4)))
+#ifndef GS_TC_MIN_BLOCKS
+#define GS_TC_MIN_BLOCKS 3
+#endif
+template <int D, bool CONTRIB, bool TC>
+__global__ void __launch_bounds__(RT_THREADS, (TC ? (D > 32 ? 1 : GS_TC_MIN_BLOCKS) : (D > 32 ? 1 : (D > 0 ? 2 : 4))))
 rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record* __restrict__ rec,
                  const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ sorted_gid,
                  const uint32_t* __restrict__ ranges, uint32_t n_tiles, uint32_t* __restrict__ tile_sched,
-                 const float* __restrict__ feat,
+                 const float* __restrict__ feat, const __half* __restrict__ feat_h,
                  gs_params P, float* __restrict__ out_rgb, float* __restrict__ out_depth,
                  float* __restrict__ out_alpha, float* __restrict__ out_feat,
                  unsigned long long* __restrict__ contrib, const uint32_t* __restrict__ status) {
-    constexpr bool WB = RasterSmem<D, CONTRIB>::WB;
+    static_assert(!TC || TcCfg<D>::eligible, "tcgen05 feature path needs D in {16, 32, 48, 64}");
+    using Smem = RasterSmem<D, CONTRIB, TC>;
+    constexpr bool WB = Smem::WB;
     if (*status) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    RasterSmem<D, CONTRIB>& sm = *reinterpret_cast<RasterSmem<D, CONTRIB>*>(smem_raw);
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < NST * 4; i += blockDim.x) sm.rec[i / 4][SE][i % 4] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if constexpr (D > 0)
-        for (int i = threadIdx.x; i < NST * RasterSmem<D, CONTRIB>::FS; i += blockDim.x)
-            sm.feat[i / RasterSmem<D, CONTRIB>::FS][SE][i % RasterSmem<D, CONTRIB>::FS] = 0.f;
+    if constexpr (TC)
+        for (int i = threadIdx.x; i < NST * Smem::FSH; i += blockDim.x)
+            sm.feath[i / Smem::FSH][SE][i % Smem::FSH] = __float2half_rn(0.f);
+    else if constexpr (D > 0)
+        for (int i = threadIdx.x; i < NST * Smem::FS; i += blockDim.x) sm.feat[i / Smem::FS][SE][i % Smem::FS] = 0.f;
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(&sm.full[s], 33);     // 32 cp.async arrivals + 1 metadata arrival
             mbar_init(&sm.empty[s], NCW);
         }
+        if constexpr (TC)
+            for (int w = 0; w < NCW; ++w) { mbar_init(&sm.mma_bar[w][0], 1); mbar_init(&sm.mma_bar[w][1], 1); }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    if constexpr (TC) {
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                             smem_u32(&sm.tmem_base)),
+                         "r"(TcCfg<D>::cols)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+        }
+        tc_fence_before();
+    }
     __syncthreads();
+    if constexpr (TC) tc_fence_after();
 
     if (warp == NCW) {
         // ------------------------------------------------------------ producer
@@ -264,7 +355,11 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     if constexpr (CONTRIB) sm.slots[buf * (SE + 1) + j] = slot[q];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) cp_async16(&sm.rec[buf][j][e], src + e, pol);
-                    if constexpr (D > 0) {
+                    if constexpr (TC) {
+                        const uint4* fs = reinterpret_cast<const uint4*>(feat_h + (int64_t)gid[q] * D);
+#pragma unroll
+                        for (int e = 0; e < D / 8; ++e) cp_async16(&sm.feath[buf][j][e * 8], fs + e, pol);
+                    } else if constexpr (D > 0) {
                         const float4* fs = reinterpret_cast<const float4*>(feat + (int64_t)gid[q] * D);
 #pragma unroll
                         for (int e = 0; e < D / 4; ++e) cp_async16(&sm.feat[buf][j][e * 4], fs + e, pol);
@@ -292,8 +387,16 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
 
     // ---------------------------------------------------------------- consumers
     const int g = (int)(lane >> 2), t4 = (int)(lane & 3u);
-    constexpr int NTP = D > 0 ? (D + 7) / 8 : 1;
-    float acc[2][NTP][4];
+    constexpr int NTP = (D > 0 && !TC) ? (D + 7) / 8 : 1;
+    float acc[TC ? 1 : 2][NTP][4];
+    // tcgen05 state: TMEM addresses of this warp's accumulator / A buffers, k-step count
+    const uint32_t tq = warp & 3u, tgrp = warp >> 2;
+    const uint32_t tmem = TC ? sm.tmem_base : 0u;
+    const uint32_t tD = tmem + tgrp * (uint32_t)D;                     // MMA operand address (lane field 0)
+    const uint32_t tA = tmem + 2u * (uint32_t)D + tgrp * 32u;
+    const uint32_t my_lanes = (tq * 32u) << 16;
+    constexpr uint32_t IDESC = (1u << 4) | (1u << 16) | ((uint32_t)(D >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    uint32_t kstep = 0, tile_acc = 0;
     // per-tile state
     const gs_view* V = nullptr;
     int W = 0, H = 0, sx = 0, sy = 0, px = 0, py = 0;
@@ -319,7 +422,52 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     atomicAdd(&contrib[sm.slots[kr]], (unsigned long long)__float2ll_rn(sum * 4294967296.0f));
             }
         }
-        if constexpr (D > 0) {
+        if constexpr (TC) {
+            // one k-step of 16 weight rows on tcgen05: A (this warp's 32 pixel rows, fp16
+            // hi + lo weight pairs) -> TMEM, B (16 feature rows -> fp16) -> the canonical
+            // smem tile, then two lane-masked M=128 N=D K=16 MMAs issued by lane 0
+            const uint32_t b = kstep & 1u;
+            if (kstep >= 2) mbar_wait(&sm.mma_bar[warp][b], ((kstep >> 1) - 1u) & 1u);
+            uint32_t hi[8], lo[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float w0 = sm.wbuf[warp][2 * c][lane], w1 = sm.wbuf[warp][2 * c + 1][lane];
+                const __half2 h = __floats2half2_rn(w0, w1);
+                const float2 hf = __half22float2(h);
+                const __half2 l = __floats2half2_rn(w0 - hf.x, w1 - hf.y);
+                hi[c] = *reinterpret_cast<const uint32_t*>(&h);
+                lo[c] = *reinterpret_cast<const uint32_t*>(&l);
+            }
+            tmem_st8(tA + my_lanes + b * 16u, hi);
+            tmem_st8(tA + my_lanes + b * 16u + 8u, lo);
+            // the B tile is built while the TMEM stores are in flight
+            constexpr int NC8 = D / 8;
+            const __half* fb = &sm.feath[0][0][0];
+            __half* bt = &sm.bbuf[warp][b][0];
+#pragma unroll
+            for (int c = (int)lane; c < 16 * NC8; c += 32) {
+                const int k = c / NC8, n8 = c % NC8;
+                const uint4 o = *reinterpret_cast<const uint4*>(fb + sm.kent[warp][k] * Smem::FSH + n8 * 8);
+                // element (k, n) at n8*64 + (k%8)*8 + (k/8)*8*D halves (SBO = 128 B, LBO = 16 D B)
+                *reinterpret_cast<uint4*>(bt + n8 * 64 + (k & 7) * 8 + (k >> 3) * 8 * D) = o;
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                tc_fence_after();
+                const uint64_t desc = (uint64_t)((smem_u32(bt) >> 4) & 0x3FFFu) |
+                                      ((uint64_t)(((16u * D) >> 4) & 0x3FFFu) << 16) |
+                                      ((uint64_t)((128u >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46);
+                tc_mma_f16(tD, tA + b * 16u, desc, IDESC, tile_acc, tq);
+                tc_mma_f16(tD, tA + b * 16u + 8u, desc, IDESC, 1u, tq);
+                tc_commit(&sm.mma_bar[warp][b]);
+            }
+            __syncwarp();
+            tile_acc = 1;
+            ++kstep;
+        } else if constexpr (D > 0) {
             // m16n8k16 FP16 MMAs: weights split hi + lo (fp16 pairs, ~2^-22 exact), feature
             // rows rounded once to fp16 (error <= 2^-11 sum w|f|, inside 1e-3 max(1,|f|))
             for (int k0 = kb; k0 < ke; k0 += 16) {
@@ -339,7 +487,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     }
                 }
                 const float* fb = &sm.feat[0][0][0];
-                constexpr int FS = RasterSmem<D, CONTRIB>::FS;
+                constexpr int FS = Smem::FS;
                 const float* f0 = fb + sm.kent[warp][k0 + 2 * t4] * FS;
                 const float* f1 = fb + sm.kent[warp][k0 + 2 * t4 + 1] * FS;
                 const float* f2 = fb + sm.kent[warp][k0 + 2 * t4 + 8] * FS;
@@ -417,10 +565,13 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             T = 1.0f; C0 = C1 = C2 = Dz = 0.f;
             done = !inside;
             warp_done = __all_sync(0xffffffffu, done);
+            tile_acc = 0;
+            if constexpr (!TC) {
 #pragma unroll
-            for (int a = 0; a < 2; ++a)
+                for (int a = 0; a < 2; ++a)
 #pragma unroll
-                for (int n = 0; n < NTP; ++n) acc[a][n][0] = acc[a][n][1] = acc[a][n][2] = acc[a][n][3] = 0.f;
+                    for (int n = 0; n < NTP; ++n) acc[a][n][0] = acc[a][n][1] = acc[a][n][2] = acc[a][n][3] = 0.f;
+            }
         }
         if (!warp_done && m.cnt > 0) {
             const int flat0 = buf * (SE + 1);
@@ -484,7 +635,29 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 __stcs(&out_depth[po + loc], Dz);
                 __stcs(&out_alpha[po + loc], 1.0f - T);
             }
-            if constexpr (D > 0) {
+            if constexpr (TC) {
+                // this lane's pixel row of the group accumulator: D channels
+                float f[D];
+                if (tile_acc) {
+                    const uint32_t jl = kstep - 1u;
+                    mbar_wait(&sm.mma_bar[warp][jl & 1u], (jl >> 1) & 1u);
+                    tc_fence_after();
+#pragma unroll
+                    for (int c = 0; c < D; c += 16) tmem_ld16(tD + my_lanes + (uint32_t)c, f + c);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                } else {
+#pragma unroll
+                    for (int c = 0; c < D; ++c) f[c] = 0.f;
+                }
+                if (inside) {
+                    float* q = out_feat + (int64_t)D * po + (int64_t)py * W + px;
+#pragma unroll
+                    for (int c = 0; c < D; ++c) {
+                        __stcs(q, f[c]);
+                        q += HW;
+                    }
+                }
+            } else if constexpr (D > 0) {
                 // accumulator (a, n, i): pixel (sx + g, sy + 2a + (i >> 1)), channel 8n + 2 t4 + (i & 1);
                 // one 64-bit base pointer per (a, i) and a plain pointer walk over the channel planes
                 const int fx = sx + g;
@@ -512,17 +685,46 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
         for (; rel < lim; ++rel)
             if (lane == 0) mbar_arrive(&sm.empty[rel % NST]);
     }
+    if constexpr (TC) {
+        // every MMA was waited for at its tile's epilogue; free TMEM once all consumers are done
+        tc_fence_before();
+        asm volatile("bar.sync 1, %0;\n" ::"n"(NCW * 32) : "memory");
+        if (warp == 0) {
+            tc_fence_after();
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TcCfg<D>::cols)
+                         : "memory");
+        }
+    }
 }
 
-template <int D, bool CONTRIB>
+template <int D, bool CONTRIB, bool TC>
 gs_status launch(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins, const gs_view* views_dev,
                  int n_views, int64_t T, const gs_params* P, gs_images* out, cudaStream_t s) {
-    const int smem = (int)sizeof(RasterSmem<D, CONTRIB>);
+    const int smem = (int)sizeof(RasterSmem<D, CONTRIB, TC>);
     static int blocks_per_sm = 0;
     if (blocks_per_sm == 0) {
-        cudaFuncSetAttribute(rasterize_kernel<D, CONTRIB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(rasterize_kernel<D, CONTRIB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rasterize_kernel<D, CONTRIB>, RT_THREADS, smem);
+        cudaFuncSetAttribute(rasterize_kernel<D, CONTRIB, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(rasterize_kernel<D, CONTRIB, TC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        const cudaError_t e =
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rasterize_kernel<D, CONTRIB, TC>, RT_THREADS, smem);
+        if (TC) {
+            // the occupancy calculator reports 1 CTA/SM for kernels that allocate TMEM;
+            // the real limits are shared memory, registers and the 512 TMEM columns
+            int dev = 0, smem_sm = 0, regs_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+            cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, rasterize_kernel<D, CONTRIB, TC>);
+            const int by_smem = smem_sm / (smem + 1024);
+            const int by_regs = regs_sm / (std::max(fa.numRegs, 1) * RT_THREADS);
+            const int by_tmem = 512 / (int)TcCfg<D>::cols;
+            blocks_per_sm = std::min(std::min(by_smem, by_regs), by_tmem);
+        }
+        if (const char* o = getenv("GS_RASTER_CTAS_PER_SM")) blocks_per_sm = atoi(o);
+        if (getenv("GS_DEBUG"))
+            fprintf(stderr, "[gs] rasterize<%d,%d>: smem %d B, occupancy %d CTAs/SM (%s)\n", D, (int)CONTRIB, smem,
+                    blocks_per_sm, cudaGetErrorString(e));
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     const int64_t grid =
@@ -530,9 +732,9 @@ gs_status launch(const gs_scene* scene, const gs_projected* proj, const gs_bins*
     if (grid <= 0) return GS_OK;
     if (bins->tile_sched) cudaMemsetAsync(bins->tile_sched, 0, sizeof(uint32_t), s);
     if (CONTRIB) cudaMemsetAsync(proj->contrib, 0, sizeof(unsigned long long) * (size_t)n_views * proj->rec_capacity, s);
-    rasterize_kernel<D, CONTRIB><<<(unsigned)grid, RT_THREADS, smem, s>>>(
+    rasterize_kernel<D, CONTRIB, TC><<<(unsigned)grid, RT_THREADS, smem, s>>>(
         views_dev, n_views, proj->rec, bins->sorted_rec, bins->sorted_gid, bins->ranges, (uint32_t)T, bins->tile_sched,
-        scene->feat,
+        scene->feat, reinterpret_cast<const __half*>(scene->feat_h),
         *P, out->rgb, out->depth, out->alpha, out->feat, proj->contrib, proj->status);
     return check_launch("rasterize_kernel");
 }
@@ -560,16 +762,53 @@ extern "C" gs_status gs_rasterize(const gs_scene* scene, const gs_projected* pro
     GS_REQUIRE(((uintptr_t)proj->rec & 15) == 0 && (scene->feat_dim == 0 || ((uintptr_t)scene->feat & 15) == 0),
                GS_INVALID_ARG, "records and features must be 16-byte aligned");
     cudaStream_t s = (cudaStream_t)stream;
+    const bool tc = scene->feat_h != nullptr;
+    GS_REQUIRE(!tc || ((uintptr_t)scene->feat_h & 15) == 0, GS_INVALID_ARG, "feat_h must be 16-byte aligned");
     switch (scene->feat_dim) {
 #define GS_CASE(d) \
     case d:                                                                                       \
-        return proj->contrib ? launch<d, true>(scene, proj, bins, views_dev, n_views, T, params, out, s) \
-                             : launch<d, false>(scene, proj, bins, views_dev, n_views, T, params, out, s);
-        GS_CASE(0) GS_CASE(4) GS_CASE(8) GS_CASE(12) GS_CASE(16) GS_CASE(20) GS_CASE(24) GS_CASE(28) GS_CASE(32)
-        GS_CASE(36) GS_CASE(40) GS_CASE(44) GS_CASE(48) GS_CASE(52) GS_CASE(56) GS_CASE(60) GS_CASE(64)
+        return proj->contrib ? launch<d, true, false>(scene, proj, bins, views_dev, n_views, T, params, out, s) \
+                             : launch<d, false, false>(scene, proj, bins, views_dev, n_views, T, params, out, s);
+#define GS_CASE_TC(d) \
+    case d:                                                                                              \
+        if (tc)                                                                                          \
+            return proj->contrib ? launch<d, true, true>(scene, proj, bins, views_dev, n_views, T, params, out, s) \
+                                 : launch<d, false, true>(scene, proj, bins, views_dev, n_views, T, params, out, s); \
+        return proj->contrib ? launch<d, true, false>(scene, proj, bins, views_dev, n_views, T, params, out, s) \
+                             : launch<d, false, false>(scene, proj, bins, views_dev, n_views, T, params, out, s);
+        GS_CASE(0) GS_CASE(4) GS_CASE(8) GS_CASE(12) GS_CASE_TC(16) GS_CASE(20) GS_CASE(24) GS_CASE(28)
+        GS_CASE_TC(32) GS_CASE(36) GS_CASE(40) GS_CASE(44) GS_CASE_TC(48) GS_CASE(52) GS_CASE(56) GS_CASE(60)
+        GS_CASE_TC(64)
 #undef GS_CASE
+#undef GS_CASE_TC
         default:
             gs::set_error("feat_dim = %d unsupported", scene->feat_dim);
             return GS_UNSUPPORTED;
     }
+}
+
+namespace gs {
+namespace {
+__global__ void features_f16_kernel(const float4* __restrict__ f, uint2* __restrict__ out, int64_t n4) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 x = f[i];
+        const __half2 a = __floats2half2_rn(x.x, x.y), b = __floats2half2_rn(x.z, x.w);
+        out[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+    }
+}
+}  // namespace
+}  // namespace gs
+
+extern "C" gs_status gs_scene_features_f16(const gs_scene* scene, void* feat_h_out, void* stream) {
+    gs_status st = validate_scene(scene, false);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(scene->feat_dim > 0 && scene->feat != nullptr, GS_INVALID_ARG, "scene has no features");
+    GS_REQUIRE(feat_h_out != nullptr && ((uintptr_t)feat_h_out & 15) == 0 && ((uintptr_t)scene->feat & 15) == 0,
+               GS_INVALID_ARG, "feature buffers must be non-NULL and 16-byte aligned");
+    const int64_t n4 = scene->n * scene->feat_dim / 4;
+    if (n4 == 0) return GS_OK;
+    const int64_t blocks = std::min<int64_t>((n4 + 255) / 256, (int64_t)num_sms() * 8);
+    features_f16_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const float4*>(scene->feat), reinterpret_cast<uint2*>(feat_h_out), n4);
+    return check_launch("features_f16_kernel");
 }

@@ -18,7 +18,8 @@ import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgs.so")
+# GS_LIB overrides the library path (experiments with alternative builds)
+LIB_PATH = os.environ.get("GS_LIB") or os.path.join(_PKG, "libgs.so")
 
 GS_OK, GS_INVALID_ARG, GS_UNSUPPORTED, GS_WORKSPACE_TOO_SMALL, GS_CUDA_ERROR = range(5)
 GS_STATUS_RECORD_OVERFLOW = 0x1
@@ -43,7 +44,7 @@ class gs_scene(ctypes.Structure):
                 ("pos", ctypes.c_void_p), ("quat", ctypes.c_void_p), ("scale", ctypes.c_void_p),
                 ("opacity", ctypes.c_void_p), ("sh", ctypes.c_void_p), ("feat", ctypes.c_void_p),
                 ("n_blocks", ctypes.c_int32), ("reserved", ctypes.c_int32),
-                ("block_offsets", ctypes.c_void_p), ("block_bounds", ctypes.c_void_p)]
+                ("block_offsets", ctypes.c_void_p), ("block_bounds", ctypes.c_void_p), ("feat_h", ctypes.c_void_p)]
 
 
 class gs_params(ctypes.Structure):
@@ -68,6 +69,7 @@ class gs_images(ctypes.Structure):
 
 
 EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_layout", "gs_scene_block_bounds",
+           "gs_scene_features_f16",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_backproject", "gs_visibility_score", "gs_visibility_workspace_bytes"]
 
@@ -122,7 +124,7 @@ def default_params() -> gs_params:
 class DeviceScene:
     """Scene planes resident in HBM (SoA float32, block-major when partitioned)."""
 
-    def __init__(self, scene, device="cuda", compute_block_bounds: bool = True):
+    def __init__(self, scene, device="cuda", compute_block_bounds: bool = True, use_f16_features: bool = True):
         dev = torch.device(device)
         t = lambda a, dt=torch.float32: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)
         self.n = scene.n
@@ -136,7 +138,15 @@ class DeviceScene:
         if scene.block_offsets is not None and len(scene.block_offsets) > 1:
             self.block_offsets = t(scene.block_offsets, torch.int64)
             self.block_bounds = torch.zeros((len(scene.block_offsets) - 1, 8), device=dev)
+        # fp16 copy of the features (scene preparation, like the block bounds): the
+        # rasterizer's tcgen05 feature path gathers these 2-byte rows
+        self.feat_h = None
+        if self.feat is not None and use_f16_features:
+            self.feat_h = torch.empty(self.feat.shape, dtype=torch.float16, device=dev)
         self.struct = self._make_struct()
+        if self.feat_h is not None:
+            _check(lib().gs_scene_features_f16(ctypes.byref(self.struct), _ptr(self.feat_h), _stream(None)),
+                   "gs_scene_features_f16")
         if self.block_bounds is not None and compute_block_bounds:
             _check(lib().gs_scene_block_bounds(ctypes.byref(self.struct), _ptr(self.block_bounds), _stream(None)),
                    "gs_scene_block_bounds")
@@ -150,6 +160,7 @@ class DeviceScene:
         s.n, s.sh_degree, s.feat_dim = self.n, self.sh_degree, self.feat_dim
         s.pos, s.quat, s.scale = _ptr(self.pos), _ptr(self.quat), _ptr(self.scale)
         s.opacity, s.sh, s.feat = _ptr(self.opacity), _ptr(self.sh), _ptr(self.feat)
+        s.feat_h = _ptr(getattr(self, "feat_h", None))
         if use_blocks and self.block_offsets is not None:
             s.n_blocks = self.n_blocks
             s.block_offsets, s.block_bounds = _ptr(self.block_offsets), _ptr(self.block_bounds)
@@ -159,7 +170,7 @@ class DeviceScene:
         return self._make_struct(use_blocks=False)
 
     def nbytes(self) -> int:
-        ts = [self.pos, self.quat, self.scale, self.opacity, self.sh, self.feat]
+        ts = [self.pos, self.quat, self.scale, self.opacity, self.sh, self.feat, self.feat_h]
         return sum(x.numel() * x.element_size() for x in ts if x is not None)
 
 

@@ -24,7 +24,7 @@ def G():
 def declared_functions():
     src = open(os.path.join(ROOT, "include", "gs.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(gs_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(gs_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declares_the_four_calls():
@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol(G):
 
 def test_abi_version_and_defaults(G):
     L = G.lib()
-    assert L.gs_abi_version() == 1
+    assert L.gs_abi_version() == 2
     p = G.default_params()
     import oracle
     o = oracle.Params()
@@ -52,7 +52,7 @@ def test_abi_version_and_defaults(G):
 
 def test_struct_sizes_match_header(G):
     assert ctypes.sizeof(G.gs.gs_view) == 88
-    assert ctypes.sizeof(G.gs.gs_scene) == 88
+    assert ctypes.sizeof(G.gs.gs_scene) == 96
     assert ctypes.sizeof(G.gs.gs_params) == 24
     assert G.gs.RECORD_BYTES == 64
 

@@ -24,8 +24,8 @@ def G():
     return G
 
 
-def _gpu_render(G, scene, views, use_blocks=True, debug_keys=True, feat=True, **kw):
-    ds = G.DeviceScene(scene)
+def _gpu_render(G, scene, views, use_blocks=True, debug_keys=True, feat=True, f16=True, **kw):
+    ds = G.DeviceScene(scene, use_f16_features=f16)
     r = G.Renderer(ds, views, debug_keys=debug_keys, use_blocks=use_blocks, **kw)
     r.render()
     torch.cuda.synchronize()
@@ -87,6 +87,26 @@ def test_random_tiny_ragged(G, orc, seed):
     r = _gpu_render(G, sc, [v])
     o = orc.render(sc, v, a_min=0.5)
     compare_view(G, r, 0, sc, v, o)
+
+
+@pytest.mark.parametrize("D,seed", [(16, 0), (32, 1), (48, 2), (64, 3), (32, 4), (16, 5)])
+def test_feature_contraction_tcgen05_and_mma_sync(G, orc, D, seed):
+    """Feature blend F = sum_k w_k f_k on both tensor-core paths:
+    tcgen05 (fp16 feature rows, TMEM accumulators; D in {16, 32, 48, 64}) and
+    mma.sync (fp32 rows).  Both against the oracle, ragged image sizes."""
+    rng = np.random.default_rng(1300 + seed)
+    sc = random_tiny_scene(rng, int(rng.integers(100, 600)), feat_dim=D, sh_degree=seed % 4)
+    W, H = int(rng.integers(20, 120)), int(rng.integers(10, 90))
+    v = synth.make_view(np.eye(3), np.zeros(3), 40.0, 40.0, W / 2 - 0.5, H / 2 - 0.5, W, H)
+    o = orc.render(sc, v, a_min=0.5)
+    feats = []
+    for f16 in (True, False):
+        r = _gpu_render(G, sc, [v], f16=f16)
+        compare_view(G, r, 0, sc, v, o)
+        feats.append(r.view_images(0)["feat"].clone())
+    # same fp16-rounded features and hi+lo weights: the paths differ by fp32 summation order only
+    scale = max(1.0, float(np.abs(sc.feat).max()))
+    assert float((feats[0] - feats[1]).abs().max()) <= 1e-4 * scale
 
 
 def test_empty_scene(G, orc):
