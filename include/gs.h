@@ -138,18 +138,22 @@ typedef struct gs_params {
 } gs_params;
 
 /*
- * One projected (view, Gaussian) record, 64 bytes.  u, v, z, conic, rect,
- * radius are computed in IEEE fp32 in the operation order of DESIGN.md §4.1
- * (bit-identical to the oracle); rgb is SH colour (tolerance only); q_cut is
- * the alpha >= alpha_min ellipse threshold on q(d) = d^T conic d,
- * 2 ln(opacity / alpha_min), inflated by 5% + 0.01 (used only by the
- * rasterizer to skip provably-zero work).
+ * One projected (view, Gaussian) record, 64 bytes.  u, v, z, the exponent
+ * coefficients, rect, radius are computed in IEEE fp32 in the operation order
+ * of DESIGN.md §4.1 (bit-identical to the oracle); rgb is SH colour
+ * (tolerance only).  The Gaussian exponent at offset d = mean - pixel is, in
+ * log2 units (reading Q29), p(d) = dx (ea dx + eb dy) + ec dy dy =
+ * log2(e) * (-1/2) d^T conic d, with ea = k conic_a, eb = 2k conic_b,
+ * ec = k conic_c and k = fp32(-log2(e)/2) -- power-of-two multiples of one
+ * rounded constant, so conic = (ea, eb/2, ec)/k.  e_cut = k (2 ln(opacity /
+ * alpha_min) 1.05 + 0.01): p(d) < e_cut implies alpha < alpha_min with margin
+ * (used only by the rasterizer to skip provably-zero work).
  */
 typedef struct gs_record {
     float u, v;                       /* pixel-space mean */
-    float conic_a, conic_b, conic_c;  /* inverse 2D covariance (a, b; b, c) */
+    float ea, eb, ec;                 /* exponent coefficients, log2 units (see above) */
     float opacity;
-    float q_cut;
+    float e_cut;
     float reserved;
     float rgb[3];
     float z;                          /* camera-space depth (depth key = its bits, O9) */

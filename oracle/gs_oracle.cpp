@@ -347,6 +347,10 @@ struct PixelOut {
     int64_t evals, blends;
 };
 
+// Q29: the Gaussian exponent is evaluated in log2 units with the fp32 constant
+// k = -log2(e)/2 (the literal rounds to the nearest fp32)
+const float K_EXP2 = -0.72134752044448170368f;
+
 // flag bands (Q20): alpha within 2^-18 (relative) of alpha_min, Tn within 2^-12 of t_min
 const double FLAG_ALPHA_REL = 1.0 / 262144.0;
 const double FLAG_T_REL = 1.0 / 4096.0;
@@ -366,14 +370,17 @@ void composite_pixel(const Records& rc, const or_params* P, int32_t pxi, int32_t
         o.evals++;
         // 1. offset of the mean from the pixel centre (integer centres, Q4)
         const float dx = rc.u[i] - pxf, dy = rc.v[i] - pyf;
-        // 2. power = -0.5 (ca dx dx + cc dy dy) - cb dx dy   (fp32, pinned order)
+        // 2. power = -0.5 (ca dx dx + cc dy dy) - cb dx dy, evaluated in log2 units (reading
+        //    Q29): p = power log2(e) = dx (ea dx + eb dy) + ec dy dy with ea = k ca, eb = 2k cb,
+        //    ec = k cc, k = fp32(-log2(e) / 2), fp32 fused multiply-adds in this order
         const float ca = rc.conic[i * 3 + 0], cb = rc.conic[i * 3 + 1], cc = rc.conic[i * 3 + 2];
-        const float t1 = (ca * dx) * dx, t2 = (cc * dy) * dy, t3 = (cb * dx) * dy;
-        const float power = -0.5f * (t1 + t2) - t3;
+        const float ea = K_EXP2 * ca, eb = (2.0f * K_EXP2) * cb, ec = K_EXP2 * cc;
+        const float p = std::fmaf(dx, std::fmaf(ea, dx, eb * dy), (ec * dy) * dy);
         // 3. skip if power > 0
-        if (power > 0.0f) continue;
-        // 4. alpha = min(alpha_max, o exp(power)); exp in fp64 rounded once to fp32
-        const float araw = (float)((double)rc.opacity[i] * std::exp((double)power));
+        if (p > 0.0f) continue;
+        // 4. alpha = min(alpha_max, o exp(power)) = min(alpha_max, o 2^p); 2^p in fp64 rounded
+        //    once to fp32
+        const float araw = (float)((double)rc.opacity[i] * std::exp2((double)p));
         if (std::fabs((double)araw - (double)P->alpha_min) <= FLAG_ALPHA_REL * P->alpha_min)
             o.flags |= 1;
         const float alpha = std::min(P->alpha_max, araw);

@@ -19,6 +19,9 @@
 namespace gs {
 namespace {
 
+// reading Q29: k = -log2(e)/2 as the nearest fp32 (same literal as the oracle's)
+constexpr float K_EXP2 = -0.72134752044448170368f;
+
 struct ViewConst {        // per-view constants (pinned fp32, computed once per batch)
     float lox, hix, loy, hiy;   // Jacobian clamp bounds on x/z, y/z (Q6)
     float ccx, ccy, ccz;        // camera centre in world, -R^T t (SH direction)
@@ -339,12 +342,15 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
                     r.y0 = (uint16_t)fmaxf(fy0, 0.0f);
                     r.y1 = (uint16_t)fminf(fy1, c.tyf - 1.0f);
                     r.u = u; r.v = v; r.z = pz;
-                    r.conic_a = ca; r.conic_b = cb; r.conic_c = ccn;
+                    // exponent coefficients in log2 units (reading Q29): k = fp32(-log2(e)/2),
+                    // ea = k ca, eb = 2k cb, ec = k cc
+                    r.ea = K_EXP2 * ca; r.eb = (2.0f * K_EXP2) * cb; r.ec = K_EXP2 * ccn;
                     r.opacity = op;
                     // alpha >= alpha_min  <=>  q(d) = d^T conic d <= thr = 2 ln(o / alpha_min).
-                    // q_cut inflates thr (5% + 0.01) so the rasterizer's per-warp ellipse cull stays
-                    // conservative against fp32 evaluation noise of power and exp.
-                    r.q_cut = thr * 1.05f + 0.01f;
+                    // thr inflated by 5% + 0.01 so the rasterizer's per-warp ellipse cull stays
+                    // conservative against fp32 evaluation noise of the exponent and exp2, then
+                    // scaled to log2 units: cull iff max over the rectangle of p(d) < e_cut.
+                    r.e_cut = K_EXP2 * (thr * 1.05f + 0.01f);
                     r.reserved = 0.0f;
                     r.gid = (uint32_t)i;
                     r.view_radius = (uint32_t)vi | ((uint32_t)fminf(rad, 65535.0f) << 16);

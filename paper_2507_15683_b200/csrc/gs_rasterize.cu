@@ -15,7 +15,7 @@
 //     running ahead across tile boundaries; consumers release stages through
 //     "empty" mbarriers -- no CTA-wide barrier anywhere in the loop;
 //   * exact warp-level culling: each lane tests one staged entry: does the
-//     entry's alpha >= alpha_min ellipse (q <= q_cut, inflated) touch the warp's
+//     entry's alpha >= alpha_min ellipse (p >= e_cut, inflated) touch the warp's
 //     8x4 pixel rectangle?  A ballot gives the entries the warp walks
 //     (conservative, so it never drops a Gaussian the oracle blends -- Q11);
 //   * per pixel the skip / stop decisions (power, alpha, Tn) are evaluated with
@@ -192,37 +192,36 @@ struct RasterSmem {
     uint32_t tmem_base;
 };
 
-// min over the 8x4 pixel-centre rectangle [x0,x1]x[y0,y1] of
-// q(d) = ca dx^2 + 2 cb dx dy + cc dy^2 (d = p - mean), compared with q_cut.
-__device__ __forceinline__ bool ellipse_hits_rect(float u, float v, float ca, float cb, float cc, float qcut,
+// max over the 8x4 pixel-centre rectangle [x0,x1]x[y0,y1] of the log2-unit
+// exponent p(d) = ea dx^2 + eb dx dy + ec dy^2 (d = p - mean; ea, ec < 0),
+// compared with e_cut (the alpha >= alpha_min ellipse, inflated).
+__device__ __forceinline__ bool ellipse_hits_rect(float u, float v, float ea, float eb, float ec, float ecut,
                                                   float x0, float x1, float y0, float y1) {
     const bool inx = u >= x0 && u <= x1, iny = v >= y0 && v <= y1;
     if (inx && iny) return true;
-    float qmin = 3.4e38f;
-    if (!inx) {               // facing vertical edge
+    float pmax = -3.4e38f;
+    if (!inx) {               // facing vertical edge: best dy = -eb dx / (2 ec), clamped
         const float dx = (u < x0 ? x0 : x1) - u;
-        const float dy = fminf(fmaxf(-cb * dx * __frcp_rn(cc), y0 - v), y1 - v);
-        qmin = fminf(qmin, ca * dx * dx + 2.f * cb * dx * dy + cc * dy * dy);
+        const float dy = fminf(fmaxf(-eb * dx * __frcp_rn(2.f * ec), y0 - v), y1 - v);
+        pmax = fmaxf(pmax, ea * dx * dx + eb * dx * dy + ec * dy * dy);
     }
-    if (!iny) {               // facing horizontal edge
+    if (!iny) {               // facing horizontal edge: best dx = -eb dy / (2 ea), clamped
         const float dy = (v < y0 ? y0 : y1) - v;
-        const float dx = fminf(fmaxf(-cb * dy * __frcp_rn(ca), x0 - u), x1 - u);
-        qmin = fminf(qmin, ca * dx * dx + 2.f * cb * dx * dy + cc * dy * dy);
+        const float dx = fminf(fmaxf(-eb * dy * __frcp_rn(2.f * ea), x0 - u), x1 - u);
+        pmax = fmaxf(pmax, ea * dx * dx + eb * dx * dy + ec * dy * dy);
     }
-    return qmin <= qcut;
+    return pmax >= ecut;
 }
 
-// alpha of entry k at this lane's pixel, or 0 when the oracle skips it
-// (power > 0 or alpha < alpha_min).  power in the oracle's op order.
+// alpha of entry k at this lane's pixel, or 0 when the oracle skips it (p > 0
+// or alpha < alpha_min).  p(d) = dx (ea dx + eb dy) + ec dy dy with the oracle's
+// fused multiply-adds (reading Q29); alpha = min(alpha_max, o 2^p).
 __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, float pxf, float pyf,
                                              const gs_params& P) {
     const float dx = __fsub_rn(a.x, pxf), dy = __fsub_rn(a.y, pyf);
-    const float t1 = __fmul_rn(__fmul_rn(a.z, dx), dx);
-    const float t2 = __fmul_rn(__fmul_rn(b.x, dy), dy);
-    const float t3 = __fmul_rn(__fmul_rn(a.w, dx), dy);
-    const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), t3);
-    const float alpha = fminf(P.alpha_max, __fmul_rn(b.y, ex2_ftz(power * 1.4426950408889634f)));
-    return ((power > 0.0f) || (alpha < P.alpha_min)) ? 0.0f : alpha;
+    const float p = __fmaf_rn(dx, __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy)), __fmul_rn(__fmul_rn(b.x, dy), dy));
+    const float alpha = fminf(P.alpha_max, __fmul_rn(b.y, ex2_ftz(p)));
+    return ((p > 0.0f) || (alpha < P.alpha_min)) ? 0.0f : alpha;
 }
 
 // Persistent kernel: each CTA renders a sequence of tiles handed out in order by
@@ -578,8 +577,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             const int j = (int)lane;
             bool hit = false;
             if (j < m.cnt) {
-                const float4 a = sm.rec[buf][j][0];   // u, v, ca, cb
-                const float4 b = sm.rec[buf][j][1];   // cc, o, q_cut, -
+                const float4 a = sm.rec[buf][j][0];   // u, v, ea, eb
+                const float4 b = sm.rec[buf][j][1];   // ec, o, e_cut, -
                 hit = ellipse_hits_rect(a.x, a.y, a.z, a.w, b.x, b.z, rx0, rx1, ry0, ry1);
             }
             const uint32_t msk = __ballot_sync(0xffffffffu, hit);

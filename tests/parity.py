@@ -1,7 +1,7 @@
 """GPU-vs-oracle comparison helpers (BASELINE.json north_star tolerances,
 SURVEY.md §8(c) 'Parity criteria').
 
-* records: u, v, z, conic, radius, tile rectangle bit-exact; rgb 1e-5
+* records: u, v, z, exponent coefficients, radius, tile rectangle bit-exact; rgb 1e-5
 * keys (tile, depth_bits, gid) and tile ranges: bit-exact
 * rgb, alpha: max abs 1e-3 on pixels not flagged by the oracle (Q20)
 * depth Dz: |d| <= 1e-4 |Dz| where A >= 1e-3, else <= 1e-4 z_near
@@ -27,7 +27,7 @@ def decode_records(rec_i32: np.ndarray):
     r = np.ascontiguousarray(rec_i32)
     f = r.view(np.float32)
     u32 = r.view(np.uint32)
-    return dict(u=f[:, 0], v=f[:, 1], conic=f[:, 2:5], opacity=f[:, 5], q_cut=f[:, 6], rgb=f[:, 8:11],
+    return dict(u=f[:, 0], v=f[:, 1], ecoef=f[:, 2:5], opacity=f[:, 5], e_cut=f[:, 6], rgb=f[:, 8:11],
                 z=f[:, 11], gid=u32[:, 12], view=u32[:, 13] & 0xFFFF, radius=(u32[:, 13] >> 16).astype(np.float32),
                 rect=np.stack([u32[:, 14] & 0xFFFF, u32[:, 14] >> 16, u32[:, 15] & 0xFFFF, u32[:, 15] >> 16], 1))
 
@@ -39,8 +39,12 @@ def check_records(gpu_rec: dict, orc_rec: dict, view_index: int):
     assert (g["view"] == view_index).all()
     for k in ("u", "v", "z"):
         np.testing.assert_array_equal(g[k].view(np.uint32), orc_rec[k].view(np.uint32), err_msg=f"{k} not bit-exact")
-    np.testing.assert_array_equal(g["conic"].view(np.uint32), orc_rec["conic"].view(np.uint32),
-                                  err_msg="conic not bit-exact")
+    # the record holds the exponent coefficients (k a, 2k b, k c), k = fp32(-log2(e)/2) (reading Q29)
+    k = np.float32(-0.72134752044448170368)
+    c = orc_rec["conic"].astype(np.float32)
+    expect = np.stack([k * c[:, 0], (np.float32(2) * k) * c[:, 1], k * c[:, 2]], 1).astype(np.float32)
+    np.testing.assert_array_equal(g["ecoef"].view(np.uint32), expect.view(np.uint32),
+                                  err_msg="exponent coefficients not bit-exact")
     np.testing.assert_array_equal(g["radius"], np.minimum(orc_rec["radius"], 65535), err_msg="radius")
     np.testing.assert_array_equal(g["rect"].astype(np.int64), orc_rec["rect"].astype(np.int64), err_msg="rect")
     np.testing.assert_array_equal(g["opacity"], orc_rec["opacity"])
