@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--gather", action="store_true", help="NCCL all_gather of RGB+depth+opacity (N>1)")
     ap.add_argument("--feature-path", default="tcgen05", choices=["tcgen05", "mma_sync"],
                     help="feature contraction: tcgen05 (fp16 rows, TMEM) or mma.sync (fp32 rows)")
+    ap.add_argument("--binning", default="tight", choices=["tight", "square"],
+                    help="tile binning: tight alpha-ellipse tiles (N3, Q30) or the 3-sigma square (O8); same images")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-views", type=int, default=2)
@@ -225,7 +227,7 @@ def main():
     if args.views:
         views = views[:args.views]
     ds = G.DeviceScene(scene, device=dev, use_f16_features=args.feature_path == "tcgen05")
-    r = G.Renderer(ds, views, device=dev, backproject=True, contrib=args.n1)
+    r = G.Renderer(ds, views, device=dev, backproject=True, contrib=args.n1, binning=args.binning)
     scorer, fmaps = None, None
     if args.n1:
         if scene.feat_dim == 0:
@@ -371,7 +373,7 @@ def main():
                       "resolution": f"{views[0].width}x{views[0].height}", "sh_degree": scene.sh_degree,
                       "feat_dim": D, "l2": "inputs larger than L2 (scene %.2f GB, %.1f GB written per step)" % (
                           ds.nbytes() / 1e9, (total_px * (5 + D) * 4 + total_px * 13) / 1e9),
-                      "gather": bool(args.gather and world > 1), "n1": bool(args.n1),
+                      "gather": bool(args.gather and world > 1), "n1": bool(args.n1), "binning": args.binning,
                       "feature_path": (args.feature_path if scene.feat_dim in (16, 32, 48, 64) else "mma_sync")
                       if scene.feat_dim else None},
            "stages_ms": {n: float(m) for n, m in zip(names, stage_ms) if n != names[4] or scorer is not None},

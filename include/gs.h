@@ -145,16 +145,21 @@ typedef struct gs_params {
  * log2 units (reading Q29), p(d) = dx (ea dx + eb dy) + ec dy dy =
  * log2(e) * (-1/2) d^T conic d, with ea = k conic_a, eb = 2k conic_b,
  * ec = k conic_c and k = fp32(-log2(e)/2) -- power-of-two multiples of one
- * rounded constant, so conic = (ea, eb/2, ec)/k.  e_cut = k (2 ln(opacity /
- * alpha_min) 1.05 + 0.01): p(d) < e_cut implies alpha < alpha_min with margin
- * (used only by the rasterizer to skip provably-zero work).
+ * rounded constant, so conic = (ea, eb/2, ec)/k.  e_cut (reading Q30) =
+ * -((k' + (m - 0.9135)) 1.05 + 0.0075) for opacity / alpha_min = m 2^k',
+ * m in [1, 2): an exactly reproducible bound with p(d) < e_cut implying
+ * alpha < alpha_min with margin (used by the tight binning mode and the
+ * rasterizer's cull to skip provably-zero work).
  */
 typedef struct gs_record {
     float u, v;                       /* pixel-space mean */
     float ea, eb, ec;                 /* exponent coefficients, log2 units (see above) */
     float opacity;
     float e_cut;
-    float reserved;
+    uint32_t tile_mask;               /* N3: bit (ty-y0)*nx + (tx-x0) set iff tile (tx, ty) of the
+                                         rectangle is reached by the alpha >= alpha_min ellipse
+                                         (reading Q30), rectangles of <= 31 tiles; bit 31 set =
+                                         larger rectangle (decided per tile when binning) */
     float rgb[3];
     float z;                          /* camera-space depth (depth key = its bits, O9) */
     uint32_t gid;                     /* Gaussian index in the scene */
@@ -187,7 +192,16 @@ typedef struct gs_bins {
                                 feature rows without a dependent record load) */
     uint32_t* tile_sched;    /* optional [1]: scratch counter of gs_rasterize's dynamic tile
                                 scheduler (zeroed by gs_rasterize on its stream); NULL = static */
+    int32_t mode;            /* GS_BIN_SQUARE: every tile of the 3-sigma rectangle (O8);
+                                GS_BIN_TIGHT (N3, reading Q30): only the rectangle's tiles whose
+                                pixel centres the alpha >= alpha_min ellipse p(d) >= e_cut can
+                                reach (pinned fp32 test, bit-exact with the oracle's tight mode).
+                                Both modes render bit-identical RGB, depth, opacity and
+                                contributions; features agree up to fp32 summation grouping. */
+    int32_t reserved;        /* must be 0 */
 } gs_bins;
+#define GS_BIN_SQUARE 0
+#define GS_BIN_TIGHT 1
 
 typedef struct gs_images {
     float* rgb;     /* [3 * total_pixels] */
@@ -232,6 +246,30 @@ gs_status gs_scene_block_bounds(const gs_scene* scene, float* block_bounds_out, 
  * misaligned.
  */
 gs_status gs_scene_features_f16(const gs_scene* scene, void* feat_h_out, void* stream);
+
+/*
+ * gs_validate_scene -- debug check of SPEC's Gaussian invariants over
+ * the whole scene, reporting the first offending Gaussian ("naming the
+ * offending record index").  Not on the hot path; the hot path never rejects
+ * data (degenerate Gaussians are counted in diag).
+ *   first_bad (device, 1 x int64): smallest index i violating an invariant,
+ *     or -1 when the scene is valid; used as scratch during the call.
+ *   reason (device, 1 x int32): the smallest GS_BAD_* code violated by
+ *     Gaussian first_bad (GS_BAD_NONE when valid).
+ *   unit_quat: 1 = also require | |q| - 1 | <= 1e-6; 0 = only
+ *     a finite, non-zero q (gs_project normalises q, reading Q2).
+ * Asynchronous on `stream`.  Errors: GS_INVALID_ARG for NULL pointers.
+ */
+#define GS_BAD_NONE 0
+#define GS_BAD_POSITION 1   /* non-finite mean */
+#define GS_BAD_QUAT 2       /* non-finite or zero quaternion */
+#define GS_BAD_QUAT_NORM 3  /* | |q| - 1 | > 1e-6 (unit_quat = 1 only) */
+#define GS_BAD_SCALE 4      /* scale not finite or <= 0 */
+#define GS_BAD_OPACITY 5    /* opacity outside [0, 1] or NaN */
+#define GS_BAD_SH 6         /* non-finite SH coefficient */
+#define GS_BAD_FEATURE 7    /* non-finite feature */
+gs_status gs_validate_scene(const gs_scene* scene, int32_t unit_quat, int64_t* first_bad, int32_t* reason,
+                            void* stream);
 
 /* Workspace of gs_project: a (view x block) visibility bitmask. */
 size_t gs_project_workspace_bytes(int32_t n_blocks, int32_t n_views);

@@ -107,15 +107,16 @@ def project(scene, view, params: Optional[Params] = None) -> Dict[str, np.ndarra
     rgb = np.empty((n, 3), np.float32)
     opac = np.empty(n, np.float32)
     cov = np.empty((n, 3), np.float32)
+    ecut = np.empty(n, np.float32)
     diag = np.zeros(4, np.int64)
     vc, pc = _view_c(view), params.c()
     cnt = lib().oracle_project(ctypes.c_int64(n), _p(pos), _p(quat), _p(scale), _p(op), _p(sh),
                                ctypes.c_int32(scene.sh_degree), ctypes.byref(vc), ctypes.byref(pc),
                                _p(gid), _p(u), _p(v), _p(z), _p(conic), _p(radius), _p(rect), _p(rgb),
-                               _p(opac), _p(cov), _p(diag))
+                               _p(opac), _p(cov), _p(ecut), _p(diag))
     return dict(gid=gid[:cnt].copy(), u=u[:cnt].copy(), v=v[:cnt].copy(), z=z[:cnt].copy(),
                 conic=conic[:cnt].copy(), radius=radius[:cnt].copy(), rect=rect[:cnt].copy(),
-                rgb=rgb[:cnt].copy(), opacity=opac[:cnt].copy(), cov=cov[:cnt].copy(),
+                rgb=rgb[:cnt].copy(), opacity=opac[:cnt].copy(), cov=cov[:cnt].copy(), e_cut=ecut[:cnt].copy(),
                 diag=dict(near=int(diag[0]), transparent=int(diag[1]), degenerate=int(diag[2]),
                           offscreen=int(diag[3])))
 
@@ -124,19 +125,34 @@ def tiles(view):
     return (view.width + 15) // 16, (view.height + 15) // 16
 
 
-def bin_keys(rec, view) -> Dict[str, np.ndarray]:
-    """O11: sorted (tile, depth_bits, gid) keys, their record index, ranges [T][2]."""
+class _Tight(ctypes.Structure):
+    _fields_ = [("u", ctypes.c_void_p), ("v", ctypes.c_void_p), ("conic", ctypes.c_void_p), ("ecut", ctypes.c_void_p)]
+
+
+def bin_keys(rec, view, binning: str = "square") -> Dict[str, np.ndarray]:
+    """O11: sorted (tile, depth_bits, gid) keys, their record index, ranges [T][2].
+    binning "square": every tile of the 3-sigma rectangle (O8); "tight" (N3,
+    reading Q30): only the rectangle's tiles the alpha >= alpha_min ellipse reaches."""
     tx, ty = tiles(view)
     cnt = len(rec["gid"])
     rect = np.ascontiguousarray(rec["rect"], np.int32)
-    P = int(lib().oracle_count_pairs(ctypes.c_int64(cnt), _p(rect)))
+    keep = []
+    tight = None
+    if binning == "tight":
+        arrs = [_c32(rec["u"]), _c32(rec["v"]), _c32(rec["conic"]), _c32(rec["e_cut"])]
+        keep = arrs
+        tight = ctypes.byref(_Tight(*[a.ctypes.data for a in arrs]))
+    elif binning != "square":
+        raise ValueError(binning)
+    P = int(lib().oracle_count_pairs(ctypes.c_int64(cnt), _p(rect), tight))
     kt = np.empty(P, np.uint32)
     kd = np.empty(P, np.uint32)
     kg = np.empty(P, np.uint32)
     kr = np.empty(P, np.uint32)
     ranges = np.empty((tx * ty, 2), np.uint32)
-    lib().oracle_bin(ctypes.c_int64(cnt), _p(np.ascontiguousarray(rec["gid"])), _p(_c32(rec["z"])), _p(rect),
+    lib().oracle_bin(ctypes.c_int64(cnt), _p(np.ascontiguousarray(rec["gid"])), _p(_c32(rec["z"])), _p(rect), tight,
                      ctypes.c_int32(tx), ctypes.c_int32(ty), _p(kt), _p(kd), _p(kg), _p(kr), _p(ranges))
+    del keep
     return dict(tile=kt, depth=kd, gid=kg, rec=kr, ranges=ranges)
 
 
@@ -198,10 +214,10 @@ def backproject(view, depth, alpha, a_min: float = 0.5, flags=None):
     return xyz, valid, fl
 
 
-def render(scene, view, params: Optional[Params] = None, a_min: Optional[float] = None):
+def render(scene, view, params: Optional[Params] = None, a_min: Optional[float] = None, binning: str = "square"):
     """Full oracle pipeline for one view: project -> bin -> composite (-> backproject)."""
     rec = project(scene, view, params)
-    keys = bin_keys(rec, view)
+    keys = bin_keys(rec, view, binning)
     img = composite(view, rec, keys, scene.feat, params)
     out = dict(rec=rec, keys=keys, **img)
     if a_min is not None:

@@ -119,6 +119,10 @@ void sh_color(int deg, const double* coeff /*[nk][3]*/, double dx, double dy, do
     }
 }
 
+// Q29: the Gaussian exponent is evaluated in log2 units with the fp32 constant
+// k = -log2(e)/2 (the literal rounds to the nearest fp32)
+const float K_EXP2 = -0.72134752044448170368f;
+
 inline uint32_t float_bits(float f) {
     uint32_t u;
     std::memcpy(&u, &f, 4);
@@ -141,6 +145,56 @@ void oracle_sh_color(int32_t deg, const double* coeff, const double* dir, double
 }
 
 // ---------------------------------------------------------------------------
+// Reading Q30: the alpha >= alpha_min cut in log2 units, from operations that
+// round identically everywhere.  alpha = o 2^p >= alpha_min <=> p >= -log2(x),
+// x = o / alpha_min >= 1.  For x = m 2^k, m in [1, 2): log2(m) lies below its
+// tangent at m0 = 1/ln 2, m - 0.913929 (log2 is concave), so
+// log2(x) <= k + (m - 0.9135) (0.0004 slack covers the fp32 rounding; the
+// bound is at most 0.0865 loose); inflated by 5% + 0.0075:
+// e_cut = -((k + (m - 0.9135)) 1.05 + 0.0075) <= -1.05 log2(x) - 0.0075.
+// ---------------------------------------------------------------------------
+static float e_cut_of(float op, float alpha_min) {
+    const float x = op / alpha_min;
+    const uint32_t b = float_bits(x);
+    const int32_t k = (int32_t)((b >> 23) & 0xffu) - 127;
+    const uint32_t mb = (b & 0x7fffffu) | 0x3f800000u;
+    float m;
+    std::memcpy(&m, &mb, 4);
+    const float lub = (float)k + (m - 0.9135f);
+    return -(lub * 1.05f + 0.0075f);
+}
+
+// Reading Q30 (N3 tight binning): does the alpha >= alpha_min ellipse
+// {d : p(d) >= e_cut}, p(d) = ea dx^2 + eb dx dy + ec dy^2 (ea, ec < 0), reach
+// the pixel centres [16tx, 16tx+15] x [16ty, 16ty+15] of tile (tx, ty)?  p is
+// concave, so if the mean is outside the rectangle its maximum lies on a
+// facing edge, at the edge point nearest the 1-D stationary point.  fp32, this
+// exact operation order (the GPU's is identical, so key lists are bit-exact).
+static float p_at(float ea, float eb, float ec, float dx, float dy) {
+    return ((ea * dx) * dx + (eb * dx) * dy) + (ec * dy) * dy;
+}
+static bool tile_hit(float u, float v, float ea, float eb, float ec, float ecut, int32_t tx, int32_t ty) {
+    const float X0 = (float)(tx * 16), X1 = (float)(tx * 16 + 15);
+    const float Y0 = (float)(ty * 16), Y1 = (float)(ty * 16 + 15);
+    const bool inx = X0 <= u && u <= X1, iny = Y0 <= v && v <= Y1;
+    if (inx && iny) return true;
+    float pmax = -INFINITY;
+    // stationary-point slopes, one rounded division each: dy*(dx) = sy dx, dx*(dy) = sx dy
+    const float sy = -eb / (2.0f * ec), sx = -eb / (2.0f * ea);
+    if (!inx) {   // facing vertical edge
+        const float dx = (u < X0 ? X0 : X1) - u;
+        const float dy = std::fmin(std::fmax(sy * dx, Y0 - v), Y1 - v);
+        pmax = std::fmax(pmax, p_at(ea, eb, ec, dx, dy));
+    }
+    if (!iny) {   // facing horizontal edge
+        const float dy = (v < Y0 ? Y0 : Y1) - v;
+        const float dx = std::fmin(std::fmax(sx * dy, X0 - u), X1 - u);
+        pmax = std::fmax(pmax, p_at(ea, eb, ec, dx, dy));
+    }
+    return pmax >= ecut;
+}
+
+// ---------------------------------------------------------------------------
 // O1-O10 for one view.  Scene planes are SoA: pos[3][n], quat[4][n] (w,x,y,z),
 // scale[3][n], opacity[n], sh[(deg+1)^2*3][n].  Visible Gaussians are written
 // in ascending gid order; returns their count.  diag[4] += cull counters.
@@ -153,7 +207,7 @@ int64_t oracle_project(int64_t n, const float* pos, const float* quat, const flo
                        int32_t* out_rect /*[cnt][4] = x0,x1,y0,y1 inclusive*/,
                        float* out_rgb /*[cnt][3]*/, float* out_opacity,
                        float* out_cov /*[cnt][3] = a,b,c incl. dilation (diagnostic)*/,
-                       int64_t* diag) {
+                       float* out_ecut /*[cnt] reading Q30*/, int64_t* diag) {
     const float* R = V->R;
     const float W = (float)V->width, H = (float)V->height;
     const int32_t TX = (V->width + 15) / 16, TY = (V->height + 15) / 16;
@@ -273,6 +327,7 @@ int64_t oracle_project(int64_t n, const float* pos, const float* quat, const flo
         out_cov[cnt * 3 + 0] = a;
         out_cov[cnt * 3 + 1] = b;
         out_cov[cnt * 3 + 2] = c;
+        out_ecut[cnt] = e_cut_of(op, P->alpha_min);
         ++cnt;
     }
     return cnt;
@@ -281,10 +336,24 @@ int64_t oracle_project(int64_t n, const float* pos, const float* quat, const flo
 // ---------------------------------------------------------------------------
 // O11: number of (tile, Gaussian) pairs = sum of rectangle areas.
 // ---------------------------------------------------------------------------
-int64_t oracle_count_pairs(int64_t cnt, const int32_t* rect) {
+// Binning mode (N3, reading Q30): tight == NULL -> every tile of the 3-sigma
+// rectangle (O8); else only the rectangle's tiles with tile_hit, from the
+// record fields u, v, conic and e_cut (exponent coefficients as in Q29).
+struct Tight {
+    const float *u, *v, *conic, *ecut;
+};
+static bool keep_tile(const Tight* tight, int64_t i, int32_t tx, int32_t ty) {
+    if (!tight) return true;
+    const float* c = tight->conic + i * 3;
+    const float ea = K_EXP2 * c[0], eb = (2.0f * K_EXP2) * c[1], ec = K_EXP2 * c[2];
+    return tile_hit(tight->u[i], tight->v[i], ea, eb, ec, tight->ecut[i], tx, ty);
+}
+
+int64_t oracle_count_pairs(int64_t cnt, const int32_t* rect, const Tight* tight) {
     int64_t p = 0;
     for (int64_t i = 0; i < cnt; ++i)
-        p += (int64_t)(rect[i * 4 + 1] - rect[i * 4 + 0] + 1) * (rect[i * 4 + 3] - rect[i * 4 + 2] + 1);
+        for (int32_t ty = rect[i * 4 + 2]; ty <= rect[i * 4 + 3]; ++ty)
+            for (int32_t tx = rect[i * 4 + 0]; tx <= rect[i * 4 + 1]; ++tx) p += keep_tile(tight, i, tx, ty);
     return p;
 }
 
@@ -298,15 +367,16 @@ struct Key {
     uint32_t tile, depth, gid, rec;
 };
 
-void oracle_bin(int64_t cnt, const int32_t* gid, const float* zv, const int32_t* rect,
+void oracle_bin(int64_t cnt, const int32_t* gid, const float* zv, const int32_t* rect, const Tight* tight,
                 int32_t tiles_x, int32_t tiles_y, uint32_t* key_tile, uint32_t* key_depth,
                 uint32_t* key_gid, uint32_t* key_rec, uint32_t* ranges /*[T][2]*/) {
     std::vector<Key> keys;
     for (int64_t i = 0; i < cnt; ++i)
         for (int32_t ty = rect[i * 4 + 2]; ty <= rect[i * 4 + 3]; ++ty)
             for (int32_t tx = rect[i * 4 + 0]; tx <= rect[i * 4 + 1]; ++tx)
-                keys.push_back({(uint32_t)(ty * tiles_x + tx), float_bits(zv[i]), (uint32_t)gid[i],
-                                (uint32_t)i});
+                if (keep_tile(tight, i, tx, ty))
+                    keys.push_back({(uint32_t)(ty * tiles_x + tx), float_bits(zv[i]), (uint32_t)gid[i],
+                                    (uint32_t)i});
     std::sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
         if (a.tile != b.tile) return a.tile < b.tile;
         if (a.depth != b.depth) return a.depth < b.depth;
@@ -346,10 +416,6 @@ struct PixelOut {
     uint8_t flags;
     int64_t evals, blends;
 };
-
-// Q29: the Gaussian exponent is evaluated in log2 units with the fp32 constant
-// k = -log2(e)/2 (the literal rounds to the nearest fp32)
-const float K_EXP2 = -0.72134752044448170368f;
 
 // flag bands (Q20): alpha within 2^-18 (relative) of alpha_min, Tn within 2^-12 of t_min
 const double FLAG_ALPHA_REL = 1.0 / 262144.0;

@@ -7,8 +7,8 @@ and the multi-GPU pose-sharding host logic (``dist``).  There is no CPU
 fallback.
 """
 from .gs import (GSError, DeviceScene, ViewBatch, Projected, Bins, Images, default_params,  # noqa: F401
-                 gs_project, gs_bin_sort, gs_rasterize, gs_backproject, gs_visibility_score, lib, LIB_PATH,
-                 EXPORTS)
+                 gs_project, gs_bin_sort, gs_rasterize, gs_backproject, gs_visibility_score, gs_validate_scene,
+                 lib, LIB_PATH, EXPORTS)
 from .pipeline import Renderer, SignificanceScorer  # noqa: F401
 
 __all__ = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_backproject", "gs_visibility_score", "DeviceScene",

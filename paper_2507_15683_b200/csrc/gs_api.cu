@@ -113,3 +113,63 @@ gs_status gs_views_layout(gs_view* views_host, int32_t n_views, int64_t* total_p
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// gs_validate_scene (debug): per Gaussian invariant checks, first offender by
+// a 64-bit atomicMin on (index << 8 | reason).
+// ---------------------------------------------------------------------------
+namespace gs {
+namespace {
+__device__ __forceinline__ bool finite_f(float x) { return isfinite(x); }
+
+__global__ void validate_scene_kernel(gs_scene S, int32_t unit_quat, unsigned long long* key) {
+    const int64_t n = S.n;
+    const int nk = (S.sh_degree + 1) * (S.sh_degree + 1) * 3;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t r = GS_BAD_NONE;
+        const float px = S.pos[i], py = S.pos[n + i], pz = S.pos[2 * n + i];
+        const float qw = S.quat[i], qx = S.quat[n + i], qy = S.quat[2 * n + i], qz = S.quat[3 * n + i];
+        const float sx = S.scale[i], sy = S.scale[n + i], sz = S.scale[2 * n + i];
+        const float o = S.opacity[i];
+        const double qn = sqrt((double)qw * qw + (double)qx * qx + (double)qy * qy + (double)qz * qz);
+        if (!(finite_f(px) && finite_f(py) && finite_f(pz))) r = GS_BAD_POSITION;
+        else if (!(finite_f(qw) && finite_f(qx) && finite_f(qy) && finite_f(qz)) || !(qn > 0.0)) r = GS_BAD_QUAT;
+        else if (unit_quat && fabs(qn - 1.0) > 1e-6) r = GS_BAD_QUAT_NORM;
+        else if (!(finite_f(sx) && finite_f(sy) && finite_f(sz) && sx > 0.f && sy > 0.f && sz > 0.f))
+            r = GS_BAD_SCALE;
+        else if (!(o >= 0.f && o <= 1.f)) r = GS_BAD_OPACITY;
+        else {
+            for (int k = 0; k < nk && r == GS_BAD_NONE; ++k)
+                if (!finite_f(S.sh[(int64_t)k * n + i])) r = GS_BAD_SH;
+            for (int c = 0; c < S.feat_dim && r == GS_BAD_NONE; ++c)
+                if (!finite_f(S.feat[i * S.feat_dim + c])) r = GS_BAD_FEATURE;
+        }
+        if (r != GS_BAD_NONE) atomicMin(key, ((unsigned long long)i << 8) | r);
+    }
+}
+
+__global__ void validate_finish_kernel(unsigned long long* key, int32_t* reason) {
+    const unsigned long long k = *key;
+    const bool valid = k == ~0ull;
+    *reason = valid ? GS_BAD_NONE : (int32_t)(k & 0xffull);
+    *reinterpret_cast<int64_t*>(key) = valid ? -1 : (int64_t)(k >> 8);
+}
+}  // namespace
+}  // namespace gs
+
+extern "C" gs_status gs_validate_scene(const gs_scene* scene, int32_t unit_quat, int64_t* first_bad, int32_t* reason,
+                                       void* stream) {
+    gs_status st = gs::validate_scene(scene, true);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(first_bad != nullptr && reason != nullptr, GS_INVALID_ARG, "first_bad / reason is NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(first_bad);
+    cudaMemsetAsync(key, 0xff, sizeof(*key), s);
+    if (scene->n > 0) {
+        const int64_t blocks = std::min<int64_t>((scene->n + 255) / 256, (int64_t)gs::num_sms() * 8);
+        gs::validate_scene_kernel<<<(unsigned)blocks, 256, 0, s>>>(*scene, unit_quat, key);
+        if ((st = gs::check_launch("validate_scene_kernel")) != GS_OK) return st;
+    }
+    gs::validate_finish_kernel<<<1, 1, 0, s>>>(key, reason);
+    return gs::check_launch("validate_finish_kernel");
+}

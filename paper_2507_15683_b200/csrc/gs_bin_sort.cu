@@ -102,8 +102,9 @@ __device__ __forceinline__ void rect_of(const uint4& q3, uint32_t& x0, uint32_t&
 }
 
 __global__ void __launch_bounds__(BIN_THREADS)
-count_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
-             const gs_view* __restrict__ views, uint32_t* __restrict__ counts, const uint32_t* __restrict__ status) {
+count_kernel(gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
+             const gs_view* __restrict__ views, uint32_t* __restrict__ counts, const uint32_t* __restrict__ status,
+             int tight) {
     if (*status & GS_STATUS_RECORD_OVERFLOW) return;
     extern __shared__ uint32_t hist[];
     const int v = blockIdx.y;
@@ -119,14 +120,75 @@ count_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __r
         for (int t = threadIdx.x; t < Tv; t += blockDim.x) hist[t] = 0u;
         __syncthreads();
     }
-    for (uint32_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-        const uint4 q3 = __ldg(reinterpret_cast<const uint4*>(rec + (int64_t)v * cap + k) + 3);
-        uint32_t x0, y0, nx, np;
-        rect_of(q3, x0, y0, nx, np);
-        for (uint32_t p = 0; p < np; ++p) {
-            const uint32_t t = (y0 + p / nx) * TX + x0 + p % nx;
-            if (onchip) atomicAdd(&hist[t], 1u);
-            else atomicAdd(&counts[toff + t], 1u);
+    auto bump = [&](uint32_t t) {
+        if (onchip) atomicAdd(&hist[t], 1u);
+        else atomicAdd(&counts[toff + t], 1u);
+    };
+    if (!tight) {
+        for (uint32_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+            const uint4 q3 = __ldg(reinterpret_cast<const uint4*>(rec + (int64_t)v * cap + k) + 3);
+            uint32_t x0, y0, nx, np;
+            rect_of(q3, x0, y0, nx, np);
+            for (uint32_t p = 0; p < np; ++p) bump((y0 + p / nx) * TX + x0 + p % nx);
+        }
+    } else {
+        // N3 (reading Q30): decide every (record, tile) of rectangles of <= 31 tiles with
+        // the whole warp -- the warp's 32 records' tiles are flattened over the lanes --
+        // and store the decision as the record's tile_mask for the scatter pass
+        __shared__ TightRec tr[BIN_THREADS];
+        __shared__ uint32_t trect[BIN_THREADS], tnx[BIN_THREADS], tpre[BIN_THREADS], tmask[BIN_THREADS];
+        const uint32_t lane = threadIdx.x & 31u, wb = threadIdx.x & ~31u;
+        for (uint32_t kb = k0 + wb; kb < k1; kb += blockDim.x) {
+            const uint32_t k = kb + lane;
+            gs_record* r = rec + (int64_t)v * cap + k;
+            uint32_t x0 = 0, y0 = 0, nx = 1, np = 0, small = 0;
+            if (k < k1) {
+                const uint4 q3 = __ldg(reinterpret_cast<const uint4*>(r) + 3);
+                rect_of(q3, x0, y0, nx, np);
+                if (np <= 31u) {
+                    tr[threadIdx.x] = tight_of(r);
+                    small = np;
+                }
+            }
+            trect[threadIdx.x] = x0 | (y0 << 16);
+            tnx[threadIdx.x] = nx;
+            tmask[threadIdx.x] = 0u;
+            uint32_t inc = small;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if ((int)lane >= o) inc += y;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+            tpre[threadIdx.x] = inc - small;
+            __syncwarp();
+            for (uint32_t idx = lane; idx < total; idx += 32u) {
+                // owner: the last record of the warp whose exclusive prefix is <= idx
+                uint32_t lo = 0;
+#pragma unroll
+                for (uint32_t step = 16; step; step >>= 1)
+                    if (tpre[wb + lo + step] <= idx) lo += step;
+                const uint32_t o = wb + lo, p = idx - tpre[o], nxo = tnx[o], rx = trect[o];
+                const uint32_t tx = (rx & 0xffffu) + p % nxo, ty = (rx >> 16) + p / nxo;
+                if (tile_hit(tr[o], tx, ty)) {
+                    atomicOr(&tmask[o], 1u << p);
+                    bump(ty * TX + tx);
+                }
+            }
+            __syncwarp();
+            if (k < k1) {
+                uint32_t m = tmask[threadIdx.x];
+                if (np > 31u) {   // large rectangle: decided per tile here and again in the scatter
+                    m = GS_TILE_MASK_FULL;
+                    const TightRec g = tight_of(r);
+                    for (uint32_t p = 0; p < np; ++p) {
+                        const uint32_t tx = x0 + p % nx, ty = y0 + p / nx;
+                        if (tile_hit(g, tx, ty)) bump(ty * TX + tx);
+                    }
+                }
+                r->tile_mask = m;
+            }
+            __syncwarp();
         }
     }
     if (onchip) {
@@ -231,7 +293,7 @@ scan_down_kernel(const uint32_t* __restrict__ counts, int64_t T, const unsigned 
 __global__ void __launch_bounds__(BIN_THREADS)
 scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
                const gs_view* __restrict__ views, uint32_t* __restrict__ cursor, uint4* __restrict__ bucket,
-               const uint32_t* __restrict__ status) {
+               const uint32_t* __restrict__ status, int tight) {
     if (*status) return;
     extern __shared__ uint32_t hist[];
     const int v = blockIdx.y;
@@ -247,10 +309,26 @@ scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* _
         for (int t = threadIdx.x; t < Tv; t += blockDim.x) hist[t] = 0u;
         __syncthreads();
         for (uint32_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-            const uint4 q3 = __ldg(reinterpret_cast<const uint4*>(rec + (int64_t)v * cap + k) + 3);
+            const gs_record* r = rec + (int64_t)v * cap + k;
+            const uint4 q3 = __ldg(reinterpret_cast<const uint4*>(r) + 3);
             uint32_t x0, y0, nx, np;
             rect_of(q3, x0, y0, nx, np);
-            for (uint32_t p = 0; p < np; ++p) atomicAdd(&hist[(y0 + p / nx) * TX + x0 + p % nx], 1u);
+            if (tight) {
+                const uint32_t tm = __ldg(&r->tile_mask);
+                if (!(tm & GS_TILE_MASK_FULL)) {
+                    for (uint32_t m = tm; m; m &= m - 1u) {
+                        const uint32_t p = __ffs(m) - 1u;
+                        atomicAdd(&hist[(y0 + p / nx) * TX + x0 + p % nx], 1u);
+                    }
+                    continue;
+                }
+            }
+            const TightRec g = tight ? tight_of(r) : TightRec{};
+            for (uint32_t p = 0; p < np; ++p) {
+                const uint32_t tx = x0 + p % nx, ty = y0 + p / nx;
+                if (tight && !tile_hit(g, tx, ty)) continue;
+                atomicAdd(&hist[ty * TX + tx], 1u);
+            }
         }
         __syncthreads();
         for (int t = threadIdx.x; t < Tv; t += blockDim.x) {
@@ -266,19 +344,46 @@ scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* _
         const uint4 ent = make_uint4(q2.w, slot, q3.x, 0u);   // bits(z), slot, gid
         uint32_t x0, y0, nx, np;
         rect_of(q3, x0, y0, nx, np);
+        if (tight) {
+            const uint32_t tm = __ldg(&rec[slot].tile_mask);
+            if (!(tm & GS_TILE_MASK_FULL)) {
+                for (uint32_t m = tm; m;) {
+                    uint32_t pos[4], pp[4];
+                    int c = 0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (m) {
+                            pp[q] = __ffs(m) - 1u;
+                            m &= m - 1u;
+                            const uint32_t t = (y0 + pp[q] / nx) * TX + x0 + pp[q] % nx;
+                            pos[q] = onchip ? atomicAdd(&hist[t], 1u) : atomicAdd(&cursor[toff + t], 1u);
+                            c = q + 1;
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (q < c) bucket[pos[q]] = ent;
+                }
+                continue;
+            }
+        }
+        const TightRec g = tight ? tight_of(rec + slot) : TightRec{};
         for (uint32_t p0 = 0; p0 < np; p0 += 4) {
             uint32_t pos[4];
+            bool keep[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t p = p0 + q;
-                if (p < np) {
-                    const uint32_t t = (y0 + p / nx) * TX + x0 + p % nx;
+                const uint32_t tx = x0 + p % nx, ty = y0 + p / nx;
+                keep[q] = p < np && (!tight || tile_hit(g, tx, ty));
+                if (keep[q]) {
+                    const uint32_t t = ty * TX + tx;
                     pos[q] = onchip ? atomicAdd(&hist[t], 1u) : atomicAdd(&cursor[toff + t], 1u);
                 }
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (p0 + q < np) bucket[pos[q]] = ent;
+                if (keep[q]) bucket[pos[q]] = ent;
         }
     }
 }
@@ -652,6 +757,8 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     if (st != GS_OK) return st;
     GS_REQUIRE(proj && proj->rec && proj->n_rec && proj->status, GS_INVALID_ARG, "proj has a NULL pointer");
     GS_REQUIRE(out && out->ranges && out->sorted_rec && out->n_pairs, GS_INVALID_ARG, "bins has a NULL pointer");
+    GS_REQUIRE(out->mode == GS_BIN_SQUARE || out->mode == GS_BIN_TIGHT, GS_INVALID_ARG, "bins mode = %d invalid",
+               out->mode);
     GS_REQUIRE(out->pair_capacity >= 1 && out->pair_capacity < (int64_t(1) << 32), GS_INVALID_ARG,
                "pair_capacity = %lld not in [1, 2^32)", (long long)out->pair_capacity);
     const size_t need = ws_bytes(out->pair_capacity, T);
@@ -677,7 +784,9 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
         cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_MAX * 4);
         hist_attr = true;
     }
-    count_kernel<<<rgrid, BIN_THREADS, hist_smem, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.counts, proj->status);
+    const int tight = out->mode == GS_BIN_TIGHT;
+    count_kernel<<<rgrid, BIN_THREADS, hist_smem, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.counts, proj->status,
+                                                       tight);
     if ((st = check_launch("count_kernel")) != GS_OK) return st;
     const int64_t nb = (T + SCAN_TILE - 1) / SCAN_TILE;
     scan_reduce_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(w.counts, T, w.block_sums);
@@ -685,7 +794,7 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     scan_down_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(w.counts, T, w.block_sums, out->ranges, w.cursor);
     if ((st = check_launch("scan kernels")) != GS_OK) return st;
     scatter_kernel<<<rgrid, BIN_THREADS, hist_smem, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.cursor, w.bucket,
-                                                          proj->status);
+                                                          proj->status, tight);
     if ((st = check_launch("scatter_kernel")) != GS_OK) return st;
     // small batches (single views, pyramids): every list > 256 gets a 16-warp CTA
     // (latency); large batches: one warp per list <= 512, 4-warp CTAs above (throughput)

@@ -53,6 +53,51 @@ inline int num_sms() {
 }
 
 // ---------------------------------------------------------------- device side
+// Reading Q30 (N3 tight binning): does the alpha >= alpha_min ellipse p(d) >=
+// e_cut reach the pixel centres [16tx, 16tx+15] x [16ty, 16ty+15]?  p is
+// concave: with the mean outside the rectangle its maximum lies on a facing
+// edge at the clamped 1-D stationary point.  IEEE fp32 in the oracle's exact
+// order (explicit _rn intrinsics: no contraction), so key lists are bit-exact.
+__device__ __forceinline__ float p_at(float ea, float eb, float ec, float dx, float dy) {
+    return __fadd_rn(__fadd_rn(__fmul_rn(__fmul_rn(ea, dx), dx), __fmul_rn(__fmul_rn(eb, dx), dy)),
+                     __fmul_rn(__fmul_rn(ec, dy), dy));
+}
+struct TightRec {
+    float u, v, ea, eb, ec, ecut, sx, sy;
+};
+__device__ __forceinline__ TightRec tight_make(float u, float v, float ea, float eb, float ec, float ecut) {
+    // stationary-point slopes, one rounded division each (the oracle's sx, sy)
+    const float sy = __fdiv_rn(-eb, __fmul_rn(2.0f, ec)), sx = __fdiv_rn(-eb, __fmul_rn(2.0f, ea));
+    return TightRec{u, v, ea, eb, ec, ecut, sx, sy};
+}
+__device__ __forceinline__ TightRec tight_of(const gs_record* r) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(r));       // u, v, ea, eb
+    const float4 b = __ldg(reinterpret_cast<const float4*>(r) + 1);   // ec, o, e_cut, tile_mask
+    return tight_make(a.x, a.y, a.z, a.w, b.x, b.z);
+}
+// record.tile_mask: bit p = (ty - y0) nx + (tx - x0) set iff tile (tx, ty) of the
+// rectangle passes tile_hit, for rectangles of <= 31 tiles; GS_TILE_MASK_FULL
+// (bit 31) = larger rectangle, test per tile when binning
+constexpr uint32_t GS_TILE_MASK_FULL = 0x80000000u;
+__device__ __forceinline__ bool tile_hit(const TightRec& g, uint32_t tx, uint32_t ty) {
+    const float X0 = (float)(tx * 16u), X1 = (float)(tx * 16u + 15u);
+    const float Y0 = (float)(ty * 16u), Y1 = (float)(ty * 16u + 15u);
+    const bool inx = X0 <= g.u && g.u <= X1, iny = Y0 <= g.v && g.v <= Y1;
+    if (inx && iny) return true;
+    float pmax = -INFINITY;
+    if (!inx) {
+        const float dx = __fsub_rn(g.u < X0 ? X0 : X1, g.u);
+        const float dy = fminf(fmaxf(__fmul_rn(g.sy, dx), __fsub_rn(Y0, g.v)), __fsub_rn(Y1, g.v));
+        pmax = fmaxf(pmax, p_at(g.ea, g.eb, g.ec, dx, dy));
+    }
+    if (!iny) {
+        const float dy = __fsub_rn(g.v < Y0 ? Y0 : Y1, g.v);
+        const float dx = fminf(fmaxf(__fmul_rn(g.sx, dy), __fsub_rn(X0, g.u)), __fsub_rn(X1, g.u));
+        pmax = fmaxf(pmax, p_at(g.ea, g.eb, g.ec, dx, dy));
+    }
+    return pmax >= g.ecut;
+}
+
 __device__ __forceinline__ int view_tiles_x(const gs_view& v) { return (v.width + GS_TILE - 1) / GS_TILE; }
 
 // index of the view owning batch tile `t` (views sorted by tile_offset)

@@ -261,7 +261,19 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
         blk = lo;
     }
     uint32_t c_near = 0, c_transp = 0, c_degen = 0, c_off = 0;
-    const float thr = in && !transparent ? 2.0f * logf(op / P.alpha_min) : 0.f;
+    // reading Q30: alpha >= alpha_min cut in log2 units from exactly-rounded operations
+    // (identical to the oracle's e_cut_of): x = o / alpha_min = m 2^k, m in [1, 2);
+    // log2(x) <= k + (m - 0.9135) (tangent of the concave log2 at 1/ln 2), inflated
+    // by 5% + 0.0075 so the cull and the tight binning stay conservative
+    float e_cut = 0.f;
+    if (in && !transparent) {
+        const float x = op / P.alpha_min;
+        const uint32_t xb = __float_as_uint(x);
+        const int k = (int)((xb >> 23) & 0xffu) - 127;
+        const float m = __uint_as_float((xb & 0x7fffffu) | 0x3f800000u);
+        const float lub = (float)k + (m - 0.9135f);
+        e_cut = -(lub * 1.05f + 0.0075f);
+    }
 
     for (int w = 0; w < nw; ++w) {
         uint32_t my_mask = 0;
@@ -346,12 +358,9 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
                     // ea = k ca, eb = 2k cb, ec = k cc
                     r.ea = K_EXP2 * ca; r.eb = (2.0f * K_EXP2) * cb; r.ec = K_EXP2 * ccn;
                     r.opacity = op;
-                    // alpha >= alpha_min  <=>  q(d) = d^T conic d <= thr = 2 ln(o / alpha_min).
-                    // thr inflated by 5% + 0.01 so the rasterizer's per-warp ellipse cull stays
-                    // conservative against fp32 evaluation noise of the exponent and exp2, then
-                    // scaled to log2 units: cull iff max over the rectangle of p(d) < e_cut.
-                    r.e_cut = K_EXP2 * (thr * 1.05f + 0.01f);
-                    r.reserved = 0.0f;
+                    // alpha >= alpha_min needs p(d) >= -log2(o / alpha_min) >= e_cut
+                    r.e_cut = e_cut;
+                    r.tile_mask = GS_TILE_MASK_FULL;   // decided by gs_bin_sort (tight mode)
                     r.gid = (uint32_t)i;
                     r.view_radius = (uint32_t)vi | ((uint32_t)fminf(rad, 65535.0f) << 16);
                     // O10: SH colour at d = (mu - c_cam)/|mu - c_cam|

@@ -76,6 +76,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// wait with back-off: a warp with nothing else to do (the producer when the ring is
+// full) must not steal issue slots from the consumer warps of its scheduler
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    uint32_t ok = 0;
+    for (;;) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(ns);
+    }
+}
 // 16-B global->shared copy that asks L2 to keep the line (records and feature rows
 // are re-read by the ~4 neighbouring tiles a Gaussian overlaps)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint64_t policy) {
@@ -345,7 +363,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 cnt = end ? 0 : (int)min((uint32_t)SE, re - c0);
                 load_idx(c0, cnt, nslot, ngid);
             }
-            if (s >= NST) mbar_wait(&sm.empty[buf], ((s / NST) & 1u) ^ 1u);
+            if (s >= NST) mbar_wait_sleep(&sm.empty[buf], ((s / NST) & 1u) ^ 1u, 64);
 #pragma unroll
             for (int q = 0; q < SE / 32; ++q) {
                 const int j = q * 32 + (int)lane;

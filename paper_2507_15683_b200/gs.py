@@ -60,7 +60,7 @@ class gs_projected(ctypes.Structure):
 class gs_bins(ctypes.Structure):
     _fields_ = [("ranges", ctypes.c_void_p), ("sorted_rec", ctypes.c_void_p), ("pair_capacity", ctypes.c_int64),
                 ("n_pairs", ctypes.c_void_p), ("sorted_key", ctypes.c_void_p), ("sorted_gid", ctypes.c_void_p),
-                ("tile_sched", ctypes.c_void_p)]
+                ("tile_sched", ctypes.c_void_p), ("mode", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class gs_images(ctypes.Structure):
@@ -69,7 +69,7 @@ class gs_images(ctypes.Structure):
 
 
 EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_layout", "gs_scene_block_bounds",
-           "gs_scene_features_f16",
+           "gs_scene_features_f16", "gs_validate_scene",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_backproject", "gs_visibility_score", "gs_visibility_workspace_bytes"]
 
@@ -235,10 +235,14 @@ class Projected:
         return self.rec.view(-1, RECORD_BYTES // 4)
 
 
+BINNING_MODES = {"square": 0, "tight": 1}   # GS_BIN_SQUARE, GS_BIN_TIGHT (N3, reading Q30)
+
+
 class Bins:
     def __init__(self, total_tiles: int, pair_capacity: int, device="cuda", debug_keys: bool = False,
-                 with_gid: bool = True):
+                 with_gid: bool = True, binning: str = "tight"):
         self.pair_capacity = int(pair_capacity)
+        self.binning = binning
         self.ranges = torch.empty(total_tiles * 2, dtype=torch.int32, device=device)
         self.sorted_rec = torch.empty(self.pair_capacity, dtype=torch.int32, device=device)
         self.n_pairs = torch.zeros(1, dtype=torch.int64, device=device)
@@ -249,6 +253,7 @@ class Bins:
         s.ranges, s.sorted_rec, s.pair_capacity = _ptr(self.ranges), _ptr(self.sorted_rec), self.pair_capacity
         s.n_pairs, s.sorted_key, s.sorted_gid = _ptr(self.n_pairs), _ptr(self.sorted_key), _ptr(self.sorted_gid)
         s.tile_sched = _ptr(self.tile_sched)
+        s.mode = BINNING_MODES[binning]
         self.struct = s
 
 
@@ -330,3 +335,16 @@ def gs_visibility_score(proj: Projected, views: ViewBatch, eps: float, scene: "D
                                      _ptr(fmaps), ctypes.c_int32(stride), _ptr(ws), ctypes.c_size_t(nbytes),
                                      _ptr(visible), _ptr(n_visible), _ptr(score_sum), _ptr(count), _stream(stream)),
            "gs_visibility_score")
+
+
+GS_BAD_REASONS = {0: "none", 1: "position", 2: "quat", 3: "quat_norm", 4: "scale", 5: "opacity", 6: "sh", 7: "feature"}
+
+
+def gs_validate_scene(scene: "DeviceScene", unit_quat: bool = False, stream=None):
+    """Debug check of SPEC's Gaussian invariants: (first offending index or -1, reason name)."""
+    dev = scene.pos.device
+    first = torch.empty(1, dtype=torch.int64, device=dev)
+    reason = torch.empty(1, dtype=torch.int32, device=dev)
+    _check(lib().gs_validate_scene(ctypes.byref(scene.struct), ctypes.c_int32(1 if unit_quat else 0), _ptr(first),
+                                   _ptr(reason), _stream(stream)), "gs_validate_scene")
+    return int(first.item()), GS_BAD_REASONS[int(reason.item())]

@@ -19,7 +19,7 @@ class Renderer:
     def __init__(self, scene: G.DeviceScene, views: Sequence, params: Optional[G.gs_params] = None,
                  a_min: float = 0.5, backproject: bool = True, rec_capacity: Optional[int] = None,
                  pair_capacity: Optional[int] = None, debug_keys: bool = False, use_blocks: bool = True,
-                 contrib: bool = False, device="cuda"):
+                 contrib: bool = False, binning: str = "tight", device="cuda"):
         self.device = torch.device(device)
         self.scene = scene
         self.scene_struct = scene.struct if use_blocks else scene.without_blocks()
@@ -29,6 +29,7 @@ class Renderer:
         self.do_backproject = backproject
         self.debug_keys = debug_keys
         self.with_contrib = contrib
+        self.binning = binning
         n_views = self.vb.n
         self.ws_proj = torch.empty(max(1, G.project_workspace_bytes(scene.n_blocks if use_blocks else 0, n_views)),
                                    dtype=torch.uint8, device=self.device)
@@ -60,7 +61,8 @@ class Renderer:
         if self.bins is None or self.bins.pair_capacity != pair_capacity:
             self.bins = None
             self.ws_bin = None
-            self.bins = G.Bins(self.vb.total_tiles, pair_capacity, device=self.device, debug_keys=self.debug_keys)
+            self.bins = G.Bins(self.vb.total_tiles, pair_capacity, device=self.device, debug_keys=self.debug_keys,
+                               binning=self.binning)
             self.ws_bin = torch.empty(G.bin_sort_workspace_bytes(pair_capacity, self.vb.total_tiles),
                                       dtype=torch.uint8, device=self.device)
 

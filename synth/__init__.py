@@ -359,8 +359,11 @@ def c4_views(n_side: int = 16, extent: float = 1000.0, seed: int = 4, width: int
 
 def c5_views(extent: float = 2000.0, seed: int = 5, n_pos: int = 8, n_head: int = 8,
              width: int = 1920, height: int = 1080, f: float = 1500.0) -> List[View]:
-    """C5: 64 oblique views (pitch 45 deg, altitude 300 m), 8 headings x 8 positions."""
+    """C5: 64 oblique views (pitch 45 deg, altitude 300 m at the full 2 km extent),
+    8 headings x 8 positions.  The altitude scales with the extent (at least 60 m)
+    so the reduced-size test scenes stay in view."""
     rng = np.random.default_rng(seed)
+    alt = max(0.15 * extent, 60.0)
     views = []
     for ip in range(n_pos):
         ang = 2 * np.pi * ip / n_pos
@@ -370,7 +373,7 @@ def c5_views(extent: float = 2000.0, seed: int = 5, n_pos: int = 8, n_head: int 
             hd = 2 * np.pi * ih / n_head
             fwd = np.array([math.cos(hd) * math.sin(math.pi / 4), math.sin(hd) * math.sin(math.pi / 4),
                             -math.cos(math.pi / 4)])
-            R, t = look_from([px, py, 300.0], fwd)
+            R, t = look_from([px, py, alt], fwd)
             views.append(make_view(R, t, f, f, (width - 1) / 2, (height - 1) / 2, width, height))
     return views
 

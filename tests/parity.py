@@ -45,6 +45,8 @@ def check_records(gpu_rec: dict, orc_rec: dict, view_index: int):
     expect = np.stack([k * c[:, 0], (np.float32(2) * k) * c[:, 1], k * c[:, 2]], 1).astype(np.float32)
     np.testing.assert_array_equal(g["ecoef"].view(np.uint32), expect.view(np.uint32),
                                   err_msg="exponent coefficients not bit-exact")
+    np.testing.assert_array_equal(g["e_cut"].view(np.uint32), orc_rec["e_cut"].view(np.uint32),
+                                  err_msg="e_cut not bit-exact (reading Q30)")
     np.testing.assert_array_equal(g["radius"], np.minimum(orc_rec["radius"], 65535), err_msg="radius")
     np.testing.assert_array_equal(g["rect"].astype(np.int64), orc_rec["rect"].astype(np.int64), err_msg="rect")
     np.testing.assert_array_equal(g["opacity"], orc_rec["opacity"])

@@ -59,7 +59,7 @@ def test_contrib_tiny_ragged(G, orc, seed):
     W, H = int(rng.integers(8, 90)), int(rng.integers(8, 70))
     v = synth.make_view(np.eye(3), np.zeros(3), 40.0, 40.0, W / 2 - 0.5, H / 2 - 0.5, W, H)
     ds, r = _render(G, sc, [v])
-    o = orc.render(sc, v)
+    o = orc.render(sc, v, binning="tight")
     gid, contrib, _ = _gpu_view(r, 0)
     _check_view(o, gid, contrib)
 
@@ -68,7 +68,7 @@ def test_contrib_c2_and_determinism(G, orc):
     """D = 0 path (contributions without the feature MMA), C2 at quarter size."""
     sc, vs = synth.make_config("C2", scale=0.25)
     ds, r = _render(G, sc, vs)
-    o = orc.render(sc, vs[0])
+    o = orc.render(sc, vs[0], binning="tight")
     gid, contrib, _ = _gpu_view(r, 0)
     _check_view(o, gid, contrib)
     # record slots depend on atomic order; per-Gaussian sums must not (fixed point)
@@ -96,7 +96,7 @@ def test_visibility_and_scores_c4_batch(G, orc, stride):
     cnt = np.zeros(sc.n, np.int64)
     total_bad = 0
     for i, v in enumerate(vs):
-        o = orc.render(sc, v)
+        o = orc.render(sc, v, binning="tight")
         ovis, _, _ = orc.visibility_score(v, o["rec"], o["contrib"], sc.n, 1e-6, sc.feat, maps[i], stride, ssum, cnt)
         gid, contrib, vis = _gpu_view(r, i)
         _check_view(o, gid, contrib, vis, ovis)

@@ -1,6 +1,7 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
 same seeded inputs.  Bit-exact records / keys / ranges; images within the
 north_star tolerances (tests/parity.py).  All tests need a B200."""
+import dataclasses
 import math
 
 import numpy as np
@@ -63,7 +64,7 @@ def compare_view(G, r, i, scene, view, orc, check_bp=True, report=None):
 def test_c1_full_parity(G, orc):
     sc, vs = synth.make_config("C1")
     r = _gpu_render(G, sc, vs)
-    o = orc.render(sc, vs[0], a_min=0.5)
+    o = orc.render(sc, vs[0], a_min=0.5, binning="tight")
     compare_view(G, r, 0, sc, vs[0], o)
 
 
@@ -71,7 +72,7 @@ def test_c1_features_D8(G, orc):
     sc = synth.box_v1(1000, seed=11, feat_dim=8)
     v = synth.box_view()
     r = _gpu_render(G, sc, [v])
-    o = orc.render(sc, v, a_min=0.5)
+    o = orc.render(sc, v, a_min=0.5, binning="tight")
     compare_view(G, r, 0, sc, v, o)
 
 
@@ -85,7 +86,7 @@ def test_random_tiny_ragged(G, orc, seed):
     W, H = int(rng.integers(1, 90)), int(rng.integers(1, 70))
     v = synth.make_view(np.eye(3), np.zeros(3), 40.0, 40.0, W / 2 - 0.5, H / 2 - 0.5, W, H)
     r = _gpu_render(G, sc, [v])
-    o = orc.render(sc, v, a_min=0.5)
+    o = orc.render(sc, v, a_min=0.5, binning="tight")
     compare_view(G, r, 0, sc, v, o)
 
 
@@ -98,7 +99,7 @@ def test_feature_contraction_tcgen05_and_mma_sync(G, orc, D, seed):
     sc = random_tiny_scene(rng, int(rng.integers(100, 600)), feat_dim=D, sh_degree=seed % 4)
     W, H = int(rng.integers(20, 120)), int(rng.integers(10, 90))
     v = synth.make_view(np.eye(3), np.zeros(3), 40.0, 40.0, W / 2 - 0.5, H / 2 - 0.5, W, H)
-    o = orc.render(sc, v, a_min=0.5)
+    o = orc.render(sc, v, a_min=0.5, binning="tight")
     feats = []
     for f16 in (True, False):
         r = _gpu_render(G, sc, [v], f16=f16)
@@ -149,7 +150,7 @@ def test_overflow_then_recovery(G, orc):
     assert r.status() & 1
     r.render()
     assert r.status() == 0
-    o = orc.render(sc, vs[0], a_min=0.5)
+    o = orc.render(sc, vs[0], a_min=0.5, binning="tight")
     compare_view(G, r, 0, sc, vs[0], o)
     r2 = G.Renderer(ds, vs, pair_capacity=64)
     r2.run()
@@ -161,7 +162,7 @@ def test_c2_full_size_parity(G, orc):
     """C2 at its BASELINE size (200k Gaussians, SH 3, 1024x768): whole image."""
     sc, vs = synth.make_config("C2")
     r = _gpu_render(G, sc, vs)
-    o = orc.render(sc, vs[0], a_min=0.5)
+    o = orc.render(sc, vs[0], a_min=0.5, binning="tight")
     st = compare_view(G, r, 0, sc, vs[0], o)
     print("C2 stats", st)
 
@@ -181,7 +182,7 @@ def test_c3_pyramid_parity(G, orc):
     sc, vs = synth.make_config("C3", scale=0.02)
     r = _gpu_render(G, sc, vs)
     for i, v in enumerate(vs):
-        o = orc.render(sc, v, a_min=0.5)
+        o = orc.render(sc, v, a_min=0.5, binning="tight")
         compare_view(G, r, i, sc, v, o)
     alone = _gpu_render(G, sc, [vs[-1]])
     for k in ("rgb", "depth", "alpha", "feat"):
@@ -194,7 +195,7 @@ def test_c3_coarse_level_long_lists(G, orc):
     sc, vs = synth.make_config("C3", scale=0.1)
     v = vs[0]
     r = _gpu_render(G, sc, [v])
-    o = orc.render(sc, v, a_min=0.5)
+    o = orc.render(sc, v, a_min=0.5, binning="tight")
     rg = o["keys"]["ranges"]
     assert (rg[:, 1] - rg[:, 0]).max() > 8192
     compare_view(G, r, 0, sc, v, o)
@@ -207,7 +208,7 @@ def test_c4_batch_parity_and_invariance(G, orc):
     vs = vs[:24]
     r = _gpu_render(G, sc, vs)
     for i in (0, 5, 11, 17, 23):
-        o = orc.render(sc, vs[i], a_min=0.5)
+        o = orc.render(sc, vs[i], a_min=0.5, binning="tight")
         compare_view(G, r, i, sc, vs[i], o)
     alone = _gpu_render(G, sc, [vs[11]])
     for k in ("rgb", "depth", "alpha", "feat", "xyz", "valid"):
@@ -220,7 +221,7 @@ def test_c5_oblique_parity(G, orc):
     vs = vs[:4]
     r = _gpu_render(G, sc, vs)
     for i in (0, 3):
-        o = orc.render(sc, vs[i], a_min=0.5)
+        o = orc.render(sc, vs[i], a_min=0.5, binning="tight")
         compare_view(G, r, i, sc, vs[i], o)
 
 
@@ -253,7 +254,7 @@ def test_backproject_kernel_on_oracle_images(G, orc):
     identical valid masks except flagged pixels)."""
     sc, vs = synth.make_config("C2", scale=0.25)
     v = vs[0]
-    o = orc.render(sc, v, a_min=0.5)
+    o = orc.render(sc, v, a_min=0.5, binning="tight")
     vb = G.ViewBatch([v])
     img = G.Images(vb.total_pixels, 0)
     img.depth.copy_(torch.from_numpy(o["depth"].reshape(-1)))
@@ -278,5 +279,67 @@ def test_full_size_sampled_views(G, orc, cfg, views):
     r.render()
     torch.cuda.synchronize()
     for i in views:
-        o = orc.render(sc, vs[i], a_min=0.5)
+        o = orc.render(sc, vs[i], a_min=0.5, binning="tight")
         compare_view(G, r, i, sc, vs[i], o)
+
+
+# ------------------------------------------------------------------ gs_validate_scene (debug, S:90 / S:106)
+@pytest.mark.parametrize("field,idx,value,reason", [
+    ("pos", 17, np.nan, "position"), ("quat", 3, 0.0, "quat"), ("scale", 40, -1.0, "scale"),
+    ("scale", 41, 0.0, "scale"), ("opacity", 9, 1.5, "opacity"), ("opacity", 10, np.nan, "opacity"),
+    ("sh", 55, np.inf, "sh"), ("feat", 70, np.nan, "feature")])
+def test_validate_scene_names_first_offender(G, field, idx, value, reason):
+    sc = synth.box_v1(200, seed=3, feat_dim=8, sh_degree=1)
+    ds = G.DeviceScene(sc)
+    assert G.gs_validate_scene(ds) == (-1, "none")
+    arr = getattr(sc, field).copy()
+    for i in (idx, idx + 100):                  # two offenders: the first is reported
+        if field == "quat":
+            arr[:, i] = value                   # zero quaternion
+        elif field == "feat":
+            arr[i, 1] = value
+        elif arr.ndim == 2:
+            arr[-1, i] = value                  # last component / coefficient of Gaussian i
+        else:
+            arr[i] = value
+    bad = dataclasses.replace(sc, **{field: arr})
+    assert G.gs_validate_scene(G.DeviceScene(bad)) == (idx, reason)
+
+
+def test_validate_scene_unit_quaternion_mode(G):
+    """S:90 requires |q| = 1 within 1e-6; the hot path normalises (Q2), so that
+    check is opt-in."""
+    sc = synth.box_v1(50, seed=4)
+    q = sc.quat.copy()
+    q /= np.linalg.norm(q, axis=0, keepdims=True)
+    q[:, 12] *= 1.001
+    bad = dataclasses.replace(sc, quat=q.astype(np.float32))
+    ds = G.DeviceScene(bad)
+    assert G.gs_validate_scene(ds) == (-1, "none")
+    assert G.gs_validate_scene(ds, unit_quat=True) == (12, "quat_norm")
+
+
+# ------------------------------------------------------------------ N3: binning modes
+@pytest.mark.parametrize("cfg,scale,nv", [("C2", 0.25, 1), ("C4", 0.01, 4), ("C5", 0.005, 2)])
+def test_square_and_tight_binning_keys_and_identical_images(G, orc, cfg, scale, nv):
+    """GS_BIN_SQUARE keys bit-exact against the oracle's square mode, GS_BIN_TIGHT
+    keys against its tight mode (reading Q30); the two modes render bit-identical
+    RGB, depth, opacity, back-projection and contributions on the GPU (features
+    up to fp32 summation grouping)."""
+    sc, vs = synth.make_config(cfg, scale=scale)
+    vs = vs[:nv]
+    rs = {b: _gpu_render(G, sc, vs, binning=b, contrib=True) for b in ("square", "tight")}
+    assert rs["tight"].n_pairs() < rs["square"].n_pairs()
+    for i in range(nv):
+        for b, r in rs.items():
+            o = orc.render(sc, vs[i], a_min=0.5, binning=b)
+            compare_view(G, r, i, sc, vs[i], o)
+        a, b = rs["square"].view_images(i), rs["tight"].view_images(i)
+        for k in ("rgb", "depth", "alpha", "xyz", "valid"):
+            assert torch.equal(a[k], b[k]), k
+        if "feat" in a:
+            # same blends; a zero-weight row the warp cull admits only in square mode shifts
+            # the grouping of the tensor-core k-steps, i.e. the fp32 summation order
+            scale = max(1.0, float(np.abs(sc.feat).max()))
+            assert float((a["feat"] - b["feat"]).abs().max()) <= 1e-5 * scale
+    assert torch.equal(rs["square"].proj.contrib.sum(), rs["tight"].proj.contrib.sum())
