@@ -271,6 +271,45 @@ gs_status gs_scene_features_f16(const gs_scene* scene, void* feat_h_out, void* s
 gs_status gs_validate_scene(const gs_scene* scene, int32_t unit_quat, int64_t* first_bad, int32_t* reason,
                             void* stream);
 
+/*
+ * N2 -- coarse-to-fine probabilistic mutual matching (Eq. 11 at
+ * P:312-316; readings Q31-Q34).  For each of n_pairs (query,
+ * rendered) feature-map pairs of equal size, planar [D][H][W] f32 (the layout
+ * of gs_images.feat), H and W multiples of w = 8:
+ *   coarse: w x w average pooling, cosine similarity M over the
+ *   (H/8 W/8)^2 cell pairs, P = softmax_row(M/tau) (.) softmax_col(M/tau),
+ *   mutual nearest neighbours with P > p_min (ties to the lowest index);
+ *   fine: for every coarse match, the same between the 64 pixels of the two
+ *   cells, then a 3 x 3 soft-argmax of P around the peak, clipped to the
+ *   window; optionally the peak's back-projected point (gs_backproject
+ *   output of the rendered view, [n_pairs][3][H][W] + [n_pairs][H][W]).
+ * All outputs are dense and fully overwritten; pixel index = py * W + px.
+ */
+typedef struct gs_matches {
+    int32_t* coarse;      /* [n_pairs][Nc], Nc = (H/8)(W/8): rendered cell matched to query cell, or -1 */
+    float* coarse_prob;   /* [n_pairs][Nc]: P of the coarse match (0 if none) */
+    int32_t* peak;        /* [n_pairs][H*W]: rendered pixel matched to each query pixel, or -1 */
+    float* prob;          /* [n_pairs][H*W]: P of the fine match (0 if none) */
+    float* ref;           /* [n_pairs][2][H*W]: sub-pixel rendered position (x, y) (0 if none) */
+    float* xyz;           /* optional [n_pairs][3][H*W]: back-projected point at the peak (0 if none) */
+    uint8_t* valid;       /* optional [n_pairs][H*W]: matched and the peak's depth is valid */
+} gs_matches;
+
+/* Workspace of gs_match (0 for invalid sizes). */
+size_t gs_match_workspace_bytes(int32_t n_pairs, int32_t D, int32_t H, int32_t W);
+
+/*
+ * gs_match -- N2 as above on `stream`.  D in {16, 32, 48, 64}; tau > 0
+ * (SPEC default 0.1), p_min (default 0.05).  rend_xyz / rend_valid may be
+ * NULL (then out->xyz / out->valid are written as 0 when present).  ws: device,
+ * 256-byte aligned, >= gs_match_workspace_bytes.  Errors: GS_INVALID_ARG
+ * (NULL / misaligned pointers, sizes not multiples of 8, tau <= 0),
+ * GS_UNSUPPORTED (D), GS_WORKSPACE_TOO_SMALL.
+ */
+gs_status gs_match(const float* query_feat, const float* rend_feat, int32_t n_pairs, int32_t D, int32_t H,
+                   int32_t W, float tau, float p_min, const float* rend_xyz, const uint8_t* rend_valid, void* ws,
+                   size_t ws_bytes, gs_matches* out, void* stream);
+
 /* Workspace of gs_project: a (view x block) visibility bitmask. */
 size_t gs_project_workspace_bytes(int32_t n_blocks, int32_t n_views);
 

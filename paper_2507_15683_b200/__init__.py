@@ -8,8 +8,9 @@ fallback.
 """
 from .gs import (GSError, DeviceScene, ViewBatch, Projected, Bins, Images, default_params,  # noqa: F401
                  gs_project, gs_bin_sort, gs_rasterize, gs_backproject, gs_visibility_score, gs_validate_scene,
-                 lib, LIB_PATH, EXPORTS)
+                 gs_match, Matches, match_workspace_bytes, lib, LIB_PATH, EXPORTS)
 from .pipeline import Renderer, SignificanceScorer  # noqa: F401
 
-__all__ = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_backproject", "gs_visibility_score", "DeviceScene",
+__all__ = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_backproject", "gs_visibility_score", "gs_match",
+           "gs_validate_scene", "Matches", "DeviceScene",
            "ViewBatch", "Projected", "Bins", "Images", "Renderer", "SignificanceScorer", "default_params", "GSError"]

@@ -30,8 +30,9 @@ SOURCES = {
     "gs_rasterize.cu": [],
     "gs_backproject.cu": [],
     "gs_visibility.cu": [],
+    "gs_match.cu": [],
 }
-HEADERS = [os.path.join(INCLUDE, "gs.h"), os.path.join(CSRC, "gs_common.cuh")]
+HEADERS = [os.path.join(INCLUDE, "gs.h"), os.path.join(CSRC, "gs_common.cuh"), os.path.join(CSRC, "gs_tc.cuh")]
 
 
 def _stale(target, deps):

@@ -1,0 +1,509 @@
+// gs_match.cu -- N2: coarse-to-fine
+// probabilistic mutual matching between a query feature map and a rendered
+// feature map (Eq. 11 at P:312-316; readings
+// Q31-Q34).
+//
+//   1. pool_kernel: w x w (w = 8) average pooling of both maps (Q31), L2
+//      normalisation (Q32), split into fp16 hi + lo; written twice: K-major
+//      rows (A operand, staged to TMEM) and 128-cell MN-major canonical chunks
+//      (B operand, one TMA bulk copy per chunk).
+//   2. row_kernel<STATS>: per 128 query cells, stream all column chunks of
+//      128 cells through a double-buffered shared ring (cp.async.bulk) and a
+//      double-buffered TMEM accumulator; M = A B^T by tcgen05 kind::f16 MMAs
+//      (hi.hi + hi.lo + lo.hi, ~2^-22 relative: fp32-grade cosines); the 8
+//      epilogue warps read their lane quarter / column half with tcgen05.ld and
+//      keep an online log2-sum-exp2 of x = M log2(e)/tau per row:
+//      c_i = log2 sum_j 2^(x_ij).
+//   3. row_kernel<ARGMAX>: same GEMM; log2 P_ij = 2 x_ij - c_i - c'_j (Eq. 11
+//      in log2 units), so the row argmax of P is the argmax of 2 x_ij - c'_j --
+//      no exponential per element; P is evaluated once at the maximum.
+//      Both kernels run on both directions (query rows x rendered columns and
+//      the transpose): the column statistics / column argmax of P are the row
+//      statistics / row argmax of the transposed problem, so no kernel needs
+//      a cross-CTA column reduction or atomics.
+//   4. mnn_kernel: (i, j) iff argmax_row(i) = j, argmax_col(j) = i and
+//      P_ij > p_min (ties to the lowest index, Q33).
+//   5. fine_kernel: one CTA per coarse match -- Eq. 11 + MNN between the
+//      64 pixels of the query cell and the 64 of the matched rendered cell
+//      (Q34) in fp32 on the CUDA cores (64 x 64 x D per window), 3 x 3
+//      soft-argmax around the peak, gather of the peak's back-projected point.
+#include <cuda_fp16.h>
+
+#include <cmath>
+
+#include "gs_common.cuh"
+#include "gs_tc.cuh"
+
+namespace gs {
+namespace {
+
+constexpr int MW = 8;                    // window w = H_f / H_c
+constexpr int CB = 128;                  // cells per row block (M) and per column chunk (N)
+constexpr int EPI = 8;                   // epilogue warps: 4 lane quarters x 2 column halves
+constexpr int ROW_THREADS = (EPI + 1) * 32;
+constexpr uint32_t TMEM_COLS = 512;      // 2 x 128 accumulator columns + A (hi, lo)
+constexpr float LOG2E = 1.4426950408889634f;
+
+struct MatchWs {
+    __half* a[2][2];      // [map][hi/lo] -> [n_pairs][Ncp][D] K-major rows
+    __half* bimg[2];      // [map] -> [n_pairs][Ncp/128][2][128 D] canonical chunks (hi, lo)
+    float* c2[2];         // [direction] -> [n_pairs][Ncp] row log2-sum-exp2
+    int32_t* arg[2];      // [direction] -> [n_pairs][Ncp] row argmax of P
+    float* pbest;         // [n_pairs][Ncp] P at the direction-0 argmax
+};
+
+inline int64_t pad_cells(int64_t nc) { return (nc + CB - 1) / CB * CB; }
+
+MatchWs carve(void* ws, int64_t B, int64_t Ncp, int D, size_t* total) {
+    MatchWs w{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) -> char* {
+        char* p = static_cast<char*>(ws) + off;
+        off += (bytes + 255) & ~size_t(255);
+        return p;
+    };
+    const size_t plane = (size_t)B * Ncp * D * sizeof(__half);
+    for (int m = 0; m < 2; ++m)
+        for (int h = 0; h < 2; ++h) w.a[m][h] = reinterpret_cast<__half*>(take(plane));
+    for (int m = 0; m < 2; ++m) w.bimg[m] = reinterpret_cast<__half*>(take(2 * plane));
+    for (int d = 0; d < 2; ++d) w.c2[d] = reinterpret_cast<float*>(take((size_t)B * Ncp * 4));
+    for (int d = 0; d < 2; ++d) w.arg[d] = reinterpret_cast<int32_t*>(take((size_t)B * Ncp * 4));
+    w.pbest = reinterpret_cast<float*>(take((size_t)B * Ncp * 4));
+    if (total) *total = off;
+    return w;
+}
+
+// ---------------------------------------------------------------- 1. pooling
+// one warp per (cell, map, pair); lane handles channels lane and lane + 32
+__global__ void __launch_bounds__(256) pool_kernel(const float* __restrict__ Fq, const float* __restrict__ Fr, int D,
+                                                   int H, int W, int Nc, int Ncp, MatchWs ws) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cell = blockIdx.x * 8 + warp, m = blockIdx.y, b = blockIdx.z;
+    if (cell >= Ncp) return;
+    const int Wc = W / MW;
+    const float* F = (m == 0 ? Fq : Fr) + (int64_t)b * D * H * W;
+    float v[2] = {0.f, 0.f};
+    if (cell < Nc) {
+        const int cy = cell / Wc, cx = cell % Wc;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int ch = lane + 32 * t;
+            if (ch < D) {
+                float s = 0.f;
+                const float* p = F + (int64_t)ch * H * W + (int64_t)(cy * MW) * W + cx * MW;
+                for (int y = 0; y < MW; ++y) {
+                    const float4 a = __ldg(reinterpret_cast<const float4*>(p + (int64_t)y * W));
+                    const float4 c = __ldg(reinterpret_cast<const float4*>(p + (int64_t)y * W) + 1);
+                    s += ((a.x + a.y) + (a.z + a.w)) + ((c.x + c.y) + (c.z + c.w));
+                }
+                v[t] = s * (1.0f / (MW * MW));
+            }
+        }
+    }
+    float ss = v[0] * v[0] + v[1] * v[1];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float inv = ss > 0.f ? 1.0f / sqrtf(ss) : 0.f;   // zero vector stays zero (Q32)
+    const int64_t rowbase = ((int64_t)b * Ncp + cell) * D;
+    const int chunk = cell / CB, n = cell % CB;
+    __half* bi = ws.bimg[m] + ((int64_t)b * (Ncp / CB) + chunk) * 2 * CB * D;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int k = lane + 32 * t;
+        if (k < D) {
+            const float x = v[t] * inv;
+            const __half hi = __float2half_rn(x);
+            const __half lo = __float2half_rn(x - __half2float(hi));
+            ws.a[m][0][rowbase + k] = hi;
+            ws.a[m][1][rowbase + k] = lo;
+            // canonical MN-major (k, n): n/8 * 64 + (k%8) * 8 + (k/8) * (8 * CB) + n%8 halves
+            const int64_t e = (n >> 3) * 64 + (k & 7) * 8 + (k >> 3) * (8 * CB) + (n & 7);
+            bi[e] = hi;
+            bi[CB * D + e] = lo;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- 2./3. rows
+template <int D>
+struct RowSmem {
+    alignas(128) __half b[2][2][CB * D];   // [stage][hi/lo] canonical chunk
+    float part_v[CB];                       // column-half 1 partials (m or best value)
+    float part_w[CB];                       // (l or best index)
+    uint64_t full[2], empty[2], dfull[2], dfree[2];
+    uint32_t tmem;
+};
+
+// Direction d: rows = map d (0 query, 1 rendered), columns = map 1 - d.
+template <int D, bool ARGMAX>
+__global__ void __launch_bounds__(ROW_THREADS, 1)
+row_kernel(MatchWs ws, int Nc, int Ncp, float k2) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    RowSmem<D>& sm = *reinterpret_cast<RowSmem<D>*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rb = blockIdx.x, d = blockIdx.y, b = blockIdx.z;
+    const int nch = Ncp / CB;
+    const int rows_map = d, cols_map = 1 - d;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], 1);
+            mbar_init(&sm.dfull[s], 1);
+            mbar_init(&sm.dfree[s], EPI);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) tmem_alloc(&sm.tmem, TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem;
+    const uint32_t tA = tmem + 2 * CB;           // A hi: D/2 columns, then A lo: D/2 columns
+    // A (this block's 128 rows, hi and lo) -> TMEM, one lane per row
+    if (warp < 4) {
+        const int row = warp * 32 + lane;
+        const int64_t base = ((int64_t)b * Ncp + rb * CB + row) * D;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint4* src = reinterpret_cast<const uint4*>(ws.a[rows_map][h] + base);
+#pragma unroll
+            for (int c8 = 0; c8 < D / 16; ++c8) {   // 16 halves = 8 TMEM columns per store
+                const uint4 x = __ldg(src + 2 * c8), y = __ldg(src + 2 * c8 + 1);
+                const uint32_t r[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+                tmem_st8(tA + ((uint32_t)(warp * 32) << 16) + h * (D / 2) + c8 * 8, r);
+            }
+        }
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    const __half* bsrc = ws.bimg[cols_map] + (int64_t)b * nch * 2 * CB * D;
+    constexpr uint32_t CHUNK_BYTES = 2 * CB * D * sizeof(__half);
+    if (warp == EPI) {
+        // ------------------------------------------------ producer + MMA issuer
+        if (lane == 0) {
+            for (int c = 0; c < 2 && c < nch; ++c) {
+                mbar_expect_tx(&sm.full[c], CHUNK_BYTES);
+                bulk_g2s(&sm.b[c][0][0], bsrc + (int64_t)c * 2 * CB * D, CHUNK_BYTES, &sm.full[c]);
+            }
+            constexpr uint32_t IDESC = idesc_f16(CB, CB);
+            for (int c = 0; c < nch; ++c) {
+                const int s = c & 1;
+                const uint32_t ph = (c >> 1) & 1;
+                mbar_wait(&sm.full[s], ph);
+                if (c >= 2) mbar_wait(&sm.dfree[s], ph ^ 1u);
+                tc_fence_after();
+                const uint32_t dst = tmem + s * CB;
+#pragma unroll
+                for (int ks = 0; ks < D / 16; ++ks) {
+                    // K-step ks = k-groups 2ks, 2ks+1: B start + ks * 2 * LBO, A columns + ks * 8
+                    const uint64_t bh = smem_desc(&sm.b[s][0][0] + ks * 2 * 8 * CB, 16 * CB, 128);
+                    const uint64_t bl = smem_desc(&sm.b[s][1][0] + ks * 2 * 8 * CB, 16 * CB, 128);
+                    const uint32_t ah = tA + ks * 8, al = tA + D / 2 + ks * 8;
+                    tc_mma_f16(dst, ah, bh, IDESC, ks > 0 ? 1u : 0u, 4);
+                    tc_mma_f16(dst, ah, bl, IDESC, 1u, 4);
+                    tc_mma_f16(dst, al, bh, IDESC, 1u, 4);
+                }
+                tc_commit(&sm.dfull[s]);
+                tc_commit(&sm.empty[s]);
+                if (c + 2 < nch) {
+                    mbar_wait(&sm.empty[s], ph);
+                    mbar_expect_tx(&sm.full[s], CHUNK_BYTES);
+                    bulk_g2s(&sm.b[s][0][0], bsrc + (int64_t)(c + 2) * 2 * CB * D, CHUNK_BYTES, &sm.full[s]);
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ epilogue warps
+        const int q = warp & 3, hh = warp >> 2;
+        const int row = q * 32 + lane;
+        const int64_t gi = (int64_t)b * Ncp + rb * CB + row;
+        const float* cother = ws.c2[1 - d] + (int64_t)b * Ncp;
+        float run_m = -INFINITY, run_l = 0.f;      // STATS: online log2-sum-exp2
+        float best = -INFINITY;                    // ARGMAX: max of 2x - c'_j
+        int bj = -1;
+        for (int c = 0; c < nch; ++c) {
+            const int s = c & 1;
+            const uint32_t ph = (c >> 1) & 1;
+            mbar_wait(&sm.dfull[s], ph);
+            tc_fence_after();
+            float x[64];
+            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + s * CB + hh * 64;
+            tmem_ld32(ta, x);
+            tmem_ld32(ta + 32, x + 32);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.dfree[s]);
+            const int j0 = c * CB + hh * 64;
+            const int nv = min(64, Nc - j0);
+            if constexpr (!ARGMAX) {
+                float mx = -INFINITY;
+#pragma unroll
+                for (int t = 0; t < 64; ++t) {
+                    x[t] *= k2;
+                    if (t < nv) mx = fmaxf(mx, x[t]);
+                }
+                if (nv > 0) {
+                    const float mn = fmaxf(run_m, mx);
+                    float acc = 0.f;
+#pragma unroll
+                    for (int t = 0; t < 64; ++t)
+                        if (t < nv) acc += ex2_ftz(x[t] - mn);
+                    run_l = run_l * ex2_ftz(run_m - mn) + acc;
+                    run_m = mn;
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < 64; ++t) {
+                    if (t < nv) {
+                        const float y = 2.f * (x[t] * k2) - __ldg(&cother[j0 + t]);
+                        if (y > best) { best = y; bj = j0 + t; }
+                    }
+                }
+            }
+        }
+        // combine the two column halves of each row
+        if (hh == 1) {
+            sm.part_v[row] = ARGMAX ? best : run_m;
+            sm.part_w[row] = ARGMAX ? __int_as_float(bj) : run_l;
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(EPI * 32) : "memory");
+        if (hh == 0 && rb * CB + row < Ncp) {
+            if constexpr (!ARGMAX) {
+                const float m1 = sm.part_v[row], l1 = sm.part_w[row];
+                const float mt = fmaxf(run_m, m1);
+                const float lt = (run_l > 0.f ? run_l * ex2_ftz(run_m - mt) : 0.f) +
+                                 (l1 > 0.f ? l1 * ex2_ftz(m1 - mt) : 0.f);
+                ws.c2[d][gi] = mt + log2f(lt);
+            } else {
+                const float b1 = sm.part_v[row];
+                const int j1 = __float_as_int(sm.part_w[row]);
+                if (b1 > best || (b1 == best && j1 >= 0 && (bj < 0 || j1 < bj))) { best = b1; bj = j1; }
+                ws.arg[d][gi] = (rb * CB + row < Nc) ? bj : -1;
+                if (d == 0) ws.pbest[gi] = bj >= 0 ? ex2_ftz(best - ws.c2[0][gi]) : 0.f;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, TMEM_COLS);
+    }
+}
+
+// ---------------------------------------------------------------- 4. MNN
+__global__ void mnn_kernel(MatchWs ws, int Nc, int Ncp, float p_min, int32_t* __restrict__ coarse,
+                           float* __restrict__ coarse_prob) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, b = blockIdx.y;
+    if (i >= Nc) return;
+    const int64_t gi = (int64_t)b * Ncp + i;
+    const int j = ws.arg[0][gi];
+    const float p = ws.pbest[gi];
+    const bool ok = j >= 0 && ws.arg[1][(int64_t)b * Ncp + j] == i && p > p_min;
+    coarse[(int64_t)b * Nc + i] = ok ? j : -1;
+    coarse_prob[(int64_t)b * Nc + i] = ok ? p : 0.f;
+}
+
+// ---------------------------------------------------------------- 5. fine windows
+constexpr int WP = MW * MW;   // 64 pixels per window
+
+__global__ void __launch_bounds__(256) fine_kernel(const float* __restrict__ Fq, const float* __restrict__ Fr, int D,
+                                                   int H, int W, int Nc, const int32_t* __restrict__ coarse,
+                                                   float k2, float p_min, const float* __restrict__ xyz,
+                                                   const uint8_t* __restrict__ valid, gs_matches out) {
+    extern __shared__ float fsm[];
+    float* qf = fsm;                      // [64][D + 1]
+    float* rf = qf + WP * (D + 1);        // [64][D + 1]
+    float* X = rf + WP * (D + 1);         // [64][65]  x = cos * log2(e) / tau
+    float* rc = X + WP * 65;              // [64] row log2-sum-exp2
+    float* cc = rc + WP;                  // [64] column log2-sum-exp2
+    int* carg = reinterpret_cast<int*>(cc + WP);   // [64] column argmax
+    const int ic = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+    const int Wc = W / MW;
+    const int64_t HW = (int64_t)H * W;
+    const int jc = coarse[(int64_t)b * Nc + ic];
+    const int qy0 = (ic / Wc) * MW, qx0 = (ic % Wc) * MW;
+    if (jc < 0) {   // no coarse match: the window's query pixels stay unmatched
+        if (tid < WP) {
+            const int64_t pl = (int64_t)(qy0 + tid / MW) * W + qx0 + tid % MW;
+            out.peak[(int64_t)b * HW + pl] = -1;
+            out.prob[(int64_t)b * HW + pl] = 0.f;
+            out.ref[(int64_t)b * 2 * HW + pl] = 0.f;
+            out.ref[(int64_t)b * 2 * HW + HW + pl] = 0.f;
+            if (out.xyz)
+                for (int k = 0; k < 3; ++k) out.xyz[(int64_t)b * 3 * HW + k * HW + pl] = 0.f;
+            if (out.valid) out.valid[(int64_t)b * HW + pl] = 0;
+        }
+        return;
+    }
+    const int ry0 = (jc / Wc) * MW, rx0 = (jc % Wc) * MW;
+    const float* Q = Fq + (int64_t)b * D * HW;
+    const float* R = Fr + (int64_t)b * D * HW;
+    for (int e = tid; e < D * WP; e += blockDim.x) {
+        const int ch = e / WP, a = e % WP;
+        qf[a * (D + 1) + ch] = __ldg(&Q[ch * HW + (int64_t)(qy0 + a / MW) * W + qx0 + a % MW]);
+        rf[a * (D + 1) + ch] = __ldg(&R[ch * HW + (int64_t)(ry0 + a / MW) * W + rx0 + a % MW]);
+    }
+    __syncthreads();
+    if (tid < 2 * WP) {   // normalise the 128 pixel vectors (zero stays zero, Q32)
+        float* v = (tid < WP ? qf : rf) + (tid % WP) * (D + 1);
+        float ss = 0.f;
+        for (int ch = 0; ch < D; ++ch) ss += v[ch] * v[ch];
+        const float inv = ss > 0.f ? 1.0f / sqrtf(ss) : 0.f;
+        for (int ch = 0; ch < D; ++ch) v[ch] *= inv;
+    }
+    __syncthreads();
+    for (int e = tid; e < WP * WP; e += blockDim.x) {
+        const int a = e / WP, bb = e % WP;
+        const float* qa = qf + a * (D + 1);
+        const float* rb = rf + bb * (D + 1);
+        float dot = 0.f;
+        for (int ch = 0; ch < D; ++ch) dot = fmaf(qa[ch], rb[ch], dot);
+        X[a * 65 + bb] = dot * k2;
+    }
+    __syncthreads();
+    if (tid < 2 * WP) {   // row (tid < 64) / column log2-sum-exp2
+        const int r = tid % WP;
+        const bool rowwise = tid < WP;
+        float mx = -INFINITY;
+        for (int t = 0; t < WP; ++t) mx = fmaxf(mx, rowwise ? X[r * 65 + t] : X[t * 65 + r]);
+        float l = 0.f;
+        for (int t = 0; t < WP; ++t) l += ex2_ftz((rowwise ? X[r * 65 + t] : X[t * 65 + r]) - mx);
+        (rowwise ? rc : cc)[r] = mx + log2f(l);
+    }
+    __syncthreads();
+    if (tid >= WP && tid < 2 * WP) {   // column argmax of P: max over rows of 2x - c_a
+        const int bb = tid - WP;
+        float best = -INFINITY;
+        int ba = -1;
+        for (int a = 0; a < WP; ++a) {
+            const float y = 2.f * X[a * 65 + bb] - rc[a];
+            if (y > best) { best = y; ba = a; }
+        }
+        carg[bb] = ba;
+    }
+    __syncthreads();
+    if (tid < WP) {
+        const int a = tid;
+        float best = -INFINITY;
+        int bs = -1;
+        for (int bb = 0; bb < WP; ++bb) {
+            const float y = 2.f * X[a * 65 + bb] - cc[bb];
+            if (y > best) { best = y; bs = bb; }
+        }
+        const float p = ex2_ftz(best - rc[a]);
+        const bool ok = bs >= 0 && carg[bs] == a && p > p_min;
+        const int64_t pl = (int64_t)(qy0 + a / MW) * W + qx0 + a % MW;   // query pixel in the view
+        const int64_t pq = (int64_t)b * HW + pl;
+        float rx = 0.f, ry = 0.f;
+        int64_t peak = -1;
+        if (ok) {
+            const int by = bs / MW, bx = bs % MW;
+            float num_x = 0.f, num_y = 0.f, den = 0.f;
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int y = by + dy, x = bx + dx;
+                    if (y < 0 || y >= MW || x < 0 || x >= MW) continue;
+                    const float w = ex2_ftz(2.f * X[a * 65 + y * MW + x] - rc[a] - cc[y * MW + x]);
+                    num_x += w * (float)x;
+                    num_y += w * (float)y;
+                    den += w;
+                }
+            rx = (float)rx0 + num_x / den;
+            ry = (float)ry0 + num_y / den;
+            peak = (int64_t)(ry0 + by) * W + rx0 + bx;
+        }
+        out.peak[pq] = (int32_t)peak;
+        out.prob[pq] = ok ? p : 0.f;
+        out.ref[(int64_t)b * 2 * HW + pl] = rx;
+        out.ref[(int64_t)b * 2 * HW + HW + pl] = ry;
+        if (out.xyz)
+            for (int k = 0; k < 3; ++k)
+                out.xyz[(int64_t)b * 3 * HW + k * HW + pl] =
+                    ok && xyz ? __ldg(&xyz[(int64_t)b * 3 * HW + k * HW + peak]) : 0.f;
+        if (out.valid) out.valid[pq] = ok && valid ? __ldg(&valid[(int64_t)b * HW + peak]) : 0;
+    }
+}
+
+template <int D>
+gs_status launch_rows(const MatchWs& w, int B, int Nc, int Ncp, float k2, cudaStream_t s) {
+    // each CTA allocates all 512 TMEM columns: request enough shared memory that only
+    // one CTA is resident per SM (a second would just wait in tcgen05.alloc)
+    const int smem = std::max((int)sizeof(RowSmem<D>), 120 * 1024);
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(row_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(row_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        init = true;
+    }
+    const dim3 grid(Ncp / CB, 2, B);
+    row_kernel<D, false><<<grid, ROW_THREADS, smem, s>>>(w, Nc, Ncp, k2);
+    gs_status st = check_launch("row_kernel<stats>");
+    if (st != GS_OK) return st;
+    row_kernel<D, true><<<grid, ROW_THREADS, smem, s>>>(w, Nc, Ncp, k2);
+    return check_launch("row_kernel<argmax>");
+}
+
+}  // namespace
+}  // namespace gs
+
+using namespace gs;
+
+extern "C" size_t gs_match_workspace_bytes(int32_t n_pairs, int32_t D, int32_t H, int32_t W) {
+    if (n_pairs < 1 || D < 1 || H < MW || W < MW) return 0;
+    size_t total = 0;
+    carve(nullptr, n_pairs, pad_cells((int64_t)(H / MW) * (W / MW)), D, &total);
+    return total;
+}
+
+extern "C" gs_status gs_match(const float* query_feat, const float* rend_feat, int32_t n_pairs, int32_t D, int32_t H,
+                              int32_t W, float tau, float p_min, const float* rend_xyz, const uint8_t* rend_valid,
+                              void* ws, size_t ws_bytes, gs_matches* out, void* stream) {
+    GS_REQUIRE(query_feat && rend_feat && out && out->coarse && out->coarse_prob && out->peak && out->prob &&
+                   out->ref,
+               GS_INVALID_ARG, "gs_match: NULL pointer");
+    GS_REQUIRE(n_pairs >= 1 && n_pairs <= 65535, GS_INVALID_ARG, "n_pairs = %d", n_pairs);
+    GS_REQUIRE(D == 16 || D == 32 || D == 48 || D == 64, GS_UNSUPPORTED, "gs_match: D = %d (need 16, 32, 48, 64)",
+               D);
+    GS_REQUIRE(H >= MW && W >= MW && H % MW == 0 && W % MW == 0, GS_INVALID_ARG,
+               "gs_match: H = %d, W = %d must be positive multiples of %d (Q31)", H, W, MW);
+    GS_REQUIRE((int64_t)H * W * D < (int64_t(1) << 31), GS_UNSUPPORTED, "gs_match: map too large");
+    GS_REQUIRE(tau > 0.f && std::isfinite(tau) && std::isfinite(p_min), GS_INVALID_ARG, "gs_match: tau = %g",
+               (double)tau);
+    GS_REQUIRE(((uintptr_t)query_feat & 15) == 0 && ((uintptr_t)rend_feat & 15) == 0 && ((uintptr_t)ws & 255) == 0,
+               GS_INVALID_ARG, "gs_match: feature maps must be 16-byte and ws 256-byte aligned");
+    const int Nc = (H / MW) * (W / MW);
+    const int Ncp = (int)pad_cells(Nc);
+    size_t need = 0;
+    MatchWs w = carve(ws, n_pairs, Ncp, D, &need);
+    GS_REQUIRE(ws != nullptr && ws_bytes >= need, GS_WORKSPACE_TOO_SMALL, "gs_match workspace %zu < %zu", ws_bytes,
+               need);
+    cudaStream_t s = (cudaStream_t)stream;
+    const float k2 = LOG2E / tau;
+    pool_kernel<<<dim3((Ncp + 7) / 8, 2, n_pairs), 256, 0, s>>>(query_feat, rend_feat, D, H, W, Nc, Ncp, w);
+    gs_status st = check_launch("pool_kernel");
+    if (st != GS_OK) return st;
+    switch (D) {
+        case 16: st = launch_rows<16>(w, n_pairs, Nc, Ncp, k2, s); break;
+        case 32: st = launch_rows<32>(w, n_pairs, Nc, Ncp, k2, s); break;
+        case 48: st = launch_rows<48>(w, n_pairs, Nc, Ncp, k2, s); break;
+        default: st = launch_rows<64>(w, n_pairs, Nc, Ncp, k2, s); break;
+    }
+    if (st != GS_OK) return st;
+    mnn_kernel<<<dim3((Nc + 255) / 256, n_pairs), 256, 0, s>>>(w, Nc, Ncp, p_min, out->coarse, out->coarse_prob);
+    if ((st = check_launch("mnn_kernel")) != GS_OK) return st;
+    const int fsmem = (int)sizeof(float) * (2 * WP * (D + 1) + WP * 65 + 3 * WP);
+    static bool fine_init = false;
+    if (!fine_init) {
+        cudaFuncSetAttribute(fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        fine_init = true;
+    }
+    fine_kernel<<<dim3(Nc, n_pairs), 256, fsmem, s>>>(query_feat, rend_feat, D, H, W, Nc, out->coarse, k2, p_min,
+                                                      rend_xyz, rend_valid, *out);
+    return check_launch("fine_kernel");
+}

@@ -44,6 +44,7 @@
 #include <cstdlib>
 
 #include "gs_common.cuh"
+#include "gs_tc.cuh"
 
 namespace gs {
 namespace {
@@ -57,43 +58,6 @@ constexpr int WB_ROWS = 16;            // one tensor-core k-step of weights (m16
 constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
 constexpr uint32_t SCHED_CHUNK = 2;    // tiles per scheduler claim
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// wait with back-off: a warp with nothing else to do (the producer when the ring is
-// full) must not steal issue slots from the consumer warps of its scheduler
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
-    uint32_t ok = 0;
-    for (;;) {
-        asm volatile(
-            "{\n"
-            ".reg .pred p;\n"
-            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
-            "selp.u32 %0, 1, 0, p;\n"
-            "}\n"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (ok) return;
-        __nanosleep(ns);
-    }
-}
 // 16-B global->shared copy that asks L2 to keep the line (records and feature rows
 // are re-read by the ~4 neighbouring tiles a Gaussian overlaps)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint64_t policy) {
@@ -113,11 +77,6 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
 // round a finite fp32 to the nearest tf32 (ties away from zero) with integer ops; the
 // tensor core reads only the top 19 bits of a .tf32 operand
 __device__ __forceinline__ uint32_t to_tf32(float x) { return (__float_as_uint(x) + 0x1000u) & 0xffffe000u; }
-__device__ __forceinline__ float ex2_ftz(float x) {
-    float r;
-    asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(r) : "f"(x));
-    return r;
-}
 __device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -133,48 +92,6 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// ---- tcgen05 (5th-gen tensor cores, TMEM accumulators) -------------------------
-// Used for the feature contraction when D is a multiple of 16 (N = D of an M = 128
-// MMA).  Each consumer warp owns the 32 TMEM lanes of its lane quarter (warp % 4)
-// inside a D-column accumulator region shared with the three other warps of its
-// group (warp / 4); its MMAs disable every other lane (disable-output-lane mask),
-// so the 8 warps issue independently without racing on TMEM.
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(r[0]),
-                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* f) {
-    uint32_t d[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]),
-          "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
-        : "r"(taddr)
-        : "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(d[i]);
-}
-// D[tmem] (+)= A[tmem] B[smem]: M = 128, N = n, K = 16, fp16 inputs, fp32 accumulation;
-// only the 32 TMEM lanes of quarter q are written
-__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                           uint32_t accumulate, uint32_t q) {
-    const uint32_t m0 = q == 0 ? 0u : 0xffffffffu, m1 = q == 1 ? 0u : 0xffffffffu;
-    const uint32_t m2 = q == 2 ? 0u : 0xffffffffu, m3 = q == 3 ? 0u : 0xffffffffu;
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(m0), "r"(m1), "r"(m2), "r"(m3)
-        : "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-// TMEM columns of a CTA: two group accumulators (D columns each) + per group two
-// A buffers of 16 columns (fp16 weight pairs: 8 hi + 8 lo)
 template <int D>
 struct TcCfg {
     static constexpr bool eligible = D == 16 || D == 32 || D == 48 || D == 64;

@@ -69,7 +69,7 @@ class gs_images(ctypes.Structure):
 
 
 EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_layout", "gs_scene_block_bounds",
-           "gs_scene_features_f16", "gs_validate_scene",
+           "gs_scene_features_f16", "gs_validate_scene", "gs_match", "gs_match_workspace_bytes",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_backproject", "gs_visibility_score", "gs_visibility_workspace_bytes"]
 
@@ -90,6 +90,8 @@ def lib():
         L.gs_project_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32]
         L.gs_bin_sort_workspace_bytes.restype = ctypes.c_size_t
         L.gs_bin_sort_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]
+        L.gs_match_workspace_bytes.restype = ctypes.c_size_t
+        L.gs_match_workspace_bytes.argtypes = [ctypes.c_int32] * 4
         L.gs_visibility_workspace_bytes.restype = ctypes.c_size_t
         for f in ("gs_views_layout", "gs_scene_block_bounds", "gs_project", "gs_bin_sort", "gs_rasterize",
                   "gs_backproject", "gs_visibility_score"):
@@ -348,3 +350,44 @@ def gs_validate_scene(scene: "DeviceScene", unit_quat: bool = False, stream=None
     _check(lib().gs_validate_scene(ctypes.byref(scene.struct), ctypes.c_int32(1 if unit_quat else 0), _ptr(first),
                                    _ptr(reason), _stream(stream)), "gs_validate_scene")
     return int(first.item()), GS_BAD_REASONS[int(reason.item())]
+
+
+# ---------------------------------------------------------------------- N2 matching
+class gs_matches(ctypes.Structure):
+    _fields_ = [("coarse", ctypes.c_void_p), ("coarse_prob", ctypes.c_void_p), ("peak", ctypes.c_void_p),
+                ("prob", ctypes.c_void_p), ("ref", ctypes.c_void_p), ("xyz", ctypes.c_void_p),
+                ("valid", ctypes.c_void_p)]
+
+
+class Matches:
+    """Caller-side output buffers of gs_match (dense per query cell / pixel)."""
+
+    def __init__(self, n_pairs: int, H: int, W: int, with_points: bool = True, device="cuda"):
+        nc = (H // 8) * (W // 8)
+        n = H * W
+        self.n_pairs, self.H, self.W = n_pairs, H, W
+        self.coarse = torch.empty(n_pairs * nc, dtype=torch.int32, device=device)
+        self.coarse_prob = torch.empty(n_pairs * nc, dtype=torch.float32, device=device)
+        self.peak = torch.empty(n_pairs * n, dtype=torch.int32, device=device)
+        self.prob = torch.empty(n_pairs * n, dtype=torch.float32, device=device)
+        self.ref = torch.empty(n_pairs * 2 * n, dtype=torch.float32, device=device)
+        self.xyz = torch.empty(n_pairs * 3 * n, dtype=torch.float32, device=device) if with_points else None
+        self.valid = torch.empty(n_pairs * n, dtype=torch.uint8, device=device) if with_points else None
+        s = gs_matches()
+        s.coarse, s.coarse_prob, s.peak, s.prob = _ptr(self.coarse), _ptr(self.coarse_prob), _ptr(self.peak), \
+            _ptr(self.prob)
+        s.ref, s.xyz, s.valid = _ptr(self.ref), _ptr(self.xyz), _ptr(self.valid)
+        self.struct = s
+
+
+def match_workspace_bytes(n_pairs: int, D: int, H: int, W: int) -> int:
+    return int(lib().gs_match_workspace_bytes(n_pairs, D, H, W))
+
+
+def gs_match(query_feat: torch.Tensor, rend_feat: torch.Tensor, n_pairs: int, D: int, H: int, W: int,
+             out: Matches, ws: torch.Tensor, tau: float = 0.1, p_min: float = 0.05,
+             rend_xyz: Optional[torch.Tensor] = None, rend_valid: Optional[torch.Tensor] = None, stream=None):
+    _check(lib().gs_match(_ptr(query_feat), _ptr(rend_feat), ctypes.c_int32(n_pairs), ctypes.c_int32(D),
+                          ctypes.c_int32(H), ctypes.c_int32(W), ctypes.c_float(tau), ctypes.c_float(p_min),
+                          _ptr(rend_xyz), _ptr(rend_valid), _ptr(ws), ctypes.c_size_t(ws.numel()),
+                          ctypes.byref(out.struct), _stream(stream)), "gs_match")
