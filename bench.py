@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-views", type=int, default=2)
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run only this many untimed steps")
+    ap.add_argument("--n2", action="store_true",
+                    help="also time N2 gs_match on (view i, view i+1) feature-map pairs of the rendered batch")
+    ap.add_argument("--n2-pairs", type=int, default=64)
     ap.add_argument("--n1", action="store_true",
                     help="also time N1 (per-Gaussian contributions + Alg. 1 visibility + Eq. 4-6 scoring "
                          "against stride-8 synthetic target maps) inside the step")
@@ -352,6 +355,43 @@ def main():
                "h2d_bytes_per_step": int(r.vb.pinned.numel()), "d2h_bytes_per_step": int(5 * total_px * 4)}
         del host_out
 
+    # N2: coarse-to-fine matching of rendered feature maps, (view i -> query, view i+1 -> rendered)
+    n2 = None
+    if args.n2:
+        D2 = scene.feat_dim
+        H2, W2 = views[0].height, views[0].width
+        if D2 not in (16, 32, 48, 64) or H2 % 8 or W2 % 8 or n_views < 2:
+            raise SystemExit("--n2 needs D in {16,32,48,64}, sizes multiple of 8 and >= 2 views")
+        Bp = max(1, min(args.n2_pairs, n_views - 1))
+        hw = H2 * W2
+        fq = r.images.feat[:Bp * D2 * hw]
+        fr = r.images.feat[D2 * hw:(Bp + 1) * D2 * hw]
+        mo = G.Matches(Bp, H2, W2, with_points=True, device=dev)
+        mws = torch.empty(G.match_workspace_bytes(Bp, D2, H2, W2), dtype=torch.uint8, device=dev)
+        xyz2, val2 = r.xyz[3 * hw:3 * hw * (Bp + 1)], r.valid[hw:hw * (Bp + 1)]
+
+        def match():
+            G.gs_match(fq, fr, Bp, D2, H2, W2, mo, mws, rend_xyz=xyz2, rend_valid=val2, stream=stream)
+
+        for _ in range(3):
+            match()
+        torch.cuda.synchronize()
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        for _ in range(K):
+            match()
+        m1.record(stream)
+        torch.cuda.synchronize()
+        ms2 = m0.elapsed_time(m1) / K
+        nc = (H2 // 8) * (W2 // 8)
+        n2 = {"pairs": Bp, "ms": ms2, "ms_per_pair": ms2 / Bp, "fine_resolution": f"{W2}x{H2}", "feat_dim": D2,
+              "coarse_cells": nc, "coarse_similarities_per_pair": nc * nc,
+              "coarse_matches_per_pair": float((mo.coarse >= 0).sum().item()) / Bp,
+              "fine_matches_per_pair": float((mo.peak >= 0).sum().item()) / Bp,
+              "valid_2d3d_per_pair": float(mo.valid.sum().item()) / Bp,
+              "coarse_gemm_tflops": 2.0 * 3 * 2 * 2 * nc * nc * D2 * Bp / (ms2 / 1e3) / 1e12,
+              "gpu_launches": 5, "tau": 0.1, "p_min": 0.05}
+
     # roofline of the dominant kernel
     peak, peak_src = measured_peaks()
     dom = int(np.argmax(stage_ms[:4]))
@@ -379,6 +419,8 @@ def main():
            "stages_ms": {n: float(m) for n, m in zip(names, stage_ms) if n != names[4] or scorer is not None},
            "counts": {"visible_records": n_visible, "pairs": n_pairs, "pixels": total_px},
            "roofline": roof, "gpu_launches": launches_per_step * K, "e2e": e2e, "clocks": clk.summary()}
+    if n2 is not None:
+        out["n2"] = n2
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(scene, views, args.cpu_sample_views)
     if rank == 0:
