@@ -148,10 +148,11 @@ def workload(cfg: str, scale: float, rank: int, world: int, scaling: str, views_
     return scene, views
 
 
-def algorithmic_raster_bytes(n_pairs: int, n_visible: int, total_pixels: int, D: int) -> int:
-    """P*4 (sorted list) + V*(48 + 4D) (records + features,
-    read once) + H*W*(5 + D)*4 (planar outputs)."""
-    return 4 * n_pairs + n_visible * (48 + 4 * D) + total_pixels * (5 + D) * 4
+def algorithmic_raster_bytes(n_pairs: int, n_visible: int, total_pixels: int, D: int, feat_bytes: int = 4) -> int:
+    """P*4 (sorted list) + V*(48 + D*feat_bytes) (records +
+    feature rows, read once; 2-byte rows on the tcgen05 path) + H*W*(5 + D)*4
+    (planar fp32 outputs)."""
+    return 4 * n_pairs + n_visible * (48 + feat_bytes * D) + total_pixels * (5 + D) * 4
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -397,9 +398,10 @@ def main():
     dom = int(np.argmax(stage_ms[:4]))
     names = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_backproject", "n1_visibility_score"]
     D = scene.feat_dim
-    raster_bytes = algorithmic_raster_bytes(n_pairs, n_visible, total_px, D)
+    tc_path = D in (16, 32, 48, 64) and args.feature_path == "tcgen05"
+    raster_bytes = algorithmic_raster_bytes(n_pairs, n_visible, total_px, D, 2 if tc_path else 4)
     achieved = raster_bytes / (stage_ms[2] / 1e3) / 1e9
-    traffic = ncu_traffic(f"{args.config}@{args.scale}")
+    traffic = ncu_traffic(f"{args.config}@{args.scale}/{args.binning}/{'tcgen05' if tc_path else 'mma_sync'}")
     roof = {"bound": "hbm", "kernel": "gs_rasterize", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": raster_bytes, "dominant_stage": names[dom]}
