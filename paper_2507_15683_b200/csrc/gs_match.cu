@@ -127,10 +127,11 @@ __global__ void __launch_bounds__(256) pool_kernel(const float* __restrict__ Fq,
 // ---------------------------------------------------------------- 2./3. rows
 template <int D>
 struct RowSmem {
-    alignas(128) __half b[2][2][CB * D];   // [stage][hi/lo] canonical chunk
+    alignas(128) __half b[3][2][CB * D];   // [stage][hi/lo] canonical chunk (3-stage ring)
+    alignas(16) float cc[3][CB];            // [stage] column statistics c'_j of the chunk (argmax pass)
     float part_v[CB];                       // column-half 1 partials (m or best value)
     float part_w[CB];                       // (l or best index)
-    uint64_t full[2], empty[2], dfull[2], dfree[2];
+    uint64_t full[3], empty[3], dfull[2], dfree[2];
     uint32_t tmem;
 };
 
@@ -145,9 +146,11 @@ row_kernel(MatchWs ws, int Nc, int Ncp, float k2) {
     const int nch = Ncp / CB;
     const int rows_map = d, cols_map = 1 - d;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < 3; ++s) {
             mbar_init(&sm.full[s], 1);
             mbar_init(&sm.empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&sm.dfull[s], 1);
             mbar_init(&sm.dfree[s], EPI);
         }
@@ -180,38 +183,46 @@ row_kernel(MatchWs ws, int Nc, int Ncp, float k2) {
     tc_fence_after();
 
     const __half* bsrc = ws.bimg[cols_map] + (int64_t)b * nch * 2 * CB * D;
+    const float* csrc = ws.c2[1 - d] + (int64_t)b * Ncp;
     constexpr uint32_t CHUNK_BYTES = 2 * CB * D * sizeof(__half);
     if (warp == EPI) {
         // ------------------------------------------------ producer + MMA issuer
         if (lane == 0) {
-            for (int c = 0; c < 2 && c < nch; ++c) {
-                mbar_expect_tx(&sm.full[c], CHUNK_BYTES);
-                bulk_g2s(&sm.b[c][0][0], bsrc + (int64_t)c * 2 * CB * D, CHUNK_BYTES, &sm.full[c]);
-            }
             constexpr uint32_t IDESC = idesc_f16(CB, CB);
+            auto load = [&](int c, int st) {
+                mbar_expect_tx(&sm.full[st], CHUNK_BYTES + (ARGMAX ? CB * 4u : 0u));
+                bulk_g2s(&sm.b[st][0][0], bsrc + (int64_t)c * 2 * CB * D, CHUNK_BYTES, &sm.full[st]);
+                if (ARGMAX) bulk_g2s(&sm.cc[st][0], csrc + (int64_t)c * CB, CB * 4u, &sm.full[st]);
+            };
+            for (int c = 0; c < 2 && c < nch; ++c) load(c, c);
             for (int c = 0; c < nch; ++c) {
-                const int s = c & 1;
-                const uint32_t ph = (c >> 1) & 1;
-                mbar_wait(&sm.full[s], ph);
-                if (c >= 2) mbar_wait(&sm.dfree[s], ph ^ 1u);
+                const int st = c % 3, ds = c & 1;
+                mbar_wait(&sm.full[st], (uint32_t)(c / 3) & 1u);
+                if (c >= 2) mbar_wait(&sm.dfree[ds], (uint32_t)((c >> 1) - 1) & 1u);   // epilogue c-2 done
                 tc_fence_after();
-                const uint32_t dst = tmem + s * CB;
+                const uint32_t dst = tmem + ds * CB;
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
                     // K-step ks = k-groups 2ks, 2ks+1: B start + ks * 2 * LBO, A columns + ks * 8
-                    const uint64_t bh = smem_desc(&sm.b[s][0][0] + ks * 2 * 8 * CB, 16 * CB, 128);
-                    const uint64_t bl = smem_desc(&sm.b[s][1][0] + ks * 2 * 8 * CB, 16 * CB, 128);
+                    const uint64_t bh = smem_desc(&sm.b[st][0][0] + ks * 2 * 8 * CB, 16 * CB, 128);
+                    const uint64_t bl = smem_desc(&sm.b[st][1][0] + ks * 2 * 8 * CB, 16 * CB, 128);
                     const uint32_t ah = tA + ks * 8, al = tA + D / 2 + ks * 8;
                     tc_mma_f16(dst, ah, bh, IDESC, ks > 0 ? 1u : 0u, 4);
                     tc_mma_f16(dst, ah, bl, IDESC, 1u, 4);
                     tc_mma_f16(dst, al, bh, IDESC, 1u, 4);
                 }
-                tc_commit(&sm.dfull[s]);
-                tc_commit(&sm.empty[s]);
+                tc_commit(&sm.dfull[ds]);
+                tc_commit(&sm.empty[st]);
                 if (c + 2 < nch) {
-                    mbar_wait(&sm.empty[s], ph);
-                    mbar_expect_tx(&sm.full[s], CHUNK_BYTES);
-                    bulk_g2s(&sm.b[s][0][0], bsrc + (int64_t)(c + 2) * 2 * CB * D, CHUNK_BYTES, &sm.full[s]);
+                    // chunk c+2 goes to the stage of chunk c-1: its MMAs and (argmax: its c'
+                    // values) its epilogue must be done -- the latter is what the accumulator
+                    // double buffer needs before MMA c+1 anyway
+                    const int sn = (c + 2) % 3;
+                    if (c >= 1) {
+                        mbar_wait(&sm.empty[sn], (uint32_t)((c - 1) / 3) & 1u);
+                        if (ARGMAX) mbar_wait(&sm.dfree[(c - 1) & 1], (uint32_t)((c - 1) >> 1) & 1u);
+                    }
+                    load(c + 2, sn);
                 }
             }
         }
@@ -221,7 +232,6 @@ row_kernel(MatchWs ws, int Nc, int Ncp, float k2) {
         const int q = warp & 3, hh = warp >> 2;
         const int row = q * 32 + lane;
         const int64_t gi = (int64_t)b * Ncp + rb * CB + row;
-        const float* cother = ws.c2[1 - d] + (int64_t)b * Ncp;
         float run_m = -INFINITY, run_l = 0.f;      // STATS: online log2-sum-exp2
         float best = -INFINITY;                    // ARGMAX: max of 2x - c'_j
         int bj = -1;
@@ -235,11 +245,20 @@ row_kernel(MatchWs ws, int Nc, int Ncp, float k2) {
             tmem_ld32(ta, x);
             tmem_ld32(ta + 32, x + 32);
             tmem_wait_ld();
+            const int j0 = c * CB + hh * 64;
+            const int nv = min(64, Nc - j0);
+            float cj[ARGMAX ? 64 : 1];
+            if constexpr (ARGMAX) {
+                const float4* cs = reinterpret_cast<const float4*>(&sm.cc[c % 3][hh * 64]);
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const float4 v4 = cs[t];   // broadcast
+                    cj[4 * t] = v4.x; cj[4 * t + 1] = v4.y; cj[4 * t + 2] = v4.z; cj[4 * t + 3] = v4.w;
+                }
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.dfree[s]);
-            const int j0 = c * CB + hh * 64;
-            const int nv = min(64, Nc - j0);
             if constexpr (!ARGMAX) {
                 float mx = -INFINITY;
 #pragma unroll
@@ -260,7 +279,7 @@ row_kernel(MatchWs ws, int Nc, int Ncp, float k2) {
 #pragma unroll
                 for (int t = 0; t < 64; ++t) {
                     if (t < nv) {
-                        const float y = 2.f * (x[t] * k2) - __ldg(&cother[j0 + t]);
+                        const float y = 2.f * (x[t] * k2) - cj[t];
                         if (y > best) { best = y; bj = j0 + t; }
                     }
                 }
