@@ -10,8 +10,8 @@
 //   2. row_kernel<STATS>: per 128 query cells, stream all column chunks of
 //      128 cells through a double-buffered shared ring (cp.async.bulk) and a
 //      double-buffered TMEM accumulator; M = A B^T by tcgen05 kind::f16 MMAs
-//      (hi.hi + hi.lo + lo.hi, ~2^-22 relative: fp32-grade cosines); the 8
-//      epilogue warps read their lane quarter / column half with tcgen05.ld and
+//      (hi.hi + hi.lo + lo.hi, ~2^-22 relative: fp32-grade cosines); the 16
+//      epilogue warps read their lane quarter / 32-column part with tcgen05.ld and
 //      keep an online log2-sum-exp2 of x = M log2(e)/tau per row:
 //      c_i = log2 sum_j 2^(x_ij).
 //   3. row_kernel<ARGMAX>: same GEMM; log2 P_ij = 2 x_ij - c_i - c'_j (Eq. 11
@@ -39,7 +39,9 @@ namespace {
 
 constexpr int MW = 8;                    // window w = H_f / H_c
 constexpr int CB = 128;                  // cells per row block (M) and per column chunk (N)
-constexpr int EPI = 8;                   // epilogue warps: 4 lane quarters x 2 column halves
+constexpr int NH = 4;                    // column parts per chunk
+constexpr int CW = CB / NH;              // columns per epilogue warp per chunk
+constexpr int EPI = 4 * NH;              // epilogue warps: 4 TMEM lane quarters x NH column parts
 constexpr int ROW_THREADS = (EPI + 1) * 32;
 constexpr uint32_t TMEM_COLS = 512;      // 2 x 128 accumulator columns + A (hi, lo)
 constexpr float LOG2E = 1.4426950408889634f;
@@ -129,8 +131,8 @@ template <int D>
 struct RowSmem {
     alignas(128) __half b[3][2][CB * D];   // [stage][hi/lo] canonical chunk (3-stage ring)
     alignas(16) float cc[3][CB];            // [stage] column statistics c'_j of the chunk (argmax pass)
-    float part_v[CB];                       // column-half 1 partials (m or best value)
-    float part_w[CB];                       // (l or best index)
+    float part_v[NH - 1][CB];               // column parts 1.. partials (m or best value)
+    float part_w[NH - 1][CB];               // (l or best index)
     uint64_t full[3], empty[3], dfull[2], dfree[2];
     uint32_t tmem;
 };
@@ -240,18 +242,18 @@ row_kernel(MatchWs ws, int Nc, int Ncp, float k2) {
             const uint32_t ph = (c >> 1) & 1;
             mbar_wait(&sm.dfull[s], ph);
             tc_fence_after();
-            float x[64];
-            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + s * CB + hh * 64;
-            tmem_ld32(ta, x);
-            tmem_ld32(ta + 32, x + 32);
-            tmem_wait_ld();
-            const int j0 = c * CB + hh * 64;
-            const int nv = min(64, Nc - j0);
-            float cj[ARGMAX ? 64 : 1];
-            if constexpr (ARGMAX) {
-                const float4* cs = reinterpret_cast<const float4*>(&sm.cc[c % 3][hh * 64]);
+            float x[CW];
+            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + s * CB + hh * CW;
 #pragma unroll
-                for (int t = 0; t < 16; ++t) {
+            for (int t = 0; t < CW; t += 32) tmem_ld32(ta + t, x + t);
+            tmem_wait_ld();
+            const int j0 = c * CB + hh * CW;
+            const int nv = min(CW, Nc - j0);
+            float cj[ARGMAX ? CW : 1];
+            if constexpr (ARGMAX) {
+                const float4* cs = reinterpret_cast<const float4*>(&sm.cc[c % 3][hh * CW]);
+#pragma unroll
+                for (int t = 0; t < CW / 4; ++t) {
                     const float4 v4 = cs[t];   // broadcast
                     cj[4 * t] = v4.x; cj[4 * t + 1] = v4.y; cj[4 * t + 2] = v4.z; cj[4 * t + 3] = v4.w;
                 }
@@ -262,7 +264,7 @@ row_kernel(MatchWs ws, int Nc, int Ncp, float k2) {
             if constexpr (!ARGMAX) {
                 float mx = -INFINITY;
 #pragma unroll
-                for (int t = 0; t < 64; ++t) {
+                for (int t = 0; t < CW; ++t) {
                     x[t] *= k2;
                     if (t < nv) mx = fmaxf(mx, x[t]);
                 }
@@ -270,14 +272,14 @@ row_kernel(MatchWs ws, int Nc, int Ncp, float k2) {
                     const float mn = fmaxf(run_m, mx);
                     float acc = 0.f;
 #pragma unroll
-                    for (int t = 0; t < 64; ++t)
+                    for (int t = 0; t < CW; ++t)
                         if (t < nv) acc += ex2_ftz(x[t] - mn);
                     run_l = run_l * ex2_ftz(run_m - mn) + acc;
                     run_m = mn;
                 }
             } else {
 #pragma unroll
-                for (int t = 0; t < 64; ++t) {
+                for (int t = 0; t < CW; ++t) {
                     if (t < nv) {
                         const float y = 2.f * (x[t] * k2) - cj[t];
                         if (y > best) { best = y; bj = j0 + t; }
@@ -285,23 +287,31 @@ row_kernel(MatchWs ws, int Nc, int Ncp, float k2) {
                 }
             }
         }
-        // combine the two column halves of each row
-        if (hh == 1) {
-            sm.part_v[row] = ARGMAX ? best : run_m;
-            sm.part_w[row] = ARGMAX ? __int_as_float(bj) : run_l;
+        // combine the column parts of each row
+        if (hh > 0) {
+            sm.part_v[hh - 1][row] = ARGMAX ? best : run_m;
+            sm.part_w[hh - 1][row] = ARGMAX ? __int_as_float(bj) : run_l;
         }
         asm volatile("bar.sync 1, %0;\n" ::"n"(EPI * 32) : "memory");
-        if (hh == 0 && rb * CB + row < Ncp) {
+        if (hh == 0) {
             if constexpr (!ARGMAX) {
-                const float m1 = sm.part_v[row], l1 = sm.part_w[row];
-                const float mt = fmaxf(run_m, m1);
-                const float lt = (run_l > 0.f ? run_l * ex2_ftz(run_m - mt) : 0.f) +
-                                 (l1 > 0.f ? l1 * ex2_ftz(m1 - mt) : 0.f);
+                float mt = run_m;
+#pragma unroll
+                for (int h = 0; h < NH - 1; ++h) mt = fmaxf(mt, sm.part_v[h][row]);
+                float lt = run_l > 0.f ? run_l * ex2_ftz(run_m - mt) : 0.f;
+#pragma unroll
+                for (int h = 0; h < NH - 1; ++h) {
+                    const float l1 = sm.part_w[h][row];
+                    if (l1 > 0.f) lt += l1 * ex2_ftz(sm.part_v[h][row] - mt);
+                }
                 ws.c2[d][gi] = mt + log2f(lt);
             } else {
-                const float b1 = sm.part_v[row];
-                const int j1 = __float_as_int(sm.part_w[row]);
-                if (b1 > best || (b1 == best && j1 >= 0 && (bj < 0 || j1 < bj))) { best = b1; bj = j1; }
+#pragma unroll
+                for (int h = 0; h < NH - 1; ++h) {
+                    const float b1 = sm.part_v[h][row];
+                    const int j1 = __float_as_int(sm.part_w[h][row]);
+                    if (b1 > best || (b1 == best && j1 >= 0 && (bj < 0 || j1 < bj))) { best = b1; bj = j1; }
+                }
                 ws.arg[d][gi] = (rb * CB + row < Nc) ? bj : -1;
                 if (d == 0) ws.pbest[gi] = bj >= 0 ? ex2_ftz(best - ws.c2[0][gi]) : 0.f;
             }
