@@ -115,7 +115,7 @@ struct RasterSmem {
     alignas(16) __half feath[TC ? NST : 1][TC ? SE + 1 : 1][TC ? FSH : 8];   // tcgen05 path: fp16 rows
     alignas(16) float wbuf[WB ? NCW : 1][WB_ROWS][WB_STRIDE]; // per-warp compacted weights [k][pixel]
     uint32_t slots[CONTRIB ? NST * (SE + 1) : 1];  // record slot of each ring row (contributions)
-    alignas(16) int ent[NCW][SE + 2];                // per-warp compacted ballot list (flat ring rows)
+    alignas(16) int ent[NCW][2 * SE + 2];            // per-warp compacted ballot list of a stage pair (flat rows)
     int kent[NCW][WB_ROWS];                          // ring row of each pending weight row
     StageMeta meta[NST];
     uint64_t full[NST];
@@ -477,11 +477,24 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
         }
     };
 
-    for (uint32_t s = 0;; ++s) {
+    // Consumers take the ring two stages at a time when both belong to the same tile
+    // (the producer keeps 32-entry stages): one wait / cull-compaction / walk / release
+    // cycle per 64 entries halves the per-stage bookkeeping.
+    for (uint32_t s = 0;;) {
         const int buf = (int)(s % NST);
         mbar_wait(&sm.full[buf], (s / NST) & 1u);
         const StageMeta m = sm.meta[buf];
         if (m.flags & ST_END) break;
+        const bool pair = !(m.flags & ST_LAST);   // a non-last stage is followed by one of its tile
+        const uint32_t s2 = pair ? s + 1 : s;
+        const int buf2 = (int)(s2 % NST);
+        int cnt2 = 0;
+        uint32_t last_flags = m.flags;
+        if (pair) {
+            mbar_wait(&sm.full[buf2], (s2 / NST) & 1u);
+            cnt2 = sm.meta[buf2].cnt;
+            last_flags = sm.meta[buf2].flags;
+        }
         if (m.flags & ST_FIRST) {
             V = &views[m.view];
             W = V->width;
@@ -507,20 +520,29 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     for (int n = 0; n < NTP; ++n) acc[a][n][0] = acc[a][n][1] = acc[a][n][2] = acc[a][n][3] = 0.f;
             }
         }
-        if (!warp_done && m.cnt > 0) {
-            const int flat0 = buf * (SE + 1);
+        if (!warp_done && (m.cnt > 0 || cnt2 > 0)) {
+            const int flat0 = buf * (SE + 1), flat2 = buf2 * (SE + 1);
             const int j = (int)lane;
-            bool hit = false;
+            bool hit = false, hit2 = false;
             if (j < m.cnt) {
                 const float4 a = sm.rec[buf][j][0];   // u, v, ea, eb
                 const float4 b = sm.rec[buf][j][1];   // ec, o, e_cut, -
                 hit = ellipse_hits_rect(a.x, a.y, a.z, a.w, b.x, b.z, rx0, rx1, ry0, ry1);
             }
+            if (j < cnt2) {
+                const float4 a = sm.rec[buf2][j][0];
+                const float4 b = sm.rec[buf2][j][1];
+                hit2 = ellipse_hits_rect(a.x, a.y, a.z, a.w, b.x, b.z, rx0, rx1, ry0, ry1);
+            }
             const uint32_t msk = __ballot_sync(0xffffffffu, hit);
-            const int n = __popc(msk);
+            const uint32_t msk2 = __ballot_sync(0xffffffffu, hit2);
+            const int n1 = __popc(msk);
+            const int n = n1 + __popc(msk2);
             if (n > 0) {
                 // compacted in-order entry list; an odd tail is padded with the null record
-                if (hit) sm.ent[warp][__popc(msk & ((1u << lane) - 1u))] = flat0 + j;
+                const uint32_t below = (1u << lane) - 1u;
+                if (hit) sm.ent[warp][__popc(msk & below)] = flat0 + j;
+                if (hit2) sm.ent[warp][n1 + __popc(msk2 & below)] = flat2 + j;
                 if (lane == 0 && (n & 1)) sm.ent[warp][n] = flat0 + SE;
                 __syncwarp();
 #pragma unroll 1
@@ -553,8 +575,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             }
         }
         // never pin more than half the ring: the producer must be able to refill
-        if (WB && pend > 0 && s - hold >= NST / 2) flush_pending();
-        if (m.flags & ST_LAST) {
+        if (WB && pend > 0 && s2 - hold >= NST / 2) flush_pending();
+        if (last_flags & ST_LAST) {
             flush_pending();
             // -------------------------------------------------------- outputs
             const int64_t HW = (int64_t)W * H;
@@ -614,10 +636,11 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             }
         }
         // release every stage no pending row references, in order
-        const uint32_t lim = (WB && pend > 0) ? hold : s + 1;
+        const uint32_t lim = (WB && pend > 0) ? hold : s2 + 1;
         __syncwarp();
         for (; rel < lim; ++rel)
             if (lane == 0) mbar_arrive(&sm.empty[rel % NST]);
+        s = s2 + 1;
     }
     if constexpr (TC) {
         // every MMA was waited for at its tile's epilogue; free TMEM once all consumers are done
