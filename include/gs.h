@@ -310,6 +310,43 @@ gs_status gs_match(const float* query_feat, const float* rend_feat, int32_t n_pa
                    int32_t W, float tau, float p_min, const float* rend_xyz, const uint8_t* rend_valid, void* ws,
                    size_t ws_bytes, gs_matches* out, void* stream);
 
+/*
+ * N2 pose stage -- Eq. 10 on the dense correspondences of
+ * gs_match: for problem b, correspondence = query pixel p = (px, py) with
+ * valid[b][p] != 0 and world point xyz[b][:, p] (gs_matches.valid / .xyz;
+ * the first `cap` in pixel order are used).  Reading Q35: RANSAC over n_hyp
+ * minimal 3-point samples (counter-based hash of (seed, hypothesis, draw)),
+ * each fitted exactly by 8 Gauss-Newton steps from the pose of views_in[b]
+ * (the pose the rendered view was made at), scored by inlier count
+ * (||p - pi(K[R|t]X)|| <= tau_px, z > 0); the best (or the start pose if none
+ * has more inliers) refined by 10 damped Gauss-Newton steps on
+ * rho(e) = min(e^2, tau^2).  fp64 arithmetic.
+ * views_out[b] = views_in[b] with R, t replaced (ready for the next
+ * gs_project of the refinement loop); stats[b] as below.  Device pointers,
+ * asynchronous.  ws >= gs_pnp_workspace_bytes(n_problems, cap), 16-B aligned.
+ */
+typedef struct gs_pnp_stats {
+    int32_t n_corr;          /* correspondences used (<= cap) */
+    int32_t n_inliers;       /* |I*| under the returned pose */
+    float mean_err;          /* mean reprojection error of the inliers, pixels */
+    int32_t best_hypothesis; /* winning RANSAC sample, -1 = the start pose */
+} gs_pnp_stats;
+
+size_t gs_pnp_workspace_bytes(int32_t n_problems, int32_t cap);
+gs_status gs_pnp(const uint8_t* valid, const float* xyz, int32_t n_problems, int32_t H, int32_t W,
+                 const gs_view* views_in_dev, float tau_px, int32_t n_hyp, uint32_t seed, int32_t cap, void* ws,
+                 size_t ws_bytes, gs_view* views_out_dev, gs_pnp_stats* stats_dev, void* stream);
+
+/*
+ * Algorithm 2 over a refinement trace trace_dev[i][b]
+ * (n_iters poses per problem): angle_deg[b][i] = arccos((clamp(tr(R_i R_{i+1}^T),
+ * -1, 3) - 1)/2) in degrees, dtrans[b][i] = |t_i - t_{i+1}| (computed, not
+ * gated -- as in the algorithm); verdict[b] = -1 reliable (return T_n), i = the
+ * first consecutive pair over tau_deg (unreliable), -2 when n_iters < 2.
+ */
+gs_status gs_verify_consistency(const gs_view* trace_dev, int32_t n_iters, int32_t n_problems, float tau_deg,
+                                float* angle_deg, float* dtrans, int32_t* verdict, void* stream);
+
 /* Workspace of gs_project: a (view x block) visibility bitmask. */
 size_t gs_project_workspace_bytes(int32_t n_blocks, int32_t n_views);
 

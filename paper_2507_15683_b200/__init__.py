@@ -8,9 +8,10 @@ fallback.
 """
 from .gs import (GSError, DeviceScene, ViewBatch, Projected, Bins, Images, default_params,  # noqa: F401
                  gs_project, gs_bin_sort, gs_rasterize, gs_backproject, gs_visibility_score, gs_validate_scene,
-                 gs_match, Matches, match_workspace_bytes, lib, LIB_PATH, EXPORTS)
-from .pipeline import Renderer, SignificanceScorer  # noqa: F401
+                 gs_match, Matches, match_workspace_bytes, gs_pnp, gs_verify_consistency, pnp_workspace_bytes,
+                 ViewsAt, GS_VIEW_BYTES, lib, LIB_PATH, EXPORTS)
+from .pipeline import Renderer, SignificanceScorer, Refiner  # noqa: F401
 
 __all__ = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_backproject", "gs_visibility_score", "gs_match",
-           "gs_validate_scene", "Matches", "DeviceScene",
+           "gs_validate_scene", "gs_pnp", "gs_verify_consistency", "Matches", "Refiner", "DeviceScene",
            "ViewBatch", "Projected", "Bins", "Images", "Renderer", "SignificanceScorer", "default_params", "GSError"]

@@ -31,6 +31,7 @@ SOURCES = {
     "gs_backproject.cu": [],
     "gs_visibility.cu": [],
     "gs_match.cu": [],
+    "gs_pose.cu": [],
 }
 HEADERS = [os.path.join(INCLUDE, "gs.h"), os.path.join(CSRC, "gs_common.cuh"), os.path.join(CSRC, "gs_tc.cuh")]
 

@@ -70,6 +70,7 @@ class gs_images(ctypes.Structure):
 
 EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_layout", "gs_scene_block_bounds",
            "gs_scene_features_f16", "gs_validate_scene", "gs_match", "gs_match_workspace_bytes",
+           "gs_pnp", "gs_pnp_workspace_bytes", "gs_verify_consistency",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_backproject", "gs_visibility_score", "gs_visibility_workspace_bytes"]
 
@@ -90,6 +91,8 @@ def lib():
         L.gs_project_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32]
         L.gs_bin_sort_workspace_bytes.restype = ctypes.c_size_t
         L.gs_bin_sort_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]
+        L.gs_pnp_workspace_bytes.restype = ctypes.c_size_t
+        L.gs_pnp_workspace_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32]
         L.gs_match_workspace_bytes.restype = ctypes.c_size_t
         L.gs_match_workspace_bytes.argtypes = [ctypes.c_int32] * 4
         L.gs_visibility_workspace_bytes.restype = ctypes.c_size_t
@@ -391,3 +394,58 @@ def gs_match(query_feat: torch.Tensor, rend_feat: torch.Tensor, n_pairs: int, D:
                           ctypes.c_int32(H), ctypes.c_int32(W), ctypes.c_float(tau), ctypes.c_float(p_min),
                           _ptr(rend_xyz), _ptr(rend_valid), _ptr(ws), ctypes.c_size_t(ws.numel()),
                           ctypes.byref(out.struct), _stream(stream)), "gs_match")
+
+
+# ---------------------------------------------------------------------- N2 pose stage
+GS_VIEW_BYTES = ctypes.sizeof(gs_view)
+
+
+class gs_pnp_stats(ctypes.Structure):
+    _fields_ = [("n_corr", ctypes.c_int32), ("n_inliers", ctypes.c_int32), ("mean_err", ctypes.c_float),
+                ("best_hypothesis", ctypes.c_int32)]
+
+
+class ViewsAt:
+    """A view batch whose device descriptors live at `dev` (e.g. one slot of a
+    refinement trace); the host copy (sizes, offsets) is the template batch's."""
+
+    def __init__(self, template: "ViewBatch", dev: torch.Tensor):
+        assert dev.numel() == template.n * GS_VIEW_BYTES
+        self.host, self.n, self.dev, self.views = template.host, template.n, dev, template.views
+        self.total_pixels, self.total_tiles = template.total_pixels, template.total_tiles
+
+    @property
+    def dev_ptr(self):
+        return ctypes.c_void_p(self.dev.data_ptr())
+
+
+def pnp_workspace_bytes(n_problems: int, cap: int) -> int:
+    return int(lib().gs_pnp_workspace_bytes(n_problems, cap))
+
+
+def gs_pnp(valid: torch.Tensor, xyz: torch.Tensor, n_problems: int, H: int, W: int, views_in: torch.Tensor,
+           views_out: torch.Tensor, stats: torch.Tensor, ws: torch.Tensor, cap: int, tau_px: float = 3.0,
+           n_hyp: int = 128, seed: int = 0, stream=None):
+    """views_in / views_out: device gs_view arrays (uint8 tensors of n * 88 bytes);
+    stats: int32 tensor of 4 * n (gs_pnp_stats)."""
+    _check(lib().gs_pnp(_ptr(valid), _ptr(xyz), ctypes.c_int32(n_problems), ctypes.c_int32(H), ctypes.c_int32(W),
+                        _ptr(views_in), ctypes.c_float(tau_px), ctypes.c_int32(n_hyp), ctypes.c_uint32(seed),
+                        ctypes.c_int32(cap), _ptr(ws), ctypes.c_size_t(ws.numel()), _ptr(views_out), _ptr(stats),
+                        _stream(stream)), "gs_pnp")
+
+
+def gs_verify_consistency(trace: torch.Tensor, n_iters: int, n_problems: int, angle: torch.Tensor,
+                          dtrans: torch.Tensor, verdict: torch.Tensor, tau_deg: float = 20.0, stream=None):
+    _check(lib().gs_verify_consistency(_ptr(trace), ctypes.c_int32(n_iters), ctypes.c_int32(n_problems),
+                                       ctypes.c_float(tau_deg), _ptr(angle), _ptr(dtrans), _ptr(verdict),
+                                       _stream(stream)), "gs_verify_consistency")
+
+
+def views_pose_array(dev_views: torch.Tensor, n: int):
+    """Host decode of a device gs_view array -> (R [n][3][3], t [n][3]) numpy."""
+    import numpy as _np
+    raw = dev_views.cpu().numpy().view(_np.uint8)
+    arr = (gs_view * n).from_buffer_copy(raw.tobytes())
+    R = _np.array([[arr[i].R[k] for k in range(9)] for i in range(n)], _np.float64).reshape(n, 3, 3)
+    t = _np.array([[arr[i].t[k] for k in range(3)] for i in range(n)], _np.float64)
+    return R, t

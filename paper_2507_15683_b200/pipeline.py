@@ -67,14 +67,18 @@ class Renderer:
                                       dtype=torch.uint8, device=self.device)
 
     # ------------------------------------------------------------- hot path
-    def run(self, stream=None):
-        """Enqueue the whole hot path for the batch (asynchronous)."""
-        self.proj.status.zero_()
-        G.gs_project(self.scene, self.vb, self.params, self.proj, self.ws_proj, stream, scene_struct=self.scene_struct)
-        G.gs_bin_sort(self.proj, self.vb, self.bins, self.ws_bin, stream)
-        G.gs_rasterize(self.scene, self.proj, self.bins, self.vb, self.params, self.images, stream)
+    def run(self, stream=None, views=None, zero_status: bool = True):
+        """Enqueue the whole hot path for the batch (asynchronous).  `views` may
+        replace the batch's device descriptors (same sizes), e.g. poses written
+        on the device by gs_pnp."""
+        vb = self.vb if views is None else views
+        if zero_status:
+            self.proj.status.zero_()
+        G.gs_project(self.scene, vb, self.params, self.proj, self.ws_proj, stream, scene_struct=self.scene_struct)
+        G.gs_bin_sort(self.proj, vb, self.bins, self.ws_bin, stream)
+        G.gs_rasterize(self.scene, self.proj, self.bins, vb, self.params, self.images, stream)
         if self.do_backproject:
-            G.gs_backproject(self.images, self.vb, self.a_min, self.xyz, self.valid, stream)
+            G.gs_backproject(self.images, vb, self.a_min, self.xyz, self.valid, stream)
 
     def status(self) -> int:
         return int(self.proj.status.item())
@@ -164,3 +168,88 @@ class SignificanceScorer:
         out = torch.full_like(s, float("-inf"))
         out[m] = s[m] / self.count[m].double()
         return out
+
+
+class Refiner:
+    """N2 dense refinement: n rounds of render -> gs_match ->
+    gs_pnp at the current poses of a batch of queries, then Algorithm 2
+    (gs_verify_consistency).  Every round stays on the device: gs_pnp writes
+    the refined pose into the gs_view slot the next round's gs_project reads,
+    so the loop is one stream of launches with no host synchronisation and can
+    be captured as a CUDA graph (``capture()``).
+
+    query_feat: [B][D][H][W] f32 query feature maps (the query images'
+    features at the rendering resolution); init_views: the B initial poses
+    (equal sizes, H and W multiples of 8)."""
+
+    def __init__(self, scene: G.DeviceScene, init_views: Sequence, query_feat: torch.Tensor, n_iters: int = 3,
+                 tau_px: float = 3.0, n_hyp: int = 128, seed: int = 0, cap: int = 16384, match_tau: float = 0.1,
+                 p_min: float = 0.05, a_min: float = 0.5, slack: float = 1.6, consistency_deg: float = 20.0):
+        self.B = len(init_views)
+        v0 = init_views[0]
+        self.H, self.W, self.D = v0.height, v0.width, scene.feat_dim
+        assert all(v.width == self.W and v.height == self.H for v in init_views)
+        self.n_iters, self.tau_px, self.n_hyp, self.seed, self.cap = n_iters, tau_px, n_hyp, seed, cap
+        self.match_tau, self.p_min, self.consistency_deg = match_tau, p_min, consistency_deg
+        self.query = query_feat
+        dev = query_feat.device
+        self.r = Renderer(scene, init_views, a_min=a_min, backproject=True, device=dev)
+        self.r.render()
+        # capacities with slack: later rounds render at other poses
+        self.r._alloc(int(self.r.proj.n_rec.max().item() * slack) + 256, int(self.r.bins.n_pairs.item() * slack) + 4096)
+        nb = self.B * G.GS_VIEW_BYTES
+        self.trace = torch.empty((n_iters + 1) * nb, dtype=torch.uint8, device=dev)
+        self.trace[:nb].copy_(self.r.vb.dev)
+        self.matches = G.Matches(self.B, self.H, self.W, with_points=True, device=dev)
+        self.mws = torch.empty(G.match_workspace_bytes(self.B, self.D, self.H, self.W), dtype=torch.uint8, device=dev)
+        self.pws = torch.empty(G.pnp_workspace_bytes(self.B, cap), dtype=torch.uint8, device=dev)
+        self.stats = torch.zeros((n_iters, self.B, 4), dtype=torch.int32, device=dev)
+        self.angle = torch.zeros(self.B * max(1, n_iters - 1), dtype=torch.float32, device=dev)
+        self.dtrans = torch.zeros_like(self.angle)
+        self.verdict = torch.zeros(self.B, dtype=torch.int32, device=dev)
+        self.graph = None
+
+    def slot(self, i: int) -> torch.Tensor:
+        nb = self.B * G.GS_VIEW_BYTES
+        return self.trace[i * nb:(i + 1) * nb]
+
+    def run(self, stream=None):
+        """Enqueue the n rounds + Algorithm 2 (asynchronous)."""
+        self.r.proj.status.zero_()
+        for i in range(self.n_iters):
+            self.r.run(stream, views=G.ViewsAt(self.r.vb, self.slot(i)), zero_status=False)
+            G.gs_match(self.query, self.r.images.feat, self.B, self.D, self.H, self.W, self.matches, self.mws,
+                       tau=self.match_tau, p_min=self.p_min, rend_xyz=self.r.xyz, rend_valid=self.r.valid,
+                       stream=stream)
+            G.gs_pnp(self.matches.valid, self.matches.xyz, self.B, self.H, self.W, self.slot(i), self.slot(i + 1),
+                     self.stats[i], self.pws, self.cap, tau_px=self.tau_px, n_hyp=self.n_hyp, seed=self.seed,
+                     stream=stream)
+        nb = self.B * G.GS_VIEW_BYTES
+        G.gs_verify_consistency(self.trace[nb:], self.n_iters, self.B, self.angle, self.dtrans, self.verdict,
+                                tau_deg=self.consistency_deg, stream=stream)
+
+    def capture(self):
+        """Record run() into a CUDA graph (after one eager run initialised every kernel)."""
+        self.run()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self.run(torch.cuda.current_stream())
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+        return g
+
+    def replay(self):
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    def status(self) -> int:
+        return int(self.r.proj.status.item())
+
+    def poses(self, i: int):
+        """(R [B][3][3], t [B][3]) of trace slot i (0 = initial)."""
+        return G.views_pose_array(self.slot(i), self.B)
