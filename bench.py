@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--n2", action="store_true",
                     help="also time N2 gs_match on (view i, view i+1) feature-map pairs of the rendered batch")
     ap.add_argument("--n2-pairs", type=int, default=64)
+    ap.add_argument("--refine", type=int, default=0, metavar="B",
+                    help="also time N2's n = 3 refinement loop (render -> gs_match -> gs_pnp, CUDA graph) for B "
+                         "queries: query features rendered at B of the batch's poses, starts 1 deg / ~1.4 m off")
     ap.add_argument("--n1", action="store_true",
                     help="also time N1 (per-Gaussian contributions + Alg. 1 visibility + Eq. 4-6 scoring "
                          "against stride-8 synthetic target maps) inside the step")
@@ -393,6 +396,65 @@ def main():
               "coarse_gemm_tflops": 2.0 * 3 * 2 * 2 * nc * nc * D2 * Bp / (ms2 / 1e3) / 1e12,
               "gpu_launches": 5, "tau": 0.1, "p_min": 0.05}
 
+    # N2 refinement loop: B queries, n = 3 rounds, one CUDA graph
+    refine = None
+    if args.refine:
+        import math as _m
+        import synth
+        Bq = max(1, min(args.refine, n_views))
+        qv = views[:Bq]
+        rq = G.Renderer(ds, qv, device=dev)
+        rq.render()
+        query = rq.images.feat.clone() if scene.feat_dim else None
+        del rq
+        if query is None:
+            raise SystemExit("--refine needs a feature scene (C3 / C4)")
+        rng = np.random.default_rng(7 + rank)
+        init = []
+        for v in qv:
+            R = np.asarray(v.R, np.float64).reshape(3, 3)
+            C = -R.T @ np.asarray(v.t, np.float64)
+            ax = rng.standard_normal(3)
+            ax /= np.linalg.norm(ax)
+            th = _m.radians(1.0)
+            Kx = np.array([[0, -ax[2], ax[1]], [ax[2], 0, -ax[0]], [-ax[1], ax[0], 0]])
+            dR = np.eye(3) + _m.sin(th) * Kx + (1 - _m.cos(th)) * Kx @ Kx
+            R0 = dR @ R
+            C0 = C + np.array([1.0, -1.0, 0.3])
+            init.append(synth.make_view(R0.astype(np.float32), (-R0 @ C0).astype(np.float32), v.fx, v.fy, v.cx, v.cy,
+                                        v.width, v.height))
+        ref = G.Refiner(ds, init, query, n_iters=3)
+        ref.capture()
+        for _ in range(2):
+            ref.replay()
+        torch.cuda.synchronize()
+        r0e, r1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        Kr = max(2, min(K, 5))
+        r0e.record()
+        for _ in range(Kr):
+            ref.replay()
+        r1e.record()
+        torch.cuda.synchronize()
+        ms_r = r0e.elapsed_time(r1e) / Kr
+        R0s, t0s = ref.poses(0)
+        R3s, t3s = ref.poses(3)
+        errs0, errs3 = [], []
+        for b, v in enumerate(qv):
+            Rg = np.asarray(v.R, np.float64).reshape(3, 3)
+            Cg = -Rg.T @ np.asarray(v.t, np.float64)
+            for (Rs, ts, out) in ((R0s, t0s, errs0), (R3s, t3s, errs3)):
+                c = np.linalg.norm(Rs[b] - Rg) / (2 * _m.sqrt(2))
+                out.append((_m.degrees(2 * _m.asin(min(1.0, c))), float(np.linalg.norm(-Rs[b].T @ ts[b] - Cg))))
+        e0, e3 = np.median(np.array(errs0), 0), np.median(np.array(errs3), 0)
+        refine = {"queries": Bq, "rounds": 3, "ms": ms_r, "ms_per_query": ms_r / Bq, "cuda_graph": True,
+                  "median_rot_err_deg": {"initial": float(e0[0]), "refined": float(e3[0])},
+                  "median_pos_err_m": {"initial": float(e0[1]), "refined": float(e3[1])},
+                  "reliable_fraction": float((ref.verdict == -1).float().mean().item()),
+                  "median_inliers_last_round": float(ref.stats[-1, :, 1].float().median().item()),
+                  "resolution": f"{qv[0].width}x{qv[0].height}",
+                  "launches_per_round": 12 + 5 + 1, "capacity_overflow": ref.status() != 0}
+        del ref
+
     # roofline of the dominant kernel
     peak, peak_src = measured_peaks()
     dom = int(np.argmax(stage_ms[:4]))
@@ -423,6 +485,8 @@ def main():
            "roofline": roof, "gpu_launches": launches_per_step * K, "e2e": e2e, "clocks": clk.summary()}
     if n2 is not None:
         out["n2"] = n2
+    if refine is not None:
+        out["refine"] = refine
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(scene, views, args.cpu_sample_views)
     if rank == 0:

@@ -314,7 +314,7 @@ gs_status gs_match(const float* query_feat, const float* rend_feat, int32_t n_pa
  * N2 pose stage -- Eq. 10 on the dense correspondences of
  * gs_match: for problem b, correspondence = query pixel p = (px, py) with
  * valid[b][p] != 0 and world point xyz[b][:, p] (gs_matches.valid / .xyz;
- * the first `cap` in pixel order are used).  Reading Q35: RANSAC over n_hyp
+ * in pixel order; with n > cap of them every k-th, k = ceil(n / cap), is used).  Reading Q35: RANSAC over n_hyp
  * minimal 3-point samples (counter-based hash of (seed, hypothesis, draw)),
  * each fitted exactly by 8 Gauss-Newton steps from the pose of views_in[b]
  * (the pose the rendered view was made at), scored by inlier count

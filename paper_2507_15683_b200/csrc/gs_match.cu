@@ -25,7 +25,9 @@
 //      P_ij > p_min (ties to the lowest index, Q33).
 //   5. fine_kernel: one CTA per coarse match -- Eq. 11 + MNN between the
 //      64 pixels of the query cell and the 64 of the matched rendered cell
-//      (Q34) in fp32 on the CUDA cores (64 x 64 x D per window), 3 x 3
+//      (Q34); the 64 x 64 x D cosine block on the tensor cores (mma.sync
+//      m16n8k16, fp16 hi + lo operands, 3 products -- a window is too small to
+//      amortise a TMEM allocation), the softmaxes / MNN in fp32, 3 x 3
 //      soft-argmax around the peak, gather of the peak's back-projected point.
 #include <cuda_fp16.h>
 
@@ -339,6 +341,14 @@ __global__ void mnn_kernel(MatchWs ws, int Nc, int Ncp, float p_min, int32_t* __
 }
 
 // ---------------------------------------------------------------- 5. fine windows
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
 constexpr int WP = MW * MW;   // 64 pixels per window
 
 __global__ void __launch_bounds__(256) fine_kernel(const float* __restrict__ Fq, const float* __restrict__ Fr, int D,
@@ -352,6 +362,10 @@ __global__ void __launch_bounds__(256) fine_kernel(const float* __restrict__ Fq,
     float* rc = X + WP * 65;              // [64] row log2-sum-exp2
     float* cc = rc + WP;                  // [64] column log2-sum-exp2
     int* carg = reinterpret_cast<int*>(cc + WP);   // [64] column argmax
+    __half* qh = reinterpret_cast<__half*>(carg + WP);   // [64][D + 8] fp16 hi / lo operands
+    __half* ql = qh + WP * (D + 8);
+    __half* rh = ql + WP * (D + 8);
+    __half* rl = rh + WP * (D + 8);
     const int ic = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
     const int Wc = W / MW;
     const int64_t HW = (int64_t)H * W;
@@ -387,13 +401,46 @@ __global__ void __launch_bounds__(256) fine_kernel(const float* __restrict__ Fq,
         for (int ch = 0; ch < D; ++ch) v[ch] *= inv;
     }
     __syncthreads();
-    for (int e = tid; e < WP * WP; e += blockDim.x) {
-        const int a = e / WP, bb = e % WP;
-        const float* qa = qf + a * (D + 1);
-        const float* rb = rf + bb * (D + 1);
-        float dot = 0.f;
-        for (int ch = 0; ch < D; ++ch) dot = fmaf(qa[ch], rb[ch], dot);
-        X[a * 65 + bb] = dot * k2;
+    // the 64 x 64 x D cosine block on the tensor cores: fp16 hi + lo operands,
+    // hi.hi + hi.lo + lo.hi (~2^-22 relative), fp32 accumulation
+    const int HS = D + 8;                               // half row stride (conflict-free fragments)
+    for (int e = tid; e < 2 * WP * D; e += blockDim.x) {
+        const int m = e / (WP * D), rem = e % (WP * D), a = rem / D, ch = rem % D;
+        const float x = (m == 0 ? qf : rf)[a * (D + 1) + ch];
+        const __half hi = __float2half_rn(x);
+        (m == 0 ? qh : rh)[a * HS + ch] = hi;
+        (m == 0 ? ql : rl)[a * HS + ch] = __float2half_rn(x - __half2float(hi));
+    }
+    __syncthreads();
+    {
+        const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+        const int rb = warp & 3, chf = warp >> 2;        // rows 16 rb.., columns 32 chf..
+        float acc[4][4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+        auto u32 = [](const __half* p) { return *reinterpret_cast<const uint32_t*>(p); };
+        for (int ks = 0; ks < D / 16; ++ks) {
+            const int r0 = (16 * rb + g) * HS + 16 * ks + 2 * t4, r1 = r0 + 8 * HS;
+            const uint32_t ah[4] = {u32(qh + r0), u32(qh + r1), u32(qh + r0 + 8), u32(qh + r1 + 8)};
+            const uint32_t al[4] = {u32(ql + r0), u32(ql + r1), u32(ql + r0 + 8), u32(ql + r1 + 8)};
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                const int c0 = (32 * chf + 8 * nt + g) * HS + 16 * ks + 2 * t4;
+                const uint32_t bh0 = u32(rh + c0), bh1 = u32(rh + c0 + 8);
+                const uint32_t bl0 = u32(rl + c0), bl1 = u32(rl + c0 + 8);
+                mma16816(acc[nt], ah, bh0, bh1);
+                mma16816(acc[nt], ah, bl0, bl1);
+                mma16816(acc[nt], al, bh0, bh1);
+            }
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+            const int col = 32 * chf + 8 * nt + 2 * t4, row = 16 * rb + g;
+            X[row * 65 + col] = acc[nt][0] * k2;
+            X[row * 65 + col + 1] = acc[nt][1] * k2;
+            X[(row + 8) * 65 + col] = acc[nt][2] * k2;
+            X[(row + 8) * 65 + col + 1] = acc[nt][3] * k2;
+        }
     }
     __syncthreads();
     if (tid < 2 * WP) {   // row (tid < 64) / column log2-sum-exp2
@@ -526,10 +573,10 @@ extern "C" gs_status gs_match(const float* query_feat, const float* rend_feat, i
     if (st != GS_OK) return st;
     mnn_kernel<<<dim3((Nc + 255) / 256, n_pairs), 256, 0, s>>>(w, Nc, Ncp, p_min, out->coarse, out->coarse_prob);
     if ((st = check_launch("mnn_kernel")) != GS_OK) return st;
-    const int fsmem = (int)sizeof(float) * (2 * WP * (D + 1) + WP * 65 + 3 * WP);
+    const int fsmem = (int)sizeof(float) * (2 * WP * (D + 1) + WP * 65 + 3 * WP) + 4 * WP * (D + 8) * 2;
     static bool fine_init = false;
     if (!fine_init) {
-        cudaFuncSetAttribute(fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
         fine_init = true;
     }
     fine_kernel<<<dim3(Nc, n_pairs), 256, fsmem, s>>>(query_feat, rend_feat, D, H, W, Nc, out->coarse, k2, p_min,

@@ -4,7 +4,8 @@
 // reading Q35).
 //
 // gs_pnp: one CTA per problem (query).  1. ordered compaction of the query
-// pixels whose match carries a valid 3D point (block scans, first `cap` kept);
+// pixels whose match carries a valid 3D point (block scans; with n > cap valid
+// pixels, every k-th in pixel order, k = ceil(n / cap));
 // 2. RANSAC: n_hyp hypotheses, each the exact fit of a 3-correspondence sample
 // (counter-based hash, identical to the oracle's) by Gauss-Newton from the
 // render pose, fp64, one thread each; 3. each hypothesis scored by its inlier
@@ -146,10 +147,11 @@ pnp_kernel(const uint8_t* __restrict__ valid, const float* __restrict__ xyz, int
     __shared__ int s_n;
     __shared__ int wsum[PNP_THREADS / 32];
     __shared__ Pose s_pose;
-    __shared__ Pose s_hyp[MAX_HYP];
-    __shared__ int s_cnt[MAX_HYP];
+    __shared__ Pose s_hyp[MAX_HYP + 1];
+    __shared__ int s_cnt[MAX_HYP + 1];
     __shared__ double red[PNP_THREADS / 32][28];
     __shared__ int s_stop;
+    __shared__ int s_stride;
     const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t HW = (int64_t)H * W;
     const gs_view V = views_in[b];
@@ -166,12 +168,41 @@ pnp_kernel(const uint8_t* __restrict__ valid, const float* __restrict__ xyz, int
     __syncthreads();
     const uint8_t* vb = valid + (int64_t)b * HW;
     const float* X = xyz + (int64_t)b * 3 * HW;
-    for (int64_t p0 = 0; p0 < HW; p0 += 4 * PNP_THREADS) {
-        const int64_t p = p0 + 4 * tid;
-        uint32_t f[4];
+    // pass 1: number of valid correspondences; keep every k-th (k = ceil(n / cap)) so a
+    // capped list still spans the whole image
+    {
+        int cnt = 0;
+        for (int64_t p = 4 * tid; p < HW; p += 4 * PNP_THREADS)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) f[k] = (p + k < HW && vb[p + k]) ? 1u : 0u;
-        const uint32_t c = f[0] + f[1] + f[2] + f[3];
+            for (int k = 0; k < 4; ++k) cnt += (p + k < HW && vb[p + k]) ? 1 : 0;
+        cnt = (int)warp_sum((double)cnt);
+        if (lane == 0) wsum[warp] = cnt;
+        __syncthreads();
+        if (tid == 0) {
+            int tot = 0;
+            for (int w = 0; w < PNP_THREADS / 32; ++w) tot += wsum[w];
+            s_stride = (tot + cap - 1) / cap;
+            if (s_stride < 1) s_stride = 1;
+        }
+        __syncthreads();
+    }
+    const int stride = s_stride;
+    const bool vec = ((uintptr_t)vb & 15) == 0;
+    for (int64_t p0 = 0; p0 < HW; p0 += 16 * PNP_THREADS) {
+        const int64_t p = p0 + 16 * tid;
+        uint32_t f[16];
+        if (vec && p + 16 <= HW) {
+            const uint4 q = *reinterpret_cast<const uint4*>(vb + p);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int k = 0; k < 16; ++k) f[k] = ((w[k >> 2] >> (8 * (k & 3))) & 0xffu) ? 1u : 0u;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) f[k] = (p + k < HW && vb[p + k]) ? 1u : 0u;
+        }
+        uint32_t c = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) c += f[k];
         uint32_t inc = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -185,12 +216,12 @@ pnp_kernel(const uint8_t* __restrict__ valid, const float* __restrict__ xyz, int
         for (int w = 0; w < warp; ++w) off += wsum[w];
         int pos = base + off + (int)(inc - c);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < 16; ++k) {
             if (f[k]) {
-                if (pos < cap) {
+                if (pos % stride == 0 && pos / stride < cap) {
                     const int64_t q = p + k;
-                    LX[pos] = make_float4(X[q], X[HW + q], X[2 * HW + q], 0.f);
-                    LU[pos] = make_float2((float)(q % W), (float)(q / W));
+                    LX[pos / stride] = make_float4(X[q], X[HW + q], X[2 * HW + q], 0.f);
+                    LU[pos / stride] = make_float2((float)(q % W), (float)(q / W));
                 }
                 ++pos;
             }
@@ -203,7 +234,7 @@ pnp_kernel(const uint8_t* __restrict__ valid, const float* __restrict__ xyz, int
         }
         __syncthreads();
     }
-    const int n = min(s_n, cap);
+    const int n = min((s_n + stride - 1) / stride, cap);
     // ---------------------------------------------------------- 2./3. hypotheses
     if (tid < n_hyp) {
         Pose P = s_pose;
@@ -241,29 +272,38 @@ pnp_kernel(const uint8_t* __restrict__ valid, const float* __restrict__ xyz, int
             if (!chol_solve(A, nb, xi)) { ok = false; break; }
             apply(P, xi);
         }
-        int cnt = -1;
-        if (ok) {
-            cnt = 0;
-            for (int i = 0; i < n; ++i) {
-                Obs o;
-                const float4 x = LX[i];
-                const float2 uv = LU[i];
-                observe(P, K, uv.x, uv.y, x.x, x.y, x.z, o, false);
-                cnt += is_inlier(o, tau);
-            }
-        }
         s_hyp[tid] = P;
-        s_cnt[tid] = cnt;
+        s_cnt[tid] = ok ? 0 : -1;
+    }
+    if (tid == 0) s_hyp[n_hyp] = s_pose;   // the start pose is scored alongside
+    __syncthreads();
+    // 3. inlier counts, one warp per hypothesis at a time, lanes over the points; fp32
+    //    without division: e^2 <= tau^2 <=> (fx x + (cx - u) z)^2 + (fy y + (cy - v) z)^2 <= tau^2 z^2
+    for (int h = warp; h <= n_hyp; h += PNP_THREADS / 32) {
+        if (h < n_hyp && s_cnt[h] < 0) continue;
+        const Pose& Q = s_hyp[h];
+        float R[9], t[3];
+        for (int k = 0; k < 9; ++k) R[k] = (float)Q.R[k];
+        for (int k = 0; k < 3; ++k) t[k] = (float)Q.t[k];
+        const float tau2 = tau_f * tau_f;
+        int c = 0;
+        for (int i = lane; i < n; i += 32) {
+            const float4 x = LX[i];
+            const float2 uv = LU[i];
+            const float px = fmaf(R[0], x.x, fmaf(R[1], x.y, fmaf(R[2], x.z, t[0])));
+            const float py = fmaf(R[3], x.x, fmaf(R[4], x.y, fmaf(R[5], x.z, t[1])));
+            const float pz = fmaf(R[6], x.x, fmaf(R[7], x.y, fmaf(R[8], x.z, t[2])));
+            const float ex = fmaf(K.x, px, (K.z - uv.x) * pz), ey = fmaf(K.y, py, (K.w - uv.y) * pz);
+            c += (pz > 0.f && ex * ex + ey * ey <= tau2 * pz * pz) ? 1 : 0;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) s_cnt[h] = c;
     }
     __syncthreads();
     if (tid == 0) {
         // the start pose unless a hypothesis has strictly more inliers (lowest index on ties)
-        int best_cnt = 0;
-        for (int i = 0; i < n; ++i) {
-            Obs o;
-            observe(s_pose, K, LU[i].x, LU[i].y, LX[i].x, LX[i].y, LX[i].z, o, false);
-            best_cnt += is_inlier(o, tau);
-        }
+        int best_cnt = s_cnt[n_hyp];
         int best = -1;
         for (int h = 0; h < n_hyp; ++h)
             if (s_cnt[h] > best_cnt) { best_cnt = s_cnt[h]; best = h; }
