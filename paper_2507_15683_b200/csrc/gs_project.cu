@@ -201,10 +201,23 @@ __device__ __forceinline__ void sh_color(int deg, const float* __restrict__ sh, 
 
 constexpr int PROJ_THREADS = 256;
 
-__global__ void __launch_bounds__(PROJ_THREADS)
+// a queued Gaussian's view-independent state (per-warp table, one row per lane)
+struct GTab {
+    float mx, my, mz, op;
+    float sg[6];
+    float smax, ecut;
+    uint32_t gid, pad;
+};
+
+#ifndef GS_PROJ_MIN_BLOCKS
+#define GS_PROJ_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(PROJ_THREADS, GS_PROJ_MIN_BLOCKS)
 project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* __restrict__ vcs, int n_views,
                gs_params P, const uint32_t* __restrict__ mask, gs_record* __restrict__ rec, int64_t cap,
                uint32_t* __restrict__ n_rec, uint64_t* __restrict__ diag, uint32_t* __restrict__ status) {
+    __shared__ GTab s_tab[PROJ_THREADS / 32][32];
+    __shared__ uint32_t s_queue[PROJ_THREADS / 32][64];
     const int64_t n = S.n;
     const int64_t i = (int64_t)blockIdx.x * PROJ_THREADS + threadIdx.x;
     const bool in = i < n;
@@ -275,6 +288,117 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
         e_cut = -(lub * 1.05f + 0.0075f);
     }
 
+    // Per-warp candidate queue: the cheap per-view tests run in the warp-uniform view
+    // loop; surviving (Gaussian, view) pairs are queued and the heavy EWA + SH path runs
+    // 32 of them at a time with every lane busy (a view typically keeps a few percent
+    // of a warp's Gaussians, so running it in place idles most lanes).
+    const int wid = threadIdx.x >> 5;
+    GTab& me = s_tab[wid][lane];
+    me.mx = mx; me.my = my; me.mz = mz; me.op = op;
+    for (int k = 0; k < 6; ++k) me.sg[k] = Sg[k];
+    me.smax = smax; me.ecut = e_cut; me.gid = (uint32_t)i;
+    uint32_t* queue = s_queue[wid];
+    uint32_t qn = 0;   // warp-uniform
+    __syncwarp();
+
+    // heavy path for queue items [0, cnt): lane k takes item k
+    auto process = [&](uint32_t cnt) {
+        const bool act = lane < cnt;
+        const uint32_t item = act ? queue[lane] : 0u;
+        const int vi = (int)(item >> 5);
+        const GTab& g = s_tab[wid][item & 31u];
+        bool visible = false;
+        gs_record r;
+        if (act) {
+            const gs_view& V = views[vi];
+            const ViewConst& c = vcs[vi];
+            // O1 (pinned), recomputed
+            const float px = ((V.R[0] * g.mx + V.R[1] * g.my) + V.R[2] * g.mz) + V.t[0];
+            const float py = ((V.R[3] * g.mx + V.R[4] * g.my) + V.R[5] * g.mz) + V.t[1];
+            const float pz = ((V.R[6] * g.mx + V.R[7] * g.my) + V.R[8] * g.mz) + V.t[2];
+            // O3 (pinned): divide by depth first, then apply K (Alg. 1 l.12-14)
+            const float xn = px / pz, yn = py / pz;
+            const float u = V.fx * xn + V.cx;
+            const float v = V.fy * yn + V.cy;
+            // O5 (pinned): EWA with the clamped Jacobian
+            const float xc = fminf(fmaxf(xn, c.lox), c.hix) * pz;
+            const float yc = fminf(fmaxf(yn, c.loy), c.hiy) * pz;
+            const float z2 = pz * pz;
+            const float j00 = V.fx / pz, j02 = -((V.fx * xc) / z2);
+            const float j11 = V.fy / pz, j12 = -((V.fy * yc) / z2);
+            float T0[3], T1[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                T0[k] = j00 * V.R[0 * 3 + k] + j02 * V.R[2 * 3 + k];
+                T1[k] = j11 * V.R[1 * 3 + k] + j12 * V.R[2 * 3 + k];
+            }
+            const float S00 = g.sg[0], S01 = g.sg[1], S02 = g.sg[2], S11 = g.sg[3], S12 = g.sg[4], S22 = g.sg[5];
+            const float V00 = (T0[0] * S00 + T0[1] * S01) + T0[2] * S02;
+            const float V01 = (T0[0] * S01 + T0[1] * S11) + T0[2] * S12;
+            const float V02 = (T0[0] * S02 + T0[1] * S12) + T0[2] * S22;
+            const float V10 = (T1[0] * S00 + T1[1] * S01) + T1[2] * S02;
+            const float V11 = (T1[0] * S01 + T1[1] * S11) + T1[2] * S12;
+            const float V12 = (T1[0] * S02 + T1[1] * S12) + T1[2] * S22;
+            const float s00 = (V00 * T0[0] + V01 * T0[1]) + V02 * T0[2];
+            const float s01 = (V00 * T1[0] + V01 * T1[1]) + V02 * T1[2];
+            const float s11 = (V10 * T1[0] + V11 * T1[1]) + V12 * T1[2];
+            const float a = s00 + P.dilation, b = s01, cc = s11 + P.dilation;
+            // O6 (pinned)
+            const float det = a * cc - b * b;
+            if (!(det > 0.0f)) { ++c_degen; goto done; }
+            {
+                const float ca = cc / det, cb = -(b / det), ccn = a / det;
+                // O7 (pinned)
+                const float mid = 0.5f * (a + cc);
+                const float lam = mid + sqrtf(fmaxf(mid * mid - det, 0.0f));
+                const float rad = ceilf(3.0f * sqrtf(lam));
+                // O8 (pinned)
+                if (!isfinite(u) || !isfinite(v) || !isfinite(rad)) { ++c_degen; goto done; }
+                const float fx0 = floorf((u - rad) * 0.0625f), fx1 = floorf((u + rad) * 0.0625f);
+                const float fy0 = floorf((v - rad) * 0.0625f), fy1 = floorf((v + rad) * 0.0625f);
+                if (fx1 < 0.0f || fx0 >= c.txf || fy1 < 0.0f || fy0 >= c.tyf) { ++c_off; goto done; }
+                r.x0 = (uint16_t)fmaxf(fx0, 0.0f);
+                r.x1 = (uint16_t)fminf(fx1, c.txf - 1.0f);
+                r.y0 = (uint16_t)fmaxf(fy0, 0.0f);
+                r.y1 = (uint16_t)fminf(fy1, c.tyf - 1.0f);
+                r.u = u; r.v = v; r.z = pz;
+                // exponent coefficients in log2 units (reading Q29): k = fp32(-log2(e)/2),
+                // ea = k ca, eb = 2k cb, ec = k cc
+                r.ea = K_EXP2 * ca; r.eb = (2.0f * K_EXP2) * cb; r.ec = K_EXP2 * ccn;
+                r.opacity = g.op;
+                // alpha >= alpha_min needs p(d) >= -log2(o / alpha_min) >= e_cut
+                r.e_cut = g.ecut;
+                r.tile_mask = GS_TILE_MASK_FULL;   // decided by gs_bin_sort (tight mode)
+                r.gid = g.gid;
+                r.view_radius = (uint32_t)vi | ((uint32_t)fminf(rad, 65535.0f) << 16);
+                // O10: SH colour at d = (mu - c_cam)/|mu - c_cam|
+                const float dx = g.mx - c.ccx, dy = g.my - c.ccy, dz = g.mz - c.ccz;
+                const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
+                sh_color(S.sh_degree, S.sh, n, (int64_t)g.gid, dx * inv, dy * inv, dz * inv, r.rgb);
+                visible = true;
+            }
+        done:;
+        }
+        // slot reservation: one atomic per distinct view among the visible lanes
+        const uint32_t vm = __ballot_sync(0xffffffffu, visible);
+        if (visible) {
+            const uint32_t grp = __match_any_sync(vm, vi);
+            const uint32_t leader = __ffs(grp) - 1;
+            uint32_t base = 0;
+            if (lane == leader) base = atomicAdd(&n_rec[vi], (uint32_t)__popc(grp));
+            base = __shfl_sync(grp, base, leader);
+            const uint32_t slot = base + __popc(grp & ((1u << lane) - 1u));
+            if ((int64_t)slot < cap) {
+                float4* dst = reinterpret_cast<float4*>(rec + (int64_t)vi * cap + slot);
+                const float4* src = reinterpret_cast<const float4*>(&r);
+                dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2]; dst[3] = src[3];
+            } else {
+                atomicOr(status, GS_STATUS_RECORD_OVERFLOW);
+            }
+        }
+        __syncwarp();
+    };
+
     for (int w = 0; w < nw; ++w) {
         uint32_t my_mask = 0;
         if (in) {
@@ -286,8 +410,7 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
             const int j = __ffs(any) - 1;
             any &= any - 1u;
             const int vi = w * 32 + j;
-            bool visible = false;
-            gs_record r;
+            bool cand = false;
             if ((my_mask >> j) & 1u) {
                 const gs_view& V = views[vi];
                 const ViewConst& c = vcs[vi];
@@ -295,11 +418,10 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
                 const float px = ((V.R[0] * mx + V.R[1] * my) + V.R[2] * mz) + V.t[0];
                 const float py = ((V.R[3] * mx + V.R[4] * my) + V.R[5] * mz) + V.t[1];
                 const float pz = ((V.R[6] * mx + V.R[7] * my) + V.R[8] * mz) + V.t[2];
-                if (!(pz > P.z_near)) { ++c_near; goto done; }
-                if (transparent) { ++c_transp; goto done; }
-                if (degenerate || !finite3(px, py, pz)) { ++c_degen; goto done; }
+                if (!(pz > P.z_near)) { ++c_near; goto cheap_done; }
+                if (transparent) { ++c_transp; goto cheap_done; }
+                if (degenerate || !finite3(px, py, pz)) { ++c_degen; goto cheap_done; }
                 {
-                    // O3 (pinned): divide by depth first, then apply K (Alg. 1 l.12-14)
                     const float xn = px / pz, yn = py / pz;
                     const float u = V.fx * xn + V.cx;
                     const float v = V.fy * yn + V.cy;
@@ -309,88 +431,26 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
                         const float mu = 1e-5f * (fabsf(u) + fabsf(v)) + 1.0f;
                         if (u + rb < -mu || u - rb >= c.wpix + mu || v + rb < -mu || v - rb >= c.hpix + mu) {
                             ++c_off;
-                            goto done;
+                            goto cheap_done;
                         }
                     }
-                    // O5 (pinned): EWA with the clamped Jacobian
-                    const float xc = fminf(fmaxf(xn, c.lox), c.hix) * pz;
-                    const float yc = fminf(fmaxf(yn, c.loy), c.hiy) * pz;
-                    const float z2 = pz * pz;
-                    const float j00 = V.fx / pz, j02 = -((V.fx * xc) / z2);
-                    const float j11 = V.fy / pz, j12 = -((V.fy * yc) / z2);
-                    float T0[3], T1[3];
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        T0[k] = j00 * V.R[0 * 3 + k] + j02 * V.R[2 * 3 + k];
-                        T1[k] = j11 * V.R[1 * 3 + k] + j12 * V.R[2 * 3 + k];
-                    }
-                    // Vt = T Sigma (Sigma symmetric: S(r,c) with S01=S10 ...)
-                    const float S00 = Sg[0], S01 = Sg[1], S02 = Sg[2], S11 = Sg[3], S12 = Sg[4], S22 = Sg[5];
-                    const float V00 = (T0[0] * S00 + T0[1] * S01) + T0[2] * S02;
-                    const float V01 = (T0[0] * S01 + T0[1] * S11) + T0[2] * S12;
-                    const float V02 = (T0[0] * S02 + T0[1] * S12) + T0[2] * S22;
-                    const float V10 = (T1[0] * S00 + T1[1] * S01) + T1[2] * S02;
-                    const float V11 = (T1[0] * S01 + T1[1] * S11) + T1[2] * S12;
-                    const float V12 = (T1[0] * S02 + T1[1] * S12) + T1[2] * S22;
-                    const float s00 = (V00 * T0[0] + V01 * T0[1]) + V02 * T0[2];
-                    const float s01 = (V00 * T1[0] + V01 * T1[1]) + V02 * T1[2];
-                    const float s11 = (V10 * T1[0] + V11 * T1[1]) + V12 * T1[2];
-                    const float a = s00 + P.dilation, b = s01, cc = s11 + P.dilation;
-                    // O6 (pinned)
-                    const float det = a * cc - b * b;
-                    if (!(det > 0.0f)) { ++c_degen; goto done; }
-                    const float ca = cc / det, cb = -(b / det), ccn = a / det;
-                    // O7 (pinned)
-                    const float mid = 0.5f * (a + cc);
-                    const float lam = mid + sqrtf(fmaxf(mid * mid - det, 0.0f));
-                    const float rad = ceilf(3.0f * sqrtf(lam));
-                    // O8 (pinned)
-                    if (!isfinite(u) || !isfinite(v) || !isfinite(rad)) { ++c_degen; goto done; }
-                    const float fx0 = floorf((u - rad) * 0.0625f), fx1 = floorf((u + rad) * 0.0625f);
-                    const float fy0 = floorf((v - rad) * 0.0625f), fy1 = floorf((v + rad) * 0.0625f);
-                    if (fx1 < 0.0f || fx0 >= c.txf || fy1 < 0.0f || fy0 >= c.tyf) { ++c_off; goto done; }
-                    r.x0 = (uint16_t)fmaxf(fx0, 0.0f);
-                    r.x1 = (uint16_t)fminf(fx1, c.txf - 1.0f);
-                    r.y0 = (uint16_t)fmaxf(fy0, 0.0f);
-                    r.y1 = (uint16_t)fminf(fy1, c.tyf - 1.0f);
-                    r.u = u; r.v = v; r.z = pz;
-                    // exponent coefficients in log2 units (reading Q29): k = fp32(-log2(e)/2),
-                    // ea = k ca, eb = 2k cb, ec = k cc
-                    r.ea = K_EXP2 * ca; r.eb = (2.0f * K_EXP2) * cb; r.ec = K_EXP2 * ccn;
-                    r.opacity = op;
-                    // alpha >= alpha_min needs p(d) >= -log2(o / alpha_min) >= e_cut
-                    r.e_cut = e_cut;
-                    r.tile_mask = GS_TILE_MASK_FULL;   // decided by gs_bin_sort (tight mode)
-                    r.gid = (uint32_t)i;
-                    r.view_radius = (uint32_t)vi | ((uint32_t)fminf(rad, 65535.0f) << 16);
-                    // O10: SH colour at d = (mu - c_cam)/|mu - c_cam|
-                    const float dx = mx - c.ccx, dy = my - c.ccy, dz = mz - c.ccz;
-                    const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
-                    sh_color(S.sh_degree, S.sh, n, i, dx * inv, dy * inv, dz * inv, r.rgb);
-                    visible = true;
+                    cand = true;
                 }
-            done:;
+            cheap_done:;
             }
-            // warp-aggregated slot reservation for view vi
-            const uint32_t vm = __ballot_sync(0xffffffffu, visible);
-            if (vm) {
-                uint32_t base = 0;
-                const uint32_t leader = __ffs(vm) - 1;
-                if (lane == leader) base = atomicAdd(&n_rec[vi], (uint32_t)__popc(vm));
-                base = __shfl_sync(0xffffffffu, base, leader);
-                if (visible) {
-                    const uint32_t slot = base + __popc(vm & ((1u << lane) - 1u));
-                    if ((int64_t)slot < cap) {
-                        float4* dst = reinterpret_cast<float4*>(rec + (int64_t)vi * cap + slot);
-                        const float4* src = reinterpret_cast<const float4*>(&r);
-                        dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2]; dst[3] = src[3];
-                    } else {
-                        atomicOr(status, GS_STATUS_RECORD_OVERFLOW);
-                    }
-                }
+            const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+            if (cand) queue[qn + __popc(bal & ((1u << lane) - 1u))] = lane | ((uint32_t)vi << 5);
+            qn += __popc(bal);
+            __syncwarp();
+            if (qn >= 32) {
+                process(32);
+                if (lane < qn - 32) queue[lane] = queue[32 + lane];
+                __syncwarp();
+                qn -= 32;
             }
         }
     }
+    if (qn > 0) process(qn);
     // diagnostics: warp-reduce then one atomic per counter per warp
     uint32_t cnt[4] = {c_near, c_transp, c_degen, c_off};
 #pragma unroll
