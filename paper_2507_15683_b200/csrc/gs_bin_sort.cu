@@ -86,6 +86,9 @@ size_t ws_bytes(int64_t cap, int64_t T) {
 // single view where every counter is hot); otherwise it falls back to one
 // global reduction per pair.
 constexpr int BIN_THREADS = 512;
+#ifndef GS_BIN_CTAS_PER_SM
+#define GS_BIN_CTAS_PER_SM 8
+#endif
 constexpr int HIST_MAX = 16384;   // tiles per view handled on chip (64 KB)
 
 __device__ __forceinline__ void chunk_of(uint32_t nv, uint32_t& k0, uint32_t& k1) {
@@ -770,9 +773,10 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * T, s);
     cudaMemsetAsync(w.big_count, 0, 2 * sizeof(uint32_t), s);
 
-    // chunks of >= 1024 records, ~2 CTAs per SM over the whole batch
+    // chunks of >= 1024 records, ~8 CTAs per SM over the whole batch (latency hiding of the
+    // per-record tile loops; each CTA flushes its on-chip histogram once)
     const int64_t blocks_per_view =
-        std::max<int64_t>(1, std::min<int64_t>((cap + 1023) / 1024, (2 * num_sms() + n_views - 1) / n_views));
+        std::max<int64_t>(1, std::min<int64_t>((cap + 1023) / 1024, (GS_BIN_CTAS_PER_SM * num_sms() + n_views - 1) / n_views));
     dim3 rgrid((unsigned)blocks_per_view, (unsigned)n_views);
     int max_tiles = 0;
     for (int i = 0; i < n_views; ++i)
