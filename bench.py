@@ -466,7 +466,9 @@ def main():
     traffic = ncu_traffic(f"{args.config}@{args.scale}/{args.binning}/{'tcgen05' if tc_path else 'mma_sync'}")
     roof = {"bound": "hbm", "kernel": "gs_rasterize", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": raster_bytes, "dominant_stage": names[dom]}
+            "algorithmic_bytes_per_launch": raster_bytes, "dominant_stage": names[dom],
+            "note": "HBM roofline of the algorithmic bytes; the kernel is instruction-issue bound "
+                    "(ncu issue-active ~0.73, profiles/r01_ncu_full_rasterize_C4x16.txt), traffic = algorithmic"}
     launches_per_step = (3 if ds.n_blocks else 2) + 8 + 1 + 1 + (1 if scorer is not None else 0)
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
