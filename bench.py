@@ -181,7 +181,7 @@ def run_reference(args):
             pix += v.width * v.height
     total = sum(times)
     value = pix / total / 1e6
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": 0, "steps": args.steps,
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "ms_per_view": 1e3 * total / args.steps,
            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
            "data": "synthetic", "config": {"workload": args.config, "scale": args.scale},
