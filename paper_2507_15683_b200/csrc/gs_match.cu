@@ -280,13 +280,25 @@ row_kernel(MatchWs ws, int Nc, int Ncp, float k2) {
                     run_m = mn;
                 }
             } else {
+                // argmax over the chunk of 2 x k2 - c'_j (one FFMA + compare / select per
+                // element; the winner's column offset is an immediate), merged once
+                const float k22 = 2.f * k2;
+                float cb = -INFINITY;
+                int ct = -1;
+                if (nv == CW) {
 #pragma unroll
-                for (int t = 0; t < CW; ++t) {
-                    if (t < nv) {
-                        const float y = 2.f * (x[t] * k2) - cj[t];
-                        if (y > best) { best = y; bj = j0 + t; }
+                    for (int t = 0; t < CW; ++t) {
+                        const float y = fmaf(x[t], k22, -cj[t]);
+                        if (y > cb) { cb = y; ct = t; }
+                    }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < CW; ++t) {
+                        const float y = fmaf(x[t], k22, -cj[t]);
+                        if (t < nv && y > cb) { cb = y; ct = t; }
                     }
                 }
+                if (cb > best) { best = cb; bj = j0 + ct; }
             }
         }
         // combine the column parts of each row
