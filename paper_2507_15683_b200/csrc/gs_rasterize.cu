@@ -8,18 +8,19 @@
 // Design (B200):
 //   * a 16x16 tile is rendered by 8 consumer warps (one 8x4 sub-tile each)
 //     fed by 1 producer warp;
-//   * persistent CTAs (grid = SMs x resident CTAs); the producer streams
-//     the sorted lists of the CTA's tiles through a 6-stage shared-memory ring
-//     (cp.async 16-B gathers of the 64-B records and D*4-B feature rows,
-//     completion signalled on "full" mbarriers via cp.async.mbarrier.arrive),
-//     running ahead across tile boundaries; consumers release stages through
-//     "empty" mbarriers -- no CTA-wide barrier anywhere in the loop;
-//   * exact warp-level culling: each lane tests one staged entry: does the
+//   * persistent CTAs (grid = SMs x resident CTAs, tiles handed out in order by
+//     a dynamic scheduler); the producer streams the sorted lists of the CTA's
+//     tiles through an 8-stage x 32-entry shared-memory ring (cp.async 16-B
+//     gathers of the 64-B records and the feature rows, completion signalled on
+//     "full" mbarriers via cp.async.mbarrier.arrive), running ahead across tile
+//     boundaries; consumers take stages in same-tile pairs and release them
+//     through "empty" mbarriers -- no CTA-wide barrier anywhere in the loop;
+//   * exact warp-level culling: each lane tests staged entries: does the
 //     entry's alpha >= alpha_min ellipse (p >= e_cut, inflated) touch the warp's
-//     8x4 pixel rectangle?  A ballot gives the entries the warp walks
+//     8x4 pixel rectangle?  Ballots give the entries the warp walks
 //     (conservative, so it never drops a Gaussian the oracle blends -- Q11);
-//   * per pixel the skip / stop decisions (power, alpha, Tn) are evaluated with
-//     explicit _rn intrinsics in the oracle's operation order;
+//   * per pixel the skip / stop decisions (exponent, alpha, Tn) are evaluated
+//     with explicit _rn / fma intrinsics in the oracle's operation order (Q29);
 //   * the feature blend F[px][:] += w[px][k] f[k][:] -- the one dense
 //     contraction of the path -- runs on the tensor cores.  Each warp compacts
 //     the weights of its walked entries into a 16-row shared buffer; a full
@@ -74,19 +75,9 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
-// round a finite fp32 to the nearest tf32 (ties away from zero) with integer ops; the
-// tensor core reads only the top 19 bits of a .tf32 operand
-__device__ __forceinline__ uint32_t to_tf32(float x) { return (__float_as_uint(x) + 0x1000u) & 0xffffe000u; }
 __device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};\n"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};\n"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));

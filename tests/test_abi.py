@@ -113,3 +113,54 @@ def test_no_cpu_fallback_in_product_path():
         if f.endswith(".py"):
             txt = open(os.path.join(pkg, f)).read()
             assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_new_calls_validate_on_the_host(G):
+    """gs_match / gs_pnp / gs_verify_consistency / gs_validate_scene /
+    gs_scene_features_f16 reject bad arguments before any launch (no GPU needed)."""
+    L = G.lib()
+    fake = ctypes.c_void_p(256)
+    m = G.gs.gs_matches()
+    # NULL outputs
+    st = L.gs_match(fake, fake, 1, 32, 64, 64, ctypes.c_float(0.1), ctypes.c_float(0.05), None, None, fake,
+                    ctypes.c_size_t(1 << 30), ctypes.byref(m), None)
+    assert st == 1 and b"NULL" in L.gs_last_error()
+    m.coarse = m.coarse_prob = m.peak = m.prob = m.ref = fake
+    st = L.gs_match(fake, fake, 1, 24, 64, 64, ctypes.c_float(0.1), ctypes.c_float(0.05), None, None, fake,
+                    ctypes.c_size_t(1 << 30), ctypes.byref(m), None)
+    assert st == 2 and b"D = 24" in L.gs_last_error()                 # UNSUPPORTED feature width
+    st = L.gs_match(fake, fake, 1, 32, 60, 64, ctypes.c_float(0.1), ctypes.c_float(0.05), None, None, fake,
+                    ctypes.c_size_t(1 << 30), ctypes.byref(m), None)
+    assert st == 1 and b"multiples of 8" in L.gs_last_error()
+    st = L.gs_match(fake, fake, 1, 32, 64, 64, ctypes.c_float(0.0), ctypes.c_float(0.05), None, None, fake,
+                    ctypes.c_size_t(1 << 30), ctypes.byref(m), None)
+    assert st == 1 and b"tau" in L.gs_last_error()
+    need = G.match_workspace_bytes(1, 32, 64, 64)
+    st = L.gs_match(fake, fake, 1, 32, 64, 64, ctypes.c_float(0.1), ctypes.c_float(0.05), None, None, fake,
+                    ctypes.c_size_t(need - 1), ctypes.byref(m), None)
+    assert st == 3                                                      # WORKSPACE_TOO_SMALL
+    stats = ctypes.c_void_p(512)
+    st = L.gs_pnp(fake, fake, 1, 8, 8, fake, ctypes.c_float(3.0), 999, 0, 1024, fake, ctypes.c_size_t(1 << 30),
+                  ctypes.c_void_p(1024), stats, None)
+    assert st == 2 and b"n_hyp" in L.gs_last_error()
+    st = L.gs_pnp(fake, fake, 1, 8, 8, fake, ctypes.c_float(3.0), 64, 0, 1024, fake, ctypes.c_size_t(1 << 30),
+                  fake, stats, None)
+    assert st == 1 and b"alias" in L.gs_last_error()
+    st = L.gs_pnp(fake, fake, 1, 8, 8, fake, ctypes.c_float(3.0), 64, 0, 1024, fake, ctypes.c_size_t(16),
+                  ctypes.c_void_p(1024), stats, None)
+    assert st == 3
+    st = L.gs_verify_consistency(fake, 3, 1, ctypes.c_float(20.0), None, None, fake, None)
+    assert st == 1
+    s = G.gs.gs_scene()
+    s.n, s.sh_degree, s.feat_dim = 10, 0, 0
+    st = L.gs_validate_scene(ctypes.byref(s), 0, None, None, None)
+    assert st == 1                                                      # geometry pointers NULL
+    st = L.gs_scene_features_f16(ctypes.byref(s), fake, None)
+    assert st == 1 and b"no features" in L.gs_last_error()
+    assert G.match_workspace_bytes(0, 32, 64, 64) == 0 and G.pnp_workspace_bytes(0, 10) == 0
+
+
+def test_struct_sizes_of_n2_types(G):
+    assert ctypes.sizeof(G.gs.gs_matches) == 7 * 8
+    assert ctypes.sizeof(G.gs.gs_pnp_stats) == 16
+    assert ctypes.sizeof(G.gs.gs_bins) == 8 * 7 + 8
