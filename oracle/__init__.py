@@ -185,6 +185,22 @@ def composite(view, rec, keys, feat=None, params: Optional[Params] = None) -> Di
                 blends=int(counters[1]), contrib=contrib[:len(rec["gid"])])
 
 
+def feature_grad(view, rec, keys, feat, gF, n_gauss: int, params: Optional[Params] = None,
+                 fgrad: Optional[np.ndarray] = None) -> np.ndarray:
+    """N4: dL/df [n_gauss][D] (fp64, added to `fgrad`) for a loss whose gradient
+    w.r.t. this view's rendered feature map is gF [D][H][W]: sum_px w_g(px) gF(px)
+    (F = sum_k w_k f_k with the geometry, hence the weights, frozen)."""
+    params = params or Params()
+    D = int(feat.shape[1])
+    fgrad = np.zeros((n_gauss, D), np.float64) if fgrad is None else fgrad
+    vc, pc = _view_c(view), params.c()
+    lib().oracle_feature_grad(ctypes.byref(vc), ctypes.byref(pc), _p(_c32(rec["u"])), _p(_c32(rec["v"])),
+                              _p(_c32(rec["conic"])), _p(_c32(rec["opacity"])), _p(_c32(rec["rgb"])),
+                              _p(_c32(rec["z"])), _p(np.ascontiguousarray(rec["gid"], np.int32)), _p(_c32(feat)),
+                              ctypes.c_int32(D), _p(keys["rec"]), _p(keys["ranges"]), _p(_c32(gF)), _p(fgrad))
+    return fgrad
+
+
 def brute_force(view, rec, feat=None, params: Optional[Params] = None) -> Dict[str, np.ndarray]:
     """Per-pixel brute force over all records (plain definition)."""
     params = params or Params()

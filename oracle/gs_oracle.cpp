@@ -421,8 +421,18 @@ struct PixelOut {
 const double FLAG_ALPHA_REL = 1.0 / 262144.0;
 const double FLAG_T_REL = 1.0 / 4096.0;
 
+// N4 (feature-field backward, Eq. 2 with the geometry frozen): when gF is set,
+// fgrad[gid][c] += w * gF[c][pix] for every blended entry -- dL/df of a loss
+// whose gradient w.r.t. the rendered feature map is gF, since F = sum_k w_k f_k.
+struct FeatGrad {
+    const float* gF;   // [D][H][W] upstream gradient of this view
+    int64_t HW, pix;
+    double* fgrad;     // [n_gauss][D]
+};
+
 void composite_pixel(const Records& rc, const or_params* P, int32_t pxi, int32_t pyi,
-                     const uint32_t* list, int64_t len, PixelOut& o, double* contrib) {
+                     const uint32_t* list, int64_t len, PixelOut& o, double* contrib,
+                     const FeatGrad* fg = nullptr) {
     const float pxf = (float)pxi, pyf = (float)pyi;
     float T = 1.0f;
     o.C[0] = o.C[1] = o.C[2] = 0.0;
@@ -466,6 +476,9 @@ void composite_pixel(const Records& rc, const or_params* P, int32_t pxi, int32_t
         }
         o.blends++;
         if (contrib) contrib[i] += (double)w;   // N1: per-Gaussian accumulated blend weight
+        if (fg)
+            for (int c = 0; c < rc.D; ++c)
+                fg->fgrad[(int64_t)rc.gid[i] * rc.D + c] += (double)w * fg->gF[c * fg->HW + fg->pix];
         // 8. T = Tn
         T = Tn;
     }
@@ -501,6 +514,24 @@ void oracle_composite(const or_view* V, const or_params* P, const float* u, cons
             store_pixel(o, HW, pix, out_rgb, out_depth, out_alpha, out_feat, flags, D);
             counters[0] += o.evals;
             counters[1] += o.blends;
+        }
+}
+
+// N4: dL/df accumulated over this view (fgrad [n_gauss][D], added to).
+void oracle_feature_grad(const or_view* V, const or_params* P, const float* u, const float* v,
+                         const float* conic, const float* opac, const float* rgb, const float* z,
+                         const int32_t* gid, const float* feat, int32_t D, const uint32_t* key_rec,
+                         const uint32_t* ranges, const float* gF, double* fgrad) {
+    Records rc{u, v, conic, opac, rgb, z, gid, feat, D};
+    const int32_t W = V->width, H = V->height, TX = (W + 15) / 16;
+    const int64_t HW = (int64_t)W * H;
+    PixelOut o;
+    for (int32_t py = 0; py < H; ++py)
+        for (int32_t px = 0; px < W; ++px) {
+            const int64_t t = (int64_t)(py / 16) * TX + px / 16;
+            const uint32_t s = ranges[t * 2], e = ranges[t * 2 + 1];
+            const FeatGrad fg{gF, HW, (int64_t)py * W + px, fgrad};
+            composite_pixel(rc, P, px, py, key_rec + s, (int64_t)e - s, o, nullptr, &fg);
         }
 }
 
