@@ -347,6 +347,28 @@ gs_status gs_pnp(const uint8_t* valid, const float* xyz, int32_t n_problems, int
 gs_status gs_verify_consistency(const gs_view* trace_dev, int32_t n_iters, int32_t n_problems, float tau_deg,
                                 float* angle_deg, float* dtrans, int32_t* verdict, void* stream);
 
+/*
+ * N4 -- feature-field backward of Eq. 2 with the geometry frozen
+ * (DESIGN.md §4.8): for the batch rendered by gs_project / gs_bin_sort (same
+ * proj, bins, views), grad_feat[g][c] += sum over the batch's pixels of
+ * w_g(px) * grad_image[c][px], where w are the forward blend weights and
+ * grad_image is dL/dF in the layout of gs_images.feat ([D][H][W] per view at
+ * D * pix_offset).  grad_feat [n][D] f32 is accumulated (caller zeroes).  The
+ * per-pixel walk is the forward's (same cull, exponent, stop rule).
+ * D must be a multiple of 8 (8..64).  Asynchronous; device pointers.
+ */
+gs_status gs_feature_backward(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins,
+                              const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
+                              const gs_params* params, const float* grad_image, float* grad_feat, void* stream);
+
+/* Eq. 2's L1 feature loss: grad_image[i] = scale * sign(rendered[i] - target[i]);
+ * *loss (device double, accumulated) += scale * sum |rendered - target|. */
+gs_status gs_feature_l1_grad(const float* rendered, const float* target, int64_t n, float scale,
+                             float* grad_image, double* loss, void* stream);
+
+/* feat[i] -= lr * grad_feat[i] over n floats; refreshes the fp16 copy (gs_scene.feat_h) when feat_h != NULL. */
+gs_status gs_feature_sgd(float* feat, const float* grad_feat, int64_t n, float lr, void* feat_h, void* stream);
+
 /* Workspace of gs_project: a (view x block) visibility bitmask. */
 size_t gs_project_workspace_bytes(int32_t n_blocks, int32_t n_views);
 

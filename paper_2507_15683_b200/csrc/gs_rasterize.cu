@@ -687,6 +687,193 @@ gs_status launch(const gs_scene* scene, const gs_projected* proj, const gs_bins*
     return check_launch("rasterize_kernel");
 }
 
+// ---------------------------------------------------------------- N4 backward
+// Feature-field backward of Eq. 2 with the geometry frozen:
+// dL/df_g += sum over pixels of w_g(px) * dL/dF(px).  One CTA per tile (8 warps
+// x 8x4 pixels, the forward's exact per-pixel walk: same cull, exponent, alpha,
+// stop rule), the tile list in chunks of BW_CHUNK entries.  Per warp, the
+// weights of 16 walked entries feed m16n8k16 MMAs G[entry][ch] = W[entry][px] .
+// g[px][ch] (fp16 hi + lo operands, 3 products; the warp's upstream gradients
+// live in registers as B fragments for the whole tile), reduced over the 8
+// warps in shared memory, then one global atomic per (entry, channel) per chunk.
+constexpr int BW_CHUNK = 64;
+
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256)
+feature_backward_kernel(const gs_view* __restrict__ views, int n_views, const gs_record* __restrict__ rec,
+                        const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ ranges, gs_params P,
+                        const float* __restrict__ gimg, float* __restrict__ grad, const uint32_t* __restrict__ status) {
+    if (*status) return;
+    constexpr int NT = D / 8;
+    __shared__ float4 srec[BW_CHUNK + 1][2];      // u, v, ea, eb | ec, o, e_cut, - ; row BW_CHUNK = null
+    __shared__ uint32_t sgid[BW_CHUNK];
+    __shared__ float acc[BW_CHUNK][D + 1];
+    __shared__ __align__(16) float wbuf[8][16][36];
+    __shared__ int ent[8][BW_CHUNK + 18];
+    const uint32_t tile = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+    const int vi = find_view_by_tile(views, n_views, tile);
+    const gs_view& V = views[vi];
+    const int W = V.width, H = V.height, TX = (W + GS_TILE - 1) / GS_TILE;
+    const uint32_t lt = tile - V.tile_offset;
+    const int sx = (int)(lt % (uint32_t)TX) * 16 + (warp & 1) * 8, sy = (int)(lt / (uint32_t)TX) * 16 + (warp >> 1) * 4;
+    const int px = sx + (lane & 7), py = sy + (lane >> 3);
+    const bool inside = px < W && py < H;
+    const float pxf = (float)px, pyf = (float)py;
+    const float rx0 = (float)sx, rx1 = (float)(sx + 7), ry0 = (float)sy, ry1 = (float)(sy + 3);
+    const int64_t HW = (int64_t)W * H;
+    const float* G = gimg + (int64_t)D * V.pix_offset;
+    // B fragments of this warp's upstream gradients: k = pixel p (p -> (p & 7, p >> 3)), n = channel
+    auto gval = [&](int p, int ch) -> float {
+        const int x = sx + (p & 7), y = sy + (p >> 3);
+        return (x < W && y < H) ? __ldg(&G[(int64_t)ch * HW + (int64_t)y * W + x]) : 0.f;
+    };
+    uint32_t bh[NT][2][2], bl[NT][2][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int p = 16 * ks + 8 * r + 2 * t4, ch = 8 * nt + g;
+                const float v0 = gval(p, ch), v1 = gval(p + 1, ch);
+                const __half2 h = __floats2half2_rn(v0, v1);
+                const float2 hf = __half22float2(h);
+                bh[nt][ks][r] = *reinterpret_cast<const uint32_t*>(&h);
+                bl[nt][ks][r] = pack_h2(v0 - hf.x, v1 - hf.y);
+            }
+    for (int i = tid; i < BW_CHUNK * (D + 1); i += 256) (&acc[0][0])[i] = 0.f;
+    if (tid < 2) srec[BW_CHUNK][tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float T = 1.0f;
+    bool done = !inside;
+    bool warp_done = __all_sync(0xffffffffu, done);
+    const uint32_t rs = ranges[2 * tile], re = ranges[2 * tile + 1];
+    // 16 walked entries -> G rows added to acc[chunk entry][ch]
+    auto kstep = [&](int eb) {
+        float d[NT][4];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+            uint32_t ah[4], al[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int row = g + ((i & 1) ? 8 : 0), p = 16 * ks + 2 * t4 + ((i & 2) ? 8 : 0);
+                const float w0 = wbuf[warp][row][p], w1 = wbuf[warp][row][p + 1];
+                const __half2 h = __floats2half2_rn(w0, w1);
+                const float2 hf = __half22float2(h);
+                ah[i] = *reinterpret_cast<const uint32_t*>(&h);
+                al[i] = pack_h2(w0 - hf.x, w1 - hf.y);
+            }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                mma_f16(d[nt], ah, bh[nt][ks][0], bh[nt][ks][1]);
+                mma_f16(d[nt], ah, bl[nt][ks][0], bl[nt][ks][1]);
+                mma_f16(d[nt], al, bh[nt][ks][0], bh[nt][ks][1]);
+            }
+        }
+        const int e0 = ent[warp][eb + g], e1 = ent[warp][eb + g + 8];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int ch = 8 * nt + 2 * t4;
+            if (e0 < BW_CHUNK) { atomicAdd(&acc[e0][ch], d[nt][0]); atomicAdd(&acc[e0][ch + 1], d[nt][1]); }
+            if (e1 < BW_CHUNK) { atomicAdd(&acc[e1][ch], d[nt][2]); atomicAdd(&acc[e1][ch + 1], d[nt][3]); }
+        }
+    };
+    __syncthreads();
+    for (uint32_t c0 = rs; c0 < re; c0 += BW_CHUNK) {
+        const int cnt = (int)min((uint32_t)BW_CHUNK, re - c0);
+        for (int i = tid; i < 2 * cnt; i += 256) {
+            const uint32_t slot = __ldg(&sorted_rec[c0 + i / 2]);
+            srec[i / 2][i & 1] = __ldg(reinterpret_cast<const float4*>(rec + slot) + (i & 1));
+            if ((i & 1) == 0) sgid[i / 2] = __ldg(&rec[slot].gid);
+        }
+        __syncthreads();
+        if (!warp_done) {
+            bool hit[2] = {false, false};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = lane + 32 * h;
+                if (j < cnt) {
+                    const float4 a = srec[j][0], b = srec[j][1];
+                    hit[h] = ellipse_hits_rect(a.x, a.y, a.z, a.w, b.x, b.z, rx0, rx1, ry0, ry1);
+                }
+            }
+            const uint32_t m0 = __ballot_sync(0xffffffffu, hit[0]), m1 = __ballot_sync(0xffffffffu, hit[1]);
+            const int n0 = __popc(m0), n = n0 + __popc(m1);
+            const uint32_t below = (1u << lane) - 1u;
+            if (hit[0]) ent[warp][__popc(m0 & below)] = lane;
+            if (hit[1]) ent[warp][n0 + __popc(m1 & below)] = lane + 32;
+            const int np = (n + 15) & ~15;                     // padded to whole K steps
+            if (lane < np - n) ent[warp][n + lane] = BW_CHUNK;  // null rows
+            __syncwarp();
+            for (int i = 0; i < np; ++i) {
+                const int k = ent[warp][i];
+                float a = entry_alpha(srec[k][0], srec[k][1], pxf, pyf, P);
+                a = (done || k == BW_CHUNK) ? 0.0f : a;
+                const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
+                const bool stop = Tn < P.t_min;
+                const float wgt = stop ? 0.0f : __fmul_rn(a, T);
+                T = stop ? T : Tn;
+                done = done || stop;
+                wbuf[warp][i & 15][lane] = wgt;
+                if ((i & 15) == 15) {
+                    __syncwarp();
+                    kstep(i - 15);
+                    __syncwarp();
+                }
+            }
+            warp_done = __all_sync(0xffffffffu, done);
+        }
+        __syncthreads();
+        for (int i = tid; i < cnt * D; i += 256) {
+            const int e = i / D, ch = i % D;
+            const float v = acc[e][ch];
+            if (v != 0.f) {
+                atomicAdd(&grad[(int64_t)sgid[e] * D + ch], v);
+                acc[e][ch] = 0.f;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int D>
+gs_status launch_backward(const gs_projected* proj, const gs_bins* bins, const gs_view* views_dev, int n_views,
+                          int64_t T, const gs_params* P, const float* gimg, float* grad, cudaStream_t s) {
+    if (T <= 0) return GS_OK;
+    feature_backward_kernel<D><<<(unsigned)T, 256, 0, s>>>(views_dev, n_views, proj->rec, bins->sorted_rec,
+                                                           bins->ranges, *P, gimg, grad, proj->status);
+    return check_launch("feature_backward_kernel");
+}
+
+// N4 training helpers: L1 loss of Eq. 2 and a plain gradient step
+__global__ void l1_grad_kernel(const float* __restrict__ F, const float* __restrict__ Ft, int64_t n, float scale,
+                               float* __restrict__ gF, double* __restrict__ loss) {
+    double part = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float d = F[i] - Ft[i];
+        gF[i] = d > 0.f ? scale : (d < 0.f ? -scale : 0.f);
+        part += (double)fabsf(d) * scale;
+    }
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(loss, part);
+}
+
+__global__ void sgd_kernel(float* __restrict__ feat, const float* __restrict__ grad, int64_t n, float lr,
+                           __half* __restrict__ feat_h) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float f = feat[i] - lr * grad[i];
+        feat[i] = f;
+        if (feat_h) feat_h[i] = __float2half_rn(f);
+    }
+}
+
 }  // namespace
 }  // namespace gs
 
@@ -759,4 +946,51 @@ extern "C" gs_status gs_scene_features_f16(const gs_scene* scene, void* feat_h_o
     features_f16_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
         reinterpret_cast<const float4*>(scene->feat), reinterpret_cast<uint2*>(feat_h_out), n4);
     return check_launch("features_f16_kernel");
+}
+
+extern "C" gs_status gs_feature_backward(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins,
+                                         const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
+                                         const gs_params* params, const float* grad_image, float* grad_feat,
+                                         void* stream) {
+    gs_status st = validate_scene(scene, false);
+    if (st != GS_OK) return st;
+    int64_t total_pixels = 0, T = 0;
+    st = validate_views(views_host, views_dev, n_views, &total_pixels, &T);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(params && proj && proj->rec && proj->status && bins && bins->ranges && bins->sorted_rec && grad_image &&
+                   grad_feat,
+               GS_INVALID_ARG, "gs_feature_backward: NULL pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (scene->feat_dim) {
+        case 8: return launch_backward<8>(proj, bins, views_dev, n_views, T, params, grad_image, grad_feat, s);
+        case 16: return launch_backward<16>(proj, bins, views_dev, n_views, T, params, grad_image, grad_feat, s);
+        case 24: return launch_backward<24>(proj, bins, views_dev, n_views, T, params, grad_image, grad_feat, s);
+        case 32: return launch_backward<32>(proj, bins, views_dev, n_views, T, params, grad_image, grad_feat, s);
+        case 40: return launch_backward<40>(proj, bins, views_dev, n_views, T, params, grad_image, grad_feat, s);
+        case 48: return launch_backward<48>(proj, bins, views_dev, n_views, T, params, grad_image, grad_feat, s);
+        case 56: return launch_backward<56>(proj, bins, views_dev, n_views, T, params, grad_image, grad_feat, s);
+        case 64: return launch_backward<64>(proj, bins, views_dev, n_views, T, params, grad_image, grad_feat, s);
+        default:
+            gs::set_error("gs_feature_backward: feat_dim = %d (need a multiple of 8, 8..64)", scene->feat_dim);
+            return GS_UNSUPPORTED;
+    }
+}
+
+extern "C" gs_status gs_feature_l1_grad(const float* rendered, const float* target, int64_t n, float scale,
+                                        float* grad_image, double* loss, void* stream) {
+    GS_REQUIRE(rendered && target && grad_image && loss && n >= 0, GS_INVALID_ARG, "gs_feature_l1_grad: bad args");
+    if (n == 0) return GS_OK;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+    l1_grad_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(rendered, target, n, scale, grad_image, loss);
+    return check_launch("l1_grad_kernel");
+}
+
+extern "C" gs_status gs_feature_sgd(float* feat, const float* grad_feat, int64_t n, float lr, void* feat_h,
+                                    void* stream) {
+    GS_REQUIRE(feat && grad_feat && n >= 0, GS_INVALID_ARG, "gs_feature_sgd: bad args");
+    if (n == 0) return GS_OK;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+    sgd_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(feat, grad_feat, n, lr,
+                                                                   reinterpret_cast<__half*>(feat_h));
+    return check_launch("sgd_kernel");
 }

@@ -70,7 +70,8 @@ class gs_images(ctypes.Structure):
 
 EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_layout", "gs_scene_block_bounds",
            "gs_scene_features_f16", "gs_validate_scene", "gs_match", "gs_match_workspace_bytes",
-           "gs_pnp", "gs_pnp_workspace_bytes", "gs_verify_consistency",
+           "gs_pnp", "gs_pnp_workspace_bytes", "gs_verify_consistency", "gs_feature_backward",
+           "gs_feature_l1_grad", "gs_feature_sgd",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_backproject", "gs_visibility_score", "gs_visibility_workspace_bytes"]
 
@@ -449,3 +450,24 @@ def views_pose_array(dev_views: torch.Tensor, n: int):
     R = _np.array([[arr[i].R[k] for k in range(9)] for i in range(n)], _np.float64).reshape(n, 3, 3)
     t = _np.array([[arr[i].t[k] for k in range(3)] for i in range(n)], _np.float64)
     return R, t
+
+
+# ---------------------------------------------------------------------- N4 feature-field backward
+def gs_feature_backward(scene: "DeviceScene", proj: "Projected", bins: "Bins", views, params: gs_params,
+                        grad_image: torch.Tensor, grad_feat: torch.Tensor, stream=None):
+    _check(lib().gs_feature_backward(ctypes.byref(scene.struct), ctypes.byref(proj.struct), ctypes.byref(bins.struct),
+                                     views.host, views.dev_ptr, ctypes.c_int32(views.n), ctypes.byref(params),
+                                     _ptr(grad_image), _ptr(grad_feat), _stream(stream)), "gs_feature_backward")
+
+
+def gs_feature_l1_grad(rendered: torch.Tensor, target: torch.Tensor, scale: float, grad_image: torch.Tensor,
+                       loss: torch.Tensor, stream=None):
+    _check(lib().gs_feature_l1_grad(_ptr(rendered), _ptr(target), ctypes.c_int64(rendered.numel()),
+                                    ctypes.c_float(scale), _ptr(grad_image), _ptr(loss), _stream(stream)),
+           "gs_feature_l1_grad")
+
+
+def gs_feature_sgd(feat: torch.Tensor, grad_feat: torch.Tensor, lr: float, feat_h: Optional[torch.Tensor] = None,
+                   stream=None):
+    _check(lib().gs_feature_sgd(_ptr(feat), _ptr(grad_feat), ctypes.c_int64(feat.numel()), ctypes.c_float(lr),
+                                _ptr(feat_h), _stream(stream)), "gs_feature_sgd")

@@ -253,3 +253,33 @@ class Refiner:
     def poses(self, i: int):
         """(R [B][3][3], t [B][3]) of trace slot i (0 = initial)."""
         return G.views_pose_array(self.slot(i), self.B)
+
+
+class FeatureDistiller:
+    """N4: Eq. 2 feature distillation with the geometry frozen -- per step: render
+    the batch, L1 loss gradient against target feature maps (gs_feature_l1_grad),
+    gs_feature_backward into dL/df, one gradient step on the scene's features
+    (gs_feature_sgd, which also refreshes the fp16 copy the tcgen05 path reads)."""
+
+    def __init__(self, scene: G.DeviceScene, views: Sequence, target: torch.Tensor, lr: float = 1.0):
+        assert scene.feat is not None
+        self.scene, self.lr = scene, lr
+        self.r = Renderer(scene, views, backproject=False)
+        self.r.render()
+        self.target = target
+        n_img = self.r.images.feat.numel()
+        self.scale = 1.0 / n_img                      # mean absolute error over all channels and pixels
+        self.gimg = torch.empty_like(self.r.images.feat)
+        self.gfeat = torch.zeros_like(scene.feat)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=scene.feat.device)
+
+    def step(self, stream=None) -> torch.Tensor:
+        """One iteration; returns the device loss (of the features before the update)."""
+        self.r.run(stream)
+        self.loss.zero_()
+        G.gs_feature_l1_grad(self.r.images.feat, self.target, self.scale, self.gimg, self.loss, stream)
+        self.gfeat.zero_()
+        G.gs_feature_backward(self.scene, self.r.proj, self.r.bins, self.r.vb, self.r.params, self.gimg,
+                              self.gfeat, stream)
+        G.gs_feature_sgd(self.scene.feat, self.gfeat, self.lr, self.scene.feat_h, stream)
+        return self.loss
