@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--refine", type=int, default=0, metavar="B",
                     help="also time N2's n = 3 refinement loop (render -> gs_match -> gs_pnp, CUDA graph) for B "
                          "queries: query features rendered at B of the batch's poses, starts 1 deg / ~1.4 m off")
+    ap.add_argument("--n4", action="store_true",
+                    help="also time N4's feature backward (gs_feature_backward) over the batch")
     ap.add_argument("--n1", action="store_true",
                     help="also time N1 (per-Gaussian contributions + Alg. 1 visibility + Eq. 4-6 scoring "
                          "against stride-8 synthetic target maps) inside the step")
@@ -436,6 +438,30 @@ def main():
               "coarse_gemm_tflops": 2.0 * 3 * 2 * 2 * nc * nc * D2 * Bp / (ms2 / 1e3) / 1e12,
               "gpu_launches": 5, "tau": 0.1, "p_min": 0.05}
 
+    # N4: feature-field backward of Eq. 2 over the batch (random upstream gradient)
+    n4 = None
+    if args.n4:
+        if scene.feat_dim == 0:
+            raise SystemExit("--n4 needs a feature scene (C3 / C4)")
+        g4 = torch.Generator(device=dev).manual_seed(99)
+        gimg = torch.randn(r.images.feat.numel(), generator=g4, device=dev)
+        gfeat = torch.zeros(scene.n * scene.feat_dim, dtype=torch.float32, device=dev)
+        for _ in range(2):
+            G.gs_feature_backward(ds, r.proj, r.bins, r.vb, r.params, gimg, gfeat, stream)
+        torch.cuda.synchronize()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        Kb = max(2, min(K, 5))
+        b0.record(stream)
+        for _ in range(Kb):
+            gfeat.zero_()
+            G.gs_feature_backward(ds, r.proj, r.bins, r.vb, r.params, gimg, gfeat, stream)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        ms4 = b0.elapsed_time(b1) / Kb
+        n4 = {"views": n_views, "ms": ms4, "ms_per_view": ms4 / n_views, "mpix_per_s": total_px / ms4 / 1e3,
+              "feat_dim": scene.feat_dim, "gpu_launches": 2}
+        del gimg, gfeat
+
     # N2 refinement loop: B queries, n = 3 rounds, one CUDA graph
     refine = None
     if args.refine:
@@ -529,6 +555,8 @@ def main():
         out["n2"] = n2
     if refine is not None:
         out["refine"] = refine
+    if n4 is not None:
+        out["n4"] = n4
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(scene, views, args.cpu_sample_views)
     if rank == 0:
