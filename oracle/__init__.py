@@ -201,6 +201,25 @@ def feature_grad(view, rec, keys, feat, gF, n_gauss: int, params: Optional[Param
     return fgrad
 
 
+GRAD_FIELDS = ("u", "v", "ea", "eb", "ec", "opacity", "r", "g", "b", "z")
+
+
+def radiance_backward(view, rec, keys, gC, gD, gA, params: Optional[Params] = None):
+    """N4: per-record gradient [cnt][10] (GRAD_FIELDS) of L = sum gC.C + gD Dz + gA A,
+    and L itself (fp64).  gC [3][H][W], gD / gA [H][W]."""
+    params = params or Params()
+    cnt = len(rec["gid"])
+    grec = np.zeros((max(1, cnt), 10), np.float64)
+    vc, pc = _view_c(view), params.c()
+    lib().oracle_radiance_backward.restype = ctypes.c_double
+    loss = lib().oracle_radiance_backward(
+        ctypes.byref(vc), ctypes.byref(pc), _p(_c32(rec["u"])), _p(_c32(rec["v"])), _p(_c32(rec["conic"])),
+        _p(_c32(rec["opacity"])), _p(_c32(rec["rgb"])), _p(_c32(rec["z"])),
+        _p(np.ascontiguousarray(rec["gid"], np.int32)), _p(keys["rec"]), _p(keys["ranges"]), _p(_c32(gC)),
+        _p(_c32(gD)), _p(_c32(gA)), _p(grec))
+    return grec[:cnt], float(loss)
+
+
 def brute_force(view, rec, feat=None, params: Optional[Params] = None) -> Dict[str, np.ndarray]:
     """Per-pixel brute force over all records (plain definition)."""
     params = params or Params()

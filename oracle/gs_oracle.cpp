@@ -535,6 +535,83 @@ void oracle_feature_grad(const or_view* V, const or_params* P, const float* u, c
         }
 }
 
+// N4 (radiance backward): for the linear loss L = sum_px gC . C + gD Dz + gA A
+// (any loss's first-order term), per record the gradient w.r.t.
+// g[10] = {u, v, ea, eb, ec, opacity, r, g, b, z}, fp64, front to back:
+//   dC/dalpha_k = T_k c_k - (C_f - C_{<=k}) / (1 - alpha_k),   dA/dalpha_k = T_f / (1 - alpha_k),
+//   alpha = o 2^p (unclamped): dalpha/do = 2^p, dalpha/dp = alpha ln 2,
+//   p = ea dx^2 + eb dx dy + ec dy^2 with dx = u - px, dy = v - py.
+// The skip and stop decisions are taken exactly as in composite_pixel (their
+// gradient is zero); a clamped alpha (0.99) has no opacity / exponent gradient.
+// Also returns the loss itself in fp64 (for finite-difference pins).
+double backward_pixel(const Records& rc, const or_params* P, int32_t pxi, int32_t pyi, const uint32_t* list,
+                      int64_t len, const double gC[3], double gD, double gA, double* grec /*[cnt][10]*/) {
+    PixelOut f;
+    composite_pixel(rc, P, pxi, pyi, list, len, f, nullptr);
+    const double Tf = f.T;
+    const float pxf = (float)pxi, pyf = (float)pyi;
+    float T = 1.0f;
+    double Cacc[3] = {0, 0, 0}, Dacc = 0;
+    for (int64_t k = 0; k < len; ++k) {
+        const uint32_t i = list[k];
+        const float dx = rc.u[i] - pxf, dy = rc.v[i] - pyf;
+        const float ca = rc.conic[i * 3 + 0], cb = rc.conic[i * 3 + 1], cc = rc.conic[i * 3 + 2];
+        const float ea = K_EXP2 * ca, eb = (2.0f * K_EXP2) * cb, ec = K_EXP2 * cc;
+        const float p = std::fmaf(dx, std::fmaf(ea, dx, eb * dy), (ec * dy) * dy);
+        if (p > 0.0f) continue;
+        const double e2p = std::exp2((double)p);
+        const float araw = (float)((double)rc.opacity[i] * e2p);
+        const float alpha = std::min(P->alpha_max, araw);
+        if (alpha < P->alpha_min) continue;
+        const float Tn = T * (1.0f - alpha);
+        if (Tn < P->t_min) break;
+        const float w = alpha * T;
+        const double* c = nullptr;
+        double cd[3] = {rc.rgb[i * 3], rc.rgb[i * 3 + 1], rc.rgb[i * 3 + 2]};
+        c = cd;
+        for (int q = 0; q < 3; ++q) Cacc[q] += (double)w * c[q];
+        Dacc += (double)w * rc.z[i];
+        const double om = 1.0 - (double)alpha;
+        double dLda = 0.0;
+        for (int q = 0; q < 3; ++q) dLda += gC[q] * ((double)T * c[q] - (f.C[q] - Cacc[q]) / om);
+        dLda += gD * ((double)T * rc.z[i] - (f.Dz - Dacc) / om);
+        dLda += gA * (Tf / om);
+        double* g = grec + (int64_t)i * 10;
+        for (int q = 0; q < 3; ++q) g[6 + q] += (double)w * gC[q];
+        g[9] += (double)w * gD;
+        if (araw <= P->alpha_max) {   // unclamped: alpha = o 2^p
+            g[5] += dLda * e2p;
+            const double dLdp = dLda * (double)araw * 0.69314718055994530942;
+            const double ddx = dx, ddy = dy;
+            g[2] += dLdp * ddx * ddx;
+            g[3] += dLdp * ddx * ddy;
+            g[4] += dLdp * ddy * ddy;
+            g[0] += dLdp * (2.0 * ea * ddx + eb * ddy);
+            g[1] += dLdp * (eb * ddx + 2.0 * ec * ddy);
+        }
+        T = Tn;
+    }
+    return gC[0] * f.C[0] + gC[1] * f.C[1] + gC[2] * f.C[2] + gD * f.Dz + gA * (1.0 - Tf);
+}
+
+double oracle_radiance_backward(const or_view* V, const or_params* P, const float* u, const float* v,
+                                const float* conic, const float* opac, const float* rgb, const float* z,
+                                const int32_t* gid, const uint32_t* key_rec, const uint32_t* ranges,
+                                const float* gC /*[3][H][W]*/, const float* gD, const float* gA, double* grec) {
+    Records rc{u, v, conic, opac, rgb, z, gid, nullptr, 0};
+    const int32_t W = V->width, H = V->height, TX = (W + 15) / 16;
+    const int64_t HW = (int64_t)W * H;
+    double loss = 0.0;
+    for (int32_t py = 0; py < H; ++py)
+        for (int32_t px = 0; px < W; ++px) {
+            const int64_t t = (int64_t)(py / 16) * TX + px / 16, pix = (int64_t)py * W + px;
+            const uint32_t s = ranges[t * 2], e = ranges[t * 2 + 1];
+            const double g3[3] = {gC[pix], gC[HW + pix], gC[2 * HW + pix]};
+            loss += backward_pixel(rc, P, px, py, key_rec + s, (int64_t)e - s, g3, gD[pix], gA[pix], grec);
+        }
+    return loss;
+}
+
 // Brute force (the plain definition): per pixel, scan ALL projected records,
 // keep those whose tile rectangle contains the pixel's tile, order them by
 // (depth_bits, gid) with a plain comparator, composite.

@@ -53,3 +53,80 @@ def test_feature_grad_same_in_square_and_tight_binning(orc):
     o2 = orc.render(sc, v, binning="tight")
     b = orc.feature_grad(v, o2["rec"], o2["keys"], sc.feat, g.astype(np.float32), sc.n)
     np.testing.assert_array_equal(a, b)
+
+
+# ------------------------------------------------------------------ radiance backward
+K2 = np.float32(-0.72134752044448170368)
+
+
+def _loss(orc, v, rec, keys, gC, gD, gA):
+    return orc.radiance_backward(v, rec, keys, gC, gD, gA)[1]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_radiance_grad_rgb_and_depth_exact_linearity(orc, seed):
+    """C and Dz are linear in each record's rgb and z (weights unaffected):
+    central differences equal the gradient on any scene."""
+    rng = np.random.default_rng(60 + seed)
+    sc = random_tiny_scene(rng, 150, sh_degree=seed % 4)
+    v = synth.make_view(np.eye(3), np.zeros(3), 40.0, 40.0, 23.5, 17.5, 48, 36)
+    o = orc.render(sc, v)
+    rec, keys = o["rec"], o["keys"]
+    gC = rng.standard_normal((3, 36, 48)).astype(np.float32)
+    gD = rng.standard_normal((36, 48)).astype(np.float32)
+    gA = rng.standard_normal((36, 48)).astype(np.float32)
+    grad, _ = orc.radiance_backward(v, rec, keys, gC, gD, gA)
+    hit = np.nonzero(np.abs(grad[:, 6:]).sum(1) > 0)[0]
+    assert len(hit) > 5
+    for i in rng.choice(hit, 5, replace=False):
+        for f, (field, col) in enumerate((("rgb", 0), ("rgb", 1), ("rgb", 2), ("z", None))):
+            r2 = {k: np.array(a, copy=True) for k, a in rec.items() if isinstance(a, np.ndarray)}
+            r3 = {k: np.array(a, copy=True) for k, a in rec.items() if isinstance(a, np.ndarray)}
+            h = 0.25
+            if col is None:
+                r2[field][i] += h; r3[field][i] -= h
+            else:
+                r2[field][i, col] += h; r3[field][i, col] -= h
+            fd = (_loss(orc, v, r2, keys, gC, gD, gA) - _loss(orc, v, r3, keys, gC, gD, gA)) / (2 * h)
+            np.testing.assert_allclose(fd, grad[i, 6 + f], rtol=1e-6, atol=1e-9)
+
+
+def _smooth_fixture():
+    """Three large layered Gaussians over a 24x20 image: no alpha >= 1/255 boundary,
+    clamp or stop crosses a pixel under small perturbations -- the loss is smooth."""
+    from helpers import scene_of
+    sc = scene_of([{"mu": [0.1, -0.05, 5.0], "scale": 1.2, "opacity": 0.5},
+                   {"mu": [-0.2, 0.1, 5.5], "scale": 1.5, "opacity": 0.4},
+                   {"mu": [0.05, 0.2, 6.0], "scale": 1.8, "opacity": 0.6}])
+    v = synth.make_view(np.eye(3), np.zeros(3), 20.0, 20.0, 11.5, 9.5, 24, 20)
+    return sc, v
+
+
+@pytest.mark.parametrize("field", ["u", "v", "conic0", "conic1", "conic2", "opacity"])
+def test_radiance_grad_geometry_finite_differences(orc, field):
+    sc, v = _smooth_fixture()
+    o = orc.render(sc, v)
+    assert (o["flags"] == 0).all()
+    rec, keys = o["rec"], o["keys"]
+    rng = np.random.default_rng(7)
+    gC = rng.standard_normal((3, 20, 24)).astype(np.float32)
+    gD = rng.standard_normal((20, 24)).astype(np.float32)
+    gA = rng.standard_normal((20, 24)).astype(np.float32)
+    grad, _ = orc.radiance_backward(v, rec, keys, gC, gD, gA)
+    for i in range(len(rec["gid"])):
+        r2 = {k: np.array(a, copy=True) for k, a in rec.items() if isinstance(a, np.ndarray)}
+        r3 = {k: np.array(a, copy=True) for k, a in rec.items() if isinstance(a, np.ndarray)}
+        if field.startswith("conic"):
+            c = int(field[-1])
+            # conic ~0.03, p depends on it through dx^2 (<= 144 px^2): a small step keeps the
+            # central difference's truncation error ~1e-3; the fp32 alpha noise is ~1e-5
+            h = 1e-4
+            r2["conic"][i, c] += h; r3["conic"][i, c] -= h
+            # chain through e = k conic (e_b = 2k conic_b)
+            an = grad[i, 2 + c] * float(K2) * (2.0 if c == 1 else 1.0)
+        else:
+            h = 1e-2
+            r2[field][i] += h; r3[field][i] -= h
+            an = grad[i, {"u": 0, "v": 1, "opacity": 5}[field]]
+        fd = (_loss(orc, v, r2, keys, gC, gD, gA) - _loss(orc, v, r3, keys, gC, gD, gA)) / (2 * h)
+        assert abs(fd - an) <= 5e-3 * max(abs(an), 1e-3), (i, fd, an)
