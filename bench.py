@@ -458,9 +458,24 @@ def main():
         b1.record(stream)
         torch.cuda.synchronize()
         ms4 = b0.elapsed_time(b1) / Kb
-        n4 = {"views": n_views, "ms": ms4, "ms_per_view": ms4 / n_views, "mpix_per_s": total_px / ms4 / 1e3,
-              "feat_dim": scene.feat_dim, "gpu_launches": 2}
-        del gimg, gfeat
+        # radiance backward: random upstream gradients of RGB, depth, opacity
+        gout = G.Images(total_px, 0, device=dev)
+        for t in (gout.rgb, gout.depth, gout.alpha):
+            t.normal_(generator=g4)
+        grec = torch.zeros(n_views * r.proj.rec_capacity * 10, dtype=torch.float32, device=dev)
+        G.gs_radiance_backward(r.proj, r.bins, r.vb, r.params, r.images, gout, grec, stream)
+        torch.cuda.synchronize()
+        b0.record(stream)
+        for _ in range(Kb):
+            grec.zero_()
+            G.gs_radiance_backward(r.proj, r.bins, r.vb, r.params, r.images, gout, grec, stream)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        msr = b0.elapsed_time(b1) / Kb
+        n4 = {"views": n_views, "feature_backward_ms": ms4, "feature_backward_ms_per_view": ms4 / n_views,
+              "radiance_backward_ms": msr, "radiance_backward_ms_per_view": msr / n_views,
+              "feat_dim": scene.feat_dim, "gpu_launches": 4}
+        del gimg, gfeat, gout, grec
 
     # N2 refinement loop: B queries, n = 3 rounds, one CUDA graph
     refine = None

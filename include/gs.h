@@ -361,6 +361,20 @@ gs_status gs_feature_backward(const gs_scene* scene, const gs_projected* proj, c
                               const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
                               const gs_params* params, const float* grad_image, float* grad_feat, void* stream);
 
+/*
+ * N4 radiance backward: for the batch rendered with proj /
+ * bins / views (fwd = its gs_images), the gradient of
+ * L = sum_px gC . C + gD Dz + gA A  (grad_out = dL/d{rgb, depth, alpha} in the
+ * gs_images layout; its feat is ignored) w.r.t. each record's
+ * {u, v, ea, eb, ec, opacity, r, g, b, z}: grad_rec [n_views * rec_capacity][10]
+ * f32, accumulated (caller zeroes), indexed by record slot like proj->contrib.
+ * The skip / stop decisions are the forward's (zero gradient through them);
+ * an alpha clamped at alpha_max has no opacity / exponent gradient.
+ */
+gs_status gs_radiance_backward(const gs_projected* proj, const gs_bins* bins, const gs_view* views_host,
+                               const gs_view* views_dev, int32_t n_views, const gs_params* params,
+                               const gs_images* fwd, const gs_images* grad_out, float* grad_rec, void* stream);
+
 /* Eq. 2's L1 feature loss: grad_image[i] = scale * sign(rendered[i] - target[i]);
  * *loss (device double, accumulated) += scale * sum |rendered - target|. */
 gs_status gs_feature_l1_grad(const float* rendered, const float* target, int64_t n, float scale,

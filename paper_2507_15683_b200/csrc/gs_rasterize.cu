@@ -852,6 +852,159 @@ gs_status launch_backward(const gs_projected* proj, const gs_bins* bins, const g
     return check_launch("feature_backward_kernel");
 }
 
+// Radiance backward: per record slot, the gradient of
+// L = sum_px gC . C + gD Dz + gA A w.r.t. {u, v, ea, eb, ec, opacity, r, g, b, z},
+// front to back from the forward's outputs (no division by T):
+//   dC/dalpha_k = T_k c_k - (C_f - C_<=k) / (1 - alpha_k),  dA/dalpha_k = T_f / (1 - alpha_k).
+// Same tile / chunk / warp structure as the feature backward; the 10 per-pixel
+// terms of each walked entry are warp-reduced, summed over the warps in shared
+// memory and flushed with one global atomic per (entry, field) per chunk.
+constexpr int NGRAD = 10;
+
+__global__ void __launch_bounds__(256)
+radiance_backward_kernel(const gs_view* __restrict__ views, int n_views, const gs_record* __restrict__ rec,
+                         const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ ranges, gs_params P,
+                         const float* __restrict__ img_rgb, const float* __restrict__ img_depth,
+                         const float* __restrict__ img_alpha, const float* __restrict__ g_rgb,
+                         const float* __restrict__ g_depth, const float* __restrict__ g_alpha,
+                         float* __restrict__ grec, const uint32_t* __restrict__ status) {
+    if (*status) return;
+    __shared__ float4 srec[BW_CHUNK + 1][3];
+    __shared__ uint32_t sslot[BW_CHUNK];
+    __shared__ float acc[BW_CHUNK][NGRAD + 1];
+    __shared__ int ent[8][2 * 32 + 2];
+    const uint32_t tile = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int vi = find_view_by_tile(views, n_views, tile);
+    const gs_view& V = views[vi];
+    const int W = V.width, H = V.height, TX = (W + GS_TILE - 1) / GS_TILE;
+    const uint32_t lt = tile - V.tile_offset;
+    const int sx = (int)(lt % (uint32_t)TX) * 16 + (warp & 1) * 8, sy = (int)(lt / (uint32_t)TX) * 16 + (warp >> 1) * 4;
+    const int px = sx + (lane & 7), py = sy + (lane >> 3);
+    const bool inside = px < W && py < H;
+    const float pxf = (float)px, pyf = (float)py;
+    const float rx0 = (float)sx, rx1 = (float)(sx + 7), ry0 = (float)sy, ry1 = (float)(sy + 3);
+    const int64_t HW = (int64_t)W * H, po = V.pix_offset, loc = (int64_t)py * W + px;
+    float Cf[3] = {0.f, 0.f, 0.f}, Df = 0.f, Tf = 1.f, gC[3] = {0.f, 0.f, 0.f}, gD = 0.f, gA = 0.f;
+    if (inside) {
+        for (int q = 0; q < 3; ++q) {
+            Cf[q] = __ldg(&img_rgb[3 * po + q * HW + loc]);
+            gC[q] = __ldg(&g_rgb[3 * po + q * HW + loc]);
+        }
+        Df = __ldg(&img_depth[po + loc]);
+        Tf = 1.0f - __ldg(&img_alpha[po + loc]);
+        gD = __ldg(&g_depth[po + loc]);
+        gA = __ldg(&g_alpha[po + loc]);
+    }
+    for (int i = tid; i < BW_CHUNK * (NGRAD + 1); i += 256) (&acc[0][0])[i] = 0.f;
+    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Dz = 0.f;
+    bool done = !inside;
+    bool warp_done = __all_sync(0xffffffffu, done);
+    const uint32_t rs = ranges[2 * tile], re = ranges[2 * tile + 1];
+    __syncthreads();
+    for (uint32_t c0 = rs; c0 < re; c0 += BW_CHUNK) {
+        const int cnt = (int)min((uint32_t)BW_CHUNK, re - c0);
+        for (int i = tid; i < 3 * cnt; i += 256) {
+            const uint32_t slot = __ldg(&sorted_rec[c0 + i / 3]);
+            srec[i / 3][i % 3] = __ldg(reinterpret_cast<const float4*>(rec + slot) + (i % 3));
+            if (i % 3 == 0) sslot[i / 3] = slot;
+        }
+        __syncthreads();
+        if (!warp_done) {
+            bool hit[2] = {false, false};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = lane + 32 * h;
+                if (j < cnt) {
+                    const float4 a = srec[j][0], b = srec[j][1];
+                    hit[h] = ellipse_hits_rect(a.x, a.y, a.z, a.w, b.x, b.z, rx0, rx1, ry0, ry1);
+                }
+            }
+            const uint32_t m0 = __ballot_sync(0xffffffffu, hit[0]), m1 = __ballot_sync(0xffffffffu, hit[1]);
+            const int n0 = __popc(m0), n = n0 + __popc(m1);
+            const uint32_t below = (1u << lane) - 1u;
+            if (hit[0]) ent[warp][__popc(m0 & below)] = lane;
+            if (hit[1]) ent[warp][n0 + __popc(m1 & below)] = lane + 32;
+            __syncwarp();
+            for (int i = 0; i < n; ++i) {
+                const int k = ent[warp][i];
+                const float4 a4 = srec[k][0], b4 = srec[k][1], c4 = srec[k][2];
+                // the forward's exponent / alpha (entry_alpha), keeping 2^p and the raw alpha
+                const float dx = __fsub_rn(a4.x, pxf), dy = __fsub_rn(a4.y, pyf);
+                const float p = __fmaf_rn(dx, __fmaf_rn(a4.z, dx, __fmul_rn(a4.w, dy)), __fmul_rn(__fmul_rn(b4.x, dy), dy));
+                const float e2p = ex2_ftz(p);
+                const float araw = __fmul_rn(b4.y, e2p);
+                float alpha = fminf(P.alpha_max, araw);
+                alpha = ((p > 0.0f) || (alpha < P.alpha_min) || done) ? 0.0f : alpha;
+                const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+                const bool stop = Tn < P.t_min;
+                const float wgt = stop ? 0.0f : __fmul_rn(alpha, T);
+                float g[16];   // NGRAD fields, padded for the halving reduction
+#pragma unroll
+                for (int q = 0; q < 16; ++q) g[q] = 0.f;
+                const bool blended = wgt > 0.f;
+                if (blended) {
+                    C0 = fmaf(wgt, c4.x, C0); C1 = fmaf(wgt, c4.y, C1); C2 = fmaf(wgt, c4.z, C2); Dz = fmaf(wgt, c4.w, Dz);
+                    const float iom = __frcp_rn(1.0f - alpha);
+                    const float dLda = gC[0] * (T * c4.x - (Cf[0] - C0) * iom) + gC[1] * (T * c4.y - (Cf[1] - C1) * iom) +
+                                       gC[2] * (T * c4.z - (Cf[2] - C2) * iom) + gD * (T * c4.w - (Df - Dz) * iom) +
+                                       gA * (Tf * iom);
+                    g[6] = wgt * gC[0]; g[7] = wgt * gC[1]; g[8] = wgt * gC[2]; g[9] = wgt * gD;
+                    if (araw <= P.alpha_max) {
+                        g[5] = dLda * e2p;
+                        const float dLdp = dLda * araw * 0.6931471805599453f;
+                        g[2] = dLdp * dx * dx; g[3] = dLdp * dx * dy; g[4] = dLdp * dy * dy;
+                        g[0] = dLdp * (2.f * a4.z * dx + a4.w * dy);
+                        g[1] = dLdp * (a4.w * dx + 2.f * b4.x * dy);
+                    }
+                }
+                T = stop ? T : Tn;
+                done = done || stop;
+                if (!__any_sync(0xffffffffu, blended)) continue;
+                // halving butterfly: 16 values over 32 lanes in 16 shuffles; afterwards lanes
+                // 2q and 2q + 1 hold the warp sum of field q
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const bool up = lane & 16;
+                    const float send = up ? g[j] : g[j + 8], keep = up ? g[j + 8] : g[j];
+                    g[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const bool up = lane & 8;
+                    const float send = up ? g[j] : g[j + 4], keep = up ? g[j + 4] : g[j];
+                    g[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                }
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const bool up = lane & 4;
+                    const float send = up ? g[j] : g[j + 2], keep = up ? g[j + 2] : g[j];
+                    g[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+                }
+                {
+                    const bool up = lane & 2;
+                    const float send = up ? g[0] : g[1], keep = up ? g[1] : g[0];
+                    g[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+                }
+                g[0] += __shfl_xor_sync(0xffffffffu, g[0], 1);
+                const int q = lane >> 1;
+                if ((lane & 1) == 0 && q < NGRAD && g[0] != 0.f) atomicAdd(&acc[k][q], g[0]);
+            }
+            warp_done = __all_sync(0xffffffffu, done);
+        }
+        __syncthreads();
+        for (int i = tid; i < cnt * NGRAD; i += 256) {
+            const int e = i / NGRAD, q = i % NGRAD;
+            const float v = acc[e][q];
+            if (v != 0.f) {
+                atomicAdd(&grec[(int64_t)sslot[e] * NGRAD + q], v);
+                acc[e][q] = 0.f;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // N4 training helpers: L1 loss of Eq. 2 and a plain gradient step
 __global__ void l1_grad_kernel(const float* __restrict__ F, const float* __restrict__ Ft, int64_t n, float scale,
                                float* __restrict__ gF, double* __restrict__ loss) {
@@ -993,4 +1146,22 @@ extern "C" gs_status gs_feature_sgd(float* feat, const float* grad_feat, int64_t
     sgd_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(feat, grad_feat, n, lr,
                                                                    reinterpret_cast<__half*>(feat_h));
     return check_launch("sgd_kernel");
+}
+
+extern "C" gs_status gs_radiance_backward(const gs_projected* proj, const gs_bins* bins, const gs_view* views_host,
+                                          const gs_view* views_dev, int32_t n_views, const gs_params* params,
+                                          const gs_images* fwd, const gs_images* grad_out, float* grad_rec,
+                                          void* stream) {
+    int64_t total_pixels = 0, T = 0;
+    gs_status st = validate_views(views_host, views_dev, n_views, &total_pixels, &T);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(params && proj && proj->rec && proj->status && bins && bins->ranges && bins->sorted_rec && fwd &&
+                   fwd->rgb && fwd->depth && fwd->alpha && grad_out && grad_out->rgb && grad_out->depth &&
+                   grad_out->alpha && grad_rec,
+               GS_INVALID_ARG, "gs_radiance_backward: NULL pointer");
+    if (T <= 0) return GS_OK;
+    radiance_backward_kernel<<<(unsigned)T, 256, 0, (cudaStream_t)stream>>>(
+        views_dev, n_views, proj->rec, bins->sorted_rec, bins->ranges, *params, fwd->rgb, fwd->depth, fwd->alpha,
+        grad_out->rgb, grad_out->depth, grad_out->alpha, grad_rec, proj->status);
+    return check_launch("radiance_backward_kernel");
 }

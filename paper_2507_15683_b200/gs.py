@@ -70,7 +70,7 @@ class gs_images(ctypes.Structure):
 
 EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_layout", "gs_scene_block_bounds",
            "gs_scene_features_f16", "gs_validate_scene", "gs_match", "gs_match_workspace_bytes",
-           "gs_pnp", "gs_pnp_workspace_bytes", "gs_verify_consistency", "gs_feature_backward",
+           "gs_pnp", "gs_pnp_workspace_bytes", "gs_verify_consistency", "gs_feature_backward", "gs_radiance_backward",
            "gs_feature_l1_grad", "gs_feature_sgd",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_backproject", "gs_visibility_score", "gs_visibility_workspace_bytes"]
@@ -471,3 +471,15 @@ def gs_feature_sgd(feat: torch.Tensor, grad_feat: torch.Tensor, lr: float, feat_
                    stream=None):
     _check(lib().gs_feature_sgd(_ptr(feat), _ptr(grad_feat), ctypes.c_int64(feat.numel()), ctypes.c_float(lr),
                                 _ptr(feat_h), _stream(stream)), "gs_feature_sgd")
+
+
+GRAD_FIELDS = ("u", "v", "ea", "eb", "ec", "opacity", "r", "g", "b", "z")
+
+
+def gs_radiance_backward(proj: "Projected", bins: "Bins", views, params: gs_params, fwd: "Images",
+                         grad_out: "Images", grad_rec: torch.Tensor, stream=None):
+    """grad_rec: [n_views * rec_capacity * 10] f32 (GRAD_FIELDS per record slot), accumulated."""
+    _check(lib().gs_radiance_backward(ctypes.byref(proj.struct), ctypes.byref(bins.struct), views.host, views.dev_ptr,
+                                      ctypes.c_int32(views.n), ctypes.byref(params), ctypes.byref(fwd.struct),
+                                      ctypes.byref(grad_out.struct), _ptr(grad_rec), _stream(stream)),
+           "gs_radiance_backward")
