@@ -1,0 +1,91 @@
+"""CPU oracle of N4's projection backward -- TEST INFRASTRUCTURE (see
+oracle/__init__.py for who may import it).  numpy, float64.
+
+Chains the per-record 2D gradients of `oracle.radiance_backward`
+(dL/d{u, v, e_a, e_b, e_c, z}) through the forward projection O1-O7 to the
+Gaussian's 3D mean (Alg. 1 l.10-14; the EWA Jacobian of O5 with
+the off-screen clamp of reading Q6; the conic of O6; the exponent
+coefficients e = k * conic of reading Q29):
+
+  p = R mu + t;  u = fx px/pz + cx,  v = fy py/pz + cy;  z = pz
+  J = [[fx/pz, 0, -fx xc/pz^2], [0, fy/pz, -fy yc/pz^2]],  xc = clamp(px/pz) pz
+  Sigma' = (J R) Sigma (J R)^T + dilation I = [[a, b], [b, c]]
+  conic = (c, -b, a) / (a c - b^2);  (e_a, e_b, e_c) = (k c_a, 2k c_b, k c_c)
+
+dL/dmu = R^T dL/dp.  Alg. 1's literal render-gradient test is
+||dL/dmu|| > 0 for L = the sum of the rendered colour.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+K = float(np.float32(-0.72134752044448170368))   # reading Q29 (fp32 constant)
+
+
+def _sigma3(scale, quat):
+    w, x, y, z = (float(q) for q in quat)
+    n = np.sqrt(w * w + x * x + y * y + z * z)
+    w, x, y, z = w / n, x / n, y / n, z / n
+    Rq = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                   [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                   [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+    M = Rq @ np.diag(np.asarray(scale, np.float64))
+    return M @ M.T
+
+
+def mean_backward(scene, view, rec, grec, params) -> np.ndarray:
+    """dL/dmu [cnt][3] (fp64) for each record; grec [cnt][10] from radiance_backward."""
+    R = np.asarray(view.R, np.float64).reshape(3, 3)
+    t = np.asarray(view.t, np.float64).reshape(3)
+    fx, fy, cx, cy = float(view.fx), float(view.fy), float(view.cx), float(view.cy)
+    W, H = view.width, view.height
+    m = float(params.clamp_margin)
+    lox, hix = (-(m * W) - cx) / fx, ((1.0 + m) * W - cx) / fx
+    loy, hiy = (-(m * H) - cy) / fy, ((1.0 + m) * H - cy) / fy
+    dil = float(params.dilation)
+    out = np.zeros((len(rec["gid"]), 3))
+    for r, g in enumerate(rec["gid"]):
+        mu = scene.pos[:, g].astype(np.float64)
+        p = R @ mu + t
+        px, py, pz = p
+        Sg = _sigma3(scene.scale[:, g], scene.quat[:, g])
+        xn, yn = px / pz, py / pz
+        xcl, ycl = min(max(xn, lox), hix), min(max(yn, loy), hiy)
+        j00, j11 = fx / pz, fy / pz
+        j02, j12 = -fx * xcl / pz, -fy * ycl / pz          # = -fx xc / pz^2 with xc = xcl pz
+        T0 = j00 * R[0] + j02 * R[2]
+        T1 = j11 * R[1] + j12 * R[2]
+        a = T0 @ Sg @ T0 + dil
+        b = T0 @ Sg @ T1
+        c = T1 @ Sg @ T1 + dil
+        det = a * c - b * b
+        gu, gv, gea, geb, gec, _, _, _, _, gz = grec[r]
+        gca, gcb, gcc = K * gea, 2.0 * K * geb, K * gec
+        # conic = (c, -b, a) / det
+        d2 = det * det
+        ga = gca * (-c * c / d2) + gcb * (b * c / d2) + gcc * (1.0 / det - a * c / d2)
+        gb = gca * (2.0 * b * c / d2) + gcb * (-1.0 / det - 2.0 * b * b / d2) + gcc * (2.0 * a * b / d2)
+        gc = gca * (1.0 / det - c * a / d2) + gcb * (b * a / d2) + gcc * (-a * a / d2)
+        dT0 = 2.0 * ga * (Sg @ T0) + gb * (Sg @ T1)
+        dT1 = gb * (Sg @ T0) + 2.0 * gc * (Sg @ T1)
+        gj00, gj02 = dT0 @ R[0], dT0 @ R[2]
+        gj11, gj12 = dT1 @ R[1], dT1 @ R[2]
+        gp = np.zeros(3)
+        # u, v, z
+        gp[0] += gu * fx / pz
+        gp[1] += gv * fy / pz
+        gp[2] += -gu * fx * px / (pz * pz) - gv * fy * py / (pz * pz) + gz
+        # J entries
+        gp[2] += gj00 * (-fx / (pz * pz)) + gj11 * (-fy / (pz * pz))
+        if lox < xn < hix:          # j02 = -fx px / pz^2
+            gp[0] += gj02 * (-fx / (pz * pz))
+            gp[2] += gj02 * (2.0 * fx * px / pz ** 3)
+        else:                       # j02 = -fx L / pz (L the clamp bound)
+            gp[2] += gj02 * (fx * xcl / (pz * pz))
+        if loy < yn < hiy:
+            gp[1] += gj12 * (-fy / (pz * pz))
+            gp[2] += gj12 * (2.0 * fy * py / pz ** 3)
+        else:
+            gp[2] += gj12 * (fy * ycl / (pz * pz))
+        out[r] = R.T @ gp
+    return out

@@ -3,6 +3,8 @@ Eq. 2 with the geometry frozen, dL/df_g = sum_px w_g(px) dL/dF(px).
 Pins: exact linearity (a finite difference of the linear loss <g, F(f)> in f
 equals the gradient to fp64 rounding), the sum identity sum_g dL/df_g = sum_px
 A(px) g(px) (sum_k w_k = A), and binning-mode invariance."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -130,3 +132,65 @@ def test_radiance_grad_geometry_finite_differences(orc, field):
             an = grad[i, {"u": 0, "v": 1, "opacity": 5}[field]]
         fd = (_loss(orc, v, r2, keys, gC, gD, gA) - _loss(orc, v, r3, keys, gC, gD, gA)) / (2 * h)
         assert abs(fd - an) <= 5e-3 * max(abs(an), 1e-3), (i, fd, an)
+
+
+# ------------------------------------------------------------------ projection backward (dL/dmu)
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_mean_grad_finite_differences(orc, axis):
+    """dL/dmu (oracle/backward.py chaining the record gradients through O1-O7)
+    equals central differences of the whole pipeline (project -> bin -> composite)
+    on the smooth fixture."""
+    from oracle import backward as OB
+    sc, v = _smooth_fixture()
+    rng = np.random.default_rng(11)
+    gC = rng.standard_normal((3, 20, 24)).astype(np.float32)
+    gD = rng.standard_normal((20, 24)).astype(np.float32)
+    gA = rng.standard_normal((20, 24)).astype(np.float32)
+    P = orc.Params()
+
+    def loss(scene):
+        rec = orc.project(scene, v, P)
+        keys = orc.bin_keys(rec, v)
+        return orc.radiance_backward(v, rec, keys, gC, gD, gA, P)[1]
+
+    rec = orc.project(sc, v, P)
+    keys = orc.bin_keys(rec, v)
+    grec, _ = orc.radiance_backward(v, rec, keys, gC, gD, gA, P)
+    gmu = OB.mean_backward(sc, v, rec, grec, P)
+    h = 1e-2
+    for r, g in enumerate(rec["gid"]):
+        s2, s3 = dataclasses.replace(sc, pos=sc.pos.copy()), dataclasses.replace(sc, pos=sc.pos.copy())
+        s2.pos[axis, g] += h
+        s3.pos[axis, g] -= h
+        fd = (loss(s2) - loss(s3)) / (2 * h)
+        assert abs(fd - gmu[r, axis]) <= 5e-3 * max(abs(gmu[r, axis]), 1e-2), (r, fd, gmu[r, axis])
+
+
+def test_mean_grad_with_clamped_jacobian(orc):
+    """A Gaussian far outside the frustum's x range (clamped J, reading Q6) whose
+    footprint still reaches the image: the clamp branch of the chain."""
+    from helpers import scene_of
+    from oracle import backward as OB
+    sc = scene_of([{"mu": [-6.0, 0.0, 5.0], "scale": 3.0, "opacity": 0.6}])
+    v = synth.make_view(np.eye(3), np.zeros(3), 20.0, 20.0, 11.5, 9.5, 24, 20)
+    P = orc.Params()
+    rec = orc.project(sc, v, P)
+    assert len(rec["gid"]) == 1
+    xn = -6.0 / 5.0
+    assert xn < (-(0.15 * 24) - 11.5) / 20.0               # clamped
+    rng = np.random.default_rng(12)
+    gC = rng.standard_normal((3, 20, 24)).astype(np.float32)
+    z = np.zeros((20, 24), np.float32)
+
+    def loss(scene):
+        r = orc.project(scene, v, P)
+        return orc.radiance_backward(v, r, orc.bin_keys(r, v), gC, z, z, P)[1]
+
+    grec, _ = orc.radiance_backward(v, rec, orc.bin_keys(rec, v), gC, z, z, P)
+    gmu = OB.mean_backward(sc, v, rec, grec, P)
+    for axis in range(3):
+        s2, s3 = dataclasses.replace(sc, pos=sc.pos.copy()), dataclasses.replace(sc, pos=sc.pos.copy())
+        s2.pos[axis, 0] += 1e-2
+        s3.pos[axis, 0] -= 1e-2
+        fd = (loss(s2) - loss(s3)) / 2e-2
+        assert abs(fd - gmu[0, axis]) <= 5e-3 * max(abs(gmu[0, axis]), 1e-2), (axis, fd, gmu[0, axis])
