@@ -375,6 +375,18 @@ gs_status gs_radiance_backward(const gs_projected* proj, const gs_bins* bins, co
                                const gs_view* views_dev, int32_t n_views, const gs_params* params,
                                const gs_images* fwd, const gs_images* grad_out, float* grad_rec, void* stream);
 
+/*
+ * N4 projection backward: chains grad_rec (from gs_radiance_backward, same
+ * proj) through O1-O7 -- pinhole u, v and depth z, the clamped EWA Jacobian
+ * (Q6), the 2D covariance, its inverse and e = k conic (Q29) -- to the
+ * Gaussians' 3D means: grad_pos [3][n] (the layout of gs_scene.pos) +=
+ * dL/dmu, fp64 arithmetic, f32 atomics.  Alg. 1's literal render-gradient
+ * visibility test is ||dL/dmu|| > 0 for a loss on the render.
+ */
+gs_status gs_mean_backward(const gs_scene* scene, const gs_projected* proj, const gs_view* views_host,
+                           const gs_view* views_dev, int32_t n_views, const gs_params* params,
+                           const float* grad_rec, float* grad_pos, void* stream);
+
 /* Eq. 2's L1 feature loss: grad_image[i] = scale * sign(rendered[i] - target[i]);
  * *loss (device double, accumulated) += scale * sum |rendered - target|. */
 gs_status gs_feature_l1_grad(const float* rendered, const float* target, int64_t n, float scale,

@@ -460,6 +460,88 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
     }
 }
 
+// ---------------------------------------------------------------- N4: projection backward
+// dL/dmu for every record from its 2D gradients (gs_radiance_backward's grad_rec:
+// u, v, ea, eb, ec, ..., z) through O1-O7: p = R mu + t; u, v
+// pinhole; J(p) with the Q6 clamp; Sigma' = (J R) Sigma (J R)^T + dilation I;
+// conic = (c, -b, a)/det; e = k conic.  fp64 (per-record work is small);
+// accumulated into grad_pos [3][n] (the layout of gs_scene.pos) with atomics.
+__global__ void mean_backward_kernel(gs_scene S, const gs_view* __restrict__ views, gs_params P,
+                                     const gs_record* __restrict__ rec, int64_t cap,
+                                     const uint32_t* __restrict__ n_rec, int n_views,
+                                     const float* __restrict__ grad_rec, float* __restrict__ grad_pos) {
+    const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (slot >= cap * n_views) return;
+    const int vi = (int)(slot / cap);
+    if ((uint32_t)(slot - (int64_t)vi * cap) >= min((uint64_t)n_rec[vi], (uint64_t)cap)) return;
+    const float* gr = grad_rec + slot * 10;
+    const double gu = gr[0], gv = gr[1], gea = gr[2], geb = gr[3], gec = gr[4], gz = gr[9];
+    if (gu == 0.0 && gv == 0.0 && gea == 0.0 && geb == 0.0 && gec == 0.0 && gz == 0.0) return;
+    const int64_t n = S.n;
+    const uint32_t g = rec[slot].gid;
+    const gs_view& V = views[vi];
+    double R[9], t[3];
+    for (int k = 0; k < 9; ++k) R[k] = V.R[k];
+    for (int k = 0; k < 3; ++k) t[k] = V.t[k];
+    const double mx = S.pos[g], my = S.pos[n + g], mz = S.pos[2 * n + g];
+    const double px = R[0] * mx + R[1] * my + R[2] * mz + t[0];
+    const double py = R[3] * mx + R[4] * my + R[5] * mz + t[1];
+    const double pz = R[6] * mx + R[7] * my + R[8] * mz + t[2];
+    // Sigma = M M^T, M = R(q) diag(s)
+    double qw = S.quat[g], qx = S.quat[n + g], qy = S.quat[2 * n + g], qz = S.quat[3 * n + g];
+    const double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    qw /= qn; qx /= qn; qy /= qn; qz /= qn;
+    const double s0 = S.scale[g], s1 = S.scale[n + g], s2 = S.scale[2 * n + g];
+    const double Rq[9] = {1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qw * qz), 2 * (qx * qz + qw * qy),
+                          2 * (qx * qy + qw * qz), 1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qw * qx),
+                          2 * (qx * qz - qw * qy), 2 * (qy * qz + qw * qx), 1 - 2 * (qx * qx + qy * qy)};
+    double M[9];
+    for (int r = 0; r < 3; ++r) { M[r * 3] = Rq[r * 3] * s0; M[r * 3 + 1] = Rq[r * 3 + 1] * s1; M[r * 3 + 2] = Rq[r * 3 + 2] * s2; }
+    double Sg[9];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) Sg[r * 3 + c] = M[r * 3] * M[c * 3] + M[r * 3 + 1] * M[c * 3 + 1] + M[r * 3 + 2] * M[c * 3 + 2];
+    const double fx = V.fx, fy = V.fy, cx = V.cx, cy = V.cy, W = V.width, H = V.height, m = P.clamp_margin;
+    const double lox = (-(m * W) - cx) / fx, hix = ((1.0 + m) * W - cx) / fx;
+    const double loy = (-(m * H) - cy) / fy, hiy = ((1.0 + m) * H - cy) / fy;
+    const double xn = px / pz, yn = py / pz;
+    const double xcl = fmin(fmax(xn, lox), hix), ycl = fmin(fmax(yn, loy), hiy);
+    const double j00 = fx / pz, j11 = fy / pz, j02 = -fx * xcl / pz, j12 = -fy * ycl / pz;
+    double T0[3], T1[3], ST0[3], ST1[3];
+    for (int k = 0; k < 3; ++k) { T0[k] = j00 * R[k] + j02 * R[6 + k]; T1[k] = j11 * R[3 + k] + j12 * R[6 + k]; }
+    for (int r = 0; r < 3; ++r) {
+        ST0[r] = Sg[r * 3] * T0[0] + Sg[r * 3 + 1] * T0[1] + Sg[r * 3 + 2] * T0[2];
+        ST1[r] = Sg[r * 3] * T1[0] + Sg[r * 3 + 1] * T1[1] + Sg[r * 3 + 2] * T1[2];
+    }
+    const double a = T0[0] * ST0[0] + T0[1] * ST0[1] + T0[2] * ST0[2] + P.dilation;
+    const double b = T0[0] * ST1[0] + T0[1] * ST1[1] + T0[2] * ST1[2];
+    const double c = T1[0] * ST1[0] + T1[1] * ST1[1] + T1[2] * ST1[2] + P.dilation;
+    const double det = a * c - b * b, d2 = det * det;
+    const double K = (double)K_EXP2;
+    const double gca = K * gea, gcb = 2.0 * K * geb, gcc = K * gec;
+    const double ga = gca * (-c * c / d2) + gcb * (b * c / d2) + gcc * (1.0 / det - a * c / d2);
+    const double gb = gca * (2.0 * b * c / d2) + gcb * (-1.0 / det - 2.0 * b * b / d2) + gcc * (2.0 * a * b / d2);
+    const double gc = gca * (1.0 / det - c * a / d2) + gcb * (b * a / d2) + gcc * (-a * a / d2);
+    double dT0[3], dT1[3];
+    for (int k = 0; k < 3; ++k) {
+        dT0[k] = 2.0 * ga * ST0[k] + gb * ST1[k];
+        dT1[k] = gb * ST0[k] + 2.0 * gc * ST1[k];
+    }
+    const double gj00 = dT0[0] * R[0] + dT0[1] * R[1] + dT0[2] * R[2];
+    const double gj02 = dT0[0] * R[6] + dT0[1] * R[7] + dT0[2] * R[8];
+    const double gj11 = dT1[0] * R[3] + dT1[1] * R[4] + dT1[2] * R[5];
+    const double gj12 = dT1[0] * R[6] + dT1[1] * R[7] + dT1[2] * R[8];
+    const double z2 = pz * pz;
+    double gp0 = gu * fx / pz, gp1 = gv * fy / pz;
+    double gp2 = -gu * fx * px / z2 - gv * fy * py / z2 + gz - gj00 * fx / z2 - gj11 * fy / z2;
+    if (lox < xn && xn < hix) { gp0 += -gj02 * fx / z2; gp2 += gj02 * 2.0 * fx * px / (z2 * pz); }
+    else gp2 += gj02 * fx * xcl / z2;
+    if (loy < yn && yn < hiy) { gp1 += -gj12 * fy / z2; gp2 += gj12 * 2.0 * fy * py / (z2 * pz); }
+    else gp2 += gj12 * fy * ycl / z2;
+    // dL/dmu = R^T dL/dp
+    for (int k = 0; k < 3; ++k)
+        atomicAdd(&grad_pos[(int64_t)k * n + g], (float)(R[k] * gp0 + R[3 + k] * gp1 + R[6 + k] * gp2));
+}
+
 }  // namespace
 }  // namespace gs
 
@@ -525,3 +607,19 @@ gs_status gs_project(const gs_scene* scene, const gs_view* views_host, const gs_
 }
 
 }  // extern "C"
+
+extern "C" gs_status gs_mean_backward(const gs_scene* scene, const gs_projected* proj, const gs_view* views_host,
+                                      const gs_view* views_dev, int32_t n_views, const gs_params* params,
+                                      const float* grad_rec, float* grad_pos, void* stream) {
+    gs_status st = validate_scene(scene, true);
+    if (st != GS_OK) return st;
+    st = validate_views(views_host, views_dev, n_views, nullptr, nullptr);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(params && proj && proj->rec && proj->n_rec && grad_rec && grad_pos, GS_INVALID_ARG,
+               "gs_mean_backward: NULL pointer");
+    const int64_t total = proj->rec_capacity * (int64_t)n_views;
+    if (total == 0) return GS_OK;
+    mean_backward_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        *scene, views_dev, *params, proj->rec, proj->rec_capacity, proj->n_rec, n_views, grad_rec, grad_pos);
+    return check_launch("mean_backward_kernel");
+}

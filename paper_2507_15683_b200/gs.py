@@ -71,6 +71,7 @@ class gs_images(ctypes.Structure):
 EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_layout", "gs_scene_block_bounds",
            "gs_scene_features_f16", "gs_validate_scene", "gs_match", "gs_match_workspace_bytes",
            "gs_pnp", "gs_pnp_workspace_bytes", "gs_verify_consistency", "gs_feature_backward", "gs_radiance_backward",
+           "gs_mean_backward",
            "gs_feature_l1_grad", "gs_feature_sgd",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_backproject", "gs_visibility_score", "gs_visibility_workspace_bytes"]
@@ -483,3 +484,11 @@ def gs_radiance_backward(proj: "Projected", bins: "Bins", views, params: gs_para
                                       ctypes.c_int32(views.n), ctypes.byref(params), ctypes.byref(fwd.struct),
                                       ctypes.byref(grad_out.struct), _ptr(grad_rec), _stream(stream)),
            "gs_radiance_backward")
+
+
+def gs_mean_backward(scene: "DeviceScene", proj: "Projected", views, params: gs_params, grad_rec: torch.Tensor,
+                     grad_pos: torch.Tensor, stream=None):
+    """grad_pos: [3 * n] f32 (SoA like scene.pos), accumulated."""
+    _check(lib().gs_mean_backward(ctypes.byref(scene.struct), ctypes.byref(proj.struct), views.host, views.dev_ptr,
+                                  ctypes.c_int32(views.n), ctypes.byref(params), _ptr(grad_rec), _ptr(grad_pos),
+                                  _stream(stream)), "gs_mean_backward")

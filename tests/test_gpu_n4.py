@@ -141,3 +141,74 @@ def test_radiance_backward_c2_quarter(G, orc):
     sc, vs = synth.make_config("C2", scale=0.05)
     rng = np.random.default_rng(8)
     _radiance_case(G, orc, sc, vs, rng)
+
+
+# ------------------------------------------------------------------ projection backward + Alg. 1 literal
+def _mean_case(G, orc, sc, v, rng):
+    from oracle import backward as OB
+    ds = G.DeviceScene(sc)
+    r = G.Renderer(ds, [v], backproject=False, contrib=True)
+    r.render()
+    gout = G.Images(r.vb.total_pixels, 0)
+    ups = []
+    for t in (gout.rgb, gout.depth, gout.alpha):
+        a = rng.standard_normal(t.numel()).astype(np.float32)
+        t.copy_(torch.from_numpy(a))
+        ups.append(a)
+    cap = r.proj.rec_capacity
+    grec = torch.zeros(cap * 10, dtype=torch.float32, device="cuda")
+    G.gs_radiance_backward(r.proj, r.bins, r.vb, r.params, r.images, gout, grec)
+    gpos = torch.zeros(3 * sc.n, dtype=torch.float32, device="cuda")
+    G.gs_mean_backward(ds, r.proj, r.vb, r.params, grec, gpos)
+    torch.cuda.synchronize()
+    got = gpos.view(3, sc.n).cpu().numpy().astype(np.float64).T
+    o = orc.render(sc, v, binning="tight")
+    hw = v.width * v.height
+    P = orc.Params()
+    want_rec, _ = orc.radiance_backward(v, o["rec"], o["keys"], ups[0].reshape(3, v.height, v.width),
+                                        ups[1].reshape(v.height, v.width), ups[2].reshape(v.height, v.width), P)
+    want = np.zeros((sc.n, 3))
+    want[o["rec"]["gid"]] = OB.mean_backward(sc, v, o["rec"], want_rec, P)
+    scale = float(np.abs(want).max())
+    bad = (np.abs(got - want) > 5e-3 * scale + 1e-4).any(1)
+    flagged = int((o["flags"] != 0).sum())
+    assert bad.sum() <= (max(2, 0.02 * sc.n) if flagged else 0), (bad.sum(), flagged, scale)
+    assert scale > 0
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_mean_backward_vs_oracle(G, orc, seed):
+    rng = np.random.default_rng(500 + seed)
+    sc = random_tiny_scene(rng, int(rng.integers(50, 250)), sh_degree=seed % 4)
+    W, H = int(rng.integers(16, 90)), int(rng.integers(12, 70))
+    R = np.asarray(synth.look_from([0.3, -0.2, -0.5], [0.05, 0.03, 1.0])[0], np.float32)
+    t = np.asarray(synth.look_from([0.3, -0.2, -0.5], [0.05, 0.03, 1.0])[1], np.float32)
+    v = synth.make_view(R, t, 40.0, 40.0, W / 2 - 0.5, H / 2 - 0.5, W, H)
+    _mean_case(G, orc, sc, v, rng)
+
+
+def test_alg1_literal_render_gradient_matches_forward_criterion(G):
+    """Alg. 1: a Gaussian is visible iff the render's gradient w.r.t.
+    its position is non-zero.  With L = the sum of the rendered colour the literal
+    test agrees with the forward criterion sum w > 0 (reading Q28) except on
+    exact cancellations."""
+    sc, vs = synth.make_config("C2", scale=0.05)
+    ds = G.DeviceScene(sc)
+    r = G.Renderer(ds, vs, backproject=False, contrib=True)
+    r.render()
+    gout = G.Images(r.vb.total_pixels, 0)
+    gout.rgb.fill_(1.0)
+    gout.depth.zero_()
+    gout.alpha.zero_()
+    cap = r.proj.rec_capacity
+    grec = torch.zeros(cap * 10, dtype=torch.float32, device="cuda")
+    G.gs_radiance_backward(r.proj, r.bins, r.vb, r.params, r.images, gout, grec)
+    gpos = torch.zeros(3 * sc.n, dtype=torch.float32, device="cuda")
+    G.gs_mean_backward(ds, r.proj, r.vb, r.params, grec, gpos)
+    torch.cuda.synchronize()
+    n = int(r.proj.n_rec[0].item())
+    gid = r.proj.records()[:n, 12].cpu().numpy().view(np.uint32)
+    contrib = r.proj.contrib[:n].cpu().numpy().view(np.uint64) > 0
+    literal = np.linalg.norm(gpos.view(3, sc.n).cpu().numpy()[:, gid], axis=0) > 0
+    assert contrib.sum() > 100
+    assert (literal == contrib).mean() > 0.99, ((literal != contrib).sum(), n)
