@@ -90,6 +90,10 @@ struct TcCfg {
     static constexpr uint32_t cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
 };
 
+#ifdef GS_RASTER_STATS
+__device__ unsigned long long g_raster_stats[4];   // debug: entry-walks, live lane-walks
+#endif
+
 struct StageMeta {
     uint32_t tile, c0;
     int32_t cnt, view;
@@ -540,6 +544,15 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 for (int i = 0; i < n; i += 2) {
                     // two entries per iteration: independent alphas (ILP 2), transmittance in list order
                     const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i]);   // i is even
+#ifdef GS_RASTER_STATS
+                    {
+                        const unsigned live = __ballot_sync(0xffffffffu, !done);
+                        if (lane == 0) {
+                            atomicAdd(&g_raster_stats[0], 2ull);                       // entry-walks
+                            atomicAdd(&g_raster_stats[1], 2ull * __popc(live));       // live lane-walks
+                        }
+                    }
+#endif
                     const float4* r1 = recf + 4 * kk.x;
                     const float4* r2 = recf + 4 * kk.y;
                     float a1 = entry_alpha(r1[0], r1[1], pxf, pyf, P);
@@ -1165,3 +1178,11 @@ extern "C" gs_status gs_radiance_backward(const gs_projected* proj, const gs_bin
         grad_out->rgb, grad_out->depth, grad_out->alpha, grad_rec, proj->status);
     return check_launch("radiance_backward_kernel");
 }
+
+#ifdef GS_RASTER_STATS
+extern "C" void gs_debug_raster_stats(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, gs::g_raster_stats, sizeof(unsigned long long) * 4);
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(gs::g_raster_stats, z, sizeof(z));
+}
+#endif
