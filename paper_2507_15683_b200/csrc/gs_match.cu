@@ -368,10 +368,13 @@ __global__ void __launch_bounds__(256) fine_kernel(const float* __restrict__ Fq,
                                                    float k2, float p_min, const float* __restrict__ xyz,
                                                    const uint8_t* __restrict__ valid, gs_matches out) {
     extern __shared__ float fsm[];
+    // region 0 holds the fp32 pixel vectors until they are converted to fp16, then the
+    // cosine block X (written only after the MMAs, which read the fp16 copies)
+    const int R0 = max(2 * WP * (D + 1), WP * 65);
     float* qf = fsm;                      // [64][D + 1]
     float* rf = qf + WP * (D + 1);        // [64][D + 1]
-    float* X = rf + WP * (D + 1);         // [64][65]  x = cos * log2(e) / tau
-    float* rc = X + WP * 65;              // [64] row log2-sum-exp2
+    float* X = fsm;                       // [64][65]  x = cos * log2(e) / tau
+    float* rc = fsm + R0;                 // [64] row log2-sum-exp2
     float* cc = rc + WP;                  // [64] column log2-sum-exp2
     int* carg = reinterpret_cast<int*>(cc + WP);   // [64] column argmax
     __half* qh = reinterpret_cast<__half*>(carg + WP);   // [64][D + 8] fp16 hi / lo operands
@@ -585,7 +588,7 @@ extern "C" gs_status gs_match(const float* query_feat, const float* rend_feat, i
     if (st != GS_OK) return st;
     mnn_kernel<<<dim3((Nc + 255) / 256, n_pairs), 256, 0, s>>>(w, Nc, Ncp, p_min, out->coarse, out->coarse_prob);
     if ((st = check_launch("mnn_kernel")) != GS_OK) return st;
-    const int fsmem = (int)sizeof(float) * (2 * WP * (D + 1) + WP * 65 + 3 * WP) + 4 * WP * (D + 8) * 2;
+    const int fsmem = (int)sizeof(float) * (std::max(2 * WP * (D + 1), WP * 65) + 3 * WP) + 4 * WP * (D + 8) * 2;
     static bool fine_init = false;
     if (!fine_init) {
         cudaFuncSetAttribute(fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
