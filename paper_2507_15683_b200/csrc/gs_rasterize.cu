@@ -122,6 +122,14 @@ struct RasterSmem {
     uint32_t tmem_base;
 };
 
+// 1-ulp reciprocal (MUFU): only locates the stationary point of an edge; the e_cut
+// margin absorbs the error, so the cull stays conservative
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;\n" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // max over the 8x4 pixel-centre rectangle [x0,x1]x[y0,y1] of the log2-unit
 // exponent p(d) = ea dx^2 + eb dx dy + ec dy^2 (d = p - mean; ea, ec < 0),
 // compared with e_cut (the alpha >= alpha_min ellipse, inflated).
@@ -132,12 +140,12 @@ __device__ __forceinline__ bool ellipse_hits_rect(float u, float v, float ea, fl
     float pmax = -3.4e38f;
     if (!inx) {               // facing vertical edge: best dy = -eb dx / (2 ec), clamped
         const float dx = (u < x0 ? x0 : x1) - u;
-        const float dy = fminf(fmaxf(-eb * dx * __frcp_rn(2.f * ec), y0 - v), y1 - v);
+        const float dy = fminf(fmaxf(-eb * dx * rcp_approx(2.f * ec), y0 - v), y1 - v);
         pmax = fmaxf(pmax, ea * dx * dx + eb * dx * dy + ec * dy * dy);
     }
     if (!iny) {               // facing horizontal edge: best dx = -eb dy / (2 ea), clamped
         const float dy = (v < y0 ? y0 : y1) - v;
-        const float dx = fminf(fmaxf(-eb * dy * __frcp_rn(2.f * ea), x0 - u), x1 - u);
+        const float dx = fminf(fmaxf(-eb * dy * rcp_approx(2.f * ea), x0 - u), x1 - u);
         pmax = fmaxf(pmax, ea * dx * dx + eb * dx * dy + ec * dy * dy);
     }
     return pmax >= ecut;
