@@ -13,7 +13,9 @@ coefficients e = k * conic of reading Q29):
   conic = (c, -b, a) / (a c - b^2);  (e_a, e_b, e_c) = (k c_a, 2k c_b, k c_c)
 
 dL/dmu = R^T dL/dp.  Alg. 1's literal render-gradient test is
-||dL/dmu|| > 0 for L = the sum of the rendered colour.
+||dL/dmu|| > 0 for L = the sum of the rendered colour.  The dependence of SH
+colour (degree >= 1) on mu through the view direction is not included (the
+finite-difference pins use degree-0 colour, where the chain is exact).
 """
 from __future__ import annotations
 
