@@ -382,8 +382,8 @@ gs_status gs_radiance_backward(const gs_projected* proj, const gs_bins* bins, co
  * Gaussians' 3D means: grad_pos [3][n] (the layout of gs_scene.pos) +=
  * dL/dmu, fp64 arithmetic, f32 atomics.  Alg. 1's literal render-gradient
  * visibility test is ||dL/dmu|| > 0 for a loss on the render.
- * Not included: the path through the SH view direction (colour of degree >= 1
- * depends on mu via d = (mu - c)/|mu - c|); exact for degree-0 colour.
+ * Includes the path through O10's SH view direction d = (mu - c)/|mu - c|
+ * (colour of degree >= 1; zero for a channel clamped at 0).
  */
 gs_status gs_mean_backward(const gs_scene* scene, const gs_projected* proj, const gs_view* views_host,
                            const gs_view* views_dev, int32_t n_views, const gs_params* params,

@@ -12,10 +12,12 @@ coefficients e = k * conic of reading Q29):
   Sigma' = (J R) Sigma (J R)^T + dilation I = [[a, b], [b, c]]
   conic = (c, -b, a) / (a c - b^2);  (e_a, e_b, e_c) = (k c_a, 2k c_b, k c_c)
 
-dL/dmu = R^T dL/dp.  Alg. 1's literal render-gradient test is
-||dL/dmu|| > 0 for L = the sum of the rendered colour.  The dependence of SH
-colour (degree >= 1) on mu through the view direction is not included (the
-finite-difference pins use degree-0 colour, where the chain is exact).
+dL/dmu = R^T dL/dp + (I - d d^T)/|mu - c| dL/dd, the second term the SH view
+direction of O10: rgb_c = max(sum_k b_k(d) f_kc + 0.5, 0), d = (mu - c)/|mu - c|,
+c = -R^T t, so dL/dd = sum_c dL/drgb_c [rgb_c > 0] sum_k f_kc grad b_k(d) with the
+basis polynomials of O10 differentiated term by term (zero for degree 0).
+Alg. 1's literal render-gradient test is ||dL/dmu|| > 0 for L = the
+sum of the rendered colour.
 """
 from __future__ import annotations
 
@@ -35,6 +37,45 @@ def _sigma3(scale, quat):
     return M @ M.T
 
 
+SH_C1 = 0.4886025119029199
+SH_C2 = (1.0925484305920792, -1.0925484305920792, 0.31539156525252005, -1.0925484305920792, 0.5462742152960396)
+SH_C3 = (-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
+         -0.4570457994644658, 1.445305721320277, -0.5900435899266435)
+
+
+def sh_basis_grad(deg: int, d) -> np.ndarray:
+    """[(deg+1)^2][3]: d b_k / d(x, y, z) of the O10 basis polynomials at d
+    (x, y, z treated as independent; the projection onto the sphere is applied
+    by the caller)."""
+    x, y, z = (float(a) for a in d)
+    g = np.zeros(((deg + 1) ** 2, 3))
+    if deg < 1:
+        return g
+    g[1] = (0.0, -SH_C1, 0.0)
+    g[2] = (0.0, 0.0, SH_C1)
+    g[3] = (-SH_C1, 0.0, 0.0)
+    if deg < 2:
+        return g
+    c = SH_C2
+    g[4] = (c[0] * y, c[0] * x, 0.0)
+    g[5] = (0.0, c[1] * z, c[1] * y)
+    g[6] = (-2 * c[2] * x, -2 * c[2] * y, 4 * c[2] * z)
+    g[7] = (c[3] * z, 0.0, c[3] * x)
+    g[8] = (2 * c[4] * x, -2 * c[4] * y, 0.0)
+    if deg < 3:
+        return g
+    c = SH_C3
+    xx, yy, zz = x * x, y * y, z * z
+    g[9] = (6 * c[0] * x * y, c[0] * (3 * xx - 3 * yy), 0.0)
+    g[10] = (c[1] * y * z, c[1] * x * z, c[1] * x * y)
+    g[11] = (-2 * c[2] * x * y, c[2] * (4 * zz - xx - 3 * yy), 8 * c[2] * y * z)
+    g[12] = (-6 * c[3] * x * z, -6 * c[3] * y * z, c[3] * (6 * zz - 3 * xx - 3 * yy))
+    g[13] = (c[4] * (4 * zz - 3 * xx - yy), -2 * c[4] * x * y, 8 * c[4] * x * z)
+    g[14] = (2 * c[5] * x * z, -2 * c[5] * y * z, c[5] * (xx - yy))
+    g[15] = (c[6] * (3 * xx - 3 * yy), -6 * c[6] * x * y, 0.0)
+    return g
+
+
 def mean_backward(scene, view, rec, grec, params) -> np.ndarray:
     """dL/dmu [cnt][3] (fp64) for each record; grec [cnt][10] from radiance_backward."""
     R = np.asarray(view.R, np.float64).reshape(3, 3)
@@ -45,6 +86,7 @@ def mean_backward(scene, view, rec, grec, params) -> np.ndarray:
     lox, hix = (-(m * W) - cx) / fx, ((1.0 + m) * W - cx) / fx
     loy, hiy = (-(m * H) - cy) / fy, ((1.0 + m) * H - cy) / fy
     dil = float(params.dilation)
+    cam = -R.T @ t
     out = np.zeros((len(rec["gid"]), 3))
     for r, g in enumerate(rec["gid"]):
         mu = scene.pos[:, g].astype(np.float64)
@@ -90,4 +132,15 @@ def mean_backward(scene, view, rec, grec, params) -> np.ndarray:
         else:
             gp[2] += gj12 * (fy * ycl / (pz * pz))
         out[r] = R.T @ gp
+        # SH view direction (O10)
+        deg = int(scene.sh_degree)
+        grgb = np.asarray(grec[r][6:9], np.float64) * (np.asarray(rec["rgb"][r], np.float64) > 0)
+        if deg >= 1 and grgb.any():
+            dv = mu - cam
+            dn = float(np.linalg.norm(dv))
+            d = dv / dn
+            nk = (deg + 1) ** 2
+            coeff = scene.sh[:nk * 3, g].astype(np.float64).reshape(nk, 3)
+            gd = sh_basis_grad(deg, d).T @ (coeff @ grgb)
+            out[r] += (gd - d * (d @ gd)) / dn
     return out

@@ -476,9 +476,15 @@ __global__ void mean_backward_kernel(gs_scene S, const gs_view* __restrict__ vie
     if ((uint32_t)(slot - (int64_t)vi * cap) >= min((uint64_t)n_rec[vi], (uint64_t)cap)) return;
     const float* gr = grad_rec + slot * 10;
     const double gu = gr[0], gv = gr[1], gea = gr[2], geb = gr[3], gec = gr[4], gz = gr[9];
-    if (gu == 0.0 && gv == 0.0 && gea == 0.0 && geb == 0.0 && gec == 0.0 && gz == 0.0) return;
+    const gs_record& rc = rec[slot];
+    // colour gradient through the SH view direction (zero for degree 0 or a clamped channel)
+    double grgb[3];
+    for (int c = 0; c < 3; ++c) grgb[c] = (S.sh_degree >= 1 && rc.rgb[c] > 0.0f) ? (double)gr[6 + c] : 0.0;
+    if (gu == 0.0 && gv == 0.0 && gea == 0.0 && geb == 0.0 && gec == 0.0 && gz == 0.0 && grgb[0] == 0.0 &&
+        grgb[1] == 0.0 && grgb[2] == 0.0)
+        return;
     const int64_t n = S.n;
-    const uint32_t g = rec[slot].gid;
+    const uint32_t g = rc.gid;
     const gs_view& V = views[vi];
     double R[9], t[3];
     for (int k = 0; k < 9; ++k) R[k] = V.R[k];
@@ -537,9 +543,47 @@ __global__ void mean_backward_kernel(gs_scene S, const gs_view* __restrict__ vie
     else gp2 += gj02 * fx * xcl / z2;
     if (loy < yn && yn < hiy) { gp1 += -gj12 * fy / z2; gp2 += gj12 * 2.0 * fy * py / (z2 * pz); }
     else gp2 += gj12 * fy * ycl / z2;
-    // dL/dmu = R^T dL/dp
-    for (int k = 0; k < 3; ++k)
-        atomicAdd(&grad_pos[(int64_t)k * n + g], (float)(R[k] * gp0 + R[3 + k] * gp1 + R[6 + k] * gp2));
+    // dL/dmu = R^T dL/dp + (I - d d^T)/|mu - c| dL/dd  (O10's direction d = (mu - c)/|mu - c|)
+    double gm[3];
+    for (int k = 0; k < 3; ++k) gm[k] = R[k] * gp0 + R[3 + k] * gp1 + R[6 + k] * gp2;
+    if (grgb[0] != 0.0 || grgb[1] != 0.0 || grgb[2] != 0.0) {
+        double dv[3];
+        for (int k = 0; k < 3; ++k) dv[k] = (k == 0 ? mx : k == 1 ? my : mz) + (R[k] * t[0] + R[3 + k] * t[1] + R[6 + k] * t[2]);
+        const double dn = sqrt(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
+        const double x = dv[0] / dn, y = dv[1] / dn, z = dv[2] / dn;
+        // w_k = sum_c f_kc dL/drgb_c, then dL/dd = sum_k w_k grad b_k(d)
+        const int nk = (S.sh_degree + 1) * (S.sh_degree + 1);
+        double w[16];
+        for (int k = 0; k < nk; ++k)
+            w[k] = (double)S.sh[(int64_t)(k * 3) * n + g] * grgb[0] + (double)S.sh[(int64_t)(k * 3 + 1) * n + g] * grgb[1] +
+                   (double)S.sh[(int64_t)(k * 3 + 2) * n + g] * grgb[2];
+        const double C1 = 0.4886025119029199;
+        double gx = -C1 * w[3], gy = -C1 * w[1], gz_ = C1 * w[2];
+        if (nk >= 9) {
+            const double a0 = 1.0925484305920792, a1 = -1.0925484305920792, a2 = 0.31539156525252005,
+                         a3 = -1.0925484305920792, a4 = 0.5462742152960396;
+            gx += a0 * y * w[4] - 2 * a2 * x * w[6] + a3 * z * w[7] + 2 * a4 * x * w[8];
+            gy += a0 * x * w[4] + a1 * z * w[5] - 2 * a2 * y * w[6] - 2 * a4 * y * w[8];
+            gz_ += a1 * y * w[5] + 4 * a2 * z * w[6] + a3 * x * w[7];
+        }
+        if (nk >= 16) {
+            const double b0 = -0.5900435899266435, b1 = 2.890611442640554, b2 = -0.4570457994644658,
+                         b3 = 0.3731763325901154, b4 = -0.4570457994644658, b5 = 1.445305721320277,
+                         b6 = -0.5900435899266435;
+            const double xx = x * x, yy = y * y, zz = z * z;
+            gx += 6 * b0 * x * y * w[9] + b1 * y * z * w[10] - 2 * b2 * x * y * w[11] - 6 * b3 * x * z * w[12] +
+                  b4 * (4 * zz - 3 * xx - yy) * w[13] + 2 * b5 * x * z * w[14] + b6 * (3 * xx - 3 * yy) * w[15];
+            gy += b0 * (3 * xx - 3 * yy) * w[9] + b1 * x * z * w[10] + b2 * (4 * zz - xx - 3 * yy) * w[11] -
+                  6 * b3 * y * z * w[12] - 2 * b4 * x * y * w[13] - 2 * b5 * y * z * w[14] - 6 * b6 * x * y * w[15];
+            gz_ += b1 * x * y * w[10] + 8 * b2 * y * z * w[11] + b3 * (6 * zz - 3 * xx - 3 * yy) * w[12] +
+                   8 * b4 * x * z * w[13] + b5 * (xx - yy) * w[14];
+        }
+        const double dd = x * gx + y * gy + z * gz_;
+        gm[0] += (gx - x * dd) / dn;
+        gm[1] += (gy - y * dd) / dn;
+        gm[2] += (gz_ - z * dd) / dn;
+    }
+    for (int k = 0; k < 3; ++k) atomicAdd(&grad_pos[(int64_t)k * n + g], (float)gm[k]);
 }
 
 }  // namespace

@@ -194,3 +194,65 @@ def test_mean_grad_with_clamped_jacobian(orc):
         s3.pos[axis, 0] -= 1e-2
         fd = (loss(s2) - loss(s3)) / 2e-2
         assert abs(fd - gmu[0, axis]) <= 5e-3 * max(abs(gmu[0, axis]), 1e-2), (axis, fd, gmu[0, axis])
+
+
+def test_sh_basis_gradient_equals_finite_differences_of_sh_color(orc):
+    """backward.sh_basis_grad (numpy, term-by-term derivatives) against central
+    differences of the C oracle's O10 colour (a separate implementation of the
+    basis), for every degree, coefficient and axis (off the sphere: the basis
+    polynomials are evaluated at the perturbed, unnormalised point)."""
+    from oracle import backward as OB
+    rng = np.random.default_rng(31)
+    for deg in range(4):
+        nk = (deg + 1) ** 2
+        for _ in range(5):
+            d = rng.standard_normal(3)
+            d /= np.linalg.norm(d)
+            coeff = rng.standard_normal((nk, 3))
+            coeff[0] = 60.0                                 # keep every channel above the clamp
+            an = OB.sh_basis_grad(deg, d).T @ coeff          # [3 axes][3 channels]
+            for ax in range(3):
+                e = np.zeros(3); e[ax] = 1e-6
+                fd = (orc.sh_color(deg, coeff, d + e) - orc.sh_color(deg, coeff, d - e)) / 2e-6
+                np.testing.assert_allclose(fd, an[ax], rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_mean_grad_finite_differences_with_view_dependent_colour(orc, axis):
+    """The smooth fixture with degree-3 SH colour and a camera close enough that
+    the view direction turns noticeably across a step: dL/dmu, including the SH
+    direction term, equals central differences of the whole pipeline."""
+    from helpers import scene_of
+    from oracle import backward as OB
+    rng = np.random.default_rng(41)
+    gs = []
+    for mu, s, o in (([0.1, -0.05, 2.0], 0.5, 0.5), ([-0.2, 0.1, 2.2], 0.6, 0.4), ([0.05, 0.2, 2.4], 0.7, 0.6)):
+        sh = 0.3 * rng.standard_normal(48)
+        sh[0:3] = 0.0                                       # base colour 0.5 keeps every channel > 0
+        gs.append({"mu": mu, "scale": s, "opacity": o, "sh": sh})
+    sc = scene_of(gs, sh_degree=3)
+    v = synth.make_view(np.eye(3), np.zeros(3), 8.0, 8.0, 11.5, 9.5, 24, 20)
+    P = orc.Params()
+    gC = rng.standard_normal((3, 20, 24)).astype(np.float32)
+    z = np.zeros((20, 24), np.float32)
+
+    def loss(scene):
+        r = orc.project(scene, v, P)
+        return orc.radiance_backward(v, r, orc.bin_keys(r, v), gC, z, z, P)[1]
+
+    rec = orc.project(sc, v, P)
+    assert (rec["rgb"] > 0).all()
+    o = orc.render(sc, v)
+    assert (o["flags"] == 0).all()
+    grec, _ = orc.radiance_backward(v, rec, orc.bin_keys(rec, v), gC, z, z, P)
+    gmu = OB.mean_backward(sc, v, rec, grec, P)
+    # the same chain with the colour's direction dependence dropped
+    gmu0 = OB.mean_backward(dataclasses.replace(sc, sh_degree=0, sh=sc.sh[:3].copy()), v, rec, grec, P)
+    assert np.abs(gmu - gmu0).max() > 1e-2 * np.abs(gmu).max()   # the SH term matters here
+    h = 1e-3
+    for r, g in enumerate(rec["gid"]):
+        s2, s3 = dataclasses.replace(sc, pos=sc.pos.copy()), dataclasses.replace(sc, pos=sc.pos.copy())
+        s2.pos[axis, g] += h
+        s3.pos[axis, g] -= h
+        fd = (loss(s2) - loss(s3)) / (2 * h)
+        assert abs(fd - gmu[r, axis]) <= 5e-3 * max(abs(gmu[r, axis]), 1e-2), (r, fd, gmu[r, axis])
