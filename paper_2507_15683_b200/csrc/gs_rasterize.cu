@@ -151,12 +151,40 @@ __device__ __forceinline__ bool ellipse_hits_rect(float u, float v, float ea, fl
     return pmax >= ecut;
 }
 
+// Blackwell packed fp32 (f32x2) arithmetic: each lane rounds exactly like the
+// scalar _rn operation, one issue slot for two.  Only used where no multiply feeds
+// an add (ptxas contracts f32x2 mul + add regardless of .rn).
+__device__ __forceinline__ uint64_t pk2(float x, float y) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};\n" : "=l"(r) : "f"(x), "f"(y));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(uint64_t r) {
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;\n" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+// (a.x - b.x, a.y - b.y), each rounded to nearest
+__device__ __forceinline__ float2 sub2_rn(float ax, float ay, float bx, float by) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;\n" : "=l"(r) : "l"(pk2(ax, ay)), "l"(pk2(bx, by)));
+    return upk2(r);
+}
+// (x, y) += w (a, b) as two fmaf
+__device__ __forceinline__ void fma2_acc(float& x, float& y, float w, float a, float b) {
+    uint64_t acc = pk2(x, y);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;\n" : "+l"(acc) : "l"(pk2(w, w)), "l"(pk2(a, b)));
+    const float2 v = upk2(acc);
+    x = v.x; y = v.y;
+}
+
 // alpha of entry k at this lane's pixel, or 0 when the oracle skips it (p > 0
 // or alpha < alpha_min).  p(d) = dx (ea dx + eb dy) + ec dy dy with the oracle's
 // fused multiply-adds (reading Q29); alpha = min(alpha_max, o 2^p).
 __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, float pxf, float pyf,
                                              const gs_params& P) {
-    const float dx = __fsub_rn(a.x, pxf), dy = __fsub_rn(a.y, pyf);
+    const float2 d = sub2_rn(a.x, a.y, pxf, pyf);
+    const float dx = d.x, dy = d.y;
     const float p = __fmaf_rn(dx, __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy)), __fmul_rn(__fmul_rn(b.x, dy), dy));
     const float alpha = fminf(P.alpha_max, __fmul_rn(b.y, ex2_ftz(p)));
     return ((p > 0.0f) || (alpha < P.alpha_min)) ? 0.0f : alpha;
@@ -283,7 +311,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 cnt = end ? 0 : (int)min((uint32_t)SE, re - c0);
                 load_idx(c0, cnt, nslot, ngid);
             }
-            if (s >= NST) mbar_wait_sleep(&sm.empty[buf], ((s / NST) & 1u) ^ 1u, 64);
+            if (s >= NST) mbar_wait_suspend(&sm.empty[buf], ((s / NST) & 1u) ^ 1u);
 #pragma unroll
             for (int q = 0; q < SE / 32; ++q) {
                 const int j = q * 32 + (int)lane;
@@ -446,16 +474,18 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             }
         }
     };
-    // apply one evaluated entry to this lane's pixel, branch-free.  A skipped
-    // entry (power > 0, alpha < alpha_min, or pixel already stopped) arrives as
-    // alpha = 0, which is an exact no-op: Tn = T(1 - 0) = T >= t_min, w = 0.
-    auto blend = [&](float a, const float4& c) -> float {
-        const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
-        const bool stop = Tn < P.t_min;
+    // apply one evaluated entry to this lane's pixel, branch-free (om = 1 - a).  A
+    // skipped entry (power > 0 or alpha < alpha_min) arrives as alpha = 0, an exact
+    // no-op: Tn = T(1 - 0) = T >= t_min, w = 0.  A pixel that already stopped keeps
+    // T and gets weight 0 whatever a is.
+    auto blend_om = [&](float a, float om, const float4& c) -> float {
+        const float Tn = __fmul_rn(T, om);
+        const bool stop = done || Tn < P.t_min;
         const float wgt = stop ? 0.0f : __fmul_rn(a, T);
-        C0 = fmaf(wgt, c.x, C0); C1 = fmaf(wgt, c.y, C1); C2 = fmaf(wgt, c.z, C2); Dz = fmaf(wgt, c.w, Dz);
+        fma2_acc(C0, C1, wgt, c.x, c.y);
+        fma2_acc(C2, Dz, wgt, c.z, c.w);
         T = stop ? T : Tn;
-        done = done || stop;
+        done = stop;
         return wgt;
     };
 
@@ -485,7 +515,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     // cycle per 64 entries halves the per-stage bookkeeping.
     for (uint32_t s = 0;;) {
         const int buf = (int)(s % NST);
-        mbar_wait(&sm.full[buf], (s / NST) & 1u);
+        mbar_wait_suspend(&sm.full[buf], (s / NST) & 1u);
         const StageMeta m = sm.meta[buf];
         if (m.flags & ST_END) break;
         const bool pair = !(m.flags & ST_LAST);   // a non-last stage is followed by one of its tile
@@ -494,7 +524,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
         int cnt2 = 0;
         uint32_t last_flags = m.flags;
         if (pair) {
-            mbar_wait(&sm.full[buf2], (s2 / NST) & 1u);
+            mbar_wait_suspend(&sm.full[buf2], (s2 / NST) & 1u);
             cnt2 = sm.meta[buf2].cnt;
             last_flags = sm.meta[buf2].flags;
         }
@@ -563,12 +593,12 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
 #endif
                     const float4* r1 = recf + 4 * kk.x;
                     const float4* r2 = recf + 4 * kk.y;
-                    float a1 = entry_alpha(r1[0], r1[1], pxf, pyf, P);
-                    float a2 = entry_alpha(r2[0], r2[1], pxf, pyf, P);
-                    a1 = done ? 0.0f : a1;
-                    const float w1 = blend(a1, r1[2]);
-                    a2 = done ? 0.0f : a2;
-                    const float w2 = blend(a2, r2[2]);
+                    const float a1 = entry_alpha(r1[0], r1[1], pxf, pyf, P);
+                    const float a2 = entry_alpha(r2[0], r2[1], pxf, pyf, P);
+                    // 1 - alpha of both entries at once
+                    const float2 om = sub2_rn(1.0f, 1.0f, a1, a2);
+                    const float w1 = blend_om(a1, om.x, r1[2]);
+                    const float w2 = blend_om(a2, om.y, r2[2]);
                     if constexpr (WB) {
                         if (pend == 0) hold = s;
                         sm.wbuf[warp][pend][lane] = w1;
