@@ -104,11 +104,15 @@ template <int D, bool CONTRIB, bool TC>
 struct RasterSmem {
     static constexpr int FS = D > 0 ? D + 8 : 1;   // fp32 feature row stride (floats)
     static constexpr int FSH = D + 8;              // fp16 feature row stride (halves; 16-B aligned rows)
-    static constexpr bool WB = D > 0 || CONTRIB;   // weight rows are staged (features and/or contributions)
+    static constexpr bool WB = D > 0 || CONTRIB;   // weight rows are collected (features and/or contributions)
+    // tcgen05 without contributions: each walked entry pair's fp16 hi / lo weights go
+    // straight from registers into the TMEM A buffer (no shared-memory weight rows)
+    static constexpr bool DIRECT = TC && !CONTRIB;
+    static constexpr bool WSTAGE = WB && !DIRECT;
     float4 rec[NST][SE + 1][4];                    // 64-byte records; row SE = null record (opacity 0)
     float feat[(D > 0 && !TC) ? NST : 1][(D > 0 && !TC) ? SE + 1 : 1][FS];
     alignas(16) __half feath[TC ? NST : 1][TC ? SE + 1 : 1][TC ? FSH : 8];   // tcgen05 path: fp16 rows
-    alignas(16) float wbuf[WB ? NCW : 1][WB_ROWS][WB_STRIDE]; // per-warp compacted weights [k][pixel]
+    alignas(16) float wbuf[WSTAGE ? NCW : 1][WSTAGE ? WB_ROWS : 1][WB_STRIDE]; // per-warp weights [k][pixel]
     uint32_t slots[CONTRIB ? NST * (SE + 1) : 1];  // record slot of each ring row (contributions)
     alignas(16) int ent[NCW][2 * SE + 2];            // per-warp compacted ballot list of a stage pair (flat rows)
     int kent[NCW][WB_ROWS];                          // ring row of each pending weight row
@@ -193,6 +197,14 @@ __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, f
 // Persistent kernel: each CTA renders a sequence of tiles handed out in order by
 // a dynamic scheduler.  The producer warp runs ahead across tile boundaries so
 // the consumers never wait for a tile's first records.
+// back-off of a warp waiting on the stage ring (ns): the producer when the ring is
+// full, a consumer warp that ran ahead of its CTA's slowest warp
+#ifndef GS_PROD_SLEEP
+#define GS_PROD_SLEEP 64
+#endif
+#ifndef GS_CONS_SLEEP
+#define GS_CONS_SLEEP 64
+#endif
 #ifndef GS_TC_MIN_BLOCKS
 #define GS_TC_MIN_BLOCKS 3
 #endif
@@ -311,7 +323,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 cnt = end ? 0 : (int)min((uint32_t)SE, re - c0);
                 load_idx(c0, cnt, nslot, ngid);
             }
-            if (s >= NST) mbar_wait_suspend(&sm.empty[buf], ((s / NST) & 1u) ^ 1u);
+            if (s >= NST) mbar_wait_sleep(&sm.empty[buf], ((s / NST) & 1u) ^ 1u, GS_PROD_SLEEP);
 #pragma unroll
             for (int q = 0; q < SE / 32; ++q) {
                 const int j = q * 32 + (int)lane;
@@ -392,19 +404,21 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             // hi + lo weight pairs) -> TMEM, B (16 feature rows -> fp16) -> the canonical
             // smem tile, then two lane-masked M=128 N=D K=16 MMAs issued by lane 0
             const uint32_t b = kstep & 1u;
-            if (kstep >= 2) mbar_wait(&sm.mma_bar[warp][b], ((kstep >> 1) - 1u) & 1u);
-            uint32_t hi[8], lo[8];
+            if constexpr (!Smem::DIRECT) {
+                if (kstep >= 2) mbar_wait(&sm.mma_bar[warp][b], ((kstep >> 1) - 1u) & 1u);
+                uint32_t hi[8], lo[8];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const float w0 = sm.wbuf[warp][2 * c][lane], w1 = sm.wbuf[warp][2 * c + 1][lane];
-                const __half2 h = __floats2half2_rn(w0, w1);
-                const float2 hf = __half22float2(h);
-                const __half2 l = __floats2half2_rn(w0 - hf.x, w1 - hf.y);
-                hi[c] = *reinterpret_cast<const uint32_t*>(&h);
-                lo[c] = *reinterpret_cast<const uint32_t*>(&l);
+                for (int c = 0; c < 8; ++c) {
+                    const float w0 = sm.wbuf[warp][2 * c][lane], w1 = sm.wbuf[warp][2 * c + 1][lane];
+                    const __half2 h = __floats2half2_rn(w0, w1);
+                    const float2 hf = __half22float2(h);
+                    const __half2 l = __floats2half2_rn(w0 - hf.x, w1 - hf.y);
+                    hi[c] = *reinterpret_cast<const uint32_t*>(&h);
+                    lo[c] = *reinterpret_cast<const uint32_t*>(&l);
+                }
+                tmem_st8(tA + my_lanes + b * 16u, hi);
+                tmem_st8(tA + my_lanes + b * 16u + 8u, lo);
             }
-            tmem_st8(tA + my_lanes + b * 16u, hi);
-            tmem_st8(tA + my_lanes + b * 16u + 8u, lo);
             // the B tile is built while the TMEM stores are in flight
             constexpr int NC8 = D / 8;
             const __half* fb = &sm.feath[0][0][0];
@@ -497,10 +511,28 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     int pend = 0;             // pending weight rows (< WB_ROWS between stages)
     uint32_t hold = 0;        // oldest stage a pending row references
     uint32_t rel = 0;         // next stage to release
+    // DIRECT: weights of entries (2q, 2q+1) of the current k-step -> A column q (hi) and
+    // 8 + q (lo) of TMEM buffer kstep & 1; the buffer's previous MMA is waited for first
+    auto store_pair = [&](float w1, float w2, int q) {
+        if constexpr (Smem::DIRECT) {
+            const uint32_t b = kstep & 1u;
+            if (q == 0 && kstep >= 2) mbar_wait(&sm.mma_bar[warp][b], ((kstep >> 1) - 1u) & 1u);
+            const __half2 h = __floats2half2_rn(w1, w2);
+            const float2 hf = __half22float2(h);
+            const float2 r = sub2_rn(w1, w2, hf.x, hf.y);
+            const __half2 l = __floats2half2_rn(r.x, r.y);
+            const uint32_t col = tA + my_lanes + b * 16u + (uint32_t)q;
+            tmem_st1(col, *reinterpret_cast<const uint32_t*>(&h));
+            tmem_st1(col + 8u, *reinterpret_cast<const uint32_t*>(&l));
+        }
+    };
     auto flush_pending = [&]() {
         if constexpr (WB) {
             if (pend > 0) {
-                for (int r = pend; r < WB_ROWS; ++r) sm.wbuf[warp][r][lane] = 0.f;
+                if constexpr (Smem::DIRECT)
+                    for (int q = pend >> 1; q < WB_ROWS / 2; ++q) store_pair(0.f, 0.f, q);
+                else
+                    for (int r = pend; r < WB_ROWS; ++r) sm.wbuf[warp][r][lane] = 0.f;
                 if (lane < (uint32_t)(WB_ROWS - pend)) sm.kent[warp][pend + lane] = SE;   // null row
                 __syncwarp();
                 mma_block(0, WB_ROWS);
@@ -515,7 +547,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     // cycle per 64 entries halves the per-stage bookkeeping.
     for (uint32_t s = 0;;) {
         const int buf = (int)(s % NST);
-        mbar_wait_suspend(&sm.full[buf], (s / NST) & 1u);
+        mbar_wait_sleep(&sm.full[buf], (s / NST) & 1u, GS_CONS_SLEEP);
         const StageMeta m = sm.meta[buf];
         if (m.flags & ST_END) break;
         const bool pair = !(m.flags & ST_LAST);   // a non-last stage is followed by one of its tile
@@ -524,7 +556,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
         int cnt2 = 0;
         uint32_t last_flags = m.flags;
         if (pair) {
-            mbar_wait_suspend(&sm.full[buf2], (s2 / NST) & 1u);
+            mbar_wait_sleep(&sm.full[buf2], (s2 / NST) & 1u, GS_CONS_SLEEP);
             cnt2 = sm.meta[buf2].cnt;
             last_flags = sm.meta[buf2].flags;
         }
@@ -601,8 +633,12 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     const float w2 = blend_om(a2, om.y, r2[2]);
                     if constexpr (WB) {
                         if (pend == 0) hold = s;
-                        sm.wbuf[warp][pend][lane] = w1;
-                        sm.wbuf[warp][pend + 1][lane] = w2;
+                        if constexpr (Smem::DIRECT) {
+                            store_pair(w1, w2, pend >> 1);
+                        } else {
+                            sm.wbuf[warp][pend][lane] = w1;
+                            sm.wbuf[warp][pend + 1][lane] = w2;
+                        }
                         if (lane == 0) { sm.kent[warp][pend] = kk.x; sm.kent[warp][pend + 1] = kk.y; }
                         pend += 2;
                         if (pend == WB_ROWS) {             // a full k-step: feed the tensor cores
