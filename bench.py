@@ -48,6 +48,9 @@ def parse():
                     help="feature contraction: tcgen05 (fp16 rows, TMEM) or mma.sync (fp32 rows)")
     ap.add_argument("--binning", default="tight", choices=["tight", "square"],
                     help="tile binning: tight alpha-ellipse tiles (N3, Q30) or the 3-sigma square (O8); same images")
+    ap.add_argument("--separate-backproject", action="store_true",
+                    help="time gs_rasterize + gs_backproject as two launches (default: the fused "
+                         "gs_rasterize_backproject)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="view chunks of the overlapped e2e measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -154,11 +157,13 @@ def workload(cfg: str, scale: float, rank: int, world: int, scaling: str, views_
     return scene, views
 
 
-def algorithmic_raster_bytes(n_pairs: int, n_visible: int, total_pixels: int, D: int, feat_bytes: int = 4) -> int:
+def algorithmic_raster_bytes(n_pairs: int, n_visible: int, total_pixels: int, D: int, feat_bytes: int = 4,
+                             fused_backproject: bool = False) -> int:
     """P*4 (sorted list) + V*(48 + D*feat_bytes) (records +
     feature rows, read once; 2-byte rows on the tcgen05 path) + H*W*(5 + D)*4
-    (planar fp32 outputs)."""
-    return 4 * n_pairs + n_visible * (48 + feat_bytes * D) + total_pixels * (5 + D) * 4
+    (planar fp32 outputs) [+ H*W*13 (xyz + valid) when O13 is fused]."""
+    return (4 * n_pairs + n_visible * (48 + feat_bytes * D) + total_pixels * (5 + D) * 4 +
+            (13 * total_pixels if fused_backproject else 0))
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -301,9 +306,14 @@ def main():
             e[1].record(stream)
             G.gs_bin_sort(r.proj, r.vb, r.bins, r.ws_bin, stream)
             e[2].record(stream)
-            G.gs_rasterize(r.scene, r.proj, r.bins, r.vb, r.params, r.images, stream)
-            e[3].record(stream)
-            G.gs_backproject(r.images, r.vb, r.a_min, r.xyz, r.valid, stream)
+            if args.separate_backproject:
+                G.gs_rasterize(r.scene, r.proj, r.bins, r.vb, r.params, r.images, stream)
+                e[3].record(stream)
+                G.gs_backproject(r.images, r.vb, r.a_min, r.xyz, r.valid, stream)
+            else:
+                G.gs_rasterize_backproject(r.scene, r.proj, r.bins, r.vb, r.params, r.images, r.a_min, r.xyz,
+                                           r.valid, stream)
+                e[3].record(stream)
             e[4].record(stream)
             if scorer is not None:
                 scorer.add(r, fmaps, stream)
@@ -542,7 +552,8 @@ def main():
     names = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_backproject", "n1_visibility_score"]
     D = scene.feat_dim
     tc_path = D in (16, 32, 48, 64) and args.feature_path == "tcgen05"
-    raster_bytes = algorithmic_raster_bytes(n_pairs, n_visible, total_px, D, 2 if tc_path else 4)
+    fused = not args.separate_backproject
+    raster_bytes = algorithmic_raster_bytes(n_pairs, n_visible, total_px, D, 2 if tc_path else 4, fused)
     achieved = raster_bytes / (stage_ms[2] / 1e3) / 1e9
     traffic = ncu_traffic(f"{args.config}@{args.scale}/{args.binning}/{'tcgen05' if tc_path else 'mma_sync'}")
     roof = {"bound": "hbm", "kernel": "gs_rasterize", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -550,7 +561,7 @@ def main():
             "algorithmic_bytes_per_launch": raster_bytes, "dominant_stage": names[dom],
             "note": "HBM roofline of the algorithmic bytes; the kernel is instruction-issue bound "
                     "(ncu issue-active ~0.73, profiles/r01_ncu_full_rasterize_C4x16.txt), traffic = algorithmic"}
-    launches_per_step = (3 if ds.n_blocks else 2) + 8 + 1 + 1 + (1 if scorer is not None else 0)
+    launches_per_step = (3 if ds.n_blocks else 2) + 8 + 1 + (0 if fused else 1) + (1 if scorer is not None else 0)
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
            "ms_per_step": ms_step, "ms_per_view": ms_step * world / all_views if args.scaling == "strong" else
@@ -561,6 +572,7 @@ def main():
                       "feat_dim": D, "l2": "inputs larger than L2 (scene %.2f GB, %.1f GB written per step)" % (
                           ds.nbytes() / 1e9, (total_px * (5 + D) * 4 + total_px * 13) / 1e9),
                       "gather": bool(args.gather and world > 1), "n1": bool(args.n1), "binning": args.binning,
+                      "backproject": "fused into gs_rasterize (gs_rasterize_backproject)" if fused else "separate",
                       "feature_path": (args.feature_path if scene.feat_dim in (16, 32, 48, 64) else "mma_sync")
                       if scene.feat_dim else None},
            "stages_ms": {n: float(m) for n, m in zip(names, stage_ms) if n != names[4] or scorer is not None},

@@ -439,6 +439,19 @@ gs_status gs_rasterize(const gs_scene* scene, const gs_projected* proj, const gs
                        const gs_params* params, gs_images* out, void* stream);
 
 /*
+ * gs_rasterize_backproject -- gs_rasterize with O13 (gs_backproject below) fused
+ * into its per-pixel epilogue: the same outputs as gs_rasterize followed by
+ * gs_backproject(out, ..., a_min, xyz, valid), without re-reading depth and
+ * alpha.  P:278 (rendered depth for the 2D-3D constraints).  xyz [3][H][W] and
+ * valid [H][W] per view as gs_backproject (no alignment requirement).
+ * Errors: those of gs_rasterize; GS_INVALID_ARG for NULL xyz / valid or NaN a_min.
+ */
+gs_status gs_rasterize_backproject(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins,
+                                   const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
+                                   const gs_params* params, gs_images* out, float a_min, float* xyz,
+                                   uint8_t* valid, void* stream);
+
+/*
  * gs_backproject -- O13: valid iff A >= a_min and Dz/A > 0;
  * X = R^T(((px - cx)/fx zbar, (py - cy)/fy zbar, zbar) - t), zbar = Dz/A.
  * xyz is planar [3][H][W] per view at 3*pix_offset; invalid pixels get

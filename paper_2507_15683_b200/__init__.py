@@ -7,13 +7,14 @@ and the multi-GPU pose-sharding host logic (``dist``).  There is no CPU
 fallback.
 """
 from .gs import (GSError, DeviceScene, ViewBatch, Projected, Bins, Images, default_params,  # noqa: F401
-                 gs_project, gs_bin_sort, gs_rasterize, gs_backproject, gs_visibility_score, gs_validate_scene,
+                 gs_project, gs_bin_sort, gs_rasterize, gs_rasterize_backproject, gs_backproject, gs_visibility_score,
+                 gs_validate_scene,
                  gs_match, Matches, match_workspace_bytes, gs_pnp, gs_verify_consistency, pnp_workspace_bytes,
                  ViewsAt, GS_VIEW_BYTES, gs_feature_backward, gs_feature_l1_grad, gs_feature_sgd, gs_radiance_backward, GRAD_FIELDS, gs_mean_backward,
                  lib, LIB_PATH,
                  EXPORTS)
 from .pipeline import Renderer, SignificanceScorer, Refiner, FeatureDistiller  # noqa: F401
 
-__all__ = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_backproject", "gs_visibility_score", "gs_match",
+__all__ = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_rasterize_backproject", "gs_backproject", "gs_visibility_score", "gs_match",
            "gs_validate_scene", "gs_pnp", "gs_verify_consistency", "Matches", "Refiner", "DeviceScene",
            "ViewBatch", "Projected", "Bins", "Images", "Renderer", "SignificanceScorer", "default_params", "GSError"]

@@ -12,21 +12,6 @@
 namespace gs {
 namespace {
 
-__device__ __forceinline__ void bp_pixel(const gs_view& V, float Dz, float A, float a_min, int px, int py, float& X,
-                                         float& Y, float& Z, uint8_t& ok) {
-    // validity decided in fp32 on the fp32 A (same precision as the oracle)
-    const bool valid = A >= a_min && (Dz / A) > 0.0f;
-    if (!valid) { X = Y = Z = 0.f; ok = 0; return; }
-    const float zb = Dz / A;
-    const float c0 = ((float)px - V.cx) / V.fx * zb - V.t[0];
-    const float c1 = ((float)py - V.cy) / V.fy * zb - V.t[1];
-    const float c2 = zb - V.t[2];
-    X = V.R[0] * c0 + V.R[3] * c1 + V.R[6] * c2;
-    Y = V.R[1] * c0 + V.R[4] * c1 + V.R[7] * c2;
-    Z = V.R[2] * c0 + V.R[5] * c1 + V.R[8] * c2;
-    ok = 1;
-}
-
 __global__ void __launch_bounds__(256)
 backproject_kernel(const gs_view* __restrict__ views, const float* __restrict__ depth,
                    const float* __restrict__ alpha, float a_min, float* __restrict__ xyz,

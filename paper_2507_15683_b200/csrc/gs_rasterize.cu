@@ -53,7 +53,10 @@ namespace {
 constexpr int NCW = 8;                 // consumer warps
 constexpr int RT_THREADS = (NCW + 1) * 32;
 constexpr int SE = 32;                 // entries per stage (one ballot)
-constexpr int NST = 8;                 // ring stages
+#ifndef GS_NST
+#define GS_NST 8
+#endif
+constexpr int NST = GS_NST;            // ring stages
 constexpr int WB_STRIDE = 36;          // weight-buffer row stride (conflict-free m16n8k16 A fragments)
 constexpr int WB_ROWS = 16;            // one tensor-core k-step of weights (m16n8k16)
 constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
@@ -216,7 +219,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                  const float* __restrict__ feat, const __half* __restrict__ feat_h,
                  gs_params P, float* __restrict__ out_rgb, float* __restrict__ out_depth,
                  float* __restrict__ out_alpha, float* __restrict__ out_feat,
-                 unsigned long long* __restrict__ contrib, const uint32_t* __restrict__ status) {
+                 unsigned long long* __restrict__ contrib, const uint32_t* __restrict__ status, float a_min,
+                 float* __restrict__ out_xyz, uint8_t* __restrict__ out_valid) {
     static_assert(!TC || TcCfg<D>::eligible, "tcgen05 feature path needs D in {16, 32, 48, 64}");
     using Smem = RasterSmem<D, CONTRIB, TC>;
     constexpr bool WB = Smem::WB;
@@ -668,6 +672,15 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 __stcs(&out_rgb[3 * po + 2 * HW + loc], C2);
                 __stcs(&out_depth[po + loc], Dz);
                 __stcs(&out_alpha[po + loc], 1.0f - T);
+                if (out_xyz) {   // fused O13 (gs_rasterize_backproject)
+                    float X, Y, Z;
+                    uint8_t ok;
+                    bp_pixel(*V, Dz, 1.0f - T, a_min, px, py, X, Y, Z, ok);
+                    __stcs(&out_xyz[3 * po + loc], X);
+                    __stcs(&out_xyz[3 * po + HW + loc], Y);
+                    __stcs(&out_xyz[3 * po + 2 * HW + loc], Z);
+                    out_valid[po + loc] = ok;
+                }
             }
             if constexpr (TC) {
                 // this lane's pixel row of the group accumulator: D channels
@@ -734,7 +747,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
 
 template <int D, bool CONTRIB, bool TC>
 gs_status launch(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins, const gs_view* views_dev,
-                 int n_views, int64_t T, const gs_params* P, gs_images* out, cudaStream_t s) {
+                 int n_views, int64_t T, const gs_params* P, gs_images* out, cudaStream_t s, float a_min,
+                 float* xyz, uint8_t* valid) {
     const int smem = (int)sizeof(RasterSmem<D, CONTRIB, TC>);
     static int blocks_per_sm = 0;
     if (blocks_per_sm == 0) {
@@ -770,7 +784,7 @@ gs_status launch(const gs_scene* scene, const gs_projected* proj, const gs_bins*
     rasterize_kernel<D, CONTRIB, TC><<<(unsigned)grid, RT_THREADS, smem, s>>>(
         views_dev, n_views, proj->rec, bins->sorted_rec, bins->sorted_gid, bins->ranges, (uint32_t)T, bins->tile_sched,
         scene->feat, reinterpret_cast<const __half*>(scene->feat_h),
-        *P, out->rgb, out->depth, out->alpha, out->feat, proj->contrib, proj->status);
+        *P, out->rgb, out->depth, out->alpha, out->feat, proj->contrib, proj->status, a_min, xyz, valid);
     return check_launch("rasterize_kernel");
 }
 
@@ -1119,9 +1133,10 @@ __global__ void sgd_kernel(float* __restrict__ feat, const float* __restrict__ g
 
 using namespace gs;
 
-extern "C" gs_status gs_rasterize(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins,
-                                  const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
-                                  const gs_params* params, gs_images* out, void* stream) {
+static gs_status rasterize_impl(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins,
+                                const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
+                                const gs_params* params, gs_images* out, void* stream, float a_min, float* xyz,
+                                uint8_t* valid) {
     gs_status st = validate_scene(scene, false);
     if (st != GS_OK) return st;
     int64_t total_pixels = 0, T = 0;
@@ -1142,15 +1157,15 @@ extern "C" gs_status gs_rasterize(const gs_scene* scene, const gs_projected* pro
     switch (scene->feat_dim) {
 #define GS_CASE(d) \
     case d:                                                                                       \
-        return proj->contrib ? launch<d, true, false>(scene, proj, bins, views_dev, n_views, T, params, out, s) \
-                             : launch<d, false, false>(scene, proj, bins, views_dev, n_views, T, params, out, s);
+        return proj->contrib ? launch<d, true, false>(scene, proj, bins, views_dev, n_views, T, params, out, s, a_min, xyz, valid) \
+                             : launch<d, false, false>(scene, proj, bins, views_dev, n_views, T, params, out, s, a_min, xyz, valid);
 #define GS_CASE_TC(d) \
     case d:                                                                                              \
         if (tc)                                                                                          \
-            return proj->contrib ? launch<d, true, true>(scene, proj, bins, views_dev, n_views, T, params, out, s) \
-                                 : launch<d, false, true>(scene, proj, bins, views_dev, n_views, T, params, out, s); \
-        return proj->contrib ? launch<d, true, false>(scene, proj, bins, views_dev, n_views, T, params, out, s) \
-                             : launch<d, false, false>(scene, proj, bins, views_dev, n_views, T, params, out, s);
+            return proj->contrib ? launch<d, true, true>(scene, proj, bins, views_dev, n_views, T, params, out, s, a_min, xyz, valid) \
+                                 : launch<d, false, true>(scene, proj, bins, views_dev, n_views, T, params, out, s, a_min, xyz, valid); \
+        return proj->contrib ? launch<d, true, false>(scene, proj, bins, views_dev, n_views, T, params, out, s, a_min, xyz, valid) \
+                             : launch<d, false, false>(scene, proj, bins, views_dev, n_views, T, params, out, s, a_min, xyz, valid);
         GS_CASE(0) GS_CASE(4) GS_CASE(8) GS_CASE(12) GS_CASE_TC(16) GS_CASE(20) GS_CASE(24) GS_CASE(28)
         GS_CASE_TC(32) GS_CASE(36) GS_CASE(40) GS_CASE(44) GS_CASE_TC(48) GS_CASE(52) GS_CASE(56) GS_CASE(60)
         GS_CASE_TC(64)
@@ -1160,6 +1175,22 @@ extern "C" gs_status gs_rasterize(const gs_scene* scene, const gs_projected* pro
             gs::set_error("feat_dim = %d unsupported", scene->feat_dim);
             return GS_UNSUPPORTED;
     }
+}
+
+extern "C" gs_status gs_rasterize(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins,
+                                  const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
+                                  const gs_params* params, gs_images* out, void* stream) {
+    return rasterize_impl(scene, proj, bins, views_host, views_dev, n_views, params, out, stream, 0.0f, nullptr,
+                          nullptr);
+}
+
+extern "C" gs_status gs_rasterize_backproject(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins,
+                                              const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
+                                              const gs_params* params, gs_images* out, float a_min, float* xyz,
+                                              uint8_t* valid, void* stream) {
+    GS_REQUIRE(xyz && valid, GS_INVALID_ARG, "xyz/valid is NULL");
+    GS_REQUIRE(a_min == a_min, GS_INVALID_ARG, "a_min is NaN");
+    return rasterize_impl(scene, proj, bins, views_host, views_dev, n_views, params, out, stream, a_min, xyz, valid);
 }
 
 namespace gs {

@@ -74,7 +74,8 @@ EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_lay
            "gs_mean_backward",
            "gs_feature_l1_grad", "gs_feature_sgd",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
-           "gs_rasterize", "gs_backproject", "gs_visibility_score", "gs_visibility_workspace_bytes"]
+           "gs_rasterize", "gs_rasterize_backproject", "gs_backproject", "gs_visibility_score",
+           "gs_visibility_workspace_bytes"]
 
 _lib = None
 
@@ -99,7 +100,7 @@ def lib():
         L.gs_match_workspace_bytes.argtypes = [ctypes.c_int32] * 4
         L.gs_visibility_workspace_bytes.restype = ctypes.c_size_t
         for f in ("gs_views_layout", "gs_scene_block_bounds", "gs_project", "gs_bin_sort", "gs_rasterize",
-                  "gs_backproject", "gs_visibility_score"):
+                  "gs_rasterize_backproject", "gs_backproject", "gs_visibility_score"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -316,6 +317,15 @@ def gs_rasterize(scene: DeviceScene, proj: Projected, bins: Bins, views: ViewBat
     _check(lib().gs_rasterize(ctypes.byref(scene.struct), ctypes.byref(proj.struct), ctypes.byref(bins.struct),
                               views.host, views.dev_ptr, ctypes.c_int32(views.n), ctypes.byref(params),
                               ctypes.byref(images.struct), _stream(stream)), "gs_rasterize")
+
+
+def gs_rasterize_backproject(scene: DeviceScene, proj: Projected, bins: Bins, views: ViewBatch, params: gs_params,
+                             images: Images, a_min: float, xyz: torch.Tensor, valid: torch.Tensor, stream=None):
+    _check(lib().gs_rasterize_backproject(ctypes.byref(scene.struct), ctypes.byref(proj.struct),
+                                          ctypes.byref(bins.struct), views.host, views.dev_ptr,
+                                          ctypes.c_int32(views.n), ctypes.byref(params), ctypes.byref(images.struct),
+                                          ctypes.c_float(a_min), _ptr(xyz), _ptr(valid), _stream(stream)),
+           "gs_rasterize_backproject")
 
 
 def gs_backproject(images: Images, views: ViewBatch, a_min: float, xyz: torch.Tensor, valid: torch.Tensor,

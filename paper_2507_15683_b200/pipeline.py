@@ -3,7 +3,7 @@
 ``Renderer`` owns the caller-side buffers the C ABI asks for (records, pairs,
 images, workspaces), sizes them once from the device counters (the only
 host<->device sync), and then enqueues
-gs_project -> gs_bin_sort -> gs_rasterize -> gs_backproject on a stream with
+gs_project -> gs_bin_sort -> gs_rasterize (+ fused gs_backproject) on a stream with
 no host synchronisation.  No arithmetic of the method happens here.
 """
 from __future__ import annotations
@@ -76,9 +76,12 @@ class Renderer:
             self.proj.status.zero_()
         G.gs_project(self.scene, vb, self.params, self.proj, self.ws_proj, stream, scene_struct=self.scene_struct)
         G.gs_bin_sort(self.proj, vb, self.bins, self.ws_bin, stream)
-        G.gs_rasterize(self.scene, self.proj, self.bins, vb, self.params, self.images, stream)
         if self.do_backproject:
-            G.gs_backproject(self.images, vb, self.a_min, self.xyz, self.valid, stream)
+            # O13 fused into the compositing epilogue (same values as gs_backproject)
+            G.gs_rasterize_backproject(self.scene, self.proj, self.bins, vb, self.params, self.images, self.a_min,
+                                       self.xyz, self.valid, stream)
+        else:
+            G.gs_rasterize(self.scene, self.proj, self.bins, vb, self.params, self.images, stream)
 
     def status(self) -> int:
         return int(self.proj.status.item())

@@ -268,6 +268,25 @@ def test_backproject_kernel_on_oracle_images(G, orc):
                          o["flags"], o["depth"], o["alpha"])
 
 
+def test_fused_backproject_equals_separate_kernel(G):
+    """gs_rasterize_backproject (O13 in the compositing epilogue; the Renderer's
+    default) writes exactly what gs_backproject writes from the same images."""
+    sc, vs = synth.make_config("C4", scale=0.01)
+    vs = vs[:4]
+    ds = G.DeviceScene(sc)
+    r = G.Renderer(ds, vs)
+    r.render()
+    torch.cuda.synchronize()
+    xyz2 = torch.full_like(r.xyz, float("nan"))
+    valid2 = torch.full_like(r.valid, 7)
+    G.gs_backproject(r.images, r.vb, r.a_min, xyz2, valid2)
+    torch.cuda.synchronize()
+    n = r.vb.total_pixels
+    assert int(r.valid[:n].sum()) > 0
+    assert torch.equal(r.valid[:n], valid2[:n])
+    assert torch.equal(r.xyz, xyz2)
+
+
 # ------------------------------------------------------------------ full-size sampled parity
 @pytest.mark.parametrize("cfg,views", [("C4", (0, 137)), ("C5", (9,))])
 def test_full_size_sampled_views(G, orc, cfg, views):
