@@ -635,6 +635,17 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     const float2 om = sub2_rn(1.0f, 1.0f, a1, a2);
                     const float w1 = blend_om(a1, om.x, r1[2]);
                     const float w2 = blend_om(a2, om.y, r2[2]);
+#ifdef GS_RASTER_STATS
+                    {
+                        const unsigned any1 = __ballot_sync(0xffffffffu, a1 > 0.f), any2 = __ballot_sync(0xffffffffu, a2 > 0.f);
+                        const unsigned b1 = __ballot_sync(0xffffffffu, w1 > 0.f), b2 = __ballot_sync(0xffffffffu, w2 > 0.f);
+                        if (lane == 0) {
+                            // entries with alpha >= alpha_min at some pixel of the warp; lane blends
+                            atomicAdd(&g_raster_stats[2], (unsigned long long)((any1 != 0) + (any2 != 0)));
+                            atomicAdd(&g_raster_stats[3], (unsigned long long)(__popc(b1) + __popc(b2)));
+                        }
+                    }
+#endif
                     if constexpr (WB) {
                         if (pend == 0) hold = s;
                         if constexpr (Smem::DIRECT) {

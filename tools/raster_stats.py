@@ -21,3 +21,5 @@ px = r.vb.total_pixels
 print("entry-walks per warp-tile: %.1f" % (walks / (r.vb.total_tiles * 8)))
 print("live lane fraction during walks: %.3f" % (live / (32.0 * walks)))
 print("entry-walks per pixel-lane: %.1f, live per pixel: %.1f" % (walks * 32 / px, live / px))
+print("walked entries with alpha >= alpha_min at some warp pixel: %.3f" % (out[2] / max(walks, 1)))
+print("blends per pixel: %.1f" % (out[3] / px))
