@@ -194,7 +194,18 @@ __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, f
     const float dx = d.x, dy = d.y;
     const float p = __fmaf_rn(dx, __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy)), __fmul_rn(__fmul_rn(b.x, dy), dy));
     const float alpha = fminf(P.alpha_max, __fmul_rn(b.y, ex2_ftz(p)));
-    return ((p > 0.0f) || (alpha < P.alpha_min)) ? 0.0f : alpha;
+    // skipped iff p > 0 or alpha < alpha_min (alpha is never NaN: fminf with alpha_max);
+    // one compare feeds the other so the pair costs two FSETP and one select
+    float r;
+    asm("{\n"
+        ".reg .pred pp, keep;\n"
+        "setp.gt.f32 pp, %1, 0f00000000;\n"
+        "setp.ge.and.f32 keep, %2, %3, !pp;\n"
+        "selp.f32 %0, %2, 0f00000000, keep;\n"
+        "}\n"
+        : "=f"(r)
+        : "f"(p), "f"(alpha), "f"(P.alpha_min));
+    return r;
 }
 
 // Persistent kernel: each CTA renders a sequence of tiles handed out in order by
@@ -378,6 +389,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     const uint32_t my_lanes = (tq * 32u) << 16;
     constexpr uint32_t IDESC = (1u << 4) | (1u << 16) | ((uint32_t)(D >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     uint32_t kstep = 0, tile_acc = 0;
+    uint32_t tnext = tA + my_lanes;   // DIRECT: TMEM column of the next weight pair (hi; lo at +8)
     // per-tile state
     const gs_view* V = nullptr;
     int W = 0, H = 0, sx = 0, sy = 0, px = 0, py = 0;
@@ -450,6 +462,13 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             __syncwarp();
             tile_acc = 1;
             ++kstep;
+            // DIRECT: the walk writes the next k-step's weights into the other buffer as it
+            // goes, so wait here (not per entry pair) for that buffer's MMA, issued one
+            // k-step ago and long finished
+            if constexpr (Smem::DIRECT) {
+                if (kstep >= 2) mbar_wait(&sm.mma_bar[warp][kstep & 1u], ((kstep >> 1) - 1u) & 1u);
+                tnext = tA + my_lanes + (kstep & 1u) * 16u;
+            }
         } else if constexpr (D > 0) {
             // m16n8k16 FP16 MMAs: weights split hi + lo (fp16 pairs, ~2^-22 exact), feature
             // rows rounded once to fp16 (error <= 2^-11 sum w|f|, inside 1e-3 max(1,|f|))
@@ -516,18 +535,17 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     uint32_t hold = 0;        // oldest stage a pending row references
     uint32_t rel = 0;         // next stage to release
     // DIRECT: weights of entries (2q, 2q+1) of the current k-step -> A column q (hi) and
-    // 8 + q (lo) of TMEM buffer kstep & 1; the buffer's previous MMA is waited for first
+    // 8 + q (lo) of TMEM buffer kstep & 1 (free: mma_block waited for its previous MMA)
     auto store_pair = [&](float w1, float w2, int q) {
         if constexpr (Smem::DIRECT) {
-            const uint32_t b = kstep & 1u;
-            if (q == 0 && kstep >= 2) mbar_wait(&sm.mma_bar[warp][b], ((kstep >> 1) - 1u) & 1u);
+            (void)q;   // column q of the k-step = tnext
             const __half2 h = __floats2half2_rn(w1, w2);
             const float2 hf = __half22float2(h);
             const float2 r = sub2_rn(w1, w2, hf.x, hf.y);
             const __half2 l = __floats2half2_rn(r.x, r.y);
-            const uint32_t col = tA + my_lanes + b * 16u + (uint32_t)q;
-            tmem_st1(col, *reinterpret_cast<const uint32_t*>(&h));
-            tmem_st1(col + 8u, *reinterpret_cast<const uint32_t*>(&l));
+            tmem_st1(tnext, *reinterpret_cast<const uint32_t*>(&h));
+            tmem_st1(tnext + 8u, *reinterpret_cast<const uint32_t*>(&l));
+            ++tnext;
         }
     };
     auto flush_pending = [&]() {
