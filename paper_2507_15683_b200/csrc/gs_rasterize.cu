@@ -632,10 +632,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 if (hit2) sm.ent[warp][n1 + __popc(msk2 & below)] = flat2 + j;
                 if (lane == 0 && (n & 1)) sm.ent[warp][n] = flat0 + SE;
                 __syncwarp();
-#pragma unroll 1
-                for (int i = 0; i < n; i += 2) {
-                    // two entries per iteration: independent alphas (ILP 2), transmittance in list order
-                    const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i]);   // i is even
+                // walk one entry pair: independent alphas (ILP 2), transmittance in list order
+                auto walk_pair = [&](const int2 kk, float& w1, float& w2) {
 #ifdef GS_RASTER_STATS
                     {
                         const unsigned live = __ballot_sync(0xffffffffu, !done);
@@ -651,8 +649,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     const float a2 = entry_alpha(r2[0], r2[1], pxf, pyf, P);
                     // 1 - alpha of both entries at once
                     const float2 om = sub2_rn(1.0f, 1.0f, a1, a2);
-                    const float w1 = blend_om(a1, om.x, r1[2]);
-                    const float w2 = blend_om(a2, om.y, r2[2]);
+                    w1 = blend_om(a1, om.x, r1[2]);
+                    w2 = blend_om(a2, om.y, r2[2]);
 #ifdef GS_RASTER_STATS
                     {
                         const unsigned any1 = __ballot_sync(0xffffffffu, a1 > 0.f), any2 = __ballot_sync(0xffffffffu, a2 > 0.f);
@@ -664,22 +662,41 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                         }
                     }
 #endif
-                    if constexpr (WB) {
+                };
+                const int ne = (n + 1) & ~1;   // entry pairs (an odd tail pairs with the null record)
+                if constexpr (WB) {
+                    // chunks that end at a k-step boundary: the pending-row bookkeeping (ring rows
+                    // of the weight rows, the oldest referenced stage) is done once per chunk
+                    for (int i = 0; i < ne;) {
                         if (pend == 0) hold = s;
-                        if constexpr (Smem::DIRECT) {
-                            store_pair(w1, w2, pend >> 1);
-                        } else {
-                            sm.wbuf[warp][pend][lane] = w1;
-                            sm.wbuf[warp][pend + 1][lane] = w2;
+                        const int m = min(ne - i, WB_ROWS - pend);
+                        if (lane < (uint32_t)m) sm.kent[warp][pend + (int)lane] = sm.ent[warp][i + (int)lane];
+#pragma unroll 1
+                        for (int j = 0; j < m; j += 2) {
+                            const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i + j]);   // i + j even
+                            float w1, w2;
+                            walk_pair(kk, w1, w2);
+                            if constexpr (Smem::DIRECT) {
+                                store_pair(w1, w2, (pend + j) >> 1);
+                            } else {
+                                sm.wbuf[warp][pend + j][lane] = w1;
+                                sm.wbuf[warp][pend + j + 1][lane] = w2;
+                            }
                         }
-                        if (lane == 0) { sm.kent[warp][pend] = kk.x; sm.kent[warp][pend + 1] = kk.y; }
-                        pend += 2;
+                        pend += m;
+                        i += m;
                         if (pend == WB_ROWS) {             // a full k-step: feed the tensor cores
                             __syncwarp();
                             mma_block(0, WB_ROWS);
                             __syncwarp();
                             pend = 0;
                         }
+                    }
+                } else {
+#pragma unroll 1
+                    for (int i = 0; i < ne; i += 2) {
+                        float w1, w2;
+                        walk_pair(*reinterpret_cast<const int2*>(&sm.ent[warp][i]), w1, w2);
                     }
                 }
                 warp_done = __all_sync(0xffffffffu, done);
