@@ -413,11 +413,17 @@ __device__ __forceinline__ void warp_bitonic_t(uint64_t (&k)[PER], uint32_t (&v)
 #pragma unroll
                 for (int j = 0; j < PER; ++j) {
                     if ((j & jd) == 0) {
+                        // branch-free compare-exchange (selects, no divergent swap)
                         const uint32_t e = lane * PER + (uint32_t)j;
                         const bool up = ((e >> s) & 1u) == 0u;
-                        if ((k[j] > k[j + jd]) == up) {
-                            const uint64_t t = k[j]; k[j] = k[j + jd]; k[j + jd] = t;
-                            if (PAY) { const uint32_t tv = v[j]; v[j] = v[j + jd]; v[j + jd] = tv; }
+                        const uint64_t a = k[j], b = k[j + jd];
+                        const bool sw = (a > b) == up;
+                        k[j] = sw ? b : a;
+                        k[j + jd] = sw ? a : b;
+                        if (PAY) {
+                            const uint32_t va = v[j], vb = v[j + jd];
+                            v[j] = sw ? vb : va;
+                            v[j + jd] = sw ? va : vb;
                         }
                     }
                 }
@@ -426,13 +432,16 @@ __device__ __forceinline__ void warp_bitonic_t(uint64_t (&k)[PER], uint32_t (&v)
                 const bool lower = (lane & ld) == 0u;
 #pragma unroll
                 for (int j = 0; j < PER; ++j) {
+                    // keep min(k, ok) when (lower == up), else max: one 64-bit compare + selects
                     const uint32_t e = lane * PER + (uint32_t)j;
                     const bool up = ((e >> s) & 1u) == 0u;
                     const uint64_t ok = __shfl_xor_sync(0xffffffffu, k[j], ld);
                     uint32_t ov = 0;
                     if (PAY) ov = __shfl_xor_sync(0xffffffffu, v[j], ld);
-                    const bool take = lower ? ((ok < k[j]) == up) : ((ok > k[j]) == up);
-                    if (take) { k[j] = ok; if (PAY) v[j] = ov; }
+                    const bool lt = ok < k[j];                 // keys are unique (index / gid in the key)
+                    const bool take = lt == (lower == up);
+                    k[j] = take ? ok : k[j];
+                    if (PAY) v[j] = take ? ov : v[j];
                 }
             }
         }
