@@ -142,20 +142,23 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // compared with e_cut (the alpha >= alpha_min ellipse, inflated).
 __device__ __forceinline__ bool ellipse_hits_rect(float u, float v, float ea, float eb, float ec, float ecut,
                                                   float x0, float x1, float y0, float y1) {
+    // branch-free (the lanes of a warp test different entries): both edge candidates are
+    // evaluated and the ones that do not apply are masked
     const bool inx = u >= x0 && u <= x1, iny = v >= y0 && v <= y1;
-    if (inx && iny) return true;
     float pmax = -3.4e38f;
-    if (!inx) {               // facing vertical edge: best dy = -eb dx / (2 ec), clamped
+    {                         // facing vertical edge: best dy = -eb dx / (2 ec), clamped
         const float dx = (u < x0 ? x0 : x1) - u;
         const float dy = fminf(fmaxf(-eb * dx * rcp_approx(2.f * ec), y0 - v), y1 - v);
-        pmax = fmaxf(pmax, ea * dx * dx + eb * dx * dy + ec * dy * dy);
+        const float pe = ea * dx * dx + eb * dx * dy + ec * dy * dy;
+        pmax = inx ? pmax : fmaxf(pmax, pe);
     }
-    if (!iny) {               // facing horizontal edge: best dx = -eb dy / (2 ea), clamped
+    {                         // facing horizontal edge: best dx = -eb dy / (2 ea), clamped
         const float dy = (v < y0 ? y0 : y1) - v;
         const float dx = fminf(fmaxf(-eb * dy * rcp_approx(2.f * ea), x0 - u), x1 - u);
-        pmax = fmaxf(pmax, ea * dx * dx + eb * dx * dy + ec * dy * dy);
+        const float pe = ea * dx * dx + eb * dx * dy + ec * dy * dy;
+        pmax = iny ? pmax : fmaxf(pmax, pe);
     }
-    return pmax >= ecut;
+    return (inx && iny) || pmax >= ecut;
 }
 
 // Blackwell packed fp32 (f32x2) arithmetic: each lane rounds exactly like the
