@@ -86,6 +86,9 @@ size_t ws_bytes(int64_t cap, int64_t T) {
 // single view where every counter is hot); otherwise it falls back to one
 // global reduction per pair.
 constexpr int BIN_THREADS = 512;
+#ifndef GS_BIN_MINB
+#define GS_BIN_MINB 3                  // count / scatter CTAs per SM the register budget is sized for (40 regs)
+#endif
 #ifndef GS_BIN_CTAS_PER_SM
 #define GS_BIN_CTAS_PER_SM 8
 #endif
@@ -104,7 +107,7 @@ __device__ __forceinline__ void rect_of(const uint4& q3, uint32_t& x0, uint32_t&
     npair = nx * ((q3.w >> 16) - y0 + 1);
 }
 
-__global__ void __launch_bounds__(BIN_THREADS)
+__global__ void __launch_bounds__(BIN_THREADS, GS_BIN_MINB)
 count_kernel(gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
              const gs_view* __restrict__ views, uint32_t* __restrict__ counts, const uint32_t* __restrict__ status,
              int tight) {
@@ -293,7 +296,7 @@ scan_down_kernel(const uint32_t* __restrict__ counts, int64_t T, const unsigned 
 // bucket entry: {depth_bits, record slot, gid, 0}; order inside a bucket is
 // arbitrary.  On-chip path: histogram the chunk, reserve each non-zero bin's
 // range with one global atomic, then place pairs with shared-memory atomics.
-__global__ void __launch_bounds__(BIN_THREADS)
+__global__ void __launch_bounds__(BIN_THREADS, GS_BIN_MINB)
 scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
                const gs_view* __restrict__ views, uint32_t* __restrict__ cursor, uint4* __restrict__ bucket,
                const uint32_t* __restrict__ status, int tight) {
