@@ -28,20 +28,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-// wait that suspends in hardware until the phase completes (or the time hint, in
-// ns, expires): a waiting warp issues a handful of instructions instead of
-// spinning on the scheduler its working neighbours need
-__device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(10000000u)
-        : "memory");
-}
 // wait with back-off: a warp with nothing else to do (the producer when the ring is
 // full) must not steal issue slots from the consumer warps of its scheduler
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
