@@ -110,7 +110,7 @@ __device__ __forceinline__ void rect_of(const uint4& q3, uint32_t& x0, uint32_t&
 __global__ void __launch_bounds__(BIN_THREADS, GS_BIN_MINB)
 count_kernel(gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
              const gs_view* __restrict__ views, uint32_t* __restrict__ counts, const uint32_t* __restrict__ status,
-             int tight) {
+             int tight, uint32_t* __restrict__ chunk_base, int cb_stride) {
     if (*status & GS_STATUS_RECORD_OVERFLOW) return;
     extern __shared__ uint32_t hist[];
     const int v = blockIdx.y;
@@ -199,8 +199,14 @@ count_kernel(gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restric
     }
     if (onchip) {
         __syncthreads();
-        for (int t = threadIdx.x; t < Tv; t += blockDim.x)
-            if (hist[t]) atomicAdd(&counts[toff + t], hist[t]);
+        // with chunk_base: keep this chunk's offset inside every tile's range (the scatter
+        // then needs no second histogram pass)
+        uint32_t* cb = chunk_base ? chunk_base + ((int64_t)v * gridDim.x + blockIdx.x) * cb_stride : nullptr;
+        for (int t = threadIdx.x; t < Tv; t += blockDim.x) {
+            const uint32_t c = hist[t];
+            const uint32_t b = c ? atomicAdd(&counts[toff + t], c) : 0u;
+            if (cb) cb[t] = b;
+        }
     }
 }
 
@@ -299,7 +305,8 @@ scan_down_kernel(const uint32_t* __restrict__ counts, int64_t T, const unsigned 
 __global__ void __launch_bounds__(BIN_THREADS, GS_BIN_MINB)
 scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
                const gs_view* __restrict__ views, uint32_t* __restrict__ cursor, uint4* __restrict__ bucket,
-               const uint32_t* __restrict__ status, int tight) {
+               const uint32_t* __restrict__ status, int tight, const uint32_t* __restrict__ chunk_base,
+               int cb_stride) {
     if (*status) return;
     extern __shared__ uint32_t hist[];
     const int v = blockIdx.y;
@@ -311,7 +318,12 @@ scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* _
     uint32_t k0, k1;
     chunk_of(nv, k0, k1);
     if (k0 >= k1) return;
-    if (onchip) {
+    if (onchip && chunk_base) {
+        // this chunk's base in bucket t = tile start + the chunk's offset from count_kernel
+        const uint32_t* cb = chunk_base + ((int64_t)v * gridDim.x + blockIdx.x) * cb_stride;
+        for (int t = threadIdx.x; t < Tv; t += blockDim.x) hist[t] = cursor[toff + t] + cb[t];
+        __syncthreads();
+    } else if (onchip) {
         for (int t = threadIdx.x; t < Tv; t += blockDim.x) hist[t] = 0u;
         __syncthreads();
         for (uint32_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
@@ -801,8 +813,16 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
         hist_attr = true;
     }
     const int tight = out->mode == GS_BIN_TIGHT;
+    // per-(view, chunk, tile) offsets of count_kernel for the scatter, kept in the big-sort
+    // scratch (unused until after the scatter) when it is large enough
+    const int cb_stride = std::min(max_tiles, HIST_MAX);
+    uint32_t* chunk_base = (max_tiles <= HIST_MAX &&
+                            (size_t)blocks_per_view * n_views * cb_stride * sizeof(uint32_t) <=
+                                sizeof(uint64_t) * (size_t)out->pair_capacity)
+                               ? reinterpret_cast<uint32_t*>(w.ka)
+                               : nullptr;
     count_kernel<<<rgrid, BIN_THREADS, hist_smem, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.counts, proj->status,
-                                                       tight);
+                                                       tight, chunk_base, cb_stride);
     if ((st = check_launch("count_kernel")) != GS_OK) return st;
     const int64_t nb = (T + SCAN_TILE - 1) / SCAN_TILE;
     scan_reduce_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(w.counts, T, w.block_sums);
@@ -810,7 +830,7 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     scan_down_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(w.counts, T, w.block_sums, out->ranges, w.cursor);
     if ((st = check_launch("scan kernels")) != GS_OK) return st;
     scatter_kernel<<<rgrid, BIN_THREADS, hist_smem, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.cursor, w.bucket,
-                                                          proj->status, tight);
+                                                          proj->status, tight, chunk_base, cb_stride);
     if ((st = check_launch("scatter_kernel")) != GS_OK) return st;
     // small batches (single views, pyramids): every list > 256 gets a 16-warp CTA
     // (latency); large batches: one warp per list <= 512, 4-warp CTAs above (throughput)
