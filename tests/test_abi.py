@@ -103,6 +103,14 @@ def test_validation_rejects_bad_arguments_without_touching_device(G):
     assert st == 2 and b"feat_dim" in L.gs_last_error()
     st = L.gs_backproject(None, v, ctypes.c_void_p(8), 1, ctypes.c_float(0.5), None, None, None)
     assert st == 1
+    # the fused raster + back-projection: NULL xyz / valid and a NaN a_min are rejected up front
+    s.feat_dim = 0
+    st = L.gs_rasterize_backproject(ctypes.byref(s), None, None, v, ctypes.c_void_p(8), 1, ctypes.byref(p), None,
+                                    ctypes.c_float(0.5), None, None, None)
+    assert st == 1 and b"xyz" in L.gs_last_error()
+    st = L.gs_rasterize_backproject(ctypes.byref(s), None, None, v, ctypes.c_void_p(8), 1, ctypes.byref(p), None,
+                                    ctypes.c_float(float("nan")), ctypes.c_void_p(16), ctypes.c_void_p(16), None)
+    assert st == 1 and b"a_min" in L.gs_last_error()
 
 
 def test_no_cpu_fallback_in_product_path():
