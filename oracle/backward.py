@@ -18,6 +18,16 @@ c = -R^T t, so dL/dd = sum_c dL/drgb_c [rgb_c > 0] sum_k f_kc grad b_k(d) with t
 basis polynomials of O10 differentiated term by term (zero for degree 0).
 Alg. 1's literal render-gradient test is ||dL/dmu|| > 0 for L = the
 sum of the rendered colour.
+
+`param_backward` continues the same chain to the Gaussian's other parameters
+(Theta_i of P:134: opacity, colour, scale, rotation): with G = dL/dSigma' =
+[[ga, gb/2], [gb/2, gc]] (a, b, c the entries of Sigma'), dL/dSigma =
+T^T G T (T = J R, rows T0, T1); Sigma = M M^T gives dL/dM = 2 dL/dSigma M;
+M = R(q) diag(s) gives dL/ds_i = sum_r dL/dM_ri R_ri and dL/dR = dL/dM diag(s);
+R(q) of the normalised quaternion (O4) is differentiated entry by entry and
+projected, dL/dq = (I - q^ q^T)/|q| dL/dq^; the SH coefficients get
+dL/df_kc = b_k(d) dL/drgb_c [rgb_c > 0]; the opacity gets dL/do directly (the
+record's o is the scene's linear opacity).
 """
 from __future__ import annotations
 
@@ -74,6 +84,100 @@ def sh_basis_grad(deg: int, d) -> np.ndarray:
     g[14] = (2 * c[5] * x * z, -2 * c[5] * y * z, c[5] * (xx - yy))
     g[15] = (c[6] * (3 * xx - 3 * yy), -6 * c[6] * x * y, 0.0)
     return g
+
+
+SH_C0 = 0.28209479177387814
+
+
+def sh_basis(deg: int, d) -> np.ndarray:
+    """O10's real SH basis b_k(d), k < (deg+1)^2 (the polynomials of gs_oracle.cpp)."""
+    x, y, z = (float(a) for a in d)
+    b = np.zeros((deg + 1) ** 2)
+    b[0] = SH_C0
+    if deg >= 1:
+        b[1], b[2], b[3] = -SH_C1 * y, SH_C1 * z, -SH_C1 * x
+    if deg >= 2:
+        c = SH_C2
+        b[4], b[5] = c[0] * x * y, c[1] * y * z
+        b[6] = c[2] * (2 * z * z - x * x - y * y)
+        b[7], b[8] = c[3] * x * z, c[4] * (x * x - y * y)
+    if deg >= 3:
+        c = SH_C3
+        xx, yy, zz = x * x, y * y, z * z
+        b[9] = c[0] * y * (3 * xx - yy)
+        b[10] = c[1] * x * y * z
+        b[11] = c[2] * y * (4 * zz - xx - yy)
+        b[12] = c[3] * z * (2 * zz - 3 * xx - 3 * yy)
+        b[13] = c[4] * x * (4 * zz - xx - yy)
+        b[14] = c[5] * z * (xx - yy)
+        b[15] = c[6] * x * (xx - 3 * yy)
+    return b
+
+
+def rotation_grads(q):
+    """dR/dw, dR/dx, dR/dy, dR/dz of O4's rotation matrix at the unit quaternion q."""
+    w, x, y, z = (float(a) for a in q)
+    return [np.array([[0, -2 * z, 2 * y], [2 * z, 0, -2 * x], [-2 * y, 2 * x, 0]]),
+            np.array([[0, 2 * y, 2 * z], [2 * y, -4 * x, -2 * w], [2 * z, 2 * w, -4 * x]]),
+            np.array([[-4 * y, 2 * x, 2 * w], [2 * x, 0, 2 * z], [-2 * w, 2 * z, -4 * y]]),
+            np.array([[-4 * z, -2 * w, 2 * x], [2 * w, -4 * z, 2 * y], [2 * x, 2 * y, 0]])]
+
+
+def param_backward(scene, view, rec, grec, params) -> dict:
+    """Per record: dL/d{scale [3], quat [4], opacity, sh [(deg+1)^2 * 3]} (fp64)."""
+    R = np.asarray(view.R, np.float64).reshape(3, 3)
+    t = np.asarray(view.t, np.float64).reshape(3)
+    fx, fy, cx, cy = float(view.fx), float(view.fy), float(view.cx), float(view.cy)
+    W, H = view.width, view.height
+    m = float(params.clamp_margin)
+    lox, hix = (-(m * W) - cx) / fx, ((1.0 + m) * W - cx) / fx
+    loy, hiy = (-(m * H) - cy) / fy, ((1.0 + m) * H - cy) / fy
+    dil = float(params.dilation)
+    cam = -R.T @ t
+    deg = int(scene.sh_degree)
+    nk = (deg + 1) ** 2
+    cnt = len(rec["gid"])
+    out = {"scale": np.zeros((cnt, 3)), "quat": np.zeros((cnt, 4)), "opacity": np.zeros(cnt),
+           "sh": np.zeros((cnt, nk * 3))}
+    for r, g in enumerate(rec["gid"]):
+        mu = scene.pos[:, g].astype(np.float64)
+        px, py, pz = R @ mu + t
+        qraw = scene.quat[:, g].astype(np.float64)
+        qn = float(np.linalg.norm(qraw))
+        qh = qraw / qn
+        w, x, y, z = qh
+        Rq = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                       [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                       [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+        sc = scene.scale[:, g].astype(np.float64)
+        M = Rq @ np.diag(sc)
+        Sg = M @ M.T
+        xcl = min(max(px / pz, lox), hix)
+        ycl = min(max(py / pz, loy), hiy)
+        T0 = (fx / pz) * R[0] + (-fx * xcl / pz) * R[2]
+        T1 = (fy / pz) * R[1] + (-fy * ycl / pz) * R[2]
+        a = T0 @ Sg @ T0 + dil
+        b = T0 @ Sg @ T1
+        c = T1 @ Sg @ T1 + dil
+        det = a * c - b * b
+        gu, gv, gea, geb, gec, gop, gr, gg, gb_, gz = grec[r]
+        gca, gcb, gcc = K * gea, 2.0 * K * geb, K * gec
+        d2 = det * det
+        ga = gca * (-c * c / d2) + gcb * (b * c / d2) + gcc * (1.0 / det - a * c / d2)
+        gb = gca * (2.0 * b * c / d2) + gcb * (-1.0 / det - 2.0 * b * b / d2) + gcc * (2.0 * a * b / d2)
+        gc = gca * (1.0 / det - c * a / d2) + gcb * (b * a / d2) + gcc * (-a * a / d2)
+        GS = ga * np.outer(T0, T0) + 0.5 * gb * (np.outer(T0, T1) + np.outer(T1, T0)) + gc * np.outer(T1, T1)
+        dM = 2.0 * GS @ M
+        out["scale"][r] = (dM * Rq).sum(axis=0)
+        dR = dM * sc[None, :]
+        dqh = np.array([(dR * G).sum() for G in rotation_grads(qh)])
+        out["quat"][r] = (dqh - qh * (qh @ dqh)) / qn
+        out["opacity"][r] = gop
+        grgb = np.array([gr, gg, gb_]) * (np.asarray(rec["rgb"][r], np.float64) > 0)
+        dv = mu - cam
+        bk = sh_basis(deg, dv / np.linalg.norm(dv))
+        out["sh"][r] = np.outer(bk, grgb).reshape(-1)
+    return out
 
 
 def mean_backward(scene, view, rec, grec, params) -> np.ndarray:

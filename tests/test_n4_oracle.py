@@ -256,3 +256,80 @@ def test_mean_grad_finite_differences_with_view_dependent_colour(orc, axis):
         s3.pos[axis, g] -= h
         fd = (loss(s2) - loss(s3)) / (2 * h)
         assert abs(fd - gmu[r, axis]) <= 5e-3 * max(abs(gmu[r, axis]), 1e-2), (r, fd, gmu[r, axis])
+
+
+# ------------------------------------------------------------------ projection backward (other parameters)
+def test_sh_basis_equals_the_c_oracle_colour(orc):
+    """backward.sh_basis (numpy) against the C oracle's O10 colour (a separate
+    implementation): with coefficients e_k + a large base term the colour is
+    linear and c = sum_k b_k f_k + 0.5 channel by channel."""
+    from oracle import backward as OB
+    rng = np.random.default_rng(51)
+    for deg in range(4):
+        nk = (deg + 1) ** 2
+        for _ in range(5):
+            d = rng.standard_normal(3)
+            d /= np.linalg.norm(d)
+            coeff = rng.standard_normal((nk, 3))
+            coeff[0] = 60.0
+            want = OB.sh_basis(deg, d) @ coeff + 0.5
+            np.testing.assert_allclose(orc.sh_color(deg, coeff, d), want, rtol=1e-12, atol=1e-12)
+
+
+def _aniso_fixture(deg):
+    from helpers import scene_of
+    rng = np.random.default_rng(61)
+    gs = []
+    for mu, s, o in (([0.1, -0.05, 2.0], [0.6, 0.35, 0.25], 0.5), ([-0.2, 0.1, 2.2], [0.45, 0.7, 0.3], 0.4),
+                     ([0.05, 0.2, 2.4], [0.8, 0.4, 0.5], 0.6)):
+        q = rng.standard_normal(4)
+        q = q / np.linalg.norm(q) * 1.3                    # un-normalised on purpose (O4 normalises)
+        sh = 0.3 * rng.standard_normal((deg + 1) ** 2 * 3)
+        sh[0:3] = 0.0
+        gs.append({"mu": mu, "scale": s, "opacity": o, "quat": q, "sh": sh})
+    return scene_of(gs, sh_degree=deg)
+
+
+@pytest.mark.parametrize("field", ["scale", "quat", "opacity", "sh"])
+def test_param_grads_finite_differences(orc, field):
+    """dL/d{scale, quat, opacity, SH} (oracle/backward.param_backward chaining the
+    record gradients through O4-O7 and O10) equal central differences of the
+    whole pipeline (project -> bin -> composite) on anisotropic, rotated
+    Gaussians with degree-3 colour."""
+    from oracle import backward as OB
+    sc = _aniso_fixture(3)
+    v = synth.make_view(np.eye(3), np.zeros(3), 8.0, 8.0, 11.5, 9.5, 24, 20)
+    P = orc.Params()
+    rng = np.random.default_rng(71)
+    gC = rng.standard_normal((3, 20, 24)).astype(np.float32)
+    gD = rng.standard_normal((20, 24)).astype(np.float32)
+    gA = rng.standard_normal((20, 24)).astype(np.float32)
+
+    def loss(scene):
+        r = orc.project(scene, v, P)
+        return orc.radiance_backward(v, r, orc.bin_keys(r, v), gC, gD, gA, P)[1]
+
+    rec = orc.project(sc, v, P)
+    assert (orc.render(sc, v)["flags"] == 0).all()
+    grec, _ = orc.radiance_backward(v, rec, orc.bin_keys(rec, v), gC, gD, gA, P)
+    got = OB.param_backward(sc, v, rec, grec, P)[field]
+    arr = {"scale": sc.scale, "quat": sc.quat, "opacity": sc.opacity[None, :], "sh": sc.sh}[field]
+    # a step can straddle a pixel's alpha >= 1/255 or stop threshold (the loss is only piecewise
+    # smooth); a correct derivative matches the central difference at one of three steps
+    hs = {"sh": (1e-2, 3e-3, 1e-3)}.get(field, (1e-3, 3e-4, 1e-4))
+    checked = 0
+    for r, g in enumerate(rec["gid"]):
+        for i in range(arr.shape[0]):
+            an = got[r] if field == "opacity" else got[r, i]
+            fds = []
+            for h in hs:
+                s2 = dataclasses.replace(sc, **{k: getattr(sc, k).copy() for k in ("scale", "quat", "opacity", "sh")})
+                s3 = dataclasses.replace(sc, **{k: getattr(sc, k).copy() for k in ("scale", "quat", "opacity", "sh")})
+                a2 = {"scale": s2.scale, "quat": s2.quat, "opacity": s2.opacity[None, :], "sh": s2.sh}[field]
+                a3 = {"scale": s3.scale, "quat": s3.quat, "opacity": s3.opacity[None, :], "sh": s3.sh}[field]
+                a2[i, g] += h
+                a3[i, g] -= h
+                fds.append((loss(s2) - loss(s3)) / (2 * h))
+            assert min(abs(fd - an) for fd in fds) <= 5e-3 * max(abs(an), 1e-2), (r, i, fds, an)
+            checked += abs(an) > 1e-2
+    assert checked > 0
