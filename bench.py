@@ -482,9 +482,25 @@ def main():
         b1.record(stream)
         torch.cuda.synchronize()
         msr = b0.elapsed_time(b1) / Kb
+        # projection backward: the record gradients to the 3D means and the other parameters
+        nk = (scene.sh_degree + 1) ** 2
+        gpos = torch.zeros(3 * scene.n, device=dev)
+        gsc, gq = torch.zeros(3 * scene.n, device=dev), torch.zeros(4 * scene.n, device=dev)
+        gop, gsh = torch.zeros(scene.n, device=dev), torch.zeros(nk * 3 * scene.n, device=dev)
+        G.gs_mean_backward(ds, r.proj, r.vb, r.params, grec, gpos, stream)
+        G.gs_param_backward(ds, r.proj, r.vb, r.params, grec, gsc, gq, gop, gsh, stream)
+        torch.cuda.synchronize()
+        b0.record(stream)
+        for _ in range(Kb):
+            G.gs_mean_backward(ds, r.proj, r.vb, r.params, grec, gpos, stream)
+            G.gs_param_backward(ds, r.proj, r.vb, r.params, grec, gsc, gq, gop, gsh, stream)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        msp = b0.elapsed_time(b1) / Kb
         n4 = {"views": n_views, "feature_backward_ms": ms4, "feature_backward_ms_per_view": ms4 / n_views,
               "radiance_backward_ms": msr, "radiance_backward_ms_per_view": msr / n_views,
-              "feat_dim": scene.feat_dim, "gpu_launches": 4}
+              "projection_backward_ms": msp, "feat_dim": scene.feat_dim, "gpu_launches": 6}
+        del gpos, gsc, gq, gop, gsh
         del gimg, gfeat, gout, grec
 
     # N2 refinement loop: B queries, n = 3 rounds, one CUDA graph

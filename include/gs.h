@@ -389,6 +389,24 @@ gs_status gs_mean_backward(const gs_scene* scene, const gs_projected* proj, cons
                            const gs_view* views_dev, int32_t n_views, const gs_params* params,
                            const float* grad_rec, float* grad_pos, void* stream);
 
+/*
+ * N4 projection backward, the other parameters of Theta_i: chains
+ * grad_rec through O4-O7 and O10 to the Gaussians' scale, rotation, opacity
+ * and SH coefficients.  With G = dL/dSigma' (Sigma' = [[a, b], [b, c]]),
+ * dL/dSigma = T^T G T (T = J R), Sigma = M M^T -> dL/dM = 2 dL/dSigma M,
+ * M = R(q) diag(s) -> dL/ds and dL/dR(q); the normalised quaternion's R(q) is
+ * differentiated and projected, dL/dq = (I - q^ q^T)/|q| dL/dq^;
+ * dL/df_kc = b_k(d) dL/drgb_c [rgb_c > 0]; dL/do from grad_rec directly.
+ * Outputs in the layouts of gs_scene: grad_scale [3][n], grad_quat [4][n],
+ * grad_opacity [n], grad_sh [(deg+1)^2 * 3][n]; each optional (NULL = skip);
+ * accumulated over records and views (caller zeroes), fp64 arithmetic, f32
+ * atomics.  Errors as gs_mean_backward.
+ */
+gs_status gs_param_backward(const gs_scene* scene, const gs_projected* proj, const gs_view* views_host,
+                            const gs_view* views_dev, int32_t n_views, const gs_params* params,
+                            const float* grad_rec, float* grad_scale, float* grad_quat, float* grad_opacity,
+                            float* grad_sh, void* stream);
+
 /* Eq. 2's L1 feature loss: grad_image[i] = scale * sign(rendered[i] - target[i]);
  * *loss (device double, accumulated) += scale * sum |rendered - target|. */
 gs_status gs_feature_l1_grad(const float* rendered, const float* target, int64_t n, float scale,

@@ -586,12 +586,150 @@ __global__ void mean_backward_kernel(gs_scene S, const gs_view* __restrict__ vie
     for (int k = 0; k < 3; ++k) atomicAdd(&grad_pos[(int64_t)k * n + g], (float)gm[k]);
 }
 
+// dL/d{scale, quat, opacity, SH} of one record (gs_param_backward): the chain of
+// mean_backward_kernel up to G = dL/dSigma', then dL/dSigma = T^T G T, Sigma = M M^T,
+// M = R(q) diag(s), the normalised quaternion, and O10's basis for the SH rows
+__global__ void param_backward_kernel(gs_scene S, const gs_view* __restrict__ views, gs_params P,
+                                      const gs_record* __restrict__ rec, int64_t cap,
+                                      const uint32_t* __restrict__ n_rec, int n_views,
+                                      const float* __restrict__ grad_rec, float* __restrict__ g_scale,
+                                      float* __restrict__ g_quat, float* __restrict__ g_opacity,
+                                      float* __restrict__ g_sh) {
+    const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (slot >= cap * n_views) return;
+    const int vi = (int)(slot / cap);
+    if ((uint32_t)(slot - (int64_t)vi * cap) >= min((uint64_t)n_rec[vi], (uint64_t)cap)) return;
+    const float* gr = grad_rec + slot * 10;
+    const gs_record& rc = rec[slot];
+    const int64_t n = S.n;
+    const uint32_t g = rc.gid;
+    if (g_opacity && gr[5] != 0.0f) atomicAdd(&g_opacity[g], gr[5]);
+    const gs_view& V = views[vi];
+    double R[9], t[3];
+    for (int k = 0; k < 9; ++k) R[k] = V.R[k];
+    for (int k = 0; k < 3; ++k) t[k] = V.t[k];
+    const double mx = S.pos[g], my = S.pos[n + g], mz = S.pos[2 * n + g];
+    if (g_sh) {
+        double grgb[3];
+        for (int c = 0; c < 3; ++c) grgb[c] = rc.rgb[c] > 0.0f ? (double)gr[6 + c] : 0.0;
+        if (grgb[0] != 0.0 || grgb[1] != 0.0 || grgb[2] != 0.0) {
+            double dv[3] = {mx, my, mz};
+            for (int k = 0; k < 3; ++k) dv[k] += R[k] * t[0] + R[3 + k] * t[1] + R[6 + k] * t[2];
+            const double dn = sqrt(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
+            const double x = dv[0] / dn, y = dv[1] / dn, z = dv[2] / dn;
+            double b[16];
+            b[0] = 0.28209479177387814;
+            const double C1 = 0.4886025119029199;
+            b[1] = -C1 * y; b[2] = C1 * z; b[3] = -C1 * x;
+            const double xx = x * x, yy = y * y, zz = z * z;
+            b[4] = 1.0925484305920792 * x * y; b[5] = -1.0925484305920792 * y * z;
+            b[6] = 0.31539156525252005 * (2 * zz - xx - yy); b[7] = -1.0925484305920792 * x * z;
+            b[8] = 0.5462742152960396 * (xx - yy);
+            b[9] = -0.5900435899266435 * y * (3 * xx - yy); b[10] = 2.890611442640554 * x * y * z;
+            b[11] = -0.4570457994644658 * y * (4 * zz - xx - yy);
+            b[12] = 0.3731763325901154 * z * (2 * zz - 3 * xx - 3 * yy);
+            b[13] = -0.4570457994644658 * x * (4 * zz - xx - yy); b[14] = 1.445305721320277 * z * (xx - yy);
+            b[15] = -0.5900435899266435 * x * (xx - 3 * yy);
+            const int nk = (S.sh_degree + 1) * (S.sh_degree + 1);
+            for (int k = 0; k < nk; ++k)
+                for (int c = 0; c < 3; ++c)
+                    if (grgb[c] != 0.0) atomicAdd(&g_sh[(int64_t)(k * 3 + c) * n + g], (float)(b[k] * grgb[c]));
+        }
+    }
+    const double gea = gr[2], geb = gr[3], gec = gr[4];
+    if ((!g_scale && !g_quat) || (gea == 0.0 && geb == 0.0 && gec == 0.0)) return;
+    const double px = R[0] * mx + R[1] * my + R[2] * mz + t[0];
+    const double py = R[3] * mx + R[4] * my + R[5] * mz + t[1];
+    const double pz = R[6] * mx + R[7] * my + R[8] * mz + t[2];
+    const double q0 = S.quat[g], q1 = S.quat[n + g], q2 = S.quat[2 * n + g], q3 = S.quat[3 * n + g];
+    const double qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+    const double qw = q0 / qn, qx = q1 / qn, qy = q2 / qn, qz = q3 / qn;
+    const double sc[3] = {S.scale[g], S.scale[n + g], S.scale[2 * n + g]};
+    const double Rq[9] = {1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qw * qz), 2 * (qx * qz + qw * qy),
+                          2 * (qx * qy + qw * qz), 1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qw * qx),
+                          2 * (qx * qz - qw * qy), 2 * (qy * qz + qw * qx), 1 - 2 * (qx * qx + qy * qy)};
+    double M[9];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) M[r * 3 + c] = Rq[r * 3 + c] * sc[c];
+    double Sg[9];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) Sg[r * 3 + c] = M[r * 3] * M[c * 3] + M[r * 3 + 1] * M[c * 3 + 1] + M[r * 3 + 2] * M[c * 3 + 2];
+    const double fx = V.fx, fy = V.fy, cx = V.cx, cy = V.cy, W = V.width, H = V.height, m = P.clamp_margin;
+    const double lox = (-(m * W) - cx) / fx, hix = ((1.0 + m) * W - cx) / fx;
+    const double loy = (-(m * H) - cy) / fy, hiy = ((1.0 + m) * H - cy) / fy;
+    const double xcl = fmin(fmax(px / pz, lox), hix), ycl = fmin(fmax(py / pz, loy), hiy);
+    const double j00 = fx / pz, j11 = fy / pz, j02 = -fx * xcl / pz, j12 = -fy * ycl / pz;
+    double T0[3], T1[3], ST0[3], ST1[3];
+    for (int k = 0; k < 3; ++k) { T0[k] = j00 * R[k] + j02 * R[6 + k]; T1[k] = j11 * R[3 + k] + j12 * R[6 + k]; }
+    for (int r = 0; r < 3; ++r) {
+        ST0[r] = Sg[r * 3] * T0[0] + Sg[r * 3 + 1] * T0[1] + Sg[r * 3 + 2] * T0[2];
+        ST1[r] = Sg[r * 3] * T1[0] + Sg[r * 3 + 1] * T1[1] + Sg[r * 3 + 2] * T1[2];
+    }
+    const double a = T0[0] * ST0[0] + T0[1] * ST0[1] + T0[2] * ST0[2] + P.dilation;
+    const double b = T0[0] * ST1[0] + T0[1] * ST1[1] + T0[2] * ST1[2];
+    const double c = T1[0] * ST1[0] + T1[1] * ST1[1] + T1[2] * ST1[2] + P.dilation;
+    const double det = a * c - b * b, d2 = det * det;
+    const double K = (double)K_EXP2;
+    const double gca = K * gea, gcb = 2.0 * K * geb, gcc = K * gec;
+    const double ga = gca * (-c * c / d2) + gcb * (b * c / d2) + gcc * (1.0 / det - a * c / d2);
+    const double gb = gca * (2.0 * b * c / d2) + gcb * (-1.0 / det - 2.0 * b * b / d2) + gcc * (2.0 * a * b / d2);
+    const double gc = gca * (1.0 / det - c * a / d2) + gcb * (b * a / d2) + gcc * (-a * a / d2);
+    // dL/dM = 2 GS M, GS = ga T0 T0^T + gb (T0 T1^T + T1 T0^T) / 2 + gc T1 T1^T
+    double GS[9];
+    for (int r = 0; r < 3; ++r)
+        for (int cc = 0; cc < 3; ++cc)
+            GS[r * 3 + cc] = ga * T0[r] * T0[cc] + 0.5 * gb * (T0[r] * T1[cc] + T1[r] * T0[cc]) + gc * T1[r] * T1[cc];
+    double dM[9];
+    for (int r = 0; r < 3; ++r)
+        for (int cc = 0; cc < 3; ++cc)
+            dM[r * 3 + cc] = 2.0 * (GS[r * 3] * M[cc] + GS[r * 3 + 1] * M[3 + cc] + GS[r * 3 + 2] * M[6 + cc]);
+    if (g_scale)
+        for (int i = 0; i < 3; ++i)
+            atomicAdd(&g_scale[(int64_t)i * n + g],
+                      (float)(dM[i] * Rq[i] + dM[3 + i] * Rq[3 + i] + dM[6 + i] * Rq[6 + i]));
+    if (g_quat) {
+        double dR[9];
+        for (int r = 0; r < 3; ++r)
+            for (int cc = 0; cc < 3; ++cc) dR[r * 3 + cc] = dM[r * 3 + cc] * sc[cc];
+        // dR/dw, dR/dx, dR/dy, dR/dz of O4's matrix (row-major)
+        const double Gw[9] = {0, -2 * qz, 2 * qy, 2 * qz, 0, -2 * qx, -2 * qy, 2 * qx, 0};
+        const double Gx[9] = {0, 2 * qy, 2 * qz, 2 * qy, -4 * qx, -2 * qw, 2 * qz, 2 * qw, -4 * qx};
+        const double Gy[9] = {-4 * qy, 2 * qx, 2 * qw, 2 * qx, 0, 2 * qz, -2 * qw, 2 * qz, -4 * qy};
+        const double Gz[9] = {-4 * qz, -2 * qw, 2 * qx, 2 * qw, -4 * qz, 2 * qy, 2 * qx, 2 * qy, 0};
+        double dq[4] = {0, 0, 0, 0};
+        for (int k = 0; k < 9; ++k) {
+            dq[0] += dR[k] * Gw[k]; dq[1] += dR[k] * Gx[k]; dq[2] += dR[k] * Gy[k]; dq[3] += dR[k] * Gz[k];
+        }
+        const double qh[4] = {qw, qx, qy, qz};
+        const double pr = qh[0] * dq[0] + qh[1] * dq[1] + qh[2] * dq[2] + qh[3] * dq[3];
+        for (int i = 0; i < 4; ++i) atomicAdd(&g_quat[(int64_t)i * n + g], (float)((dq[i] - qh[i] * pr) / qn));
+    }
+}
+
 }  // namespace
 }  // namespace gs
 
 using namespace gs;
 
 extern "C" {
+
+gs_status gs_param_backward(const gs_scene* scene, const gs_projected* proj, const gs_view* views_host,
+                            const gs_view* views_dev, int32_t n_views, const gs_params* params,
+                            const float* grad_rec, float* grad_scale, float* grad_quat, float* grad_opacity,
+                            float* grad_sh, void* stream) {
+    gs_status st = validate_scene(scene, true);
+    if (st != GS_OK) return st;
+    st = validate_views(views_host, views_dev, n_views, nullptr, nullptr);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(params && proj && proj->rec && proj->n_rec && grad_rec, GS_INVALID_ARG,
+               "gs_param_backward: NULL pointer");
+    const int64_t total = proj->rec_capacity * (int64_t)n_views;
+    if (total == 0 || (!grad_scale && !grad_quat && !grad_opacity && !grad_sh)) return GS_OK;
+    param_backward_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        *scene, views_dev, *params, proj->rec, proj->rec_capacity, proj->n_rec, n_views, grad_rec, grad_scale,
+        grad_quat, grad_opacity, grad_sh);
+    return check_launch("param_backward_kernel");
+}
 
 size_t gs_project_workspace_bytes(int32_t n_blocks, int32_t n_views) {
     if (n_views < 1) n_views = 1;

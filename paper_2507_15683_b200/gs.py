@@ -71,7 +71,7 @@ class gs_images(ctypes.Structure):
 EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_layout", "gs_scene_block_bounds",
            "gs_scene_features_f16", "gs_validate_scene", "gs_match", "gs_match_workspace_bytes",
            "gs_pnp", "gs_pnp_workspace_bytes", "gs_verify_consistency", "gs_feature_backward", "gs_radiance_backward",
-           "gs_mean_backward",
+           "gs_mean_backward", "gs_param_backward",
            "gs_feature_l1_grad", "gs_feature_sgd",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_rasterize_backproject", "gs_backproject", "gs_visibility_score",
@@ -502,3 +502,13 @@ def gs_mean_backward(scene: "DeviceScene", proj: "Projected", views, params: gs_
     _check(lib().gs_mean_backward(ctypes.byref(scene.struct), ctypes.byref(proj.struct), views.host, views.dev_ptr,
                                   ctypes.c_int32(views.n), ctypes.byref(params), _ptr(grad_rec), _ptr(grad_pos),
                                   _stream(stream)), "gs_mean_backward")
+
+
+def gs_param_backward(scene: "DeviceScene", proj: "Projected", views, params: gs_params, grad_rec: torch.Tensor,
+                      grad_scale=None, grad_quat=None, grad_opacity=None, grad_sh=None, stream=None):
+    """Accumulated SoA gradients like the scene planes: grad_scale [3 * n], grad_quat [4 * n],
+    grad_opacity [n], grad_sh [(deg+1)^2 * 3 * n] (f32; each optional)."""
+    _check(lib().gs_param_backward(ctypes.byref(scene.struct), ctypes.byref(proj.struct), views.host, views.dev_ptr,
+                                   ctypes.c_int32(views.n), ctypes.byref(params), _ptr(grad_rec), _ptr(grad_scale),
+                                   _ptr(grad_quat), _ptr(grad_opacity), _ptr(grad_sh), _stream(stream)),
+           "gs_param_backward")

@@ -212,3 +212,48 @@ def test_alg1_literal_render_gradient_matches_forward_criterion(G):
     literal = np.linalg.norm(gpos.view(3, sc.n).cpu().numpy()[:, gid], axis=0) > 0
     assert contrib.sum() > 100
     assert (literal == contrib).mean() > 0.99, ((literal != contrib).sum(), n)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_param_backward_vs_oracle(G, orc, seed):
+    """gs_param_backward (scale, rotation, opacity, SH rows) against
+    oracle/backward.param_backward on the same record gradients."""
+    from oracle import backward as OB
+    rng = np.random.default_rng(700 + seed)
+    sc = random_tiny_scene(rng, int(rng.integers(50, 250)), sh_degree=seed % 4)
+    W, H = int(rng.integers(16, 90)), int(rng.integers(12, 70))
+    R, t = synth.look_from([0.3, -0.2, -0.5], [0.05, 0.03, 1.0])
+    v = synth.make_view(np.asarray(R, np.float32), np.asarray(t, np.float32), 40.0, 40.0, W / 2 - 0.5, H / 2 - 0.5,
+                        W, H)
+    ds = G.DeviceScene(sc)
+    r = G.Renderer(ds, [v], backproject=False)
+    r.render()
+    gout = G.Images(r.vb.total_pixels, 0)
+    ups = []
+    for tt in (gout.rgb, gout.depth, gout.alpha):
+        a = rng.standard_normal(tt.numel()).astype(np.float32)
+        tt.copy_(torch.from_numpy(a))
+        ups.append(a)
+    cap = r.proj.rec_capacity
+    grec = torch.zeros(cap * 10, dtype=torch.float32, device="cuda")
+    G.gs_radiance_backward(r.proj, r.bins, r.vb, r.params, r.images, gout, grec)
+    nk = (sc.sh_degree + 1) ** 2
+    outs = {"scale": torch.zeros(3 * sc.n, device="cuda"), "quat": torch.zeros(4 * sc.n, device="cuda"),
+            "opacity": torch.zeros(sc.n, device="cuda"), "sh": torch.zeros(nk * 3 * sc.n, device="cuda")}
+    G.gs_param_backward(ds, r.proj, r.vb, r.params, grec, outs["scale"], outs["quat"], outs["opacity"], outs["sh"])
+    torch.cuda.synchronize()
+    o = orc.render(sc, v, binning="tight")
+    P = orc.Params()
+    want_rec, _ = orc.radiance_backward(v, o["rec"], o["keys"], ups[0].reshape(3, H, W), ups[1].reshape(H, W),
+                                        ups[2].reshape(H, W), P)
+    want = OB.param_backward(sc, v, o["rec"], want_rec, P)
+    flagged = int((o["flags"] != 0).sum())
+    gids = o["rec"]["gid"]
+    for name, rows in (("scale", 3), ("quat", 4), ("opacity", 1), ("sh", nk * 3)):
+        got = outs[name].view(rows, sc.n).cpu().numpy().astype(np.float64).T       # [n][rows]
+        w = np.zeros((sc.n, rows))
+        w[gids] = want[name].reshape(len(gids), rows)
+        scale = float(np.abs(w).max())
+        bad = (np.abs(got - w) > 5e-3 * scale + 1e-4).any(1)
+        assert bad.sum() <= (max(2, 0.02 * sc.n) if flagged else 0), (name, bad.sum(), flagged, scale)
+        assert scale > 0, name
