@@ -14,7 +14,7 @@ from .gs import (GSError, DeviceScene, ViewBatch, Projected, Bins, Images, defau
                  gs_param_backward,
                  lib, LIB_PATH,
                  EXPORTS)
-from .pipeline import Renderer, SignificanceScorer, Refiner, FeatureDistiller  # noqa: F401
+from .pipeline import Renderer, SignificanceScorer, Refiner, FeatureDistiller, SceneTrainer  # noqa: F401
 
 __all__ = ["gs_project", "gs_bin_sort", "gs_rasterize", "gs_rasterize_backproject", "gs_backproject", "gs_visibility_score", "gs_match",
            "gs_validate_scene", "gs_pnp", "gs_verify_consistency", "Matches", "Refiner", "DeviceScene",

@@ -478,6 +478,12 @@ def gs_feature_l1_grad(rendered: torch.Tensor, target: torch.Tensor, scale: floa
            "gs_feature_l1_grad")
 
 
+def gs_scene_block_bounds(scene: "DeviceScene", stream=None):
+    """Recompute the scene's per-block culling bounds (after its means or scales changed)."""
+    _check(lib().gs_scene_block_bounds(ctypes.byref(scene.struct), _ptr(scene.block_bounds), _stream(stream)),
+           "gs_scene_block_bounds")
+
+
 def gs_feature_sgd(feat: torch.Tensor, grad_feat: torch.Tensor, lr: float, feat_h: Optional[torch.Tensor] = None,
                    stream=None):
     _check(lib().gs_feature_sgd(_ptr(feat), _ptr(grad_feat), ctypes.c_int64(feat.numel()), ctypes.c_float(lr),

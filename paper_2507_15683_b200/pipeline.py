@@ -286,3 +286,64 @@ class FeatureDistiller:
                               self.gfeat, stream)
         G.gs_feature_sgd(self.scene.feat, self.gfeat, self.lr, self.scene.feat_h, stream)
         return self.loss
+
+
+class SceneTrainer:
+    """N4: a joint training step of Eq. 1, L = alpha L_f + beta L_rgb, with L1 terms
+    (Eq. 2's feature term; the RGB term without Eq. 3's D-SSIM part).  Per step:
+    render the batch; gs_feature_l1_grad on the RGB planes; gs_radiance_backward to
+    the records; gs_mean_backward + gs_param_backward to every Gaussian parameter;
+    for a feature scene also gs_feature_l1_grad + gs_feature_backward on the
+    features (geometry frozen for L_f); then one gs_feature_sgd step per parameter
+    plane and the block bounds refreshed.  No densification / pruning."""
+
+    PLANES = ("pos", "scale", "quat", "opacity", "sh")
+
+    def __init__(self, scene: G.DeviceScene, views: Sequence, target_rgb: torch.Tensor,
+                 target_feat: Optional[torch.Tensor] = None, lr: Optional[dict] = None, alpha: float = 1.0,
+                 beta: float = 1.0):
+        self.scene = scene
+        self.r = Renderer(scene, views, backproject=False)
+        self.r.render().fit_capacities(slack=1.5)
+        self.target_rgb, self.target_feat = target_rgb, target_feat
+        # steps for losses that are means over all pixels (and channels)
+        self.lr = {"pos": 1.0, "scale": 1e-2, "quat": 1e-1, "opacity": 1.0, "sh": 10.0, "feat": 1000.0}
+        self.lr.update(lr or {})
+        dev = scene.pos.device
+        self.rgb_scale = beta / self.r.images.rgb.numel()
+        self.gout = G.Images(self.r.vb.total_pixels, 0, device=dev)
+        self.gout.depth.zero_()
+        self.gout.alpha.zero_()
+        self.grec = torch.zeros(self.r.vb.n * self.r.proj.rec_capacity * 10, dtype=torch.float32, device=dev)
+        self.grads = {k: torch.zeros_like(getattr(scene, k)) for k in self.PLANES}
+        self.feat_scale = 0.0
+        if target_feat is not None:
+            assert scene.feat is not None
+            self.feat_scale = alpha / self.r.images.feat.numel()
+            self.gimg = torch.empty_like(self.r.images.feat)
+            self.gfeat = torch.zeros_like(scene.feat)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def step(self, stream=None) -> torch.Tensor:
+        """One iteration; returns the device loss of the parameters before the update."""
+        sc, r = self.scene, self.r
+        r.run(stream)
+        self.loss.zero_()
+        G.gs_feature_l1_grad(r.images.rgb, self.target_rgb, self.rgb_scale, self.gout.rgb, self.loss, stream)
+        self.grec.zero_()
+        G.gs_radiance_backward(r.proj, r.bins, r.vb, r.params, r.images, self.gout, self.grec, stream)
+        for g in self.grads.values():
+            g.zero_()
+        G.gs_mean_backward(sc, r.proj, r.vb, r.params, self.grec, self.grads["pos"], stream)
+        G.gs_param_backward(sc, r.proj, r.vb, r.params, self.grec, self.grads["scale"], self.grads["quat"],
+                            self.grads["opacity"], self.grads["sh"], stream)
+        if self.target_feat is not None:
+            G.gs_feature_l1_grad(r.images.feat, self.target_feat, self.feat_scale, self.gimg, self.loss, stream)
+            self.gfeat.zero_()
+            G.gs_feature_backward(sc, r.proj, r.bins, r.vb, r.params, self.gimg, self.gfeat, stream)
+            G.gs_feature_sgd(sc.feat, self.gfeat, self.lr["feat"], sc.feat_h, stream)
+        for k in self.PLANES:
+            G.gs_feature_sgd(getattr(sc, k), self.grads[k], self.lr[k], None, stream)
+        if sc.block_bounds is not None:
+            G.gs_scene_block_bounds(sc, stream)   # the means moved
+        return self.loss

@@ -257,3 +257,24 @@ def test_param_backward_vs_oracle(G, orc, seed):
         bad = (np.abs(got - w) > 5e-3 * scale + 1e-4).any(1)
         assert bad.sum() <= (max(2, 0.02 * sc.n) if flagged else 0), (name, bad.sum(), flagged, scale)
         assert scale > 0, name
+
+
+def test_scene_training_reduces_rgb_loss(G):
+    """Eq. 1 with the RGB term (SceneTrainer): targets rendered from the true scene,
+    training starts from jittered means and colours; every parameter plane gets its
+    gradient from gs_radiance_backward -> gs_mean_backward / gs_param_backward.
+    40 steps cut the L1 loss by > 40 %."""
+    base = synth.box_v1(1500, seed=21, sh_degree=1)
+    v = synth.box_view()
+    rt = G.Renderer(G.DeviceScene(base), [v], backproject=False)
+    rt.render()
+    target = rt.images.rgb.clone()
+    rng = np.random.default_rng(5)
+    start = dataclasses.replace(base, pos=base.pos + rng.normal(0, 0.02, base.pos.shape).astype(np.float32),
+                                sh=base.sh + rng.normal(0, 0.3, base.sh.shape).astype(np.float32))
+    t = G.SceneTrainer(G.DeviceScene(start), [v], target)
+    losses = [float(t.step().item()) for _ in range(40)]
+    torch.cuda.synchronize()
+    assert t.r.status() == 0
+    assert losses[0] > 0.02
+    assert losses[-1] < 0.6 * losses[0], losses[::8]
