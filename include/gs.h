@@ -415,6 +415,14 @@ gs_status gs_feature_l1_grad(const float* rendered, const float* target, int64_t
 /* feat[i] -= lr * grad_feat[i] over n floats; refreshes the fp16 copy (gs_scene.feat_h) when feat_h != NULL. */
 gs_status gs_feature_sgd(float* feat, const float* grad_feat, int64_t n, float lr, void* feat_h, void* stream);
 
+/* One Adam step over n floats (the optimiser of 3DGS-style training, N4):
+ * m = b1 m + (1 - b1) g; v = b2 v + (1 - b2) g^2;
+ * param -= lr (m / (1 - b1^step)) / (sqrt(v / (1 - b2^step)) + eps), step >= 1.
+ * m, v: caller-owned state (zero-initialised), fp32; param_h as in gs_feature_sgd.
+ * Errors: GS_INVALID_ARG for NULL pointers, n < 0 or step < 1. */
+gs_status gs_adam(float* param, const float* grad, float* m, float* v, int64_t n, float lr, float beta1,
+                  float beta2, float eps, int32_t step, void* param_h, void* stream);
+
 /* Workspace of gs_project: a (view x block) visibility bitmask. */
 size_t gs_project_workspace_bytes(int32_t n_blocks, int32_t n_views);
 

@@ -41,6 +41,7 @@
 //   * warp-ballot early termination once all 32 pixels have T < t_min.
 #include <cuda_fp16.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1168,6 +1169,21 @@ __global__ void l1_grad_kernel(const float* __restrict__ F, const float* __restr
     if ((threadIdx.x & 31) == 0) atomicAdd(loss, part);
 }
 
+__global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps, float bc1,
+                            float bc2, __half* __restrict__ ph) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float gi = g[i];
+        const float mi = b1 * m[i] + (1.0f - b1) * gi;
+        const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+        m[i] = mi;
+        v[i] = vi;
+        const float pi = p[i] - lr * (mi * bc1) / (sqrtf(vi * bc2) + eps);
+        p[i] = pi;
+        if (ph) ph[i] = __float2half_rn(pi);
+    }
+}
+
 __global__ void sgd_kernel(float* __restrict__ feat, const float* __restrict__ grad, int64_t n, float lr,
                            __half* __restrict__ feat_h) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1313,6 +1329,18 @@ extern "C" gs_status gs_feature_sgd(float* feat, const float* grad_feat, int64_t
     sgd_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(feat, grad_feat, n, lr,
                                                                    reinterpret_cast<__half*>(feat_h));
     return check_launch("sgd_kernel");
+}
+
+extern "C" gs_status gs_adam(float* param, const float* grad, float* m, float* v, int64_t n, float lr, float beta1,
+                              float beta2, float eps, int32_t step, void* param_h, void* stream) {
+    GS_REQUIRE(param && grad && m && v && n >= 0 && step >= 1, GS_INVALID_ARG, "gs_adam: bad args");
+    if (n == 0) return GS_OK;
+    const float bc1 = (float)(1.0 / (1.0 - std::pow((double)beta1, step)));
+    const float bc2 = (float)(1.0 / (1.0 - std::pow((double)beta2, step)));
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+    adam_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(param, grad, m, v, n, lr, beta1, beta2, eps, bc1,
+                                                                    bc2, reinterpret_cast<__half*>(param_h));
+    return check_launch("adam_kernel");
 }
 
 extern "C" gs_status gs_radiance_backward(const gs_projected* proj, const gs_bins* bins, const gs_view* views_host,

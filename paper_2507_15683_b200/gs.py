@@ -71,7 +71,7 @@ class gs_images(ctypes.Structure):
 EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_layout", "gs_scene_block_bounds",
            "gs_scene_features_f16", "gs_validate_scene", "gs_match", "gs_match_workspace_bytes",
            "gs_pnp", "gs_pnp_workspace_bytes", "gs_verify_consistency", "gs_feature_backward", "gs_radiance_backward",
-           "gs_mean_backward", "gs_param_backward",
+           "gs_mean_backward", "gs_param_backward", "gs_adam",
            "gs_feature_l1_grad", "gs_feature_sgd",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_rasterize_backproject", "gs_backproject", "gs_visibility_score",
@@ -482,6 +482,14 @@ def gs_scene_block_bounds(scene: "DeviceScene", stream=None):
     """Recompute the scene's per-block culling bounds (after its means or scales changed)."""
     _check(lib().gs_scene_block_bounds(ctypes.byref(scene.struct), _ptr(scene.block_bounds), _stream(stream)),
            "gs_scene_block_bounds")
+
+
+def gs_adam(param: torch.Tensor, grad: torch.Tensor, m: torch.Tensor, v: torch.Tensor, lr: float, step: int,
+            beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-15, param_h: Optional[torch.Tensor] = None,
+            stream=None):
+    _check(lib().gs_adam(_ptr(param), _ptr(grad), _ptr(m), _ptr(v), ctypes.c_int64(param.numel()), ctypes.c_float(lr),
+                         ctypes.c_float(beta1), ctypes.c_float(beta2), ctypes.c_float(eps), ctypes.c_int32(step),
+                         _ptr(param_h), _stream(stream)), "gs_adam")
 
 
 def gs_feature_sgd(feat: torch.Tensor, grad_feat: torch.Tensor, lr: float, feat_h: Optional[torch.Tensor] = None,

@@ -294,20 +294,25 @@ class SceneTrainer:
     render the batch; gs_feature_l1_grad on the RGB planes; gs_radiance_backward to
     the records; gs_mean_backward + gs_param_backward to every Gaussian parameter;
     for a feature scene also gs_feature_l1_grad + gs_feature_backward on the
-    features (geometry frozen for L_f); then one gs_feature_sgd step per parameter
-    plane and the block bounds refreshed.  No densification / pruning."""
+    features (geometry frozen for L_f); then one gs_feature_sgd or gs_adam step per
+    parameter plane and the block bounds refreshed.  No densification / pruning."""
 
     PLANES = ("pos", "scale", "quat", "opacity", "sh")
 
     def __init__(self, scene: G.DeviceScene, views: Sequence, target_rgb: torch.Tensor,
                  target_feat: Optional[torch.Tensor] = None, lr: Optional[dict] = None, alpha: float = 1.0,
-                 beta: float = 1.0):
+                 beta: float = 1.0, optimizer: str = "sgd"):
         self.scene = scene
         self.r = Renderer(scene, views, backproject=False)
         self.r.render().fit_capacities(slack=1.5)
         self.target_rgb, self.target_feat = target_rgb, target_feat
         # steps for losses that are means over all pixels (and channels)
-        self.lr = {"pos": 1.0, "scale": 1e-2, "quat": 1e-1, "opacity": 1.0, "sh": 10.0, "feat": 1000.0}
+        assert optimizer in ("sgd", "adam")
+        self.optimizer, self.t = optimizer, 0
+        if optimizer == "sgd":
+            self.lr = {"pos": 1.0, "scale": 1e-2, "quat": 1e-1, "opacity": 1.0, "sh": 10.0, "feat": 1000.0}
+        else:   # Adam steps are scale-free: per-parameter step sizes in parameter units
+            self.lr = {"pos": 1e-3, "scale": 1e-3, "quat": 1e-3, "opacity": 1e-2, "sh": 1e-2, "feat": 1e-2}
         self.lr.update(lr or {})
         dev = scene.pos.device
         self.rgb_scale = beta / self.r.images.rgb.numel()
@@ -323,10 +328,22 @@ class SceneTrainer:
             self.gimg = torch.empty_like(self.r.images.feat)
             self.gfeat = torch.zeros_like(scene.feat)
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.state = {}
+        if optimizer == "adam":
+            keys = list(self.PLANES) + (["feat"] if target_feat is not None else [])
+            self.state = {k: (torch.zeros_like(getattr(scene, k)), torch.zeros_like(getattr(scene, k))) for k in keys}
+
+    def _update(self, key, param, grad, param_h, stream):
+        if self.optimizer == "sgd":
+            G.gs_feature_sgd(param, grad, self.lr[key], param_h, stream)
+        else:
+            m, v = self.state[key]
+            G.gs_adam(param, grad, m, v, self.lr[key], self.t, param_h=param_h, stream=stream)
 
     def step(self, stream=None) -> torch.Tensor:
         """One iteration; returns the device loss of the parameters before the update."""
         sc, r = self.scene, self.r
+        self.t += 1
         r.run(stream)
         self.loss.zero_()
         G.gs_feature_l1_grad(r.images.rgb, self.target_rgb, self.rgb_scale, self.gout.rgb, self.loss, stream)
@@ -341,9 +358,9 @@ class SceneTrainer:
             G.gs_feature_l1_grad(r.images.feat, self.target_feat, self.feat_scale, self.gimg, self.loss, stream)
             self.gfeat.zero_()
             G.gs_feature_backward(sc, r.proj, r.bins, r.vb, r.params, self.gimg, self.gfeat, stream)
-            G.gs_feature_sgd(sc.feat, self.gfeat, self.lr["feat"], sc.feat_h, stream)
+            self._update("feat", sc.feat, self.gfeat, sc.feat_h, stream)
         for k in self.PLANES:
-            G.gs_feature_sgd(getattr(sc, k), self.grads[k], self.lr[k], None, stream)
+            self._update(k, getattr(sc, k), self.grads[k], None, stream)
         if sc.block_bounds is not None:
             G.gs_scene_block_bounds(sc, stream)   # the means moved
         return self.loss

@@ -278,3 +278,41 @@ def test_scene_training_reduces_rgb_loss(G):
     assert t.r.status() == 0
     assert losses[0] > 0.02
     assert losses[-1] < 0.6 * losses[0], losses[::8]
+
+
+def test_adam_matches_plain_reference(G):
+    """gs_adam against the textbook update written out in numpy (fp64), 5 steps."""
+    rng = np.random.default_rng(17)
+    n = 10007
+    p0 = rng.standard_normal(n).astype(np.float32)
+    grads = [rng.standard_normal(n).astype(np.float32) for _ in range(5)]
+    p = torch.from_numpy(p0.copy()).cuda()
+    ph = torch.empty(n, dtype=torch.float16, device="cuda")
+    m, v = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    b1, b2, eps, lr = 0.9, 0.999, 1e-8, 1e-2
+    pr, mr, vr = p0.astype(np.float64), np.zeros(n), np.zeros(n)
+    for t, g in enumerate(grads, start=1):
+        G.gs_adam(p, torch.from_numpy(g).cuda(), m, v, lr, t, b1, b2, eps, param_h=ph)
+        gd = g.astype(np.float64)
+        mr = b1 * mr + (1 - b1) * gd
+        vr = b2 * vr + (1 - b2) * gd * gd
+        pr = pr - lr * (mr / (1 - b1 ** t)) / (np.sqrt(vr / (1 - b2 ** t)) + eps)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(p.cpu().numpy(), pr, rtol=0, atol=1e-5)
+    np.testing.assert_allclose(ph.float().cpu().numpy(), p.cpu().numpy(), rtol=1e-3, atol=1e-3)
+
+
+def test_scene_training_with_adam(G):
+    base = synth.box_v1(1500, seed=21, sh_degree=1)
+    v = synth.box_view()
+    rt = G.Renderer(G.DeviceScene(base), [v], backproject=False)
+    rt.render()
+    target = rt.images.rgb.clone()
+    rng = np.random.default_rng(5)
+    start = dataclasses.replace(base, pos=base.pos + rng.normal(0, 0.02, base.pos.shape).astype(np.float32),
+                                sh=base.sh + rng.normal(0, 0.3, base.sh.shape).astype(np.float32))
+    t = G.SceneTrainer(G.DeviceScene(start), [v], target, optimizer="adam")
+    losses = [float(t.step().item()) for _ in range(40)]
+    torch.cuda.synchronize()
+    assert t.r.status() == 0
+    assert losses[-1] < 0.6 * losses[0], losses[::8]
