@@ -48,3 +48,27 @@ def test_identities():
     assert abs(OS.dssim(x, x)) < 1e-12
     assert abs(OS.dssim(x, y) - OS.dssim(y, x)) < 1e-12
     assert 0.0 < OS.dssim(x, y) < 2.0
+
+
+def test_dssim_grad_matches_central_differences():
+    """The chain-rule gradient against fp64 central differences of dssim() at every
+    pixel of a small ragged image (window overhangs every border)."""
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0, 1, (2, 7, 12))
+    y = np.clip(x + rng.normal(0, 0.15, x.shape), 0, 1)
+    g = OS.dssim_grad(x, y)
+    h = 1e-6
+    fd = np.empty_like(x)
+    for idx in np.ndindex(x.shape):
+        xp, xm = x.copy(), x.copy()
+        xp[idx] += h
+        xm[idx] -= h
+        fd[idx] = (OS.dssim(xp, y) - OS.dssim(xm, y)) / (2 * h)
+    np.testing.assert_allclose(g, fd, rtol=1e-5, atol=1e-9)
+
+
+def test_dssim_grad_vanishes_at_the_minimum():
+    """x = y is the minimum of 1 - SSIM (S <= 1): the gradient is zero there."""
+    rng = np.random.default_rng(6)
+    x = rng.uniform(0, 1, (3, 10, 9))
+    assert np.abs(OS.dssim_grad(x, x)).max() < 1e-12
