@@ -412,6 +412,23 @@ gs_status gs_param_backward(const gs_scene* scene, const gs_projected* proj, con
 gs_status gs_feature_l1_grad(const float* rendered, const float* target, int64_t n, float scale,
                              float* grad_image, double* loss, void* stream);
 
+/* Eq. 3's D-SSIM term (reading Q37: 1 - SSIM with an
+ * 11 x 11 Gaussian window, sigma 1.5, zero padding, C1 = 0.01^2, C2 = 0.03^2)
+ * over n_planes contiguous fp32 planes of height x width (row-major; e.g. the
+ * [3][H][W] RGB planes of one view of gs_images, or several equal-size views).
+ * *loss (device double, accumulated) += scale * sum over planes and pixels of
+ * (1 - S); grad_image (same layout, ACCUMULATED: the caller zeroes it or lets it
+ * hold the L1 gradient of gs_feature_l1_grad) += scale * d sum(1 - S) / d rendered.
+ * With scale = lambda / (C H W) this is lambda * L_D-SSIM and its gradient.
+ * workspace: device, >= gs_dssim_workspace_bytes(...) bytes, caller-owned
+ * scratch (three fp32 partial-derivative planes per input plane).
+ * Errors: GS_INVALID_ARG for negative sizes, n_planes > 65535, NULL pointers
+ * (when the size is non-zero) or a short workspace; empty input is a no-op. */
+size_t gs_dssim_workspace_bytes(int32_t n_planes, int32_t height, int32_t width);
+gs_status gs_dssim_grad(const float* rendered, const float* target, int32_t n_planes, int32_t height, int32_t width,
+                        float scale, float* grad_image, float* workspace, size_t workspace_bytes, double* loss,
+                        void* stream);
+
 /* feat[i] -= lr * grad_feat[i] over n floats; refreshes the fp16 copy (gs_scene.feat_h) when feat_h != NULL. */
 gs_status gs_feature_sgd(float* feat, const float* grad_feat, int64_t n, float lr, void* feat_h, void* stream);
 

@@ -32,6 +32,7 @@ SOURCES = {
     "gs_visibility.cu": [],
     "gs_match.cu": [],
     "gs_pose.cu": [],
+    "gs_ssim.cu": [],
 }
 HEADERS = [os.path.join(INCLUDE, "gs.h"), os.path.join(CSRC, "gs_common.cuh"), os.path.join(CSRC, "gs_tc.cuh")]
 

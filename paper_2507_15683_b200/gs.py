@@ -72,7 +72,7 @@ EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_lay
            "gs_scene_features_f16", "gs_validate_scene", "gs_match", "gs_match_workspace_bytes",
            "gs_pnp", "gs_pnp_workspace_bytes", "gs_verify_consistency", "gs_feature_backward", "gs_radiance_backward",
            "gs_mean_backward", "gs_param_backward", "gs_adam",
-           "gs_feature_l1_grad", "gs_feature_sgd",
+           "gs_feature_l1_grad", "gs_feature_sgd", "gs_dssim_grad", "gs_dssim_workspace_bytes",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_rasterize_backproject", "gs_backproject", "gs_visibility_score",
            "gs_visibility_workspace_bytes"]
@@ -99,6 +99,8 @@ def lib():
         L.gs_match_workspace_bytes.restype = ctypes.c_size_t
         L.gs_match_workspace_bytes.argtypes = [ctypes.c_int32] * 4
         L.gs_visibility_workspace_bytes.restype = ctypes.c_size_t
+        L.gs_dssim_workspace_bytes.restype = ctypes.c_size_t
+        L.gs_dssim_workspace_bytes.argtypes = [ctypes.c_int32] * 3
         for f in ("gs_views_layout", "gs_scene_block_bounds", "gs_project", "gs_bin_sort", "gs_rasterize",
                   "gs_rasterize_backproject", "gs_backproject", "gs_visibility_score"):
             getattr(L, f).restype = ctypes.c_int
@@ -476,6 +478,20 @@ def gs_feature_l1_grad(rendered: torch.Tensor, target: torch.Tensor, scale: floa
     _check(lib().gs_feature_l1_grad(_ptr(rendered), _ptr(target), ctypes.c_int64(rendered.numel()),
                                     ctypes.c_float(scale), _ptr(grad_image), _ptr(loss), _stream(stream)),
            "gs_feature_l1_grad")
+
+
+def gs_dssim_grad(rendered: torch.Tensor, target: torch.Tensor, n_planes: int, height: int, width: int,
+                  scale: float, grad_image: torch.Tensor, loss: torch.Tensor, workspace: Optional[torch.Tensor] = None,
+                  stream=None) -> torch.Tensor:
+    """Eq. 3's D-SSIM (reading Q37): loss += scale sum(1 - S), grad_image += its gradient
+    (include/gs.h).  Returns the workspace (pass it back to reuse it)."""
+    nb = lib().gs_dssim_workspace_bytes(n_planes, height, width)
+    if workspace is None or workspace.numel() * 4 < nb:
+        workspace = torch.empty(max(nb // 4, 1), dtype=torch.float32, device=rendered.device)
+    _check(lib().gs_dssim_grad(_ptr(rendered), _ptr(target), ctypes.c_int32(n_planes), ctypes.c_int32(height),
+                               ctypes.c_int32(width), ctypes.c_float(scale), _ptr(grad_image), _ptr(workspace),
+                               ctypes.c_size_t(workspace.numel() * 4), _ptr(loss), _stream(stream)), "gs_dssim_grad")
+    return workspace
 
 
 def gs_scene_block_bounds(scene: "DeviceScene", stream=None):

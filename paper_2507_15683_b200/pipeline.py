@@ -289,9 +289,11 @@ class FeatureDistiller:
 
 
 class SceneTrainer:
-    """N4: a joint training step of Eq. 1, L = alpha L_f + beta L_rgb, with L1 terms
-    (Eq. 2's feature term; the RGB term without Eq. 3's D-SSIM part).  Per step:
-    render the batch; gs_feature_l1_grad on the RGB planes; gs_radiance_backward to
+    """N4: a joint training step of Eq. 1, L = alpha L_f + beta L_rgb, with Eq. 2's L1
+    feature term and Eq. 3's L_rgb = (1 - lam) L1 + lam L_D-SSIM (reading Q37;
+    lam = 0.2 as in [3DGS], the paper gives no value; lam = 0 is L1 only).  Per step:
+    render the batch; gs_feature_l1_grad on the RGB planes, then gs_dssim_grad adding
+    the D-SSIM gradient per run of equal-size views; gs_radiance_backward to
     the records; gs_mean_backward + gs_param_backward to every Gaussian parameter;
     for a feature scene also gs_feature_l1_grad + gs_feature_backward on the
     features (geometry frozen for L_f); then one gs_feature_sgd or gs_adam step per
@@ -301,7 +303,7 @@ class SceneTrainer:
 
     def __init__(self, scene: G.DeviceScene, views: Sequence, target_rgb: torch.Tensor,
                  target_feat: Optional[torch.Tensor] = None, lr: Optional[dict] = None, alpha: float = 1.0,
-                 beta: float = 1.0, optimizer: str = "sgd"):
+                 beta: float = 1.0, optimizer: str = "sgd", lam: float = 0.2):
         self.scene = scene
         self.r = Renderer(scene, views, backproject=False)
         self.r.render().fit_capacities(slack=1.5)
@@ -315,7 +317,16 @@ class SceneTrainer:
             self.lr = {"pos": 1e-3, "scale": 1e-3, "quat": 1e-3, "opacity": 1e-2, "sh": 1e-2, "feat": 1e-2}
         self.lr.update(lr or {})
         dev = scene.pos.device
-        self.rgb_scale = beta / self.r.images.rgb.numel()
+        self.rgb_scale = beta * (1.0 - lam) / self.r.images.rgb.numel()
+        self.dssim_scale = beta * lam / self.r.images.rgb.numel()
+        # runs of consecutive equal-size views: their RGB planes are contiguous
+        self.dssim_runs, vb = [], self.r.vb
+        for i, v in enumerate(vb.views):
+            if self.dssim_runs and self.dssim_runs[-1][2:] == (v.height, v.width):
+                self.dssim_runs[-1][1] += 1
+            else:
+                self.dssim_runs.append([i, 1, v.height, v.width])
+        self.dssim_ws = None
         self.gout = G.Images(self.r.vb.total_pixels, 0, device=dev)
         self.gout.depth.zero_()
         self.gout.alpha.zero_()
@@ -347,6 +358,13 @@ class SceneTrainer:
         r.run(stream)
         self.loss.zero_()
         G.gs_feature_l1_grad(r.images.rgb, self.target_rgb, self.rgb_scale, self.gout.rgb, self.loss, stream)
+        if self.dssim_scale != 0.0:
+            for i0, cnt, h, w in self.dssim_runs:
+                o = 3 * r.vb.pix_offset(i0)
+                n = 3 * cnt * h * w
+                self.dssim_ws = G.gs_dssim_grad(r.images.rgb[o:o + n], self.target_rgb[o:o + n], 3 * cnt, h, w,
+                                                self.dssim_scale, self.gout.rgb[o:o + n], self.loss, self.dssim_ws,
+                                                stream)
         self.grec.zero_()
         G.gs_radiance_backward(r.proj, r.bins, r.vb, r.params, r.images, self.gout, self.grec, stream)
         for g in self.grads.values():

@@ -272,7 +272,7 @@ def test_scene_training_reduces_rgb_loss(G):
     rng = np.random.default_rng(5)
     start = dataclasses.replace(base, pos=base.pos + rng.normal(0, 0.02, base.pos.shape).astype(np.float32),
                                 sh=base.sh + rng.normal(0, 0.3, base.sh.shape).astype(np.float32))
-    t = G.SceneTrainer(G.DeviceScene(start), [v], target)
+    t = G.SceneTrainer(G.DeviceScene(start), [v], target, lam=0.0)   # L1 only
     losses = [float(t.step().item()) for _ in range(40)]
     torch.cuda.synchronize()
     assert t.r.status() == 0
@@ -311,8 +311,34 @@ def test_scene_training_with_adam(G):
     rng = np.random.default_rng(5)
     start = dataclasses.replace(base, pos=base.pos + rng.normal(0, 0.02, base.pos.shape).astype(np.float32),
                                 sh=base.sh + rng.normal(0, 0.3, base.sh.shape).astype(np.float32))
-    t = G.SceneTrainer(G.DeviceScene(start), [v], target, optimizer="adam")
+    t = G.SceneTrainer(G.DeviceScene(start), [v], target, optimizer="adam", lam=0.0)
     losses = [float(t.step().item()) for _ in range(40)]
+    torch.cuda.synchronize()
+    assert t.r.status() == 0
+    assert losses[-1] < 0.6 * losses[0], losses[::8]
+
+
+def test_scene_training_with_dssim(G):
+    """Eq. 3 in full: L_rgb = (1 - lam) L1 + lam D-SSIM (lam = 0.2, reading Q37).  The
+    first step's loss equals the oracle's value of that expression on the rendered
+    image (the render is the parameters before the update), and 40 Adam steps cut it
+    by > 40 %."""
+    from oracle import ssim as OS
+    base = synth.box_v1(1500, seed=21, sh_degree=1)
+    v = synth.box_view()
+    rt = G.Renderer(G.DeviceScene(base), [v], backproject=False)
+    rt.render()
+    target = rt.images.rgb.clone()
+    rng = np.random.default_rng(5)
+    start = dataclasses.replace(base, pos=base.pos + rng.normal(0, 0.02, base.pos.shape).astype(np.float32),
+                                sh=base.sh + rng.normal(0, 0.3, base.sh.shape).astype(np.float32))
+    t = G.SceneTrainer(G.DeviceScene(start), [v], target, optimizer="adam")
+    first = float(t.step().item())
+    x = t.r.images.rgb.double().cpu().numpy().reshape(3, v.height, v.width)
+    y = target.double().cpu().numpy().reshape(3, v.height, v.width)
+    want = 0.8 * np.abs(x - y).mean() + 0.2 * OS.dssim(x, y)
+    assert abs(first - want) <= 1e-5 * want, (first, want)
+    losses = [first] + [float(t.step().item()) for _ in range(39)]
     torch.cuda.synchronize()
     assert t.r.status() == 0
     assert losses[-1] < 0.6 * losses[0], losses[::8]

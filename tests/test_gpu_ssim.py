@@ -1,0 +1,113 @@
+"""GPU parity of gs_dssim_grad (Eq. 3's D-SSIM term, reading Q37) against
+oracle/ssim.py: the loss and the gradient w.r.t. the rendered planes, element by
+element, on seeded render-like planes (smooth shading + texture noise + an empty
+background region, values in [0, 1]) at tile-spanning ragged sizes, planes
+smaller than the window, and one full C4 view (3 x 768 x 1024).
+
+Tolerance (fp32 kernel vs fp64 oracle): the partials carry 1/B2 <= 1/C2 ~ 1.1e3
+and dmu's terms cancel against 2 x w*dxx, so an element's absolute error is
+about u_fp32 * 1e3 * (a few window sums) ~ 1e-4 of the largest gradient
+magnitude; the test allows 2e-3 * max|g| absolute plus 2e-3 relative.  The loss
+is a mean of per-pixel terms accumulated in fp64: relative 1e-5."""
+import numpy as np
+import pytest
+
+from oracle import ssim as OS
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def G():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2507_15683_b200 as G
+    G.lib()
+    return G
+
+
+def _planes(seed, C, H, W):
+    """Render-like planes: a smooth gradient, texture noise, a zero (empty) corner;
+    the target is the same scene with a shifted shading and its own noise."""
+    rng = np.random.default_rng(seed)
+    yy, xx = np.mgrid[0:H, 0:W] / max(H, W)
+    x = np.empty((C, H, W))
+    y = np.empty((C, H, W))
+    for c in range(C):
+        base = 0.5 + 0.4 * np.sin(6 * xx + 3 * c) * np.cos(5 * yy)
+        x[c] = np.clip(base + rng.normal(0, 0.05, (H, W)), 0, 1)
+        y[c] = np.clip(base + 0.05 * np.cos(9 * yy) + rng.normal(0, 0.05, (H, W)), 0, 1)
+    x[:, : H // 4, : W // 5] = 0.0
+    y[:, : H // 4, : W // 6] = 0.0
+    return x.astype(np.float32), y.astype(np.float32)
+
+
+def _run(G, x, y, scale, g0=None):
+    C, H, W = x.shape
+    X = torch.from_numpy(x.reshape(-1).copy()).cuda()
+    Y = torch.from_numpy(y.reshape(-1).copy()).cuda()
+    g = torch.zeros_like(X) if g0 is None else torch.from_numpy(g0.reshape(-1).copy()).cuda()
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    G.gs_dssim_grad(X, Y, C, H, W, scale, g, loss)
+    torch.cuda.synchronize()
+    return g.cpu().numpy().reshape(C, H, W).astype(np.float64), float(loss.item())
+
+
+def _check(x, y, g, loss, lam=1.0):
+    xd, yd = x.astype(np.float64), y.astype(np.float64)
+    ref_loss = lam * OS.dssim(xd, yd)
+    ref_g = lam * OS.dssim_grad(xd, yd)
+    assert abs(loss - ref_loss) <= 1e-5 * abs(ref_loss) + 1e-9, (loss, ref_loss)
+    tol = 2e-3 * np.abs(ref_g).max() + 2e-3 * np.abs(ref_g)
+    err = np.abs(g - ref_g)
+    assert (err <= tol).all(), (err.max(), np.abs(ref_g).max())
+
+
+@pytest.mark.parametrize("shape,seed", [((3, 45, 70), 0), ((2, 16, 32), 1), ((1, 33, 97), 2), ((3, 5, 3), 3),
+                                        ((1, 1, 1), 4), ((4, 130, 20), 5)])
+def test_dssim_grad_vs_oracle(G, shape, seed):
+    x, y = _planes(seed, *shape)
+    lam = 0.2
+    g, loss = _run(G, x, y, lam / x.size)
+    _check(x, y, g, loss, lam)
+
+
+def test_dssim_grad_accumulates(G):
+    """grad_image and *loss are accumulated: a pre-filled gradient (the L1 term)
+    is kept and added to."""
+    x, y = _planes(7, 3, 40, 50)
+    g0 = np.random.default_rng(8).normal(0, 1e-3, x.shape)
+    g, loss = _run(G, x, y, 1.0 / x.size, g0=g0)
+    g_fresh, _ = _run(G, x, y, 1.0 / x.size)
+    np.testing.assert_allclose(g - g0, g_fresh, rtol=0, atol=1e-9)
+
+
+def test_dssim_identical_planes(G):
+    """SSIM(x, x) = 1: zero loss, and the gradient vanishes (to fp32 rounding,
+    measured against the gradient's magnitude for a different target)."""
+    x, y = _planes(9, 3, 37, 41)
+    g, loss = _run(G, x, x, 1.0 / x.size)
+    assert abs(loss) < 1e-6
+    assert np.abs(g).max() <= 2e-3 * np.abs(OS.dssim_grad(x.astype(np.float64), y.astype(np.float64))).max()
+
+
+def test_dssim_full_c4_view(G):
+    """One full C4 view (3 x 768 x 1024), every element against the oracle."""
+    x, y = _planes(10, 3, 768, 1024)
+    g, loss = _run(G, x, y, 0.2 / x.size)
+    _check(x, y, g, loss, 0.2)
+
+
+def test_dssim_bad_args(G):
+    X = torch.zeros(16, device="cuda")
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    with pytest.raises(G.GSError):
+        G.gs_dssim_grad(X, X, -1, 4, 4, 1.0, X, loss)
+    ws = torch.zeros(1, device="cuda")
+    with pytest.raises(G.GSError):   # short workspace
+        G.lib()
+        import ctypes
+        G.gs._check(G.lib().gs_dssim_grad(G.gs._ptr(X), G.gs._ptr(X), 1, 4, 4, ctypes.c_float(1.0), G.gs._ptr(X),
+                                          G.gs._ptr(ws), ctypes.c_size_t(4), G.gs._ptr(loss), None), "gs_dssim_grad")
+    G.gs_dssim_grad(X, X, 0, 4, 4, 1.0, X, loss)   # empty: no-op
