@@ -3,10 +3,11 @@
 // zero padding, C1 = 0.01^2, C2 = 0.03^2).
 //
 // Two HBM-bound tiled passes over n_planes contiguous H x W planes.  Each CTA
-// owns a 32 x 16 output tile: it stages the (16 + 10) x (32 + 10) halo of its
+// owns a 32 x 32 output tile: it stages the (32 + 10) x (32 + 10) halo of its
 // input planes in shared memory (zero outside the plane = the zero padding),
-// runs the separable window horizontally into a (16 + 10) x 32 buffer and then
-// vertically, one output column per lane.
+// runs the separable window horizontally into a (32 + 10) x 32 buffer (four
+// adjacent columns per lane from a 14-value register window) and then
+// vertically (four adjacent rows per lane, one column per lane).
 //   pass 1 (ssim_moments_kernel): the five window moments of (x, y) -> the SSIM
 //     map S, *loss += scale sum (1 - S), and the three partials
 //     dS/dmu_x, dS/dE_xx, dS/dE_xy written to the workspace (12 B/px);
@@ -23,9 +24,13 @@
 namespace gs {
 namespace {
 
-constexpr int SS_TW = 32, SS_TH = 16, SS_R = 5, SS_K = 2 * SS_R + 1;
+constexpr int SS_TW = 32, SS_TH = 32, SS_R = 5, SS_K = 2 * SS_R + 1;
 constexpr int SS_HW = SS_TW + 2 * SS_R, SS_HH = SS_TH + 2 * SS_R;
-constexpr int SS_THREADS = 256;
+// halo row stride: 45 = 13 (mod 32) puts the four rows a warp's horizontal pass
+// reads (8 lanes x 4 columns each) in distinct bank classes mod 4 -> conflict-free
+constexpr int SS_RS = 45;
+constexpr int SS_THREADS = 256, SS_WARPS = SS_THREADS / 32, SS_VR = SS_TH / SS_WARPS;  // 4 rows per lane
+constexpr int SS_HJ = 4;                                                              // columns per lane
 constexpr float SS_C1 = 0.01f * 0.01f, SS_C2 = 0.03f * 0.03f;
 
 struct Win {
@@ -33,7 +38,7 @@ struct Win {
 };  // the window, passed by value (kernel-parameter constant bank)
 
 template <int NIN>
-__device__ __forceinline__ void load_halo(float (*s)[SS_HH][SS_HW], const float* const (&src)[NIN], int H, int W,
+__device__ __forceinline__ void load_halo(float (*s)[SS_HH][SS_RS], const float* const (&src)[NIN], int H, int W,
                                           int x0, int y0) {
     for (int i = threadIdx.x; i < SS_HH * SS_HW; i += SS_THREADS) {
         const int r = i / SS_HW, c = i - r * SS_HW;
@@ -45,54 +50,94 @@ __device__ __forceinline__ void load_halo(float (*s)[SS_HH][SS_HW], const float*
     }
 }
 
+// Horizontal window pass: NOUT row sums over SS_HH x SS_TW positions, each lane
+// SS_HJ adjacent columns from a register window of SS_HJ + 10 halo values per
+// input (MOM: the five moments x, y, xx, yy, xy of two inputs; else identity).
+template <int NIN, int NOUT, bool MOM>
+__device__ __forceinline__ void horizontal(const float (*s_in)[SS_HH][SS_RS], float (*s_h)[SS_HH][SS_TW],
+                                           const Win& win) {
+    constexpr int G = SS_TW / SS_HJ;
+    for (int it = threadIdx.x; it < SS_HH * G; it += SS_THREADS) {
+        const int r = it / G, c0 = (it - r * G) * SS_HJ;
+        float v[NIN][SS_HJ + SS_K - 1];
+#pragma unroll
+        for (int q = 0; q < NIN; ++q)
+#pragma unroll
+            for (int k = 0; k < SS_HJ + SS_K - 1; ++k) v[q][k] = s_in[q][r][c0 + k];
+        float acc[NOUT][SS_HJ];
+#pragma unroll
+        for (int m = 0; m < NOUT; ++m)
+#pragma unroll
+            for (int j = 0; j < SS_HJ; ++j) acc[m][j] = 0.f;
+#pragma unroll
+        for (int k = 0; k < SS_K; ++k) {
+            const float w = win.w[k];
+#pragma unroll
+            for (int j = 0; j < SS_HJ; ++j) {
+                if constexpr (MOM) {
+                    const float a = v[0][j + k], b = v[1][j + k];
+                    acc[0][j] = fmaf(w, a, acc[0][j]);
+                    acc[1][j] = fmaf(w, b, acc[1][j]);
+                    acc[2][j] = fmaf(w, a * a, acc[2][j]);
+                    acc[3][j] = fmaf(w, b * b, acc[3][j]);
+                    acc[4][j] = fmaf(w, a * b, acc[4][j]);
+                } else {
+#pragma unroll
+                    for (int m = 0; m < NOUT; ++m) acc[m][j] = fmaf(w, v[m][j + k], acc[m][j]);
+                }
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < NOUT; ++m)
+            *reinterpret_cast<float4*>(&s_h[m][r][c0]) = make_float4(acc[m][0], acc[m][1], acc[m][2], acc[m][3]);
+    }
+}
+
+// Vertical window pass for lane column tx and output rows r0 .. r0 + SS_VR - 1.
+template <int NOUT>
+__device__ __forceinline__ void vertical(const float (*s_h)[SS_HH][SS_TW], int r0, int tx, const Win& win,
+                                         float (&out)[NOUT][SS_VR]) {
+#pragma unroll
+    for (int m = 0; m < NOUT; ++m) {
+        float v[SS_VR + SS_K - 1];
+#pragma unroll
+        for (int k = 0; k < SS_VR + SS_K - 1; ++k) v[k] = s_h[m][r0 + k][tx];
+#pragma unroll
+        for (int j = 0; j < SS_VR; ++j) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < SS_K; ++k) acc = fmaf(win.w[k], v[j + k], acc);
+            out[m][j] = acc;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(SS_THREADS) ssim_moments_kernel(const float* __restrict__ X,
                                                                   const float* __restrict__ Y, int H, int W,
                                                                   float scale, float* __restrict__ dmu,
                                                                   float* __restrict__ dxx, float* __restrict__ dxy,
                                                                   int64_t ws_plane_stride, double* __restrict__ loss,
                                                                   const Win win) {
-    __shared__ float s_in[2][SS_HH][SS_HW];
-    __shared__ float s_h[5][SS_HH][SS_TW];
+    __shared__ __align__(16) float s_in[2][SS_HH][SS_RS];
+    __shared__ __align__(16) float s_h[5][SS_HH][SS_TW];
     const int64_t off = (int64_t)blockIdx.z * H * W;
     const int x0 = blockIdx.x * SS_TW, y0 = blockIdx.y * SS_TH;
     const float* const src[2] = {X + off, Y + off};
     load_halo<2>(s_in, src, H, W, x0, y0);
     __syncthreads();
-    for (int i = threadIdx.x; i < SS_HH * SS_TW; i += SS_THREADS) {
-        const int r = i / SS_TW, c = i - r * SS_TW;
-        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
-#pragma unroll
-        for (int k = 0; k < SS_K; ++k) {
-            const float a = s_in[0][r][c + k], b = s_in[1][r][c + k], w = win.w[k];
-            m0 = fmaf(w, a, m0);
-            m1 = fmaf(w, b, m1);
-            m2 = fmaf(w, a * a, m2);
-            m3 = fmaf(w, b * b, m3);
-            m4 = fmaf(w, a * b, m4);
-        }
-        s_h[0][r][c] = m0;
-        s_h[1][r][c] = m1;
-        s_h[2][r][c] = m2;
-        s_h[3][r][c] = m3;
-        s_h[4][r][c] = m4;
-    }
+    horizontal<2, 5, true>(s_in, s_h, win);
     __syncthreads();
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int tx = threadIdx.x & 31, r0 = (threadIdx.x >> 5) * SS_VR;
+    float mom[5][SS_VR];
+    vertical<5>(s_h, r0, tx, win, mom);
     double part = 0.0;
-    for (int rr = ty; rr < SS_TH; rr += SS_THREADS / 32) {
-        const int gy = y0 + rr, gx = x0 + tx;
-        float mx = 0.f, my = 0.f, exx = 0.f, eyy = 0.f, exy = 0.f;
+    const int gx = x0 + tx;
 #pragma unroll
-        for (int k = 0; k < SS_K; ++k) {
-            const float w = win.w[k];
-            mx = fmaf(w, s_h[0][rr + k][tx], mx);
-            my = fmaf(w, s_h[1][rr + k][tx], my);
-            exx = fmaf(w, s_h[2][rr + k][tx], exx);
-            eyy = fmaf(w, s_h[3][rr + k][tx], eyy);
-            exy = fmaf(w, s_h[4][rr + k][tx], exy);
-        }
+    for (int j = 0; j < SS_VR; ++j) {
+        const int gy = y0 + r0 + j;
         if (gy < H && gx < W) {
-            const float sxx = exx - mx * mx, syy = eyy - my * my, sxy = exy - mx * my;
+            const float mx = mom[0][j], my = mom[1][j];
+            const float sxx = mom[2][j] - mx * mx, syy = mom[3][j] - my * my, sxy = mom[4][j] - mx * my;
             const float A1 = 2.f * mx * my + SS_C1, A2 = 2.f * sxy + SS_C2;
             const float B1 = mx * mx + my * my + SS_C1, B2 = sxx + syy + SS_C2;
             const float iA1 = 1.f / A1, iA2 = 1.f / A2, iB1 = 1.f / B1, iB2 = 1.f / B2;
@@ -114,43 +159,26 @@ __global__ void __launch_bounds__(SS_THREADS) ssim_grad_kernel(const float* __re
                                                                const float* __restrict__ dxx,
                                                                const float* __restrict__ dxy, int64_t ws_plane_stride,
                                                                float* __restrict__ G, const Win win) {
-    __shared__ float s_in[3][SS_HH][SS_HW];
-    __shared__ float s_h[3][SS_HH][SS_TW];
+    __shared__ __align__(16) float s_in[3][SS_HH][SS_RS];
+    __shared__ __align__(16) float s_h[3][SS_HH][SS_TW];
     const int64_t off = (int64_t)blockIdx.z * H * W, woff = (int64_t)blockIdx.z * ws_plane_stride;
     const int x0 = blockIdx.x * SS_TW, y0 = blockIdx.y * SS_TH;
     const float* const src[3] = {dmu + woff, dxx + woff, dxy + woff};
     load_halo<3>(s_in, src, H, W, x0, y0);
     __syncthreads();
-    for (int i = threadIdx.x; i < SS_HH * SS_TW; i += SS_THREADS) {
-        const int r = i / SS_TW, c = i - r * SS_TW;
-        float m0 = 0.f, m1 = 0.f, m2 = 0.f;
-#pragma unroll
-        for (int k = 0; k < SS_K; ++k) {
-            const float w = win.w[k];
-            m0 = fmaf(w, s_in[0][r][c + k], m0);
-            m1 = fmaf(w, s_in[1][r][c + k], m1);
-            m2 = fmaf(w, s_in[2][r][c + k], m2);
-        }
-        s_h[0][r][c] = m0;
-        s_h[1][r][c] = m1;
-        s_h[2][r][c] = m2;
-    }
+    horizontal<3, 3, false>(s_in, s_h, win);
     __syncthreads();
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    for (int rr = ty; rr < SS_TH; rr += SS_THREADS / 32) {
-        const int gy = y0 + rr, gx = x0 + tx;
-        float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+    const int tx = threadIdx.x & 31, r0 = (threadIdx.x >> 5) * SS_VR;
+    float b[3][SS_VR];
+    vertical<3>(s_h, r0, tx, win, b);
+    const int gx = x0 + tx;
 #pragma unroll
-        for (int k = 0; k < SS_K; ++k) {
-            const float w = win.w[k];
-            b0 = fmaf(w, s_h[0][rr + k][tx], b0);
-            b1 = fmaf(w, s_h[1][rr + k][tx], b1);
-            b2 = fmaf(w, s_h[2][rr + k][tx], b2);
-        }
+    for (int j = 0; j < SS_VR; ++j) {
+        const int gy = y0 + r0 + j;
         if (gy < H && gx < W) {
             const int64_t o = off + (int64_t)gy * W + gx;
             const float x = __ldg(X + o), y = __ldg(Y + o);
-            G[o] -= scale * (b0 + 2.f * x * b1 + y * b2);
+            G[o] -= scale * (b[0][j] + 2.f * x * b[1][j] + y * b[2][j]);
         }
     }
 }

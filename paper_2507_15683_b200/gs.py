@@ -485,6 +485,7 @@ def gs_dssim_grad(rendered: torch.Tensor, target: torch.Tensor, n_planes: int, h
                   stream=None) -> torch.Tensor:
     """Eq. 3's D-SSIM (reading Q37): loss += scale sum(1 - S), grad_image += its gradient
     (include/gs.h).  Returns the workspace (pass it back to reuse it)."""
+    assert rendered.dtype == target.dtype == grad_image.dtype == torch.float32 and loss.dtype == torch.float64
     nb = lib().gs_dssim_workspace_bytes(n_planes, height, width)
     if workspace is None or workspace.numel() * 4 < nb:
         workspace = torch.empty(max(nb // 4, 1), dtype=torch.float32, device=rendered.device)
