@@ -37,16 +37,32 @@ struct Win {
     float w[SS_K];
 };  // the window, passed by value (kernel-parameter constant bank)
 
+// All of a thread's halo loads are issued before the first shared-memory store
+// (SS_LD = 7 iterations x NIN loads in flight per thread).
+constexpr int SS_LD = (SS_HH * SS_HW + SS_THREADS - 1) / SS_THREADS;
+
 template <int NIN>
 __device__ __forceinline__ void load_halo(float (*s)[SS_HH][SS_RS], const float* const (&src)[NIN], int H, int W,
                                           int x0, int y0) {
-    for (int i = threadIdx.x; i < SS_HH * SS_HW; i += SS_THREADS) {
+    float v[SS_LD][NIN];
+#pragma unroll
+    for (int t = 0; t < SS_LD; ++t) {
+        const int i = threadIdx.x + t * SS_THREADS;
         const int r = i / SS_HW, c = i - r * SS_HW;
         const int gy = y0 - SS_R + r, gx = x0 - SS_R + c;
-        const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+        const bool in = i < SS_HH * SS_HW && gy >= 0 && gy < H && gx >= 0 && gx < W;
         const int64_t o = (int64_t)gy * W + gx;
 #pragma unroll
-        for (int k = 0; k < NIN; ++k) s[k][r][c] = in ? __ldg(src[k] + o) : 0.f;
+        for (int k = 0; k < NIN; ++k) v[t][k] = in ? __ldg(src[k] + o) : 0.f;
+    }
+#pragma unroll
+    for (int t = 0; t < SS_LD; ++t) {
+        const int i = threadIdx.x + t * SS_THREADS;
+        const int r = i / SS_HW, c = i - r * SS_HW;
+        if (i < SS_HH * SS_HW) {
+#pragma unroll
+            for (int k = 0; k < NIN; ++k) s[k][r][c] = v[t][k];
+        }
     }
 }
 
@@ -59,11 +75,19 @@ __device__ __forceinline__ void horizontal(const float (*s_in)[SS_HH][SS_RS], fl
     constexpr int G = SS_TW / SS_HJ;
     for (int it = threadIdx.x; it < SS_HH * G; it += SS_THREADS) {
         const int r = it / G, c0 = (it - r * G) * SS_HJ;
-        float v[NIN][SS_HJ + SS_K - 1];
+        float v[MOM ? 5 : NIN][SS_HJ + SS_K - 1];
 #pragma unroll
         for (int q = 0; q < NIN; ++q)
 #pragma unroll
             for (int k = 0; k < SS_HJ + SS_K - 1; ++k) v[q][k] = s_in[q][r][c0 + k];
+        if constexpr (MOM) {   // the products once per halo value, not once per tap
+#pragma unroll
+            for (int k = 0; k < SS_HJ + SS_K - 1; ++k) {
+                v[2][k] = v[0][k] * v[0][k];
+                v[3][k] = v[1][k] * v[1][k];
+                v[4][k] = v[0][k] * v[1][k];
+            }
+        }
         float acc[NOUT][SS_HJ];
 #pragma unroll
         for (int m = 0; m < NOUT; ++m)
@@ -73,19 +97,9 @@ __device__ __forceinline__ void horizontal(const float (*s_in)[SS_HH][SS_RS], fl
         for (int k = 0; k < SS_K; ++k) {
             const float w = win.w[k];
 #pragma unroll
-            for (int j = 0; j < SS_HJ; ++j) {
-                if constexpr (MOM) {
-                    const float a = v[0][j + k], b = v[1][j + k];
-                    acc[0][j] = fmaf(w, a, acc[0][j]);
-                    acc[1][j] = fmaf(w, b, acc[1][j]);
-                    acc[2][j] = fmaf(w, a * a, acc[2][j]);
-                    acc[3][j] = fmaf(w, b * b, acc[3][j]);
-                    acc[4][j] = fmaf(w, a * b, acc[4][j]);
-                } else {
+            for (int j = 0; j < SS_HJ; ++j)
 #pragma unroll
-                    for (int m = 0; m < NOUT; ++m) acc[m][j] = fmaf(w, v[m][j + k], acc[m][j]);
-                }
-            }
+                for (int m = 0; m < NOUT; ++m) acc[m][j] = fmaf(w, v[m][j + k], acc[m][j]);
         }
 #pragma unroll
         for (int m = 0; m < NOUT; ++m)
@@ -140,12 +154,14 @@ __global__ void __launch_bounds__(SS_THREADS) ssim_moments_kernel(const float* _
             const float sxx = mom[2][j] - mx * mx, syy = mom[3][j] - my * my, sxy = mom[4][j] - mx * my;
             const float A1 = 2.f * mx * my + SS_C1, A2 = 2.f * sxy + SS_C2;
             const float B1 = mx * mx + my * my + SS_C1, B2 = sxx + syy + SS_C2;
-            const float iA1 = 1.f / A1, iA2 = 1.f / A2, iB1 = 1.f / B1, iB2 = 1.f / B2;
-            const float S = (A1 * A2) * (iB1 * iB2);
+            // one division: with iQ = 1 / (B1 B2), S = A1 A2 iQ, S/A1 = A2 iQ,
+            // S/A2 = A1 iQ, S/B1 = S B2 iQ, S/B2 = S B1 iQ
+            const float iQ = 1.f / (B1 * B2);
+            const float S = (A1 * A2) * iQ;
             const int64_t o = (int64_t)blockIdx.z * ws_plane_stride + (int64_t)gy * W + gx;
-            dmu[o] = 2.f * S * (my * iA1 - my * iA2 - mx * iB1 + mx * iB2);
-            dxx[o] = -S * iB2;
-            dxy[o] = 2.f * S * iA2;
+            dmu[o] = 2.f * iQ * (my * (A2 - A1) + mx * S * (B1 - B2));
+            dxx[o] = -S * B1 * iQ;
+            dxy[o] = 2.f * A1 * iQ;
             part += (double)(1.f - S);
         }
     }
