@@ -24,13 +24,23 @@
 namespace gs {
 namespace {
 
-constexpr int SS_TW = 32, SS_TH = 32, SS_R = 5, SS_K = 2 * SS_R + 1;
+#ifndef GS_SSIM_TH
+#define GS_SSIM_TH 32
+#endif
+#ifndef GS_SSIM_HJ_MOM
+#define GS_SSIM_HJ_MOM 1
+#endif
+#ifndef GS_SSIM_HJ_GRAD
+#define GS_SSIM_HJ_GRAD 4
+#endif
+constexpr int SS_TW = 32, SS_TH = GS_SSIM_TH, SS_R = 5, SS_K = 2 * SS_R + 1;
 constexpr int SS_HW = SS_TW + 2 * SS_R, SS_HH = SS_TH + 2 * SS_R;
 // halo row stride: 45 = 13 (mod 32) puts the four rows a warp's horizontal pass
 // reads (8 lanes x 4 columns each) in distinct bank classes mod 4 -> conflict-free
 constexpr int SS_RS = 45;
 constexpr int SS_THREADS = 256, SS_WARPS = SS_THREADS / 32, SS_VR = SS_TH / SS_WARPS;  // 4 rows per lane
-constexpr int SS_HJ = 4;                                                              // columns per lane
+// columns per lane in the horizontal pass (measured: pass 1 fastest at 1, pass 2 at 4)
+constexpr int SS_HJ_MOM = GS_SSIM_HJ_MOM, SS_HJ_GRAD = GS_SSIM_HJ_GRAD;
 constexpr float SS_C1 = 0.01f * 0.01f, SS_C2 = 0.03f * 0.03f;
 
 struct Win {
@@ -69,7 +79,7 @@ __device__ __forceinline__ void load_halo(float (*s)[SS_HH][SS_RS], const float*
 // Horizontal window pass: NOUT row sums over SS_HH x SS_TW positions, each lane
 // SS_HJ adjacent columns from a register window of SS_HJ + 10 halo values per
 // input (MOM: the five moments x, y, xx, yy, xy of two inputs; else identity).
-template <int NIN, int NOUT, bool MOM>
+template <int NIN, int NOUT, bool MOM, int SS_HJ>
 __device__ __forceinline__ void horizontal(const float (*s_in)[SS_HH][SS_RS], float (*s_h)[SS_HH][SS_TW],
                                            const Win& win) {
     constexpr int G = SS_TW / SS_HJ;
@@ -102,8 +112,15 @@ __device__ __forceinline__ void horizontal(const float (*s_in)[SS_HH][SS_RS], fl
                 for (int m = 0; m < NOUT; ++m) acc[m][j] = fmaf(w, v[m][j + k], acc[m][j]);
         }
 #pragma unroll
-        for (int m = 0; m < NOUT; ++m)
-            *reinterpret_cast<float4*>(&s_h[m][r][c0]) = make_float4(acc[m][0], acc[m][1], acc[m][2], acc[m][3]);
+        for (int m = 0; m < NOUT; ++m) {
+            if constexpr (SS_HJ == 4)
+                *reinterpret_cast<float4*>(&s_h[m][r][c0]) = make_float4(acc[m][0], acc[m][1], acc[m][2], acc[m][3]);
+            else if constexpr (SS_HJ == 2)
+                *reinterpret_cast<float2*>(&s_h[m][r][c0]) = make_float2(acc[m][0], acc[m][1]);
+            else
+#pragma unroll
+                for (int j = 0; j < SS_HJ; ++j) s_h[m][r][c0 + j] = acc[m][j];
+        }
     }
 }
 
@@ -139,7 +156,7 @@ __global__ void __launch_bounds__(SS_THREADS) ssim_moments_kernel(const float* _
     const float* const src[2] = {X + off, Y + off};
     load_halo<2>(s_in, src, H, W, x0, y0);
     __syncthreads();
-    horizontal<2, 5, true>(s_in, s_h, win);
+    horizontal<2, 5, true, SS_HJ_MOM>(s_in, s_h, win);
     __syncthreads();
     const int tx = threadIdx.x & 31, r0 = (threadIdx.x >> 5) * SS_VR;
     float mom[5][SS_VR];
@@ -182,7 +199,7 @@ __global__ void __launch_bounds__(SS_THREADS) ssim_grad_kernel(const float* __re
     const float* const src[3] = {dmu + woff, dxx + woff, dxy + woff};
     load_halo<3>(s_in, src, H, W, x0, y0);
     __syncthreads();
-    horizontal<3, 3, false>(s_in, s_h, win);
+    horizontal<3, 3, false, SS_HJ_GRAD>(s_in, s_h, win);
     __syncthreads();
     const int tx = threadIdx.x & 31, r0 = (threadIdx.x >> 5) * SS_VR;
     float b[3][SS_VR];
