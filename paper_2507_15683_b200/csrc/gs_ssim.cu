@@ -182,8 +182,17 @@ __global__ void __launch_bounds__(SS_THREADS) ssim_moments_kernel(const float* _
             part += (double)(1.f - S);
         }
     }
+    // one same-address fp64 atomic per CTA (per warp they serialise: ~1.2 M per 64 C4 views)
+    __shared__ double s_part[SS_WARPS];
     for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if (tx == 0 && part != 0.0) atomicAdd(loss, part * (double)scale);
+    if (tx == 0) s_part[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < SS_WARPS; ++w) sum += s_part[w];
+        if (sum != 0.0) atomicAdd(loss, sum * (double)scale);
+    }
 }
 
 __global__ void __launch_bounds__(SS_THREADS) ssim_grad_kernel(const float* __restrict__ X,
