@@ -497,10 +497,40 @@ def main():
         b1.record(stream)
         torch.cuda.synchronize()
         msp = b0.elapsed_time(b1) / Kb
+        del gpos, gsc, gq, gop, gsh
+        # Eq. 3's D-SSIM loss + gradient (gs_dssim_grad) on the batch's RGB planes, one call per
+        # run of equal-size views; target = the render with noise
+        runs = []
+        for i, v in enumerate(r.vb.views):
+            if runs and runs[-1][2:] == (v.height, v.width):
+                runs[-1][1] += 1
+            else:
+                runs.append([i, 1, v.height, v.width])
+        tgt = (r.images.rgb + 0.05 * torch.randn(r.images.rgb.numel(), generator=g4, device=dev)).clamp_(0, 1)
+        grgb = torch.zeros_like(r.images.rgb)
+        lss = torch.zeros(1, dtype=torch.float64, device=dev)
+        wsd = [None] * len(runs)
+
+        def _dssim():
+            for q, (i0, cnt, h, w) in enumerate(runs):
+                o, n = 3 * r.vb.pix_offset(i0), 3 * cnt * h * w
+                wsd[q] = G.gs_dssim_grad(r.images.rgb[o:o + n], tgt[o:o + n], 3 * cnt, h, w,
+                                         0.2 / r.images.rgb.numel(), grgb[o:o + n], lss, wsd[q], stream)
+        _dssim()
+        torch.cuda.synchronize()
+        b0.record(stream)
+        for _ in range(Kb):
+            _dssim()
+        b1.record(stream)
+        torch.cuda.synchronize()
+        msd = b0.elapsed_time(b1) / Kb
+        dssim_bytes = 48 * r.images.rgb.numel()
         n4 = {"views": n_views, "feature_backward_ms": ms4, "feature_backward_ms_per_view": ms4 / n_views,
               "radiance_backward_ms": msr, "radiance_backward_ms_per_view": msr / n_views,
-              "projection_backward_ms": msp, "feat_dim": scene.feat_dim, "gpu_launches": 6}
-        del gpos, gsc, gq, gop, gsh
+              "projection_backward_ms": msp, "dssim_grad_ms": msd, "dssim_grad_ms_per_view": msd / n_views,
+              "dssim_grad_GBps": dssim_bytes / (msd * 1e-3) / 1e9, "feat_dim": scene.feat_dim,
+              "gpu_launches": 6 + 2 * len(runs)}
+        del tgt, grgb, wsd
         del gimg, gfeat, gout, grec
 
     # N2 refinement loop: B queries, n = 3 rounds, one CUDA graph
