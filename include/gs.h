@@ -422,8 +422,8 @@ gs_status gs_feature_l1_grad(const float* rendered, const float* target, int64_t
  * With scale = lambda / (C H W) this is lambda * L_D-SSIM and its gradient.
  * workspace: device, >= gs_dssim_workspace_bytes(...) bytes, caller-owned
  * scratch (three fp32 partial-derivative planes per input plane).
- * Errors: GS_INVALID_ARG for negative sizes, n_planes > 65535, NULL pointers
- * (when the size is non-zero) or a short workspace; empty input is a no-op. */
+ * Errors: GS_INVALID_ARG for negative sizes, n_planes > 65535 or NULL pointers
+ * (when the size is non-zero); GS_WORKSPACE_TOO_SMALL; empty input is a no-op. */
 size_t gs_dssim_workspace_bytes(int32_t n_planes, int32_t height, int32_t width);
 gs_status gs_dssim_grad(const float* rendered, const float* target, int32_t n_planes, int32_t height, int32_t width,
                         float scale, float* grad_image, float* workspace, size_t workspace_bytes, double* loss,

@@ -254,7 +254,7 @@ extern "C" gs_status gs_dssim_grad(const float* rendered, const float* target, i
     GS_REQUIRE(n_planes <= 65535, GS_INVALID_ARG, "gs_dssim_grad: n_planes %d > 65535", n_planes);
     if (n_planes == 0 || height == 0 || width == 0) return GS_OK;
     GS_REQUIRE(rendered && target && grad_image && workspace && loss, GS_INVALID_ARG, "gs_dssim_grad: NULL pointer");
-    GS_REQUIRE(workspace_bytes >= gs_dssim_workspace_bytes(n_planes, height, width), GS_INVALID_ARG,
+    GS_REQUIRE(workspace_bytes >= gs_dssim_workspace_bytes(n_planes, height, width), GS_WORKSPACE_TOO_SMALL,
                "gs_dssim_grad: workspace %zu < %zu bytes", workspace_bytes,
                gs_dssim_workspace_bytes(n_planes, height, width));
     cudaStream_t s = (cudaStream_t)stream;

@@ -172,3 +172,20 @@ def test_struct_sizes_of_n2_types(G):
     assert ctypes.sizeof(G.gs.gs_matches) == 7 * 8
     assert ctypes.sizeof(G.gs.gs_pnp_stats) == 16
     assert ctypes.sizeof(G.gs.gs_bins) == 8 * 7 + 8
+
+
+def test_dssim_validates_on_the_host(G):
+    """gs_dssim_grad (Eq. 3's D-SSIM) rejects bad arguments before any launch; empty
+    input is a no-op; the workspace is three fp32 planes per input plane."""
+    L = G.lib()
+    fake = ctypes.c_void_p(256)
+    one = ctypes.c_float(1.0)
+    assert G.lib().gs_dssim_workspace_bytes(3, 768, 1024) == 3 * 3 * 768 * 1024 * 4
+    assert G.lib().gs_dssim_workspace_bytes(0, 768, 1024) == 0
+    assert L.gs_dssim_grad(fake, fake, -1, 4, 4, one, fake, fake, ctypes.c_size_t(1 << 20), fake, None) == 1
+    assert L.gs_dssim_grad(fake, fake, 70000, 4, 4, one, fake, fake, ctypes.c_size_t(1 << 30), fake, None) == 1
+    assert L.gs_dssim_grad(fake, None, 1, 4, 4, one, fake, fake, ctypes.c_size_t(1 << 20), fake, None) == 1
+    assert b"NULL" in L.gs_last_error()
+    assert L.gs_dssim_grad(fake, fake, 2, 4, 4, one, fake, fake, ctypes.c_size_t(2 * 3 * 16 * 4 - 1), fake,
+                           None) == 3
+    assert L.gs_dssim_grad(None, None, 0, 4, 4, one, None, None, ctypes.c_size_t(0), None, None) == 0

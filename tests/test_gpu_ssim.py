@@ -105,7 +105,7 @@ def test_dssim_bad_args(G):
     with pytest.raises(G.GSError):
         G.gs_dssim_grad(X, X, -1, 4, 4, 1.0, X, loss)
     ws = torch.zeros(1, device="cuda")
-    with pytest.raises(G.GSError):   # short workspace
+    with pytest.raises(G.GSError):   # short workspace (GS_WORKSPACE_TOO_SMALL)
         G.lib()
         import ctypes
         G.gs._check(G.lib().gs_dssim_grad(G.gs._ptr(X), G.gs._ptr(X), 1, 4, 4, ctypes.c_float(1.0), G.gs._ptr(X),
