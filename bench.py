@@ -500,12 +500,8 @@ def main():
         del gpos, gsc, gq, gop, gsh
         # Eq. 3's D-SSIM loss + gradient (gs_dssim_grad) on the batch's RGB planes, one call per
         # run of equal-size views; target = the render with noise
-        runs = []
-        for i, v in enumerate(r.vb.views):
-            if runs and runs[-1][2:] == (v.height, v.width):
-                runs[-1][1] += 1
-            else:
-                runs.append([i, 1, v.height, v.width])
+        from paper_2507_15683_b200.pipeline import equal_size_runs
+        runs = equal_size_runs(r.vb.views)
         tgt = (r.images.rgb + 0.05 * torch.randn(r.images.rgb.numel(), generator=g4, device=dev)).clamp_(0, 1)
         grgb = torch.zeros_like(r.images.rgb)
         lss = torch.zeros(1, dtype=torch.float64, device=dev)

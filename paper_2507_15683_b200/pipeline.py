@@ -288,6 +288,18 @@ class FeatureDistiller:
         return self.loss
 
 
+def equal_size_runs(views) -> list:
+    """Runs of consecutive equal-size views as (first, count, height, width): the
+    planes of a run are contiguous in gs_images, so one gs_dssim_grad call covers it."""
+    runs = []
+    for i, v in enumerate(views):
+        if runs and runs[-1][2:] == [v.height, v.width]:
+            runs[-1][1] += 1
+        else:
+            runs.append([i, 1, v.height, v.width])
+    return [tuple(r) for r in runs]
+
+
 class SceneTrainer:
     """N4: a joint training step of Eq. 1, L = alpha L_f + beta L_rgb, with Eq. 2's L1
     feature term and Eq. 3's L_rgb = (1 - lam) L1 + lam L_D-SSIM (reading Q37;
@@ -319,13 +331,7 @@ class SceneTrainer:
         dev = scene.pos.device
         self.rgb_scale = beta * (1.0 - lam) / self.r.images.rgb.numel()
         self.dssim_scale = beta * lam / self.r.images.rgb.numel()
-        # runs of consecutive equal-size views: their RGB planes are contiguous
-        self.dssim_runs, vb = [], self.r.vb
-        for i, v in enumerate(vb.views):
-            if self.dssim_runs and self.dssim_runs[-1][2:] == (v.height, v.width):
-                self.dssim_runs[-1][1] += 1
-            else:
-                self.dssim_runs.append([i, 1, v.height, v.width])
+        self.dssim_runs = equal_size_runs(self.r.vb.views)
         self.dssim_ws = None
         self.gout = G.Images(self.r.vb.total_pixels, 0, device=dev)
         self.gout.depth.zero_()

@@ -109,3 +109,14 @@ def test_bench_reference_arm_json():
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["unit"] == "Mpixels/s" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "oracle" and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_equal_size_runs_groups_consecutive_views():
+    """SceneTrainer / bench --n4 call gs_dssim_grad once per run of consecutive
+    equal-size views (their RGB planes are contiguous)."""
+    from types import SimpleNamespace as V
+    from paper_2507_15683_b200.pipeline import equal_size_runs
+    vs = [V(height=768, width=1024)] * 3 + [V(height=480, width=640), V(height=768, width=1024)]
+    assert equal_size_runs(vs) == [(0, 3, 768, 1024), (3, 1, 480, 640), (4, 1, 768, 1024)]
+    assert equal_size_runs([]) == []
+    assert len(equal_size_runs([V(height=8, width=8)] * 256)) == 1
