@@ -342,3 +342,33 @@ def test_scene_training_with_dssim(G):
     torch.cuda.synchronize()
     assert t.r.status() == 0
     assert losses[-1] < 0.6 * losses[0], losses[::8]
+
+
+def test_scene_training_dssim_ragged_views(G):
+    """Eq. 3 over a batch of views of three sizes (runs 64x64, 64x64, 48x80, 64x64): the
+    first step's loss equals the oracle's (1 - lam) mean|I^r - I| + lam (1 - mean SSIM),
+    the SSIM mean taken over every channel and pixel of the batch (reading Q37), which
+    checks the per-run gs_dssim_grad calls and their plane offsets."""
+    from oracle import ssim as OS
+    base = synth.box_v1(1500, seed=22, sh_degree=1)
+    views = [synth.box_view(), synth.box_view(), synth.box_view(80, 48), synth.box_view()]
+    rt = G.Renderer(G.DeviceScene(base), views, backproject=False)
+    rt.render()
+    target = rt.images.rgb.clone()
+    rng = np.random.default_rng(6)
+    start = dataclasses.replace(base, sh=base.sh + rng.normal(0, 0.3, base.sh.shape).astype(np.float32))
+    t = G.SceneTrainer(G.DeviceScene(start), views, target, optimizer="adam")
+    assert [r[1] for r in t.dssim_runs] == [2, 1, 1]
+    first = float(t.step().item())
+    torch.cuda.synchronize()
+    x_all = t.r.images.rgb.double().cpu().numpy()
+    y_all = target.double().cpu().numpy()
+    ssim_sum, o = 0.0, 0
+    for v in views:
+        n = 3 * v.height * v.width
+        x = x_all[o:o + n].reshape(3, v.height, v.width)
+        y = y_all[o:o + n].reshape(3, v.height, v.width)
+        ssim_sum += OS.ssim_map(x, y).sum()
+        o += n
+    want = 0.8 * np.abs(x_all - y_all).mean() + 0.2 * (1.0 - ssim_sum / x_all.size)
+    assert abs(first - want) <= 1e-5 * want, (first, want)
