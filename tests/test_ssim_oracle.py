@@ -72,3 +72,15 @@ def test_dssim_grad_vanishes_at_the_minimum():
     rng = np.random.default_rng(6)
     x = rng.uniform(0, 1, (3, 10, 9))
     assert np.abs(OS.dssim_grad(x, x)).max() < 1e-12
+
+
+def test_constant_planes_closed_form():
+    """Constant planes x = a, y = b: at pixels >= 5 from every border the window sees
+    no padding, the variances and covariance vanish and S reduces to the luminance
+    term (2ab + C1) / (a^2 + b^2 + C1) -- [3DGS]'s SSIM with C2 / C2 = 1."""
+    a, b = 0.7, 0.3
+    x = np.full((1, 15, 17), a)
+    y = np.full((1, 15, 17), b)
+    S = OS.ssim_map(x, y)[0, 5:-5, 5:-5]
+    want = (2 * a * b + OS.C1) / (a * a + b * b + OS.C1)
+    np.testing.assert_allclose(S, want, rtol=1e-12)
