@@ -31,6 +31,9 @@ namespace {
 #ifndef GS_SSIM_HJ_MOM
 #define GS_SSIM_HJ_MOM 4
 #endif
+#ifndef GS_SSIM_PRELOAD
+#define GS_SSIM_PRELOAD 1
+#endif
 #ifndef GS_SSIM_HJ_GRAD
 #define GS_SSIM_HJ_GRAD 4
 #endif
@@ -207,21 +210,38 @@ __global__ void __launch_bounds__(SS_THREADS) ssim_grad_kernel(const float* __re
     const int64_t off = (int64_t)blockIdx.z * H * W, woff = (int64_t)blockIdx.z * ws_plane_stride;
     const int x0 = blockIdx.x * SS_TW, y0 = blockIdx.y * SS_TH;
     const float* const src[3] = {dmu + woff, dxx + woff, dxy + woff};
+    const int tx = threadIdx.x & 31, r0 = (threadIdx.x >> 5) * SS_VR;
+    const int gx = x0 + tx;
+#if GS_SSIM_PRELOAD
+    // the epilogue's x, y and gradient loads issued first, in flight during the window passes
+    float px[SS_VR], py[SS_VR], pg[SS_VR];
+#pragma unroll
+    for (int j = 0; j < SS_VR; ++j) {
+        const int gy = y0 + r0 + j;
+        const bool in = gy < H && gx < W;
+        const int64_t o = off + (int64_t)gy * W + gx;
+        px[j] = in ? __ldg(X + o) : 0.f;
+        py[j] = in ? __ldg(Y + o) : 0.f;
+        pg[j] = in ? G[o] : 0.f;
+    }
+#endif
     load_halo<3>(s_in, src, H, W, x0, y0);
     __syncthreads();
     horizontal<3, 3, false, SS_HJ_GRAD>(s_in, s_h, win);
     __syncthreads();
-    const int tx = threadIdx.x & 31, r0 = (threadIdx.x >> 5) * SS_VR;
     float b[3][SS_VR];
     vertical<3>(s_h, r0, tx, win, b);
-    const int gx = x0 + tx;
 #pragma unroll
     for (int j = 0; j < SS_VR; ++j) {
         const int gy = y0 + r0 + j;
         if (gy < H && gx < W) {
             const int64_t o = off + (int64_t)gy * W + gx;
+#if GS_SSIM_PRELOAD
+            G[o] = pg[j] - scale * (b[0][j] + 2.f * px[j] * b[1][j] + py[j] * b[2][j]);
+#else
             const float x = __ldg(X + o), y = __ldg(Y + o);
             G[o] -= scale * (b[0][j] + 2.f * x * b[1][j] + y * b[2][j]);
+#endif
         }
     }
 }
