@@ -3,7 +3,7 @@
 // zero padding, C1 = 0.01^2, C2 = 0.03^2).
 //
 // Two tiled passes over n_planes contiguous H x W planes (measured: bound by
-// instruction issue, 77-87 %, at 0.41 of the HBM roofline).  Each CTA
+// instruction issue, 81-87 %, at 0.43 of the HBM roofline).  Each CTA
 // owns a 32 x 32 output tile: it stages the (32 + 10) x (32 + 10) halo of its
 // input planes in shared memory (zero outside the plane = the zero padding),
 // runs the separable window horizontally into a (32 + 10) x 32 buffer (four
