@@ -495,6 +495,17 @@ gs_status gs_rasterize_backproject(const gs_scene* scene, const gs_projected* pr
                                    uint8_t* valid, void* stream);
 
 /*
+ * gs_probe_alpha -- debug: alpha_out[i] = o_i 2^{p_i} evaluated exactly as
+ * gs_rasterize's walk evaluates it (the unclamped alpha of O12 step 4, P:136
+ * "alpha blending" with alpha = o exp(power) in log2 units, reading Q29), for
+ * checking the kernel's deviation from the oracle's fp64 2^p against the O14
+ * alpha band (reading Q20).  opacity, power, alpha_out: device
+ * float arrays of n elements (caller-owned; alpha_out must not alias).
+ * Errors: GS_INVALID_ARG for n < 0 or NULL pointers with n > 0.
+ */
+gs_status gs_probe_alpha(const float* opacity, const float* power, int64_t n, float* alpha_out, void* stream);
+
+/*
  * gs_backproject -- O13: valid iff A >= a_min and Dz/A > 0;
  * X = R^T(((px - cx)/fx zbar, (py - cy)/fy zbar, zbar) - t), zbar = Dz/A.
  * xyz is planar [3][H][W] per view at 3*pix_offset; invalid pixels get

@@ -173,6 +173,7 @@ def composite(view, rec, keys, feat=None, params: Optional[Params] = None) -> Di
     params = params or Params()
     D = 0 if feat is None else int(feat.shape[1])
     rgb, depth, alpha, F, flags = _alloc_images(view, D)
+    a_err = np.zeros_like(alpha)
     counters = np.zeros(2, np.int64)
     contrib = np.zeros(max(1, len(rec["gid"])), np.float64)
     vc, pc = _view_c(view), params.c()
@@ -180,9 +181,9 @@ def composite(view, rec, keys, feat=None, params: Optional[Params] = None) -> Di
                            _p(_c32(rec["conic"])), _p(_c32(rec["opacity"])), _p(_c32(rec["rgb"])),
                            _p(_c32(rec["z"])), _p(np.ascontiguousarray(rec["gid"], np.int32)), _p(_feat(feat, D)),
                            ctypes.c_int32(D), _p(keys["rec"]), _p(keys["ranges"]), _p(rgb), _p(depth), _p(alpha),
-                           _p(F), _p(flags), _p(counters), _p(contrib))
+                           _p(F), _p(flags), _p(counters), _p(contrib), _p(a_err))
     return dict(rgb=rgb, depth=depth, alpha=alpha, feat=F, flags=flags, evals=int(counters[0]),
-                blends=int(counters[1]), contrib=contrib[:len(rec["gid"])])
+                blends=int(counters[1]), contrib=contrib[:len(rec["gid"])], a_err=a_err)
 
 
 def feature_grad(view, rec, keys, feat, gF, n_gauss: int, params: Optional[Params] = None,
@@ -228,24 +229,27 @@ def brute_force(view, rec, feat=None, params: Optional[Params] = None) -> Dict[s
     vc, pc = _view_c(view), params.c()
     cnt = len(rec["gid"])
     contrib = np.zeros(max(1, cnt), np.float64)
+    a_err = np.zeros_like(alpha)
     lib().oracle_brute_force(ctypes.byref(vc), ctypes.byref(pc), ctypes.c_int64(cnt), _p(_c32(rec["u"])),
                              _p(_c32(rec["v"])), _p(_c32(rec["conic"])), _p(_c32(rec["opacity"])),
                              _p(_c32(rec["rgb"])), _p(_c32(rec["z"])),
                              _p(np.ascontiguousarray(rec["gid"], np.int32)),
                              _p(np.ascontiguousarray(rec["rect"], np.int32)), _p(_feat(feat, D)), ctypes.c_int32(D),
-                             _p(rgb), _p(depth), _p(alpha), _p(F), _p(flags), _p(contrib))
-    return dict(rgb=rgb, depth=depth, alpha=alpha, feat=F, flags=flags, contrib=contrib[:cnt])
+                             _p(rgb), _p(depth), _p(alpha), _p(F), _p(flags), _p(contrib), _p(a_err))
+    return dict(rgb=rgb, depth=depth, alpha=alpha, feat=F, flags=flags, contrib=contrib[:cnt], a_err=a_err)
 
 
-def backproject(view, depth, alpha, a_min: float = 0.5, flags=None):
-    """O13: rendered depth -> world points; returns xyz [3][H][W], valid [H][W], flags."""
+def backproject(view, depth, alpha, a_min: float = 0.5, flags=None, a_err=None):
+    """O13: rendered depth -> world points; returns xyz [3][H][W], valid [H][W], flags.
+    a_err [H][W] (from composite): O14 (c) bound on the kernel's deviation of A; pixels
+    with |A - a_min| <= a_err get flag bit 4.  None: the kernel back-projects the same A."""
     H, W = view.height, view.width
     xyz = np.zeros((3, H, W), np.float32)
     valid = np.zeros((H, W), np.uint8)
     fl = np.zeros((H, W), np.uint8) if flags is None else np.ascontiguousarray(flags, np.uint8).copy()
     vc = _view_c(view)
     lib().oracle_backproject(ctypes.byref(vc), _p(_c32(depth)), _p(_c32(alpha)), ctypes.c_float(a_min),
-                             _p(xyz), _p(valid), _p(fl))
+                             _p(xyz), _p(valid), _p(fl), None if a_err is None else _p(_c32(a_err)))
     return xyz, valid, fl
 
 
@@ -256,7 +260,7 @@ def render(scene, view, params: Optional[Params] = None, a_min: Optional[float] 
     img = composite(view, rec, keys, scene.feat, params)
     out = dict(rec=rec, keys=keys, **img)
     if a_min is not None:
-        xyz, valid, fl = backproject(view, img["depth"], img["alpha"], a_min, img["flags"])
+        xyz, valid, fl = backproject(view, img["depth"], img["alpha"], a_min, img["flags"], img["a_err"])
         out.update(xyz=xyz, valid=valid, flags=fl)
     return out
 

@@ -415,11 +415,23 @@ struct PixelOut {
     float T;
     uint8_t flags;
     int64_t evals, blends;
+    double a_err;   // O14: bound on |A_kernel - A_oracle| (absolute), for the a_min band
 };
 
-// flag bands (Q20): alpha within 2^-18 (relative) of alpha_min, Tn within 2^-12 of t_min
-const double FLAG_ALPHA_REL = 1.0 / 262144.0;
-const double FLAG_T_REL = 1.0 / 4096.0;
+// O14 flag bands (reading Q20, derived in DESIGN.md §2 "Q20 bands"): the only
+// decision input the kernel evaluates differently is 2^p (ex2.approx.ftz.f32 vs
+// the oracle's fp64 2^p).  EX2_REL bounds |ex2.approx(p) / 2^p - 1| over every
+// fp32 p <= 0 (measured exhaustively on the B200: tools/ex2_probe.cu,
+// profiles/r02_ex2_probe.json, times a margin of 2); both sides then round
+// o * 2^p once, so alpha_raw deviates by at most ALPHA_REL relative.  The
+// deviation of T is propagated step by step: 1 - alpha (absolute alpha
+// deviation, both sides' rounding), T (1 - alpha) (both sides' rounding).  A
+// decision is flagged when the oracle's value lies within BAND_SAFETY times the
+// propagated bound of its threshold.
+const double U24 = 1.0 / 16777216.0;          // 2^-24, unit roundoff of fp32
+const double EX2_REL = 1.0 / 2097152.0;       // 2^-21
+const double ALPHA_REL = EX2_REL + 2.0 * U24;
+const double BAND_SAFETY = 2.0;
 
 // N4 (feature-field backward, Eq. 2 with the geometry frozen): when gF is set,
 // fgrad[gid][c] += w * gF[c][pix] for every blended entry -- dL/df of a loss
@@ -441,6 +453,7 @@ void composite_pixel(const Records& rc, const or_params* P, int32_t pxi, int32_t
     o.flags = 0;
     o.evals = 0;
     o.blends = 0;
+    double eps_T = 0.0;   // O14: bound on |T_kernel / T_oracle - 1|
     for (int64_t k = 0; k < len; ++k) {
         const uint32_t i = list[k];
         o.evals++;
@@ -457,14 +470,21 @@ void composite_pixel(const Records& rc, const or_params* P, int32_t pxi, int32_t
         // 4. alpha = min(alpha_max, o exp(power)) = min(alpha_max, o 2^p); 2^p in fp64 rounded
         //    once to fp32
         const float araw = (float)((double)rc.opacity[i] * std::exp2((double)p));
-        if (std::fabs((double)araw - (double)P->alpha_min) <= FLAG_ALPHA_REL * P->alpha_min)
+        // O14 (a): the alpha >= alpha_min decision is ambiguous within ALPHA_REL
+        if (std::fabs((double)araw - (double)P->alpha_min) <= BAND_SAFETY * ALPHA_REL * (double)araw)
             o.flags |= 1;
         const float alpha = std::min(P->alpha_max, araw);
         // 5. skip if alpha < alpha_min (1/255)
         if (alpha < P->alpha_min) continue;
         // 6. Tn = T (1 - alpha); stop WITHOUT blending if Tn < t_min (Q15)
-        const float Tn = T * (1.0f - alpha);
-        if (std::fabs((double)Tn - (double)P->t_min) <= FLAG_T_REL * P->t_min) o.flags |= 2;
+        const float om = 1.0f - alpha;
+        const float Tn = T * om;
+        // O14 (b): deviation bound of Tn.  alpha deviates by <= ALPHA_REL alpha_raw
+        // unless both sides clamp to alpha_max (then it is identical)
+        const double d_alpha = ((double)araw > (double)P->alpha_max * (1.0 + ALPHA_REL)) ? 0.0
+                                                                                      : ALPHA_REL * (double)araw;
+        const double eps_Tn = eps_T + (d_alpha / (double)om + 2.0 * U24) + 2.0 * U24;
+        if (std::fabs((double)Tn - (double)P->t_min) <= BAND_SAFETY * eps_Tn * (double)Tn) o.flags |= 2;
         if (Tn < P->t_min) break;
         // 7. w = alpha T; accumulate colour, depth (camera z, Q16) and features (Q18)
         const float w = alpha * T;
@@ -481,12 +501,16 @@ void composite_pixel(const Records& rc, const or_params* P, int32_t pxi, int32_t
                 fg->fgrad[(int64_t)rc.gid[i] * rc.D + c] += (double)w * fg->gF[c * fg->HW + fg->pix];
         // 8. T = Tn
         T = Tn;
+        eps_T = eps_Tn;
     }
     o.T = T;
+    // O14 (c): A = 1 - T deviates by <= T eps_T plus both sides' rounding of 1 - T
+    o.a_err = BAND_SAFETY * ((double)T * eps_T + 2.0 * U24);
 }
 
 void store_pixel(const PixelOut& o, int64_t HW, int64_t pix, float* out_rgb, float* out_depth,
-                 float* out_alpha, float* out_feat, uint8_t* flags, int32_t D) {
+                 float* out_alpha, float* out_feat, uint8_t* flags, int32_t D, float* a_err) {
+    if (a_err) a_err[pix] = (float)o.a_err;
     for (int c = 0; c < 3; ++c) out_rgb[c * HW + pix] = (float)o.C[c];
     out_depth[pix] = (float)o.Dz;
     out_alpha[pix] = 1.0f - o.T;  // A = 1 - T
@@ -500,7 +524,7 @@ void oracle_composite(const or_view* V, const or_params* P, const float* u, cons
                       const int32_t* gid, const float* feat, int32_t D, const uint32_t* key_rec,
                       const uint32_t* ranges, float* out_rgb, float* out_depth, float* out_alpha,
                       float* out_feat, uint8_t* flags, int64_t* counters /*[2] E, B*/,
-                      double* contrib /*[cnt] or NULL*/) {
+                      double* contrib /*[cnt] or NULL*/, float* a_err /*[H][W] or NULL*/) {
     Records rc{u, v, conic, opac, rgb, z, gid, feat, D};
     const int32_t W = V->width, H = V->height, TX = (W + 15) / 16;
     const int64_t HW = (int64_t)W * H;
@@ -511,7 +535,7 @@ void oracle_composite(const or_view* V, const or_params* P, const float* u, cons
             const uint32_t s = ranges[t * 2], e = ranges[t * 2 + 1];
             composite_pixel(rc, P, px, py, key_rec + s, (int64_t)e - s, o, contrib);
             const int64_t pix = (int64_t)py * W + px;
-            store_pixel(o, HW, pix, out_rgb, out_depth, out_alpha, out_feat, flags, D);
+            store_pixel(o, HW, pix, out_rgb, out_depth, out_alpha, out_feat, flags, D, a_err);
             counters[0] += o.evals;
             counters[1] += o.blends;
         }
@@ -619,7 +643,8 @@ void oracle_brute_force(const or_view* V, const or_params* P, int64_t cnt, const
                         const float* v, const float* conic, const float* opac, const float* rgb,
                         const float* z, const int32_t* gid, const int32_t* rect, const float* feat,
                         int32_t D, float* out_rgb, float* out_depth, float* out_alpha,
-                        float* out_feat, uint8_t* flags, double* contrib /*[cnt] or NULL*/) {
+                        float* out_feat, uint8_t* flags, double* contrib /*[cnt] or NULL*/,
+                        float* a_err /*[H][W] or NULL*/) {
     Records rc{u, v, conic, opac, rgb, z, gid, feat, D};
     const int32_t W = V->width, H = V->height;
     const int64_t HW = (int64_t)W * H;
@@ -639,7 +664,7 @@ void oracle_brute_force(const or_view* V, const or_params* P, int64_t cnt, const
                 return gid[a] < gid[b];
             });
             composite_pixel(rc, P, px, py, list.data(), (int64_t)list.size(), o, contrib);
-            store_pixel(o, HW, (int64_t)py * W + px, out_rgb, out_depth, out_alpha, out_feat, flags, D);
+            store_pixel(o, HW, (int64_t)py * W + px, out_rgb, out_depth, out_alpha, out_feat, flags, D, a_err);
         }
 }
 
@@ -689,10 +714,12 @@ void oracle_visibility_score(const or_view* V, int64_t cnt, const float* u, cons
 // ---------------------------------------------------------------------------
 // O13: back-projection.  valid iff A >= a_min (fp32 compare) and Dz/A > 0;
 // zbar = Dz/A; X = R^T(((px - cx)/fx zbar, (py - cy)/fy zbar, zbar) - t)  (fp64).
-// flags bit 2 (value 4) marks |A - a_min| <= 2^-12 a_min (Q20).
+// flags bit 2 (value 4) marks |A - a_min| <= a_err[p], the O14 (c) bound on the
+// kernel's deviation of A (Q20); a_err = NULL means the kernel back-projects the
+// very same A (no band).
 // ---------------------------------------------------------------------------
 void oracle_backproject(const or_view* V, const float* depth, const float* alpha, float a_min,
-                        float* xyz /*[3][H][W]*/, uint8_t* valid, uint8_t* flags) {
+                        float* xyz /*[3][H][W]*/, uint8_t* valid, uint8_t* flags, const float* a_err) {
     const int32_t W = V->width, H = V->height;
     const int64_t HW = (int64_t)W * H;
     const float* R = V->R;
@@ -700,7 +727,7 @@ void oracle_backproject(const or_view* V, const float* depth, const float* alpha
         for (int32_t px = 0; px < W; ++px) {
             const int64_t p = (int64_t)py * W + px;
             const float A = alpha[p];
-            if (std::fabs((double)A - (double)a_min) <= FLAG_T_REL * a_min) flags[p] |= 4;
+            if (a_err && std::fabs((double)A - (double)a_min) <= (double)a_err[p]) flags[p] |= 4;
             const double zbar = (double)depth[p] / (double)A;
             if (!(A >= a_min) || !(zbar > 0.0)) {
                 xyz[p] = xyz[HW + p] = xyz[2 * HW + p] = 0.0f;

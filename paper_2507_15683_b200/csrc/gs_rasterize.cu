@@ -189,6 +189,11 @@ __device__ __forceinline__ void fma2_acc(float& x, float& y, float w, float a, f
     x = v.x; y = v.y;
 }
 
+// o 2^p as the walk evaluates it (ex2.approx + one rounded product): the only
+// decision input that differs from the oracle's fp64 2^p; its deviation is
+// bounded by the O14 alpha band (reading Q20, checked by gs_probe_alpha).
+__device__ __forceinline__ float alpha_raw(float o, float p) { return __fmul_rn(o, ex2_ftz(p)); }
+
 // alpha of entry k at this lane's pixel, or 0 when the oracle skips it (p > 0
 // or alpha < alpha_min).  p(d) = dx (ea dx + eb dy) + ec dy dy with the oracle's
 // fused multiply-adds (reading Q29); alpha = min(alpha_max, o 2^p).
@@ -197,7 +202,7 @@ __device__ __forceinline__ float entry_alpha(const float4& a, const float4& b, f
     const float2 d = sub2_rn(a.x, a.y, pxf, pyf);
     const float dx = d.x, dy = d.y;
     const float p = __fmaf_rn(dx, __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy)), __fmul_rn(__fmul_rn(b.x, dy), dy));
-    const float alpha = fminf(P.alpha_max, __fmul_rn(b.y, ex2_ftz(p)));
+    const float alpha = fminf(P.alpha_max, alpha_raw(b.y, p));
     // skipped iff p > 0 or alpha < alpha_min (alpha is never NaN: fminf with alpha_max);
     // one compare feeds the other so the pair costs two FSETP and one select
     float r;
@@ -1260,6 +1265,12 @@ extern "C" gs_status gs_rasterize_backproject(const gs_scene* scene, const gs_pr
 
 namespace gs {
 namespace {
+__global__ void probe_alpha_kernel(const float* __restrict__ o, const float* __restrict__ p, int64_t n,
+                                   float* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = alpha_raw(o[i], p[i]);
+}
+
 __global__ void features_f16_kernel(const float4* __restrict__ f, uint2* __restrict__ out, int64_t n4) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
         const float4 x = f[i];
@@ -1269,6 +1280,15 @@ __global__ void features_f16_kernel(const float4* __restrict__ f, uint2* __restr
 }
 }  // namespace
 }  // namespace gs
+
+extern "C" gs_status gs_probe_alpha(const float* opacity, const float* power, int64_t n, float* alpha_out,
+                                    void* stream) {
+    GS_REQUIRE(n >= 0 && (n == 0 || (opacity && power && alpha_out)), GS_INVALID_ARG, "gs_probe_alpha: bad arguments");
+    if (n == 0) return GS_OK;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+    probe_alpha_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(opacity, power, n, alpha_out);
+    return check_launch("probe_alpha_kernel");
+}
 
 extern "C" gs_status gs_scene_features_f16(const gs_scene* scene, void* feat_h_out, void* stream) {
     gs_status st = validate_scene(scene, false);

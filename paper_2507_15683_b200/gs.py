@@ -75,7 +75,7 @@ EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_lay
            "gs_feature_l1_grad", "gs_feature_sgd", "gs_dssim_grad", "gs_dssim_workspace_bytes",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_rasterize_backproject", "gs_backproject", "gs_visibility_score",
-           "gs_visibility_workspace_bytes"]
+           "gs_visibility_workspace_bytes", "gs_probe_alpha"]
 
 _lib = None
 
@@ -493,6 +493,15 @@ def gs_dssim_grad(rendered: torch.Tensor, target: torch.Tensor, n_planes: int, h
                                ctypes.c_int32(width), ctypes.c_float(scale), _ptr(grad_image), _ptr(workspace),
                                ctypes.c_size_t(workspace.numel() * 4), _ptr(loss), _stream(stream)), "gs_dssim_grad")
     return workspace
+
+
+def gs_probe_alpha(opacity: torch.Tensor, power: torch.Tensor, out: torch.Tensor, stream=None):
+    """Debug: out = o 2^p as gs_rasterize's walk evaluates it (reading Q20 / Q29)."""
+    assert opacity.dtype == power.dtype == out.dtype == torch.float32
+    n = opacity.numel()
+    assert power.numel() == n and out.numel() == n
+    _check(lib().gs_probe_alpha(_ptr(opacity), _ptr(power), ctypes.c_int64(n), _ptr(out), _stream(stream)),
+           "gs_probe_alpha")
 
 
 def gs_scene_block_bounds(scene: "DeviceScene", stream=None):
