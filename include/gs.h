@@ -272,6 +272,21 @@ gs_status gs_validate_scene(const gs_scene* scene, int32_t unit_quat, int64_t* f
                             void* stream);
 
 /*
+ * gs_sanitize_scene -- N4 training helper: after an optimizer step on the raw
+ * parameter planes (Eq. 1-3 update Theta_i), project every Gaussian
+ * back onto the set gs_project renders (readings Q3, Q19): opacity clamped to
+ * [opacity_min, 1] (opacity_min >= alpha_min keeps it from being culled as
+ * transparent and never receiving a gradient again), each scale to a finite
+ * value >= scale_min (a scale <= 0 is degenerate, Q19), and a zero or
+ * non-finite quaternion reset to identity.  Scene planes are modified in place
+ * (device); changed (device, 1 x uint64) is incremented by the number of
+ * Gaussians changed.  Errors: GS_INVALID_ARG for a bad scene, NULL changed,
+ * opacity_min outside [0, 1] or scale_min <= 0.
+ */
+gs_status gs_sanitize_scene(const gs_scene* scene, float opacity_min, float scale_min, uint64_t* changed,
+                            void* stream);
+
+/*
  * N2 -- coarse-to-fine probabilistic mutual matching (Eq. 11 at
  * P:312-316; readings Q31-Q34).  For each of n_pairs (query,
  * rendered) feature-map pairs of equal size, planar [D][H][W] f32 (the layout

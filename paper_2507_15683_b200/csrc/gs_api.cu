@@ -148,6 +148,36 @@ __global__ void validate_scene_kernel(gs_scene S, int32_t unit_quat, unsigned lo
     }
 }
 
+// gs_sanitize_scene: project the parameters back onto the set gs_project renders
+// (opacity in [opacity_min, 1], finite scales >= scale_min, a non-zero finite
+// quaternion); counts the Gaussians it changed.
+__global__ void sanitize_scene_kernel(gs_scene S, float opacity_min, float scale_min, unsigned long long* changed) {
+    const int64_t n = S.n;
+    unsigned long long local = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        bool ch = false;
+        float* op = const_cast<float*>(S.opacity) + i;
+        const float o = *op;
+        const float oc = (o == o) ? fminf(fmaxf(o, opacity_min), 1.0f) : opacity_min;
+        if (oc != o) { *op = oc; ch = true; }
+        for (int k = 0; k < 3; ++k) {
+            float* sp = const_cast<float*>(S.scale) + (int64_t)k * n + i;
+            const float sv = *sp;
+            const float sc = (sv == sv) ? fminf(fmaxf(sv, scale_min), 3.0e38f) : scale_min;   // NaN -> scale_min
+            if (sc != sv) { *sp = sc; ch = true; }
+        }
+        float* q = const_cast<float*>(S.quat);
+        const float qw = q[i], qx = q[n + i], qy = q[2 * n + i], qz = q[3 * n + i];
+        const float qq = qw * qw + qx * qx + qy * qy + qz * qz;
+        if (!(isfinite(qq) && qq > 1e-30f)) {
+            q[i] = 1.f; q[n + i] = 0.f; q[2 * n + i] = 0.f; q[3 * n + i] = 0.f;
+            ch = true;
+        }
+        local += ch;
+    }
+    if (local) atomicAdd(changed, local);
+}
+
 __global__ void validate_finish_kernel(unsigned long long* key, int32_t* reason) {
     const unsigned long long k = *key;
     const bool valid = k == ~0ull;
@@ -172,4 +202,17 @@ extern "C" gs_status gs_validate_scene(const gs_scene* scene, int32_t unit_quat,
     }
     gs::validate_finish_kernel<<<1, 1, 0, s>>>(key, reason);
     return gs::check_launch("validate_finish_kernel");
+}
+
+extern "C" gs_status gs_sanitize_scene(const gs_scene* scene, float opacity_min, float scale_min, uint64_t* changed,
+                                       void* stream) {
+    gs_status st = gs::validate_scene(scene, true);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(opacity_min >= 0.f && opacity_min <= 1.f && scale_min > 0.f && changed != nullptr, GS_INVALID_ARG,
+               "gs_sanitize_scene: need 0 <= opacity_min <= 1, scale_min > 0, changed != NULL");
+    if (scene->n == 0) return GS_OK;
+    const int64_t blocks = std::min<int64_t>((scene->n + 255) / 256, (int64_t)gs::num_sms() * 8);
+    gs::sanitize_scene_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        *scene, opacity_min, scale_min, reinterpret_cast<unsigned long long*>(changed));
+    return gs::check_launch("sanitize_scene_kernel");
 }

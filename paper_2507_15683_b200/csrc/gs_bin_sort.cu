@@ -806,12 +806,9 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     for (int i = 0; i < n_views; ++i)
         max_tiles = std::max(max_tiles, tiles_x(views_host[i]) * tiles_y(views_host[i]));
     const int hist_smem = (int)sizeof(uint32_t) * std::min(max_tiles, HIST_MAX);
-    static bool hist_attr = false;
-    if (!hist_attr) {
-        cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_MAX * 4);
-        cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_MAX * 4);
-        hist_attr = true;
-    }
+    // kernel attributes are per device: set on every call (cheap)
+    cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_MAX * 4);
+    cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_MAX * 4);
     const int tight = out->mode == GS_BIN_TIGHT;
     // per-(view, chunk, tile) offsets of count_kernel for the scatter, kept in the big-sort
     // scratch (unused until after the scatter) when it is large enough
@@ -845,12 +842,8 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
                                                       out->sorted_key, w.big_count, w.mid_list, proj->status);
         if ((st = check_launch("mid_sort_kernel")) != GS_OK) return st;
     }
-    static bool attr_set = false;
     const int smem = 2 * RUN_PAD * (int)(sizeof(uint64_t) + sizeof(uint32_t));
-    if (!attr_set) {
-        cudaFuncSetAttribute(big_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr_set = true;
-    }
+    cudaFuncSetAttribute(big_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int big_threads = latency ? LAT_THREADS : BIG_THREADS;
     const int big_grid = latency ? 2 * num_sms() : 4 * num_sms();
     big_sort_kernel<<<big_grid, big_threads, smem, s>>>(out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb,

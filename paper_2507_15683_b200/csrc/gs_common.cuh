@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdarg>
 
@@ -41,15 +42,25 @@ gs_status validate_views(const gs_view* views_host, const gs_view* views_dev, in
                          int64_t* total_pixels, int64_t* total_tiles);
 gs_status validate_scene(const gs_scene* s, bool need_geometry);
 
+// Per-device caches (a process may drive several GPUs; kernel attributes and
+// occupancy are per device): index = the current device, atomic so concurrent
+// host threads never race.
+constexpr int GS_MAX_DEVICES = 64;
+inline int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
 inline int num_sms() {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+    static std::atomic<int> cache[GS_MAX_DEVICES];
+    const int dev = current_device();
+    int v = (dev >= 0 && dev < GS_MAX_DEVICES) ? cache[dev].load(std::memory_order_relaxed) : 0;
+    if (v <= 0) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 148;
+        if (dev >= 0 && dev < GS_MAX_DEVICES) cache[dev].store(v, std::memory_order_relaxed);
     }
-    return sms;
+    return v;
 }
 
 // ---------------------------------------------------------------- device side

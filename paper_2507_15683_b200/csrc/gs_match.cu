@@ -526,12 +526,8 @@ gs_status launch_rows(const MatchWs& w, int B, int Nc, int Ncp, float k2, cudaSt
     // each CTA allocates all 512 TMEM columns: request enough shared memory that only
     // one CTA is resident per SM (a second would just wait in tcgen05.alloc)
     const int smem = std::max((int)sizeof(RowSmem<D>), 120 * 1024);
-    static bool init = false;
-    if (!init) {
-        cudaFuncSetAttribute(row_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(row_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        init = true;
-    }
+    cudaFuncSetAttribute(row_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(row_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const dim3 grid(Ncp / CB, 2, B);
     row_kernel<D, false><<<grid, ROW_THREADS, smem, s>>>(w, Nc, Ncp, k2);
     gs_status st = check_launch("row_kernel<stats>");
@@ -589,11 +585,7 @@ extern "C" gs_status gs_match(const float* query_feat, const float* rend_feat, i
     mnn_kernel<<<dim3((Nc + 255) / 256, n_pairs), 256, 0, s>>>(w, Nc, Ncp, p_min, out->coarse, out->coarse_prob);
     if ((st = check_launch("mnn_kernel")) != GS_OK) return st;
     const int fsmem = (int)sizeof(float) * (std::max(2 * WP * (D + 1), WP * 65) + 3 * WP) + 4 * WP * (D + 8) * 2;
-    static bool fine_init = false;
-    if (!fine_init) {
-        cudaFuncSetAttribute(fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
-        fine_init = true;
-    }
+    cudaFuncSetAttribute(fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     fine_kernel<<<dim3(Nc, n_pairs), 256, fsmem, s>>>(query_feat, rend_feat, D, H, W, Nc, out->coarse, k2, p_min,
                                                       rend_xyz, rend_valid, *out);
     return check_launch("fine_kernel");

@@ -805,10 +805,15 @@ gs_status launch(const gs_scene* scene, const gs_projected* proj, const gs_bins*
                  int n_views, int64_t T, const gs_params* P, gs_images* out, cudaStream_t s, float a_min,
                  float* xyz, uint8_t* valid) {
     const int smem = (int)sizeof(RasterSmem<D, CONTRIB, TC>);
-    static int blocks_per_sm = 0;
+    // kernel attributes are per device: set on every call (cheap); the occupancy is
+    // cached per device
+    cudaFuncSetAttribute(rasterize_kernel<D, CONTRIB, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(rasterize_kernel<D, CONTRIB, TC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    static std::atomic<int> bps_cache[GS_MAX_DEVICES];
+    const int cur_dev = current_device();
+    const bool cacheable = cur_dev >= 0 && cur_dev < GS_MAX_DEVICES;
+    int blocks_per_sm = cacheable ? bps_cache[cur_dev].load(std::memory_order_relaxed) : 0;
     if (blocks_per_sm == 0) {
-        cudaFuncSetAttribute(rasterize_kernel<D, CONTRIB, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(rasterize_kernel<D, CONTRIB, TC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         const cudaError_t e =
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rasterize_kernel<D, CONTRIB, TC>, RT_THREADS, smem);
         if (TC) {
@@ -830,6 +835,7 @@ gs_status launch(const gs_scene* scene, const gs_projected* proj, const gs_bins*
             fprintf(stderr, "[gs] rasterize<%d,%d>: smem %d B, occupancy %d CTAs/SM (%s)\n", D, (int)CONTRIB, smem,
                     blocks_per_sm, cudaGetErrorString(e));
         if (blocks_per_sm < 1) blocks_per_sm = 1;
+        if (cacheable) bps_cache[cur_dev].store(blocks_per_sm, std::memory_order_relaxed);
     }
     const int64_t grid =
         std::min<int64_t>((T + SCHED_CHUNK - 1) / SCHED_CHUNK, (int64_t)num_sms() * blocks_per_sm);

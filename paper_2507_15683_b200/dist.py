@@ -11,8 +11,9 @@ in the CPU tests).  No arithmetic of the method happens here.
 from __future__ import annotations
 
 import heapq
+import math
 import os
-from typing import List, Optional, Sequence
+from typing import Callable, List, Optional, Sequence
 
 import torch
 import torch.distributed as dist
@@ -52,34 +53,109 @@ def shard_sizes(n_views: int, world: int, costs: Optional[Sequence[float]] = Non
     return [len(shard_views(n_views, world, r, costs)) for r in range(world)]
 
 
-def pack_planes(rgb: torch.Tensor, depth: torch.Tensor, alpha: torch.Tensor, n_views: int, hw: int,
-                pad_views: int) -> torch.Tensor:
-    """[pad_views, 5, hw] float32 payload (RGB, Dz, A per view; zero padded)."""
-    out = torch.zeros((pad_views, 5, hw), dtype=torch.float32, device=rgb.device)
-    if n_views:
-        out[:n_views, 0:3] = rgb.view(n_views, 3, hw)
-        out[:n_views, 3] = depth.view(n_views, hw)
-        out[:n_views, 4] = alpha.view(n_views, hw)
-    return out
+def all_gather_flat(out: torch.Tensor, x: torch.Tensor, group=None):
+    """out[r * n:(r + 1) * n] = rank r's x.  NCCL: all_gather_into_tensor (one
+    contiguous receive buffer); gloo (CPU tests): all_gather into views of out."""
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, x, group=group)
+    else:
+        dist.all_gather(list(out.view(world, -1).unbind(0)), x, group=group)
 
 
-def gather_planes(payload: torch.Tensor, world: int, group=None) -> torch.Tensor:
-    """all_gather_into_tensor of equally padded per-rank payloads
-    -> [world * pad_views, 5, hw]."""
-    if world == 1:
-        return payload
-    out = torch.empty((world * payload.shape[0],) + tuple(payload.shape[1:]), dtype=payload.dtype,
-                      device=payload.device)
-    dist.all_gather_into_tensor(out, payload.contiguous(), group=group)
-    return out
+class ChunkedGather:
+    """The multi-GPU step of SURVEY.md §8(e): every rank renders its shard of the
+    pose batch in chunks of `chunk` views; each chunk is rendered straight into
+    its send buffer and gathered with one collective on a dedicated comm stream
+    that waits only for that chunk's render, so the gather of chunk k overlaps
+    the render of chunk k + 1.
+
+    Send buffer of chunk k (one flat tensor, the render's output planes):
+        [ RGB  3 x c x hw | Dz  c x hw | A  c x hw ]   (c = `chunk` views)
+    i.e. the planar layout of gs_images for the chunk's views (RGB at
+    3 * pix_offset, Dz / A at pix_offset) -- no packing copy, no zero fill.  A
+    rank whose shard is shorter renders fewer views into its last chunk(s); the
+    unused tail is never read.  Views are assigned by shard_views (LPT over
+    per-view costs when given, e.g. pair counts of a projection pre-pass).
+    Every rank issues the same number of equally sized collectives."""
+
+    def __init__(self, n_views: int, hw: int, world: int, rank: int, chunk: int,
+                 costs: Optional[Sequence[float]] = None, device="cpu", group=None, comm_stream=None):
+        self.n_views, self.hw, self.world, self.rank, self.chunk = n_views, hw, world, rank, max(1, chunk)
+        self.costs = costs
+        self.group = group
+        self.shards = [shard_views(n_views, world, r, costs) for r in range(world)]
+        self.mine = self.shards[rank]
+        self.n_chunks = max(1, math.ceil(max(len(sh) for sh in self.shards) / self.chunk))
+        n = 5 * self.chunk * hw
+        self.send = [torch.empty(n, dtype=torch.float32, device=device) for _ in range(self.n_chunks)]
+        self.recv = [torch.empty(world * n, dtype=torch.float32, device=device) for _ in range(self.n_chunks)]
+        self.cuda = torch.device(device).type == "cuda"
+        self.comm = comm_stream if comm_stream is not None else (torch.cuda.Stream(device) if self.cuda else None)
+        self.rendered = [torch.cuda.Event() for _ in range(self.n_chunks)] if self.cuda else None
+        self.sent = [torch.cuda.Event() for _ in range(self.n_chunks)] if self.cuda else None
+        self.steps = 0
+
+    def chunk_views(self, k: int) -> List[int]:
+        """Global indices of the views this rank renders in chunk k (may be empty)."""
+        return self.mine[k * self.chunk:(k + 1) * self.chunk]
+
+    def planes(self, k: int):
+        """(rgb, depth, alpha) output planes of chunk k inside its send buffer."""
+        c, hw, b = self.chunk, self.hw, self.send[k]
+        return b[:3 * c * hw], b[3 * c * hw:4 * c * hw], b[4 * c * hw:5 * c * hw]
+
+    @property
+    def bytes_per_step(self) -> int:
+        """Bytes each rank receives per step (all chunks, all ranks' payloads)."""
+        return sum(t.numel() * t.element_size() for t in self.recv)
+
+    def step(self, render_chunk: Callable[[int], None], stream=None, gather: bool = True):
+        """render_chunk(k) enqueues chunk k's render (into planes(k)) on `stream`."""
+        for k in range(self.n_chunks):
+            if self.cuda and self.steps > 0 and gather:
+                stream.wait_event(self.sent[k])          # the send buffer is free again
+            render_chunk(k)
+            if not gather or self.world == 1:
+                continue
+            if self.cuda:
+                self.rendered[k].record(stream)
+                self.comm.wait_event(self.rendered[k])
+                with torch.cuda.stream(self.comm):
+                    all_gather_flat(self.recv[k], self.send[k], self.group)
+                self.sent[k].record(self.comm)
+            else:
+                all_gather_flat(self.recv[k], self.send[k], self.group)
+        self.steps += 1
+
+    def wait(self, stream=None):
+        """Make `stream` wait for every gather of the last step."""
+        if self.cuda and self.world > 1:
+            for e in self.sent:
+                stream.wait_event(e)
+
+    def assemble(self) -> torch.Tensor:
+        """[n_views, 5, hw] in global view order from the receive buffers (planes
+        RGB, Dz, A) -- what a consumer of the gathered batch reads."""
+        c, hw = self.chunk, self.hw
+        out = torch.empty((self.n_views, 5, hw), dtype=torch.float32, device=self.recv[0].device)
+        for k in range(self.n_chunks):
+            rv = self.recv[k].view(self.world, 5 * c * hw) if self.world > 1 else self.send[k].view(1, -1)
+            for r in range(self.world):
+                idx = self.shards[r][k * c:(k + 1) * c]
+                for j, g in enumerate(idx):
+                    buf = rv[r]
+                    out[g, 0:3] = buf[3 * j * hw:3 * (j + 1) * hw].view(3, hw)
+                    out[g, 3] = buf[3 * c * hw + j * hw:3 * c * hw + (j + 1) * hw]
+                    out[g, 4] = buf[4 * c * hw + j * hw:4 * c * hw + (j + 1) * hw]
+        return out
 
 
-def unshard(gathered: torch.Tensor, n_views: int, world: int, costs: Optional[Sequence[float]] = None) -> torch.Tensor:
-    """Reorder a gathered [world * pad, 5, hw] tensor into global view order."""
-    pad = gathered.shape[0] // world
-    out = torch.empty((n_views,) + tuple(gathered.shape[1:]), dtype=gathered.dtype, device=gathered.device)
-    for r in range(world):
-        idx = shard_views(n_views, world, r, costs)
-        if idx:
-            out[torch.tensor(idx, device=gathered.device)] = gathered[r * pad:r * pad + len(idx)]
+def view_costs_from_ranges(ranges: torch.Tensor, tile_offsets: Sequence[int], tiles_per_view: Sequence[int]):
+    """Per-view pair counts from a binned batch's tile ranges (lower-bound
+    convention: a view's pairs are [start of its first tile, end of its last))."""
+    r = ranges.view(-1, 2).to("cpu").numpy().view("uint32").astype("int64")
+    out = []
+    for t0, nt in zip(tile_offsets, tiles_per_view):
+        out.append(float(r[t0 + nt - 1, 1] - r[t0, 0]))
     return out

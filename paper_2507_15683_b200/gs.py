@@ -75,7 +75,7 @@ EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_lay
            "gs_feature_l1_grad", "gs_feature_sgd", "gs_dssim_grad", "gs_dssim_workspace_bytes",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_rasterize_backproject", "gs_backproject", "gs_visibility_score",
-           "gs_visibility_workspace_bytes", "gs_probe_alpha"]
+           "gs_visibility_workspace_bytes", "gs_probe_alpha", "gs_sanitize_scene"]
 
 _lib = None
 
@@ -268,10 +268,18 @@ class Bins:
 
 
 class Images:
-    def __init__(self, total_pixels: int, feat_dim: int, device="cuda"):
-        self.rgb = torch.empty(3 * total_pixels, dtype=torch.float32, device=device)
-        self.depth = torch.empty(total_pixels, dtype=torch.float32, device=device)
-        self.alpha = torch.empty(total_pixels, dtype=torch.float32, device=device)
+    def __init__(self, total_pixels: int, feat_dim: int, device="cuda", rgb=None, depth=None, alpha=None):
+        """Output planes; rgb / depth / alpha may be caller tensors (e.g. views into a
+        collective's send buffer, dist.ChunkedGather) of at least 3x / 1x / 1x
+        total_pixels float32 elements."""
+        def buf(t, n):
+            if t is None:
+                return torch.empty(n, dtype=torch.float32, device=device)
+            assert t.dtype == torch.float32 and t.is_contiguous() and t.numel() >= n
+            return t[:n]
+        self.rgb = buf(rgb, 3 * total_pixels)
+        self.depth = buf(depth, total_pixels)
+        self.alpha = buf(alpha, total_pixels)
         self.feat = torch.empty(feat_dim * total_pixels, dtype=torch.float32, device=device) if feat_dim else None
         s = gs_images()
         s.rgb, s.depth, s.alpha, s.feat = _ptr(self.rgb), _ptr(self.depth), _ptr(self.alpha), _ptr(self.feat)
@@ -493,6 +501,14 @@ def gs_dssim_grad(rendered: torch.Tensor, target: torch.Tensor, n_planes: int, h
                                ctypes.c_int32(width), ctypes.c_float(scale), _ptr(grad_image), _ptr(workspace),
                                ctypes.c_size_t(workspace.numel() * 4), _ptr(loss), _stream(stream)), "gs_dssim_grad")
     return workspace
+
+
+def gs_sanitize_scene(scene: "DeviceScene", opacity_min: float, scale_min: float, changed: torch.Tensor,
+                      stream=None):
+    """N4: clamp opacity to [opacity_min, 1], scales to >= scale_min, reset zero
+    quaternions (in place); `changed` (int64 [1], device) counts the Gaussians changed."""
+    _check(lib().gs_sanitize_scene(ctypes.byref(scene.struct), ctypes.c_float(opacity_min), ctypes.c_float(scale_min),
+                                   _ptr(changed), _stream(stream)), "gs_sanitize_scene")
 
 
 def gs_probe_alpha(opacity: torch.Tensor, power: torch.Tensor, out: torch.Tensor, stream=None):

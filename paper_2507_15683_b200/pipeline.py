@@ -19,7 +19,8 @@ class Renderer:
     def __init__(self, scene: G.DeviceScene, views: Sequence, params: Optional[G.gs_params] = None,
                  a_min: float = 0.5, backproject: bool = True, rec_capacity: Optional[int] = None,
                  pair_capacity: Optional[int] = None, debug_keys: bool = False, use_blocks: bool = True,
-                 contrib: bool = False, binning: str = "tight", device="cuda"):
+                 contrib: bool = False, binning: str = "tight", device="cuda", out_planes=None,
+                 alloc_images: bool = True):
         self.device = torch.device(device)
         self.scene = scene
         self.scene_struct = scene.struct if use_blocks else scene.without_blocks()
@@ -33,7 +34,13 @@ class Renderer:
         n_views = self.vb.n
         self.ws_proj = torch.empty(max(1, G.project_workspace_bytes(scene.n_blocks if use_blocks else 0, n_views)),
                                    dtype=torch.uint8, device=self.device)
-        self.images = G.Images(self.vb.total_pixels, scene.feat_dim, device=self.device)
+        # out_planes = (rgb, depth, alpha) caller tensors, e.g. a gather send buffer
+        rgb, dep, alp = out_planes if out_planes is not None else (None, None, None)
+        # alloc_images=False: projection + binning only (e.g. a pair-count pre-pass)
+        self.images = G.Images(self.vb.total_pixels, scene.feat_dim, device=self.device, rgb=rgb, depth=dep,
+                               alpha=alp) if alloc_images else None
+        backproject = backproject and alloc_images
+        self.do_backproject = backproject
         self.xyz = torch.empty(3 * self.vb.total_pixels, dtype=torch.float32, device=self.device) if backproject else None
         self.valid = torch.empty(self.vb.total_pixels + 4, dtype=torch.uint8, device=self.device) if backproject else None
         self.proj = None
@@ -76,6 +83,8 @@ class Renderer:
             self.proj.status.zero_()
         G.gs_project(self.scene, vb, self.params, self.proj, self.ws_proj, stream, scene_struct=self.scene_struct)
         G.gs_bin_sort(self.proj, vb, self.bins, self.ws_bin, stream)
+        if self.images is None:
+            return
         if self.do_backproject:
             # O13 fused into the compositing epilogue (same values as gs_backproject)
             G.gs_rasterize_backproject(self.scene, self.proj, self.bins, vb, self.params, self.images, self.a_min,
@@ -85,6 +94,14 @@ class Renderer:
 
     def status(self) -> int:
         return int(self.proj.status.item())
+
+    def view_pair_counts(self):
+        """Per-view pair counts of the last run (from the tile ranges), e.g. the
+        costs of dist.shard_views' LPT assignment."""
+        from .dist import view_costs_from_ranges
+        offs = [self.vb.tile_offset(i) for i in range(self.vb.n)]
+        nts = [((v.width + 15) // 16) * ((v.height + 15) // 16) for v in self.vb.views]
+        return view_costs_from_ranges(self.bins.ranges, offs, nts)
 
     def render(self, max_retries: int = 4):
         """Run, and on capacity overflow grow the buffers to the reported sizes and re-run."""
@@ -278,7 +295,7 @@ class FeatureDistiller:
 
     def step(self, stream=None) -> torch.Tensor:
         """One iteration; returns the device loss (of the features before the update)."""
-        self.r.run(stream)
+        ensure_rendered(self.r, stream)
         self.loss.zero_()
         G.gs_feature_l1_grad(self.r.images.feat, self.target, self.scale, self.gimg, self.loss, stream)
         self.gfeat.zero_()
@@ -288,12 +305,26 @@ class FeatureDistiller:
         return self.loss
 
 
-def equal_size_runs(views) -> list:
+def ensure_rendered(r: Renderer, stream=None):
+    """Run the hot path for a training step and check the device status (one sync):
+    on a capacity overflow (Gaussians moved / grew since the buffers were sized) grow
+    the buffers and re-render, so no loss or gradient is ever computed from a stale
+    or partial render."""
+    r.run(stream)
+    if r.status() != 0:
+        r.render()
+        r.fit_capacities(slack=1.5)
+        r.render()
+
+
+def equal_size_runs(views, max_views: Optional[int] = None) -> list:
     """Runs of consecutive equal-size views as (first, count, height, width): the
-    planes of a run are contiguous in gs_images, so one gs_dssim_grad call covers it."""
+    planes of a run are contiguous in gs_images, so one gs_dssim_grad call covers it.
+    max_views splits longer runs, bounding gs_dssim_grad's workspace (12 B per pixel
+    per plane of one call) -- SceneTrainer uses 64 views per call."""
     runs = []
     for i, v in enumerate(views):
-        if runs and runs[-1][2:] == [v.height, v.width]:
+        if runs and runs[-1][2:] == [v.height, v.width] and (max_views is None or runs[-1][1] < max_views):
             runs[-1][1] += 1
         else:
             runs.append([i, 1, v.height, v.width])
@@ -331,7 +362,7 @@ class SceneTrainer:
         dev = scene.pos.device
         self.rgb_scale = beta * (1.0 - lam) / self.r.images.rgb.numel()
         self.dssim_scale = beta * lam / self.r.images.rgb.numel()
-        self.dssim_runs = equal_size_runs(self.r.vb.views)
+        self.dssim_runs = equal_size_runs(self.r.vb.views, max_views=64)
         self.dssim_ws = None
         self.gout = G.Images(self.r.vb.total_pixels, 0, device=dev)
         self.gout.depth.zero_()
@@ -345,6 +376,9 @@ class SceneTrainer:
             self.gimg = torch.empty_like(self.r.images.feat)
             self.gfeat = torch.zeros_like(scene.feat)
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.opacity_min = float(self.r.params.alpha_min)
+        self.scale_min = 1e-6
+        self.sanitized = torch.zeros(1, dtype=torch.int64, device=dev)   # Gaussians clamped so far
         self.state = {}
         if optimizer == "adam":
             keys = list(self.PLANES) + (["feat"] if target_feat is not None else [])
@@ -361,7 +395,7 @@ class SceneTrainer:
         """One iteration; returns the device loss of the parameters before the update."""
         sc, r = self.scene, self.r
         self.t += 1
-        r.run(stream)
+        ensure_rendered(r, stream)
         self.loss.zero_()
         G.gs_feature_l1_grad(r.images.rgb, self.target_rgb, self.rgb_scale, self.gout.rgb, self.loss, stream)
         if self.dssim_scale != 0.0:
@@ -385,6 +419,8 @@ class SceneTrainer:
             self._update("feat", sc.feat, self.gfeat, sc.feat_h, stream)
         for k in self.PLANES:
             self._update(k, getattr(sc, k), self.grads[k], None, stream)
+        # keep every Gaussian renderable: opacity in [alpha_min, 1], scale > 0
+        G.gs_sanitize_scene(sc, self.opacity_min, self.scale_min, self.sanitized, stream)
         if sc.block_bounds is not None:
             G.gs_scene_block_bounds(sc, stream)   # the means moved
         return self.loss

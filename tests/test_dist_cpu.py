@@ -1,8 +1,9 @@
 """Multi-process host logic of the pose-sharded path on CPU (gloo, world size 2):
-view sharding, RGB+depth+opacity packing, the all_gather and the unshard back to
-global view order.  Each rank "renders" its shard with the CPU oracle (test
-infrastructure), so the gathered planes must equal a single-process render
-bit for bit."""
+view sharding (contiguous / LPT over pre-pass costs), the chunked gather of
+dist.ChunkedGather (render straight into per-chunk send buffers, one collective
+per chunk) and the assembly back to global view order.  Each rank "renders" its
+shard with the CPU oracle (test infrastructure), so the gathered planes must
+equal a single-process render bit for bit."""
 import json
 import os
 import socket
@@ -52,53 +53,87 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n_views, use_costs, out_path):
+def _views(n_views):
+    import synth
+    return [synth.make_view(np.eye(3), [0.05 * i, -0.03 * i, 0.0], 48, 48, 23.5, 15.5, 48, 32) for i in range(n_views)]
+
+
+def _oracle_render_chunk(cg, views, scene):
+    """Fill chunk k's send buffer in the gs_images planar layout (what the GPU
+    Renderer writes through out_planes): view j of the chunk at RGB 3 j hw,
+    Dz / A at j hw."""
+    import oracle
+
+    def render(k):
+        rgb, dep, alp = cg.planes(k)
+        hw = cg.hw
+        for j, i in enumerate(cg.chunk_views(k)):
+            r = oracle.render(scene, views[i])
+            rgb[3 * j * hw:3 * (j + 1) * hw] = torch.from_numpy(r["rgb"].reshape(-1))
+            dep[j * hw:(j + 1) * hw] = torch.from_numpy(r["depth"].reshape(-1))
+            alp[j * hw:(j + 1) * hw] = torch.from_numpy(r["alpha"].reshape(-1))
+    return render
+
+
+def _worker(rank, world, port, n_views, use_costs, chunk, out_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    import oracle
     import synth
     scene = synth.box_v1(300, seed=9)
-    views = [synth.make_view(np.eye(3), [0.05 * i, -0.03 * i, 0.0], 48, 48, 23.5, 15.5, 48, 32)
-             for i in range(n_views)]
+    views = _views(n_views)
     costs = [float(i % 3 + 1) for i in range(n_views)] if use_costs else None
-    mine = GD.shard_views(n_views, world, rank, costs)
-    hw = 48 * 32
-    rgb = np.zeros((len(mine), 3, hw), np.float32)
-    dep = np.zeros((len(mine), hw), np.float32)
-    alp = np.zeros((len(mine), hw), np.float32)
-    for k, i in enumerate(mine):
-        r = oracle.render(scene, views[i])
-        rgb[k] = r["rgb"].reshape(3, hw)
-        dep[k] = r["depth"].reshape(hw)
-        alp[k] = r["alpha"].reshape(hw)
-    pad = max(GD.shard_sizes(n_views, world, costs))
-    payload = GD.pack_planes(torch.from_numpy(rgb.reshape(-1)), torch.from_numpy(dep.reshape(-1)),
-                             torch.from_numpy(alp.reshape(-1)), len(mine), hw, pad)
-    gathered = GD.gather_planes(payload, world)
-    full = GD.unshard(gathered, n_views, world, costs)
+    cg = GD.ChunkedGather(n_views, 48 * 32, world, rank, chunk, costs)
+    assert cg.n_chunks == -(-max(len(s) for s in cg.shards) // chunk)
+    render = _oracle_render_chunk(cg, views, scene)
+    for _ in range(2):                       # two steps reuse the send / receive buffers
+        cg.step(render)
+    full = cg.assemble()
     if rank == 0:
         torch.save(full, out_path)
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("use_costs", [False, True])
-def test_gloo_gather_equals_single_process(tmp_path, use_costs):
+def _single_process(n_views):
     import oracle
     import synth
+    scene = synth.box_v1(300, seed=9)
+    return [oracle.render(scene, v) for v in _views(n_views)]
+
+
+@pytest.mark.parametrize("use_costs,chunk", [(False, 2), (True, 2), (True, 1), (False, 8)])
+def test_gloo_chunked_gather_equals_single_process(tmp_path, use_costs, chunk):
+    """dist.ChunkedGather (the bench's multi-GPU step: per-chunk render straight
+    into the send buffer, one all_gather per chunk) at world size 2 assembles
+    planes bit-identical to a single-process render."""
+    import oracle
     oracle.build()
     n_views = 5
     out = str(tmp_path / "gathered.pt")
-    mp.spawn(_worker, args=(2, _free_port(), n_views, use_costs, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), n_views, use_costs, chunk, out), nprocs=2, join=True)
     full = torch.load(out)
-    scene = synth.box_v1(300, seed=9)
-    for i in range(n_views):
-        v = synth.make_view(np.eye(3), [0.05 * i, -0.03 * i, 0.0], 48, 48, 23.5, 15.5, 48, 32)
-        r = oracle.render(scene, v)
+    for i, r in enumerate(_single_process(n_views)):
         assert np.array_equal(full[i, 0:3].numpy(), r["rgb"].reshape(3, -1))
         assert np.array_equal(full[i, 3].numpy(), r["depth"].reshape(-1))
         assert np.array_equal(full[i, 4].numpy(), r["alpha"].reshape(-1))
+
+
+def test_chunked_gather_world_one_is_the_render():
+    import synth
+    scene = synth.box_v1(300, seed=9)
+    views = _views(3)
+    cg = GD.ChunkedGather(3, 48 * 32, 1, 0, 2)
+    cg.step(_oracle_render_chunk(cg, views, scene))
+    full = cg.assemble()
+    for i, r in enumerate(_single_process(3)):
+        assert np.array_equal(full[i, 4].numpy(), r["alpha"].reshape(-1))
+
+
+def test_view_costs_from_ranges():
+    # two views of 3 and 2 tiles; lower-bound ranges (empty tiles start = end)
+    ranges = torch.tensor([0, 4, 4, 4, 4, 9, 9, 10, 10, 10], dtype=torch.int32)
+    assert GD.view_costs_from_ranges(ranges, [0, 3], [3, 2]) == [9.0, 1.0]
 
 
 def test_bench_reference_arm_json():
@@ -120,3 +155,5 @@ def test_equal_size_runs_groups_consecutive_views():
     assert equal_size_runs(vs) == [(0, 3, 768, 1024), (3, 1, 480, 640), (4, 1, 768, 1024)]
     assert equal_size_runs([]) == []
     assert len(equal_size_runs([V(height=8, width=8)] * 256)) == 1
+    # bounded calls (gs_dssim_grad workspace): 256 views in groups of <= 64
+    assert equal_size_runs([V(height=8, width=8)] * 130, max_views=64) == [(0, 64, 8, 8), (64, 64, 8, 8), (128, 2, 8, 8)]

@@ -372,3 +372,56 @@ def test_scene_training_dssim_ragged_views(G):
         o += n
     want = 0.8 * np.abs(x_all - y_all).mean() + 0.2 * (1.0 - ssim_sum / x_all.size)
     assert abs(first - want) <= 1e-5 * want, (first, want)
+
+
+def test_sanitize_scene_projects_onto_renderable_set(G):
+    """gs_sanitize_scene: opacity -> [opacity_min, 1], scales -> finite >= scale_min,
+    zero / non-finite quaternions -> identity; valid Gaussians untouched; the count."""
+    sc = synth.box_v1(64, seed=3)
+    ds = G.DeviceScene(sc)
+    ds.opacity[1] = -0.5
+    ds.opacity[2] = 1.7
+    ds.opacity[3] = float("nan")
+    ds.scale[0 * 64 + 5] = 0.0
+    ds.scale[1 * 64 + 6] = -3.0
+    ds.scale[2 * 64 + 7] = float("nan")
+    ds.quat[0 * 64 + 9] = 0.0
+    ds.quat[1 * 64 + 9] = 0.0
+    ds.quat[2 * 64 + 9] = 0.0
+    ds.quat[3 * 64 + 9] = 0.0
+    before = {k: getattr(ds, k).clone() for k in ("opacity", "scale", "quat")}
+    changed = torch.zeros(1, dtype=torch.int64, device="cuda")
+    G.gs_sanitize_scene(ds, 1.0 / 255.0, 1e-6, changed)
+    torch.cuda.synchronize()
+    assert int(changed.item()) == 7
+    op = ds.opacity.cpu().numpy()
+    assert abs(op[1] - np.float32(1 / 255)) == 0 and op[2] == 1.0 and op[3] == np.float32(1 / 255)
+    s = ds.scale.view(3, 64).cpu().numpy()
+    assert s[0, 5] == np.float32(1e-6) and s[1, 6] == np.float32(1e-6) and s[2, 7] == np.float32(1e-6)
+    assert list(ds.quat.view(4, 64)[:, 9].cpu().numpy()) == [1.0, 0.0, 0.0, 0.0]
+    untouched = np.setdiff1d(np.arange(64), [1, 2, 3, 5, 6, 7, 9])
+    for k, n in (("opacity", 1), ("scale", 3), ("quat", 4)):
+        a = getattr(ds, k).view(n, 64)[:, untouched]
+        assert torch.equal(a, before[k].view(n, 64)[:, untouched]), k
+
+
+def test_training_keeps_every_gaussian_renderable(G):
+    """an aggressive SGD step size drives raw opacities below alpha_min and
+    scales towards 0; after every step the trainer's gs_sanitize_scene keeps them
+    renderable (opacity in [alpha_min, 1], scale > 0) and the status is checked each
+    step (a capacity overflow re-renders instead of training on a stale image)."""
+    base = synth.box_v1(800, seed=33, sh_degree=0)
+    v = synth.box_view()
+    rt = G.Renderer(G.DeviceScene(base), [v], backproject=False)
+    rt.render()
+    target = torch.zeros_like(rt.images.rgb)          # a black target pulls opacity down
+    ds = G.DeviceScene(base)
+    t = G.SceneTrainer(ds, [v], target, lam=0.0, lr={"opacity": 5e3, "scale": 50.0})
+    for _ in range(15):
+        t.step()
+    torch.cuda.synchronize()
+    op, s = ds.opacity.cpu().numpy(), ds.scale.cpu().numpy()
+    assert op.min() >= np.float32(1 / 255) and op.max() <= 1.0
+    assert s.min() > 0 and np.isfinite(s).all()
+    assert int(t.sanitized.item()) > 0
+    assert t.r.status() == 0
