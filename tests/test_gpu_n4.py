@@ -382,13 +382,11 @@ def test_sanitize_scene_projects_onto_renderable_set(G):
     ds.opacity[1] = -0.5
     ds.opacity[2] = 1.7
     ds.opacity[3] = float("nan")
-    ds.scale[0 * 64 + 5] = 0.0
-    ds.scale[1 * 64 + 6] = -3.0
-    ds.scale[2 * 64 + 7] = float("nan")
-    ds.quat[0 * 64 + 9] = 0.0
-    ds.quat[1 * 64 + 9] = 0.0
-    ds.quat[2 * 64 + 9] = 0.0
-    ds.quat[3 * 64 + 9] = 0.0
+    sc3, q4 = ds.scale.view(3, 64), ds.quat.view(4, 64)
+    sc3[0, 5] = 0.0
+    sc3[1, 6] = -3.0
+    sc3[2, 7] = float("nan")
+    q4[:, 9] = 0.0
     before = {k: getattr(ds, k).clone() for k in ("opacity", "scale", "quat")}
     changed = torch.zeros(1, dtype=torch.int64, device="cuda")
     G.gs_sanitize_scene(ds, 1.0 / 255.0, 1e-6, changed)
