@@ -205,9 +205,10 @@ def feature_grad(view, rec, keys, feat, gF, n_gauss: int, params: Optional[Param
 GRAD_FIELDS = ("u", "v", "ea", "eb", "ec", "opacity", "r", "g", "b", "z")
 
 
-def radiance_backward(view, rec, keys, gC, gD, gA, params: Optional[Params] = None):
-    """N4: per-record gradient [cnt][10] (GRAD_FIELDS) of L = sum gC.C + gD Dz + gA A,
-    and L itself (fp64).  gC [3][H][W], gD / gA [H][W]."""
+def radiance_backward(view, rec, keys, gC, gD, gA, params: Optional[Params] = None, feat=None, gF=None):
+    """N4: per-record gradient [cnt][10] (GRAD_FIELDS) of L = sum gC.C + gD Dz + gA A
+    (+ sum gF.F with gF [D][H][W] and the scene features [n][D]: Eq. 2's feature term
+    through the blend weights), and L itself (fp64).  gC [3][H][W], gD / gA [H][W]."""
     params = params or Params()
     cnt = len(rec["gid"])
     grec = np.zeros((max(1, cnt), 10), np.float64)
@@ -217,7 +218,8 @@ def radiance_backward(view, rec, keys, gC, gD, gA, params: Optional[Params] = No
         ctypes.byref(vc), ctypes.byref(pc), _p(_c32(rec["u"])), _p(_c32(rec["v"])), _p(_c32(rec["conic"])),
         _p(_c32(rec["opacity"])), _p(_c32(rec["rgb"])), _p(_c32(rec["z"])),
         _p(np.ascontiguousarray(rec["gid"], np.int32)), _p(keys["rec"]), _p(keys["ranges"]), _p(_c32(gC)),
-        _p(_c32(gD)), _p(_c32(gA)), _p(grec))
+        _p(_c32(gD)), _p(_c32(gA)), _p(grec), None if gF is None else _p(_c32(feat)),
+        ctypes.c_int32(0 if gF is None else int(feat.shape[1])), None if gF is None else _p(_c32(gF)))
     return grec[:cnt], float(loss)
 
 

@@ -568,10 +568,18 @@ void oracle_feature_grad(const or_view* V, const or_params* P, const float* u, c
 // The skip and stop decisions are taken exactly as in composite_pixel (their
 // gradient is zero); a clamped alpha (0.99) has no opacity / exponent gradient.
 // Also returns the loss itself in fp64 (for finite-difference pins).
+// N4 joint step (Eq. 1 with Eq. 2's feature term through the geometry):
+// gF (may be NULL) is this pixel's upstream gradient of the rendered feature
+// vector F = sum_k w_k f_k; it enters exactly like a colour channel,
+//   dF_c/dalpha_k = T_k f_kc - (F_c - F_c,<=k) / (1 - alpha_k),
+// and the returned loss includes sum_c gF_c F_c.
 double backward_pixel(const Records& rc, const or_params* P, int32_t pxi, int32_t pyi, const uint32_t* list,
-                      int64_t len, const double gC[3], double gD, double gA, double* grec /*[cnt][10]*/) {
+                      int64_t len, const double gC[3], double gD, double gA, double* grec /*[cnt][10]*/,
+                      const double* gF = nullptr) {
     PixelOut f;
     composite_pixel(rc, P, pxi, pyi, list, len, f, nullptr);
+    const int32_t DF = gF ? rc.D : 0;
+    std::vector<double> Facc(DF, 0.0);
     const double Tf = f.T;
     const float pxf = (float)pxi, pyf = (float)pyi;
     float T = 1.0f;
@@ -600,6 +608,13 @@ double backward_pixel(const Records& rc, const or_params* P, int32_t pxi, int32_
         for (int q = 0; q < 3; ++q) dLda += gC[q] * ((double)T * c[q] - (f.C[q] - Cacc[q]) / om);
         dLda += gD * ((double)T * rc.z[i] - (f.Dz - Dacc) / om);
         dLda += gA * (Tf / om);
+        if (DF) {
+            const float* fk = rc.feat + (int64_t)rc.gid[i] * rc.D;
+            for (int q = 0; q < DF; ++q) {
+                Facc[q] += (double)w * fk[q];
+                dLda += gF[q] * ((double)T * fk[q] - (f.F[q] - Facc[q]) / om);
+            }
+        }
         double* g = grec + (int64_t)i * 10;
         for (int q = 0; q < 3; ++q) g[6 + q] += (double)w * gC[q];
         g[9] += (double)w * gD;
@@ -615,23 +630,31 @@ double backward_pixel(const Records& rc, const or_params* P, int32_t pxi, int32_
         }
         T = Tn;
     }
-    return gC[0] * f.C[0] + gC[1] * f.C[1] + gC[2] * f.C[2] + gD * f.Dz + gA * (1.0 - Tf);
+    double loss = gC[0] * f.C[0] + gC[1] * f.C[1] + gC[2] * f.C[2] + gD * f.Dz + gA * (1.0 - Tf);
+    for (int q = 0; q < DF; ++q) loss += gF[q] * f.F[q];
+    return loss;
 }
 
 double oracle_radiance_backward(const or_view* V, const or_params* P, const float* u, const float* v,
                                 const float* conic, const float* opac, const float* rgb, const float* z,
                                 const int32_t* gid, const uint32_t* key_rec, const uint32_t* ranges,
-                                const float* gC /*[3][H][W]*/, const float* gD, const float* gA, double* grec) {
-    Records rc{u, v, conic, opac, rgb, z, gid, nullptr, 0};
+                                const float* gC /*[3][H][W]*/, const float* gD, const float* gA, double* grec,
+                                const float* feat /*[n_gauss][D] or NULL*/, int32_t D,
+                                const float* gF /*[D][H][W] or NULL*/) {
+    Records rc{u, v, conic, opac, rgb, z, gid, feat, gF ? D : 0};
     const int32_t W = V->width, H = V->height, TX = (W + 15) / 16;
     const int64_t HW = (int64_t)W * H;
     double loss = 0.0;
+    std::vector<double> gpx(gF ? D : 0);
     for (int32_t py = 0; py < H; ++py)
         for (int32_t px = 0; px < W; ++px) {
             const int64_t t = (int64_t)(py / 16) * TX + px / 16, pix = (int64_t)py * W + px;
             const uint32_t s = ranges[t * 2], e = ranges[t * 2 + 1];
             const double g3[3] = {gC[pix], gC[HW + pix], gC[2 * HW + pix]};
-            loss += backward_pixel(rc, P, px, py, key_rec + s, (int64_t)e - s, g3, gD[pix], gA[pix], grec);
+            if (gF)
+                for (int32_t q = 0; q < D; ++q) gpx[q] = gF[(int64_t)q * HW + pix];
+            loss += backward_pixel(rc, P, px, py, key_rec + s, (int64_t)e - s, g3, gD[pix], gA[pix], grec,
+                                   gF ? gpx.data() : nullptr);
         }
     return loss;
 }

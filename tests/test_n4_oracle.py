@@ -333,3 +333,67 @@ def test_param_grads_finite_differences(orc, field):
             assert min(abs(fd - an) for fd in fds) <= 5e-3 * max(abs(an), 1e-2), (r, i, fds, an)
             checked += abs(an) > 1e-2
     assert checked > 0
+
+
+# ------------------------------------------------------------------ Eq. 1 joint step: L_f through the geometry
+def _smooth_feature_fixture():
+    from helpers import scene_of
+    rng = np.random.default_rng(31)
+    feat = rng.standard_normal((3, 8)).astype(np.float32)
+    sc = scene_of([{"mu": [0.1, -0.05, 5.0], "scale": 1.2, "opacity": 0.5},
+                   {"mu": [-0.2, 0.1, 5.5], "scale": 1.5, "opacity": 0.4},
+                   {"mu": [0.05, 0.2, 6.0], "scale": 1.8, "opacity": 0.6}], feat=feat)
+    v = synth.make_view(np.eye(3), np.zeros(3), 20.0, 20.0, 11.5, 9.5, 24, 20)
+    return sc, v
+
+
+@pytest.mark.parametrize("field", ["u", "v", "conic0", "conic1", "conic2", "opacity"])
+def test_feature_loss_geometry_gradient_finite_differences(orc, field):
+    """Eq. 1-2: the feature term's gradient through the blend weights
+    into each record's (u, v, conic, opacity) -- central differences of
+    L = sum_px gF(px) . F(px) (the forward composite) on the smooth fixture."""
+    sc, v = _smooth_feature_fixture()
+    o = orc.render(sc, v)
+    assert (o["flags"] == 0).all()
+    rec, keys = o["rec"], o["keys"]
+    rng = np.random.default_rng(8)
+    z3 = np.zeros((3, 20, 24), np.float32)
+    z1 = np.zeros((20, 24), np.float32)
+    gF = rng.standard_normal((8, 20, 24)).astype(np.float32)
+    grad, loss = orc.radiance_backward(v, rec, keys, z3, z1, z1, feat=sc.feat, gF=gF)
+    np.testing.assert_allclose(loss, float((gF.astype(np.float64) * o["feat"]).sum()), rtol=1e-6)
+    lossf = lambda r: orc.radiance_backward(v, r, keys, z3, z1, z1, feat=sc.feat, gF=gF)[1]
+    for i in range(len(rec["gid"])):
+        r2 = {k: np.array(a, copy=True) for k, a in rec.items() if isinstance(a, np.ndarray)}
+        r3 = {k: np.array(a, copy=True) for k, a in rec.items() if isinstance(a, np.ndarray)}
+        if field.startswith("conic"):
+            c = int(field[-1])
+            h = 1e-4
+            r2["conic"][i, c] += h; r3["conic"][i, c] -= h
+            an = grad[i, 2 + c] * float(K2) * (2.0 if c == 1 else 1.0)
+        else:
+            h = 1e-2
+            r2[field][i] += h; r3[field][i] -= h
+            an = grad[i, {"u": 0, "v": 1, "opacity": 5}[field]]
+        fd = (lossf(r2) - lossf(r3)) / (2 * h)
+        assert abs(fd - an) <= 5e-3 * max(abs(an), 1e-3), (i, fd, an)
+    assert np.abs(grad[:, 6:]).max() == 0          # the feature term moves no colour / depth
+
+
+def test_feature_term_adds_linearly(orc):
+    """grad(gC, gD, gA, gF) = grad(gC, gD, gA) + grad(0, 0, 0, gF) (the loss is linear
+    in the upstream gradients) on a random tiny scene with features."""
+    rng = np.random.default_rng(90)
+    sc = random_tiny_scene(rng, 150, feat_dim=8, sh_degree=1)
+    v = synth.make_view(np.eye(3), np.zeros(3), 40.0, 40.0, 23.5, 17.5, 48, 36)
+    o = orc.render(sc, v)
+    gC = rng.standard_normal((3, 36, 48)).astype(np.float32)
+    gD = rng.standard_normal((36, 48)).astype(np.float32)
+    gA = rng.standard_normal((36, 48)).astype(np.float32)
+    gF = rng.standard_normal((8, 36, 48)).astype(np.float32)
+    a, la = orc.radiance_backward(v, o["rec"], o["keys"], gC, gD, gA)
+    b, lb = orc.radiance_backward(v, o["rec"], o["keys"], 0 * gC, 0 * gD, 0 * gA, feat=sc.feat, gF=gF)
+    c, lc = orc.radiance_backward(v, o["rec"], o["keys"], gC, gD, gA, feat=sc.feat, gF=gF)
+    np.testing.assert_allclose(c, a + b, rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(lc, la + lb, rtol=1e-9)
+    assert np.abs(b[:, :6]).max() > 0
