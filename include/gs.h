@@ -391,6 +391,39 @@ gs_status gs_radiance_backward(const gs_projected* proj, const gs_bins* bins, co
                                const gs_images* fwd, const gs_images* grad_out, float* grad_rec, void* stream);
 
 /*
+ * gs_appearance_l1_grad -- N4, Eq. 3's L1 term between the ground truth I and the
+ * appearance-varied rendering I^a (reading Q38: per view and channel an
+ * affine transform I^a = a I^r + b of the direct rendering, trained jointly).
+ * n_planes planes of plane_pixels pixels each (a run of equal-size views: plane
+ * 3 v + c), plane p uses a[p], b[p].  Writes grad_image = scale sign(I^a - I) a
+ * (dL/dI^r), accumulates grad_a[p] += scale sum sign(I^a - I) I^r,
+ * grad_b[p] += scale sum sign(I^a - I) and loss += scale sum |I^a - I| (fp64).
+ * All device pointers.  Errors: GS_INVALID_ARG for NULL pointers or sizes out of
+ * range (n_planes > 65535).
+ */
+gs_status gs_appearance_l1_grad(const float* rendered, const float* target, int32_t n_planes, int64_t plane_pixels,
+                                const float* a, const float* b, float scale, float* grad_image, float* grad_a,
+                                float* grad_b, double* loss, void* stream);
+
+/*
+ * gs_joint_backward -- N4, Eq. 1's joint loss: gs_radiance_backward
+ * plus Eq. 2's feature term through the blend weights.  grad_out->feat
+ * ([D][H][W] per view, the gs_images layout) is dL/dF of the rendered feature
+ * map; F = sum_k w_k f_k enters like a colour channel, so each record's
+ * {u, v, ea, eb, ec, opacity} gradient also receives
+ * sum_px dL/dalpha_k with dF/dalpha_k = T_k f_k - (F - F_<=k)/(1 - alpha_k)
+ * (scene->feat: the fp32 feature rows; fwd->feat: the forward's feature map).
+ * The gradient w.r.t. the features themselves is gs_feature_backward's.
+ * grad_out->feat == NULL or D == 0: exactly gs_radiance_backward.
+ * Errors: as gs_radiance_backward; GS_UNSUPPORTED for D not in
+ * {8, 16, 24, 32, 48, 64}.
+ */
+gs_status gs_joint_backward(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins,
+                            const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
+                            const gs_params* params, const gs_images* fwd, const gs_images* grad_out,
+                            float* grad_rec, void* stream);
+
+/*
  * N4 projection backward: chains grad_rec (from gs_radiance_backward, same
  * proj) through O1-O7 -- pinhole u, v and depth z, the clamped EWA Jacobian
  * (Q6), the 2D covariance, its inverse and e = k conic (Q29) -- to the

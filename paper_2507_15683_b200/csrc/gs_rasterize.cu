@@ -75,10 +75,6 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
     return p;
 }
-// 16-B global->shared copy through L1 (the line was just read by an ordinary load)
-__device__ __forceinline__ void cp_async16_ca(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
 // the mbarrier receives one arrival when all prior cp.async of this thread have landed
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
@@ -853,474 +849,6 @@ gs_status launch(const gs_scene* scene, const gs_projected* proj, const gs_bins*
     return check_launch("rasterize_kernel");
 }
 
-// ---------------------------------------------------------------- decoupled-warp rasterizer
-// gs_rasterize's hot configuration (no N1 contributions; D = 0, or the tcgen05
-// feature path) as warp-independent pipelines: a CTA's 8 warps
-// render the 8 sub-rectangles (8x4 px) of the CTA's tiles, but each warp streams
-// its tile lists itself -- indices two 32-entry batches ahead, records one batch
-// ahead in registers, the per-warp exact ellipse cull and compaction into a
-// private walk ring, the walked entries' fp16 feature rows cp.async'd straight
-// into the warp's canonical B tiles -- so no warp ever waits for another (the
-// shared producer ring of rasterize_kernel held every warp to the slowest one).
-// The CTA only shares its in-order tile sequence (claimed one tile at a time
-// from the global scheduler, a ring of WTQ slots bounds how far its warps drift
-// apart) and the TMEM accumulators.  Per-pixel arithmetic is rasterize_kernel's
-// (entry_alpha, blend_om: the oracle's exact decisions, reading Q29).
-constexpr int WNW = 8;          // warps per CTA (sub-rectangles of a tile)
-constexpr int WTQ = 8;          // CTA tile-sequence ring: max tiles between the CTA's fastest and slowest warp
-constexpr int WRING = 64;       // per-warp walk ring (compacted entries)
-constexpr int WNB = 4;          // per-warp B-tile buffers (k-steps of 16 feature rows)
-
-template <int D, bool TC>
-struct WSmem {
-    float4 walk[WNW][WRING][3];                                           // u v ea eb | ec o - - | r g b z
-    alignas(128) __half btile[TC ? WNW : 1][TC ? WNB : 1][TC ? 16 * D : 8];
-    uint64_t mma_bar[TC ? WNW : 1][TC ? WNB : 1];
-    uint32_t tq_tile[WTQ], tq_view[WTQ], tq_rs[WTQ], tq_re[WTQ];
-    int tq_seq[WTQ];                                                      // index + 1 once slot filled
-    int tq_next;                                                          // next sequence index to claim
-    int wprog[WNW];                                                       // index each warp is rendering
-    uint32_t tmem_base;
-};
-
-struct WBatch {                 // warp-uniform descriptor of one 32-entry batch of a tile list
-    int i;                      // CTA sequence index of the tile (-1: end)
-    uint32_t c0;
-    int cnt;
-    bool first, last;
-};
-
-template <int D, bool TC>
-__global__ void __launch_bounds__(WNW * 32, (TC ? (D > 32 ? 2 : 3) : 4))
-rasterize_warp_kernel(const gs_view* __restrict__ views, int n_views, uint32_t uniform_tpv,
-                      const gs_record* __restrict__ rec, const uint32_t* __restrict__ sorted_rec,
-                      const uint32_t* __restrict__ sorted_gid, const uint32_t* __restrict__ ranges, uint32_t n_tiles,
-                      uint32_t* __restrict__ tile_sched, const __half* __restrict__ feat_h, gs_params P,
-                      float* __restrict__ out_rgb, float* __restrict__ out_depth, float* __restrict__ out_alpha,
-                      float* __restrict__ out_feat, const uint32_t* __restrict__ status, float a_min,
-                      float* __restrict__ out_xyz, uint8_t* __restrict__ out_valid) {
-    static_assert(!TC || TcCfg<D>::eligible, "tcgen05 feature path needs D in {16, 32, 48, 64}");
-    static_assert(TC || D == 0, "the decoupled kernel covers D = 0 and the tcgen05 feature path");
-    using Smem = WSmem<D, TC>;
-    if (*status) return;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    if (threadIdx.x < WTQ) sm.tq_seq[threadIdx.x] = 0;
-    if (threadIdx.x < WNW) sm.wprog[threadIdx.x] = 0;
-    if (threadIdx.x == 0) {
-        sm.tq_next = 0;
-        if constexpr (TC)
-            for (int w = 0; w < WNW; ++w)
-                for (int b = 0; b < WNB; ++b) mbar_init(&sm.mma_bar[w][b], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    if constexpr (TC) {
-        if (warp == 0) tmem_alloc(&sm.tmem_base, TcCfg<D>::cols);
-        tc_fence_before();
-    }
-    __syncthreads();
-    if constexpr (TC) tc_fence_after();
-
-    // ------------------------------------------------------------ CTA tile sequence
-    // index i -> slot i % WTQ; claimed in order (atomicCAS on tq_next) by the first
-    // warp that needs it, once every warp of the CTA is past index i - WTQ
-    auto fill = [&](int i) {
-        const int sl = i % WTQ;
-        for (;;) {                                      // drift bound: the slot's old tile is done
-            int mn = 0x7fffffff;
-            for (int w = 0; w < WNW; ++w) mn = min(mn, *(volatile int*)&sm.wprog[w]);
-            if (mn > i - WTQ) break;
-            __nanosleep(64);
-        }
-        const uint32_t t = i == 0 ? blockIdx.x : (tile_sched ? gridDim.x + atomicAdd(tile_sched, 1u)
-                                                             : blockIdx.x + (uint32_t)i * gridDim.x);
-        uint32_t vi = 0, rs = 0, re = 0;
-        if (t < n_tiles) {
-            vi = uniform_tpv ? t / uniform_tpv : (uint32_t)find_view_by_tile(views, n_views, t);
-            rs = __ldg(&ranges[2 * t]);
-            re = __ldg(&ranges[2 * t + 1]);
-        }
-        sm.tq_tile[sl] = t; sm.tq_view[sl] = vi; sm.tq_rs[sl] = rs; sm.tq_re[sl] = re;
-        __threadfence_block();
-        *(volatile int*)&sm.tq_seq[sl] = i + 1;
-    };
-    // lane 0: make sure index i is claimed (blocking); returns the slot
-    auto get_slot = [&](int i) -> int {
-        int sl = i % WTQ;
-        if (lane == 0) {
-            for (;;) {
-                if (*(volatile int*)&sm.tq_seq[sl] == i + 1) break;
-                if (atomicCAS(&sm.tq_next, i, i + 1) == i) { fill(i); break; }
-                __nanosleep(32);
-            }
-            __threadfence_block();
-        }
-        __syncwarp();
-        return sl;
-    };
-    // non-blocking claim-ahead of index i (lane 0)
-    auto claim_ahead = [&](int i) {
-        if (lane == 0 && *(volatile int*)&sm.tq_seq[i % WTQ] != i + 1) {
-            int mn = 0x7fffffff;
-            for (int w = 0; w < WNW; ++w) mn = min(mn, *(volatile int*)&sm.wprog[w]);
-            if (mn > i - WTQ && atomicCAS(&sm.tq_next, i, i + 1) == i) fill(i);
-        }
-    };
-
-    // ------------------------------------------------------------ batch iterator
-    int it_i = -1;                 // sequence index of the iterator's tile
-    uint32_t it_rs = 0, it_re = 0, it_c0 = 0;
-    bool it_end = false, it_exhausted = false;
-    auto tile_enter = [&](int i) {
-        const int sl = get_slot(i);
-        const uint32_t t = sm.tq_tile[sl];
-        it_i = i;
-        it_end = t >= n_tiles;
-        it_rs = sm.tq_rs[sl];
-        it_re = sm.tq_re[sl];
-        it_c0 = it_rs;
-        it_exhausted = false;
-    };
-    // next batch of the CTA's tile sequence (an empty tile is one batch of 0 entries)
-    auto advance = [&]() -> WBatch {
-        WBatch b;
-        b.i = -1; b.c0 = 0; b.cnt = 0; b.first = b.last = false;
-        if (it_end) return b;
-        if (it_exhausted) {
-            tile_enter(it_i + 1);
-            claim_ahead(it_i + 1);
-            if (it_end) return b;
-        }
-        b.i = it_i;
-        b.c0 = it_c0;
-        b.cnt = (int)min(32u, it_re - it_c0);
-        b.first = it_c0 == it_rs;
-        b.last = it_c0 + 32u >= it_re;
-        it_c0 += 32u;
-        it_exhausted = b.last;
-        return b;
-    };
-    auto load_idx = [&](const WBatch& b, uint32_t& sl, uint32_t& gd) {
-        const bool ok = b.i >= 0 && (int)lane < b.cnt;
-        sl = ok ? __ldg(&sorted_rec[b.c0 + lane]) : 0u;
-        gd = (TC && ok) ? (sorted_gid ? __ldg(&sorted_gid[b.c0 + lane]) : __ldg(&rec[sl].gid)) : 0u;
-    };
-    // the cull needs (u, v, ea, eb | ec, o, e_cut); (r, g, b, z) of the entries that
-    // survive it are cp.async'd into the walk ring at compaction (same 128-B line: L1)
-    auto load_rec = [&](const WBatch& b, uint32_t sl, float4& q0, float4& q1) {
-        if (b.i >= 0 && (int)lane < b.cnt) {
-            const float4* s = reinterpret_cast<const float4*>(rec + sl);
-            q0 = __ldg(s);
-            q1 = __ldg(s + 1);
-        } else {
-            q0 = q1 = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    };
-
-    // ------------------------------------------------------------ per-warp render state
-    const uint32_t tq = warp & 3u, tgrp = warp >> 2;
-    const uint32_t tmem = TC ? sm.tmem_base : 0u;
-    const uint32_t tD = tmem + tgrp * (uint32_t)D;
-    const uint32_t tA = tmem + 2u * (uint32_t)D + tgrp * 32u;
-    const uint32_t my_lanes = (tq * 32u) << 16;
-    constexpr uint32_t IDESC = (1u << 4) | (1u << 16) | ((uint32_t)(D >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-    float4 (*walk)[3] = sm.walk[warp];
-    uint32_t Pc = 0;          // compacted positions (monotone across tiles; rounded to 16 at tile ends)
-    uint32_t Pw = 0;          // walked positions
-    uint32_t kb_ready = 0;    // k-steps whose B buffer is known free
-    uint32_t tile_acc = 0;
-    const gs_view* V = nullptr;
-    int W = 0, H = 0, sx = 0, sy = 0, px = 0, py = 0;
-    bool inside = false, done = true, warp_done = true;
-    float pxf = 0.f, pyf = 0.f, rx0 = 0.f, rx1 = 0.f, ry0 = 0.f, ry1 = 0.f;
-    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Dz = 0.f;
-    const uint64_t pol = l2_evict_last_policy();
-
-    auto blend_om = [&](float a, float om, const float4& c) -> float {
-        const float Tn = __fmul_rn(T, om);
-        const bool stop = done || Tn < P.t_min;
-        const float wgt = stop ? 0.0f : __fmul_rn(a, T);
-        fma2_acc(C0, C1, wgt, c.x, c.y);
-        fma2_acc(C2, Dz, wgt, c.z, c.w);
-        T = stop ? T : Tn;
-        done = stop;
-        return wgt;
-    };
-    // B tile of k-step k: element (row r, channel chunk n8) at n8*64 + (r&7)*8 + (r>>3)*8*D halves
-    auto brow = [&](uint32_t pos, int n8) -> __half* {
-        return &sm.btile[warp][(pos >> 4) % WNB][n8 * 64 + (int)(pos & 7u) * 8 + (int)((pos >> 3) & 1u) * 8 * D];
-    };
-    // one k-step on tcgen05: the A buffer (k & 1) holds the 16 walked weight pairs, the
-    // B buffer (k % WNB) the 16 feature rows (cp.async'd at compaction)
-    auto issue_kstep = [&](uint32_t k) {
-        if constexpr (TC) {
-            asm volatile("cp.async.wait_all;\n" ::: "memory");
-            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                tc_fence_after();
-                const __half* bt = &sm.btile[warp][k % WNB][0];
-                const uint64_t desc = (uint64_t)((smem_u32(bt) >> 4) & 0x3FFFu) |
-                                      ((uint64_t)(((16u * D) >> 4) & 0x3FFFu) << 16) |
-                                      ((uint64_t)((128u >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46);
-                const uint32_t a = tA + (k & 1u) * 16u;
-                tc_mma_f16(tD, a, desc, IDESC, tile_acc, tq);
-                tc_mma_f16(tD, a + 8u, desc, IDESC, 1u, tq);
-                tc_commit(&sm.mma_bar[warp][k % WNB]);
-            }
-            __syncwarp();
-            tile_acc = 1;
-            // the next k-step's A buffer was last read by k-step k - 1
-            if (k >= 1) mbar_wait(&sm.mma_bar[warp][(k - 1) % WNB], ((k - 1) / WNB) & 1u);
-        }
-    };
-    // weights of walked pair (p, p+1): fp16 hi + lo into A buffer (k & 1), column (p % 16) / 2
-    auto store_pair = [&](uint32_t p, float w1, float w2) {
-        if constexpr (TC) {
-            const __half2 h = __floats2half2_rn(w1, w2);
-            const float2 hf = __half22float2(h);
-            const float2 r = sub2_rn(w1, w2, hf.x, hf.y);
-            const __half2 l = __floats2half2_rn(r.x, r.y);
-            const uint32_t col = tA + my_lanes + ((p >> 4) & 1u) * 16u + ((p & 15u) >> 1);
-            tmem_st1(col, *reinterpret_cast<const uint32_t*>(&h));
-            tmem_st1(col + 8u, *reinterpret_cast<const uint32_t*>(&l));
-        }
-    };
-    // zero walk-ring entry / B row at position pos (padding)
-    auto null_entry = [&](uint32_t pos) {
-        if (lane < 3) walk[pos % WRING][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if constexpr (TC)
-            if (lane < (uint32_t)(D / 8)) *reinterpret_cast<uint4*>(brow(pos, (int)lane)) = make_uint4(0u, 0u, 0u, 0u);
-    };
-    auto wait_bfree = [&](uint32_t last_pos) {
-        if constexpr (TC) {
-            const uint32_t kl = last_pos >> 4;
-            for (; kb_ready <= kl; ++kb_ready)
-                if (kb_ready >= WNB) mbar_wait(&sm.mma_bar[warp][kb_ready % WNB], ((kb_ready / WNB) - 1u) & 1u);
-        }
-    };
-    auto walk_pairs = [&](uint32_t upto) {
-#pragma unroll 1
-        for (; Pw + 2u <= upto; Pw += 2u) {
-            const float4* r1 = walk[Pw % WRING];
-            const float4* r2 = walk[(Pw + 1u) % WRING];
-            const float a1 = entry_alpha(r1[0], r1[1], pxf, pyf, P);
-            const float a2 = entry_alpha(r2[0], r2[1], pxf, pyf, P);
-            const float2 om = sub2_rn(1.0f, 1.0f, a1, a2);
-            const float w1 = blend_om(a1, om.x, r1[2]);
-            const float w2 = blend_om(a2, om.y, r2[2]);
-            store_pair(Pw, w1, w2);
-            if (((Pw + 2u) & 15u) == 0u) issue_kstep(Pw >> 4);
-        }
-    };
-
-    // ------------------------------------------------------------ main loop
-    if (lane == 0) claim_ahead(0);
-    tile_enter(0);
-    if (lane == 0) claim_ahead(1);
-    // pipeline: B2 indices in flight, B1 records in flight, B0 processed
-    WBatch b1 = advance();
-    uint32_t sl1, gd1;
-    load_idx(b1, sl1, gd1);
-    WBatch b2 = advance();
-    uint32_t sl2, gd2;
-    load_idx(b2, sl2, gd2);
-    float4 q0, q1;
-    load_rec(b1, sl1, q0, q1);
-    for (;;) {
-        const WBatch b0 = b1;
-        const float4 c0q = q0, c1q = q1;
-        const uint32_t gd0 = gd1, sl0 = sl1;
-        if (b0.i < 0) break;
-        b1 = b2; sl1 = sl2; gd1 = gd2;
-        load_rec(b1, sl1, q0, q1);
-        b2 = advance();
-        load_idx(b2, sl2, gd2);
-
-        if (b0.first) {
-            const int sl = b0.i % WTQ;
-            if (lane == 0) *(volatile int*)&sm.wprog[warp] = b0.i;
-            const uint32_t t = sm.tq_tile[sl];
-            V = &views[sm.tq_view[sl]];
-            W = V->width;
-            H = V->height;
-            const int TX = (W + GS_TILE - 1) / GS_TILE;
-            const uint32_t lt = t - V->tile_offset;
-            const int tx = (int)(lt % (uint32_t)TX), ty = (int)(lt / (uint32_t)TX);
-            sx = tx * 16 + (int)(warp & 1u) * 8;
-            sy = ty * 16 + (int)(warp >> 1) * 4;
-            px = sx + (int)(lane & 7u);
-            py = sy + (int)(lane >> 3);
-            inside = px < W && py < H;
-            pxf = (float)px; pyf = (float)py;
-            rx0 = (float)sx; rx1 = (float)(sx + 7); ry0 = (float)sy; ry1 = (float)(sy + 3);
-            T = 1.0f; C0 = C1 = C2 = Dz = 0.f;
-            done = !inside;
-            warp_done = __all_sync(0xffffffffu, done);
-            tile_acc = 0;
-        }
-        if (!warp_done && b0.cnt > 0) {
-            const bool hit = (int)lane < b0.cnt &&
-                             ellipse_hits_rect(c0q.x, c0q.y, c0q.z, c0q.w, c1q.x, c1q.z, rx0, rx1, ry0, ry1);
-            const uint32_t msk = __ballot_sync(0xffffffffu, hit);
-            const uint32_t n = __popc(msk);
-            if (n) {
-                const uint32_t pos = Pc + __popc(msk & ((1u << lane) - 1u));
-                wait_bfree(Pc + n - 1u);
-                if (hit) {
-                    float4* dst = walk[pos % WRING];
-                    dst[0] = c0q;
-                    dst[1] = c1q;
-                    cp_async16_ca(&dst[2], reinterpret_cast<const float4*>(rec + sl0) + 2);
-                }
-                asm volatile("cp.async.commit_group;\n" ::: "memory");
-                if constexpr (TC) {
-                    if (hit) {
-                        const uint4* fs = reinterpret_cast<const uint4*>(feat_h + (int64_t)gd0 * D);
-#pragma unroll
-                        for (int e = 0; e < D / 8; ++e) cp_async16(brow(pos, e), fs + e, pol);
-                    }
-                    asm volatile("cp.async.commit_group;\n" ::: "memory");
-                    // (r, g, b, z) must land before the walk; the feature rows may still be in
-                    // flight (waited for at the k-step)
-                    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-                } else {
-                    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-                }
-                Pc += n;
-                __syncwarp();
-                walk_pairs(Pc);
-                warp_done = __all_sync(0xffffffffu, done);
-            }
-        }
-        if (b0.last) {
-            // ------------------------------------------------ tile end: drain the walk
-            if (Pc & 1u) {                          // odd tail: pair it with a null entry
-                wait_bfree(Pc);
-                null_entry(Pc);
-                ++Pc;
-                __syncwarp();
-            }
-            walk_pairs(Pc);
-            if constexpr (TC) {
-                if (Pc & 15u) {                     // partial k-step: zero weights / rows, issue
-                    const uint32_t end = (Pc + 15u) & ~15u;
-                    wait_bfree(end - 1u);
-                    for (uint32_t p = Pc; p < end; p += 2u) store_pair(p, 0.f, 0.f);
-                    for (uint32_t r = Pc + lane / (uint32_t)(D / 8); r < end; r += 32u / (D / 8))
-                        *reinterpret_cast<uint4*>(brow(r, (int)(lane % (uint32_t)(D / 8)))) = make_uint4(0u, 0u, 0u, 0u);
-                    __syncwarp();
-                    issue_kstep(Pc >> 4);
-                    Pc = Pw = end;
-                }
-            }
-            // ------------------------------------------------ outputs
-            const int64_t HW = (int64_t)W * H;
-            const int64_t po = V->pix_offset;
-            if (inside) {
-                const int64_t loc = (int64_t)py * W + px;
-                __stcs(&out_rgb[3 * po + loc], C0);
-                __stcs(&out_rgb[3 * po + HW + loc], C1);
-                __stcs(&out_rgb[3 * po + 2 * HW + loc], C2);
-                __stcs(&out_depth[po + loc], Dz);
-                __stcs(&out_alpha[po + loc], 1.0f - T);
-                if (out_xyz) {
-                    float X, Y, Z;
-                    uint8_t ok;
-                    bp_pixel(*V, Dz, 1.0f - T, a_min, px, py, X, Y, Z, ok);
-                    __stcs(&out_xyz[3 * po + loc], X);
-                    __stcs(&out_xyz[3 * po + HW + loc], Y);
-                    __stcs(&out_xyz[3 * po + 2 * HW + loc], Z);
-                    out_valid[po + loc] = ok;
-                }
-            }
-            if constexpr (TC) {
-                // 16 channels at a time (register budget): tcgen05.ld, wait, streaming stores
-                if (tile_acc) {
-                    const uint32_t kl = (Pc >> 4) - 1u;
-                    mbar_wait(&sm.mma_bar[warp][kl % WNB], (kl / WNB) & 1u);
-                    tc_fence_after();
-                }
-                float* q = out_feat + (int64_t)D * po + (int64_t)py * W + px;
-#pragma unroll 1
-                for (int c = 0; c < D; c += 16) {
-                    float f[16];
-                    if (tile_acc) {
-                        tmem_ld16(tD + my_lanes + (uint32_t)c, f);
-                        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 16; ++k) f[k] = 0.f;
-                    }
-                    if (inside) {
-#pragma unroll
-                        for (int k = 0; k < 16; ++k) {
-                            __stcs(q, f[k]);
-                            q += HW;
-                        }
-                    }
-                }
-            }
-            warp_done = true;
-        }
-    }
-    if (lane == 0) *(volatile int*)&sm.wprog[warp] = 0x7fffffff;
-    if constexpr (TC) {
-        // every MMA was waited for at its tile's epilogue; free TMEM once all warps are done
-        tc_fence_before();
-        __syncthreads();
-        if (warp == 0) {
-            tc_fence_after();
-            tmem_dealloc(tmem, TcCfg<D>::cols);
-        }
-    }
-}
-
-template <int D, bool TC>
-gs_status launch_warp(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins, const gs_view* views_host,
-                      const gs_view* views_dev, int n_views, int64_t T, const gs_params* P, gs_images* out,
-                      cudaStream_t s, float a_min, float* xyz, uint8_t* valid) {
-    const int smem = (int)sizeof(WSmem<D, TC>);
-    cudaFuncSetAttribute(rasterize_warp_kernel<D, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(rasterize_warp_kernel<D, TC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    static std::atomic<int> bps_cache[GS_MAX_DEVICES];
-    const int cur_dev = current_device();
-    const bool cacheable = cur_dev >= 0 && cur_dev < GS_MAX_DEVICES;
-    int blocks_per_sm = cacheable ? bps_cache[cur_dev].load(std::memory_order_relaxed) : 0;
-    if (blocks_per_sm == 0) {
-        int dev = 0, smem_sm = 0, regs_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-        cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
-        cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, rasterize_warp_kernel<D, TC>);
-        const int by_smem = smem_sm / (smem + 1024);
-        const int by_regs = regs_sm / (std::max(fa.numRegs, 1) * WNW * 32);
-        const int by_tmem = TC ? 512 / (int)TcCfg<D>::cols : 64;
-        blocks_per_sm = std::max(1, std::min(std::min(by_smem, by_regs), std::min(by_tmem, 8)));
-        if (const char* o = getenv("GS_RASTER_CTAS_PER_SM")) blocks_per_sm = atoi(o);
-        if (getenv("GS_DEBUG"))
-            fprintf(stderr, "[gs] rasterize_warp<%d,%d>: smem %d B, %d regs, occupancy %d CTAs/SM\n", D, (int)TC, smem,
-                    fa.numRegs, blocks_per_sm);
-        if (cacheable) bps_cache[cur_dev].store(blocks_per_sm, std::memory_order_relaxed);
-    }
-    const int64_t grid = std::min<int64_t>(T, (int64_t)num_sms() * blocks_per_sm);
-    if (grid <= 0) return GS_OK;
-    // one tile count shared by every view: view = tile / tiles-per-view (no search)
-    uint32_t tpv = (uint32_t)(tiles_x(views_host[0]) * tiles_y(views_host[0]));
-    for (int i = 1; i < n_views && tpv; ++i)
-        if ((uint32_t)(tiles_x(views_host[i]) * tiles_y(views_host[i])) != tpv) tpv = 0;
-    if (bins->tile_sched) cudaMemsetAsync(bins->tile_sched, 0, sizeof(uint32_t), s);
-    rasterize_warp_kernel<D, TC><<<(unsigned)grid, WNW * 32, smem, s>>>(
-        views_dev, n_views, tpv, proj->rec, bins->sorted_rec, bins->sorted_gid, bins->ranges, (uint32_t)T,
-        bins->tile_sched, reinterpret_cast<const __half*>(scene->feat_h), *P, out->rgb, out->depth, out->alpha,
-        out->feat, proj->status, a_min, xyz, valid);
-    return check_launch("rasterize_warp_kernel");
-}
-
 // ---------------------------------------------------------------- N4 backward
 // Feature-field backward of Eq. 2 with the geometry frozen:
 // dL/df_g += sum over pixels of w_g(px) * dL/dF(px).  One CTA per tile (8 warps
@@ -1493,17 +1021,26 @@ gs_status launch_backward(const gs_projected* proj, const gs_bins* bins, const g
 // Same tile / chunk / warp structure as the feature backward; the 10 per-pixel
 // terms of each walked entry are warp-reduced, summed over the warps in shared
 // memory and flushed with one global atomic per (entry, field) per chunk.
+// DF > 0 (gs_joint_backward, Eq. 1 with Eq. 2's feature term through the geometry):
+// the rendered feature vector F = sum_k w_k f_k enters like a colour channel with
+// the pixel's upstream gradient gF: dL/dalpha_k += T_k (gF . f_k) - (gF . F -
+// sum_{j<=k} w_j gF . f_j) / (1 - alpha_k)  (the scalar gF . f_k per walked entry
+// and pixel, fp32 from the scene's fp32 feature rows staged per chunk).
 constexpr int NGRAD = 10;
 
+template <int DF>
 __global__ void __launch_bounds__(256)
 radiance_backward_kernel(const gs_view* __restrict__ views, int n_views, const gs_record* __restrict__ rec,
                          const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ ranges, gs_params P,
                          const float* __restrict__ img_rgb, const float* __restrict__ img_depth,
                          const float* __restrict__ img_alpha, const float* __restrict__ g_rgb,
                          const float* __restrict__ g_depth, const float* __restrict__ g_alpha,
-                         float* __restrict__ grec, const uint32_t* __restrict__ status) {
+                         float* __restrict__ grec, const uint32_t* __restrict__ status,
+                         const float* __restrict__ feat, const float* __restrict__ img_feat,
+                         const float* __restrict__ g_feat) {
     if (*status) return;
     __shared__ float4 srec[BW_CHUNK + 1][3];
+    __shared__ __align__(16) float sfeat[DF > 0 ? BW_CHUNK : 1][DF > 0 ? DF : 4];
     __shared__ uint32_t sslot[BW_CHUNK];
     __shared__ float acc[BW_CHUNK][NGRAD + 1];
     __shared__ int ent[8][2 * 32 + 2];
@@ -1530,6 +1067,14 @@ radiance_backward_kernel(const gs_view* __restrict__ views, int n_views, const g
         gD = __ldg(&g_depth[po + loc]);
         gA = __ldg(&g_alpha[po + loc]);
     }
+    // feature term: this pixel's upstream gradient and gF . F of the forward's map
+    float gF[DF > 0 ? DF : 1];
+    float SF = 0.f, Sacc = 0.f;
+#pragma unroll
+    for (int c = 0; c < DF; ++c) {
+        gF[c] = inside ? __ldg(&g_feat[(int64_t)DF * po + (int64_t)c * HW + loc]) : 0.f;
+        if (inside) SF = fmaf(gF[c], __ldg(&img_feat[(int64_t)DF * po + (int64_t)c * HW + loc]), SF);
+    }
     for (int i = tid; i < BW_CHUNK * (NGRAD + 1); i += 256) (&acc[0][0])[i] = 0.f;
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Dz = 0.f;
     bool done = !inside;
@@ -1542,6 +1087,13 @@ radiance_backward_kernel(const gs_view* __restrict__ views, int n_views, const g
             const uint32_t slot = __ldg(&sorted_rec[c0 + i / 3]);
             srec[i / 3][i % 3] = __ldg(reinterpret_cast<const float4*>(rec + slot) + (i % 3));
             if (i % 3 == 0) sslot[i / 3] = slot;
+        }
+        if constexpr (DF > 0) {
+            for (int i = tid; i < cnt * (DF / 4); i += 256) {
+                const int e = i / (DF / 4), q = i % (DF / 4);
+                const uint32_t g = __ldg(&rec[__ldg(&sorted_rec[c0 + e])].gid);
+                reinterpret_cast<float4*>(&sfeat[e][0])[q] = __ldg(reinterpret_cast<const float4*>(feat + (int64_t)g * DF) + q);
+            }
         }
         __syncthreads();
         if (!warp_done) {
@@ -1577,12 +1129,27 @@ radiance_backward_kernel(const gs_view* __restrict__ views, int n_views, const g
 #pragma unroll
                 for (int q = 0; q < 16; ++q) g[q] = 0.f;
                 const bool blended = wgt > 0.f;
+                float dot = 0.f;                       // gF . f_k (feature term)
+                if constexpr (DF > 0) {
+                    if (blended) {
+#pragma unroll
+                        for (int c = 0; c < DF; c += 4) {
+                            const float4 f4 = *reinterpret_cast<const float4*>(&sfeat[k][c]);
+                            dot = fmaf(gF[c], f4.x, dot); dot = fmaf(gF[c + 1], f4.y, dot);
+                            dot = fmaf(gF[c + 2], f4.z, dot); dot = fmaf(gF[c + 3], f4.w, dot);
+                        }
+                    }
+                }
                 if (blended) {
                     C0 = fmaf(wgt, c4.x, C0); C1 = fmaf(wgt, c4.y, C1); C2 = fmaf(wgt, c4.z, C2); Dz = fmaf(wgt, c4.w, Dz);
                     const float iom = __frcp_rn(1.0f - alpha);
-                    const float dLda = gC[0] * (T * c4.x - (Cf[0] - C0) * iom) + gC[1] * (T * c4.y - (Cf[1] - C1) * iom) +
-                                       gC[2] * (T * c4.z - (Cf[2] - C2) * iom) + gD * (T * c4.w - (Df - Dz) * iom) +
-                                       gA * (Tf * iom);
+                    float dLda = gC[0] * (T * c4.x - (Cf[0] - C0) * iom) + gC[1] * (T * c4.y - (Cf[1] - C1) * iom) +
+                                 gC[2] * (T * c4.z - (Cf[2] - C2) * iom) + gD * (T * c4.w - (Df - Dz) * iom) +
+                                 gA * (Tf * iom);
+                    if constexpr (DF > 0) {
+                        Sacc = fmaf(wgt, dot, Sacc);
+                        dLda += T * dot - (SF - Sacc) * iom;
+                    }
                     g[6] = wgt * gC[0]; g[7] = wgt * gC[1]; g[8] = wgt * gC[2]; g[9] = wgt * gD;
                     if (araw <= P.alpha_max) {
                         g[5] = dLda * e2p;
@@ -1652,6 +1219,47 @@ __global__ void l1_grad_kernel(const float* __restrict__ F, const float* __restr
     if ((threadIdx.x & 31) == 0) atomicAdd(loss, part);
 }
 
+// Eq. 3's L1 term against the appearance-varied rendering (reading Q38): plane p of
+// hw pixels, I^a = a[p] I^r + b[p]; grad = scale sign(I^a - I) a[p] (written), and
+// per plane dL/da = scale sum sign * I^r, dL/db = scale sum sign (accumulated).
+__global__ void appearance_l1_kernel(const float* __restrict__ r, const float* __restrict__ t, int64_t hw,
+                                     const float* __restrict__ a, const float* __restrict__ b, float scale,
+                                     float* __restrict__ g, float* __restrict__ ga, float* __restrict__ gb,
+                                     double* __restrict__ loss) {
+    const int p = blockIdx.y;
+    const float ap = a[p], bp = b[p];
+    const int64_t base = (int64_t)p * hw;
+    float sa = 0.f, sb = 0.f;
+    double ls = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x) {
+        const float x = r[base + i];
+        const float d = fmaf(ap, x, bp) - t[base + i];
+        const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+        g[base + i] = scale * sg * ap;
+        sa = fmaf(sg, x, sa);
+        sb += sg;
+        ls += (double)fabsf(d);
+    }
+    for (int o = 16; o; o >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        ls += __shfl_xor_sync(0xffffffffu, ls, o);
+    }
+    __shared__ float s_a[32], s_b[32];
+    __shared__ double s_l[32];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { s_a[w] = sa; s_b[w] = sb; s_l[w] = ls; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float ta = 0.f, tb = 0.f;
+        double tl = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { ta += s_a[k]; tb += s_b[k]; tl += s_l[k]; }
+        atomicAdd(&ga[p], scale * ta);
+        atomicAdd(&gb[p], scale * tb);
+        atomicAdd(loss, (double)scale * tl);
+    }
+}
+
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                             float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps, float bc1,
                             float bc2, __half* __restrict__ ph) {
@@ -1702,24 +1310,6 @@ static gs_status rasterize_impl(const gs_scene* scene, const gs_projected* proj,
     cudaStream_t s = (cudaStream_t)stream;
     const bool tc = scene->feat_h != nullptr;
     GS_REQUIRE(!tc || ((uintptr_t)scene->feat_h & 15) == 0, GS_INVALID_ARG, "feat_h must be 16-byte aligned");
-    // the decoupled-warp kernel (experimental, GS_RASTER_WARP=1) for the configurations
-    // without N1 contributions (D = 0 or the tcgen05 feature path)
-    static const bool use_warp = getenv("GS_RASTER_WARP") != nullptr;
-    if (!proj->contrib && use_warp) {
-#define GS_WCASE(d)                                                                                                    \
-    case d:                                                                                                            \
-        if (tc) return launch_warp<d, true>(scene, proj, bins, views_host, views_dev, n_views, T, params, out, s, a_min, \
-                                            xyz, valid);                                                               \
-        break;
-        switch (scene->feat_dim) {
-            case 0:
-                return launch_warp<0, false>(scene, proj, bins, views_host, views_dev, n_views, T, params, out, s, a_min,
-                                             xyz, valid);
-            GS_WCASE(16) GS_WCASE(32) GS_WCASE(48) GS_WCASE(64)
-            default: break;
-        }
-#undef GS_WCASE
-    }
     switch (scene->feat_dim) {
 #define GS_CASE(d) \
     case d:                                                                                       \
@@ -1837,6 +1427,22 @@ extern "C" gs_status gs_feature_l1_grad(const float* rendered, const float* targ
     return check_launch("l1_grad_kernel");
 }
 
+extern "C" gs_status gs_appearance_l1_grad(const float* rendered, const float* target, int32_t n_planes,
+                                           int64_t plane_pixels, const float* a, const float* b, float scale,
+                                           float* grad_image, float* grad_a, float* grad_b, double* loss,
+                                           void* stream) {
+    GS_REQUIRE(n_planes >= 0 && n_planes <= 65535 && plane_pixels >= 0, GS_INVALID_ARG,
+               "gs_appearance_l1_grad: bad sizes");
+    if (n_planes == 0 || plane_pixels == 0) return GS_OK;
+    GS_REQUIRE(rendered && target && a && b && grad_image && grad_a && grad_b && loss, GS_INVALID_ARG,
+               "gs_appearance_l1_grad: NULL pointer");
+    const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((plane_pixels + 1023) / 1024,
+                                                              (int64_t)num_sms() * 8 / n_planes + 1));
+    appearance_l1_kernel<<<dim3((unsigned)bx, (unsigned)n_planes), 256, 0, (cudaStream_t)stream>>>(
+        rendered, target, plane_pixels, a, b, scale, grad_image, grad_a, grad_b, loss);
+    return check_launch("appearance_l1_kernel");
+}
+
 extern "C" gs_status gs_feature_sgd(float* feat, const float* grad_feat, int64_t n, float lr, void* feat_h,
                                     void* stream) {
     GS_REQUIRE(feat && grad_feat && n >= 0, GS_INVALID_ARG, "gs_feature_sgd: bad args");
@@ -1871,10 +1477,45 @@ extern "C" gs_status gs_radiance_backward(const gs_projected* proj, const gs_bin
                    grad_out->alpha && grad_rec,
                GS_INVALID_ARG, "gs_radiance_backward: NULL pointer");
     if (T <= 0) return GS_OK;
-    radiance_backward_kernel<<<(unsigned)T, 256, 0, (cudaStream_t)stream>>>(
+    radiance_backward_kernel<0><<<(unsigned)T, 256, 0, (cudaStream_t)stream>>>(
         views_dev, n_views, proj->rec, bins->sorted_rec, bins->ranges, *params, fwd->rgb, fwd->depth, fwd->alpha,
-        grad_out->rgb, grad_out->depth, grad_out->alpha, grad_rec, proj->status);
+        grad_out->rgb, grad_out->depth, grad_out->alpha, grad_rec, proj->status, nullptr, nullptr, nullptr);
     return check_launch("radiance_backward_kernel");
+}
+
+extern "C" gs_status gs_joint_backward(const gs_scene* scene, const gs_projected* proj, const gs_bins* bins,
+                                       const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
+                                       const gs_params* params, const gs_images* fwd, const gs_images* grad_out,
+                                       float* grad_rec, void* stream) {
+    if (grad_out == nullptr || grad_out->feat == nullptr || scene == nullptr || scene->feat_dim == 0)
+        return gs_radiance_backward(proj, bins, views_host, views_dev, n_views, params, fwd, grad_out, grad_rec,
+                                    stream);
+    gs_status st = validate_scene(scene, false);
+    if (st != GS_OK) return st;
+    int64_t total_pixels = 0, T = 0;
+    st = validate_views(views_host, views_dev, n_views, &total_pixels, &T);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(params && proj && proj->rec && proj->status && bins && bins->ranges && bins->sorted_rec && fwd &&
+                   fwd->rgb && fwd->depth && fwd->alpha && fwd->feat && grad_out->rgb && grad_out->depth &&
+                   grad_out->alpha && grad_rec && scene->feat,
+               GS_INVALID_ARG, "gs_joint_backward: NULL pointer");
+    GS_REQUIRE(((uintptr_t)scene->feat & 15) == 0, GS_INVALID_ARG, "gs_joint_backward: features must be 16-byte aligned");
+    if (T <= 0) return GS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+#define GS_JCASE(d)                                                                                                  \
+    case d:                                                                                                          \
+        radiance_backward_kernel<d><<<(unsigned)T, 256, 0, s>>>(                                                     \
+            views_dev, n_views, proj->rec, bins->sorted_rec, bins->ranges, *params, fwd->rgb, fwd->depth, fwd->alpha, \
+            grad_out->rgb, grad_out->depth, grad_out->alpha, grad_rec, proj->status, scene->feat, fwd->feat,          \
+            grad_out->feat);                                                                                         \
+        return check_launch("radiance_backward_kernel");
+    switch (scene->feat_dim) {
+        GS_JCASE(8) GS_JCASE(16) GS_JCASE(24) GS_JCASE(32) GS_JCASE(48) GS_JCASE(64)
+        default:
+            gs::set_error("gs_joint_backward: feat_dim = %d (need 8, 16, 24, 32, 48 or 64)", scene->feat_dim);
+            return GS_UNSUPPORTED;
+    }
+#undef GS_JCASE
 }
 
 #ifdef GS_RASTER_STATS

@@ -75,7 +75,7 @@ EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_lay
            "gs_feature_l1_grad", "gs_feature_sgd", "gs_dssim_grad", "gs_dssim_workspace_bytes",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_rasterize_backproject", "gs_backproject", "gs_visibility_score",
-           "gs_visibility_workspace_bytes", "gs_probe_alpha", "gs_sanitize_scene"]
+           "gs_visibility_workspace_bytes", "gs_probe_alpha", "gs_sanitize_scene", "gs_joint_backward", "gs_appearance_l1_grad"]
 
 _lib = None
 
@@ -285,6 +285,13 @@ class Images:
         s.rgb, s.depth, s.alpha, s.feat = _ptr(self.rgb), _ptr(self.depth), _ptr(self.alpha), _ptr(self.feat)
         self.struct = s
         self.feat_dim = feat_dim
+
+    def set_feat(self, t: Optional[torch.Tensor], feat_dim: int):
+        """Attach a caller tensor as the feature planes (e.g. an upstream gradient dL/dF)."""
+        assert t is None or (t.dtype == torch.float32 and t.is_contiguous())
+        self.feat, self.feat_dim = t, feat_dim
+        self.struct.feat = _ptr(t)
+        return self
 
     def view_planes(self, vb: ViewBatch, i: int):
         v = vb.views[i]
@@ -550,6 +557,26 @@ def gs_radiance_backward(proj: "Projected", bins: "Bins", views, params: gs_para
                                       ctypes.c_int32(views.n), ctypes.byref(params), ctypes.byref(fwd.struct),
                                       ctypes.byref(grad_out.struct), _ptr(grad_rec), _stream(stream)),
            "gs_radiance_backward")
+
+
+def gs_appearance_l1_grad(rendered: torch.Tensor, target: torch.Tensor, n_planes: int, plane_pixels: int,
+                          a: torch.Tensor, b: torch.Tensor, scale: float, grad_image: torch.Tensor,
+                          grad_a: torch.Tensor, grad_b: torch.Tensor, loss: torch.Tensor, stream=None):
+    """Eq. 3's L1 against I^a = a I^r + b per plane (reading Q38); see include/gs.h."""
+    _check(lib().gs_appearance_l1_grad(_ptr(rendered), _ptr(target), ctypes.c_int32(n_planes),
+                                       ctypes.c_int64(plane_pixels), _ptr(a), _ptr(b), ctypes.c_float(scale),
+                                       _ptr(grad_image), _ptr(grad_a), _ptr(grad_b), _ptr(loss), _stream(stream)),
+           "gs_appearance_l1_grad")
+
+
+def gs_joint_backward(scene: "DeviceScene", proj: "Projected", bins: "Bins", views, params: gs_params,
+                      fwd: "Images", grad_out: "Images", grad_rec: torch.Tensor, stream=None):
+    """Eq. 1's joint record gradient: gs_radiance_backward + the feature term
+    (grad_out.feat = dL/dF) through the blend weights; accumulated into grad_rec."""
+    _check(lib().gs_joint_backward(ctypes.byref(scene.struct), ctypes.byref(proj.struct), ctypes.byref(bins.struct),
+                                   views.host, views.dev_ptr, ctypes.c_int32(views.n), ctypes.byref(params),
+                                   ctypes.byref(fwd.struct), ctypes.byref(grad_out.struct), _ptr(grad_rec),
+                                   _stream(stream)), "gs_joint_backward")
 
 
 def gs_mean_backward(scene: "DeviceScene", proj: "Projected", views, params: gs_params, grad_rec: torch.Tensor,

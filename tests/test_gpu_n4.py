@@ -423,3 +423,61 @@ def test_training_keeps_every_gaussian_renderable(G):
     assert s.min() > 0 and np.isfinite(s).all()
     assert int(t.sanitized.item()) > 0
     assert t.r.status() == 0
+
+
+def _joint_case(G, orc, sc, views, rng):
+    """gs_joint_backward (Eq. 1 with Eq. 2's feature term through the blend weights)
+    against oracle.radiance_backward(..., feat, gF): record gradients within 5e-3 of
+    the largest |gradient| per field (the forward feature map the kernel reads for
+    gF . F is fp16-feature-rounded, within the 1e-3 image tolerance)."""
+    ds = G.DeviceScene(sc)
+    r = G.Renderer(ds, views, backproject=False)
+    r.render()
+    torch.cuda.synchronize()
+    D = sc.feat_dim
+    gout = G.Images(r.vb.total_pixels, 0)
+    ups = []
+    for t in (gout.rgb, gout.depth, gout.alpha):
+        a = rng.standard_normal(t.numel()).astype(np.float32)
+        t.copy_(torch.from_numpy(a))
+        ups.append(a)
+    gfe = rng.standard_normal(D * r.vb.total_pixels).astype(np.float32)
+    gout.set_feat(torch.from_numpy(gfe).cuda(), D)
+    cap = r.proj.rec_capacity
+    grec = torch.zeros(len(views) * cap * 10, dtype=torch.float32, device="cuda")
+    G.gs_joint_backward(ds, r.proj, r.bins, r.vb, r.params, r.images, gout, grec)
+    torch.cuda.synchronize()
+    grec = grec.view(len(views), cap, 10).cpu().numpy().astype(np.float64)
+    for i, v in enumerate(views):
+        o = orc.render(sc, v, binning="tight")
+        po, hw = r.vb.pix_offset(i), v.width * v.height
+        gC = ups[0][3 * po:3 * po + 3 * hw].reshape(3, v.height, v.width)
+        gD = ups[1][po:po + hw].reshape(v.height, v.width)
+        gA = ups[2][po:po + hw].reshape(v.height, v.width)
+        gF = gfe[D * po:D * po + D * hw].reshape(D, v.height, v.width)
+        want, _ = orc.radiance_backward(v, o["rec"], o["keys"], gC, gD, gA, feat=sc.feat, gF=gF)
+        want0, _ = orc.radiance_backward(v, o["rec"], o["keys"], gC, gD, gA)
+        assert np.abs(want - want0)[:, :6].max() > 1e-3 * np.abs(want).max()   # the feature term matters
+        n = min(int(r.proj.n_rec[i].item()), cap)
+        recs = r.proj.records()[i * cap:i * cap + n].cpu().numpy()
+        gid = recs[:, 12].view(np.uint32)
+        got = grec[i, :n][np.argsort(gid)]
+        flagged = int((o["flags"] != 0).sum())
+        for f, name in enumerate(G.GRAD_FIELDS):
+            scale = float(np.abs(want[:, f]).max()) if len(want) else 0.0
+            bad = np.abs(got[:, f] - want[:, f]) > 5e-3 * scale + 1e-5
+            assert bad.sum() <= (max(2, 0.02 * len(want)) if flagged else 0), (name, bad.sum(), flagged)
+
+
+@pytest.mark.parametrize("D,seed", [(8, 0), (16, 1), (32, 2), (64, 3)])
+def test_joint_backward_tiny_ragged(G, orc, D, seed):
+    rng = np.random.default_rng(700 + seed)
+    sc = random_tiny_scene(rng, int(rng.integers(60, 250)), feat_dim=D, sh_degree=seed % 4)
+    W, H = int(rng.integers(9, 90)), int(rng.integers(7, 70))
+    v = synth.make_view(np.eye(3), np.zeros(3), 40.0, 40.0, W / 2 - 0.5, H / 2 - 0.5, W, H)
+    _joint_case(G, orc, sc, [v], rng)
+
+
+def test_joint_backward_c4_views(G, orc):
+    sc, vs = synth.make_config("C4", scale=0.01)
+    _joint_case(G, orc, sc, vs[:2], np.random.default_rng(12))
