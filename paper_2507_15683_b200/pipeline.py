@@ -332,21 +332,25 @@ def equal_size_runs(views, max_views: Optional[int] = None) -> list:
 
 
 class SceneTrainer:
-    """N4: a joint training step of Eq. 1, L = alpha L_f + beta L_rgb, with Eq. 2's L1
-    feature term and Eq. 3's L_rgb = (1 - lam) L1 + lam L_D-SSIM (reading Q37;
-    lam = 0.2 as in [3DGS], the paper gives no value; lam = 0 is L1 only).  Per step:
-    render the batch; gs_feature_l1_grad on the RGB planes, then gs_dssim_grad adding
-    the D-SSIM gradient per run of equal-size views; gs_radiance_backward to
-    the records; gs_mean_backward + gs_param_backward to every Gaussian parameter;
-    for a feature scene also gs_feature_l1_grad + gs_feature_backward on the
-    features (geometry frozen for L_f); then one gs_feature_sgd or gs_adam step per
-    parameter plane and the block bounds refreshed.  No densification / pruning."""
+    """N4: a joint training step of Eq. 1, L = alpha L_f + beta L_rgb, with
+    Eq. 2's L1 feature term and Eq. 3's L_rgb = (1 - lam) L1(I, I^a) + lam
+    L_D-SSIM(I, I^r) (reading Q37: lam = 0.2 as in [3DGS]; reading Q38:
+    I^a = a I^r + b per view and channel, trained jointly; appearance=False uses I^r).
+    Per step: render the batch; gs_appearance_l1_grad (or gs_feature_l1_grad) on the
+    RGB planes, gs_dssim_grad adding the D-SSIM gradient per run of equal-size views;
+    for a feature scene gs_feature_l1_grad on the feature planes; gs_joint_backward to
+    the records (the RGB terms and the feature term through the blend weights: the
+    geometry receives L_f's gradient too); gs_mean_backward + gs_param_backward to
+    every Gaussian parameter; gs_feature_backward to the features; then one
+    gs_feature_sgd or gs_adam step per parameter plane (and the appearance
+    parameters), gs_sanitize_scene, and the block bounds refreshed.  No
+    densification / pruning."""
 
     PLANES = ("pos", "scale", "quat", "opacity", "sh")
 
     def __init__(self, scene: G.DeviceScene, views: Sequence, target_rgb: torch.Tensor,
                  target_feat: Optional[torch.Tensor] = None, lr: Optional[dict] = None, alpha: float = 1.0,
-                 beta: float = 1.0, optimizer: str = "sgd", lam: float = 0.2):
+                 beta: float = 1.0, optimizer: str = "sgd", lam: float = 0.2, appearance: bool = True):
         self.scene = scene
         self.r = Renderer(scene, views, backproject=False)
         self.r.render().fit_capacities(slack=1.5)
@@ -355,9 +359,11 @@ class SceneTrainer:
         assert optimizer in ("sgd", "adam")
         self.optimizer, self.t = optimizer, 0
         if optimizer == "sgd":
-            self.lr = {"pos": 1.0, "scale": 1e-2, "quat": 1e-1, "opacity": 1.0, "sh": 10.0, "feat": 1000.0}
+            self.lr = {"pos": 1.0, "scale": 1e-2, "quat": 1e-1, "opacity": 1.0, "sh": 10.0, "feat": 1000.0,
+                       "app": 1.0}
         else:   # Adam steps are scale-free: per-parameter step sizes in parameter units
-            self.lr = {"pos": 1e-3, "scale": 1e-3, "quat": 1e-3, "opacity": 1e-2, "sh": 1e-2, "feat": 1e-2}
+            self.lr = {"pos": 1e-3, "scale": 1e-3, "quat": 1e-3, "opacity": 1e-2, "sh": 1e-2, "feat": 1e-2,
+                       "app": 1e-3}
         self.lr.update(lr or {})
         dev = scene.pos.device
         self.rgb_scale = beta * (1.0 - lam) / self.r.images.rgb.numel()
@@ -367,6 +373,13 @@ class SceneTrainer:
         self.gout = G.Images(self.r.vb.total_pixels, 0, device=dev)
         self.gout.depth.zero_()
         self.gout.alpha.zero_()
+        # Eq. 3's appearance-varied rendering I^a = a I^r + b (reading Q38): 3 planes per view
+        self.appearance = appearance
+        self.rgb_runs = equal_size_runs(self.r.vb.views)
+        n_planes = 3 * self.r.vb.n
+        self.app_a = torch.ones(n_planes, device=dev)
+        self.app_b = torch.zeros(n_planes, device=dev)
+        self.grad_app = (torch.zeros(n_planes, device=dev), torch.zeros(n_planes, device=dev))
         self.grec = torch.zeros(self.r.vb.n * self.r.proj.rec_capacity * 10, dtype=torch.float32, device=dev)
         self.grads = {k: torch.zeros_like(getattr(scene, k)) for k in self.PLANES}
         self.feat_scale = 0.0
@@ -383,13 +396,16 @@ class SceneTrainer:
         if optimizer == "adam":
             keys = list(self.PLANES) + (["feat"] if target_feat is not None else [])
             self.state = {k: (torch.zeros_like(getattr(scene, k)), torch.zeros_like(getattr(scene, k))) for k in keys}
+            self.state["app_a"] = (torch.zeros_like(self.app_a), torch.zeros_like(self.app_a))
+            self.state["app_b"] = (torch.zeros_like(self.app_b), torch.zeros_like(self.app_b))
 
-    def _update(self, key, param, grad, param_h, stream):
+    def _update(self, key, param, grad, param_h, stream, lr_key=None):
+        lr = self.lr[lr_key or key]
         if self.optimizer == "sgd":
-            G.gs_feature_sgd(param, grad, self.lr[key], param_h, stream)
+            G.gs_feature_sgd(param, grad, lr, param_h, stream)
         else:
             m, v = self.state[key]
-            G.gs_adam(param, grad, m, v, self.lr[key], self.t, param_h=param_h, stream=stream)
+            G.gs_adam(param, grad, m, v, lr, self.t, param_h=param_h, stream=stream)
 
     def step(self, stream=None) -> torch.Tensor:
         """One iteration; returns the device loss of the parameters before the update."""
@@ -397,7 +413,18 @@ class SceneTrainer:
         self.t += 1
         ensure_rendered(r, stream)
         self.loss.zero_()
-        G.gs_feature_l1_grad(r.images.rgb, self.target_rgb, self.rgb_scale, self.gout.rgb, self.loss, stream)
+        if self.appearance:
+            ga, gb = self.grad_app
+            ga.zero_()
+            gb.zero_()
+            for i0, cnt, h, w in self.rgb_runs:
+                o, n = 3 * r.vb.pix_offset(i0), 3 * cnt * h * w
+                G.gs_appearance_l1_grad(r.images.rgb[o:o + n], self.target_rgb[o:o + n], 3 * cnt, h * w,
+                                        self.app_a[3 * i0:3 * (i0 + cnt)], self.app_b[3 * i0:3 * (i0 + cnt)],
+                                        self.rgb_scale, self.gout.rgb[o:o + n], ga[3 * i0:3 * (i0 + cnt)],
+                                        gb[3 * i0:3 * (i0 + cnt)], self.loss, stream)
+        else:
+            G.gs_feature_l1_grad(r.images.rgb, self.target_rgb, self.rgb_scale, self.gout.rgb, self.loss, stream)
         if self.dssim_scale != 0.0:
             for i0, cnt, h, w in self.dssim_runs:
                 o = 3 * r.vb.pix_offset(i0)
@@ -405,20 +432,28 @@ class SceneTrainer:
                 self.dssim_ws = G.gs_dssim_grad(r.images.rgb[o:o + n], self.target_rgb[o:o + n], 3 * cnt, h, w,
                                                 self.dssim_scale, self.gout.rgb[o:o + n], self.loss, self.dssim_ws,
                                                 stream)
+        if self.target_feat is not None:
+            # Eq. 2's gradient w.r.t. the rendered feature map (the geometry receives it
+            # through gs_joint_backward, the features through gs_feature_backward)
+            G.gs_feature_l1_grad(r.images.feat, self.target_feat, self.feat_scale, self.gimg, self.loss, stream)
+        self.gout.set_feat(self.gimg if self.target_feat is not None else None,
+                           sc.feat_dim if self.target_feat is not None else 0)
         self.grec.zero_()
-        G.gs_radiance_backward(r.proj, r.bins, r.vb, r.params, r.images, self.gout, self.grec, stream)
+        G.gs_joint_backward(sc, r.proj, r.bins, r.vb, r.params, r.images, self.gout, self.grec, stream)
         for g in self.grads.values():
             g.zero_()
         G.gs_mean_backward(sc, r.proj, r.vb, r.params, self.grec, self.grads["pos"], stream)
         G.gs_param_backward(sc, r.proj, r.vb, r.params, self.grec, self.grads["scale"], self.grads["quat"],
                             self.grads["opacity"], self.grads["sh"], stream)
         if self.target_feat is not None:
-            G.gs_feature_l1_grad(r.images.feat, self.target_feat, self.feat_scale, self.gimg, self.loss, stream)
             self.gfeat.zero_()
             G.gs_feature_backward(sc, r.proj, r.bins, r.vb, r.params, self.gimg, self.gfeat, stream)
             self._update("feat", sc.feat, self.gfeat, sc.feat_h, stream)
         for k in self.PLANES:
             self._update(k, getattr(sc, k), self.grads[k], None, stream)
+        if self.appearance:
+            self._update("app_a", self.app_a, self.grad_app[0], None, stream, lr_key="app")
+            self._update("app_b", self.app_b, self.grad_app[1], None, stream, lr_key="app")
         # keep every Gaussian renderable: opacity in [alpha_min, 1], scale > 0
         G.gs_sanitize_scene(sc, self.opacity_min, self.scale_min, self.sanitized, stream)
         if sc.block_bounds is not None:
