@@ -360,7 +360,7 @@ class SceneTrainer:
         self.optimizer, self.t = optimizer, 0
         if optimizer == "sgd":
             self.lr = {"pos": 1.0, "scale": 1e-2, "quat": 1e-1, "opacity": 1.0, "sh": 10.0, "feat": 1000.0,
-                       "app": 1.0}
+                       "app": 0.01}
         else:   # Adam steps are scale-free: per-parameter step sizes in parameter units
             self.lr = {"pos": 1e-3, "scale": 1e-3, "quat": 1e-3, "opacity": 1e-2, "sh": 1e-2, "feat": 1e-2,
                        "app": 1e-3}
