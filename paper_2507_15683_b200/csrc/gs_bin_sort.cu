@@ -100,6 +100,12 @@ __device__ __forceinline__ void chunk_of(uint32_t nv, uint32_t& k0, uint32_t& k1
     k1 = min(nv, k0 + per);
 }
 
+// p / nx and p % nx for the flattened (tile) index p of a rectangle nx tiles wide without a
+// per-tile integer division: m = ceil(2^32 / nx) = floor((2^32 - 1) / nx) + 1 (one 32-bit
+// division per record), q = (p m) >> 32 is exact for p nx < 2^32 (rectangles < 2^16 wide and long)
+__device__ __forceinline__ uint64_t div_magic(uint32_t nx) { return (uint64_t)(0xffffffffu / nx) + 1u; }
+__device__ __forceinline__ uint32_t div_by(uint32_t p, uint64_t m) { return (uint32_t)(((uint64_t)p * m) >> 32); }
+
 __device__ __forceinline__ void rect_of(const uint4& q3, uint32_t& x0, uint32_t& y0, uint32_t& nx, uint32_t& npair) {
     x0 = q3.z & 0xffffu;
     y0 = q3.w & 0xffffu;
@@ -135,7 +141,9 @@ count_kernel(gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restric
             const uint4 q3 = __ldg(reinterpret_cast<const uint4*>(rec + (int64_t)v * cap + k) + 3);
             uint32_t x0, y0, nx, np;
             rect_of(q3, x0, y0, nx, np);
-            for (uint32_t p = 0; p < np; ++p) bump((y0 + p / nx) * TX + x0 + p % nx);
+            const uint32_t ny = nx ? np / nx : 0u;
+            for (uint32_t ty = y0; ty < y0 + ny; ++ty)
+                for (uint32_t tx = x0; tx < x0 + nx; ++tx) bump(ty * TX + tx);
         }
     } else {
         // N3 (reading Q30): decide every (record, tile) of rectangles of <= 31 tiles with
@@ -143,6 +151,7 @@ count_kernel(gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restric
         // and store the decision as the record's tile_mask for the scatter pass
         __shared__ TightRec tr[BIN_THREADS];
         __shared__ uint32_t trect[BIN_THREADS], tnx[BIN_THREADS], tpre[BIN_THREADS], tmask[BIN_THREADS];
+        __shared__ uint64_t tdiv[BIN_THREADS];
         const uint32_t lane = threadIdx.x & 31u, wb = threadIdx.x & ~31u;
         for (uint32_t kb = k0 + wb; kb < k1; kb += blockDim.x) {
             const uint32_t k = kb + lane;
@@ -158,6 +167,7 @@ count_kernel(gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restric
             }
             trect[threadIdx.x] = x0 | (y0 << 16);
             tnx[threadIdx.x] = nx;
+            tdiv[threadIdx.x] = div_magic(nx);
             tmask[threadIdx.x] = 0u;
             uint32_t inc = small;
 #pragma unroll
@@ -175,7 +185,8 @@ count_kernel(gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restric
                 for (uint32_t step = 16; step; step >>= 1)
                     if (tpre[wb + lo + step] <= idx) lo += step;
                 const uint32_t o = wb + lo, p = idx - tpre[o], nxo = tnx[o], rx = trect[o];
-                const uint32_t tx = (rx & 0xffffu) + p % nxo, ty = (rx >> 16) + p / nxo;
+                const uint32_t pq = div_by(p, tdiv[o]);
+                const uint32_t tx = (rx & 0xffffu) + (p - pq * nxo), ty = (rx >> 16) + pq;
                 if (tile_hit(tr[o], tx, ty)) {
                     atomicOr(&tmask[o], 1u << p);
                     bump(ty * TX + tx);
@@ -187,10 +198,10 @@ count_kernel(gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restric
                 if (np > 31u) {   // large rectangle: decided per tile here and again in the scatter
                     m = GS_TILE_MASK_FULL;
                     const TightRec g = tight_of(r);
-                    for (uint32_t p = 0; p < np; ++p) {
-                        const uint32_t tx = x0 + p % nx, ty = y0 + p / nx;
-                        if (tile_hit(g, tx, ty)) bump(ty * TX + tx);
-                    }
+                    const uint32_t ny = np / nx;
+                    for (uint32_t ty = y0; ty < y0 + ny; ++ty)
+                        for (uint32_t tx = x0; tx < x0 + nx; ++tx)
+                            if (tile_hit(g, tx, ty)) bump(ty * TX + tx);
                 }
                 r->tile_mask = m;
             }
@@ -334,19 +345,21 @@ scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* _
             if (tight) {
                 const uint32_t tm = __ldg(&r->tile_mask);
                 if (!(tm & GS_TILE_MASK_FULL)) {
+                    const uint64_t dm = div_magic(nx);
                     for (uint32_t m = tm; m; m &= m - 1u) {
-                        const uint32_t p = __ffs(m) - 1u;
-                        atomicAdd(&hist[(y0 + p / nx) * TX + x0 + p % nx], 1u);
+                        const uint32_t p = __ffs(m) - 1u, pq = div_by(p, dm);
+                        atomicAdd(&hist[(y0 + pq) * TX + x0 + (p - pq * nx)], 1u);
                     }
                     continue;
                 }
             }
             const TightRec g = tight ? tight_of(r) : TightRec{};
-            for (uint32_t p = 0; p < np; ++p) {
-                const uint32_t tx = x0 + p % nx, ty = y0 + p / nx;
-                if (tight && !tile_hit(g, tx, ty)) continue;
-                atomicAdd(&hist[ty * TX + tx], 1u);
-            }
+            const uint32_t ny = np / nx;
+            for (uint32_t ty = y0; ty < y0 + ny; ++ty)
+                for (uint32_t tx = x0; tx < x0 + nx; ++tx) {
+                    if (tight && !tile_hit(g, tx, ty)) continue;
+                    atomicAdd(&hist[ty * TX + tx], 1u);
+                }
         }
         __syncthreads();
         for (int t = threadIdx.x; t < Tv; t += blockDim.x) {
@@ -355,16 +368,28 @@ scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* _
         }
         __syncthreads();
     }
-    for (uint32_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+    // one record per thread and iteration; the next record's fields are loaded before
+    // the current one's atomics and stores (the loop was bound by this load latency)
+    uint32_t k = k0 + threadIdx.x;
+    uint4 n1 = make_uint4(0u, 0u, 0u, 0u), n2 = n1, n3 = n1;
+    auto fetch = [&](uint32_t kk) {
+        const uint4* q4 = reinterpret_cast<const uint4*>(rec + (int64_t)v * cap + kk);
+        n1 = __ldg(q4 + 1);
+        n2 = __ldg(q4 + 2);
+        n3 = __ldg(q4 + 3);
+    };
+    if (k < k1) fetch(k);
+    for (; k < k1; k += blockDim.x) {
         const uint32_t slot = (uint32_t)((int64_t)v * cap + k);
-        const uint4* q4 = reinterpret_cast<const uint4*>(rec + slot);
-        const uint4 q2 = __ldg(q4 + 2), q3 = __ldg(q4 + 3);
+        const uint4 q1 = n1, q2 = n2, q3 = n3;
+        if (k + blockDim.x < k1) fetch(k + blockDim.x);
         const uint4 ent = make_uint4(q2.w, slot, q3.x, 0u);   // bits(z), slot, gid
         uint32_t x0, y0, nx, np;
         rect_of(q3, x0, y0, nx, np);
         if (tight) {
-            const uint32_t tm = __ldg(&rec[slot].tile_mask);
+            const uint32_t tm = q1.w;                            // tile_mask
             if (!(tm & GS_TILE_MASK_FULL)) {
+                const uint64_t dm = div_magic(nx);
                 for (uint32_t m = tm; m;) {
                     uint32_t pos[4], pp[4];
                     int c = 0;
@@ -373,7 +398,8 @@ scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* _
                         if (m) {
                             pp[q] = __ffs(m) - 1u;
                             m &= m - 1u;
-                            const uint32_t t = (y0 + pp[q] / nx) * TX + x0 + pp[q] % nx;
+                            const uint32_t pq = div_by(pp[q], dm);
+                            const uint32_t t = (y0 + pq) * TX + x0 + (pp[q] - pq * nx);
                             pos[q] = onchip ? atomicAdd(&hist[t], 1u) : atomicAdd(&cursor[toff + t], 1u);
                             c = q + 1;
                         }
@@ -386,13 +412,14 @@ scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* _
             }
         }
         const TightRec g = tight ? tight_of(rec + slot) : TightRec{};
+        const uint64_t dm = div_magic(nx);
         for (uint32_t p0 = 0; p0 < np; p0 += 4) {
             uint32_t pos[4];
             bool keep[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const uint32_t p = p0 + q;
-                const uint32_t tx = x0 + p % nx, ty = y0 + p / nx;
+                const uint32_t p = p0 + q, pq = div_by(p, dm);
+                const uint32_t tx = x0 + (p - pq * nx), ty = y0 + pq;
                 keep[q] = p < np && (!tight || tile_hit(g, tx, ty));
                 if (keep[q]) {
                     const uint32_t t = ty * TX + tx;

@@ -108,10 +108,10 @@ template <int D, bool CONTRIB, bool TC>
 struct RasterSmem {
     static constexpr int FS = D > 0 ? D + 8 : 1;   // fp32 feature row stride (floats)
     static constexpr int FSH = D + 8;              // fp16 feature row stride (halves; 16-B aligned rows)
-    static constexpr bool WB = D > 0 || CONTRIB;   // weight rows are collected (features and/or contributions)
-    // tcgen05 without contributions: each walked entry pair's fp16 hi / lo weights go
-    // straight from registers into the TMEM A buffer (no shared-memory weight rows)
-    static constexpr bool DIRECT = TC && !CONTRIB;
+    static constexpr bool WB = D > 0;              // weight rows are collected (features)
+    // tcgen05: each walked entry pair's fp16 hi / lo weights go straight from registers
+    // into the TMEM A buffer (no shared-memory weight rows)
+    static constexpr bool DIRECT = TC;
     static constexpr bool WSTAGE = WB && !DIRECT;
     float4 rec[NST][SE + 1][4];                    // 64-byte records; row SE = null record (opacity 0)
     float feat[(D > 0 && !TC) ? NST : 1][(D > 0 && !TC) ? SE + 1 : 1][FS];
@@ -408,22 +408,6 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
 
     // F[px][:] += W[px][0..nk) F_entries[0..nk)[:] on the tensor cores (nk multiple of 8)
     auto mma_block = [&](int kb, int ke) {
-        if constexpr (CONTRIB) {
-            // N1: per-entry sum of the warp's 32 pixel weights (lane l: row l/4, columns
-            // 8 (l%4) .. +7, then a 4-lane shuffle reduction), added to the record's
-            // contribution as 2^-32 fixed point: order-independent, hence deterministic
-            for (int k0 = kb; k0 < ke; k0 += 8) {
-                const int r = k0 + (int)(lane >> 2), c0 = (int)(lane & 3u) * 8;
-                float sum = 0.f;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) sum += sm.wbuf[warp][r][c0 + c];
-                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-                sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-                const int kr = sm.kent[warp][r];
-                if ((lane & 3u) == 0u && sum > 0.f && (kr % (SE + 1)) != SE)
-                    atomicAdd(&contrib[sm.slots[kr]], (unsigned long long)__float2ll_rn(sum * 4294967296.0f));
-            }
-        }
         if constexpr (TC) {
             // one k-step of 16 weight rows on tcgen05: A (this warp's 32 pixel rows, fp16
             // hi + lo weight pairs) -> TMEM, B (16 feature rows -> fp16) -> the canonical
@@ -517,6 +501,20 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                         mma_f16(acc[m][n], alo[m], b0, b1);
                     }
                 }
+            }
+        }
+    };
+    // N1: each walked entry's blend weights summed over the warp's 32 pixels with one
+    // integer warp reduction (REDUX) in 2^-27 fixed point (w <= alpha_max = 0.99, so 32
+    // lanes stay below 2^32) and added to the record's contribution in 2^-32 units by
+    // one 64-bit atomic: order-independent, hence run-to-run deterministic
+    auto contrib_add = [&](const int2 kk, float w1, float w2) {
+        if constexpr (CONTRIB) {
+            const uint32_t c1 = __reduce_add_sync(0xffffffffu, __float2uint_rn(w1 * 134217728.0f));
+            const uint32_t c2 = __reduce_add_sync(0xffffffffu, __float2uint_rn(w2 * 134217728.0f));
+            if (lane == 0) {
+                if (c1 && (kk.x % (SE + 1)) != SE) atomicAdd(&contrib[sm.slots[kk.x]], (unsigned long long)c1 << 5);
+                if (c2 && (kk.y % (SE + 1)) != SE) atomicAdd(&contrib[sm.slots[kk.y]], (unsigned long long)c2 << 5);
             }
         }
     };
@@ -685,6 +683,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                             const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i + j]);   // i + j even
                             float w1, w2;
                             walk_pair(kk, w1, w2);
+                            contrib_add(kk, w1, w2);
                             if constexpr (Smem::DIRECT) {
                                 store_pair(w1, w2, (pend + j) >> 1);
                             } else {
@@ -705,7 +704,9 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
 #pragma unroll 1
                     for (int i = 0; i < ne; i += 2) {
                         float w1, w2;
-                        walk_pair(*reinterpret_cast<const int2*>(&sm.ent[warp][i]), w1, w2);
+                        const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i]);
+                        walk_pair(kk, w1, w2);
+                        contrib_add(kk, w1, w2);
                     }
                 }
                 warp_done = __all_sync(0xffffffffu, done);
