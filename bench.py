@@ -78,18 +78,40 @@ def parse():
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region: NVML polled every
+    ~2 ms from a thread (short single-view regions last only milliseconds), falling
+    back to `nvidia-smi -lms 100`."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown"}
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.nvml = None
+        self.samples = []
+        self.max_mhz = None
+        self.reasons = set()
+        self.stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            dev = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            idx = int(dev.split(",")[self.gpu]) if dev and dev.split(",")[0].isdigit() else self.gpu
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nvml = (pynvml, h)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -100,11 +122,27 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        pynvml, h = self.nvml
+        while not self.stop.is_set():
+            try:
+                self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -113,6 +151,9 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        if self.nvml is not None and self.samples:
+            return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                    "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -129,7 +170,8 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvidia-smi"}
 
 
 # --------------------------------------------------------------------------- helpers
@@ -616,6 +658,19 @@ def main():
         b1.record(stream)
         torch.cuda.synchronize()
         msr = b0.elapsed_time(b1) / Kb
+        # Eq. 1's joint record gradient: the radiance terms + the feature term through the
+        # blend weights (gs_joint_backward, the upstream feature gradient = gimg)
+        gout.set_feat(gimg, scene.feat_dim)
+        G.gs_joint_backward(ds, r.proj, r.bins, r.vb, r.params, r.images, gout, grec, stream)
+        torch.cuda.synchronize()
+        b0.record(stream)
+        for _ in range(Kb):
+            grec.zero_()
+            G.gs_joint_backward(ds, r.proj, r.bins, r.vb, r.params, r.images, gout, grec, stream)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        msj = b0.elapsed_time(b1) / Kb
+        gout.set_feat(None, 0)
         # projection backward: the record gradients to the 3D means and the other parameters
         nk = (scene.sh_degree + 1) ** 2
         gpos = torch.zeros(3 * scene.n, device=dev)
@@ -657,9 +712,10 @@ def main():
         dssim_bytes = 48 * r.images.rgb.numel()
         n4 = {"views": n_views, "feature_backward_ms": ms4, "feature_backward_ms_per_view": ms4 / n_views,
               "radiance_backward_ms": msr, "radiance_backward_ms_per_view": msr / n_views,
+              "joint_backward_ms": msj, "joint_backward_ms_per_view": msj / n_views,
               "projection_backward_ms": msp, "dssim_grad_ms": msd, "dssim_grad_ms_per_view": msd / n_views,
               "dssim_grad_GBps": dssim_bytes / (msd * 1e-3) / 1e9, "feat_dim": scene.feat_dim,
-              "gpu_launches": 6 + 2 * len(runs)}
+              "gpu_launches": 7 + 2 * len(runs)}
         del tgt, grgb, wsd
         del gimg, gfeat, gout, grec
 

@@ -133,6 +133,7 @@ count_kernel(gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restric
         __syncthreads();
     }
     auto bump = [&](uint32_t t) {
+        GS_DCHECK(t < (uint32_t)Tv);
         if (onchip) atomicAdd(&hist[t], 1u);
         else atomicAdd(&counts[toff + t], 1u);
     };
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(BIN_THREADS, GS_BIN_MINB)
 scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* __restrict__ n_rec,
                const gs_view* __restrict__ views, uint32_t* __restrict__ cursor, uint4* __restrict__ bucket,
                const uint32_t* __restrict__ status, int tight, const uint32_t* __restrict__ chunk_base,
-               int cb_stride) {
+               int cb_stride, uint64_t pair_cap) {
     if (*status) return;
     extern __shared__ uint32_t hist[];
     const int v = blockIdx.y;
@@ -406,7 +407,10 @@ scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* _
                     }
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
-                        if (q < c) bucket[pos[q]] = ent;
+                        if (q < c) {
+                            GS_DCHECK(pos[q] < pair_cap);
+                            bucket[pos[q]] = ent;
+                        }
                 }
                 continue;
             }
@@ -428,7 +432,10 @@ scatter_kernel(const gs_record* __restrict__ rec, int64_t cap, const uint32_t* _
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (keep[q]) bucket[pos[q]] = ent;
+                if (keep[q]) {
+                    GS_DCHECK(pos[q] < pair_cap);
+                    bucket[pos[q]] = ent;
+                }
         }
     }
 }
@@ -854,7 +861,8 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     scan_down_kernel<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(w.counts, T, w.block_sums, out->ranges, w.cursor);
     if ((st = check_launch("scan kernels")) != GS_OK) return st;
     scatter_kernel<<<rgrid, BIN_THREADS, hist_smem, s>>>(proj->rec, cap, proj->n_rec, views_dev, w.cursor, w.bucket,
-                                                          proj->status, tight, chunk_base, cb_stride);
+                                                          proj->status, tight, chunk_base, cb_stride,
+                                                          (uint64_t)out->pair_capacity);
     if ((st = check_launch("scatter_kernel")) != GS_OK) return st;
     // small batches (single views, pyramids): every list > 256 gets a 16-warp CTA
     // (latency); large batches: one warp per list <= 512, 4-warp CTAs above (throughput)

@@ -14,6 +14,24 @@
 
 namespace gs {
 
+// Device-side bounds checks (substitute for compute-sanitizer, which the GPU pool
+// disables): built with -DGS_CHECKS they trap with the failing condition; compiled out
+// otherwise.  tools/build_checks.sh builds the checked library.
+#ifdef GS_CHECKS
+#define GS_DCHECK(c)                                                                       \
+    do {                                                                                   \
+        if (!(c)) {                                                                        \
+            printf("GS_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,  \
+                   (int)blockIdx.x, (int)threadIdx.x, #c);                                 \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define GS_DCHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 // thread-local last-error message (gs_api.cu)
 void set_error(const char* fmt, ...);
 

@@ -435,6 +435,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
 #pragma unroll
             for (int c = (int)lane; c < 16 * NC8; c += 32) {
                 const int k = c / NC8, n8 = c % NC8;
+                GS_DCHECK(sm.kent[warp][k] >= 0 && sm.kent[warp][k] < NST * (SE + 1));
                 const uint4 o = *reinterpret_cast<const uint4*>(fb + sm.kent[warp][k] * Smem::FSH + n8 * 8);
                 // element (k, n) at n8*64 + (k%8)*8 + (k/8)*8*D halves (SBO = 128 B, LBO = 16 D B)
                 *reinterpret_cast<uint4*>(bt + n8 * 64 + (k & 7) * 8 + (k >> 3) * 8 * D) = o;
@@ -506,16 +507,27 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     };
     // N1: each walked entry's blend weights summed over the warp's 32 pixels with one
     // integer warp reduction (REDUX) in 2^-27 fixed point (w <= alpha_max = 0.99, so 32
-    // lanes stay below 2^32) and added to the record's contribution in 2^-32 units by
-    // one 64-bit atomic: order-independent, hence run-to-run deterministic
-    auto contrib_add = [&](const int2 kk, float w1, float w2) {
+    // lanes stay below 2^32); the sum of the entry at compacted-list index idx is kept
+    // by lane idx % 32 and every 32 entries the lanes add theirs to the records'
+    // contributions (2^-32 units) with one 64-bit atomic each: order-independent, hence
+    // run-to-run deterministic, and no per-entry divergent atomics
+    uint32_t csum = 0;
+    auto contrib_put = [&](int idx, float w1, float w2) {
         if constexpr (CONTRIB) {
             const uint32_t c1 = __reduce_add_sync(0xffffffffu, __float2uint_rn(w1 * 134217728.0f));
             const uint32_t c2 = __reduce_add_sync(0xffffffffu, __float2uint_rn(w2 * 134217728.0f));
-            if (lane == 0) {
-                if (c1 && (kk.x % (SE + 1)) != SE) atomicAdd(&contrib[sm.slots[kk.x]], (unsigned long long)c1 << 5);
-                if (c2 && (kk.y % (SE + 1)) != SE) atomicAdd(&contrib[sm.slots[kk.y]], (unsigned long long)c2 << 5);
+            csum = ((uint32_t)idx & 31u) == lane ? c1 : csum;
+            csum = ((uint32_t)(idx + 1) & 31u) == lane ? c2 : csum;
+        }
+    };
+    auto contrib_flush = [&](int base, int cnt) {   // entries [base, base + cnt) of the list, cnt <= 32
+        if constexpr (CONTRIB) {
+            if ((int)lane < cnt && csum) {
+                const int row = sm.ent[warp][base + (int)lane];
+                if ((row % (SE + 1)) != SE)
+                    atomicAdd(&contrib[sm.slots[row]], (unsigned long long)csum << 5);
             }
+            csum = 0;
         }
     };
     // apply one evaluated entry to this lane's pixel, branch-free (om = 1 - a).  A
@@ -550,6 +562,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             const float2 hf = __half22float2(h);
             const float2 r = sub2_rn(w1, w2, hf.x, hf.y);
             const __half2 l = __floats2half2_rn(r.x, r.y);
+            GS_DCHECK((tnext & 0xffffu) >= (tA & 0xffffu) && (tnext & 0xffffu) < (tA & 0xffffu) + 24u);
             tmem_st1(tnext, *reinterpret_cast<const uint32_t*>(&h));
             tmem_st1(tnext + 8u, *reinterpret_cast<const uint32_t*>(&l));
             ++tnext;
@@ -650,6 +663,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                         }
                     }
 #endif
+                    GS_DCHECK(kk.x >= 0 && kk.x < NST * (SE + 1) && kk.y >= 0 && kk.y < NST * (SE + 1));
                     const float4* r1 = recf + 4 * kk.x;
                     const float4* r2 = recf + 4 * kk.y;
                     const float a1 = entry_alpha(r1[0], r1[1], pxf, pyf, P);
@@ -683,7 +697,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                             const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i + j]);   // i + j even
                             float w1, w2;
                             walk_pair(kk, w1, w2);
-                            contrib_add(kk, w1, w2);
+                            contrib_put(i + j, w1, w2);
+                            if (((i + j + 2) & 31) == 0) contrib_flush(i + j - 30, 32);
                             if constexpr (Smem::DIRECT) {
                                 store_pair(w1, w2, (pend + j) >> 1);
                             } else {
@@ -693,6 +708,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                         }
                         pend += m;
                         i += m;
+                        if (i >= ne && (ne & 31)) contrib_flush(ne & ~31, ne & 31);
                         if (pend == WB_ROWS) {             // a full k-step: feed the tensor cores
                             __syncwarp();
                             mma_block(0, WB_ROWS);
@@ -706,8 +722,10 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                         float w1, w2;
                         const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i]);
                         walk_pair(kk, w1, w2);
-                        contrib_add(kk, w1, w2);
+                        contrib_put(i, w1, w2);
+                        if (((i + 2) & 31) == 0) contrib_flush(i - 30, 32);
                     }
+                    if (ne & 31) contrib_flush(ne & ~31, ne & 31);
                 }
                 warp_done = __all_sync(0xffffffffu, done);
             }
@@ -721,6 +739,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             const int64_t po = V->pix_offset;
             if (inside) {
                 const int64_t loc = (int64_t)py * W + px;
+                GS_DCHECK(loc >= 0 && loc < HW && m.view < n_views);
                 // streaming stores (evict-first in L2): the 37-plane output stream must not
                 // evict the records / feature rows that neighbouring tiles re-read
                 __stcs(&out_rgb[3 * po + loc], C0);
