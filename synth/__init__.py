@@ -213,12 +213,17 @@ def _albedo(x, y):
 
 
 def aerial_v1(n: int, lx: float, ly: float, sh_degree: int = 3, feat_dim: int = 0,
-              blocks: Sequence[int] = (4, 2), seed: int = 2, chunk: int = 1 << 21) -> Scene:
+              blocks: Sequence[int] = (4, 2), seed: int = 2, chunk: int = 1 << 21,
+              sub: Sequence[int] = (1, 1)) -> Scene:
     """Aerial-like scene: 85% ground Gaussians on terrain h(x,y), 15% on box
     structures (roofs + walls).  Opacity mixture 60% U(0.7,1), 25% U(0.2,0.7),
     15% U(0.004,0.2).  SH DC from a smooth albedo field + N(0,0.05), higher
     orders N(0, 0.02^2).  Features normalize(N(0, I_D)).  Block-major order on
-    a ``blocks[0] x blocks[1]`` grid of cells (stable within a block)."""
+    a ``blocks[0] x blocks[1]`` grid of cells (the partition, PAPER.md l.134);
+    each cell is stored as ``sub[0] x sub[1]`` row-major sub-blocks (stable
+    within a sub-block), so every cell stays one contiguous range while
+    ``block_offsets`` describe the sub-blocks -- the granularity of
+    gs_project's per-(block, view) frustum cull."""
     rng = np.random.default_rng(seed)
     n_ground = int(round(0.85 * n))
     n_struct = n - n_ground
@@ -277,13 +282,15 @@ def aerial_v1(n: int, lx: float, ly: float, sh_degree: int = 3, feat_dim: int = 
     quat = np.concatenate([gq, sq], axis=1)
     del gx, gy, gz, sx, sy, sz, gq, sq
 
-    # ---- block-major order (stable within a block) ----
+    # ---- block-major order (cells, then sub-blocks inside a cell; stable within) ----
     nbx, nby = int(blocks[0]), int(blocks[1])
-    ix = np.clip(((x + lx / 2) / lx * nbx).astype(np.int64), 0, nbx - 1)
-    iy = np.clip(((y + ly / 2) / ly * nby).astype(np.int64), 0, nby - 1)
-    bid = iy * nbx + ix
+    sbx, sby = int(sub[0]), int(sub[1])
+    ix = np.clip(((x + lx / 2) / lx * (nbx * sbx)).astype(np.int64), 0, nbx * sbx - 1)
+    iy = np.clip(((y + ly / 2) / ly * (nby * sby)).astype(np.int64), 0, nby * sby - 1)
+    cell = (iy // sby) * nbx + (ix // sbx)
+    bid = cell * (sbx * sby) + (iy % sby) * sbx + (ix % sbx)
     order = np.argsort(bid, kind="stable")
-    counts = np.bincount(bid, minlength=nbx * nby)
+    counts = np.bincount(bid, minlength=nbx * nby * sbx * sby)
     block_offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
     x, y, z = x[order], y[order], z[order]
     scale = scale[:, order]
@@ -412,6 +419,8 @@ def make_config(name: str, scale: float = 1.0):
     if name == "C5":
         n = int(20_000_000 * scale)
         ext = 2000.0 * math.sqrt(scale)
-        return (aerial_v1(n, ext, ext, sh_degree=3, feat_dim=0, blocks=(4, 2), seed=5),
+        # the 4 x 2 partition (8 cells of 500 x 1000 m), each stored as 8 x 16 sub-blocks
+        # of 62.5 m (the block cull's granularity)
+        return (aerial_v1(n, ext, ext, sh_degree=3, feat_dim=0, blocks=(4, 2), seed=5, sub=(8, 16)),
                 c5_views(extent=ext))
     raise KeyError(name)
