@@ -59,6 +59,8 @@ def parse():
                     help="time gs_rasterize + gs_backproject as two launches (default: the fused "
                          "gs_rasterize_backproject)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="also time the step replayed as one CUDA graph (default for batches of <= 8 views)")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="view chunks of the overlapped e2e measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run only this many untimed steps")
@@ -517,6 +519,37 @@ def main():
 
     # e2e through the public API with host buffers: H2D of the pose batch from pinned
     # memory + the hot path + D2H of RGB + depth + opacity into pinned memory.
+    # the same step replayed as one CUDA graph (single-view configs are also
+    # timed as a graph -- their eager step is bound by launch gaps)
+    graph_info = None
+    if not sharded and scorer is None and (args.graph or n_views <= 8):
+        gr = torch.cuda.CUDAGraph()
+        gs_ = torch.cuda.Stream()
+        gs_.wait_stream(stream)
+        with torch.cuda.stream(gs_):
+            r.run(gs_)
+            with torch.cuda.graph(gr, stream=gs_):
+                r.run(torch.cuda.current_stream())
+        stream.wait_stream(gs_)
+        for _ in range(3):
+            gr.replay()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        g0.record(stream)
+        for _ in range(K):
+            gr.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        assert r.status() == 0
+        ms_g = max_over_ranks(g0.elapsed_time(g1))
+        graph_info = {"ms_per_step": ms_g / K, "value": all_px * K / (ms_g / 1e3) / 1e6,
+                      "note": "the same step (project, bin_sort, rasterize + back-projection) captured once and "
+                              "replayed as a CUDA graph"}
+        del gr
+
     e2e = None
     if sharded:
         del chunk_r, r, cg
@@ -792,7 +825,8 @@ def main():
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": raster_bytes, "dominant_stage": names[dom],
             "note": "HBM roofline of the algorithmic bytes; the kernel is instruction-issue bound "
-                    "(ncu issue-active ~0.73, profiles/r01_ncu_full_rasterize_C4x16.txt), traffic = algorithmic"}
+                    "(ncu issue-active 0.70, ~2,900 thread-instructions per pixel, "
+                    "profiles/r02_ncu_full_rasterize_C4x16.txt; DESIGN.md §4.3b), traffic = algorithmic"}
     launches_per_step = (3 if ds.n_blocks else 2) + 8 + 1 + (0 if fused else 1) + (1 if scorer is not None else 0)
     if sharded:
         launches_per_step = ((3 if ds.n_blocks else 2) + 8 + 1) * sharded_info["chunks_rendered"]
@@ -815,6 +849,8 @@ def main():
            "roofline": roof, "gpu_launches": launches_per_step * K, "e2e": e2e, "clocks": clk.summary()}
     if sharded_info is not None:
         out["sharded"] = sharded_info
+    if graph_info is not None:
+        out["graph"] = graph_info
     if n2 is not None:
         out["n2"] = n2
     if refine is not None:
