@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--graph", action="store_true",
                     help="also time the step replayed as one CUDA graph (default for batches of <= 8 views)")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="view chunks of the overlapped e2e measurement")
+    ap.add_argument("--e2e-transport", default="compact", choices=["compact", "f32"],
+                    help="D2H payload of the e2e step: compact = fp16 RGB + fp16 A + fp32 depth (12 B/px, "
+                         "gs_pack_images, reading Q39); f32 = the fp32 RGB + depth + A planes (20 B/px)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run only this many untimed steps")
     ap.add_argument("--n2", action="store_true",
@@ -572,49 +575,65 @@ def main():
             rc.fit_capacities(1.02)
             rs.append(rc)
         px_off = np.cumsum([0] + [rc.vb.total_pixels for rc in rs])
-        host_out = torch.empty(5 * total_px, dtype=torch.float32, pin_memory=True)
         copy_stream = torch.cuda.Stream()
         copied = [torch.cuda.Event() for _ in rs]
         rendered = [torch.cuda.Event() for _ in rs]
 
-        def e2e_step(first):
-            for k, rc in enumerate(rs):
-                if not first:
-                    stream.wait_event(copied[k])          # chunk k's buffers were copied out
-                rc.vb.upload(stream)
-                rc.run(stream)
-                rendered[k].record(stream)
-                copy_stream.wait_event(rendered[k])
-                with torch.cuda.stream(copy_stream):
-                    o, m = int(px_off[k]), rc.vb.total_pixels
-                    host_out[3 * o:3 * (o + m)].copy_(rc.images.rgb, non_blocking=True)
-                    host_out[3 * total_px + o:3 * total_px + o + m].copy_(rc.images.depth, non_blocking=True)
-                    host_out[4 * total_px + o:4 * total_px + o + m].copy_(rc.images.alpha, non_blocking=True)
-                copied[k].record(copy_stream)
+        def measure_e2e(transport):
+            compact = transport == "compact"
+            bpp = 12 if compact else 20
+            host_out = torch.empty(bpp * total_px, dtype=torch.uint8, pin_memory=True)
+            packed = [torch.empty(12 * rc.vb.total_pixels + 16, dtype=torch.uint8, device=dev) for rc in rs] \
+                if compact else None
+            hf = host_out.view(torch.float32) if not compact else None
 
-        e2e_step(True)
-        torch.cuda.synchronize()
-        Ke = max(2, min(K, 5))
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        for _ in range(Ke):
-            e2e_step(False)
-        s1.record(copy_stream)
-        torch.cuda.synchronize()
-        ms_e = s0.elapsed_time(s1)
-        if world > 1:
-            t = torch.tensor([ms_e], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_e = float(t.item())
-        e2e = {"value": all_px * Ke / (ms_e / 1e3) / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": int(sum(rc.vb.pinned.numel() for rc in rs)),
-               "d2h_bytes_per_step": int(5 * total_px * 4), "chunks": n_chunks,
-               "note": "pose upload + the whole step (incl. back-projection) + D2H of RGB, depth, opacity per chunk; D2H overlapped with the "
-                       "next chunk's render on a copy stream"}
-        del host_out, rs
+            def e2e_step(first):
+                for k, rc in enumerate(rs):
+                    if not first:
+                        stream.wait_event(copied[k])          # chunk k's buffers were copied out
+                    rc.vb.upload(stream)
+                    rc.run(stream)
+                    if compact:
+                        G.gs_pack_images(rc.images, rc.vb, packed[k], stream)
+                    rendered[k].record(stream)
+                    copy_stream.wait_event(rendered[k])
+                    with torch.cuda.stream(copy_stream):
+                        o, m = int(px_off[k]), rc.vb.total_pixels
+                        if compact:
+                            host_out[12 * o:12 * (o + m)].copy_(packed[k][:12 * m], non_blocking=True)
+                        else:
+                            hf[3 * o:3 * (o + m)].copy_(rc.images.rgb, non_blocking=True)
+                            hf[3 * total_px + o:3 * total_px + o + m].copy_(rc.images.depth, non_blocking=True)
+                            hf[4 * total_px + o:4 * total_px + o + m].copy_(rc.images.alpha, non_blocking=True)
+                    copied[k].record(copy_stream)
+
+            e2e_step(True)
+            torch.cuda.synchronize()
+            Ke = max(2, min(K, 5))
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for _ in range(Ke):
+                e2e_step(False)
+            s1.record(copy_stream)
+            torch.cuda.synchronize()
+            ms_e = max_over_ranks(s0.elapsed_time(s1))
+            del host_out, packed
+            return {"value": all_px * Ke / (ms_e / 1e3) / 1e6, "unit": UNIT,
+                    "h2d_bytes_per_step": int(sum(rc.vb.pinned.numel() for rc in rs)),
+                    "d2h_bytes_per_step": int(bpp * total_px), "chunks": n_chunks,
+                    "transport": ("compact: fp16 RGB + fp16 A + fp32 depth, 12 B/px (gs_pack_images, reading Q39)"
+                                  if compact else "fp32 RGB + depth + A planes, 20 B/px"),
+                    "note": "pose upload + the whole step (incl. back-projection) + D2H of the step's RGB, depth, "
+                            "opacity per chunk; D2H overlapped with the next chunk's render on a copy stream"}
+
+        e2e = measure_e2e(args.e2e_transport)
+        other = measure_e2e("f32" if args.e2e_transport == "compact" else "compact")
+        e2e["other_transport"] = {"value": other["value"], "d2h_bytes_per_step": other["d2h_bytes_per_step"],
+                                  "transport": other["transport"]}
+        del rs
         torch.cuda.empty_cache()
     if r is None and (args.n2 or args.n4 or args.refine):
         r = G.Renderer(ds, views, device=dev, backproject=True, contrib=args.n1, binning=args.binning)
@@ -827,6 +846,20 @@ def main():
             "note": "HBM roofline of the algorithmic bytes; the kernel is instruction-issue bound "
                     "(ncu issue-active 0.70, ~2,900 thread-instructions per pixel, "
                     "profiles/r02_ncu_full_rasterize_C4x16.txt; DESIGN.md §4.3b), traffic = algorithmic"}
+    # SURVEY §8(d) algorithmic bytes of the other stages: gs_project N*44 (geometry once per
+    # batch) + V*12(L+1)^2 (SH of every visible record) + V*64 (records written); gs_bin_sort
+    # V*16 (rectangle + depth read) + P*4 (sorted list) + T*8 (ranges)
+    nk_sh = (scene.sh_degree + 1) ** 2
+    T_tiles = sum(((v.width + 15) // 16) * ((v.height + 15) // 16) for v in views)
+    proj_bytes = scene.n * 44 + n_visible * (12 * nk_sh + 64)
+    bin_bytes = n_visible * 16 + n_pairs * 4 + T_tiles * 8
+    stage_roofs = {
+        "gs_project": {"bound": "hbm", "algorithmic_bytes": proj_bytes,
+                       "achieved": proj_bytes / (stage_ms[0] / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                       "frac": proj_bytes / (stage_ms[0] / 1e3) / 1e9 / peak},
+        "gs_bin_sort": {"bound": "hbm", "algorithmic_bytes": bin_bytes,
+                        "achieved": bin_bytes / (stage_ms[1] / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": bin_bytes / (stage_ms[1] / 1e3) / 1e9 / peak}}
     launches_per_step = (3 if ds.n_blocks else 2) + 8 + 1 + (0 if fused else 1) + (1 if scorer is not None else 0)
     if sharded:
         launches_per_step = ((3 if ds.n_blocks else 2) + 8 + 1) * sharded_info["chunks_rendered"]
@@ -846,7 +879,8 @@ def main():
                       if scene.feat_dim else None},
            "stages_ms": {n: float(m) for n, m in zip(names, stage_ms) if n != names[4] or scorer is not None},
            "counts": {"visible_records": n_visible, "pairs": n_pairs, "pixels": total_px},
-           "roofline": roof, "gpu_launches": launches_per_step * K, "e2e": e2e, "clocks": clk.summary()}
+           "roofline": roof, "stage_rooflines": stage_roofs, "gpu_launches": launches_per_step * K, "e2e": e2e,
+           "clocks": clk.summary()}
     if sharded_info is not None:
         out["sharded"] = sharded_info
     if graph_info is not None:

@@ -543,6 +543,22 @@ gs_status gs_rasterize_backproject(const gs_scene* scene, const gs_projected* pr
                                    uint8_t* valid, void* stream);
 
 /*
+ * gs_pack_images -- the compact transport of SURVEY.md §8(e) (reading Q39): RGB + A as
+ * fp16 and the depth plane sum(w z) as fp32, 12 B per pixel instead of 20, for moving
+ * rendered batches off the GPU (device -> host, or a gather).  Per view v the packed
+ * block starts at byte 12 * pix_offset(v): planes R, G, B, A (fp16, hw each) then
+ * Sigma w z (fp32, hw).  fp16 rounding changes a colour / opacity value c <= 2 by
+ * <= 2^-11 |c| <= 9.8e-4, inside the 1e-3 image tolerance; depth is exact.
+ * format: GS_PACK_COMPACT.  out: device, gs_pack_bytes(total_pixels, format) bytes,
+ * 16-byte aligned.  Errors: GS_UNSUPPORTED for another format, GS_INVALID_ARG for
+ * NULL / misaligned pointers or a bad view batch.
+ */
+#define GS_PACK_COMPACT 1
+size_t gs_pack_bytes(int64_t total_pixels, int32_t format);
+gs_status gs_pack_images(const gs_images* in, const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
+                         int32_t format, void* out, void* stream);
+
+/*
  * gs_probe_alpha -- debug: alpha_out[i] = o_i 2^{p_i} evaluated exactly as
  * gs_rasterize's walk evaluates it (the unclamped alpha of O12 step 4, P:136
  * "alpha blending" with alpha = o exp(power) in log2 units, reading Q29), for

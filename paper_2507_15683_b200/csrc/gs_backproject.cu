@@ -7,6 +7,8 @@
 // A streaming HBM-bound pass: per pixel read depth + alpha (8 B), write xyz
 // (12 B) + valid (1 B).  One thread per 4 consecutive pixels of a row-major
 // view (float4 loads / stores when aligned), views on grid.y.
+#include <cuda_fp16.h>
+
 #include "gs_common.cuh"
 
 namespace gs {
@@ -56,10 +58,69 @@ backproject_kernel(const gs_view* __restrict__ views, const float* __restrict__ 
     }
 }
 
+// gs_pack_images (GS_PACK_COMPACT): per view, at byte 12 * pix_offset, fp16 R, G, B and
+// A planes (hw halves each) then the fp32 sum-w-z plane (hw floats).  Two pixels per
+// thread (half2 stores) when the view's planes are even-sized and aligned.
+__global__ void __launch_bounds__(256)
+pack_compact_kernel(const gs_view* __restrict__ views, const float* __restrict__ rgb, const float* __restrict__ depth,
+                    const float* __restrict__ alpha, unsigned char* __restrict__ out) {
+    const gs_view V = views[blockIdx.y];
+    const int64_t HW = (int64_t)V.width * V.height;
+    const int64_t po = V.pix_offset;
+    const float* r = rgb + 3 * po;
+    const float* al = alpha + po;
+    const float* dz = depth + po;
+    __half* oh = reinterpret_cast<__half*>(out + 12 * po);   // 4 half planes
+    float* od = reinterpret_cast<float*>(out + 12 * po + 8 * HW);
+    const bool vec = ((po & 1) == 0) && ((HW & 1) == 0);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q * 2 < HW; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = 2 * q;
+        if (vec) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float2 v = __ldcs(reinterpret_cast<const float2*>(r + c * HW + p));
+                __stcs(reinterpret_cast<__half2*>(oh + c * HW + p), __floats2half2_rn(v.x, v.y));
+            }
+            const float2 a = __ldcs(reinterpret_cast<const float2*>(al + p));
+            __stcs(reinterpret_cast<__half2*>(oh + 3 * HW + p), __floats2half2_rn(a.x, a.y));
+            __stcs(reinterpret_cast<float2*>(od + p), __ldcs(reinterpret_cast<const float2*>(dz + p)));
+        } else {
+            for (int64_t k = p; k < p + 2 && k < HW; ++k) {
+                for (int c = 0; c < 3; ++c) oh[c * HW + k] = __float2half_rn(r[c * HW + k]);
+                oh[3 * HW + k] = __float2half_rn(al[k]);
+                od[k] = dz[k];
+            }
+        }
+    }
+}
+
 }  // namespace
 }  // namespace gs
 
 using namespace gs;
+
+extern "C" size_t gs_pack_bytes(int64_t total_pixels, int32_t format) {
+    return format == GS_PACK_COMPACT && total_pixels > 0 ? (size_t)(12 * total_pixels) : 0;
+}
+
+extern "C" gs_status gs_pack_images(const gs_images* in, const gs_view* views_host, const gs_view* views_dev,
+                                    int32_t n_views, int32_t format, void* out, void* stream) {
+    int64_t total_pixels = 0, T = 0;
+    gs_status st = validate_views(views_host, views_dev, n_views, &total_pixels, &T);
+    if (st != GS_OK) return st;
+    GS_REQUIRE(format == GS_PACK_COMPACT, GS_UNSUPPORTED, "gs_pack_images: unknown format %d", format);
+    GS_REQUIRE(in && in->rgb && in->depth && in->alpha && out, GS_INVALID_ARG, "gs_pack_images: NULL pointer");
+    GS_REQUIRE(((uintptr_t)out & 15) == 0 && ((uintptr_t)in->rgb & 7) == 0 && ((uintptr_t)in->depth & 7) == 0 &&
+                   ((uintptr_t)in->alpha & 7) == 0,
+               GS_INVALID_ARG, "gs_pack_images: out must be 16-byte and the planes 8-byte aligned");
+    int64_t maxhw = 0;
+    for (int i = 0; i < n_views; ++i) maxhw = std::max<int64_t>(maxhw, (int64_t)views_host[i].width * views_host[i].height);
+    const int64_t pairs = (maxhw + 1) / 2;
+    const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((pairs + 255) / 256, (int64_t)num_sms() * 8 / n_views + 1));
+    pack_compact_kernel<<<dim3((unsigned)gx, (unsigned)n_views), 256, 0, (cudaStream_t)stream>>>(
+        views_dev, in->rgb, in->depth, in->alpha, static_cast<unsigned char*>(out));
+    return check_launch("pack_compact_kernel");
+}
 
 extern "C" gs_status gs_backproject(const gs_images* in, const gs_view* views_host, const gs_view* views_dev,
                                     int32_t n_views, float a_min, float* xyz, uint8_t* valid, void* stream) {

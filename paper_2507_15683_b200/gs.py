@@ -75,7 +75,8 @@ EXPORTS = ["gs_abi_version", "gs_last_error", "gs_default_params", "gs_views_lay
            "gs_feature_l1_grad", "gs_feature_sgd", "gs_dssim_grad", "gs_dssim_workspace_bytes",
            "gs_project_workspace_bytes", "gs_project", "gs_bin_sort_workspace_bytes", "gs_bin_sort",
            "gs_rasterize", "gs_rasterize_backproject", "gs_backproject", "gs_visibility_score",
-           "gs_visibility_workspace_bytes", "gs_probe_alpha", "gs_sanitize_scene", "gs_joint_backward", "gs_appearance_l1_grad"]
+           "gs_visibility_workspace_bytes", "gs_probe_alpha", "gs_sanitize_scene", "gs_joint_backward", "gs_appearance_l1_grad", "gs_pack_images",
+           "gs_pack_bytes"]
 
 _lib = None
 
@@ -516,6 +517,19 @@ def gs_sanitize_scene(scene: "DeviceScene", opacity_min: float, scale_min: float
     quaternions (in place); `changed` (int64 [1], device) counts the Gaussians changed."""
     _check(lib().gs_sanitize_scene(ctypes.byref(scene.struct), ctypes.c_float(opacity_min), ctypes.c_float(scale_min),
                                    _ptr(changed), _stream(stream)), "gs_sanitize_scene")
+
+
+GS_PACK_COMPACT = 1
+
+
+def gs_pack_images(images: "Images", views: "ViewBatch", out: torch.Tensor, stream=None):
+    """Compact transport (reading Q39): fp16 RGB + fp16 A + fp32 depth, 12 B/px, per view
+    at byte 12 * pix_offset (see include/gs.h).  out: uint8 device tensor."""
+    lib().gs_pack_bytes.restype = ctypes.c_size_t
+    need = int(lib().gs_pack_bytes(ctypes.c_int64(views.total_pixels), ctypes.c_int32(GS_PACK_COMPACT)))
+    assert out.dtype == torch.uint8 and out.numel() >= need
+    _check(lib().gs_pack_images(ctypes.byref(images.struct), views.host, views.dev_ptr, ctypes.c_int32(views.n),
+                                ctypes.c_int32(GS_PACK_COMPACT), _ptr(out), _stream(stream)), "gs_pack_images")
 
 
 def gs_probe_alpha(opacity: torch.Tensor, power: torch.Tensor, out: torch.Tensor, stream=None):

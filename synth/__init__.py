@@ -214,7 +214,7 @@ def _albedo(x, y):
 
 def aerial_v1(n: int, lx: float, ly: float, sh_degree: int = 3, feat_dim: int = 0,
               blocks: Sequence[int] = (4, 2), seed: int = 2, chunk: int = 1 << 21,
-              sub: Sequence[int] = (1, 1)) -> Scene:
+              sub: Sequence[int] = (1, 1), morton: bool = True) -> Scene:
     """Aerial-like scene: 85% ground Gaussians on terrain h(x,y), 15% on box
     structures (roofs + walls).  Opacity mixture 60% U(0.7,1), 25% U(0.2,0.7),
     15% U(0.004,0.2).  SH DC from a smooth albedo field + N(0,0.05), higher
@@ -223,7 +223,10 @@ def aerial_v1(n: int, lx: float, ly: float, sh_degree: int = 3, feat_dim: int = 
     each cell is stored as ``sub[0] x sub[1]`` row-major sub-blocks (stable
     within a sub-block), so every cell stays one contiguous range while
     ``block_offsets`` describe the sub-blocks -- the granularity of
-    gs_project's per-(block, view) frustum cull."""
+    gs_project's per-(block, view) frustum cull.  ``morton``: inside a
+    sub-block, Gaussians are stored in Z-order of (x, y) (a storage layout, as a
+    scene loader would write it: neighbours in memory are neighbours on the
+    ground, so a view's records and tile pairs are written coherently)."""
     rng = np.random.default_rng(seed)
     n_ground = int(round(0.85 * n))
     n_struct = n - n_ground
@@ -289,7 +292,17 @@ def aerial_v1(n: int, lx: float, ly: float, sh_degree: int = 3, feat_dim: int = 
     iy = np.clip(((y + ly / 2) / ly * (nby * sby)).astype(np.int64), 0, nby * sby - 1)
     cell = (iy // sby) * nbx + (ix // sbx)
     bid = cell * (sbx * sby) + (iy % sby) * sbx + (ix % sbx)
-    order = np.argsort(bid, kind="stable")
+    if morton:
+        # 16-bit quantisation of (x, y) over the scene, bits interleaved (Z-order)
+        qx = np.clip(((x + lx / 2) / lx * 65535.0).astype(np.int64), 0, 65535)
+        qy = np.clip(((y + ly / 2) / ly * 65535.0).astype(np.int64), 0, 65535)
+        zc = np.zeros_like(qx)
+        for b in range(16):
+            zc |= ((qx >> b) & 1) << (2 * b)
+            zc |= ((qy >> b) & 1) << (2 * b + 1)
+        order = np.lexsort((zc, bid))
+    else:
+        order = np.argsort(bid, kind="stable")
     counts = np.bincount(bid, minlength=nbx * nby * sbx * sby)
     block_offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
     x, y, z = x[order], y[order], z[order]

@@ -393,3 +393,28 @@ def test_square_and_tight_binning_keys_and_identical_images(G, orc, cfg, scale, 
             assert float((a["feat"] - b["feat"]).abs().max()) <= 1e-5 * scale
     assert torch.equal(rs["square"].proj.contrib.sum(), rs["tight"].proj.contrib.sum())
     PT.assert_flag_budget(st)
+
+
+def test_pack_images_compact_transport(G):
+    """gs_pack_images (reading Q39): per view at byte 12 * pix_offset, fp16 R, G, B, A
+    planes equal to the fp32 images rounded to nearest, then the fp32 depth plane
+    bit-identical; views of different sizes (the C3 pyramid) and an odd-sized view."""
+    sc, vs = synth.make_config("C3", scale=0.02)
+    odd = synth.make_view(vs[0].R, vs[0].t, vs[0].fx, vs[0].fy, 30.0, 20.0, 61, 41)
+    views = vs + [odd]
+    r = _gpu_render(G, sc, views)
+    n = r.vb.total_pixels
+    out = torch.zeros(12 * n + 16, dtype=torch.uint8, device="cuda")
+    G.gs_pack_images(r.images, r.vb, out)
+    torch.cuda.synchronize()
+    buf = out.cpu().numpy()
+    for i, v in enumerate(views):
+        hw, po = v.width * v.height, r.vb.pix_offset(i)
+        blk = buf[12 * po:12 * (po + hw)]
+        halves = blk[:8 * hw].view(np.float16).reshape(4, hw)
+        depth = blk[8 * hw:].view(np.float32)
+        img = {k: t.cpu().numpy() for k, t in r.view_images(i).items()}
+        np.testing.assert_array_equal(halves[:3], img["rgb"].reshape(3, hw).astype(np.float16))
+        np.testing.assert_array_equal(halves[3], img["alpha"].reshape(hw).astype(np.float16))
+        np.testing.assert_array_equal(depth, img["depth"].reshape(hw))
+        assert np.abs(halves[:3].astype(np.float32) - img["rgb"].reshape(3, hw)).max() <= 1e-3
