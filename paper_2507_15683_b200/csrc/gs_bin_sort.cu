@@ -45,6 +45,7 @@ struct BinWs {
     uint32_t* big_count;   // [0] mid list size, [1] big list size
     uint32_t* mid_list;
     uint32_t* big_list;
+    uint32_t* cls_list;    // [4][T]: tiles of 2-32, 33-64, 65-128, 129-256 pairs (throughput mode)
     uint4* bucket;
     uint64_t* ka;
     uint32_t* va;
@@ -64,6 +65,7 @@ BinWs carve(void* ws, int64_t cap, int64_t T) {
     w.big_count = reinterpret_cast<uint32_t*>(p); p += 256;
     w.mid_list = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * T);
     w.big_list = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * T);
+    w.cls_list = reinterpret_cast<uint32_t*>(p); p += 4 * align256(sizeof(uint32_t) * T);
     w.bucket = reinterpret_cast<uint4*>(p); p += align256(sizeof(uint4) * cap);
     w.ka = reinterpret_cast<uint64_t*>(p); p += align256(sizeof(uint64_t) * cap);
     w.va = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * cap);
@@ -75,7 +77,7 @@ BinWs carve(void* ws, int64_t cap, int64_t T) {
 size_t ws_bytes(int64_t cap, int64_t T) {
     const int64_t nb = (T + SCAN_TILE - 1) / SCAN_TILE + 1;
     return align256(sizeof(uint32_t) * T) * 2 + align256(sizeof(unsigned long long) * nb) + 256 +
-           2 * align256(sizeof(uint32_t) * T) + align256(sizeof(uint4) * cap) +
+           6 * align256(sizeof(uint32_t) * T) + align256(sizeof(uint4) * cap) +
            2 * (align256(sizeof(uint64_t) * cap) + align256(sizeof(uint32_t) * cap));
 }
 
@@ -611,6 +613,62 @@ warp_sort_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint4* __
     }
 }
 
+// Throughput mode: one thread per tile sorts it into a size-class list (warp-aggregated
+// appends; single-pair tiles are written here directly), then one kernel per class
+// runs the same warp sort for every tile of the class -- uniform work per warp and one
+// code path per kernel (the mixed-size kernel above spent a fifth of its stalls on
+// instruction fetch).  counts: [0] mid, [1] big, [2 + c] class c.
+__global__ void __launch_bounds__(256)
+classify_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint4* __restrict__ bucket,
+                uint32_t* __restrict__ out, uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg,
+                uint32_t* __restrict__ counts, uint32_t* __restrict__ mid_list, uint32_t* __restrict__ big_list,
+                uint32_t* __restrict__ cls_list, uint32_t mid_max, const uint32_t* __restrict__ status) {
+    if (*status) return;
+    const int64_t tile = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t lane = threadIdx.x & 31u;
+    int cls = -1;
+    if (tile < T) {
+        const uint32_t st = ranges[2 * tile], len = ranges[2 * tile + 1] - st;
+        if (len == 1) {
+            const uint4 b = bucket[st];
+            out[st] = b.y;
+            if (ogid) ogid[st] = b.z;
+            if (dbg) dbg[st] = ((uint64_t)tile << 32) | b.x;
+        } else if (len >= 2) {
+            cls = len <= 32 ? 2 : len <= 64 ? 3 : len <= 128 ? 4 : len <= SMALL_MAX ? 5 : len <= mid_max ? 0 : 1;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+        const uint32_t m = __ballot_sync(0xffffffffu, cls == c);
+        if (!m) continue;
+        const uint32_t leader = __ffs(m) - 1u;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(&counts[c], (uint32_t)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (cls == c) {
+            uint32_t* list = c == 0 ? mid_list : c == 1 ? big_list : cls_list + (int64_t)(c - 2) * T;
+            list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)tile;
+        }
+    }
+}
+
+template <int PER>
+__global__ void __launch_bounds__(256)
+class_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ bucket, uint32_t* __restrict__ out,
+                  uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg, const uint32_t* __restrict__ count,
+                  const uint32_t* __restrict__ list, const uint32_t* __restrict__ status) {
+    if (*status) return;
+    __shared__ uint2 stage[8][32 * PER];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t n = *count;
+    for (uint32_t i = blockIdx.x * 8 + warp; i < n; i += gridDim.x * 8) {
+        const uint32_t tile = list[i];
+        const uint32_t s = ranges[2 * tile], len = ranges[2 * tile + 1] - s;
+        warp_sort_tile<PER>(bucket, s, len, tile, lane, stage[warp], out, ogid, dbg);
+    }
+}
+
 // 257..512 pairs: one warp per tile (PER = 16), persistent over the mid list
 __global__ void __launch_bounds__(256)
 mid_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ bucket, uint32_t* __restrict__ out,
@@ -829,7 +887,7 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     BinWs w = carve(ws, out->pair_capacity, T);
     const int64_t cap = proj->rec_capacity;
     cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * T, s);
-    cudaMemsetAsync(w.big_count, 0, 2 * sizeof(uint32_t), s);
+    cudaMemsetAsync(w.big_count, 0, 6 * sizeof(uint32_t), s);
 
     // chunks of >= 1024 records, ~8 CTAs per SM over the whole batch (latency hiding of the
     // per-record tile loops; each CTA flushes its on-chip histogram once)
@@ -867,11 +925,28 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     // small batches (single views, pyramids): every list > 256 gets a 16-warp CTA
     // (latency); large batches: one warp per list <= 512, 4-warp CTAs above (throughput)
     const bool latency = T <= LAT_TILES;
-    warp_sort_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(out->ranges, T, w.bucket, out->sorted_rec,
-                                                             out->sorted_gid, out->sorted_key, w.big_count,
-                                                             w.mid_list, w.big_list, latency ? 0u : WARP_SORT_MAX,
-                                                             proj->status);
-    if ((st = check_launch("warp_sort_kernel")) != GS_OK) return st;
+    if (latency) {
+        warp_sort_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(out->ranges, T, w.bucket, out->sorted_rec,
+                                                                 out->sorted_gid, out->sorted_key, w.big_count,
+                                                                 w.mid_list, w.big_list, 0u, proj->status);
+        if ((st = check_launch("warp_sort_kernel")) != GS_OK) return st;
+    } else {
+        classify_kernel<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(out->ranges, T, w.bucket, out->sorted_rec,
+                                                                    out->sorted_gid, out->sorted_key, w.big_count,
+                                                                    w.mid_list, w.big_list, w.cls_list,
+                                                                    WARP_SORT_MAX, proj->status);
+        if ((st = check_launch("classify_kernel")) != GS_OK) return st;
+        const unsigned cg = 8 * num_sms();
+        class_sort_kernel<1><<<cg, 256, 0, s>>>(out->ranges, w.bucket, out->sorted_rec, out->sorted_gid,
+                                                out->sorted_key, w.big_count + 2, w.cls_list, proj->status);
+        class_sort_kernel<2><<<cg, 256, 0, s>>>(out->ranges, w.bucket, out->sorted_rec, out->sorted_gid,
+                                                out->sorted_key, w.big_count + 3, w.cls_list + T, proj->status);
+        class_sort_kernel<4><<<cg, 256, 0, s>>>(out->ranges, w.bucket, out->sorted_rec, out->sorted_gid,
+                                                out->sorted_key, w.big_count + 4, w.cls_list + 2 * T, proj->status);
+        class_sort_kernel<8><<<cg, 256, 0, s>>>(out->ranges, w.bucket, out->sorted_rec, out->sorted_gid,
+                                                out->sorted_key, w.big_count + 5, w.cls_list + 3 * T, proj->status);
+        if ((st = check_launch("class_sort_kernel")) != GS_OK) return st;
+    }
     if (!latency) {
         mid_sort_kernel<<<4 * num_sms(), 256, 0, s>>>(out->ranges, w.bucket, out->sorted_rec, out->sorted_gid,
                                                       out->sorted_key, w.big_count, w.mid_list, proj->status);
