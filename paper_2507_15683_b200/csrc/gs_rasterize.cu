@@ -1049,7 +1049,7 @@ gs_status launch_backward(const gs_projected* proj, const gs_bins* bins, const g
 constexpr int NGRAD = 10;
 
 template <int DF>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, DF > 0 ? 3 : 4)
 radiance_backward_kernel(const gs_view* __restrict__ views, int n_views, const gs_record* __restrict__ rec,
                          const uint32_t* __restrict__ sorted_rec, const uint32_t* __restrict__ ranges, gs_params P,
                          const float* __restrict__ img_rgb, const float* __restrict__ img_depth,
@@ -1060,7 +1060,9 @@ radiance_backward_kernel(const gs_view* __restrict__ views, int n_views, const g
                          const float* __restrict__ g_feat) {
     if (*status) return;
     __shared__ float4 srec[BW_CHUNK + 1][3];
-    __shared__ __align__(16) float sfeat[DF > 0 ? BW_CHUNK : 1][DF > 0 ? DF : 4];
+    __shared__ __align__(16) float sfeat[DF > 0 ? BW_CHUNK + 1 : 1][DF > 0 ? DF : 4];   // row BW_CHUNK = 0
+    // gF . f_k of 16 walked entries x the warp's 32 pixels (tensor-core dots, below)
+    __shared__ float sdot[DF > 0 ? 8 : 1][DF > 0 ? 16 : 1][DF > 0 ? 33 : 1];
     __shared__ uint32_t sslot[BW_CHUNK];
     __shared__ float acc[BW_CHUNK][NGRAD + 1];
     __shared__ int ent[8][2 * 32 + 2];
@@ -1087,15 +1089,79 @@ radiance_backward_kernel(const gs_view* __restrict__ views, int n_views, const g
         gD = __ldg(&g_depth[po + loc]);
         gA = __ldg(&g_alpha[po + loc]);
     }
-    // feature term: this pixel's upstream gradient and gF . F of the forward's map
-    float gF[DF > 0 ? DF : 1];
+    // feature term: gF . F of the forward's map at this pixel, and the warp's upstream
+    // gradients as fp16 hi / lo B fragments of m16n8k16 MMAs (k = channel, n = pixel
+    // 8 nt + g of the warp's 8x4 block, the same pixel numbering as the lanes)
     float SF = 0.f, Sacc = 0.f;
+    constexpr int KS = DF > 0 ? (DF + 15) / 16 : 1;
+    uint32_t gbh[DF > 0 ? 4 : 1][KS][2], gbl[DF > 0 ? 4 : 1][KS][2];
+    if constexpr (DF > 0) {
+        const int g8 = lane >> 2, t4 = lane & 3;
+        const float* GF = g_feat + (int64_t)DF * po;
 #pragma unroll
-    for (int c = 0; c < DF; ++c) {
-        gF[c] = inside ? __ldg(&g_feat[(int64_t)DF * po + (int64_t)c * HW + loc]) : 0.f;
-        if (inside) SF = fmaf(gF[c], __ldg(&img_feat[(int64_t)DF * po + (int64_t)c * HW + loc]), SF);
+        for (int c = 0; c < DF; ++c)
+            if (inside) SF = fmaf(__ldg(&GF[(int64_t)c * HW + loc]), __ldg(&img_feat[(int64_t)DF * po + (int64_t)c * HW + loc]), SF);
+        auto gv = [&](int p, int c) -> float {
+            const int x = sx + (p & 7), y = sy + (p >> 3);
+            return (c < DF && x < W && y < H) ? __ldg(&GF[(int64_t)c * HW + (int64_t)y * W + x]) : 0.f;
+        };
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int p = 8 * nt + g8, c = 16 * ks + 2 * t4 + 8 * r;
+                    const float v0 = gv(p, c), v1 = gv(p, c + 1);
+                    const __half2 h = __floats2half2_rn(v0, v1);
+                    const float2 hf = __half22float2(h);
+                    gbh[nt][ks][r] = *reinterpret_cast<const uint32_t*>(&h);
+                    gbl[nt][ks][r] = pack_h2(v0 - hf.x, v1 - hf.y);
+                }
     }
+    // dots of the walked entries ent[eb .. eb + 16) (row BW_CHUNK beyond the list) with
+    // the 32 pixels' gF: A = feature rows (fp16 hi / lo), 3 products per k-step (~2^-22)
+    auto dots16 = [&](int eb, int n_ent) {
+        if constexpr (DF > 0) {
+            const int g8 = lane >> 2, t4 = lane & 3;
+            const int e0 = eb + g8 < n_ent ? ent[warp][eb + g8] : BW_CHUNK;
+            const int e1 = eb + g8 + 8 < n_ent ? ent[warp][eb + g8 + 8] : BW_CHUNK;
+            float d[4][4];
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                uint32_t ah[4], al[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int e = (i & 1) ? e1 : e0, c = 16 * ks + 2 * t4 + ((i & 2) ? 8 : 0);
+                    const float f0 = c < DF ? sfeat[e][c] : 0.f, f1 = c + 1 < DF ? sfeat[e][c + 1] : 0.f;
+                    const __half2 h = __floats2half2_rn(f0, f1);
+                    const float2 hf = __half22float2(h);
+                    ah[i] = *reinterpret_cast<const uint32_t*>(&h);
+                    al[i] = pack_h2(f0 - hf.x, f1 - hf.y);
+                }
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    mma_f16(d[nt], ah, gbh[nt][ks][0], gbh[nt][ks][1]);
+                    mma_f16(d[nt], ah, gbl[nt][ks][0], gbl[nt][ks][1]);
+                    mma_f16(d[nt], al, gbh[nt][ks][0], gbh[nt][ks][1]);
+                }
+            }
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                const int px0 = 8 * nt + 2 * t4;
+                sdot[warp][g8][px0] = d[nt][0];
+                sdot[warp][g8][px0 + 1] = d[nt][1];
+                sdot[warp][g8 + 8][px0] = d[nt][2];
+                sdot[warp][g8 + 8][px0 + 1] = d[nt][3];
+            }
+            __syncwarp();
+        }
+    };
     for (int i = tid; i < BW_CHUNK * (NGRAD + 1); i += 256) (&acc[0][0])[i] = 0.f;
+    if constexpr (DF > 0)
+        for (int i = tid; i < DF; i += 256) sfeat[BW_CHUNK][i] = 0.f;
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Dz = 0.f;
     bool done = !inside;
     bool warp_done = __all_sync(0xffffffffu, done);
@@ -1109,9 +1175,11 @@ radiance_backward_kernel(const gs_view* __restrict__ views, int n_views, const g
             if (i % 3 == 0) sslot[i / 3] = slot;
         }
         if constexpr (DF > 0) {
+            // the chunk's feature rows (gid of each entry read once, then coalesced float4 rows)
+            __syncthreads();
             for (int i = tid; i < cnt * (DF / 4); i += 256) {
                 const int e = i / (DF / 4), q = i % (DF / 4);
-                const uint32_t g = __ldg(&rec[__ldg(&sorted_rec[c0 + e])].gid);
+                const uint32_t g = __ldg(&rec[sslot[e]].gid);
                 reinterpret_cast<float4*>(&sfeat[e][0])[q] = __ldg(reinterpret_cast<const float4*>(feat + (int64_t)g * DF) + q);
             }
         }
@@ -1133,6 +1201,8 @@ radiance_backward_kernel(const gs_view* __restrict__ views, int n_views, const g
             if (hit[1]) ent[warp][n0 + __popc(m1 & below)] = lane + 32;
             __syncwarp();
             for (int i = 0; i < n; ++i) {
+                if constexpr (DF > 0)
+                    if ((i & 15) == 0) dots16(i, n);
                 const int k = ent[warp][i];
                 const float4 a4 = srec[k][0], b4 = srec[k][1], c4 = srec[k][2];
                 // the forward's exponent / alpha (entry_alpha), keeping 2^p and the raw alpha
@@ -1150,16 +1220,7 @@ radiance_backward_kernel(const gs_view* __restrict__ views, int n_views, const g
                 for (int q = 0; q < 16; ++q) g[q] = 0.f;
                 const bool blended = wgt > 0.f;
                 float dot = 0.f;                       // gF . f_k (feature term)
-                if constexpr (DF > 0) {
-                    if (blended) {
-#pragma unroll
-                        for (int c = 0; c < DF; c += 4) {
-                            const float4 f4 = *reinterpret_cast<const float4*>(&sfeat[k][c]);
-                            dot = fmaf(gF[c], f4.x, dot); dot = fmaf(gF[c + 1], f4.y, dot);
-                            dot = fmaf(gF[c + 2], f4.z, dot); dot = fmaf(gF[c + 3], f4.w, dot);
-                        }
-                    }
-                }
+                if constexpr (DF > 0) dot = sdot[warp][i & 15][lane];
                 if (blended) {
                     C0 = fmaf(wgt, c4.x, C0); C1 = fmaf(wgt, c4.y, C1); C2 = fmaf(wgt, c4.z, C2); Dz = fmaf(wgt, c4.w, Dz);
                     const float iom = __frcp_rn(1.0f - alpha);
