@@ -53,9 +53,13 @@ namespace {
 
 constexpr int NCW = 8;                 // consumer warps
 constexpr int RT_THREADS = (NCW + 1) * 32;
-constexpr int SE = 32;                 // entries per stage (one ballot)
+#ifndef GS_SE
+#define GS_SE 64                       // r2: 64-entry stages, 5 of them (C4 27.66 -> 27.34 ms)
+#endif
+constexpr int SE = GS_SE;              // entries per stage (SE / 32 ballots)
+constexpr int SPL = SE / 32;           // entries per lane per stage
 #ifndef GS_NST
-#define GS_NST 8
+#define GS_NST 5
 #endif
 constexpr int NST = GS_NST;            // ring stages
 constexpr int WB_STRIDE = 36;          // weight-buffer row stride (conflict-free m16n8k16 A fragments)
@@ -629,27 +633,35 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
         }
         if (!warp_done && (m.cnt > 0 || cnt2 > 0)) {
             const int flat0 = buf * (SE + 1), flat2 = buf2 * (SE + 1);
-            const int j = (int)lane;
-            bool hit = false, hit2 = false;
-            if (j < m.cnt) {
-                const float4 a = sm.rec[buf][j][0];   // u, v, ea, eb
-                const float4 b = sm.rec[buf][j][1];   // ec, o, e_cut, -
-                hit = ellipse_hits_rect(a.x, a.y, a.z, a.w, b.x, b.z, rx0, rx1, ry0, ry1);
+            bool hit[2 * SPL];
+            uint32_t mk[2 * SPL];
+#pragma unroll
+            for (int h = 0; h < 2 * SPL; ++h) {
+                const int j = (int)lane + 32 * (h % SPL);
+                const int b = h < SPL ? buf : buf2;
+                hit[h] = false;
+                if (j < (h < SPL ? m.cnt : cnt2)) {
+                    const float4 a = sm.rec[b][j][0];   // u, v, ea, eb
+                    const float4 q = sm.rec[b][j][1];   // ec, o, e_cut, -
+                    hit[h] = ellipse_hits_rect(a.x, a.y, a.z, a.w, q.x, q.z, rx0, rx1, ry0, ry1);
+                }
             }
-            if (j < cnt2) {
-                const float4 a = sm.rec[buf2][j][0];
-                const float4 b = sm.rec[buf2][j][1];
-                hit2 = ellipse_hits_rect(a.x, a.y, a.z, a.w, b.x, b.z, rx0, rx1, ry0, ry1);
+            int off[2 * SPL + 1];
+            off[0] = 0;
+#pragma unroll
+            for (int h = 0; h < 2 * SPL; ++h) {
+                mk[h] = __ballot_sync(0xffffffffu, hit[h]);
+                off[h + 1] = off[h] + __popc(mk[h]);
             }
-            const uint32_t msk = __ballot_sync(0xffffffffu, hit);
-            const uint32_t msk2 = __ballot_sync(0xffffffffu, hit2);
-            const int n1 = __popc(msk);
-            const int n = n1 + __popc(msk2);
+            const int n = off[2 * SPL];
             if (n > 0) {
                 // compacted in-order entry list; an odd tail is padded with the null record
                 const uint32_t below = (1u << lane) - 1u;
-                if (hit) sm.ent[warp][__popc(msk & below)] = flat0 + j;
-                if (hit2) sm.ent[warp][n1 + __popc(msk2 & below)] = flat2 + j;
+#pragma unroll
+                for (int h = 0; h < 2 * SPL; ++h)
+                    if (hit[h])
+                        sm.ent[warp][off[h] + __popc(mk[h] & below)] =
+                            (h < SPL ? flat0 : flat2) + (int)lane + 32 * (h % SPL);
                 if (lane == 0 && (n & 1)) sm.ent[warp][n] = flat0 + SE;
                 __syncwarp();
                 // walk one entry pair: independent alphas (ILP 2), transmittance in list order
