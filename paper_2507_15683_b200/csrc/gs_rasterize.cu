@@ -784,11 +784,14 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     for (int c = 0; c < D; ++c) f[c] = 0.f;
                 }
                 if (inside) {
-                    float* q = out_feat + (int64_t)D * po + (int64_t)py * W + px;
+                    // byte address stepped by one plane per channel (64-bit add + store per
+                    // channel; the float-index form compiled to index arithmetic + LEA pairs)
+                    uint64_t qa = reinterpret_cast<uint64_t>(out_feat + (int64_t)D * po + (int64_t)py * W + px);
+                    const uint64_t step = 4ull * (uint64_t)HW;
 #pragma unroll
                     for (int c = 0; c < D; ++c) {
-                        __stcs(q, f[c]);
-                        q += HW;
+                        __stcs(reinterpret_cast<float*>(qa), f[c]);
+                        qa += step;
                     }
                 }
             } else if constexpr (D > 0) {
