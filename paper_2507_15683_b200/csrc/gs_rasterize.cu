@@ -10,7 +10,7 @@
 //     fed by 1 producer warp;
 //   * persistent CTAs (grid = SMs x resident CTAs, tiles handed out in order by
 //     a dynamic scheduler); the producer streams the sorted lists of the CTA's
-//     tiles through an 8-stage x 32-entry shared-memory ring (cp.async 16-B
+//     tiles through a 5-stage x 64-entry shared-memory ring (cp.async 16-B
 //     gathers of the 64-B records and the feature rows, completion signalled on
 //     "full" mbarriers via cp.async.mbarrier.arrive), running ahead across tile
 //     boundaries; consumers take stages in same-tile pairs and release them
@@ -589,7 +589,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     };
 
     // Consumers take the ring two stages at a time when both belong to the same tile
-    // (the producer keeps 32-entry stages): one wait / cull-compaction / walk / release
+    // (SE-entry stages): one wait / cull-compaction / walk / release
     // cycle per 64 entries halves the per-stage bookkeeping.
     for (uint32_t s = 0;;) {
         const int buf = (int)(s % NST);
