@@ -142,18 +142,15 @@ __device__ __forceinline__ int find_view_by_tile(const gs_view* __restrict__ vie
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
 // O13 for one pixel (gs_backproject and the fused epilogue of gs_rasterize_backproject):
-// valid iff A >= a_min and Dz/A > 0 -- with A >= a_min > 0 the second test is Dz > 0,
-// decided on the fp32 inputs exactly as the oracle (which divides in fp64); the point
-// X = R^T(((px - cx)/fx zb, (py - cy)/fy zb, zb) - t), zb = Dz/A, is a value (tolerance
-// 1e-3 of the scene scale, not a decision), so its divisions use the MUFU reciprocal
-// (relative error ~2^-22) instead of the IEEE sequence
+// valid iff A >= a_min and Dz/A > 0 (fp32); X = R^T(((px - cx)/fx zb, (py - cy)/fy zb, zb) - t)
 __device__ __forceinline__ void bp_pixel(const gs_view& V, float Dz, float A, float a_min, int px, int py, float& X,
                                          float& Y, float& Z, uint8_t& ok) {
-    const bool valid = A >= a_min && a_min > 0.0f ? Dz > 0.0f : (A >= a_min && (Dz / A) > 0.0f);
+    // validity decided in fp32 on the fp32 A (same precision as the oracle)
+    const bool valid = A >= a_min && (Dz / A) > 0.0f;
     if (!valid) { X = Y = Z = 0.f; ok = 0; return; }
-    const float zb = __fdividef(Dz, A);
-    const float c0 = __fdividef((float)px - V.cx, V.fx) * zb - V.t[0];
-    const float c1 = __fdividef((float)py - V.cy, V.fy) * zb - V.t[1];
+    const float zb = Dz / A;
+    const float c0 = ((float)px - V.cx) / V.fx * zb - V.t[0];
+    const float c1 = ((float)py - V.cy) / V.fy * zb - V.t[1];
     const float c2 = zb - V.t[2];
     X = V.R[0] * c0 + V.R[3] * c1 + V.R[6] * c2;
     Y = V.R[1] * c0 + V.R[4] * c1 + V.R[7] * c2;
