@@ -65,7 +65,10 @@ constexpr int NST = GS_NST;            // ring stages
 constexpr int WB_STRIDE = 36;          // weight-buffer row stride (conflict-free m16n8k16 A fragments)
 constexpr int WB_ROWS = 16;            // one tensor-core k-step of weights (m16n8k16)
 constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
-constexpr uint32_t SCHED_CHUNK = 2;    // tiles per scheduler claim
+#ifndef GS_SCHED_CHUNK
+#define GS_SCHED_CHUNK 2
+#endif
+constexpr uint32_t SCHED_CHUNK = GS_SCHED_CHUNK;   // tiles per scheduler claim
 
 // 16-B global->shared copy that asks L2 to keep the line (records and feature rows
 // are re-read by the ~4 neighbouring tiles a Gaussian overlaps)
