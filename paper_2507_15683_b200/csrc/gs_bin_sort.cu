@@ -45,7 +45,7 @@ struct BinWs {
     uint32_t* big_count;   // [0] mid list size, [1] big list size
     uint32_t* mid_list;
     uint32_t* big_list;
-    uint32_t* cls_list;    // [4][T]: tiles of 2-32, 33-64, 65-128, 129-256 pairs (throughput mode)
+    uint32_t* cls_list;    // [5][T]: tiles of 2-32, 33-64, 65-128, 129-256, 513-1024 pairs (throughput mode)
     uint4* bucket;
     uint64_t* ka;
     uint32_t* va;
@@ -65,7 +65,7 @@ BinWs carve(void* ws, int64_t cap, int64_t T) {
     w.big_count = reinterpret_cast<uint32_t*>(p); p += 256;
     w.mid_list = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * T);
     w.big_list = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * T);
-    w.cls_list = reinterpret_cast<uint32_t*>(p); p += 4 * align256(sizeof(uint32_t) * T);
+    w.cls_list = reinterpret_cast<uint32_t*>(p); p += 5 * align256(sizeof(uint32_t) * T);
     w.bucket = reinterpret_cast<uint4*>(p); p += align256(sizeof(uint4) * cap);
     w.ka = reinterpret_cast<uint64_t*>(p); p += align256(sizeof(uint64_t) * cap);
     w.va = reinterpret_cast<uint32_t*>(p); p += align256(sizeof(uint32_t) * cap);
@@ -77,7 +77,7 @@ BinWs carve(void* ws, int64_t cap, int64_t T) {
 size_t ws_bytes(int64_t cap, int64_t T) {
     const int64_t nb = (T + SCAN_TILE - 1) / SCAN_TILE + 1;
     return align256(sizeof(uint32_t) * T) * 2 + align256(sizeof(unsigned long long) * nb) + 256 +
-           6 * align256(sizeof(uint32_t) * T) + align256(sizeof(uint4) * cap) +
+           7 * align256(sizeof(uint32_t) * T) + align256(sizeof(uint4) * cap) +
            2 * (align256(sizeof(uint64_t) * cap) + align256(sizeof(uint32_t) * cap));
 }
 
@@ -635,11 +635,12 @@ classify_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint4* __r
             if (ogid) ogid[st] = b.z;
             if (dbg) dbg[st] = ((uint64_t)tile << 32) | b.x;
         } else if (len >= 2) {
-            cls = len <= 32 ? 2 : len <= 64 ? 3 : len <= 128 ? 4 : len <= SMALL_MAX ? 5 : len <= mid_max ? 0 : 1;
+            cls = len <= 32 ? 2 : len <= 64 ? 3 : len <= 128 ? 4 : len <= SMALL_MAX ? 5 : len <= mid_max ? 0
+                : len <= 1024u ? 6 : 1;
         }
     }
 #pragma unroll
-    for (int c = 0; c < 6; ++c) {
+    for (int c = 0; c < 7; ++c) {
         const uint32_t m = __ballot_sync(0xffffffffu, cls == c);
         if (!m) continue;
         const uint32_t leader = __ffs(m) - 1u;
@@ -647,7 +648,7 @@ classify_kernel(const uint32_t* __restrict__ ranges, int64_t T, const uint4* __r
         if (lane == leader) base = atomicAdd(&counts[c], (uint32_t)__popc(m));
         base = __shfl_sync(0xffffffffu, base, leader);
         if (cls == c) {
-            uint32_t* list = c == 0 ? mid_list : c == 1 ? big_list : cls_list + (int64_t)(c - 2) * T;
+            uint32_t* list = c == 0 ? mid_list : c == 1 ? big_list : cls_list + (int64_t)(c - 2) * T;   // c = 6: 513..1024
             list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)tile;
         }
     }
@@ -786,7 +787,8 @@ __device__ int smem_sort_run(uint64_t* ak, uint32_t* av, uint64_t* bk, uint32_t*
     return in_b;
 }
 
-__global__ void __launch_bounds__(LAT_THREADS)
+template <int SMAX>
+__global__ void __launch_bounds__(SMAX <= 1024 ? BIG_THREADS : LAT_THREADS, SMAX <= 1024 ? 6 : 1)
 big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ bucket, uint64_t* __restrict__ ka,
                 uint32_t* __restrict__ va, uint64_t* __restrict__ kb, uint32_t* __restrict__ vb,
                 uint32_t* __restrict__ out, uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg,
@@ -796,16 +798,17 @@ big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ b
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t nwarp = blockDim.x >> 5;
     uint64_t* sk0 = reinterpret_cast<uint64_t*>(smem_raw);
-    uint64_t* sk1 = sk0 + RUN_PAD;
-    uint32_t* sv0 = reinterpret_cast<uint32_t*>(sk1 + RUN_PAD);
-    uint32_t* sv1 = sv0 + RUN_PAD;
-    const uint32_t nbig = big_count[1];
+    constexpr int PAD = SMAX + SMAX / 16;
+    uint64_t* sk1 = sk0 + PAD;
+    uint32_t* sv0 = reinterpret_cast<uint32_t*>(sk1 + PAD);
+    uint32_t* sv1 = sv0 + PAD;
+    const uint32_t nbig = *big_count;
     for (uint32_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
         const uint32_t tile = big_list[bi];
         const uint32_t s = ranges[2 * tile], len = ranges[2 * tile + 1] - s;
-        const bool one_run = len <= SMEM_SORT_MAX;
-        for (uint32_t r0 = 0; r0 < len; r0 += SMEM_SORT_MAX) {
-            const uint32_t rl = min((uint32_t)SMEM_SORT_MAX, len - r0);
+        const bool one_run = len <= SMAX;
+        for (uint32_t r0 = 0; r0 < len; r0 += SMAX) {
+            const uint32_t rl = min((uint32_t)SMAX, len - r0);
             for (uint32_t e = threadIdx.x; e < rl; e += blockDim.x) {
                 const uint4 b = bucket[s + r0 + e];
                 sk0[pidx(e)] = ((uint64_t)b.x << 32) | b.z;
@@ -836,7 +839,7 @@ big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ b
         if (one_run) continue;
         uint64_t* ck = ka + s; uint32_t* cv = va + s;
         uint64_t* nk = kb + s; uint32_t* nv = vb + s;
-        for (uint32_t width = SMEM_SORT_MAX; width < len; width <<= 1) {
+        for (uint32_t width = SMAX; width < len; width <<= 1) {
             for (uint32_t a0 = 0; a0 < len; a0 += 2 * width) {
                 const uint32_t na = min(width, len - a0);
                 const uint32_t nb = a0 + na < len ? min(width, len - a0 - na) : 0u;
@@ -887,7 +890,7 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
     BinWs w = carve(ws, out->pair_capacity, T);
     const int64_t cap = proj->rec_capacity;
     cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * T, s);
-    cudaMemsetAsync(w.big_count, 0, 6 * sizeof(uint32_t), s);
+    cudaMemsetAsync(w.big_count, 0, 7 * sizeof(uint32_t), s);
 
     // chunks of >= 1024 records, ~8 CTAs per SM over the whole batch (latency hiding of the
     // per-record tile loops; each CTA flushes its on-chip histogram once)
@@ -953,12 +956,22 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
         if ((st = check_launch("mid_sort_kernel")) != GS_OK) return st;
     }
     const int smem = 2 * RUN_PAD * (int)(sizeof(uint64_t) + sizeof(uint32_t));
-    cudaFuncSetAttribute(big_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(big_sort_kernel<SMEM_SORT_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int big_threads = latency ? LAT_THREADS : BIG_THREADS;
     const int big_grid = latency ? 2 * num_sms() : 4 * num_sms();
-    big_sort_kernel<<<big_grid, big_threads, smem, s>>>(out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb,
-                                                        out->sorted_rec, out->sorted_gid, out->sorted_key, w.big_count,
-                                                        w.big_list, proj->status);
+    if (!latency) {
+        // 513..1024 pairs: half the shared memory per CTA, twice the CTAs per SM
+        constexpr int S1K = 1024;
+        const int smem1k = 2 * (S1K + S1K / 16) * (int)(sizeof(uint64_t) + sizeof(uint32_t));
+        cudaFuncSetAttribute(big_sort_kernel<S1K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1k);
+        big_sort_kernel<S1K><<<6 * num_sms(), BIG_THREADS, smem1k, s>>>(
+            out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb, out->sorted_rec, out->sorted_gid, out->sorted_key,
+            w.big_count + 6, w.cls_list + 4 * T, proj->status);
+        if ((st = check_launch("big_sort_kernel<1024>")) != GS_OK) return st;
+    }
+    big_sort_kernel<SMEM_SORT_MAX><<<big_grid, big_threads, smem, s>>>(out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb,
+                                                        out->sorted_rec, out->sorted_gid, out->sorted_key,
+                                                        w.big_count + 1, w.big_list, proj->status);
     return check_launch("big_sort_kernel");
 }
 
