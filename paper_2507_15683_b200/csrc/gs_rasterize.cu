@@ -69,6 +69,9 @@ constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
 #define GS_SCHED_CHUNK 2
 #endif
 constexpr uint32_t SCHED_CHUNK = GS_SCHED_CHUNK;   // tiles per scheduler claim
+#ifndef GS_WALK4
+#define GS_WALK4 1                     // r2: four entries per walk iteration (4 independent alphas)
+#endif
 
 // 16-B global->shared copy that asks L2 to keep the line (records and feature rows
 // are re-read by the ~4 neighbouring tiles a Gaussian overlaps)
@@ -699,6 +702,22 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     }
 #endif
                 };
+                // two entry pairs: four independent alphas (ILP 4), then the transmittance chain
+                auto walk_quad = [&](const int2 ka, const int2 kb, float (&w)[4]) {
+                    const float4* r0 = recf + 4 * ka.x;
+                    const float4* r1 = recf + 4 * ka.y;
+                    const float4* r2 = recf + 4 * kb.x;
+                    const float4* r3 = recf + 4 * kb.y;
+                    const float a0 = entry_alpha(r0[0], r0[1], pxf, pyf, P);
+                    const float a1 = entry_alpha(r1[0], r1[1], pxf, pyf, P);
+                    const float a2 = entry_alpha(r2[0], r2[1], pxf, pyf, P);
+                    const float a3 = entry_alpha(r3[0], r3[1], pxf, pyf, P);
+                    const float2 om01 = sub2_rn(1.0f, 1.0f, a0, a1), om23 = sub2_rn(1.0f, 1.0f, a2, a3);
+                    w[0] = blend_om(a0, om01.x, r0[2]);
+                    w[1] = blend_om(a1, om01.y, r1[2]);
+                    w[2] = blend_om(a2, om23.x, r2[2]);
+                    w[3] = blend_om(a3, om23.y, r3[2]);
+                };
                 const int ne = (n + 1) & ~1;   // entry pairs (an odd tail pairs with the null record)
                 if constexpr (WB) {
                     // chunks that end at a k-step boundary: the pending-row bookkeeping (ring rows
@@ -707,8 +726,29 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                         if (pend == 0) hold = s;
                         const int m = min(ne - i, WB_ROWS - pend);
                         if (lane < (uint32_t)m) sm.kent[warp][pend + (int)lane] = sm.ent[warp][i + (int)lane];
+                        int j = 0;
+#if GS_WALK4
 #pragma unroll 1
-                        for (int j = 0; j < m; j += 2) {
+                        for (; j + 4 <= m; j += 4) {
+                            const int2 ka = *reinterpret_cast<const int2*>(&sm.ent[warp][i + j]);   // i + j even
+                            const int2 kb = *reinterpret_cast<const int2*>(&sm.ent[warp][i + j + 2]);
+                            float w[4];
+                            walk_quad(ka, kb, w);
+                            contrib_put(i + j, w[0], w[1]);
+                            if (((i + j + 2) & 31) == 0) contrib_flush(i + j - 30, 32);
+                            contrib_put(i + j + 2, w[2], w[3]);
+                            if (((i + j + 4) & 31) == 0) contrib_flush(i + j - 28, 32);
+                            if constexpr (Smem::DIRECT) {
+                                store_pair(w[0], w[1], (pend + j) >> 1);
+                                store_pair(w[2], w[3], (pend + j + 2) >> 1);
+                            } else {
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) sm.wbuf[warp][pend + j + q][lane] = w[q];
+                            }
+                        }
+#endif
+#pragma unroll 1
+                        for (; j < m; j += 2) {
                             const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i + j]);   // i + j even
                             float w1, w2;
                             walk_pair(kk, w1, w2);
@@ -732,8 +772,22 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                         }
                     }
                 } else {
+                    int i = 0;
+#if GS_WALK4
 #pragma unroll 1
-                    for (int i = 0; i < ne; i += 2) {
+                    for (; i + 4 <= ne; i += 4) {
+                        const int2 ka = *reinterpret_cast<const int2*>(&sm.ent[warp][i]);
+                        const int2 kb = *reinterpret_cast<const int2*>(&sm.ent[warp][i + 2]);
+                        float w[4];
+                        walk_quad(ka, kb, w);
+                        contrib_put(i, w[0], w[1]);
+                        if (((i + 2) & 31) == 0) contrib_flush(i - 30, 32);
+                        contrib_put(i + 2, w[2], w[3]);
+                        if (((i + 4) & 31) == 0) contrib_flush(i - 28, 32);
+                    }
+#endif
+#pragma unroll 1
+                    for (; i < ne; i += 2) {
                         float w1, w2;
                         const int2 kk = *reinterpret_cast<const int2*>(&sm.ent[warp][i]);
                         walk_pair(kk, w1, w2);
