@@ -272,15 +272,26 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
         if (qbad) degenerate = true;
     }
     const float smax = fmaxf(fmaxf(s0, s1), s2);
-    // block of this Gaussian
+    // block of this Gaussian: one binary search per CTA (its first Gaussian), then a short
+    // forward scan per thread (a CTA's 256 consecutive Gaussians span one or two blocks)
     int blk = -1;
-    if (S.n_blocks > 0 && in) {
-        int lo = 0, hi = S.n_blocks - 1;
-        while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (__ldg(&S.block_offsets[mid]) <= i) lo = mid; else hi = mid - 1;
+    if (S.n_blocks > 0) {
+        __shared__ int s_blk0;
+        if (threadIdx.x == 0) {
+            const int64_t i0 = min((int64_t)blockIdx.x * PROJ_THREADS, n - 1);
+            int lo = 0, hi = S.n_blocks - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (__ldg(&S.block_offsets[mid]) <= i0) lo = mid; else hi = mid - 1;
+            }
+            s_blk0 = lo;
         }
-        blk = lo;
+        __syncthreads();
+        if (in) {
+            int lo = s_blk0;
+            while (lo + 1 < S.n_blocks && __ldg(&S.block_offsets[lo + 1]) <= i) ++lo;
+            blk = lo;
+        }
     }
     uint32_t c_near = 0, c_transp = 0, c_degen = 0, c_off = 0;
     // reading Q30: alpha >= alpha_min cut in log2 units from exactly-rounded operations

@@ -7,7 +7,7 @@ for rep in 1 2; do for v in $VARS; do
   if [ "$v" == "main" ]; then L=paper_2507_15683_b200/libgs.so; else L=paper_2507_15683_b200/_build/var_$v/libgs.so; fi
   for c in C4 C5; do
   GS_DEBUG=1 GS_LIB=$L timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>$O/err_${v}_$c | python -c "
-import json,sys;d=json.loads(sys.stdin.read());print('$v $c', round(d['stages_ms']['gs_rasterize'],3), round(d['ms_per_step'],3))"
+import json,sys;d=json.loads(sys.stdin.read());print('$v $c', round(d['stages_ms']['gs_rasterize'],3), round(d['stages_ms']['gs_project'],3), round(d['stages_ms']['gs_bin_sort'],3), round(d['ms_per_step'],3))"
   grep -m1 "rasterize<" $O/err_${v}_$c
   done
 done; done > $O/var.txt 2>&1
