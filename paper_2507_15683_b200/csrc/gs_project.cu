@@ -164,8 +164,10 @@ __device__ __forceinline__ bool finite3(float a, float b, float c) {
     return isfinite(a) && isfinite(b) && isfinite(c);
 }
 
-// SH colour (O10, fp32, tolerance-checked): [3DGS] real SH basis up to degree 3
-__device__ __forceinline__ void sh_color(int deg, const float* __restrict__ sh, int64_t n, int64_t i, float dx,
+// SH colour (O10, fp32, tolerance-checked): [3DGS] real SH basis up to degree 3.
+// Coefficient k of channel c is coef[(k * 3 + c) * stride] (global SoA plane: stride
+// n; the warp's shared-memory copy: stride 32).
+__device__ __forceinline__ void sh_color(int deg, const float* __restrict__ coef, int64_t stride, float dx,
                                          float dy, float dz, float* rgb) {
     const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
     float b[16];
@@ -198,9 +200,11 @@ __device__ __forceinline__ void sh_color(int deg, const float* __restrict__ sh, 
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
         if (k < nk) {
-            r += b[k] * __ldg(&sh[(int64_t)(k * 3 + 0) * n + i]);
-            g += b[k] * __ldg(&sh[(int64_t)(k * 3 + 1) * n + i]);
-            bl += b[k] * __ldg(&sh[(int64_t)(k * 3 + 2) * n + i]);
+            // fused (the file is built with -fmad=false for the pinned geometry; the colour
+            // decides nothing and is tolerance-checked, so it may use FMAs)
+            r = __fmaf_rn(b[k], coef[(int64_t)(k * 3 + 0) * stride], r);
+            g = __fmaf_rn(b[k], coef[(int64_t)(k * 3 + 1) * stride], g);
+            bl = __fmaf_rn(b[k], coef[(int64_t)(k * 3 + 2) * stride], bl);
         }
     }
     rgb[0] = fmaxf(r, 0.f);
@@ -218,8 +222,14 @@ struct GTab {
     uint32_t gid, pad;
 };
 
+// r2: each warp copies its 32 Gaussians' SH coefficients into shared memory once
+// (coalesced rows) instead of every queued (view, Gaussian) pair re-reading 48
+// scattered coefficients from L2 -- the per-pair SH reads were a third of the stage
+#ifndef GS_PROJ_SH_SMEM
+#define GS_PROJ_SH_SMEM 1
+#endif
 #ifndef GS_PROJ_MIN_BLOCKS
-#define GS_PROJ_MIN_BLOCKS 4
+#define GS_PROJ_MIN_BLOCKS (GS_PROJ_SH_SMEM ? 3 : 4)
 #endif
 __global__ void __launch_bounds__(PROJ_THREADS, GS_PROJ_MIN_BLOCKS)
 project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* __restrict__ vcs, int n_views,
@@ -313,6 +323,12 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
     // 32 of them at a time with every lane busy (a view typically keeps a few percent
     // of a warp's Gaussians, so running it in place idles most lanes).
     const int wid = threadIdx.x >> 5;
+#if GS_PROJ_SH_SMEM
+    extern __shared__ float s_sh[];   // [warp][(deg+1)^2 * 3][32]
+    const int nk3 = (S.sh_degree + 1) * (S.sh_degree + 1) * 3;
+    float* my_sh = s_sh + (int64_t)wid * nk3 * 32;
+    bool sh_staged = false;           // warp-uniform
+#endif
     GTab& me = s_tab[wid][lane];
     me.mx = mx; me.my = my; me.mz = mz; me.op = op;
     for (int k = 0; k < 6; ++k) me.sg[k] = Sg[k];
@@ -323,6 +339,13 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
 
     // heavy path for queue items [0, cnt): lane k takes item k
     auto process = [&](uint32_t cnt) {
+#if GS_PROJ_SH_SMEM
+        if (!sh_staged) {   // first visible pair of this warp: stage its Gaussians' SH rows
+            for (int q = 0; q < nk3; ++q) my_sh[q * 32 + lane] = in ? __ldg(&S.sh[(int64_t)q * n + i]) : 0.f;
+            __syncwarp();
+            sh_staged = true;
+        }
+#endif
         const bool act = lane < cnt;
         const uint32_t item = act ? queue[lane] : 0u;
         const int vi = (int)(item >> 5);
@@ -394,7 +417,11 @@ project_kernel(gs_scene S, const gs_view* __restrict__ views, const ViewConst* _
                 // O10: SH colour at d = (mu - c_cam)/|mu - c_cam|
                 const float dx = g.mx - c.ccx, dy = g.my - c.ccy, dz = g.mz - c.ccz;
                 const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
-                sh_color(S.sh_degree, S.sh, n, (int64_t)g.gid, dx * inv, dy * inv, dz * inv, r.rgb);
+#if GS_PROJ_SH_SMEM
+                sh_color(S.sh_degree, my_sh + (item & 31u), 32, dx * inv, dy * inv, dz * inv, r.rgb);
+#else
+                sh_color(S.sh_degree, S.sh + g.gid, n, dx * inv, dy * inv, dz * inv, r.rgb);
+#endif
                 visible = true;
             }
         done:;
@@ -805,7 +832,13 @@ gs_status gs_project(const gs_scene* scene, const gs_view* views_host, const gs_
         if ((st = check_launch("block_cull_kernel")) != GS_OK) return st;
     }
     const unsigned grid = (unsigned)((scene->n + PROJ_THREADS - 1) / PROJ_THREADS);
-    project_kernel<<<grid, PROJ_THREADS, 0, s>>>(*scene, views_dev, vc, n_views, *params, mask, out->rec,
+    int sh_smem = 0;
+#if GS_PROJ_SH_SMEM
+    sh_smem = (PROJ_THREADS / 32) * (scene->sh_degree + 1) * (scene->sh_degree + 1) * 3 * 32 * (int)sizeof(float);
+    // kernel attributes are per device: set on every call (cheap)
+    cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sh_smem);
+#endif
+    project_kernel<<<grid, PROJ_THREADS, sh_smem, s>>>(*scene, views_dev, vc, n_views, *params, mask, out->rec,
                                                  out->rec_capacity, out->n_rec, out->diag, out->status);
     return check_launch("project_kernel");
 }
