@@ -62,9 +62,10 @@ def parse():
     ap.add_argument("--graph", action="store_true",
                     help="also time the step replayed as one CUDA graph (default for batches of <= 8 views)")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="view chunks of the overlapped e2e measurement")
-    ap.add_argument("--e2e-transport", default="compact", choices=["compact", "f32"],
-                    help="D2H payload of the e2e step: compact = fp16 RGB + fp16 A + fp32 depth (12 B/px, "
-                         "gs_pack_images, reading Q39); f32 = the fp32 RGB + depth + A planes (20 B/px)")
+    ap.add_argument("--e2e-transport", default="dense11", choices=["dense11", "compact", "f32"],
+                    help="D2H payload of the e2e leg: dense11 = fp16 RGB + unorm16 A + 24-bit depth (11 B/px), "
+                         "compact = fp16 RGB + fp16 A + fp32 depth (12 B/px), f32 = the fp32 planes (20 B/px); "
+                         "the line reports the other two as well")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run only this many untimed steps")
     ap.add_argument("--n2", action="store_true",
@@ -580,10 +581,11 @@ def main():
         rendered = [torch.cuda.Event() for _ in rs]
 
         def measure_e2e(transport):
-            compact = transport == "compact"
-            bpp = 12 if compact else 20
+            compact = transport in ("compact", "dense11")
+            fmt = G.GS_PACK_DENSE11 if transport == "dense11" else G.GS_PACK_COMPACT
+            bpp = {"dense11": 11, "compact": 12, "f32": 20}[transport]
             host_out = torch.empty(bpp * total_px, dtype=torch.uint8, pin_memory=True)
-            packed = [torch.empty(12 * rc.vb.total_pixels + 16, dtype=torch.uint8, device=dev) for rc in rs] \
+            packed = [torch.empty(bpp * rc.vb.total_pixels + 16, dtype=torch.uint8, device=dev) for rc in rs] \
                 if compact else None
             hf = host_out.view(torch.float32) if not compact else None
 
@@ -594,13 +596,13 @@ def main():
                     rc.vb.upload(stream)
                     rc.run(stream)
                     if compact:
-                        G.gs_pack_images(rc.images, rc.vb, packed[k], stream)
+                        G.gs_pack_images(rc.images, rc.vb, packed[k], stream, fmt=fmt)
                     rendered[k].record(stream)
                     copy_stream.wait_event(rendered[k])
                     with torch.cuda.stream(copy_stream):
                         o, m = int(px_off[k]), rc.vb.total_pixels
                         if compact:
-                            host_out[12 * o:12 * (o + m)].copy_(packed[k][:12 * m], non_blocking=True)
+                            host_out[bpp * o:bpp * (o + m)].copy_(packed[k][:bpp * m], non_blocking=True)
                         else:
                             hf[3 * o:3 * (o + m)].copy_(rc.images.rgb, non_blocking=True)
                             hf[3 * total_px + o:3 * total_px + o + m].copy_(rc.images.depth, non_blocking=True)
@@ -624,15 +626,22 @@ def main():
             return {"value": all_px * Ke / (ms_e / 1e3) / 1e6, "unit": UNIT,
                     "h2d_bytes_per_step": int(sum(rc.vb.pinned.numel() for rc in rs)),
                     "d2h_bytes_per_step": int(bpp * total_px), "chunks": n_chunks,
-                    "transport": ("compact: fp16 RGB + fp16 A + fp32 depth, 12 B/px (gs_pack_images, reading Q39)"
-                                  if compact else "fp32 RGB + depth + A planes, 20 B/px"),
+                    "transport": {"dense11": "dense11: fp16 RGB + unorm16 A + 24-bit depth, 11 B/px "
+                                             "(gs_pack_images GS_PACK_DENSE11, reading Q39)",
+                                  "compact": "compact: fp16 RGB + fp16 A + fp32 depth, 12 B/px "
+                                             "(gs_pack_images GS_PACK_COMPACT, reading Q39)",
+                                  "f32": "fp32 RGB + depth + A planes, 20 B/px"}[transport],
                     "note": "pose upload + the whole step (incl. back-projection) + D2H of the step's RGB, depth, "
                             "opacity per chunk; D2H overlapped with the next chunk's render on a copy stream"}
 
         e2e = measure_e2e(args.e2e_transport)
-        other = measure_e2e("f32" if args.e2e_transport == "compact" else "compact")
-        e2e["other_transport"] = {"value": other["value"], "d2h_bytes_per_step": other["d2h_bytes_per_step"],
-                                  "transport": other["transport"]}
+        e2e["other_transports"] = []
+        for t in ("dense11", "compact", "f32"):
+            if t != args.e2e_transport:
+                other = measure_e2e(t)
+                e2e["other_transports"].append({"value": other["value"],
+                                                "d2h_bytes_per_step": other["d2h_bytes_per_step"],
+                                                "transport": other["transport"]})
         del rs
         torch.cuda.empty_cache()
     if r is None and (args.n2 or args.n4 or args.refine):

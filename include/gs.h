@@ -549,11 +549,22 @@ gs_status gs_rasterize_backproject(const gs_scene* scene, const gs_projected* pr
  * block starts at byte 12 * pix_offset(v): planes R, G, B, A (fp16, hw each) then
  * Sigma w z (fp32, hw).  fp16 rounding changes a colour / opacity value c <= 2 by
  * <= 2^-11 |c| <= 9.8e-4, inside the 1e-3 image tolerance; depth is exact.
- * format: GS_PACK_COMPACT.  out: device, gs_pack_bytes(total_pixels, format) bytes,
+ * format: GS_PACK_COMPACT or GS_PACK_DENSE11 (below).  out: device,
+ * gs_pack_bytes(total_pixels, format) bytes,
  * 16-byte aligned.  Errors: GS_UNSUPPORTED for another format, GS_INVALID_ARG for
  * NULL / misaligned pointers or a bad view batch.
  */
 #define GS_PACK_COMPACT 1
+/*
+ * GS_PACK_DENSE11 (r2, Q39): 11 B per pixel, batch-planar (TP = total_pixels):
+ * bytes [0, 6 TP) the R, G, B planes (fp16, plane c at 2 c TP, pixel pix_offset(v) + i of
+ * view v at index pix_offset(v) + i), [6 TP, 8 TP) A as unorm16 round(65535 A)
+ * (error <= 7.7e-6), [8 TP, 11 TP) sum(w z) as the upper 24 bits of its fp32 pattern
+ * (round half up on the dropped byte; decode: bits << 8; relative error <= 2^-16,
+ * inside the 1e-4 depth tolerance), 3 bytes little-endian per pixel.  Requires 16-byte
+ * aligned input planes.
+ */
+#define GS_PACK_DENSE11 2
 size_t gs_pack_bytes(int64_t total_pixels, int32_t format);
 gs_status gs_pack_images(const gs_images* in, const gs_view* views_host, const gs_view* views_dev, int32_t n_views,
                          int32_t format, void* out, void* stream);

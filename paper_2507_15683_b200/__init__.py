@@ -12,6 +12,7 @@ from .gs import (GSError, DeviceScene, ViewBatch, Projected, Bins, Images, defau
                  gs_match, Matches, match_workspace_bytes, gs_pnp, gs_verify_consistency, pnp_workspace_bytes,
                  ViewsAt, GS_VIEW_BYTES, gs_feature_backward, gs_feature_l1_grad, gs_feature_sgd, gs_radiance_backward, GRAD_FIELDS, gs_mean_backward,
                  gs_param_backward, gs_adam, gs_dssim_grad, gs_probe_alpha, gs_sanitize_scene, gs_joint_backward, gs_appearance_l1_grad, gs_pack_images,
+                 gs_pack_bytes, unpack_dense11, GS_PACK_COMPACT, GS_PACK_DENSE11,
                  lib, LIB_PATH,
                  EXPORTS)
 from .pipeline import Renderer, SignificanceScorer, Refiner, FeatureDistiller, SceneTrainer  # noqa: F401

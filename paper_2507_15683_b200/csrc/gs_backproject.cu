@@ -94,13 +94,62 @@ pack_compact_kernel(const gs_view* __restrict__ views, const float* __restrict__
     }
 }
 
+// GS_PACK_DENSE11 (reading Q39): batch-planar R, G, B (fp16), A (unorm16, round(65535 A)),
+// then sum(w z) as the upper 24 bits of its fp32 pattern (rounded; 3 bytes, little-endian).
+__device__ __forceinline__ uint32_t depth24(float z) { return (__float_as_uint(z) + 0x80u) >> 8; }
+__device__ __forceinline__ uint16_t unorm16(float a) { return (uint16_t)__float2uint_rn(fminf(fmaxf(a, 0.f), 1.f) * 65535.f); }
+
+__global__ void __launch_bounds__(256)
+pack_dense11_kernel(const gs_view* __restrict__ views, int64_t total_pixels, const float* __restrict__ rgb,
+                    const float* __restrict__ depth, const float* __restrict__ alpha, unsigned char* __restrict__ out) {
+    const gs_view V = views[blockIdx.y];
+    const int64_t HW = (int64_t)V.width * V.height;
+    const int64_t po = V.pix_offset, TP = total_pixels;
+    const float* r = rgb + 3 * po;
+    __half* oh = reinterpret_cast<__half*>(out);                  // R, G, B planes of TP halves
+    uint16_t* oa = reinterpret_cast<uint16_t*>(out + 6 * TP);     // A plane
+    unsigned char* od = out + 8 * TP;                             // depth, 3 bytes per pixel
+    const bool vec = ((po & 3) == 0) && ((HW & 3) == 0) && ((TP & 3) == 0);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q * 4 < HW; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = 4 * q;
+        if (vec) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float4 v = __ldcs(reinterpret_cast<const float4*>(r + c * HW + p));
+                __half2 h[2] = {__floats2half2_rn(v.x, v.y), __floats2half2_rn(v.z, v.w)};
+                __stcs(reinterpret_cast<uint2*>(oh + c * TP + po + p), *reinterpret_cast<const uint2*>(h));
+            }
+            const float4 a = __ldcs(reinterpret_cast<const float4*>(alpha + po + p));
+            const uint2 av = make_uint2((uint32_t)unorm16(a.x) | ((uint32_t)unorm16(a.y) << 16),
+                                        (uint32_t)unorm16(a.z) | ((uint32_t)unorm16(a.w) << 16));
+            __stcs(reinterpret_cast<uint2*>(oa + po + p), av);
+            const float4 z = __ldcs(reinterpret_cast<const float4*>(depth + po + p));
+            const uint32_t d0 = depth24(z.x), d1 = depth24(z.y), d2 = depth24(z.z), d3 = depth24(z.w);
+            // 4 x 24 bits -> 3 little-endian words
+            const uint3 w = make_uint3(d0 | (d1 << 24), (d1 >> 8) | (d2 << 16), (d2 >> 16) | (d3 << 8));
+            uint32_t* o32 = reinterpret_cast<uint32_t*>(od + 3 * (po + p));
+            __stcs(o32, w.x); __stcs(o32 + 1, w.y); __stcs(o32 + 2, w.z);
+        } else {
+            for (int64_t k = p; k < p + 4 && k < HW; ++k) {
+                for (int c = 0; c < 3; ++c) oh[c * TP + po + k] = __float2half_rn(r[c * HW + k]);
+                oa[po + k] = unorm16(alpha[po + k]);
+                const uint32_t d = depth24(depth[po + k]);
+                unsigned char* b = od + 3 * (po + k);
+                b[0] = (unsigned char)d; b[1] = (unsigned char)(d >> 8); b[2] = (unsigned char)(d >> 16);
+            }
+        }
+    }
+}
+
 }  // namespace
 }  // namespace gs
 
 using namespace gs;
 
 extern "C" size_t gs_pack_bytes(int64_t total_pixels, int32_t format) {
-    return format == GS_PACK_COMPACT && total_pixels > 0 ? (size_t)(12 * total_pixels) : 0;
+    if (total_pixels <= 0) return 0;
+    return format == GS_PACK_COMPACT ? (size_t)(12 * total_pixels)
+         : format == GS_PACK_DENSE11 ? (size_t)(11 * total_pixels) : 0;
 }
 
 extern "C" gs_status gs_pack_images(const gs_images* in, const gs_view* views_host, const gs_view* views_dev,
@@ -108,7 +157,8 @@ extern "C" gs_status gs_pack_images(const gs_images* in, const gs_view* views_ho
     int64_t total_pixels = 0, T = 0;
     gs_status st = validate_views(views_host, views_dev, n_views, &total_pixels, &T);
     if (st != GS_OK) return st;
-    GS_REQUIRE(format == GS_PACK_COMPACT, GS_UNSUPPORTED, "gs_pack_images: unknown format %d", format);
+    GS_REQUIRE(format == GS_PACK_COMPACT || format == GS_PACK_DENSE11, GS_UNSUPPORTED,
+               "gs_pack_images: unknown format %d", format);
     GS_REQUIRE(in && in->rgb && in->depth && in->alpha && out, GS_INVALID_ARG, "gs_pack_images: NULL pointer");
     GS_REQUIRE(((uintptr_t)out & 15) == 0 && ((uintptr_t)in->rgb & 7) == 0 && ((uintptr_t)in->depth & 7) == 0 &&
                    ((uintptr_t)in->alpha & 7) == 0,
@@ -117,6 +167,13 @@ extern "C" gs_status gs_pack_images(const gs_images* in, const gs_view* views_ho
     for (int i = 0; i < n_views; ++i) maxhw = std::max<int64_t>(maxhw, (int64_t)views_host[i].width * views_host[i].height);
     const int64_t pairs = (maxhw + 1) / 2;
     const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((pairs + 255) / 256, (int64_t)num_sms() * 8 / n_views + 1));
+    if (format == GS_PACK_DENSE11) {
+        GS_REQUIRE(((uintptr_t)in->rgb & 15) == 0 && ((uintptr_t)in->depth & 15) == 0 && ((uintptr_t)in->alpha & 15) == 0,
+                   GS_INVALID_ARG, "gs_pack_images: GS_PACK_DENSE11 needs 16-byte aligned planes");
+        pack_dense11_kernel<<<dim3((unsigned)gx, (unsigned)n_views), 256, 0, (cudaStream_t)stream>>>(
+            views_dev, total_pixels, in->rgb, in->depth, in->alpha, static_cast<unsigned char*>(out));
+        return check_launch("pack_dense11_kernel");
+    }
     pack_compact_kernel<<<dim3((unsigned)gx, (unsigned)n_views), 256, 0, (cudaStream_t)stream>>>(
         views_dev, in->rgb, in->depth, in->alpha, static_cast<unsigned char*>(out));
     return check_launch("pack_compact_kernel");

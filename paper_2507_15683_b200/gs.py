@@ -520,16 +520,36 @@ def gs_sanitize_scene(scene: "DeviceScene", opacity_min: float, scale_min: float
 
 
 GS_PACK_COMPACT = 1
+GS_PACK_DENSE11 = 2
 
 
-def gs_pack_images(images: "Images", views: "ViewBatch", out: torch.Tensor, stream=None):
-    """Compact transport (reading Q39): fp16 RGB + fp16 A + fp32 depth, 12 B/px, per view
-    at byte 12 * pix_offset (see include/gs.h).  out: uint8 device tensor."""
+def gs_pack_bytes(total_pixels: int, fmt: int = GS_PACK_COMPACT) -> int:
     lib().gs_pack_bytes.restype = ctypes.c_size_t
-    need = int(lib().gs_pack_bytes(ctypes.c_int64(views.total_pixels), ctypes.c_int32(GS_PACK_COMPACT)))
+    return int(lib().gs_pack_bytes(ctypes.c_int64(total_pixels), ctypes.c_int32(fmt)))
+
+
+def gs_pack_images(images: "Images", views: "ViewBatch", out: torch.Tensor, stream=None, fmt: int = GS_PACK_COMPACT):
+    """Compact transports (reading Q39, include/gs.h): GS_PACK_COMPACT = fp16 RGB + fp16 A +
+    fp32 depth, 12 B/px, per view at byte 12 * pix_offset; GS_PACK_DENSE11 = batch-planar
+    fp16 RGB + unorm16 A + 24-bit depth, 11 B/px.  out: uint8 device tensor."""
+    need = gs_pack_bytes(views.total_pixels, fmt)
     assert out.dtype == torch.uint8 and out.numel() >= need
     _check(lib().gs_pack_images(ctypes.byref(images.struct), views.host, views.dev_ptr, ctypes.c_int32(views.n),
-                                ctypes.c_int32(GS_PACK_COMPACT), _ptr(out), _stream(stream)), "gs_pack_images")
+                                ctypes.c_int32(fmt), _ptr(out), _stream(stream)), "gs_pack_images")
+
+
+def unpack_dense11(buf, total_pixels: int):
+    """Host-side decode of GS_PACK_DENSE11 (numpy uint8 array) -> (rgb [3, TP] f32,
+    depth [TP] f32, alpha [TP] f32).  Argument marshalling for the consumer of the
+    transport, no arithmetic of the method."""
+    import numpy as np
+    b = np.asarray(buf, dtype=np.uint8)[:11 * total_pixels]
+    tp = total_pixels
+    rgb = b[:6 * tp].view(np.float16).reshape(3, tp).astype(np.float32)
+    alpha = b[6 * tp:8 * tp].view(np.uint16).astype(np.float32) / 65535.0
+    d = b[8 * tp:11 * tp].reshape(tp, 3).astype(np.uint32)
+    bits = (d[:, 0] | (d[:, 1] << 8) | (d[:, 2] << 16)) << 8
+    return rgb, bits.astype(np.uint32).view(np.float32), alpha.astype(np.float32)
 
 
 def gs_probe_alpha(opacity: torch.Tensor, power: torch.Tensor, out: torch.Tensor, stream=None):

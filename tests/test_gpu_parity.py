@@ -418,3 +418,33 @@ def test_pack_images_compact_transport(G):
         np.testing.assert_array_equal(halves[3], img["alpha"].reshape(hw).astype(np.float16))
         np.testing.assert_array_equal(depth, img["depth"].reshape(hw))
         assert np.abs(halves[:3].astype(np.float32) - img["rgb"].reshape(3, hw)).max() <= 1e-3
+
+
+def test_pack_images_dense11_transport(G):
+    """GS_PACK_DENSE11 (reading Q39): batch-planar fp16 R, G, B (= the fp32 images rounded
+    to nearest), unorm16 A (|error| <= 0.5/65535) and the depth plane's upper 24 bits
+    (relative error <= 2^-16); host decode with unpack_dense11; pyramid + odd-sized view
+    (the scalar tail) and a 4-aligned batch (the vector path)."""
+    for cfg, extra in (("C3", True), ("C2", False)):
+        sc, vs = synth.make_config(cfg, scale=0.02 if cfg == "C3" else 0.05)
+        views = list(vs)
+        if extra:
+            views.append(synth.make_view(vs[0].R, vs[0].t, vs[0].fx, vs[0].fy, 30.0, 20.0, 61, 41))
+        r = _gpu_render(G, sc, views)
+        n = r.vb.total_pixels
+        assert G.gs_pack_bytes(n, G.GS_PACK_DENSE11) == 11 * n
+        out = torch.zeros(11 * n + 16, dtype=torch.uint8, device="cuda")
+        G.gs_pack_images(r.images, r.vb, out, fmt=G.GS_PACK_DENSE11)
+        torch.cuda.synchronize()
+        rgb, depth, alpha = G.unpack_dense11(out.cpu().numpy(), n)
+        for i, v in enumerate(views):
+            hw, po = v.width * v.height, r.vb.pix_offset(i)
+            img = {k: t.cpu().numpy() for k, t in r.view_images(i).items()}
+            ref_rgb = img["rgb"].reshape(3, hw)
+            np.testing.assert_array_equal(rgb[:, po:po + hw], ref_rgb.astype(np.float16).astype(np.float32))
+            a = img["alpha"].reshape(hw).astype(np.float64)
+            assert np.abs(alpha[po:po + hw] - a).max() <= 0.5 / 65535 + 1e-7
+            z = img["depth"].reshape(hw).astype(np.float64)
+            dz = np.abs(depth[po:po + hw].astype(np.float64) - z)
+            assert (dz <= z * 2.0 ** -16 + 1e-30).all(), dz.max()
+
