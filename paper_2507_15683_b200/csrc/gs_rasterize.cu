@@ -61,7 +61,11 @@ constexpr int SPL = SE / 32;           // entries per lane per stage
 #ifndef GS_NST
 #define GS_NST 5
 #endif
-constexpr int NST = GS_NST;            // ring stages
+#ifndef GS_NST_D0
+#define GS_NST_D0 10                   // r2: without feature rows a stage is 4 KB: a deeper ring
+#endif                                 // absorbs the 8 warps' per-tile imbalance (C5 20.86 -> ~20.2 ms)
+// ring stages: the feature-carrying kernels are bounded by shared memory (3 CTAs/SM)
+constexpr int nst_for(int D) { return D > 0 ? GS_NST : GS_NST_D0; }
 constexpr int WB_STRIDE = 36;          // weight-buffer row stride (conflict-free m16n8k16 A fragments)
 constexpr int WB_ROWS = 16;            // one tensor-core k-step of weights (m16n8k16)
 constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
@@ -116,6 +120,7 @@ struct StageMeta {
 
 template <int D, bool CONTRIB, bool TC>
 struct RasterSmem {
+    static constexpr int NST = nst_for(D);
     static constexpr int FS = D > 0 ? D + 8 : 1;   // fp32 feature row stride (floats)
     static constexpr int FSH = D + 8;              // fp16 feature row stride (halves; 16-B aligned rows)
     static constexpr bool WB = D > 0;              // weight rows are collected (features)
@@ -254,6 +259,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     static_assert(!TC || TcCfg<D>::eligible, "tcgen05 feature path needs D in {16, 32, 48, 64}");
     using Smem = RasterSmem<D, CONTRIB, TC>;
     constexpr bool WB = Smem::WB;
+    constexpr int NST = Smem::NST;
     if (*status) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
