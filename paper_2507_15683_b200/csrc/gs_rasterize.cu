@@ -64,8 +64,22 @@ constexpr int SPL = SE / 32;           // entries per lane per stage
 #ifndef GS_NST_D0
 #define GS_NST_D0 10                   // r2: without feature rows a stage is 4 KB: a deeper ring
 #endif                                 // absorbs the 8 warps' per-tile imbalance (C5 20.86 -> ~20.2 ms)
-// ring stages: the feature-carrying kernels are bounded by shared memory (3 CTAs/SM)
-constexpr int nst_for(int D) { return D > 0 ? GS_NST : GS_NST_D0; }
+#ifndef GS_TC_DIRECT_B
+#define GS_TC_DIRECT_B 1               // r2: tcgen05 path fetches a k-step's feature rows straight into its B tile
+#endif
+#ifndef GS_NST_TCB
+#define GS_NST_TCB 10                  // ring stages when the ring carries records only (tcgen05, direct B)
+#endif
+// ring stages: a ring carrying feature rows is bounded by shared memory (3 CTAs/SM)
+constexpr int nst_for(int D, bool TC) {
+    return D == 0 ? GS_NST_D0 : (TC && GS_TC_DIRECT_B) ? GS_NST_TCB : GS_NST;
+}
+// 16-B global->shared copy that zero-fills instead when !valid (src-size 0)
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+                 "r"(valid ? 16 : 0)
+                 : "memory");
+}
 constexpr int WB_STRIDE = 36;          // weight-buffer row stride (conflict-free m16n8k16 A fragments)
 constexpr int WB_ROWS = 16;            // one tensor-core k-step of weights (m16n8k16)
 constexpr uint32_t ST_FIRST = 1u, ST_LAST = 2u, ST_END = 4u;
@@ -120,7 +134,10 @@ struct StageMeta {
 
 template <int D, bool CONTRIB, bool TC>
 struct RasterSmem {
-    static constexpr int NST = nst_for(D);
+    static constexpr int NST = nst_for(D, TC);
+    // tcgen05 direct-B: feature rows skip the ring (the consumer warps cp.async them into
+    // their B tiles), so weight rows pin no ring stage
+    static constexpr bool DIRECT_B = TC && GS_TC_DIRECT_B;
     static constexpr int FS = D > 0 ? D + 8 : 1;   // fp32 feature row stride (floats)
     static constexpr int FSH = D + 8;              // fp16 feature row stride (halves; 16-B aligned rows)
     static constexpr bool WB = D > 0;              // weight rows are collected (features)
@@ -130,7 +147,7 @@ struct RasterSmem {
     static constexpr bool WSTAGE = WB && !DIRECT;
     float4 rec[NST][SE + 1][4];                    // 64-byte records; row SE = null record (opacity 0)
     float feat[(D > 0 && !TC) ? NST : 1][(D > 0 && !TC) ? SE + 1 : 1][FS];
-    alignas(16) __half feath[TC ? NST : 1][TC ? SE + 1 : 1][TC ? FSH : 8];   // tcgen05 path: fp16 rows
+    alignas(16) __half feath[(TC && !DIRECT_B) ? NST : 1][(TC && !DIRECT_B) ? SE + 1 : 1][(TC && !DIRECT_B) ? FSH : 8];
     alignas(16) float wbuf[WSTAGE ? NCW : 1][WSTAGE ? WB_ROWS : 1][WB_STRIDE]; // per-warp weights [k][pixel]
     uint32_t slots[CONTRIB ? NST * (SE + 1) : 1];  // record slot of each ring row (contributions)
     alignas(16) int ent[NCW][2 * SE + 2];            // per-warp compacted ballot list of a stage pair (flat rows)
@@ -260,12 +277,18 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     using Smem = RasterSmem<D, CONTRIB, TC>;
     constexpr bool WB = Smem::WB;
     constexpr int NST = Smem::NST;
+    constexpr bool HOLD = WB && !Smem::DIRECT_B;   // pending weight rows pin the ring stages of their features
     if (*status) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < NST * 4; i += blockDim.x) sm.rec[i / 4][SE][i % 4] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if constexpr (TC)
+    if constexpr (Smem::DIRECT_B) {
+        // padding rows of a k-step keep the buffer's previous (finite) rows under zero
+        // weights; start from zeros so no uninitialised pattern (NaN) is ever multiplied
+        __half* bb = &sm.bbuf[0][0][0];
+        for (int i = threadIdx.x; i < (int)(sizeof(sm.bbuf) / sizeof(__half)); i += blockDim.x) bb[i] = __float2half_rn(0.f);
+    } else if constexpr (TC)
         for (int i = threadIdx.x; i < NST * Smem::FSH; i += blockDim.x)
             sm.feath[i / Smem::FSH][SE][i % Smem::FSH] = __float2half_rn(0.f);
     else if constexpr (D > 0)
@@ -338,7 +361,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             for (int q = 0; q < SE / 32; ++q) {
                 const int j = q * 32 + (int)lane;
                 sl[q] = j < cnt ? __ldg(&sorted_rec[c0 + j]) : 0u;
-                gd[q] = (D > 0 && j < cnt) ? (sorted_gid ? __ldg(&sorted_gid[c0 + j]) : __ldg(&rec[sl[q]].gid)) : 0u;
+                gd[q] = (D > 0 && !Smem::DIRECT_B && j < cnt)
+                            ? (sorted_gid ? __ldg(&sorted_gid[c0 + j]) : __ldg(&rec[sl[q]].gid)) : 0u;
             }
         };
         tile_begin(ch_base);
@@ -372,11 +396,11 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     if constexpr (CONTRIB) sm.slots[buf * (SE + 1) + j] = slot[q];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) cp_async16(&sm.rec[buf][j][e], src + e, pol);
-                    if constexpr (TC) {
+                    if constexpr (TC && !Smem::DIRECT_B) {
                         const uint4* fs = reinterpret_cast<const uint4*>(feat_h + (int64_t)gid[q] * D);
 #pragma unroll
                         for (int e = 0; e < D / 8; ++e) cp_async16(&sm.feath[buf][j][e * 8], fs + e, pol);
-                    } else if constexpr (D > 0) {
+                    } else if constexpr (D > 0 && !TC) {
                         const float4* fs = reinterpret_cast<const float4*>(feat + (int64_t)gid[q] * D);
 #pragma unroll
                         for (int e = 0; e < D / 4; ++e) cp_async16(&sm.feat[buf][j][e * 4], fs + e, pol);
@@ -444,17 +468,23 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                 tmem_st8(tA + my_lanes + b * 16u, hi);
                 tmem_st8(tA + my_lanes + b * 16u + 8u, lo);
             }
-            // the B tile is built while the TMEM stores are in flight
-            constexpr int NC8 = D / 8;
-            const __half* fb = &sm.feath[0][0][0];
             __half* bt = &sm.bbuf[warp][b][0];
+            if constexpr (Smem::DIRECT_B) {
+                // the k-step's feature rows were cp.async'd into this B tile as its entries
+                // were walked (feed_rows): wait for this lane's copies
+                asm volatile("cp.async.wait_all;\n" ::: "memory");
+            } else {
+                // the B tile is built while the TMEM stores are in flight
+                constexpr int NC8 = D / 8;
+                const __half* fb = &sm.feath[0][0][0];
 #pragma unroll
-            for (int c = (int)lane; c < 16 * NC8; c += 32) {
-                const int k = c / NC8, n8 = c % NC8;
-                GS_DCHECK(sm.kent[warp][k] >= 0 && sm.kent[warp][k] < NST * (SE + 1));
-                const uint4 o = *reinterpret_cast<const uint4*>(fb + sm.kent[warp][k] * Smem::FSH + n8 * 8);
-                // element (k, n) at n8*64 + (k%8)*8 + (k/8)*8*D halves (SBO = 128 B, LBO = 16 D B)
-                *reinterpret_cast<uint4*>(bt + n8 * 64 + (k & 7) * 8 + (k >> 3) * 8 * D) = o;
+                for (int c = (int)lane; c < 16 * NC8; c += 32) {
+                    const int k = c / NC8, n8 = c % NC8;
+                    GS_DCHECK(sm.kent[warp][k] >= 0 && sm.kent[warp][k] < NST * (SE + 1));
+                    const uint4 o = *reinterpret_cast<const uint4*>(fb + sm.kent[warp][k] * Smem::FSH + n8 * 8);
+                    // element (k, n) at n8*64 + (k%8)*8 + (k/8)*8*D halves (SBO = 128 B, LBO = 16 D B)
+                    *reinterpret_cast<uint4*>(bt + n8 * 64 + (k & 7) * 8 + (k >> 3) * 8 * D) = o;
+                }
             }
             asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -584,6 +614,26 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             ++tnext;
         }
     };
+    // direct B: entries [i, i + m) of the compacted list become rows pend.. of the k-step
+    // being filled; lane l < m copies entry i + l's fp16 feature row (D / 8 16-B chunks) into
+    // the canonical B tile (element (k, n) at n8*64 + (k%8)*8 + (k/8)*8*D halves); the null
+    // record (odd-tail padding) gets a zero row
+    auto feed_rows = [&](int i, int m) {
+        if constexpr (Smem::DIRECT_B) {
+            if (lane < (uint32_t)m) {
+                const int row = sm.ent[warp][i + (int)lane];
+                GS_DCHECK(row >= 0 && row < NST * (SE + 1));
+                const bool real = (row % (SE + 1)) != SE;
+                const uint32_t g = __float_as_uint(recf[4 * row + 3].x);   // record gid
+                const uint4* src = reinterpret_cast<const uint4*>(feat_h + (int64_t)(real ? g : 0u) * D);
+                const int k = pend + (int)lane;
+                GS_DCHECK(k < WB_ROWS && (!real || g < 0x10000000u));
+                __half* dst = &sm.bbuf[warp][kstep & 1u][0] + (k & 7) * 8 + (k >> 3) * 8 * D;
+#pragma unroll
+                for (int n8 = 0; n8 < D / 8; ++n8) cp_async16_zfill(dst + n8 * 64, src + n8, real);
+            }
+        }
+    };
     auto flush_pending = [&]() {
         if constexpr (WB) {
             if (pend > 0) {
@@ -591,7 +641,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     for (int q = pend >> 1; q < WB_ROWS / 2; ++q) store_pair(0.f, 0.f, q);
                 else
                     for (int r = pend; r < WB_ROWS; ++r) sm.wbuf[warp][r][lane] = 0.f;
-                if (lane < (uint32_t)(WB_ROWS - pend)) sm.kent[warp][pend + lane] = SE;   // null row
+                if (!Smem::DIRECT_B && lane < (uint32_t)(WB_ROWS - pend)) sm.kent[warp][pend + lane] = SE;   // null row
                 __syncwarp();
                 mma_block(0, WB_ROWS);
                 __syncwarp();
@@ -731,7 +781,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
                     for (int i = 0; i < ne;) {
                         if (pend == 0) hold = s;
                         const int m = min(ne - i, WB_ROWS - pend);
-                        if (lane < (uint32_t)m) sm.kent[warp][pend + (int)lane] = sm.ent[warp][i + (int)lane];
+                        if constexpr (Smem::DIRECT_B) feed_rows(i, m);
+                        else if (lane < (uint32_t)m) sm.kent[warp][pend + (int)lane] = sm.ent[warp][i + (int)lane];
                         int j = 0;
 #if GS_WALK4
 #pragma unroll 1
@@ -806,7 +857,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             }
         }
         // never pin more than half the ring: the producer must be able to refill
-        if (WB && pend > 0 && s2 - hold >= NST / 2) flush_pending();
+        if (HOLD && pend > 0 && s2 - hold >= NST / 2) flush_pending();
         if (last_flags & ST_LAST) {
             flush_pending();
             // -------------------------------------------------------- outputs
@@ -880,7 +931,7 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
             }
         }
         // release every stage no pending row references, in order
-        const uint32_t lim = (WB && pend > 0) ? hold : s2 + 1;
+        const uint32_t lim = (HOLD && pend > 0) ? hold : s2 + 1;
         __syncwarp();
         for (; rel < lim; ++rel)
             if (lane == 0) mbar_arrive(&sm.empty[rel % NST]);
