@@ -56,8 +56,6 @@ constexpr int RT_THREADS = (NCW + 1) * 32;
 #ifndef GS_SE
 #define GS_SE 64                       // r2: 64-entry stages, 5 of them (C4 27.66 -> 27.34 ms)
 #endif
-constexpr int SE = GS_SE;              // entries per stage (SE / 32 ballots)
-constexpr int SPL = SE / 32;           // entries per lane per stage
 #ifndef GS_NST
 #define GS_NST 5
 #endif
@@ -68,12 +66,17 @@ constexpr int SPL = SE / 32;           // entries per lane per stage
 #define GS_TC_DIRECT_B 1               // r2: tcgen05 path fetches a k-step's feature rows straight into its B tile
 #endif
 #ifndef GS_NST_TCB
-#define GS_NST_TCB 10                  // ring stages when the ring carries records only (tcgen05, direct B)
+#define GS_NST_TCB 5                   // ring stages when the ring carries records only (tcgen05, direct B)
+#endif
+#ifndef GS_SE_TCB
+#define GS_SE_TCB 128                  // entries per stage there (C4: 128 x 5 24.51 ms, 64 x 10 24.85 ms)
 #endif
 // ring stages: a ring carrying feature rows is bounded by shared memory (3 CTAs/SM)
 constexpr int nst_for(int D, bool TC) {
     return D == 0 ? GS_NST_D0 : (TC && GS_TC_DIRECT_B) ? GS_NST_TCB : GS_NST;
 }
+// entries per stage (SE / 32 ballots per lane)
+constexpr int se_for(int D, bool TC) { return (D > 0 && TC && GS_TC_DIRECT_B) ? GS_SE_TCB : GS_SE; }
 // 16-B global->shared copy that zero-fills instead when !valid (src-size 0)
 __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
@@ -135,6 +138,8 @@ struct StageMeta {
 template <int D, bool CONTRIB, bool TC>
 struct RasterSmem {
     static constexpr int NST = nst_for(D, TC);
+    static constexpr int SE = se_for(D, TC);       // entries per stage
+    static constexpr int SPL = SE / 32;            // entries per lane per stage
     // tcgen05 direct-B: feature rows skip the ring (the consumer warps cp.async them into
     // their B tiles), so weight rows pin no ring stage
     static constexpr bool DIRECT_B = TC && GS_TC_DIRECT_B;
@@ -277,6 +282,8 @@ rasterize_kernel(const gs_view* __restrict__ views, int n_views, const gs_record
     using Smem = RasterSmem<D, CONTRIB, TC>;
     constexpr bool WB = Smem::WB;
     constexpr int NST = Smem::NST;
+    constexpr int SE = Smem::SE;
+    constexpr int SPL = Smem::SPL;
     constexpr bool HOLD = WB && !Smem::DIRECT_B;   // pending weight rows pin the ring stages of their features
     if (*status) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
