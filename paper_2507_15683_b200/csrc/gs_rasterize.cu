@@ -10,11 +10,12 @@
 //     fed by 1 producer warp;
 //   * persistent CTAs (grid = SMs x resident CTAs, tiles handed out in order by
 //     a dynamic scheduler); the producer streams the sorted lists of the CTA's
-//     tiles through a 5-stage x 64-entry shared-memory ring (cp.async 16-B
-//     gathers of the 64-B records and the feature rows, completion signalled on
-//     "full" mbarriers via cp.async.mbarrier.arrive), running ahead across tile
-//     boundaries; consumers take stages in same-tile pairs and release them
-//     through "empty" mbarriers -- no CTA-wide barrier anywhere in the loop;
+//     tiles through a shared-memory ring (cp.async 16-B gathers of the 64-B
+//     records -- and, on the mma.sync feature path only, the feature rows --
+//     completion signalled on "full" mbarriers via cp.async.mbarrier.arrive),
+//     running ahead across tile boundaries; consumers take stages in same-tile
+//     pairs and release them through "empty" mbarriers -- no CTA-wide barrier
+//     anywhere in the loop;
 //   * exact warp-level culling: each lane tests staged entries: does the
 //     entry's alpha >= alpha_min ellipse (p >= e_cut, inflated) touch the warp's
 //     8x4 pixel rectangle?  Ballots give the entries the warp walks
@@ -22,12 +23,12 @@
 //   * per pixel the skip / stop decisions (exponent, alpha, Tn) are evaluated
 //     with explicit _rn / fma intrinsics in the oracle's operation order (Q29);
 //   * the feature blend F[px][:] += w[px][k] f[k][:] -- the one dense
-//     contraction of the path -- runs on the tensor cores.  Each warp compacts
-//     the weights of its walked entries into a 16-row shared buffer; a full
-//     buffer is one K = 16 step.  tcgen05 path (D in {16,32,48,64}, fp16
-//     feature rows from gs_scene_features_f16): the warp writes its 32 pixel
-//     rows of A (weights as fp16 hi + lo) to TMEM with tcgen05.st, copies the
-//     16 feature rows into a canonical (no-swizzle, MN-major) smem B tile, and
+//     contraction of the path -- runs on the tensor cores; 16 walked entries
+//     are one K = 16 step.  tcgen05 path (D in {16,32,48,64}, fp16 feature
+//     rows from gs_scene_features_f16): the warp writes its 32 pixel rows of A
+//     (weights as fp16 hi + lo) to TMEM with tcgen05.st, its lanes cp.async the
+//     16 feature rows from global/L2 straight into a canonical (no-swizzle,
+//     MN-major) smem B tile as the entries are walked, and
 //     one lane issues two M=128 N=D K=16 kind::f16 MMAs whose
 //     disable-output-lane mask leaves only the warp's own 32 TMEM lanes
 //     writable -- the 8 warps share two D-column accumulators (one per lane
