@@ -191,14 +191,15 @@ def measured_peaks():
 
 
 def ncu_traffic(config_key: str):
-    """DRAM bytes per gs_rasterize launch from a committed ncu --set full capture."""
+    """The committed ncu record of one gs_rasterize launch in this configuration
+    (profiles/ncu_traffic.json: DRAM bytes, issue activity, thread-instructions per
+    pixel), or {}."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
+        return {}
     with open(p) as f:
         d = json.load(f)
-    e = d.get(config_key)
-    return None if e is None else e.get("rasterize_dram_bytes_per_launch")
+    return d.get(config_key) or {}
 
 
 def workload(cfg: str, scale: float, rank: int, world: int, scaling: str, views_limit: int):
@@ -848,13 +849,17 @@ def main():
     fused = not args.separate_backproject
     raster_bytes = algorithmic_raster_bytes(n_pairs, n_visible, total_px, D, 2 if tc_path else 4, fused)
     achieved = raster_bytes / (stage_ms[2] / 1e3) / 1e9
-    traffic = ncu_traffic(f"{args.config}@{args.scale}/{args.binning}/{'tcgen05' if tc_path else 'mma_sync'}")
+    nrec = ncu_traffic(f"{args.config}@{args.scale}/{args.binning}/{'tcgen05' if tc_path else 'mma_sync'}")
+    traffic = nrec.get("rasterize_dram_bytes_per_launch")
     roof = {"bound": "hbm", "kernel": "gs_rasterize", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": raster_bytes, "dominant_stage": names[dom],
-            "note": "HBM roofline of the algorithmic bytes; the kernel is instruction-issue bound "
-                    "(ncu issue-active 0.70, ~2,900 thread-instructions per pixel, "
-                    "profiles/r02_ncu_full_rasterize_C4x16.txt; DESIGN.md §4.3b), traffic = algorithmic"}
+            "ncu_issue_active": nrec.get("issue_active"),
+            "ncu_thread_instructions_per_pixel": nrec.get("thread_instructions_per_pixel"),
+            "note": "HBM roofline of the algorithmic bytes; the kernel is bound by instruction issue and "
+                    "dependent latency, not bytes: ncu_issue_active / ncu_thread_instructions_per_pixel and "
+                    "traffic come from one committed ncu launch of this configuration "
+                    "(profiles/ncu_traffic.json, tools/gpu_traffic.sh; DESIGN.md §4.3b)"}
     # SURVEY §8(d) algorithmic bytes of the other stages: gs_project N*44 (geometry once per
     # batch) + V*12(L+1)^2 (SH of every visible record) + V*64 (records written); gs_bin_sort
     # V*16 (rectangle + depth read) + P*4 (sorted list) + T*8 (ranges)
