@@ -787,8 +787,11 @@ __device__ int smem_sort_run(uint64_t* ak, uint32_t* av, uint64_t* bk, uint32_t*
     return in_b;
 }
 
-template <int SMAX>
-__global__ void __launch_bounds__(SMAX <= 1024 ? BIG_THREADS : LAT_THREADS, SMAX <= 1024 ? 6 : 1)
+#ifndef GS_BIG_TP_THREADS
+#define GS_BIG_TP_THREADS 256          // threads of the throughput-mode 2048-entry sort CTA
+#endif
+template <int SMAX, int NT = (SMAX <= 1024 ? BIG_THREADS : LAT_THREADS)>
+__global__ void __launch_bounds__(NT, SMAX <= 1024 ? 6 : (NT <= 256 ? 4 : 1))
 big_sort_kernel(const uint32_t* __restrict__ ranges, const uint4* __restrict__ bucket, uint64_t* __restrict__ ka,
                 uint32_t* __restrict__ va, uint64_t* __restrict__ kb, uint32_t* __restrict__ vb,
                 uint32_t* __restrict__ out, uint32_t* __restrict__ ogid, uint64_t* __restrict__ dbg,
@@ -969,9 +972,19 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
             w.big_count + 6, w.cls_list + 4 * T, proj->status);
         if ((st = check_launch("big_sort_kernel<1024>")) != GS_OK) return st;
     }
-    big_sort_kernel<SMEM_SORT_MAX><<<big_grid, big_threads, smem, s>>>(out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb,
-                                                        out->sorted_rec, out->sorted_gid, out->sorted_key,
-                                                        w.big_count + 1, w.big_list, proj->status);
+    if (latency) {
+        big_sort_kernel<SMEM_SORT_MAX><<<big_grid, big_threads, smem, s>>>(out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb,
+                                                                out->sorted_rec, out->sorted_gid, out->sorted_key,
+                                                                w.big_count + 1, w.big_list, proj->status);
+    } else {
+        // throughput mode: more warps per list (shorter warp runs, one more merge round) at
+        // 4 CTAs/SM (the shared-memory limit)
+        constexpr int NT = GS_BIG_TP_THREADS;
+        cudaFuncSetAttribute(big_sort_kernel<SMEM_SORT_MAX, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        big_sort_kernel<SMEM_SORT_MAX, NT><<<4 * num_sms(), NT, smem, s>>>(
+            out->ranges, w.bucket, w.ka, w.va, w.kb, w.vb, out->sorted_rec, out->sorted_gid, out->sorted_key,
+            w.big_count + 1, w.big_list, proj->status);
+    }
     return check_launch("big_sort_kernel");
 }
 
