@@ -51,6 +51,9 @@ def parse():
                     help="views per render/gather chunk of the sharded step (0 = a quarter of the largest shard)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded chunked-gather step at N=1 too (exercises the N>1 code path)")
+    ap.add_argument("--force-gather", action="store_true",
+                    help="sharded step with the per-chunk NCCL all_gather even at N = 1 (a one-rank NCCL group: "
+                         "exercises the collective, comm stream and events of the N > 1 path on one GPU)")
     ap.add_argument("--feature-path", default="tcgen05", choices=["tcgen05", "mma_sync"],
                     help="feature contraction: tcgen05 (fp16 rows, TMEM) or mma.sync (fp32 rows)")
     ap.add_argument("--binning", default="tight", choices=["tight", "square"],
@@ -317,7 +320,12 @@ def main():
     from paper_2507_15683_b200 import dist as GD
 
     rank, world, local = GD.env_rank_world()
-    if world > 1:
+    use_pg = world > 1 or args.force_gather
+    if use_pg:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -330,7 +338,7 @@ def main():
     ds = G.DeviceScene(scene, device=dev, use_f16_features=args.feature_path == "tcgen05")
     stream = torch.cuda.current_stream()
     D = scene.feat_dim
-    sharded = (world > 1 and args.scaling == "strong") or args.sharded
+    sharded = (world > 1 and args.scaling == "strong") or args.sharded or args.force_gather
     sharded_info = None
     if sharded:
         # cost-balanced shard of the pose batch (LPT over per-view pair
@@ -345,7 +353,8 @@ def main():
         hw = views_all[0].width * views_all[0].height
         assert all(v.width * v.height == hw for v in views_all), "the gather needs equal-size views"
         chunk = args.chunk or max(1, -(-max(GD.shard_sizes(len(views_all), world, costs)) // 4))
-        cg = GD.ChunkedGather(len(views_all), hw, world, rank, chunk, costs, device=dev)
+        cg = GD.ChunkedGather(len(views_all), hw, world, rank, chunk, costs, device=dev,
+                              always_gather=args.force_gather)
         views = [views_all[i] for i in cg.mine]
         chunk_r = []
         for k in range(cg.n_chunks):
@@ -433,7 +442,7 @@ def main():
             scorer.add(rr, fmaps, stream)
         e[5].record(stream)
 
-    gather = sharded and world > 1 and not args.no_gather
+    gather = sharded and (world > 1 or args.force_gather) and not args.no_gather
     with ClockSampler(torch.cuda.current_device() if world == 1 else local) as clk:
         if not sharded:
             # warm-up, then the timed region: CUDA events on the launching stream, per-stage
@@ -512,7 +521,8 @@ def main():
                     "value": all_px_r * K / (ms_total / 1e3) / 1e6, "ms_per_step": ms_total / K,
                     "bytes_received_per_rank_per_step": cg.bytes_per_step,
                     "achieved_GBps": cg.bytes_per_step / (ms_total / K / 1e3) / 1e9,
-                    "collective": "all_gather_into_tensor per chunk on a comm stream (RGB + Dz + A fp32)"}}
+                    "collective": "all_gather_into_tensor per chunk on a comm stream (RGB + Dz + A fp32)",
+                    "received_equals_sent": cg.check_own_slot()}}
     stage_ms = np.median(stage, axis=0)
     ms_total = max_over_ranks(ms_total)
     all_px = sum_over_ranks(float(total_px))
@@ -909,7 +919,7 @@ def main():
         out["cpu_baseline"] = cpu_baseline(scene, views)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if use_pg:
         dist.destroy_process_group()
     return 0
 

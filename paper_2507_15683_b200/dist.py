@@ -80,8 +80,12 @@ class ChunkedGather:
     Every rank issues the same number of equally sized collectives."""
 
     def __init__(self, n_views: int, hw: int, world: int, rank: int, chunk: int,
-                 costs: Optional[Sequence[float]] = None, device="cpu", group=None, comm_stream=None):
+                 costs: Optional[Sequence[float]] = None, device="cpu", group=None, comm_stream=None,
+                 always_gather: bool = False):
         self.n_views, self.hw, self.world, self.rank, self.chunk = n_views, hw, world, rank, max(1, chunk)
+        # always_gather: issue the collectives even for a one-rank group (exercises the N > 1
+        # path -- collective, comm stream, events -- on one GPU)
+        self.always = always_gather
         self.costs = costs
         self.group = group
         self.shards = [shard_views(n_views, world, r, costs) for r in range(world)]
@@ -116,7 +120,7 @@ class ChunkedGather:
             if self.cuda and self.steps > 0 and gather:
                 stream.wait_event(self.sent[k])          # the send buffer is free again
             render_chunk(k)
-            if not gather or self.world == 1:
+            if not gather or (self.world == 1 and not self.always):
                 continue
             if self.cuda:
                 self.rendered[k].record(stream)
@@ -130,9 +134,22 @@ class ChunkedGather:
 
     def wait(self, stream=None):
         """Make `stream` wait for every gather of the last step."""
-        if self.cuda and self.world > 1:
+        if self.cuda and (self.world > 1 or self.always):
             for e in self.sent:
                 stream.wait_event(e)
+
+    def check_own_slot(self) -> bool:
+        """After a gathered step: this rank's slot of every receive buffer equals its send
+        buffer bit for bit (the collective moved the rendered planes unchanged)."""
+        if self.world == 1 and not self.always:
+            return True
+        if self.cuda:
+            torch.cuda.synchronize()
+        n = self.send[0].numel()
+        # bit patterns (an unused tail of a short shard's buffer may hold NaN patterns)
+        return all(torch.equal(self.recv[k][self.rank * n:(self.rank + 1) * n].view(torch.int32),
+                               self.send[k].view(torch.int32))
+                   for k in range(self.n_chunks))
 
     def assemble(self) -> torch.Tensor:
         """[n_views, 5, hw] in global view order from the receive buffers (planes

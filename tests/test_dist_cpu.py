@@ -88,6 +88,7 @@ def _worker(rank, world, port, n_views, use_costs, chunk, out_path):
     render = _oracle_render_chunk(cg, views, scene)
     for _ in range(2):                       # two steps reuse the send / receive buffers
         cg.step(render)
+    assert cg.check_own_slot()               # this rank's slot of every receive buffer = its send buffer
     full = cg.assemble()
     if rank == 0:
         torch.save(full, out_path)
@@ -157,3 +158,32 @@ def test_equal_size_runs_groups_consecutive_views():
     assert len(equal_size_runs([V(height=8, width=8)] * 256)) == 1
     # bounded calls (gs_dssim_grad workspace): 256 views in groups of <= 64
     assert equal_size_runs([V(height=8, width=8)] * 130, max_views=64) == [(0, 64, 8, 8), (64, 64, 8, 8), (128, 2, 8, 8)]
+
+
+def _worker_one(rank, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    import synth
+    scene = synth.box_v1(300, seed=9)
+    views = _views(3)
+    cg = GD.ChunkedGather(3, 48 * 32, 1, 0, 2, always_gather=True)
+    cg.step(_oracle_render_chunk(cg, views, scene))
+    torch.save({"ok": cg.check_own_slot(), "recv": [t.clone() for t in cg.recv]}, out_path)
+    dist.destroy_process_group()
+
+
+def test_always_gather_one_rank_group(tmp_path):
+    """--force-gather's host path: a one-rank group still issues the per-chunk collective
+    (bench.py uses it to exercise the N > 1 step on one GPU); the receive buffers hold the
+    rendered planes bit for bit."""
+    import oracle
+    oracle.build()
+    out = str(tmp_path / "one.pt")
+    mp.spawn(_worker_one, args=(_free_port(), out), nprocs=1, join=True)
+    d = torch.load(out)
+    assert d["ok"]
+    r = _single_process(3)
+    np.testing.assert_array_equal(d["recv"][0][4 * 2 * 48 * 32:4 * 2 * 48 * 32 + 48 * 32].numpy(),
+                                  r[0]["alpha"].reshape(-1))
+
