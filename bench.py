@@ -51,6 +51,10 @@ def parse():
                     help="views per render/gather chunk of the sharded step (0 = a quarter of the largest shard)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded chunked-gather step at N=1 too (exercises the N>1 code path)")
+    ap.add_argument("--gather-transport", default="dense11", choices=["dense11", "f32"],
+                    help="payload of the N > 1 gather: dense11 = GS_PACK_DENSE11 bytes (11 B/px, packed after "
+                         "each chunk's render; reading Q39), f32 = the fp32 planes rendered straight into the "
+                         "send buffer (20 B/px, lossless)")
     ap.add_argument("--force-gather", action="store_true",
                     help="sharded step with the per-chunk NCCL all_gather even at N = 1 (a one-rank NCCL group: "
                          "exercises the collective, comm stream and events of the N > 1 path on one GPU)")
@@ -354,7 +358,8 @@ def main():
         assert all(v.width * v.height == hw for v in views_all), "the gather needs equal-size views"
         chunk = args.chunk or max(1, -(-max(GD.shard_sizes(len(views_all), world, costs)) // 4))
         cg = GD.ChunkedGather(len(views_all), hw, world, rank, chunk, costs, device=dev,
-                              always_gather=args.force_gather)
+                              always_gather=args.force_gather, payload=args.gather_transport)
+        packed = args.gather_transport == "dense11"
         views = [views_all[i] for i in cg.mine]
         chunk_r = []
         for k in range(cg.n_chunks):
@@ -362,7 +367,8 @@ def main():
             if not cv:
                 chunk_r.append(None)
                 continue
-            rk = G.Renderer(ds, cv, device=dev, backproject=True, binning=args.binning, out_planes=cg.planes(k))
+            rk = G.Renderer(ds, cv, device=dev, backproject=True, binning=args.binning,
+                            out_planes=None if packed else cg.planes(k))
             rk.render()
             rk.fit_capacities()
             rk.render()
@@ -397,7 +403,13 @@ def main():
     if args.profile_steps:
         for _ in range(args.profile_steps):
             if sharded:
-                cg.step(lambda k: chunk_r[k] is not None and chunk_r[k].run(stream), stream, gather=not args.no_gather)
+                def prof_chunk(k):
+                    if chunk_r[k] is not None:
+                        chunk_r[k].run(stream)
+                        if packed:
+                            G.gs_pack_images(chunk_r[k].images, chunk_r[k].vb, cg.send[k], stream,
+                                             fmt=G.GS_PACK_DENSE11)
+                cg.step(prof_chunk, stream, gather=not args.no_gather)
             else:
                 r.run()
         torch.cuda.synchronize()
@@ -472,6 +484,9 @@ def main():
             def render_chunk(k):
                 if chunk_r[k] is not None:
                     chunk_r[k].run(stream)
+                    if packed:   # the chunk's images -> its send buffer (GS_PACK_DENSE11)
+                        G.gs_pack_images(chunk_r[k].images, chunk_r[k].vb, cg.send[k], stream,
+                                         fmt=G.GS_PACK_DENSE11)
 
             def timed(gather_on):
                 for _ in range(max(3, args.warmup)):
@@ -521,7 +536,9 @@ def main():
                     "value": all_px_r * K / (ms_total / 1e3) / 1e6, "ms_per_step": ms_total / K,
                     "bytes_received_per_rank_per_step": cg.bytes_per_step,
                     "achieved_GBps": cg.bytes_per_step / (ms_total / K / 1e3) / 1e9,
-                    "collective": "all_gather_into_tensor per chunk on a comm stream (RGB + Dz + A fp32)",
+                    "collective": "all_gather_into_tensor per chunk on a comm stream: " + (
+                        "GS_PACK_DENSE11 bytes (fp16 RGB, unorm16 A, 24-bit depth; 11 B/px)" if packed
+                        else "RGB + Dz + A fp32 planes (20 B/px)"),
                     "received_equals_sent": cg.check_own_slot()}}
     stage_ms = np.median(stage, axis=0)
     ms_total = max_over_ranks(ms_total)
@@ -886,7 +903,8 @@ def main():
                         "frac": bin_bytes / (stage_ms[1] / 1e3) / 1e9 / peak}}
     launches_per_step = (3 if ds.n_blocks else 2) + 8 + 1 + (0 if fused else 1) + (1 if scorer is not None else 0)
     if sharded:
-        launches_per_step = ((3 if ds.n_blocks else 2) + 8 + 1) * sharded_info["chunks_rendered"]
+        launches_per_step = ((3 if ds.n_blocks else 2) + 8 + 1 + (1 if args.gather_transport == "dense11" else 0)) \
+            * sharded_info["chunks_rendered"]
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
            "ms_per_step": ms_step, "ms_per_view": ms_step * world / all_views, "step_ms": step_stats,

@@ -81,8 +81,13 @@ class ChunkedGather:
 
     def __init__(self, n_views: int, hw: int, world: int, rank: int, chunk: int,
                  costs: Optional[Sequence[float]] = None, device="cpu", group=None, comm_stream=None,
-                 always_gather: bool = False):
+                 always_gather: bool = False, payload: str = "f32"):
         self.n_views, self.hw, self.world, self.rank, self.chunk = n_views, hw, world, rank, max(1, chunk)
+        # payload "f32": the fp32 RGB + Dz + A planes, rendered straight into the send buffer;
+        # "dense11": the GS_PACK_DENSE11 bytes of the chunk (11 B/px, gs_pack_images, reading
+        # Q39), packed into the send buffer after the render
+        assert payload in ("f32", "dense11")
+        self.payload = payload
         # always_gather: issue the collectives even for a one-rank group (exercises the N > 1
         # path -- collective, comm stream, events -- on one GPU)
         self.always = always_gather
@@ -91,9 +96,12 @@ class ChunkedGather:
         self.shards = [shard_views(n_views, world, r, costs) for r in range(world)]
         self.mine = self.shards[rank]
         self.n_chunks = max(1, math.ceil(max(len(sh) for sh in self.shards) / self.chunk))
-        n = 5 * self.chunk * hw
-        self.send = [torch.empty(n, dtype=torch.float32, device=device) for _ in range(self.n_chunks)]
-        self.recv = [torch.empty(world * n, dtype=torch.float32, device=device) for _ in range(self.n_chunks)]
+        if payload == "f32":
+            n, dt = 5 * self.chunk * hw, torch.float32
+        else:
+            n, dt = (11 * self.chunk * hw + 15) // 16 * 16, torch.uint8
+        self.send = [torch.empty(n, dtype=dt, device=device) for _ in range(self.n_chunks)]
+        self.recv = [torch.empty(world * n, dtype=dt, device=device) for _ in range(self.n_chunks)]
         self.cuda = torch.device(device).type == "cuda"
         self.comm = comm_stream if comm_stream is not None else (torch.cuda.Stream(device) if self.cuda else None)
         self.rendered = [torch.cuda.Event() for _ in range(self.n_chunks)] if self.cuda else None
@@ -105,7 +113,8 @@ class ChunkedGather:
         return self.mine[k * self.chunk:(k + 1) * self.chunk]
 
     def planes(self, k: int):
-        """(rgb, depth, alpha) output planes of chunk k inside its send buffer."""
+        """(rgb, depth, alpha) output planes of chunk k inside its send buffer (f32 payload)."""
+        assert self.payload == "f32"
         c, hw, b = self.chunk, self.hw, self.send[k]
         return b[:3 * c * hw], b[3 * c * hw:4 * c * hw], b[4 * c * hw:5 * c * hw]
 
@@ -151,9 +160,17 @@ class ChunkedGather:
                                self.send[k].view(torch.int32))
                    for k in range(self.n_chunks))
 
+    def received(self, k: int, r: int) -> torch.Tensor:
+        """Rank r's payload of chunk k in this rank's receive buffer."""
+        n = self.send[0].numel()
+        if self.world == 1 and not self.always:
+            return self.send[k]
+        return self.recv[k][r * n:(r + 1) * n]
+
     def assemble(self) -> torch.Tensor:
         """[n_views, 5, hw] in global view order from the receive buffers (planes
-        RGB, Dz, A) -- what a consumer of the gathered batch reads."""
+        RGB, Dz, A) -- what a consumer of the gathered batch reads (f32 payload)."""
+        assert self.payload == "f32"
         c, hw = self.chunk, self.hw
         out = torch.empty((self.n_views, 5, hw), dtype=torch.float32, device=self.recv[0].device)
         for k in range(self.n_chunks):

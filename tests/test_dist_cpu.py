@@ -187,3 +187,81 @@ def test_always_gather_one_rank_group(tmp_path):
     np.testing.assert_array_equal(d["recv"][0][4 * 2 * 48 * 32:4 * 2 * 48 * 32 + 48 * 32].numpy(),
                                   r[0]["alpha"].reshape(-1))
 
+
+def _pack_dense11_np(rgb, depth, alpha):
+    """Test-side writer of the GS_PACK_DENSE11 layout (include/gs.h) for the gloo test."""
+    tp = depth.size
+    out = np.zeros(11 * tp, np.uint8)
+    out[:6 * tp] = rgb.reshape(3, tp).astype(np.float16).reshape(-1).view(np.uint8)
+    a = np.rint(np.clip(alpha, 0, 1).astype(np.float32) * np.float32(65535)).astype(np.uint16)
+    out[6 * tp:8 * tp] = a.view(np.uint8)
+    d = (depth.astype(np.float32).view(np.uint32) + np.uint32(0x80)) >> np.uint32(8)
+    b = np.stack([d & 0xFF, (d >> 8) & 0xFF, (d >> 16) & 0xFF], axis=1).astype(np.uint8)
+    out[8 * tp:11 * tp] = b.reshape(-1)
+    return out
+
+
+def _worker_dense(rank, world, port, n_views, chunk, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import synth
+    scene = synth.box_v1(300, seed=9)
+    views = _views(n_views)
+    hw = 48 * 32
+    cg = GD.ChunkedGather(n_views, hw, world, rank, chunk, payload="dense11")
+
+    def render(k):
+        idx = cg.chunk_views(k)
+        if not idx:
+            return
+        rs = [oracle.render(scene, views[i]) for i in idx]
+        rgb = np.concatenate([r["rgb"].reshape(3, -1) for r in rs], axis=1)
+        dep = np.concatenate([r["depth"].reshape(-1) for r in rs])
+        alp = np.concatenate([r["alpha"].reshape(-1) for r in rs])
+        b = _pack_dense11_np(rgb, dep, alp)
+        cg.send[k][:b.size] = torch.from_numpy(b)
+
+    cg.step(render)
+    assert cg.check_own_slot()
+    if rank == 0:
+        torch.save({"recv": [t.clone() for t in cg.recv], "shards": cg.shards, "chunk": cg.chunk}, out_path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_chunked_gather_dense11_payload(tmp_path):
+    """The bench's default N > 1 payload: each rank packs its chunk's planes as GS_PACK_DENSE11
+    bytes and gathers them; rank 0 decodes every rank's slot (unpack_dense11) to the oracle's
+    planes within the format's rounding (fp16 RGB exact-rounded, A <= 0.5/65535, depth
+    <= 2^-16 relative)."""
+    import oracle
+    oracle.build()
+    n_views, chunk, hw = 5, 2, 48 * 32
+    out = str(tmp_path / "dense.pt")
+    mp.spawn(_worker_dense, args=(2, _free_port(), n_views, chunk, out), nprocs=2, join=True)
+    d = torch.load(out)
+    ref = _single_process(n_views)
+    n = d["recv"][0].numel() // 2
+    seen = 0
+    for k, rv in enumerate(d["recv"]):
+        for r in range(2):
+            idx = d["shards"][r][k * d["chunk"]:(k + 1) * d["chunk"]]
+            if not idx:
+                continue
+            rgb, dep, alp = GD_unpack(rv[r * n:(r + 1) * n].numpy(), len(idx) * hw)
+            for j, g in enumerate(idx):
+                sl = slice(j * hw, (j + 1) * hw)
+                np.testing.assert_array_equal(rgb[:, sl], ref[g]["rgb"].reshape(3, -1).astype(np.float16).astype(np.float32))
+                assert np.abs(alp[sl] - ref[g]["alpha"].reshape(-1)).max() <= 0.5 / 65535 + 1e-7
+                z = ref[g]["depth"].reshape(-1).astype(np.float64)
+                assert (np.abs(dep[sl].astype(np.float64) - z) <= z * 2.0 ** -16 + 1e-30).all()
+                seen += 1
+    assert seen == n_views
+
+
+def GD_unpack(buf, tp):
+    from paper_2507_15683_b200.gs import unpack_dense11
+    return unpack_dense11(buf, tp)
+

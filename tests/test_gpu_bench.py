@@ -58,10 +58,12 @@ def test_bench_small_batch_graph_timing():
 def test_bench_force_gather_one_rank_nccl():
     """The N > 1 step on one GPU: sharded chunks, one NCCL all_gather_into_tensor per chunk
     on the comm stream (a one-rank group), the received planes equal to the rendered ones."""
-    d = _bench("--config", "C4", "--scale", "0.02", "--views", "16", "--steps", "3", "--warmup", "3",
-               "--force-gather", "--chunk", "4", "--no-cpu-baseline", "--no-e2e")
-    _contract(d)
-    wg = d["sharded"]["with_gather"]
-    assert wg is not None and wg["received_equals_sent"] is True
-    assert wg["bytes_received_per_rank_per_step"] == 4 * 5 * 4 * 1024 * 768 * 4
+    hw = 1024 * 768
+    for transport, nbytes in (("dense11", 4 * ((11 * 4 * hw + 15) // 16 * 16)), ("f32", 4 * 5 * 4 * hw * 4)):
+        d = _bench("--config", "C4", "--scale", "0.02", "--views", "16", "--steps", "3", "--warmup", "3",
+                   "--force-gather", "--gather-transport", transport, "--chunk", "4", "--no-cpu-baseline", "--no-e2e")
+        _contract(d)
+        wg = d["sharded"]["with_gather"]
+        assert wg is not None and wg["received_equals_sent"] is True
+        assert wg["bytes_received_per_rank_per_step"] == nbytes
 

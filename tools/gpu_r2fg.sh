@@ -7,3 +7,6 @@ timeout 600 python bench.py --force-gather --steps 10 --warmup 3 --no-cpu-baseli
 python -c "
 import json; d=json.loads(open('$O/bench_C4_force_gather.json').read().strip().splitlines()[-1]); print(json.dumps(d['sharded'])[:800]); print(d['value'], d['ms_per_step'])"
 tail -3 $O/fg.err
+timeout 600 python bench.py --force-gather --gather-transport f32 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $O/bench_C4_force_gather_f32.json 2> $O/fg32.err
+python -c "
+import json; d=json.loads(open('$O/bench_C4_force_gather_f32.json').read().strip().splitlines()[-1]); print(json.dumps(d['sharded']['with_gather'])[:500]); print(d['value'], d['ms_per_step'])"
