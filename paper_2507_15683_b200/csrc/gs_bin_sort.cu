@@ -91,6 +91,12 @@ constexpr int BIN_THREADS = 512;
 #ifndef GS_BIN_MINB
 #define GS_BIN_MINB 3                  // count / scatter CTAs per SM the register budget is sized for (40 regs)
 #endif
+#ifndef GS_CLS_GRID
+#define GS_CLS_GRID 16                 // class-sort CTAs per SM (persistent, 8 warps each; r2: 8 -> 16)
+#endif
+#ifndef GS_MID_GRID
+#define GS_MID_GRID 8                  // mid-sort CTAs per SM (r2: 4 -> 8)
+#endif
 #ifndef GS_BIN_CTAS_PER_SM
 #define GS_BIN_CTAS_PER_SM 32                // r2: 8 -> 32 (C4 bin_sort 4.48 -> 4.18 ms, C5 11.51 -> 11.02)
 #endif
@@ -943,7 +949,7 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
                                                                     w.mid_list, w.big_list, w.cls_list,
                                                                     WARP_SORT_MAX, proj->status);
         if ((st = check_launch("classify_kernel")) != GS_OK) return st;
-        const unsigned cg = 8 * num_sms();
+        const unsigned cg = GS_CLS_GRID * num_sms();
         class_sort_kernel<1><<<cg, 256, 0, s>>>(out->ranges, w.bucket, out->sorted_rec, out->sorted_gid,
                                                 out->sorted_key, w.big_count + 2, w.cls_list, proj->status);
         class_sort_kernel<2><<<cg, 256, 0, s>>>(out->ranges, w.bucket, out->sorted_rec, out->sorted_gid,
@@ -955,7 +961,7 @@ gs_status gs_bin_sort(const gs_projected* proj, const gs_view* views_host, const
         if ((st = check_launch("class_sort_kernel")) != GS_OK) return st;
     }
     if (!latency) {
-        mid_sort_kernel<<<4 * num_sms(), 256, 0, s>>>(out->ranges, w.bucket, out->sorted_rec, out->sorted_gid,
+        mid_sort_kernel<<<GS_MID_GRID * num_sms(), 256, 0, s>>>(out->ranges, w.bucket, out->sorted_rec, out->sorted_gid,
                                                       out->sorted_key, w.big_count, w.mid_list, proj->status);
         if ((st = check_launch("mid_sort_kernel")) != GS_OK) return st;
     }
