@@ -89,7 +89,7 @@ size_t ws_bytes(int64_t cap, int64_t T) {
 // global reduction per pair.
 constexpr int BIN_THREADS = 512;
 #ifndef GS_BIN_MINB
-#define GS_BIN_MINB 3                  // count / scatter CTAs per SM the register budget is sized for (40 regs)
+#define GS_BIN_MINB 2                  // count / scatter CTAs per SM the register budget is sized for (r2: 3 -> 2, C5 -0.16 ms)
 #endif
 #ifndef GS_CLS_GRID
 #define GS_CLS_GRID 16                 // class-sort CTAs per SM (persistent, 8 warps each; r2: 8 -> 16)
